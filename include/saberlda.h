@@ -1,0 +1,216 @@
+/*
+ * saberlda.h -- C-ABI of the B200-native SaberLDA/ESCA engine.
+ *
+ * The drop-in boundary for the reference's hot path (arxiv/paper_1610_02496,
+ * `proj/`): one ESCA training iteration plus its setup.  Plain pointers and
+ * sizes only; no torch or C++ types.  Every entry point names the reference
+ * interface it replaces (paths relative to /root/reference/proj).
+ *
+ * Threading: calls on one engine are serialised by the caller (the reference
+ * ModelState is not re-entrant either, trainer.cpp:325-332); different
+ * engines are independent.  Ownership: the engine owns every device buffer;
+ * host arrays passed in are borrowed and copied during the call; getters fill
+ * caller-allocated buffers.
+ *
+ * Errors: every int-returning call returns SLDA_OK or one of the codes below,
+ * mirroring sparselda::ValidationError / IoError (types.hpp:28-35) plus a
+ * device code; slda_last_error() returns the calling thread's message.
+ */
+#ifndef SABERLDA_H
+#define SABERLDA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SLDA_ABI_VERSION 1u
+
+enum {
+    SLDA_OK = 0,
+    SLDA_ERR_VALIDATION = 1, /* sparselda::ValidationError, CLI exit 1, Python ValueError */
+    SLDA_ERR_IO = 2,         /* sparselda::IoError, CLI exit 2, Python IOError */
+    SLDA_ERR_DEVICE = 3      /* CUDA / NCCL failure (no reference analogue) */
+};
+
+#define SLDA_INVALID_TOPIC 0xFFFFFFFFu /* kInvalidTopic, types.hpp:17 */
+
+/* How initial topics are chosen (trainer.cpp:369-388). */
+enum {
+    SLDA_INIT_AUTO = 0,  /* reference rule over the tokens passed in: if any topic is
+                            kInvalidTopic, draw all uniformly; else validate topic < K */
+    SLDA_INIT_DRAW = 1,  /* draw all uniformly (sharded runs: the host decided globally) */
+    SLDA_INIT_GIVEN = 2  /* keep the given topics (validated < K) */
+};
+
+typedef struct slda_engine slda_engine;
+
+/* A borrowed view of (a document shard of) a sparselda::Corpus (corpus.hpp:12-20).
+ * tokens is T x 3 uint32 (doc, word, topic), the exact layout of sparselda::Token
+ * (types.hpp:21-25).  Every token's doc must lie in [doc_begin, doc_end). */
+typedef struct slda_corpus_view {
+    uint32_t num_docs;        /* D of the whole corpus */
+    uint32_t vocab_size;      /* V */
+    uint64_t num_tokens;      /* T of this view (< 2^32 per engine) */
+    const uint32_t* tokens;   /* T x 3 AoS */
+    uint32_t doc_begin;       /* shard document range; [0, D) for one GPU */
+    uint32_t doc_end;
+    uint64_t token_id_base;   /* corpus position of tokens[0] */
+    const uint64_t* token_ids;/* optional: per-token corpus position (RNG element id,
+                                 trainer.cpp:275); NULL -> token_id_base + i */
+} slda_corpus_view;
+
+/* sparselda::TrainConfig (trainer.hpp:20-36) plus device placement. */
+typedef struct slda_config {
+    uint32_t num_topics;      /* K >= 1 */
+    double alpha;             /* <= 0 resolves to 50/K (trainer.cpp:18) */
+    double beta;              /* > 0 */
+    uint64_t seed;
+    uint32_t tree_branch;     /* W: capacity check K <= W^3 as the reference (trainer.cpp:19-26);
+                                 0 -> 32.  The device search is layout-free (acceptance.cpp:140-200). */
+    uint32_t init_mode;       /* SLDA_INIT_* */
+    int32_t device;           /* CUDA ordinal; -1 = current device */
+    uint32_t rank;            /* document shard index (0 for one GPU) */
+    uint32_t world_size;      /* number of shards/GPUs (1 = no collectives) */
+    const void* nccl_id;      /* 128-byte ncclUniqueId from rank 0 when world_size > 1 */
+} slda_config;
+
+/* sparselda::IterationStats (trainer.hpp:38-44) + device timings. */
+typedef struct slda_iteration_stats {
+    uint32_t iteration;       /* 1-based count after the call */
+    uint64_t tokens;          /* T of this engine's shard */
+    double elapsed_s;         /* host wall time of the iteration (trainer.cpp:422-447 span) */
+    double mtokens_per_s;
+    double mean_doc_topics;   /* K_d over this engine's documents (trainer.cpp:335-350) */
+    double device_ms;         /* CUDA-event time of the iteration on the engine stream */
+} slda_iteration_stats;
+
+typedef struct slda_info {
+    uint32_t num_docs, vocab_size, num_topics, iteration;
+    uint64_t num_tokens;      /* shard tokens */
+    uint32_t doc_begin, doc_end, rank, world_size;
+    double alpha, beta;
+    uint64_t seed;
+    uint32_t num_segments;    /* distinct words in the shard (PDOW word segments) */
+    uint32_t num_units;       /* sampler work units after heavy-word splitting */
+    uint64_t doc_topic_nnz;   /* nnz of the shard's C_dk (after the last rebuild) */
+    uint64_t device_bytes;    /* bytes of device memory held by the engine */
+    uint32_t doc_major;       /* 1 if tokens came doc-sorted (no slot permutation) */
+    uint32_t padded_topics;   /* K rounded up to the L4 block width (32) */
+} slda_info;
+
+/* Per-kernel device times (ms) of the last iteration, for roofline accounting. */
+typedef struct slda_kernel_times {
+    double reset_ms, sampler_ms, ssc_ms, colsum_ms, phi_ms, comm_ms, total_ms;
+    uint64_t sampler_row_entries; /* sum over tokens of nnz(A_d) read by the sampler */
+    uint32_t launches;            /* kernels launched by the iteration */
+} slda_kernel_times;
+
+/* ------------------------------------------------------------------ engine -- */
+
+/* init_state (trainer.cpp:354-417): copies the corpus, builds the PDOW layout on device
+ * (build_chunks corpus.cpp:125-198, build_schedule :200-210), initial topics
+ * (init_assignments corpus.cpp:87-96), C_dk (rebuild_doc_topic counts.cpp:103-125),
+ * C_wk (count_chunk_into trainer.cpp:223-235), phi (preprocess counts.cpp:37-63)
+ * and the sampling trees (rebuild_trees trainer.cpp:237-248). */
+int slda_create(const slda_corpus_view* corpus, const slda_config* config, slda_engine** out);
+
+/* Eval-only model from checkpointed counts (model_from_checkpoint trainer.cpp:514-532):
+ * word_topic is V x K; no tokens. */
+int slda_create_from_counts(uint32_t vocab_size, const uint32_t* word_topic,
+                            uint64_t num_tokens, uint32_t iteration, const slda_config* config,
+                            slda_engine** out);
+
+void slda_destroy(slda_engine* e);
+
+/* run_iteration (trainer.cpp:419-449): synchronous; fills stats (may be NULL). */
+int slda_iterate(slda_engine* e, slda_iteration_stats* stats);
+/* Enqueue one iteration on the engine stream without waiting (bench / pipelining). */
+int slda_iterate_async(slda_engine* e);
+int slda_synchronize(slda_engine* e);
+/* Sets the RNG stream of the next iteration (resume; trainer.cpp:423). */
+int slda_set_iteration(slda_engine* e, uint32_t iteration);
+
+int slda_get_info(const slda_engine* e, slda_info* info);
+int slda_get_kernel_times(const slda_engine* e, slda_kernel_times* t);
+/* Average over the last `last_n` iterations (1..64), e.g. a run of slda_iterate_async. */
+int slda_get_kernel_times_avg(const slda_engine* e, uint32_t last_n, slda_kernel_times* t);
+/* cudaStream_t the engine launches on (as void*). */
+void* slda_stream(const slda_engine* e);
+
+/* ------------------------------------------------------------------ getters -- */
+
+/* ModelState::word_topic (trainer.hpp:158), V x K row-major.  Sharded: collective. */
+int slda_get_word_topic(slda_engine* e, uint32_t* out);
+/* ModelState::word_topic_prob (trainer.hpp:159), V x K f32. */
+int slda_get_word_topic_prob(slda_engine* e, float* out);
+/* ModelState::tree_mass (trainer.hpp:160), V f32. */
+int slda_get_tree_mass(slda_engine* e, float* out);
+/* WaryTree::prefix() of every word (sampler.hpp:119), V x K f32 (the L4 level). */
+int slda_get_tree_prefix(slda_engine* e, float* out);
+/* ModelState::gather_assignments (trainer.cpp:203-213): T topics in view order. */
+int slda_get_assignments(slda_engine* e, uint32_t* out);
+/* DocTopicMatrix rows of the shard's documents (counts.hpp:33-80):
+ * row_offsets has (doc_end-doc_begin)+1 entries; topics/counts have nnz entries. */
+int slda_get_doc_topic_nnz(slda_engine* e, uint64_t* nnz);
+int slda_get_doc_topic(slda_engine* e, uint64_t* row_offsets, uint32_t* topics,
+                       uint32_t* counts);
+/* Chunk PDOW arrays of the shard as one chunk (corpus.hpp:33-43): tokens sorted by
+ * (word, doc, token_id) -> sorted_doc/sorted_word/token_ids (corpus positions, u64),
+ * shuffle_ptrs, doc_offsets (docs+1), word_segments ascending (seg_*, num_segments),
+ * and the heavy-first schedule (build_schedule) as segment indices. */
+int slda_get_pdow(slda_engine* e, uint32_t* sorted_doc, uint32_t* sorted_word,
+                  uint64_t* token_ids, uint32_t* shuffle_ptrs, uint32_t* doc_offsets,
+                  uint32_t* seg_word, uint32_t* seg_offset, uint32_t* seg_length,
+                  uint32_t* schedule);
+
+/* ------------------------------------------------------------------ eval -- */
+
+/* heldout_ll (eval.cpp:49-133) over a held-out corpus (AoS tokens, all docs), split by
+ * HeldoutSet::from_corpus (eval.cpp:14-28). */
+int slda_heldout_ll(slda_engine* e, uint32_t num_docs, uint32_t vocab_size, uint64_t num_tokens,
+                    const uint32_t* tokens, uint32_t burn_in, uint64_t seed,
+                    double* per_token_ll, uint64_t* tokens_evaluated);
+
+/* ------------------------------------------------------------------ misc -- */
+
+const char* slda_last_error(void);
+uint32_t slda_abi_version(void);
+/* Fills a 128-byte ncclUniqueId (rank 0 of a sharded run). */
+int slda_nccl_unique_id(void* out128);
+/* Document shard bounds by the chunk_boundaries rule (corpus.cpp:103-121):
+ * bounds has num_shards+1 entries.  Host-only. */
+int slda_shard_bounds(uint32_t num_docs, uint64_t num_tokens, const uint32_t* doc_lengths,
+                      uint32_t num_shards, uint32_t* bounds);
+
+/* Synthetic corpora.  Host-only, multi-threaded, deterministic in
+ * (params, seed) regardless of thread count.  family 0 = G (LDA-generative: Zipf(1)
+ * topics over seeded vocabulary permutations, Dirichlet(0.1) docs, lognormal(0.6)
+ * lengths rescaled to sum to T), family 1 = U (uniform words, Poisson lengths).
+ * Doc-major output: tokens T x 3 (doc, word, kInvalidTopic). */
+typedef struct slda_gen_params {
+    uint32_t family;
+    uint32_t num_docs, vocab_size;
+    uint64_t num_tokens;      /* exact T for family G; family U: mean length = T/D */
+    uint32_t latent_topics;   /* family G K_true (default 100) */
+    double zipf_s;            /* family G (default 1.0) */
+    double doc_dirichlet;     /* family G (default 0.1) */
+    double length_sigma;      /* family G lognormal sigma (default 0.6) */
+    uint64_t seed;            /* default 20161008 */
+    uint32_t threads;         /* 0 = hardware concurrency */
+} slda_gen_params;
+/* Returns the exact T that will be generated (two-phase use: size, then fill). */
+int slda_generate_corpus_size(const slda_gen_params* p, uint64_t* num_tokens);
+int slda_generate_corpus(const slda_gen_params* p, uint32_t* tokens, uint64_t capacity);
+/* Per-document lengths (num_docs entries) and the tokens of documents [doc_begin, doc_end)
+ * only, identical to the corresponding slice of slda_generate_corpus (sharded ranks). */
+int slda_generate_doc_lengths(const slda_gen_params* p, uint32_t* lengths);
+int slda_generate_docs(const slda_gen_params* p, uint32_t doc_begin, uint32_t doc_end,
+                       uint32_t* tokens, uint64_t capacity);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SABERLDA_H */

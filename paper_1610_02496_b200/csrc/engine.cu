@@ -1,0 +1,989 @@
+// engine.cu -- the C-ABI (include/saberlda.h) over the sm_100a kernels.
+//
+// One engine = one GPU = one document shard (the reference's chunk,
+// PAPER.md:403, with chunk -> GPU).  The whole ESCA state lives in HBM:
+//   tok   uint2[T]      PDOW order (word, doc, token_id): {doc_local, slot}
+//   z     u16[T]        topic per slot; slots are doc-grouped (slot == corpus
+//                       position for a doc-sorted corpus)
+//   A     u32[4*Q]      C_dk rows, entry = topic | count << tbits, row d at a
+//                       16-byte aligned offset with capacity len_d, padded with
+//                       zero-count entries; hdr[d] = {row offset / 4, nnz}
+//   B     u32[V_pad][K_pad], bhat/L4 f32[V_pad][K_pad], L3 f32[V_pad][l3s], Q f32[V_pad]
+// Reference paths are relative to /root/reference/proj.
+#include <dlfcn.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cstring>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include <cub/cub.cuh>
+#include <nccl.h>
+
+#include "../../include/saberlda.h"
+#include "common.cuh"
+#include "heldout.hpp"
+#include "kernels.hpp"
+
+namespace {
+
+thread_local std::string g_error;
+
+struct SldaError : std::runtime_error {
+    int code;
+    SldaError(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+[[noreturn]] void validation(const std::string& m) { throw SldaError(SLDA_ERR_VALIDATION, m); }
+
+void cuda_check(cudaError_t e, const char* what) {
+    if (e != cudaSuccess)
+        throw SldaError(SLDA_ERR_DEVICE, std::string(what) + ": " + cudaGetErrorString(e));
+}
+#define CK(x) cuda_check((x), #x)
+
+template <class F>
+int guarded(F&& f) {
+    try {
+        f();
+        return SLDA_OK;
+    } catch (const SldaError& e) {
+        g_error = e.what();
+        return e.code;
+    } catch (const std::bad_alloc&) {
+        g_error = "host allocation failed";
+        return SLDA_ERR_DEVICE;
+    } catch (const std::exception& e) {
+        g_error = e.what();
+        return SLDA_ERR_DEVICE;
+    }
+}
+
+// ------------------------------------------------------------------ NCCL --
+// Loaded lazily (world_size > 1 only) so a single-GPU process never binds a
+// second libnccl next to the one torch may already have loaded.
+struct Nccl {
+    void* h = nullptr;
+    decltype(&ncclGetUniqueId) GetUniqueId = nullptr;
+    decltype(&ncclCommInitRank) CommInitRank = nullptr;
+    decltype(&ncclCommDestroy) CommDestroy = nullptr;
+    decltype(&ncclReduceScatter) ReduceScatter = nullptr;
+    decltype(&ncclAllReduce) AllReduce = nullptr;
+    decltype(&ncclAllGather) AllGather = nullptr;
+    decltype(&ncclGetErrorString) GetErrorString = nullptr;
+    decltype(&ncclGroupStart) GroupStart = nullptr;
+    decltype(&ncclGroupEnd) GroupEnd = nullptr;
+};
+
+Nccl& nccl() {
+    static Nccl n;
+    if (!n.h) {
+        for (const char* name : {"libnccl.so.2", "libnccl.so"}) {
+            n.h = dlopen(name, RTLD_NOW | RTLD_NOLOAD | RTLD_GLOBAL);
+            if (!n.h) n.h = dlopen(name, RTLD_NOW | RTLD_GLOBAL);
+            if (n.h) break;
+        }
+        if (!n.h) throw SldaError(SLDA_ERR_DEVICE, "libnccl.so.2 not found");
+#define SYM(f) n.f = reinterpret_cast<decltype(n.f)>(dlsym(n.h, "nccl" #f))
+        SYM(GetUniqueId); SYM(CommInitRank); SYM(CommDestroy); SYM(ReduceScatter);
+        SYM(AllReduce); SYM(AllGather); SYM(GetErrorString); SYM(GroupStart); SYM(GroupEnd);
+#undef SYM
+        if (!n.CommInitRank || !n.AllGather) throw SldaError(SLDA_ERR_DEVICE, "incomplete libnccl");
+    }
+    return n;
+}
+
+void nccl_check(ncclResult_t r, const char* what) {
+    if (r != ncclSuccess)
+        throw SldaError(SLDA_ERR_DEVICE, std::string(what) + ": " + nccl().GetErrorString(r));
+}
+
+// --------------------------------------------------------------- buffers --
+struct DevMem {
+    void* p = nullptr;
+    size_t bytes = 0;
+    DevMem() = default;
+    DevMem(const DevMem&) = delete;
+    DevMem& operator=(const DevMem&) = delete;
+    ~DevMem() { release(); }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        bytes = 0;
+    }
+    void alloc(size_t n, size_t* tally) {
+        release();
+        if (n == 0) n = 16;
+        cuda_check(cudaMalloc(&p, n), "cudaMalloc");
+        bytes = n;
+        if (tally) *tally += n;
+    }
+    template <class T> T* as() const { return static_cast<T*>(p); }
+};
+
+uint32_t bits_for(uint64_t max_value) {
+    uint32_t b = 1;
+    while (b < 64 && (max_value >> b) != 0) ++b;
+    return b;
+}
+
+}  // namespace
+
+// =========================================================================
+struct slda_engine {
+    // Shape / config
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    uint32_t D_all = 0, doc_begin = 0, doc_end = 0, D = 0;  // D = shard documents
+    uint32_t V = 0, V_pad = 0, K = 0, K_pad = 0, l3_stride = 0, n_l3 = 0, tbits = 1;
+    uint64_t T = 0;
+    double alpha = 0, beta = 0;
+    float falpha = 0;
+    uint64_t seed = 0, id_base = 0;
+    uint32_t iteration = 0;
+    uint32_t rank = 0, world = 1;
+    uint32_t nseg = 0, n_units = 0, n_long = 0;
+    bool doc_major = true;
+    size_t device_bytes = 0;
+    uint64_t nnz = 0;
+
+    // Device state
+    DevMem tok, z, doc_start, hdr, A, units, long_docs, hist_scratch;
+    DevMem seg_word, seg_off, seg_len, schedule;  // PDOW getters
+    DevMem input_of_slot, ids;                    // only for non doc-major input / explicit ids
+    DevMem B, bhat, l4, l3, q, colsum, denom, zv, counters;
+
+    // Per-iteration phase events, a ring so async iterations can be profiled afterwards.
+    static constexpr uint32_t kRing = 64;
+    cudaEvent_t ring[kRing][7] = {};
+    cudaEvent_t* ev = ring[0];
+    uint32_t ring_launches[kRing] = {};
+    uint32_t slot = 0;
+    ncclComm_t comm = nullptr;
+    uint32_t launches = 0;
+
+    unsigned long long* nnz_counter() const { return counters.as<unsigned long long>(); }
+    unsigned long long* entries_counter(uint32_t s) const { return counters.as<unsigned long long>() + 1 + s; }
+    unsigned long long* entries_counter() const { return entries_counter(slot); }
+
+    uint32_t slice_rows() const { return V_pad / world; }
+    uint32_t row_begin() const { return std::min(V, rank * slice_rows()); }
+    uint32_t row_end() const { return std::min(V, (rank + 1) * slice_rows()); }
+
+    ~slda_engine() {
+        if (device >= 0) cudaSetDevice(device);
+        if (stream) cudaStreamSynchronize(stream);
+        for (auto& set : ring)
+            for (auto& e : set)
+                if (e) cudaEventDestroy(e);
+        if (comm) nccl().CommDestroy(comm);
+        if (stream) cudaStreamDestroy(stream);
+    }
+
+    void set_device() const { CK(cudaSetDevice(device)); }
+
+    // ---- CUB helpers (setup only) ----
+    template <class Fn>
+    void cub_call(Fn&& fn) {
+        size_t tmp = 0;
+        CK(fn(nullptr, tmp));
+        DevMem t;
+        t.alloc(tmp, nullptr);
+        CK(fn(t.p, tmp));
+    }
+    void exclusive_sum(const uint32_t* in, uint32_t* out, uint64_t n) {
+        if (n == 0) return;
+        cub_call([&](void* t, size_t& b) {
+            return cub::DeviceScan::ExclusiveSum(t, b, in, out, static_cast<int64_t>(n), stream);
+        });
+    }
+    template <class T> T d2h_scalar(const T* p) {
+        T v;
+        CK(cudaMemcpyAsync(&v, p, sizeof(T), cudaMemcpyDeviceToHost, stream));
+        CK(cudaStreamSynchronize(stream));
+        return v;
+    }
+
+    void configure(const slda_config& c, uint32_t vocab) {
+        if (c.num_topics == 0) validation("number of topics must be >= 1");
+        K = c.num_topics;
+        alpha = c.alpha <= 0.0 ? 50.0 / K : c.alpha;  // trainer.cpp:18
+        beta = c.beta;
+        if (!(beta > 0.0)) validation("beta must be > 0");
+        const uint32_t W = c.tree_branch ? c.tree_branch : 32u;
+        if (W < 2) validation("tree branch must be >= 2");
+        const uint64_t cap = static_cast<uint64_t>(W) * W * W;
+        if (K > cap)
+            validation("K=" + std::to_string(K) + " exceeds tree capacity W^3=" + std::to_string(cap));
+        if (K > 65536) validation("device engine supports K <= 65536 (16-bit topics)");
+        if (vocab == 0) validation("preprocess requires V >= 1");
+        world = c.world_size ? c.world_size : 1;
+        rank = c.rank;
+        if (rank >= world) validation("rank must be < world_size");
+        seed = c.seed;
+        falpha = static_cast<float>(alpha);
+        V = vocab;
+        V_pad = (V + world - 1) / world * world;
+        K_pad = (K + slda::kBlock - 1) / slda::kBlock * slda::kBlock;
+        n_l3 = K_pad / slda::kBlock;
+        l3_stride = (n_l3 + 3) / 4 * 4;
+        tbits = bits_for(K - 1 ? K - 1 : 1);
+        device = c.device;
+        if (device < 0) CK(cudaGetDevice(&device));
+        set_device();
+        CK(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+        for (auto& set : ring)
+            for (auto& e : set) CK(cudaEventCreate(&e));
+        if (world > 1) {
+            if (!c.nccl_id) validation("nccl_id required when world_size > 1");
+            ncclUniqueId id;
+            std::memcpy(&id, c.nccl_id, sizeof(id));
+            nccl_check(nccl().CommInitRank(&comm, static_cast<int>(world), id, static_cast<int>(rank)),
+                       "ncclCommInitRank");
+        }
+    }
+
+    void alloc_model() {
+        const size_t cells = static_cast<size_t>(V_pad) * K_pad;
+        B.alloc(cells * 4, &device_bytes);
+        bhat.alloc(cells * 4, &device_bytes);
+        l4.alloc(cells * 4, &device_bytes);
+        l3.alloc(static_cast<size_t>(V_pad) * l3_stride * 4, &device_bytes);
+        q.alloc(static_cast<size_t>(V_pad) * 4, &device_bytes);
+        colsum.alloc(static_cast<size_t>(K_pad) * 8, &device_bytes);
+        denom.alloc(static_cast<size_t>(K_pad) * 8, &device_bytes);
+        zv.alloc(static_cast<size_t>(K_pad) * 4, &device_bytes);
+        counters.alloc(8 * (1 + kRing), &device_bytes);
+        CK(cudaMemsetAsync(bhat.p, 0, bhat.bytes, stream));
+        CK(cudaMemsetAsync(l4.p, 0, l4.bytes, stream));
+        CK(cudaMemsetAsync(l3.p, 0, l3.bytes, stream));
+        CK(cudaMemsetAsync(q.p, 0, q.bytes, stream));
+    }
+
+    // ---- init_state (trainer.cpp:354-417) ----
+    void build(const slda_corpus_view& cv, const slda_config& c);
+    // ---- run_iteration (trainer.cpp:419-449) ----
+    void enqueue_iteration();
+    void m_step();
+    void ssc();
+};
+
+// ----------------------------------------------------------------- build --
+void slda_engine::build(const slda_corpus_view& cv, const slda_config& c) {
+    D_all = cv.num_docs;
+    doc_begin = cv.doc_begin;
+    doc_end = cv.doc_end;
+    if (doc_begin > doc_end || doc_end > D_all) validation("invalid document shard range");
+    D = doc_end - doc_begin;
+    T = cv.num_tokens;
+    if (T >= (1ull << 32)) validation("a single engine holds < 2^32 tokens; shard documents across GPUs");
+    if (T > 0 && !cv.tokens) validation("tokens is null");
+    id_base = cv.token_id_base;
+    configure(c, cv.vocab_size);
+    alloc_model();
+
+    // Copy the borrowed AoS tokens (sparselda::Token layout) and validate on device.
+    DevMem aos, val;
+    aos.alloc(T * 12, nullptr);
+    val.alloc(sizeof(slda::ValidateOut), nullptr);
+    if (T) CK(cudaMemcpyAsync(aos.p, cv.tokens, T * 12, cudaMemcpyHostToDevice, stream));
+    {
+        slda::ValidateOut init{~0ull, ~0ull, ~0ull, ~0ull, 0u};
+        CK(cudaMemcpyAsync(val.p, &init, sizeof(init), cudaMemcpyHostToDevice, stream));
+    }
+    CK(slda::launch_validate(aos.as<uint32_t>(), T, doc_begin, doc_end, V, K,
+                             val.as<slda::ValidateOut>(), stream));
+    slda::ValidateOut vo;
+    CK(cudaMemcpyAsync(&vo, val.p, sizeof(vo), cudaMemcpyDeviceToHost, stream));
+    CK(cudaStreamSynchronize(stream));
+    if (vo.bad_doc != ~0ull) validation("token " + std::to_string(vo.bad_doc) + ": doc outside the shard range");
+    if (vo.bad_word != ~0ull) validation("token " + std::to_string(vo.bad_word) + ": word id out of range");
+    bool draw = false;
+    if (c.init_mode == SLDA_INIT_DRAW) {
+        draw = true;
+    } else if (c.init_mode == SLDA_INIT_GIVEN) {
+        if (vo.first_invalid != ~0ull || vo.first_big != ~0ull)
+            validation("token topic exceeds configured K");
+    } else {
+        // trainer.cpp:369-378: the first invalid topic ends the K check.
+        if (vo.first_big < vo.first_invalid) validation("token topic exceeds configured K");
+        draw = vo.first_invalid != ~0ull;
+    }
+    doc_major = vo.unsorted == 0 && cv.token_ids == nullptr;
+
+    DevMem doc_local, word, topic_in;
+    doc_local.alloc(T * 4, nullptr);
+    word.alloc(T * 4, nullptr);
+    if (!draw) topic_in.alloc(T * 4, nullptr);
+    CK(slda::launch_deinterleave(aos.as<uint32_t>(), T, doc_begin, doc_local.as<uint32_t>(),
+                                 word.as<uint32_t>(), draw ? nullptr : topic_in.as<uint32_t>(), stream));
+    aos.release();
+
+    // Doc-grouped slot offsets (corpus.cpp:186-189).
+    doc_start.alloc((static_cast<size_t>(D) + 1) * 4, &device_bytes);
+    {
+        DevMem counts;
+        counts.alloc((static_cast<size_t>(D) + 1) * 4, nullptr);
+        CK(cudaMemsetAsync(counts.p, 0, counts.bytes, stream));
+        CK(slda::launch_doc_hist(doc_local.as<uint32_t>(), T, counts.as<uint32_t>(), stream));
+        exclusive_sum(counts.as<uint32_t>(), doc_start.as<uint32_t>(), static_cast<uint64_t>(D) + 1);
+        uint32_t max_len = 0;
+        if (D) {
+            DevMem mx;
+            mx.alloc(4, nullptr);
+            cub_call([&](void* t, size_t& b) {
+                return cub::DeviceReduce::Max(t, b, counts.as<uint32_t>(), mx.as<uint32_t>(),
+                                              static_cast<int64_t>(D), stream);
+            });
+            max_len = d2h_scalar(mx.as<uint32_t>());
+        }
+        if (tbits < 32 && (static_cast<uint64_t>(max_len) >> (32 - tbits)) != 0)
+            validation("document of length " + std::to_string(max_len) +
+                       " exceeds the packed C_dk count range at this K");
+    }
+
+    // Slot permutation for corpora that are not doc-sorted: stable by doc keeps
+    // corpus order within a document.
+    if (!doc_major) {
+        input_of_slot.alloc(T * 4, &device_bytes);
+        DevMem iota, keys_out;
+        iota.alloc(T * 4, nullptr);
+        keys_out.alloc(T * 4, nullptr);
+        CK(slda::launch_iota(iota.as<uint32_t>(), T, stream));
+        const int dbits = static_cast<int>(bits_for(D ? D - 1 : 1));
+        cub_call([&](void* t, size_t& b) {
+            return cub::DeviceRadixSort::SortPairs(t, b, doc_local.as<uint32_t>(), keys_out.as<uint32_t>(),
+                                                   iota.as<uint32_t>(), input_of_slot.as<uint32_t>(),
+                                                   static_cast<int64_t>(T), 0, dbits, stream);
+        });
+        // RNG element id per slot (trainer.cpp:275 keys streams by corpus position).
+        ids.alloc(T * 8, &device_bytes);
+        DevMem ids_in;
+        if (cv.token_ids) {
+            ids_in.alloc(T * 8, nullptr);
+            CK(cudaMemcpyAsync(ids_in.p, cv.token_ids, T * 8, cudaMemcpyHostToDevice, stream));
+        }
+        CK(slda::launch_ids_by_slot(cv.token_ids ? ids_in.as<uint64_t>() : nullptr,
+                                    input_of_slot.as<uint32_t>(), T, id_base, ids.as<uint64_t>(), stream));
+        CK(cudaStreamSynchronize(stream));
+    }
+
+    // PDOW: stable radix sort by (word, doc) of keys laid out in slot order
+    // == the reference's (word, doc, token_id) sort (corpus.cpp:157-175).
+    tok.alloc(T * 8, &device_bytes);
+    const uint32_t dbits = bits_for(D ? D - 1 : 1);
+    const uint32_t wbits = bits_for(V - 1 ? V - 1 : 1);
+    {
+        DevMem keys, keys_sorted, vals, slots_sorted, flags, seg_index;
+        keys.alloc(T * 8, nullptr);
+        keys_sorted.alloc(T * 8, nullptr);
+        vals.alloc(T * 4, nullptr);
+        slots_sorted.alloc(T * 4, nullptr);
+        CK(slda::launch_make_keys(word.as<uint32_t>(), doc_local.as<uint32_t>(),
+                                  doc_major ? nullptr : input_of_slot.as<uint32_t>(), T, dbits,
+                                  keys.as<unsigned long long>(), vals.as<uint32_t>(), stream));
+        if (T) {
+            cub_call([&](void* t, size_t& b) {
+                return cub::DeviceRadixSort::SortPairs(
+                    t, b, keys.as<unsigned long long>(), keys_sorted.as<unsigned long long>(),
+                    vals.as<uint32_t>(), slots_sorted.as<uint32_t>(), static_cast<int64_t>(T), 0,
+                    static_cast<int>(dbits + wbits), stream);
+            });
+        }
+        keys.release();
+        vals.release();
+        flags.alloc(T * 4, nullptr);
+        seg_index.alloc(T * 4, nullptr);
+        CK(slda::launch_make_tok(keys_sorted.as<unsigned long long>(), slots_sorted.as<uint32_t>(), T, dbits,
+                                 tok.as<uint2>(), flags.as<uint32_t>(), stream));
+        exclusive_sum(flags.as<uint32_t>(), seg_index.as<uint32_t>(), T);
+        nseg = T ? d2h_scalar(seg_index.as<uint32_t>() + T - 1) + d2h_scalar(flags.as<uint32_t>() + T - 1) : 0;
+        seg_word.alloc(static_cast<size_t>(nseg) * 4, &device_bytes);
+        seg_off.alloc(static_cast<size_t>(nseg) * 4, &device_bytes);
+        seg_len.alloc(static_cast<size_t>(nseg) * 4, &device_bytes);
+        schedule.alloc(static_cast<size_t>(nseg) * 4, &device_bytes);
+        CK(slda::launch_emit_segments(keys_sorted.as<unsigned long long>(), flags.as<uint32_t>(),
+                                      seg_index.as<uint32_t>(), T, dbits, seg_word.as<uint32_t>(),
+                                      seg_off.as<uint32_t>(), stream));
+    }
+    // build_schedule (corpus.cpp:200-210): heavy first, ties by ascending word.
+    if (nseg) {
+        DevMem skeys, skeys_sorted, svals, counts, starts;
+        skeys.alloc(static_cast<size_t>(nseg) * 8, nullptr);
+        skeys_sorted.alloc(static_cast<size_t>(nseg) * 8, nullptr);
+        svals.alloc(static_cast<size_t>(nseg) * 4, nullptr);
+        CK(slda::launch_segment_lengths(seg_off.as<uint32_t>(), nseg, T, seg_len.as<uint32_t>(),
+                                        skeys.as<unsigned long long>(), svals.as<uint32_t>(),
+                                        seg_word.as<uint32_t>(), nullptr, stream));
+        cub_call([&](void* t, size_t& b) {
+            return cub::DeviceRadixSort::SortPairs(t, b, skeys.as<unsigned long long>(),
+                                                   skeys_sorted.as<unsigned long long>(), svals.as<uint32_t>(),
+                                                   schedule.as<uint32_t>(), static_cast<int64_t>(nseg), 0, 64,
+                                                   stream);
+        });
+        counts.alloc(static_cast<size_t>(nseg) * 4, nullptr);
+        starts.alloc(static_cast<size_t>(nseg) * 4, nullptr);
+        CK(slda::launch_sched_counts(schedule.as<uint32_t>(), seg_len.as<uint32_t>(), nseg,
+                                     counts.as<uint32_t>(), stream));
+        exclusive_sum(counts.as<uint32_t>(), starts.as<uint32_t>(), nseg);
+        n_units = d2h_scalar(starts.as<uint32_t>() + nseg - 1) + d2h_scalar(counts.as<uint32_t>() + nseg - 1);
+        units.alloc(static_cast<size_t>(n_units) * sizeof(slda::Unit), &device_bytes);
+        CK(slda::launch_emit_units(schedule.as<uint32_t>(), seg_word.as<uint32_t>(), seg_off.as<uint32_t>(),
+                                   seg_len.as<uint32_t>(), starts.as<uint32_t>(), nseg,
+                                   units.as<slda::Unit>(), stream));
+    } else {
+        units.alloc(sizeof(slda::Unit), &device_bytes);
+    }
+
+    // C_dk rows: capacity len_d, 16-byte aligned (nnz_d <= len_d).
+    hdr.alloc(static_cast<size_t>(D) * 8, &device_bytes);
+    {
+        DevMem quads, row4;
+        quads.alloc((static_cast<size_t>(D) + 1) * 4, nullptr);
+        row4.alloc((static_cast<size_t>(D) + 1) * 4, nullptr);
+        CK(cudaMemsetAsync(quads.p, 0, quads.bytes, stream));
+        CK(slda::launch_row_quads(doc_start.as<uint32_t>(), D, quads.as<uint32_t>(), stream));
+        exclusive_sum(quads.as<uint32_t>(), row4.as<uint32_t>(), static_cast<uint64_t>(D) + 1);
+        const uint32_t total_quads = D ? d2h_scalar(row4.as<uint32_t>() + D) : 0;
+        A.alloc(static_cast<size_t>(total_quads) * 16, &device_bytes);
+        CK(slda::launch_init_hdr(row4.as<uint32_t>(), D, hdr.as<uint2>(), stream));
+    }
+    // Long documents take the CTA histogram path of SSC.
+    {
+        DevMem flags, iota, cnt;
+        flags.alloc(static_cast<size_t>(D) * 4, nullptr);
+        iota.alloc(static_cast<size_t>(D) * 4, nullptr);
+        cnt.alloc(8, nullptr);
+        long_docs.alloc(static_cast<size_t>(D) * 4, &device_bytes);
+        if (D) {
+            CK(slda::launch_long_flags(doc_start.as<uint32_t>(), D, flags.as<uint32_t>(), stream));
+            CK(slda::launch_iota(iota.as<uint32_t>(), D, stream));
+            cub_call([&](void* t, size_t& b) {
+                return cub::DeviceSelect::Flagged(t, b, iota.as<uint32_t>(), flags.as<uint32_t>(),
+                                                  long_docs.as<uint32_t>(), cnt.as<uint32_t>(),
+                                                  static_cast<int64_t>(D), stream);
+            });
+            n_long = d2h_scalar(cnt.as<uint32_t>());
+        }
+        if (n_long && static_cast<size_t>(K_pad) * 4 > 200 * 1024)
+            hist_scratch.alloc(static_cast<size_t>(std::min<uint32_t>(n_long, 296)) * K_pad * 4, &device_bytes);
+    }
+
+    // Initial topics (trainer.cpp:383-388 / corpus.cpp:87-96), by slot.
+    z.alloc(T * 2, &device_bytes);
+    if (draw) {
+        CK(slda::launch_init_topics(T, ids.p ? ids.as<uint64_t>() : nullptr, id_base, seed, K,
+                                    z.as<uint16_t>(), stream));
+    } else {
+        CK(slda::launch_given_topics(topic_in.as<uint32_t>(), doc_major ? nullptr : input_of_slot.as<uint32_t>(),
+                                     T, z.as<uint16_t>(), stream));
+    }
+    doc_local.release();
+    word.release();
+    topic_in.release();
+
+    // C_dk (rebuild_doc_topic), C_wk (count_chunk_into), phi + trees.
+    ssc();
+    CK(cudaMemsetAsync(B.p, 0, B.bytes, stream));
+    CK(slda::launch_recount(tok.as<uint2>(), units.as<slda::Unit>(), n_units, z.as<uint16_t>(),
+                            B.as<uint32_t>(), K_pad, stream));
+    m_step();
+    CK(cudaStreamSynchronize(stream));
+    nnz = d2h_scalar(nnz_counter());
+}
+
+void slda_engine::ssc() {
+    CK(cudaMemsetAsync(nnz_counter(), 0, 8, stream));
+    slda::SscArgs s{};
+    s.z = z.as<uint16_t>();
+    s.doc_start = doc_start.as<uint32_t>();
+    s.D = D;
+    s.hdr = hdr.as<uint2>();
+    s.A = A.as<uint32_t>();
+    s.tbits = tbits;
+    s.K_pad = K_pad;
+    s.long_docs = long_docs.as<uint32_t>();
+    s.n_long = n_long;
+    s.hist_scratch = hist_scratch.as<uint32_t>();
+    s.nnz_total = nnz_counter();
+    CK(slda::launch_ssc(s, stream));
+    launches += (D > 0) + (n_long > 0);
+}
+
+// M-step after the E-step's B: (reduce-scatter) -> colsum -> (all-reduce) -> phi/L4 on the
+// own word slice -> (all-gather).  preprocess (counts.cpp:37-63) + rebuild_trees.
+void slda_engine::m_step() {
+    const uint32_t r0 = row_begin(), r1 = row_end();
+    const size_t slice_cells = static_cast<size_t>(slice_rows()) * K_pad;
+    CK(cudaEventRecord(ev[3], stream));
+    if (world > 1) {
+        auto& n = nccl();
+        nccl_check(n.ReduceScatter(B.p, B.as<uint32_t>() + rank * slice_cells, slice_cells, ncclUint32,
+                                   ncclSum, comm, stream), "ncclReduceScatter(B)");
+    }
+    CK(cudaMemsetAsync(colsum.p, 0, colsum.bytes, stream));
+    CK(slda::launch_colsum(B.as<uint32_t>(), r0, r1, K_pad, colsum.as<unsigned long long>(), stream));
+    if (world > 1) {
+        nccl_check(nccl().AllReduce(colsum.p, colsum.p, K_pad, ncclUint64, ncclSum, comm, stream),
+                   "ncclAllReduce(C_k)");
+    }
+    CK(slda::launch_denom(colsum.as<unsigned long long>(), K, K_pad, V, beta, denom.as<double>(),
+                          zv.as<float>(), stream));
+    CK(cudaEventRecord(ev[4], stream));
+    CK(slda::launch_phi(B.as<uint32_t>(), denom.as<double>(), zv.as<float>(), bhat.as<float>(), l4.as<float>(),
+                        l3.as<float>(), q.as<float>(), r0, r1, K, K_pad, l3_stride, beta, falpha, stream));
+    launches += 3;
+    CK(cudaEventRecord(ev[5], stream));
+    if (world > 1) {
+        auto& n = nccl();
+        const size_t l3_slice = static_cast<size_t>(slice_rows()) * l3_stride;
+        nccl_check(n.GroupStart(), "ncclGroupStart");
+        nccl_check(n.AllGather(bhat.as<float>() + rank * slice_cells, bhat.p, slice_cells, ncclFloat32, comm,
+                               stream), "ncclAllGather(bhat)");
+        nccl_check(n.AllGather(l4.as<float>() + rank * slice_cells, l4.p, slice_cells, ncclFloat32, comm,
+                               stream), "ncclAllGather(L4)");
+        nccl_check(n.AllGather(l3.as<float>() + rank * l3_slice, l3.p, l3_slice, ncclFloat32, comm, stream),
+                   "ncclAllGather(L3)");
+        nccl_check(n.AllGather(q.as<float>() + rank * slice_rows(), q.p, slice_rows(), ncclFloat32, comm,
+                               stream), "ncclAllGather(Q)");
+        nccl_check(n.GroupEnd(), "ncclGroupEnd");
+    }
+    CK(cudaEventRecord(ev[6], stream));
+}
+
+// run_iteration (trainer.cpp:419-449) on the engine stream.
+void slda_engine::enqueue_iteration() {
+    launches = 0;
+    slot = iteration % kRing;
+    ev = ring[slot];
+    CK(cudaEventRecord(ev[0], stream));
+    CK(cudaMemsetAsync(B.p, 0, B.bytes, stream));  // reset_word_topic (counts.cpp:134-138)
+    CK(cudaMemsetAsync(entries_counter(), 0, 8, stream));
+    CK(cudaEventRecord(ev[1], stream));
+    slda::SamplerArgs a{};
+    a.tok = tok.as<uint2>();
+    a.units = units.as<slda::Unit>();
+    a.hdr = hdr.as<uint2>();
+    a.A = A.as<uint32_t>();
+    a.bhat = bhat.as<float>();
+    a.l4 = l4.as<float>();
+    a.l3 = l3.as<float>();
+    a.q = q.as<float>();
+    a.ids = ids.p ? ids.as<uint64_t>() : nullptr;
+    a.z = z.as<uint16_t>();
+    a.B = B.as<uint32_t>();
+    a.seed = seed;
+    a.id_base = id_base;
+    a.stream_kind = iteration;  // trainer.cpp:423
+    a.K = K;
+    a.K_pad = K_pad;
+    a.l3_stride = l3_stride;
+    a.n_l3 = n_l3;
+    a.tbits = tbits;
+    a.row_entries = entries_counter();
+    CK(slda::launch_sampler(a, n_units, stream));
+    launches += n_units > 0;
+    CK(cudaEventRecord(ev[2], stream));
+    ssc();  // the chunk's doc-topic rebuild (trainer.cpp:319-321), all documents
+    m_step();
+    ring_launches[slot] = launches;
+    ++iteration;
+}
+
+void slda_set_error_internal(const std::string& msg) { g_error = msg; }
+
+// =========================================================================
+extern "C" {
+
+const char* slda_last_error(void) { return g_error.c_str(); }
+uint32_t slda_abi_version(void) { return SLDA_ABI_VERSION; }
+
+int slda_create(const slda_corpus_view* corpus, const slda_config* config, slda_engine** out) {
+    return guarded([&] {
+        if (!corpus || !config || !out) validation("null argument");
+        *out = nullptr;
+        auto e = std::make_unique<slda_engine>();
+        e->build(*corpus, *config);
+        *out = e.release();
+    });
+}
+
+int slda_create_from_counts(uint32_t vocab_size, const uint32_t* word_topic, uint64_t num_tokens,
+                            uint32_t iteration, const slda_config* config, slda_engine** out) {
+    return guarded([&] {
+        if (!config || !out || !word_topic) validation("null argument");
+        *out = nullptr;
+        auto e = std::make_unique<slda_engine>();
+        e->configure(*config, vocab_size);
+        e->alloc_model();
+        e->iteration = iteration;
+        e->T = 0;
+        (void)num_tokens;
+        e->units.alloc(sizeof(slda::Unit), &e->device_bytes);
+        CK(cudaMemsetAsync(e->B.p, 0, e->B.bytes, e->stream));
+        CK(cudaMemcpy2DAsync(e->B.p, static_cast<size_t>(e->K_pad) * 4, word_topic,
+                             static_cast<size_t>(e->K) * 4, static_cast<size_t>(e->K) * 4, e->V,
+                             cudaMemcpyHostToDevice, e->stream));
+        if (e->world > 1) validation("create_from_counts is single-GPU");
+        e->m_step();
+        CK(cudaStreamSynchronize(e->stream));
+        *out = e.release();
+    });
+}
+
+void slda_destroy(slda_engine* e) { delete e; }
+
+int slda_iterate_async(slda_engine* e) {
+    return guarded([&] {
+        if (!e) validation("null engine");
+        e->set_device();
+        e->enqueue_iteration();
+    });
+}
+
+int slda_synchronize(slda_engine* e) {
+    return guarded([&] {
+        if (!e) validation("null engine");
+        CK(cudaStreamSynchronize(e->stream));
+    });
+}
+
+int slda_iterate(slda_engine* e, slda_iteration_stats* stats) {
+    return guarded([&] {
+        if (!e) validation("null engine");
+        e->set_device();
+        const auto start = std::chrono::steady_clock::now();
+        e->enqueue_iteration();
+        CK(cudaStreamSynchronize(e->stream));
+        unsigned long long nnz_local = 0;
+        CK(cudaMemcpy(&nnz_local, e->nnz_counter(), 8, cudaMemcpyDeviceToHost));
+        e->nnz = nnz_local;
+        const double elapsed = std::chrono::duration<double>(std::chrono::steady_clock::now() - start).count();
+        if (stats) {
+            float ms = 0;
+            CK(cudaEventElapsedTime(&ms, e->ev[0], e->ev[6]));
+            stats->iteration = e->iteration;
+            stats->tokens = e->T;
+            stats->elapsed_s = elapsed;
+            stats->mtokens_per_s = elapsed > 0 ? static_cast<double>(e->T) / elapsed / 1e6 : 0.0;
+            stats->mean_doc_topics = e->D ? static_cast<double>(nnz_local) / e->D : 0.0;
+            stats->device_ms = ms;
+        }
+    });
+}
+
+int slda_set_iteration(slda_engine* e, uint32_t iteration) {
+    return guarded([&] {
+        if (!e) validation("null engine");
+        e->iteration = iteration;
+    });
+}
+
+int slda_get_info(const slda_engine* e, slda_info* info) {
+    return guarded([&] {
+        if (!e || !info) validation("null argument");
+        info->num_docs = e->D_all;
+        info->vocab_size = e->V;
+        info->num_topics = e->K;
+        info->iteration = e->iteration;
+        info->num_tokens = e->T;
+        info->doc_begin = e->doc_begin;
+        info->doc_end = e->doc_end;
+        info->rank = e->rank;
+        info->world_size = e->world;
+        info->alpha = e->alpha;
+        info->beta = e->beta;
+        info->seed = e->seed;
+        info->num_segments = e->nseg;
+        info->num_units = e->n_units;
+        info->doc_topic_nnz = e->nnz;
+        info->device_bytes = e->device_bytes;
+        info->doc_major = e->doc_major ? 1u : 0u;
+        info->padded_topics = e->K_pad;
+    });
+}
+
+int slda_get_kernel_times_avg(const slda_engine* e, uint32_t last_n, slda_kernel_times* t) {
+    return guarded([&] {
+        if (!e || !t) validation("null argument");
+        if (last_n == 0 || last_n > slda_engine::kRing || last_n > e->iteration)
+            validation("last_n must be in [1, min(64, iterations run)]");
+        CK(cudaSetDevice(e->device));
+        CK(cudaStreamSynchronize(e->stream));
+        std::memset(t, 0, sizeof(*t));
+        std::vector<unsigned long long> entries(slda_engine::kRing);
+        CK(cudaMemcpy(entries.data(), e->entries_counter(0), 8 * slda_engine::kRing, cudaMemcpyDeviceToHost));
+        for (uint32_t i = 0; i < last_n; ++i) {
+            const uint32_t s = (e->iteration - 1 - i) % slda_engine::kRing;
+            cudaEvent_t* ev = const_cast<cudaEvent_t*>(e->ring[s]);
+            auto ms = [&](int a, int b) {
+                float x = 0;
+                CK(cudaEventElapsedTime(&x, ev[a], ev[b]));
+                return static_cast<double>(x);
+            };
+            t->reset_ms += ms(0, 1);
+            t->sampler_ms += ms(1, 2);
+            t->ssc_ms += ms(2, 3);
+            t->colsum_ms += ms(3, 4);
+            t->phi_ms += ms(4, 5);
+            t->comm_ms += ms(5, 6);
+            t->total_ms += ms(0, 6);
+            t->sampler_row_entries += entries[s];
+            t->launches += e->ring_launches[s];
+        }
+        const double n = last_n;
+        t->reset_ms /= n;
+        t->sampler_ms /= n;
+        t->ssc_ms /= n;
+        t->colsum_ms /= n;
+        t->phi_ms /= n;
+        t->comm_ms /= n;
+        t->total_ms /= n;
+        t->sampler_row_entries /= last_n;
+        t->launches /= last_n;
+    });
+}
+
+int slda_get_kernel_times(const slda_engine* e, slda_kernel_times* t) {
+    return slda_get_kernel_times_avg(e, 1, t);
+}
+
+void* slda_stream(const slda_engine* e) { return e ? static_cast<void*>(e->stream) : nullptr; }
+
+namespace {
+void copy_matrix(slda_engine* e, const DevMem& m, void* out) {
+    e->set_device();
+    CK(cudaStreamSynchronize(e->stream));
+    CK(cudaMemcpy2D(out, static_cast<size_t>(e->K) * 4, m.p, static_cast<size_t>(e->K_pad) * 4,
+                    static_cast<size_t>(e->K) * 4, e->V, cudaMemcpyDeviceToHost));
+}
+}  // namespace
+
+int slda_get_word_topic(slda_engine* e, uint32_t* out) {
+    return guarded([&] {
+        if (!e || !out) validation("null argument");
+        e->set_device();
+        if (e->world > 1) {
+            // After the reduce-scatter each rank owns its slice; gather the rest.
+            const size_t slice = static_cast<size_t>(e->slice_rows()) * e->K_pad;
+            nccl_check(nccl().AllGather(e->B.as<uint32_t>() + e->rank * slice, e->B.p, slice, ncclUint32,
+                                        e->comm, e->stream), "ncclAllGather(B)");
+        }
+        copy_matrix(e, e->B, out);
+    });
+}
+
+int slda_get_word_topic_prob(slda_engine* e, float* out) {
+    return guarded([&] {
+        if (!e || !out) validation("null argument");
+        copy_matrix(e, e->bhat, out);
+    });
+}
+
+int slda_get_tree_prefix(slda_engine* e, float* out) {
+    return guarded([&] {
+        if (!e || !out) validation("null argument");
+        copy_matrix(e, e->l4, out);
+    });
+}
+
+int slda_get_tree_mass(slda_engine* e, float* out) {
+    return guarded([&] {
+        if (!e || !out) validation("null argument");
+        e->set_device();
+        CK(cudaStreamSynchronize(e->stream));
+        CK(cudaMemcpy(out, e->q.p, static_cast<size_t>(e->V) * 4, cudaMemcpyDeviceToHost));
+    });
+}
+
+int slda_get_assignments(slda_engine* e, uint32_t* out) {
+    return guarded([&] {
+        if (!e || (!out && e->T)) validation("null argument");
+        e->set_device();
+        CK(cudaStreamSynchronize(e->stream));
+        std::vector<uint16_t> z(e->T);
+        if (e->T) CK(cudaMemcpy(z.data(), e->z.p, e->T * 2, cudaMemcpyDeviceToHost));
+        if (e->doc_major) {
+            for (uint64_t i = 0; i < e->T; ++i) out[i] = z[i];
+        } else {
+            std::vector<uint32_t> inv(e->T);
+            CK(cudaMemcpy(inv.data(), e->input_of_slot.p, e->T * 4, cudaMemcpyDeviceToHost));
+            for (uint64_t j = 0; j < e->T; ++j) out[inv[j]] = z[j];
+        }
+    });
+}
+
+int slda_get_doc_topic_nnz(slda_engine* e, uint64_t* nnz) {
+    return guarded([&] {
+        if (!e || !nnz) validation("null argument");
+        e->set_device();
+        CK(cudaStreamSynchronize(e->stream));
+        std::vector<uint2> hdr(e->D);
+        if (e->D) CK(cudaMemcpy(hdr.data(), e->hdr.p, static_cast<size_t>(e->D) * 8, cudaMemcpyDeviceToHost));
+        uint64_t n = 0;
+        for (const uint2& h : hdr) n += h.y;
+        *nnz = n;
+    });
+}
+
+int slda_get_doc_topic(slda_engine* e, uint64_t* row_offsets, uint32_t* topics, uint32_t* counts) {
+    return guarded([&] {
+        if (!e || !row_offsets) validation("null argument");
+        e->set_device();
+        CK(cudaStreamSynchronize(e->stream));
+        std::vector<uint2> hdr(e->D);
+        std::vector<uint32_t> A(e->A.bytes / 4);
+        if (e->D) CK(cudaMemcpy(hdr.data(), e->hdr.p, static_cast<size_t>(e->D) * 8, cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(A.data(), e->A.p, e->A.bytes, cudaMemcpyDeviceToHost));
+        const uint32_t mask = (1u << e->tbits) - 1u;
+        uint64_t pos = 0;
+        row_offsets[0] = 0;
+        for (uint32_t d = 0; d < e->D; ++d) {
+            const uint32_t* row = A.data() + static_cast<size_t>(hdr[d].x) * 4;
+            for (uint32_t i = 0; i < hdr[d].y; ++i, ++pos) {
+                topics[pos] = row[i] & mask;
+                counts[pos] = row[i] >> e->tbits;
+            }
+            row_offsets[d + 1] = pos;
+        }
+    });
+}
+
+int slda_get_pdow(slda_engine* e, uint32_t* sorted_doc, uint32_t* sorted_word, uint64_t* token_ids,
+                  uint32_t* shuffle_ptrs, uint32_t* doc_offsets, uint32_t* seg_word,
+                  uint32_t* seg_offset, uint32_t* seg_length, uint32_t* schedule) {
+    return guarded([&] {
+        if (!e) validation("null engine");
+        e->set_device();
+        CK(cudaStreamSynchronize(e->stream));
+        const uint64_t T = e->T;
+        std::vector<uint2> tok(T);
+        std::vector<uint32_t> dst(static_cast<size_t>(e->D) + 1), sw(e->nseg), so(e->nseg), sl(e->nseg),
+            sc(e->nseg);
+        std::vector<uint64_t> ids;
+        if (T) CK(cudaMemcpy(tok.data(), e->tok.p, T * 8, cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(dst.data(), e->doc_start.p, dst.size() * 4, cudaMemcpyDeviceToHost));
+        if (e->nseg) {
+            CK(cudaMemcpy(sw.data(), e->seg_word.p, e->nseg * 4ull, cudaMemcpyDeviceToHost));
+            CK(cudaMemcpy(so.data(), e->seg_off.p, e->nseg * 4ull, cudaMemcpyDeviceToHost));
+            CK(cudaMemcpy(sl.data(), e->seg_len.p, e->nseg * 4ull, cudaMemcpyDeviceToHost));
+            CK(cudaMemcpy(sc.data(), e->schedule.p, e->nseg * 4ull, cudaMemcpyDeviceToHost));
+        }
+        if (e->ids.p) {
+            ids.resize(T);
+            CK(cudaMemcpy(ids.data(), e->ids.p, T * 8, cudaMemcpyDeviceToHost));
+        }
+        // shuffle_ptrs: doc-grouped slot in word-major order per doc (corpus.cpp:190-195).
+        std::vector<uint32_t> cursor(dst.begin(), dst.end() - 1);
+        uint32_t seg = 0;
+        for (uint64_t i = 0; i < T; ++i) {
+            while (seg + 1 < e->nseg && so[seg + 1] <= i) ++seg;
+            if (sorted_doc) sorted_doc[i] = tok[i].x + e->doc_begin;
+            if (sorted_word) sorted_word[i] = sw[seg];
+            if (token_ids) token_ids[i] = ids.empty() ? e->id_base + tok[i].y : ids[tok[i].y];
+            if (shuffle_ptrs) shuffle_ptrs[i] = cursor[tok[i].x]++;
+        }
+        if (doc_offsets) std::memcpy(doc_offsets, dst.data(), dst.size() * 4);
+        if (seg_word) std::memcpy(seg_word, sw.data(), sw.size() * 4);
+        if (seg_offset) std::memcpy(seg_offset, so.data(), so.size() * 4);
+        if (seg_length) std::memcpy(seg_length, sl.data(), sl.size() * 4);
+        if (schedule) std::memcpy(schedule, sc.data(), sc.size() * 4);
+    });
+}
+
+int slda_heldout_ll(slda_engine* e, uint32_t num_docs, uint32_t vocab_size, uint64_t num_tokens,
+                    const uint32_t* tokens, uint32_t burn_in, uint64_t seed, double* per_token_ll,
+                    uint64_t* tokens_evaluated) {
+    return guarded([&] {
+        if (!e || !per_token_ll || !tokens_evaluated || (num_tokens && !tokens)) validation("null argument");
+        // eval.cpp:53-59 validations, HeldoutSet::from_corpus split (eval.cpp:14-28).
+        if (num_docs == 0) validation("held-out set is empty");
+        if (vocab_size != e->V) validation("held-out vocabulary size does not match model");
+        std::vector<uint64_t> est_off(static_cast<size_t>(num_docs) + 1, 0), evl_off(est_off);
+        std::vector<uint32_t> seen(num_docs, 0);
+        for (uint64_t t = 0; t < num_tokens; ++t) {
+            const uint32_t d = tokens[3 * t], w = tokens[3 * t + 1];
+            if (d >= num_docs || w >= vocab_size) validation("held-out token id out of range");
+            (seen[d]++ % 2 == 0 ? est_off : evl_off)[d + 1]++;
+        }
+        for (uint32_t d = 0; d < num_docs; ++d) {
+            est_off[d + 1] += est_off[d];
+            evl_off[d + 1] += evl_off[d];
+        }
+        const uint64_t n_est = est_off[num_docs], n_evl = evl_off[num_docs];
+        if (n_evl == 0) validation("held-out set has no evaluation tokens");
+        std::vector<uint32_t> est_w(n_est ? n_est : 1), evl_w(n_evl);
+        std::vector<uint64_t> ce(est_off.begin(), est_off.end() - 1), cv(evl_off.begin(), evl_off.end() - 1);
+        std::fill(seen.begin(), seen.end(), 0u);
+        uint64_t max_est = 0;
+        for (uint64_t t = 0; t < num_tokens; ++t) {
+            const uint32_t d = tokens[3 * t], w = tokens[3 * t + 1];
+            if (seen[d]++ % 2 == 0) est_w[ce[d]++] = w; else evl_w[cv[d]++] = w;
+        }
+        for (uint32_t d = 0; d < num_docs; ++d) max_est = std::max(max_est, est_off[d + 1] - est_off[d]);
+        uint32_t cap = 1;
+        while (cap < max_est) cap <<= 1;
+        if (static_cast<size_t>(cap) * 20 > 220 * 1024)
+            validation("held-out document estimation half longer than the device limit (8192)");
+
+        e->set_device();
+        DevMem d_est_off, d_evl_off, d_est, d_evl, d_ll, d_mass;
+        d_est_off.alloc(est_off.size() * 8, nullptr);
+        d_evl_off.alloc(evl_off.size() * 8, nullptr);
+        d_est.alloc(est_w.size() * 4, nullptr);
+        d_evl.alloc(evl_w.size() * 4, nullptr);
+        d_ll.alloc(n_evl * 8, nullptr);
+        d_mass.alloc(static_cast<size_t>(e->V) * 8, nullptr);
+        CK(cudaMemcpyAsync(d_est_off.p, est_off.data(), est_off.size() * 8, cudaMemcpyHostToDevice, e->stream));
+        CK(cudaMemcpyAsync(d_evl_off.p, evl_off.data(), evl_off.size() * 8, cudaMemcpyHostToDevice, e->stream));
+        CK(cudaMemcpyAsync(d_est.p, est_w.data(), est_w.size() * 4, cudaMemcpyHostToDevice, e->stream));
+        CK(cudaMemcpyAsync(d_evl.p, evl_w.data(), evl_w.size() * 4, cudaMemcpyHostToDevice, e->stream));
+        slda::HeldoutArgs a{};
+        a.est_off = d_est_off.as<uint64_t>();
+        a.est_word = d_est.as<uint32_t>();
+        a.evl_off = d_evl_off.as<uint64_t>();
+        a.evl_word = d_evl.as<uint32_t>();
+        a.bhat = e->bhat.as<float>();
+        a.l4 = e->l4.as<float>();
+        a.l3 = e->l3.as<float>();
+        a.q = e->q.as<float>();
+        a.row_mass = d_mass.as<double>();
+        a.ll_out = d_ll.as<double>();
+        a.seed = seed;
+        a.alpha = e->alpha;
+        a.burn_in = burn_in;
+        a.K = e->K;
+        a.K_pad = e->K_pad;
+        a.l3_stride = e->l3_stride;
+        a.n_l3 = e->n_l3;
+        a.cap = cap;
+        CK(slda::launch_heldout(a, num_docs, e->V, e->K, e->K_pad, d_mass.as<double>(), e->stream));
+        std::vector<double> ll(n_evl);
+        CK(cudaMemcpyAsync(ll.data(), d_ll.p, n_evl * 8, cudaMemcpyDeviceToHost, e->stream));
+        CK(cudaStreamSynchronize(e->stream));
+        // eval.cpp:110-130: per-doc sequential sum, then the doc sums in doc order.
+        double total = 0.0;
+        for (uint32_t d = 0; d < num_docs; ++d) {
+            double doc = 0.0;
+            if (est_off[d + 1] > est_off[d])
+                for (uint64_t j = evl_off[d]; j < evl_off[d + 1]; ++j) doc += ll[j];
+            total += doc;
+        }
+        *per_token_ll = total / static_cast<double>(n_evl);
+        *tokens_evaluated = n_evl;
+    });
+}
+
+int slda_nccl_unique_id(void* out128) {
+    return guarded([&] {
+        if (!out128) validation("null argument");
+        ncclUniqueId id;
+        nccl_check(nccl().GetUniqueId(&id), "ncclGetUniqueId");
+        std::memcpy(out128, &id, sizeof(id));
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,757 @@
+// kernels.cu -- sm_100a kernels of one ESCA iteration and its setup.
+//
+// Reference paths are relative to /root/reference/proj.  Each kernel names the
+// reference function it replaces.  See DESIGN.md for layouts and rooflines.
+#include "common.cuh"
+#include "kernels.hpp"
+
+namespace slda {
+
+namespace {
+
+inline uint32_t grid_for(uint64_t n, uint32_t threads, uint32_t cap = 148u * 32u) {
+    const uint64_t g = (n + threads - 1) / threads;
+    return static_cast<uint32_t>(g == 0 ? 1 : (g > cap ? cap : g));
+}
+
+__device__ __forceinline__ uint4 ldg_nc_v4(const uint4* p) {
+    uint4 r;
+    asm volatile("ld.global.nc.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "l"(p));
+    return r;
+}
+
+}  // namespace
+
+// ============================================================================
+// K3 sampler -- process_segment (trainer.cpp:265-291) + sample_token<float>
+// (sampler.hpp:166-204) + the C_wk accumulation of accumulate_word_topic
+// (counts.cpp:127-132).  One CTA per heavy-first work unit of one word; the
+// word's phi row and its L3 block maxima are staged in shared memory; each
+// thread samples whole tokens (lane-per-token) so that the sparse mass S and
+// the in-place prefix run as the reference's sequential f32 chains.
+// ============================================================================
+
+__device__ __forceinline__ float entry_mass(uint32_t e, uint32_t tbits, uint32_t tmask,
+                                            const float* s_bhat) {
+    return __fmul_rn(__uint2float_rn(e >> tbits), s_bhat[e & tmask]);
+}
+
+template <int NT>
+__global__ void __launch_bounds__(NT) sampler_kernel(SamplerArgs a) {
+    extern __shared__ __align__(16) float sm[];
+    float* s_bhat = sm;
+    float* s_l3 = sm + a.K_pad;
+
+    const Unit unit = a.units[blockIdx.x];
+    const uint32_t v = unit.word;
+    {
+        const float4* gb = reinterpret_cast<const float4*>(a.bhat + static_cast<size_t>(v) * a.K_pad);
+        float4* sb = reinterpret_cast<float4*>(s_bhat);
+        for (uint32_t i = threadIdx.x; i < a.K_pad / 4; i += NT) sb[i] = __ldg(gb + i);
+        const float4* gl = reinterpret_cast<const float4*>(a.l3 + static_cast<size_t>(v) * a.l3_stride);
+        float4* sl = reinterpret_cast<float4*>(s_l3);
+        for (uint32_t i = threadIdx.x; i < a.l3_stride / 4; i += NT) sl[i] = __ldg(gl + i);
+    }
+    const float qv = __ldg(a.q + v);
+    const float* l4row = a.l4 + static_cast<size_t>(v) * a.K_pad;
+    const float total = __ldg(l4row + a.K_pad - 1);  // padded with the row total
+    uint32_t* brow = a.B + static_cast<size_t>(v) * a.K_pad;
+    const uint32_t tbits = a.tbits;
+    const uint32_t tmask = (1u << tbits) - 1u;
+    const uint4* A4 = reinterpret_cast<const uint4*>(a.A);
+    unsigned long long entries = 0;
+    __syncthreads();
+
+    for (uint32_t i = threadIdx.x; i < unit.length; i += NT) {
+        const uint2 t = __ldg(a.tok + unit.offset + i);
+        const uint2 h = __ldg(a.hdr + t.x);
+        const uint64_t id = a.ids ? __ldg(a.ids + t.y) : a.id_base + t.y;
+        float ub, up;
+        draw2_f32(a.seed, a.stream_kind, id, ub, up);
+
+        // make_branch_context: S = sum_i f32(cnt_i) * bhat[top_i], ascending topic.
+        const uint4* row = A4 + h.x;
+        const uint32_t nq = (h.y + 3u) >> 2;  // rows are padded with zero-count entries
+        entries += h.y;
+        float s = 0.0f;
+        for (uint32_t j = 0; j < nq; ++j) {
+            const uint4 e = ldg_nc_v4(row + j);
+            s = __fadd_rn(s, entry_mass(e.x, tbits, tmask, s_bhat));
+            s = __fadd_rn(s, entry_mass(e.y, tbits, tmask, s_bhat));
+            s = __fadd_rn(s, entry_mass(e.z, tbits, tmask, s_bhat));
+            s = __fadd_rn(s, entry_mass(e.w, tbits, tmask, s_bhat));
+        }
+        uint32_t topic;
+        if (ub < __fdiv_rn(s, __fadd_rn(s, qv))) {
+            // Sparse branch: first running prefix >= p*S (prefix_search, sampler.hpp:18-41).
+            // Zero-count padding adds +0 and never precedes a real hit (x <= S).
+            const float x = __fmul_rn(up, s);
+            float run = 0.0f;
+            topic = 0;
+            bool found = false;
+            for (uint32_t j = 0; j < nq && !found; ++j) {
+                const uint4 e = ldg_nc_v4(row + j);
+                const uint32_t es[4] = {e.x, e.y, e.z, e.w};
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    run = __fadd_rn(run, entry_mass(es[u], tbits, tmask, s_bhat));
+                    if (!found && run >= x) {
+                        topic = es[u] & tmask;
+                        found = true;
+                    }
+                }
+            }
+        } else {
+            // Word branch: WaryTree::sample(p * total) == lower_bound(L4, x), clamped.
+            float x = __fmul_rn(up, total);
+            if (!(x <= total)) x = total;
+            uint32_t lo = 0, hi = a.n_l3;
+            while (lo < hi) {
+                const uint32_t mid = (lo + hi) >> 1;
+                if (s_l3[mid] >= x) hi = mid; else lo = mid + 1;
+            }
+            const float4* blk = reinterpret_cast<const float4*>(l4row + lo * kBlock);
+            uint32_t below = 0;
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const float4 f = __ldg(blk + u);
+                below += (f.x < x) + (f.y < x) + (f.z < x) + (f.w < x);
+            }
+            topic = lo * kBlock + below;
+            if (topic >= a.K) topic = a.K - 1;
+        }
+        a.z[t.y] = static_cast<uint16_t>(topic);
+        atomicAdd(brow + topic, 1u);
+    }
+    if (a.row_entries) {
+        // One atomic per warp.
+        for (int o = 16; o > 0; o >>= 1) entries += __shfl_xor_sync(0xffffffffu, entries, o);
+        if (lane_id() == 0) atomicAdd(a.row_entries, entries);
+    }
+}
+
+cudaError_t launch_sampler(const SamplerArgs& a, uint32_t n_units, cudaStream_t s) {
+    if (n_units == 0) return cudaSuccess;
+    const size_t smem = sizeof(float) * (static_cast<size_t>(a.K_pad) + a.l3_stride);
+    if (smem <= 48 * 1024) {
+        sampler_kernel<256><<<n_units, 256, smem, s>>>(a);
+    } else {
+        static bool configured = false;
+        if (!configured) {
+            cudaFuncSetAttribute(sampler_kernel<512>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 227 * 1024);
+            configured = true;
+        }
+        sampler_kernel<512><<<n_units, 512, smem, s>>>(a);
+    }
+    return cudaGetLastError();
+}
+
+// ============================================================================
+// K4 SSC -- rebuild_doc_topic (counts.cpp:103-125) + segmented_count (:65-94).
+// Topics are already doc-grouped (the sampler writes them by slot), so the
+// shuffle is fused into the sampler's store.  Warp per document: bitonic sort
+// in shared memory, then a ballot run-length pass emitting (topic asc, count).
+// Long documents: CTA per document, K-bin histogram + ordered compaction.
+// ============================================================================
+
+constexpr int kSscWarps = 8;
+
+__global__ void __launch_bounds__(kSscWarps * 32) ssc_warp_kernel(SscArgs a) {
+    __shared__ uint32_t s_keys[kSscWarps][kSscWarpCap];
+    __shared__ uint32_t s_start[kSscWarps][kSscWarpCap];
+    const uint32_t w = threadIdx.x >> 5, lane = lane_id();
+    uint32_t* keys = s_keys[w];
+    uint32_t* starts = s_start[w];
+    unsigned long long nnz_acc = 0;
+    const uint32_t gw = blockIdx.x * kSscWarps + w, nw = gridDim.x * kSscWarps;
+    for (uint32_t d = gw; d < a.D; d += nw) {
+        const uint32_t s0 = __ldg(a.doc_start + d);
+        const uint32_t n = __ldg(a.doc_start + d + 1) - s0;
+        if (n > kSscWarpCap) continue;  // ssc_long_kernel
+        const uint32_t row = a.hdr[d].x * 4u;
+        if (n == 0) {
+            if (lane == 0) a.hdr[d].y = 0;
+            continue;
+        }
+        uint32_t N = 1;
+        while (N < n) N <<= 1;
+        for (uint32_t i = lane; i < N; i += 32) keys[i] = i < n ? a.z[s0 + i] : 0xFFFFFFFFu;
+        __syncwarp();
+        for (uint32_t k = 2; k <= N; k <<= 1) {
+            for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+                for (uint32_t i = lane; i < N; i += 32) {
+                    const uint32_t ixj = i ^ j;
+                    if (ixj > i) {
+                        const uint32_t x = keys[i], y = keys[ixj];
+                        const bool up = (i & k) == 0;
+                        if ((x > y) == up) {
+                            keys[i] = y;
+                            keys[ixj] = x;
+                        }
+                    }
+                }
+                __syncwarp();
+            }
+        }
+        uint32_t nnz = 0;
+        for (uint32_t base = 0; base < n; base += 32) {
+            const uint32_t i = base + lane;
+            const bool start = i < n && (i == 0 || keys[i] != keys[i - 1]);
+            const uint32_t ballot = __ballot_sync(0xffffffffu, start);
+            if (start) starts[nnz + __popc(ballot & ((1u << lane) - 1u))] = i;
+            nnz += __popc(ballot);
+        }
+        __syncwarp();
+        for (uint32_t r = lane; r < nnz; r += 32) {
+            const uint32_t st = starts[r];
+            const uint32_t en = r + 1 < nnz ? starts[r + 1] : n;
+            a.A[row + r] = keys[st] | ((en - st) << a.tbits);
+        }
+        const uint32_t padded = (nnz + 3u) & ~3u;
+        for (uint32_t r = nnz + lane; r < padded; r += 32) a.A[row + r] = 0u;
+        if (lane == 0) {
+            a.hdr[d].y = nnz;
+            nnz_acc += nnz;
+        }
+        __syncwarp();
+    }
+    if (lane == 0 && nnz_acc) atomicAdd(a.nnz_total, nnz_acc);
+}
+
+// Long documents: one CTA per document (grid-stride over the long-doc list).
+template <bool kSmemHist>
+__global__ void __launch_bounds__(256) ssc_long_kernel(SscArgs a) {
+    extern __shared__ __align__(16) uint32_t s_dyn[];
+    __shared__ uint32_t s_scan[256];
+    uint32_t* hist = kSmemHist ? s_dyn : a.hist_scratch + static_cast<size_t>(blockIdx.x) * a.K_pad;
+    const uint32_t tid = threadIdx.x;
+    const uint32_t per = (a.K_pad + 255u) / 256u;
+    for (uint32_t li = blockIdx.x; li < a.n_long; li += gridDim.x) {
+        const uint32_t d = a.long_docs[li];
+        const uint32_t s0 = a.doc_start[d];
+        const uint32_t n = a.doc_start[d + 1] - s0;
+        const uint32_t row = a.hdr[d].x * 4u;
+        for (uint32_t k = tid; k < a.K_pad; k += 256) hist[k] = 0;
+        __syncthreads();
+        for (uint32_t i = tid; i < n; i += 256) atomicAdd(hist + a.z[s0 + i], 1u);
+        __syncthreads();
+        const uint32_t b0 = tid * per, b1 = min(a.K_pad, b0 + per);
+        uint32_t mine = 0;
+        for (uint32_t k = b0; k < b1; ++k) mine += hist[k] != 0;
+        s_scan[tid] = mine;
+        __syncthreads();
+        for (uint32_t off = 1; off < 256; off <<= 1) {
+            const uint32_t add = tid >= off ? s_scan[tid - off] : 0;
+            __syncthreads();
+            s_scan[tid] += add;
+            __syncthreads();
+        }
+        const uint32_t nnz = s_scan[255];
+        uint32_t pos = s_scan[tid] - mine;
+        for (uint32_t k = b0; k < b1; ++k) {
+            const uint32_t c = hist[k];
+            if (c) a.A[row + pos++] = k | (c << a.tbits);
+        }
+        const uint32_t padded = (nnz + 3u) & ~3u;
+        for (uint32_t r = nnz + tid; r < padded; r += 256) a.A[row + r] = 0u;
+        if (tid == 0) {
+            a.hdr[d].y = nnz;
+            atomicAdd(a.nnz_total, static_cast<unsigned long long>(nnz));
+        }
+        __syncthreads();
+    }
+}
+
+cudaError_t launch_ssc(const SscArgs& a, cudaStream_t s) {
+    if (a.D > 0) {
+        const uint32_t blocks = grid_for(a.D, kSscWarps, 148u * 8u);
+        ssc_warp_kernel<<<blocks, kSscWarps * 32, 0, s>>>(a);
+    }
+    if (a.n_long > 0) {
+        const size_t smem = sizeof(uint32_t) * a.K_pad;
+        const uint32_t blocks = a.n_long < 148u * 2u ? a.n_long : 148u * 2u;
+        if (smem <= 200 * 1024) {
+            static bool configured = false;
+            if (!configured) {
+                cudaFuncSetAttribute(ssc_long_kernel<true>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+                configured = true;
+            }
+            ssc_long_kernel<true><<<blocks, 256, smem, s>>>(a);
+        } else {
+            ssc_long_kernel<false><<<blocks, 256, 0, s>>>(a);
+        }
+    }
+    return cudaGetLastError();
+}
+
+// ============================================================================
+// K5/K6 -- preprocess (counts.cpp:37-63) + rebuild_trees (trainer.cpp:237-248,
+// sampler.hpp:58-90, :142-149).  colsum: integer column sums (order-free).
+// phi: thread per word row, 32-column tiles transposed through shared memory
+// so global traffic is coalesced while each thread runs the row's sequential
+// f32 prefix (the L4 level) exactly as WaryTree::build.
+// ============================================================================
+
+__global__ void __launch_bounds__(256) colsum_kernel(const uint32_t* __restrict__ B, uint32_t row_begin,
+                                                     uint32_t row_end, uint32_t cols4,
+                                                     uint32_t rows_per_chunk,
+                                                     unsigned long long* __restrict__ colsum) {
+    __shared__ unsigned long long s_acc[256][4];
+    const uint32_t c4 = blockIdx.x * blockDim.x + threadIdx.x;
+    const uint32_t r0 = row_begin + blockIdx.y * rows_per_chunk;
+    const uint32_t r1 = min(row_end, r0 + rows_per_chunk);
+    unsigned long long acc[4] = {0, 0, 0, 0};
+    if (c4 < cols4) {
+        const uint4* B4 = reinterpret_cast<const uint4*>(B);
+        for (uint32_t r = r0 + threadIdx.y; r < r1; r += blockDim.y) {
+            const uint4 b = __ldg(B4 + static_cast<size_t>(r) * cols4 + c4);
+            acc[0] += b.x; acc[1] += b.y; acc[2] += b.z; acc[3] += b.w;
+        }
+    }
+    const uint32_t tid = threadIdx.y * blockDim.x + threadIdx.x;
+    for (int j = 0; j < 4; ++j) s_acc[tid][j] = acc[j];
+    __syncthreads();
+    if (threadIdx.y == 0 && c4 < cols4) {
+        for (uint32_t y = 1; y < blockDim.y; ++y)
+            for (int j = 0; j < 4; ++j) acc[j] += s_acc[y * blockDim.x + threadIdx.x][j];
+        for (int j = 0; j < 4; ++j)
+            if (acc[j]) atomicAdd(colsum + 4 * c4 + j, acc[j]);
+    }
+}
+
+cudaError_t launch_colsum(const uint32_t* B, uint32_t row_begin, uint32_t row_end, uint32_t K_pad,
+                          unsigned long long* colsum, cudaStream_t s) {
+    if (row_end <= row_begin) return cudaSuccess;
+    const uint32_t cols4 = K_pad / 4;
+    const uint32_t bx = cols4 < 256 ? cols4 : 256;
+    const uint32_t by = 256 / bx;
+    const uint32_t gx = (cols4 + bx - 1) / bx;
+    const uint32_t rows = row_end - row_begin;
+    // ~4 waves of CTAs.
+    uint32_t gy = (148u * 8u + gx - 1) / gx;
+    uint32_t per = (rows + gy - 1) / gy;
+    if (per < by) per = by;
+    gy = (rows + per - 1) / per;
+    colsum_kernel<<<dim3(gx, gy), dim3(bx, by), 0, s>>>(B, row_begin, row_end, cols4, per, colsum);
+    return cudaGetLastError();
+}
+
+// denom_k = f64(colsum_k) + V*beta (counts.cpp:49-50); zero-count cells share
+// bhat = f32(beta / denom_k), so the phi kernel divides only non-zero cells.
+__global__ void denom_kernel(const unsigned long long* colsum, uint32_t K, uint32_t K_pad, uint32_t V,
+                             double beta, double* denom, float* zv) {
+    const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= K_pad) return;
+    if (k < K) {
+        const double d = __dadd_rn(static_cast<double>(colsum[k]),
+                                   __dmul_rn(static_cast<double>(V), beta));
+        denom[k] = d;
+        zv[k] = __double2float_rn(__ddiv_rn(__dadd_rn(0.0, beta), d));
+    } else {
+        denom[k] = 1.0;
+        zv[k] = 0.0f;
+    }
+}
+
+cudaError_t launch_denom(const unsigned long long* colsum, uint32_t K, uint32_t K_pad, uint32_t V,
+                         double beta, double* denom, float* zv, cudaStream_t s) {
+    denom_kernel<<<(K_pad + 255) / 256, 256, 0, s>>>(colsum, K, K_pad, V, beta, denom, zv);
+    return cudaGetLastError();
+}
+
+constexpr int kPhiRows = 128;
+
+__global__ void __launch_bounds__(kPhiRows) phi_kernel(const uint32_t* __restrict__ B,
+                                                       const double* __restrict__ denom,
+                                                       const float* __restrict__ zv,
+                                                       float* __restrict__ bhat, float* __restrict__ l4,
+                                                       float* __restrict__ l3, float* __restrict__ q,
+                                                       uint32_t row_begin, uint32_t row_end, uint32_t K,
+                                                       uint32_t K_pad, uint32_t l3_stride, double beta,
+                                                       float falpha) {
+    // t_bh aliases t_in: thread r overwrites cell [r][c] only after reading it.
+    __shared__ uint32_t t_in[kPhiRows][kBlock + 1];
+    __shared__ float t_l4[kPhiRows][kBlock + 1];
+    float(*t_bh)[kBlock + 1] = reinterpret_cast<float(*)[kBlock + 1]>(t_in);
+    const uint32_t r = threadIdx.x;
+    const uint32_t v0 = row_begin + blockIdx.x * kPhiRows;
+    const uint32_t v = v0 + r;
+    float run = 0.0f;
+    for (uint32_t c0 = 0; c0 < K_pad; c0 += kBlock) {
+#pragma unroll 8
+        for (uint32_t it = 0; it < kBlock; ++it) {
+            const uint32_t idx = it * kPhiRows + r;
+            const uint32_t rr = idx >> 5, cc = idx & 31u;
+            const uint32_t vv = v0 + rr;
+            t_in[rr][cc] = vv < row_end ? __ldg(B + static_cast<size_t>(vv) * K_pad + c0 + cc) : 0u;
+        }
+        __syncthreads();
+#pragma unroll 4
+        for (uint32_t c = 0; c < kBlock; ++c) {
+            const uint32_t k = c0 + c;
+            float bh = 0.0f;
+            if (k < K) {
+                const uint32_t cnt = t_in[r][c];
+                bh = cnt ? __double2float_rn(__ddiv_rn(__dadd_rn(static_cast<double>(cnt), beta),
+                                                       __ldg(denom + k)))
+                         : __ldg(zv + k);
+                run = __fadd_rn(run, bh);
+            }
+            t_bh[r][c] = bh;
+            t_l4[r][c] = run;
+        }
+        if (v < row_end) l3[static_cast<size_t>(v) * l3_stride + c0 / kBlock] = run;
+        __syncthreads();
+#pragma unroll 8
+        for (uint32_t it = 0; it < kBlock; ++it) {
+            const uint32_t idx = it * kPhiRows + r;
+            const uint32_t rr = idx >> 5, cc = idx & 31u;
+            const uint32_t vv = v0 + rr;
+            if (vv < row_end) {
+                const size_t o = static_cast<size_t>(vv) * K_pad + c0 + cc;
+                bhat[o] = t_bh[rr][cc];
+                l4[o] = t_l4[rr][cc];
+            }
+        }
+        __syncthreads();  // the next tile load overwrites t_in (== t_bh)
+    }
+    if (v < row_end) {
+        for (uint32_t j = K_pad / kBlock; j < l3_stride; ++j) l3[static_cast<size_t>(v) * l3_stride + j] = run;
+        q[v] = __fmul_rn(falpha, run);  // trainer.cpp:245
+    }
+}
+
+cudaError_t launch_phi(const uint32_t* B, const double* denom, const float* zv, float* bhat,
+                       float* l4, float* l3, float* q, uint32_t row_begin, uint32_t row_end,
+                       uint32_t K, uint32_t K_pad, uint32_t l3_stride, double beta, float falpha,
+                       cudaStream_t s) {
+    if (row_end <= row_begin) return cudaSuccess;
+    const uint32_t blocks = (row_end - row_begin + kPhiRows - 1) / kPhiRows;
+    phi_kernel<<<blocks, kPhiRows, 0, s>>>(B, denom, zv, bhat, l4, l3, q, row_begin, row_end, K, K_pad,
+                                           l3_stride, beta, falpha);
+    return cudaGetLastError();
+}
+
+// ============================================================================
+// K1/K2 setup -- build_chunks (corpus.cpp:125-198), build_schedule (:200-210),
+// init_assignments (corpus.cpp:87-96), count_chunk_into (trainer.cpp:223-235).
+// ============================================================================
+
+__global__ void deinterleave_kernel(const uint32_t* __restrict__ aos, uint64_t T, uint32_t doc_begin,
+                                    uint32_t* doc_local, uint32_t* word, uint32_t* topic) {
+    for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < T;
+         i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        doc_local[i] = aos[3 * i] - doc_begin;
+        word[i] = aos[3 * i + 1];
+        if (topic) topic[i] = aos[3 * i + 2];
+    }
+}
+
+cudaError_t launch_deinterleave(const uint32_t* aos, uint64_t T, uint32_t doc_begin,
+                                uint32_t* doc_local, uint32_t* word, uint32_t* topic,
+                                cudaStream_t s) {
+    if (T == 0) return cudaSuccess;
+    deinterleave_kernel<<<grid_for(T, 256), 256, 0, s>>>(aos, T, doc_begin, doc_local, word, topic);
+    return cudaGetLastError();
+}
+
+__global__ void check_sorted_kernel(const uint32_t* doc_local, uint64_t T, uint32_t* flag) {
+    for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x + 1; i < T;
+         i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        if (doc_local[i] < doc_local[i - 1]) *flag = 1u;
+    }
+}
+
+cudaError_t launch_check_sorted(const uint32_t* doc_local, uint64_t T, uint32_t* unsorted_flag,
+                                cudaStream_t s) {
+    if (T < 2) return cudaSuccess;
+    check_sorted_kernel<<<grid_for(T, 256), 256, 0, s>>>(doc_local, T, unsorted_flag);
+    return cudaGetLastError();
+}
+
+__global__ void doc_hist_kernel(const uint32_t* doc_local, uint64_t T, uint32_t* counts) {
+    for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < T;
+         i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+        atomicAdd(counts + doc_local[i], 1u);
+}
+
+cudaError_t launch_doc_hist(const uint32_t* doc_local, uint64_t T, uint32_t* counts, cudaStream_t s) {
+    if (T == 0) return cudaSuccess;
+    doc_hist_kernel<<<grid_for(T, 256), 256, 0, s>>>(doc_local, T, counts);
+    return cudaGetLastError();
+}
+
+__global__ void iota_kernel(uint32_t* out, uint64_t n) {
+    for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+        out[i] = static_cast<uint32_t>(i);
+}
+
+cudaError_t launch_iota(uint32_t* out, uint64_t n, cudaStream_t s) {
+    if (n == 0) return cudaSuccess;
+    iota_kernel<<<grid_for(n, 256), 256, 0, s>>>(out, n);
+    return cudaGetLastError();
+}
+
+__global__ void invert_perm_kernel(const uint32_t* input_of_slot, uint64_t T, uint32_t* slot_of_input) {
+    for (uint64_t j = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; j < T;
+         j += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+        slot_of_input[input_of_slot[j]] = static_cast<uint32_t>(j);
+}
+
+cudaError_t launch_invert_perm(const uint32_t* input_of_slot, uint64_t T, uint32_t* slot_of_input,
+                               cudaStream_t s) {
+    if (T == 0) return cudaSuccess;
+    invert_perm_kernel<<<grid_for(T, 256), 256, 0, s>>>(input_of_slot, T, slot_of_input);
+    return cudaGetLastError();
+}
+
+// Keys in slot order so that equal (word, doc) keep slot (== corpus) order
+// under the stable radix sort: the reference's (word, doc, token_id) order
+// (corpus.cpp:157-167).
+__global__ void make_keys_kernel(const uint32_t* word, const uint32_t* doc_local,
+                                 const uint32_t* input_of_slot, uint64_t T, uint32_t dbits,
+                                 unsigned long long* keys, uint32_t* vals) {
+    for (uint64_t j = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; j < T;
+         j += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        const uint64_t i = input_of_slot ? input_of_slot[j] : j;
+        keys[j] = (static_cast<unsigned long long>(word[i]) << dbits) | doc_local[i];
+        vals[j] = static_cast<uint32_t>(j);
+    }
+}
+
+cudaError_t launch_make_keys(const uint32_t* word, const uint32_t* doc_local,
+                             const uint32_t* input_of_slot, uint64_t T, uint32_t dbits,
+                             unsigned long long* keys, uint32_t* vals, cudaStream_t s) {
+    if (T == 0) return cudaSuccess;
+    make_keys_kernel<<<grid_for(T, 256), 256, 0, s>>>(word, doc_local, input_of_slot, T, dbits, keys, vals);
+    return cudaGetLastError();
+}
+
+__global__ void make_tok_kernel(const unsigned long long* keys, const uint32_t* slots, uint64_t T,
+                                uint32_t dbits, uint2* tok, uint32_t* seg_flag) {
+    const unsigned long long dmask = (1ull << dbits) - 1ull;
+    for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < T;
+         i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        const unsigned long long k = keys[i];
+        tok[i] = make_uint2(static_cast<uint32_t>(k & dmask), slots[i]);
+        seg_flag[i] = (i == 0 || (keys[i - 1] >> dbits) != (k >> dbits)) ? 1u : 0u;
+    }
+}
+
+cudaError_t launch_make_tok(const unsigned long long* keys, const uint32_t* slots, uint64_t T,
+                            uint32_t dbits, uint2* tok, uint32_t* seg_flag, cudaStream_t s) {
+    if (T == 0) return cudaSuccess;
+    make_tok_kernel<<<grid_for(T, 256), 256, 0, s>>>(keys, slots, T, dbits, tok, seg_flag);
+    return cudaGetLastError();
+}
+
+__global__ void emit_segments_kernel(const unsigned long long* keys, const uint32_t* seg_flag,
+                                     const uint32_t* seg_index, uint64_t T, uint32_t dbits,
+                                     uint32_t* seg_word, uint32_t* seg_off) {
+    for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < T;
+         i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        if (seg_flag[i]) {
+            const uint32_t s = seg_index[i];
+            seg_word[s] = static_cast<uint32_t>(keys[i] >> dbits);
+            seg_off[s] = static_cast<uint32_t>(i);
+        }
+    }
+}
+
+cudaError_t launch_emit_segments(const unsigned long long* keys, const uint32_t* seg_flag,
+                                 const uint32_t* seg_index, uint64_t T, uint32_t dbits,
+                                 uint32_t* seg_word, uint32_t* seg_off, cudaStream_t s) {
+    if (T == 0) return cudaSuccess;
+    emit_segments_kernel<<<grid_for(T, 256), 256, 0, s>>>(keys, seg_flag, seg_index, T, dbits, seg_word,
+                                                         seg_off);
+    return cudaGetLastError();
+}
+
+// build_schedule sort key: (length desc, word asc) -- corpus.cpp:201-205.
+__global__ void segment_lengths_kernel(const uint32_t* seg_off, uint32_t nseg, uint64_t T,
+                                       uint32_t* seg_len, unsigned long long* sched_keys,
+                                       uint32_t* sched_vals, const uint32_t* seg_word,
+                                       uint32_t* unit_count) {
+    const uint32_t s = blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= nseg) return;
+    const uint64_t end = s + 1 < nseg ? seg_off[s + 1] : T;
+    const uint32_t len = static_cast<uint32_t>(end - seg_off[s]);
+    seg_len[s] = len;
+    sched_keys[s] = (static_cast<unsigned long long>(0xFFFFFFFFu - len) << 32) | seg_word[s];
+    sched_vals[s] = s;
+    if (unit_count) unit_count[s] = (len + kUnitMaxTokens - 1) / kUnitMaxTokens;
+}
+
+cudaError_t launch_segment_lengths(const uint32_t* seg_off, uint32_t nseg, uint64_t T,
+                                   uint32_t* seg_len, unsigned long long* sched_keys,
+                                   uint32_t* sched_vals, const uint32_t* seg_word,
+                                   uint32_t* unit_count, cudaStream_t s) {
+    if (nseg == 0) return cudaSuccess;
+    segment_lengths_kernel<<<(nseg + 255) / 256, 256, 0, s>>>(seg_off, nseg, T, seg_len, sched_keys,
+                                                             sched_vals, seg_word, unit_count);
+    return cudaGetLastError();
+}
+
+// unit_count here is indexed by schedule position (permuted by the caller).
+__global__ void emit_units_kernel(const uint32_t* schedule, const uint32_t* seg_word,
+                                  const uint32_t* seg_off, const uint32_t* seg_len,
+                                  const uint32_t* unit_start, uint32_t nseg, Unit* units) {
+    const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= nseg) return;
+    const uint32_t s = schedule[p];
+    const uint32_t len = seg_len[s];
+    uint32_t u = unit_start[p];
+    for (uint32_t o = 0; o < len; o += kUnitMaxTokens, ++u) {
+        const uint32_t l = len - o < kUnitMaxTokens ? len - o : kUnitMaxTokens;
+        units[u] = Unit{seg_word[s], seg_off[s] + o, l, 0u};
+    }
+}
+
+cudaError_t launch_emit_units(const uint32_t* schedule, const uint32_t* seg_word,
+                              const uint32_t* seg_off, const uint32_t* seg_len,
+                              const uint32_t* unit_start, uint32_t nseg, Unit* units,
+                              cudaStream_t s) {
+    if (nseg == 0) return cudaSuccess;
+    emit_units_kernel<<<(nseg + 255) / 256, 256, 0, s>>>(schedule, seg_word, seg_off, seg_len,
+                                                        unit_start, nseg, units);
+    return cudaGetLastError();
+}
+
+// A row capacity in uint4 units: nnz_d <= len_d (test_counts.cpp:149-150).
+__global__ void row_quads_kernel(const uint32_t* doc_start, uint32_t D, uint32_t* quads) {
+    const uint32_t d = blockIdx.x * blockDim.x + threadIdx.x;
+    if (d >= D) return;
+    quads[d] = (doc_start[d + 1] - doc_start[d] + 3u) >> 2;
+}
+
+cudaError_t launch_row_quads(const uint32_t* doc_start, uint32_t D, uint32_t* quads, cudaStream_t s) {
+    if (D == 0) return cudaSuccess;
+    row_quads_kernel<<<(D + 255) / 256, 256, 0, s>>>(doc_start, D, quads);
+    return cudaGetLastError();
+}
+
+__global__ void init_hdr_kernel(const uint32_t* row4, uint32_t D, uint2* hdr) {
+    const uint32_t d = blockIdx.x * blockDim.x + threadIdx.x;
+    if (d >= D) return;
+    hdr[d] = make_uint2(row4[d], 0u);
+}
+
+cudaError_t launch_init_hdr(const uint32_t* row4, uint32_t D, uint2* hdr, cudaStream_t s) {
+    if (D == 0) return cudaSuccess;
+    init_hdr_kernel<<<(D + 255) / 256, 256, 0, s>>>(row4, D, hdr);
+    return cudaGetLastError();
+}
+
+__global__ void long_flags_kernel(const uint32_t* doc_start, uint32_t D, uint32_t* flags) {
+    const uint32_t d = blockIdx.x * blockDim.x + threadIdx.x;
+    if (d >= D) return;
+    flags[d] = (doc_start[d + 1] - doc_start[d]) > kSscWarpCap ? 1u : 0u;
+}
+
+cudaError_t launch_long_flags(const uint32_t* doc_start, uint32_t D, uint32_t* flags, cudaStream_t s) {
+    if (D == 0) return cudaSuccess;
+    long_flags_kernel<<<(D + 255) / 256, 256, 0, s>>>(doc_start, D, flags);
+    return cudaGetLastError();
+}
+
+__global__ void init_topics_kernel(uint64_t T, const uint64_t* ids, uint64_t id_base, uint64_t seed,
+                                   uint32_t K, uint16_t* z) {
+    for (uint64_t j = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; j < T;
+         j += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        const uint64_t id = ids ? ids[j] : id_base + j;
+        z[j] = static_cast<uint16_t>(uniform_topic(seed, kInitAssignStream, id, K));
+    }
+}
+
+cudaError_t launch_init_topics(uint64_t T, const uint64_t* ids, uint64_t id_base, uint64_t seed,
+                               uint32_t K, uint16_t* z, cudaStream_t s) {
+    if (T == 0) return cudaSuccess;
+    init_topics_kernel<<<grid_for(T, 256), 256, 0, s>>>(T, ids, id_base, seed, K, z);
+    return cudaGetLastError();
+}
+
+__global__ void given_topics_kernel(const uint32_t* topic_in, const uint32_t* input_of_slot, uint64_t T,
+                                    uint16_t* z) {
+    for (uint64_t j = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; j < T;
+         j += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+        z[j] = static_cast<uint16_t>(topic_in[input_of_slot ? input_of_slot[j] : j]);
+}
+
+cudaError_t launch_given_topics(const uint32_t* topic_in, const uint32_t* input_of_slot, uint64_t T,
+                                uint16_t* z, cudaStream_t s) {
+    if (T == 0) return cudaSuccess;
+    given_topics_kernel<<<grid_for(T, 256), 256, 0, s>>>(topic_in, input_of_slot, T, z);
+    return cudaGetLastError();
+}
+
+__global__ void ids_by_slot_kernel(const uint64_t* ids_in, const uint32_t* input_of_slot, uint64_t T,
+                                   uint64_t id_base, uint64_t* ids_out) {
+    for (uint64_t j = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; j < T;
+         j += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        const uint64_t i = input_of_slot ? input_of_slot[j] : j;
+        ids_out[j] = ids_in ? ids_in[i] : id_base + i;
+    }
+}
+
+cudaError_t launch_ids_by_slot(const uint64_t* ids_in, const uint32_t* input_of_slot, uint64_t T,
+                               uint64_t id_base, uint64_t* ids_out, cudaStream_t s) {
+    if (T == 0) return cudaSuccess;
+    ids_by_slot_kernel<<<grid_for(T, 256), 256, 0, s>>>(ids_in, input_of_slot, T, id_base, ids_out);
+    return cudaGetLastError();
+}
+
+__global__ void __launch_bounds__(256) recount_kernel(const uint2* tok, const Unit* units,
+                                                      const uint16_t* z, uint32_t* B, uint32_t K_pad) {
+    const Unit u = units[blockIdx.x];
+    uint32_t* brow = B + static_cast<size_t>(u.word) * K_pad;
+    for (uint32_t i = threadIdx.x; i < u.length; i += blockDim.x)
+        atomicAdd(brow + z[tok[u.offset + i].y], 1u);
+}
+
+cudaError_t launch_recount(const uint2* tok, const Unit* units, uint32_t n_units, const uint16_t* z,
+                           uint32_t* B, uint32_t K_pad, cudaStream_t s) {
+    if (n_units == 0) return cudaSuccess;
+    recount_kernel<<<n_units, 256, 0, s>>>(tok, units, z, B, K_pad);
+    return cudaGetLastError();
+}
+
+__global__ void validate_kernel(const uint32_t* __restrict__ aos, uint64_t T, uint32_t doc_begin,
+                                uint32_t doc_end, uint32_t V, uint32_t K, ValidateOut* out) {
+    for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < T;
+         i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        const uint32_t d = aos[3 * i], w = aos[3 * i + 1], t = aos[3 * i + 2];
+        if (d < doc_begin || d >= doc_end) atomicMin(&out->bad_doc, static_cast<unsigned long long>(i));
+        if (w >= V) atomicMin(&out->bad_word, static_cast<unsigned long long>(i));
+        if (t == kInvalidTopic) atomicMin(&out->first_invalid, static_cast<unsigned long long>(i));
+        else if (t >= K) atomicMin(&out->first_big, static_cast<unsigned long long>(i));
+        if (i > 0 && aos[3 * (i - 1)] > d) out->unsorted = 1u;
+    }
+}
+
+cudaError_t launch_validate(const uint32_t* aos, uint64_t T, uint32_t doc_begin, uint32_t doc_end,
+                            uint32_t V, uint32_t K, ValidateOut* out, cudaStream_t s) {
+    if (T == 0) return cudaSuccess;
+    validate_kernel<<<grid_for(T, 256), 256, 0, s>>>(aos, T, doc_begin, doc_end, V, K, out);
+    return cudaGetLastError();
+}
+
+__global__ void sched_counts_kernel(const uint32_t* schedule, const uint32_t* seg_len, uint32_t nseg,
+                                    uint32_t* counts) {
+    const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= nseg) return;
+    counts[p] = (seg_len[schedule[p]] + kUnitMaxTokens - 1) / kUnitMaxTokens;
+}
+
+cudaError_t launch_sched_counts(const uint32_t* schedule, const uint32_t* seg_len, uint32_t nseg,
+                                uint32_t* counts, cudaStream_t s) {
+    if (nseg == 0) return cudaSuccess;
+    sched_counts_kernel<<<(nseg + 255) / 256, 256, 0, s>>>(schedule, seg_len, nseg, counts);
+    return cudaGetLastError();
+}
+
+}  // namespace slda

@@ -1,0 +1,113 @@
+// kernels.hpp -- host launchers for the ESCA device kernels (kernels.cu).
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace slda {
+
+// Sampler work unit: one (word, token range) slice of a PDOW word segment.
+// Heavy words are split into several units (PAPER.md:621-636 heavy-first).
+struct Unit {
+    uint32_t word, offset, length, pad;
+};
+
+constexpr uint32_t kUnitMaxTokens = 8192;  // sampler: max tokens per unit (one CTA)
+constexpr uint32_t kSscWarpCap = 512;      // SSC: docs up to this length take the warp path
+
+struct SamplerArgs {
+    const uint2* tok;       // PDOW order: {doc_local, slot}
+    const Unit* units;      // heavy-first
+    const uint2* hdr;       // per doc: {row offset in uint4 units, nnz}
+    const uint32_t* A;      // packed C_dk entries: topic | count << tbits
+    const float* bhat;      // V_pad x K_pad
+    const float* l4;        // V_pad x K_pad (inclusive prefix, padded with the total)
+    const float* l3;        // V_pad x l3_stride (L4 block maxima)
+    const float* q;         // V_pad
+    const uint64_t* ids;    // RNG element id per slot, or null -> id_base + slot
+    uint16_t* z;            // new topic per slot
+    uint32_t* B;            // V_pad x K_pad, zeroed by the caller
+    uint64_t seed, id_base;
+    uint32_t stream_kind;   // iteration number (trainer.cpp:423)
+    uint32_t K, K_pad, l3_stride, n_l3, tbits;
+    unsigned long long* row_entries;  // optional: sum of nnz over tokens (roofline)
+};
+
+cudaError_t launch_sampler(const SamplerArgs& a, uint32_t n_units, cudaStream_t s);
+
+struct SscArgs {
+    const uint16_t* z;          // topics by slot (doc-grouped)
+    const uint32_t* doc_start;  // D+1 slot offsets
+    uint32_t D;
+    uint2* hdr;                 // writes .y = nnz
+    uint32_t* A;
+    uint32_t tbits, K_pad;
+    const uint32_t* long_docs;  // docs longer than kSscWarpCap
+    uint32_t n_long;
+    uint32_t* hist_scratch;     // n_long_ctas x K_pad (global fallback for large K)
+    unsigned long long* nnz_total;
+};
+
+cudaError_t launch_ssc(const SscArgs& a, cudaStream_t s);
+
+cudaError_t launch_colsum(const uint32_t* B, uint32_t row_begin, uint32_t row_end, uint32_t K_pad,
+                          unsigned long long* colsum, cudaStream_t s);
+cudaError_t launch_denom(const unsigned long long* colsum, uint32_t K, uint32_t K_pad, uint32_t V,
+                         double beta, double* denom, float* zv, cudaStream_t s);
+cudaError_t launch_phi(const uint32_t* B, const double* denom, const float* zv, float* bhat,
+                       float* l4, float* l3, float* q, uint32_t row_begin, uint32_t row_end,
+                       uint32_t K, uint32_t K_pad, uint32_t l3_stride, double beta, float falpha,
+                       cudaStream_t s);
+
+// Setup kernels.
+cudaError_t launch_deinterleave(const uint32_t* aos, uint64_t T, uint32_t doc_begin,
+                                uint32_t* doc_local, uint32_t* word, uint32_t* topic,
+                                cudaStream_t s);
+cudaError_t launch_check_sorted(const uint32_t* doc_local, uint64_t T, uint32_t* unsorted_flag,
+                                cudaStream_t s);
+cudaError_t launch_doc_hist(const uint32_t* doc_local, uint64_t T, uint32_t* counts,
+                            cudaStream_t s);
+cudaError_t launch_iota(uint32_t* out, uint64_t n, cudaStream_t s);
+cudaError_t launch_invert_perm(const uint32_t* input_of_slot, uint64_t T, uint32_t* slot_of_input,
+                               cudaStream_t s);
+cudaError_t launch_make_keys(const uint32_t* word, const uint32_t* doc_local,
+                             const uint32_t* input_of_slot, uint64_t T, uint32_t dbits,
+                             unsigned long long* keys, uint32_t* vals, cudaStream_t s);
+cudaError_t launch_make_tok(const unsigned long long* keys, const uint32_t* slots, uint64_t T,
+                            uint32_t dbits, uint2* tok, uint32_t* seg_flag, cudaStream_t s);
+cudaError_t launch_emit_segments(const unsigned long long* keys, const uint32_t* seg_flag,
+                                 const uint32_t* seg_index, uint64_t T, uint32_t dbits,
+                                 uint32_t* seg_word, uint32_t* seg_off, cudaStream_t s);
+cudaError_t launch_segment_lengths(const uint32_t* seg_off, uint32_t nseg, uint64_t T,
+                                   uint32_t* seg_len, unsigned long long* sched_keys,
+                                   uint32_t* sched_vals, const uint32_t* seg_word,
+                                   uint32_t* unit_count, cudaStream_t s);
+cudaError_t launch_emit_units(const uint32_t* schedule, const uint32_t* seg_word,
+                              const uint32_t* seg_off, const uint32_t* seg_len,
+                              const uint32_t* unit_start, uint32_t nseg, Unit* units,
+                              cudaStream_t s);
+cudaError_t launch_row_quads(const uint32_t* doc_start, uint32_t D, uint32_t* quads,
+                             cudaStream_t s);
+cudaError_t launch_init_hdr(const uint32_t* row4, uint32_t D, uint2* hdr, cudaStream_t s);
+cudaError_t launch_long_flags(const uint32_t* doc_start, uint32_t D, uint32_t* flags,
+                              cudaStream_t s);
+cudaError_t launch_init_topics(uint64_t T, const uint64_t* ids, uint64_t id_base, uint64_t seed,
+                               uint32_t K, uint16_t* z, cudaStream_t s);
+cudaError_t launch_given_topics(const uint32_t* topic_in, const uint32_t* input_of_slot,
+                                uint64_t T, uint16_t* z, cudaStream_t s);
+cudaError_t launch_ids_by_slot(const uint64_t* ids_in, const uint32_t* input_of_slot, uint64_t T,
+                               uint64_t id_base, uint64_t* ids_out, cudaStream_t s);
+// Range checks + the reference's topic rule (trainer.cpp:369-378): records the first
+// token index with an invalid topic and the first with topic >= K.
+struct ValidateOut {
+    unsigned long long first_invalid, first_big, bad_doc, bad_word;
+    uint32_t unsorted;
+};
+cudaError_t launch_validate(const uint32_t* aos, uint64_t T, uint32_t doc_begin, uint32_t doc_end,
+                            uint32_t V, uint32_t K, ValidateOut* out, cudaStream_t s);
+cudaError_t launch_sched_counts(const uint32_t* schedule, const uint32_t* seg_len, uint32_t nseg,
+                                uint32_t* counts, cudaStream_t s);
+cudaError_t launch_recount(const uint2* tok, const Unit* units, uint32_t n_units,
+                           const uint16_t* z, uint32_t* B, uint32_t K_pad, cudaStream_t s);
+
+}  // namespace slda

@@ -1,0 +1,63 @@
+"""Deterministic test corpora shared by the golden generator and the tests.
+
+Corpora are produced by the product's host-only generator
+(``Corpus.generate`` -> slda_generate_corpus; no GPU needed) and optionally
+transformed to exercise edge cases the reference tests: non doc-sorted token
+order, empty documents, long documents, K = 1, K above the 48 KB shared
+memory line, given (non-sentinel) topics.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+
+def corpus_arrays(spec: dict):
+    """Returns (doc, word, D, V) as uint32 arrays in corpus order."""
+    import paper_1610_02496_b200 as slda
+
+    c = slda.Corpus.generate(spec["family"], spec["D"], spec["V"], spec["T"], seed=spec["seed"],
+                             latent_topics=spec.get("latent", 100), threads=0)
+    toks = c.tokens()
+    doc = toks[:, 0].copy()
+    word = toks[:, 1].copy()
+    D, V = spec["D"], spec["V"]
+    if spec.get("spread_docs"):
+        # Every other document id is empty (docs with zero tokens in the shard).
+        doc = doc * 2
+        D = 2 * D
+    if spec.get("shuffle_seed") is not None:
+        perm = np.random.default_rng(spec["shuffle_seed"]).permutation(len(doc))
+        doc, word = doc[perm], word[perm]
+    return doc.astype(np.uint32), word.astype(np.uint32), D, V
+
+
+G = 0
+U = 1
+
+CASES: dict[str, dict] = {
+    # BASELINE.json configs[0]: D=1K, V=1K, T=100K, K=100, 50 iterations.
+    "c1": {"corpus": {"family": G, "D": 1000, "V": 1000, "T": 100_000, "seed": 20161008},
+           "K": 100, "seed": 42, "iterations": 50, "pdow": True,
+           "heldout": {"family": G, "D": 200, "V": 1000, "T": 20_000, "seed": 7}},
+    "k1": {"corpus": {"family": U, "D": 30, "V": 12, "T": 180, "seed": 5},
+           "K": 1, "seed": 11, "iterations": 3},
+    "u_k7_chunks": {"corpus": {"family": U, "D": 300, "V": 200, "T": 12_000, "seed": 6},
+                    "K": 7, "seed": 11, "iterations": 5, "chunks": 3, "workers": 4, "pdow": True},
+    "u_k64": {"corpus": {"family": U, "D": 120, "V": 64, "T": 10_200, "seed": 21},
+              "K": 64, "seed": 7, "iterations": 4},
+    "long_docs": {"corpus": {"family": U, "D": 40, "V": 500, "T": 40_000, "seed": 8},
+                  "K": 300, "seed": 3, "iterations": 3, "pdow": True},
+    "shuffled": {"corpus": {"family": U, "D": 200, "V": 300, "T": 8_000, "seed": 9, "shuffle_seed": 1},
+                 "K": 16, "seed": 99, "iterations": 3, "pdow": True},
+    "empty_docs": {"corpus": {"family": U, "D": 100, "V": 80, "T": 3_000, "seed": 10, "spread_docs": True},
+                   "K": 12, "seed": 5, "iterations": 3, "pdow": True},
+    "given_topics": {"corpus": {"family": U, "D": 150, "V": 120, "T": 6_000, "seed": 12},
+                     "K": 20, "seed": 4, "iterations": 3, "given_topics_seed": 77},
+    "k_large": {"corpus": {"family": U, "D": 50, "V": 50, "T": 5_000, "seed": 13},
+                "K": 20_000, "seed": 2, "iterations": 2},
+    "alpha_beta": {"corpus": {"family": G, "D": 400, "V": 600, "T": 40_000, "seed": 14, "latent": 20},
+                   "K": 25, "alpha": 0.3, "beta": 0.05, "seed": 8, "iterations": 4,
+                   "heldout": {"family": G, "D": 60, "V": 600, "T": 6_000, "seed": 15, "latent": 20}},
+    "nytimes_small": {"corpus": {"family": G, "D": 1000, "V": 5000, "T": 300_000, "seed": 16},
+                      "K": 1000, "seed": 42, "iterations": 3, "chunks": 4, "workers": 8},
+}

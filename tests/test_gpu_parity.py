@@ -1,0 +1,200 @@
+"""GPU parity: the B200 engine against the reference, bit for bit.
+
+Every case in tests/corpora.py is run through the product path (pybind ->
+C++ shim -> C-ABI -> sm_100a kernels) and compared, at EVERY iteration, with
+sha256 digests the reference itself produced (tests/golden/, made by
+oracle/_ref): assignments, C_wk, phi, the tree's L4 prefix, Q and C_dk.
+PDOW layouts are compared array-for-array with the C oracle.  Held-out LL is
+compared with a stated tolerance (device log vs glibc log: |rel| <= 1e-12).
+"""
+import numpy as np
+import pytest
+
+from corpora import CASES, corpus_arrays
+from oracle_lib import OracleModel, digest
+
+pytestmark = pytest.mark.gpu
+
+HELDOUT_REL_TOL = 1e-12  # only the f64 log() may differ from glibc by an ulp
+
+
+def slda():
+    import paper_1610_02496_b200 as m
+
+    return m
+
+
+def make_model(spec, iterations=None):
+    s = slda()
+    doc, word, D, V = corpus_arrays(spec["corpus"])
+    topic = None
+    if spec.get("given_topics_seed") is not None:
+        topic = np.random.default_rng(spec["given_topics_seed"]).integers(0, spec["K"], size=len(doc),
+                                                                          dtype=np.uint32)
+    corpus = s.Corpus.from_arrays(D, V, doc, word, topic)
+    cfg = s.TrainConfig()
+    cfg.num_topics = spec["K"]
+    cfg.alpha = spec.get("alpha", 0.0)
+    cfg.beta = spec.get("beta", 0.01)
+    cfg.seed = spec["seed"]
+    cfg.iterations = spec["iterations"] if iterations is None else iterations
+    cfg.tree_branch = 32
+    return s.init_state(corpus, cfg), cfg, corpus
+
+
+def model_digests(m):
+    offs, tops, cnts = m.doc_topic()
+    return {
+        "assignments": digest(m.assignments()),
+        "word_topic": digest(m.word_topic()),
+        "word_topic_prob": digest(m.word_topic_prob()),
+        "l4": digest(m.tree_prefix()),
+        "tree_mass": digest(m.tree_mass()),
+        "doc_topic": digest(np.concatenate([offs.view(np.uint32), tops, cnts])),
+    }
+
+
+@pytest.mark.parametrize("name", sorted(CASES))
+def test_engine_matches_reference_every_iteration(name, golden):
+    spec = CASES[name]
+    fx = golden["cases"][name]
+    m, cfg, _ = make_model(spec)
+    assert m.alpha == fx["alpha"]
+    for it, expect in enumerate(fx["iterations"]):
+        got = model_digests(m)
+        assert got == expect, (name, it, sorted(k for k in got if got[k] != expect[k]))
+        if it + 1 < len(fx["iterations"]):
+            st = m.run_iteration(cfg)
+            assert st.iteration == it + 1
+            assert st.tokens == fx["T"]
+            assert st.mean_doc_topics == fx["mean_doc_topics"][it]
+
+
+@pytest.mark.parametrize("name", sorted(n for n, s in CASES.items() if s.get("pdow")))
+def test_pdow_layout_matches_reference(name, golden):
+    spec = CASES[name]
+    m, _, _ = make_model(spec, iterations=0)
+    lay = m.chunk_layout()
+    doc, word, D, V = corpus_arrays(spec["corpus"])
+    o = OracleModel(D, V, doc, word, None, K=spec["K"], seed=spec["seed"])
+    p = o.pdow()
+    for key in ("sorted_doc", "sorted_word", "shuffle_ptrs", "doc_offsets", "seg_word", "seg_offset",
+                "seg_length"):
+        assert np.array_equal(np.asarray(lay[key]), p[key].astype(np.asarray(lay[key]).dtype)), key
+    assert np.array_equal(lay["token_ids"], p["token_ids"].astype(np.uint64))
+    # build_schedule (corpus.cpp:200-210): stable by (length desc, word asc).
+    order = sorted(range(len(p["seg_word"])), key=lambda s: (-int(p["seg_length"][s]), int(p["seg_word"][s])))
+    assert lay["schedule"].tolist() == order
+    # ... and the reference's own chunk arrays (digests from oracle/_ref).
+    ref = golden["cases"][name]["pdow"]
+    assert digest(lay["sorted_doc"]) == ref["sorted_doc"]
+    assert digest(lay["sorted_word"]) == ref["sorted_word"]
+    assert digest(lay["token_ids"].astype(np.uint32)) == ref["token_ids"]
+    assert digest(lay["shuffle_ptrs"]) == ref["shuffle_ptrs"]
+    assert digest(lay["doc_offsets"]) == ref["doc_offsets"]
+
+
+@pytest.mark.parametrize("name", sorted(n for n, s in CASES.items() if s.get("heldout")))
+def test_heldout_ll_matches_reference(name, golden):
+    spec = CASES[name]
+    fx = golden["cases"][name]
+    m, cfg, _ = make_model(spec)
+    for _ in range(spec["iterations"]):
+        m.run_iteration(cfg)
+    hd, hw, hD, V = corpus_arrays(spec["heldout"])
+    held = slda().Corpus.from_arrays(hD, V, hd, hw)
+    ll, n = slda().heldout_ll(m, held, burn_in=20, workers=1, seed=spec["seed"])
+    assert n == fx["heldout"]["tokens"]
+    ref = fx["heldout"]["per_token_ll"]
+    assert abs(ll - ref) <= HELDOUT_REL_TOL * abs(ref), (ll, ref)
+
+
+def test_async_iterations_equal_sync():
+    spec = CASES["u_k64"]
+    a, cfg, _ = make_model(spec)
+    b, _, _ = make_model(spec)
+    for _ in range(3):
+        a.run_iteration(cfg)
+        b.iterate_async()
+    b.synchronize()
+    assert model_digests(a) == model_digests(b)
+
+
+def test_raw_c_abi_round_trip(golden):
+    import abi
+
+    spec = CASES["u_k7_chunks"]
+    doc, word, D, V = corpus_arrays(spec["corpus"])
+    e = abi.Engine(D, V, doc, word, spec["K"], seed=spec["seed"])
+    for it in range(spec["iterations"]):
+        st = e.iterate()
+        assert st.iteration == it + 1 and st.device_ms > 0
+    exp = golden["cases"]["u_k7_chunks"]["iterations"][-1]
+    assert digest(e.assignments()) == exp["assignments"]
+    assert digest(e.word_topic()) == exp["word_topic"]
+    assert digest(e.word_topic_prob()) == exp["word_topic_prob"]
+    t = e.kernel_times()
+    assert t.sampler_ms > 0 and t.launches >= 5
+    assert t.sampler_row_entries > 0
+
+
+def test_validation_errors_map_to_value_error():
+    s = slda()
+    doc, word, D, V = corpus_arrays(CASES["k1"]["corpus"])
+    corpus = s.Corpus.from_arrays(D, V, doc, word)
+    cfg = s.TrainConfig()
+    cfg.num_topics = 70000
+    cfg.tree_branch = 64
+    with pytest.raises(ValueError, match="65536"):
+        s.init_state(corpus, cfg)
+    cfg = s.TrainConfig()
+    cfg.num_topics = 3
+    bad = s.Corpus.from_arrays(D, V, doc, word, np.full(len(doc), 7, np.uint32))
+    with pytest.raises(ValueError, match="exceeds configured K"):
+        s.init_state(bad, cfg)
+    cfg.beta = 0.0
+    with pytest.raises(ValueError):
+        s.init_state(corpus, cfg)
+
+
+def test_training_is_deterministic_and_normalized():
+    s = slda()
+    spec = CASES["alpha_beta"]
+    a, cfg, _ = make_model(spec)
+    b, _, _ = make_model(spec)
+    for _ in range(3):
+        a.run_iteration(cfg)
+        b.run_iteration(cfg)
+    assert (a.assignments() == b.assignments()).all()
+    bhat = a.word_topic_prob().astype(np.float64)
+    assert np.all(np.abs(bhat.sum(axis=0) - 1.0) < 1e-5)  # acceptance.cpp:281-303
+    wt = a.word_topic()
+    assert int(wt.sum()) == a.num_tokens
+    ranked = s.top_words(a, 3)
+    assert len(ranked) == a.num_topics and all(len(w) == 3 for w in ranked)
+
+
+def test_checkpoint_roundtrip_and_resume(tmp_path):
+    s = slda()
+    spec = CASES["given_topics"]
+    full, cfg, corpus = make_model(spec)
+    for _ in range(4):
+        full.run_iteration(cfg)
+    half, _, _ = make_model(spec)
+    for _ in range(2):
+        half.run_iteration(cfg)
+    path = str(tmp_path / "half.ckpt")
+    half.save(path)
+    loaded = s.Model.load(path)
+    assert (loaded.word_topic() == half.word_topic()).all()
+    assert (loaded.word_topic_prob() == half.word_topic_prob()).all()
+    assert loaded.iteration == 2
+    resumed = s.resume(corpus, path, cfg)
+    for _ in range(2):
+        resumed.run_iteration(cfg)
+    assert (resumed.assignments() == full.assignments()).all()
+    assert (resumed.word_topic() == full.word_topic()).all()
+    # Byte format equals the reference's save_checkpoint (trainer.cpp:469-478).
+    text = open(path).read().splitlines()
+    assert text[0].startswith("sparselda-checkpoint 1 ")
+    assert len(text) == 1 + half.num_tokens + 1 + int((half.word_topic() != 0).sum())
