@@ -283,13 +283,13 @@ def main() -> None:
     del assignments
 
     # ---- device-timed: W warm-up iterations, then exactly K timed iterations.
-    for _ in range(args.warmup):
-        model.iterate_async()
-    model.synchronize()
     stream = torch.cuda.ExternalStream(model.stream_ptr())
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    barrier()
     with ClockSampler(local_rank) as clocks:
+        for _ in range(args.warmup):
+            model.iterate_async()
+        model.synchronize()
+        barrier()
         start.record(stream)
         for _ in range(args.steps):
             model.iterate_async()

@@ -2,12 +2,12 @@
 //
 // One engine = one GPU = one document shard (the reference's chunk,
 // PAPER.md:403, with chunk -> GPU).  The whole ESCA state lives in HBM:
-//   tok   uint2[T]      PDOW order (word, doc, token_id): {doc_local, slot}
+//   tok   uint2[T]      execution order (word, doc length desc, doc, token_id):
+//                       {row4[doc], slot}
 //   z     u16[T]        topic per slot; slots are doc-grouped (slot == corpus
 //                       position for a doc-sorted corpus)
-//   A     u32[4*Q]      C_dk rows, entry = topic | count << tbits, row d at a
-//                       16-byte aligned offset with capacity len_d, padded with
-//                       zero-count entries; hdr[d] = {row offset / 4, nnz}
+//   A     u32[4*Q]      C_dk rows: [nnz-1 | entries topic | count << tbits | zero
+//                       padding to a multiple of 8], 32-byte aligned at row4[d]
 //   B     u32[V_pad][K_pad], bhat/L4 f32[V_pad][K_pad], L3 f32[V_pad][l3s], Q f32[V_pad]
 // Reference paths are relative to /root/reference/proj.
 #include <dlfcn.h>
@@ -147,11 +147,12 @@ struct slda_engine {
     uint32_t rank = 0, world = 1;
     uint32_t nseg = 0, n_units = 0, n_long = 0;
     bool doc_major = true;
+    uint32_t wshift = 0;  // word field shift of the execution-order key
     size_t device_bytes = 0;
     uint64_t nnz = 0;
 
     // Device state
-    DevMem tok, z, doc_start, hdr, A, units, long_docs, hist_scratch;
+    DevMem tok, z, doc_start, row4, A, units, long_docs, hist_scratch;
     DevMem seg_word, seg_off, seg_len, schedule;  // PDOW getters
     DevMem input_of_slot, ids;                    // only for non doc-major input / explicit ids
     DevMem B, bhat, l4, l3, q, colsum, denom, zv, counters;
@@ -324,13 +325,13 @@ void slda_engine::build(const slda_corpus_view& cv, const slda_config& c) {
 
     // Doc-grouped slot offsets (corpus.cpp:186-189).
     doc_start.alloc((static_cast<size_t>(D) + 1) * 4, &device_bytes);
+    DevMem counts;  // document lengths, kept for the execution-order key
+    uint32_t max_len = 0;
     {
-        DevMem counts;
         counts.alloc((static_cast<size_t>(D) + 1) * 4, nullptr);
         CK(cudaMemsetAsync(counts.p, 0, counts.bytes, stream));
         CK(slda::launch_doc_hist(doc_local.as<uint32_t>(), T, counts.as<uint32_t>(), stream));
         exclusive_sum(counts.as<uint32_t>(), doc_start.as<uint32_t>(), static_cast<uint64_t>(D) + 1);
-        uint32_t max_len = 0;
         if (D) {
             DevMem mx;
             mx.alloc(4, nullptr);
@@ -371,11 +372,28 @@ void slda_engine::build(const slda_corpus_view& cv, const slda_config& c) {
         CK(cudaStreamSynchronize(stream));
     }
 
-    // PDOW: stable radix sort by (word, doc) of keys laid out in slot order
-    // == the reference's (word, doc, token_id) sort (corpus.cpp:157-175).
+    // C_dk rows (header + entries, capacity len_d + 1 rounded to 8 entries, 32-byte
+    // aligned); row offsets in uint4 units are static, so tok carries them.
+    row4.alloc((static_cast<size_t>(D) + 1) * 4, &device_bytes);
+    {
+        DevMem quads;
+        quads.alloc((static_cast<size_t>(D) + 1) * 4, nullptr);
+        CK(cudaMemsetAsync(quads.p, 0, quads.bytes, stream));
+        CK(slda::launch_row_quads(doc_start.as<uint32_t>(), D, quads.as<uint32_t>(), stream));
+        exclusive_sum(quads.as<uint32_t>(), row4.as<uint32_t>(), static_cast<uint64_t>(D) + 1);
+        const uint32_t total_quads = D ? d2h_scalar(row4.as<uint32_t>() + D) : 0;
+        A.alloc(static_cast<size_t>(total_quads) * 16 + 256, &device_bytes);
+        CK(cudaMemsetAsync(A.p, 0, A.bytes, stream));
+    }
+
+    // PDOW: stable radix sort of keys laid out in slot order -> the reference's
+    // (word, doc, token_id) order (corpus.cpp:157-175), refined by descending doc
+    // length inside each word (execution order; getters re-derive the canonical one).
     tok.alloc(T * 8, &device_bytes);
-    const uint32_t dbits = bits_for(D ? D - 1 : 1);
+    slda::KeyLayout kl{bits_for(D ? D - 1 : 1), bits_for(max_len ? max_len : 1), max_len};
     const uint32_t wbits = bits_for(V - 1 ? V - 1 : 1);
+    if (kl.dbits + kl.lbits + wbits > 64) kl.lbits = 0;  // canonical order only
+    wshift = kl.dbits + kl.lbits;
     {
         DevMem keys, keys_sorted, vals, slots_sorted, flags, seg_index;
         keys.alloc(T * 8, nullptr);
@@ -383,22 +401,22 @@ void slda_engine::build(const slda_corpus_view& cv, const slda_config& c) {
         vals.alloc(T * 4, nullptr);
         slots_sorted.alloc(T * 4, nullptr);
         CK(slda::launch_make_keys(word.as<uint32_t>(), doc_local.as<uint32_t>(),
-                                  doc_major ? nullptr : input_of_slot.as<uint32_t>(), T, dbits,
-                                  keys.as<unsigned long long>(), vals.as<uint32_t>(), stream));
+                                  doc_major ? nullptr : input_of_slot.as<uint32_t>(), counts.as<uint32_t>(), T,
+                                  kl, keys.as<unsigned long long>(), vals.as<uint32_t>(), stream));
         if (T) {
             cub_call([&](void* t, size_t& b) {
                 return cub::DeviceRadixSort::SortPairs(
                     t, b, keys.as<unsigned long long>(), keys_sorted.as<unsigned long long>(),
                     vals.as<uint32_t>(), slots_sorted.as<uint32_t>(), static_cast<int64_t>(T), 0,
-                    static_cast<int>(dbits + wbits), stream);
+                    static_cast<int>(wshift + wbits), stream);
             });
         }
         keys.release();
         vals.release();
         flags.alloc(T * 4, nullptr);
         seg_index.alloc(T * 4, nullptr);
-        CK(slda::launch_make_tok(keys_sorted.as<unsigned long long>(), slots_sorted.as<uint32_t>(), T, dbits,
-                                 tok.as<uint2>(), flags.as<uint32_t>(), stream));
+        CK(slda::launch_make_tok(keys_sorted.as<unsigned long long>(), slots_sorted.as<uint32_t>(),
+                                 row4.as<uint32_t>(), T, kl, tok.as<uint2>(), flags.as<uint32_t>(), stream));
         exclusive_sum(flags.as<uint32_t>(), seg_index.as<uint32_t>(), T);
         nseg = T ? d2h_scalar(seg_index.as<uint32_t>() + T - 1) + d2h_scalar(flags.as<uint32_t>() + T - 1) : 0;
         seg_word.alloc(static_cast<size_t>(nseg) * 4, &device_bytes);
@@ -406,7 +424,7 @@ void slda_engine::build(const slda_corpus_view& cv, const slda_config& c) {
         seg_len.alloc(static_cast<size_t>(nseg) * 4, &device_bytes);
         schedule.alloc(static_cast<size_t>(nseg) * 4, &device_bytes);
         CK(slda::launch_emit_segments(keys_sorted.as<unsigned long long>(), flags.as<uint32_t>(),
-                                      seg_index.as<uint32_t>(), T, dbits, seg_word.as<uint32_t>(),
+                                      seg_index.as<uint32_t>(), T, wshift, seg_word.as<uint32_t>(),
                                       seg_off.as<uint32_t>(), stream));
     }
     // build_schedule (corpus.cpp:200-210): heavy first, ties by ascending word.
@@ -438,19 +456,6 @@ void slda_engine::build(const slda_corpus_view& cv, const slda_config& c) {
         units.alloc(sizeof(slda::Unit), &device_bytes);
     }
 
-    // C_dk rows: capacity len_d, 16-byte aligned (nnz_d <= len_d).
-    hdr.alloc(static_cast<size_t>(D) * 8, &device_bytes);
-    {
-        DevMem quads, row4;
-        quads.alloc((static_cast<size_t>(D) + 1) * 4, nullptr);
-        row4.alloc((static_cast<size_t>(D) + 1) * 4, nullptr);
-        CK(cudaMemsetAsync(quads.p, 0, quads.bytes, stream));
-        CK(slda::launch_row_quads(doc_start.as<uint32_t>(), D, quads.as<uint32_t>(), stream));
-        exclusive_sum(quads.as<uint32_t>(), row4.as<uint32_t>(), static_cast<uint64_t>(D) + 1);
-        const uint32_t total_quads = D ? d2h_scalar(row4.as<uint32_t>() + D) : 0;
-        A.alloc(static_cast<size_t>(total_quads) * 16, &device_bytes);
-        CK(slda::launch_init_hdr(row4.as<uint32_t>(), D, hdr.as<uint2>(), stream));
-    }
     // Long documents take the CTA histogram path of SSC.
     {
         DevMem flags, iota, cnt;
@@ -501,7 +506,7 @@ void slda_engine::ssc() {
     s.z = z.as<uint16_t>();
     s.doc_start = doc_start.as<uint32_t>();
     s.D = D;
-    s.hdr = hdr.as<uint2>();
+    s.row4 = row4.as<uint32_t>();
     s.A = A.as<uint32_t>();
     s.tbits = tbits;
     s.K_pad = K_pad;
@@ -566,7 +571,6 @@ void slda_engine::enqueue_iteration() {
     slda::SamplerArgs a{};
     a.tok = tok.as<uint2>();
     a.units = units.as<slda::Unit>();
-    a.hdr = hdr.as<uint2>();
     a.A = A.as<uint32_t>();
     a.bhat = bhat.as<float>();
     a.l4 = l4.as<float>();
@@ -816,15 +820,38 @@ int slda_get_assignments(slda_engine* e, uint32_t* out) {
     });
 }
 
+namespace {
+// C_dk rows copied to the host: row d = [nnz-1 | entries], empty documents have none.
+struct HostRows {
+    std::vector<uint32_t> doc_start, row4, A;
+    uint32_t nnz(uint32_t d) const {
+        return doc_start[d + 1] == doc_start[d] ? 0u : (A[static_cast<size_t>(row4[d]) * 4] & mask) + 1u;
+    }
+    const uint32_t* entries(uint32_t d) const { return A.data() + static_cast<size_t>(row4[d]) * 4 + 1; }
+    uint32_t mask = 0;
+};
+
+HostRows fetch_rows(slda_engine* e) {
+    HostRows h;
+    h.mask = (1u << e->tbits) - 1u;
+    h.doc_start.resize(static_cast<size_t>(e->D) + 1);
+    h.row4.resize(static_cast<size_t>(e->D) + 1);
+    h.A.resize(e->A.bytes / 4);
+    CK(cudaMemcpy(h.doc_start.data(), e->doc_start.p, h.doc_start.size() * 4, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(h.row4.data(), e->row4.p, h.row4.size() * 4, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(h.A.data(), e->A.p, e->A.bytes, cudaMemcpyDeviceToHost));
+    return h;
+}
+}  // namespace
+
 int slda_get_doc_topic_nnz(slda_engine* e, uint64_t* nnz) {
     return guarded([&] {
         if (!e || !nnz) validation("null argument");
         e->set_device();
         CK(cudaStreamSynchronize(e->stream));
-        std::vector<uint2> hdr(e->D);
-        if (e->D) CK(cudaMemcpy(hdr.data(), e->hdr.p, static_cast<size_t>(e->D) * 8, cudaMemcpyDeviceToHost));
+        const HostRows h = fetch_rows(e);
         uint64_t n = 0;
-        for (const uint2& h : hdr) n += h.y;
+        for (uint32_t d = 0; d < e->D; ++d) n += h.nnz(d);
         *nnz = n;
     });
 }
@@ -834,17 +861,13 @@ int slda_get_doc_topic(slda_engine* e, uint64_t* row_offsets, uint32_t* topics, 
         if (!e || !row_offsets) validation("null argument");
         e->set_device();
         CK(cudaStreamSynchronize(e->stream));
-        std::vector<uint2> hdr(e->D);
-        std::vector<uint32_t> A(e->A.bytes / 4);
-        if (e->D) CK(cudaMemcpy(hdr.data(), e->hdr.p, static_cast<size_t>(e->D) * 8, cudaMemcpyDeviceToHost));
-        CK(cudaMemcpy(A.data(), e->A.p, e->A.bytes, cudaMemcpyDeviceToHost));
-        const uint32_t mask = (1u << e->tbits) - 1u;
+        const HostRows h = fetch_rows(e);
         uint64_t pos = 0;
         row_offsets[0] = 0;
         for (uint32_t d = 0; d < e->D; ++d) {
-            const uint32_t* row = A.data() + static_cast<size_t>(hdr[d].x) * 4;
-            for (uint32_t i = 0; i < hdr[d].y; ++i, ++pos) {
-                topics[pos] = row[i] & mask;
+            const uint32_t* row = h.entries(d);
+            for (uint32_t i = 0, n = h.nnz(d); i < n; ++i, ++pos) {
+                topics[pos] = row[i] & h.mask;
                 counts[pos] = row[i] >> e->tbits;
             }
             row_offsets[d + 1] = pos;
@@ -876,15 +899,23 @@ int slda_get_pdow(slda_engine* e, uint32_t* sorted_doc, uint32_t* sorted_word, u
             ids.resize(T);
             CK(cudaMemcpy(ids.data(), e->ids.p, T * 8, cudaMemcpyDeviceToHost));
         }
+        // Canonical chunk order (word, doc, token_id) from the execution order: within a
+        // word segment, sort by doc; slots are doc-grouped in corpus order, so sorting by
+        // slot gives (doc, token_id).
+        std::vector<uint32_t> slot(T), doc(T);
+        for (uint64_t i = 0; i < T; ++i) slot[i] = tok[i].y;
+        for (uint32_t s = 0; s < e->nseg; ++s) std::sort(slot.begin() + so[s], slot.begin() + so[s] + sl[s]);
+        for (uint64_t i = 0; i < T; ++i)
+            doc[i] = static_cast<uint32_t>(std::upper_bound(dst.begin(), dst.end(), slot[i]) - dst.begin() - 1);
         // shuffle_ptrs: doc-grouped slot in word-major order per doc (corpus.cpp:190-195).
         std::vector<uint32_t> cursor(dst.begin(), dst.end() - 1);
         uint32_t seg = 0;
         for (uint64_t i = 0; i < T; ++i) {
             while (seg + 1 < e->nseg && so[seg + 1] <= i) ++seg;
-            if (sorted_doc) sorted_doc[i] = tok[i].x + e->doc_begin;
+            if (sorted_doc) sorted_doc[i] = doc[i] + e->doc_begin;
             if (sorted_word) sorted_word[i] = sw[seg];
-            if (token_ids) token_ids[i] = ids.empty() ? e->id_base + tok[i].y : ids[tok[i].y];
-            if (shuffle_ptrs) shuffle_ptrs[i] = cursor[tok[i].x]++;
+            if (token_ids) token_ids[i] = ids.empty() ? e->id_base + slot[i] : ids[slot[i]];
+            if (shuffle_ptrs) shuffle_ptrs[i] = cursor[doc[i]]++;
         }
         if (doc_offsets) std::memcpy(doc_offsets, dst.data(), dst.size() * 4);
         if (seg_word) std::memcpy(seg_word, sw.data(), sw.size() * 4);

@@ -38,14 +38,68 @@ __device__ __forceinline__ float entry_mass(uint32_t e, uint32_t tbits, uint32_t
     return __fmul_rn(__uint2float_rn(e >> tbits), s_bhat[e & tmask]);
 }
 
+__device__ __forceinline__ float acc_quad(float s, const uint4& q, uint32_t tbits, uint32_t tmask,
+                                          const float* s_bhat) {
+    s = __fadd_rn(s, entry_mass(q.x, tbits, tmask, s_bhat));
+    s = __fadd_rn(s, entry_mass(q.y, tbits, tmask, s_bhat));
+    s = __fadd_rn(s, entry_mass(q.z, tbits, tmask, s_bhat));
+    return __fadd_rn(s, entry_mass(q.w, tbits, tmask, s_bhat));
+}
+
+// One 32-byte sector (8 C_dk entries) per lane: a 256-bit load (LDG.E.256 on sm_100a),
+// not allocated in L1 (rows are streamed; the reuse is in L2).
+struct Sector {
+    uint4 lo, hi;
+};
+__device__ __forceinline__ Sector ldg_sector(const uint4* p) {
+    Sector s;
+    asm volatile("ld.global.nc.L1::no_allocate.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(s.lo.x), "=r"(s.lo.y), "=r"(s.lo.z), "=r"(s.lo.w), "=r"(s.hi.x), "=r"(s.hi.y),
+                   "=r"(s.hi.z), "=r"(s.hi.w)
+                 : "l"(p));
+    return s;
+}
+
+// Rows are consumed in groups of 4 sectors (32 entries) with all 4 loads in flight.
+constexpr uint32_t kGroupSectors = 4;
+// Running sums at the end of the first kCheckpoints groups, so the prefix pass of the
+// sparse branch re-reads one group instead of the row.
+constexpr uint32_t kCheckpoints = 8;
+
+// lower_bound over the word's L4 prefix (== WaryTree::sample, acceptance.cpp:140-200)
+// by one warp: L2 (smem, <= 64 block maxima of L3) -> L3 (smem, one 32-block) -> L4
+// (global, one coalesced 128-byte block).  Returns the first index with L4 >= x.
+__device__ __forceinline__ uint32_t warp_tree_search(float x, const float* s_l2, uint32_t n_l2,
+                                                     const float* s_l3, const float* l4row, uint32_t lane) {
+    uint32_t j2;
+    {
+        const uint32_t b0 = __ballot_sync(0xffffffffu, lane < n_l2 && s_l2[lane] >= x);
+        if (b0) {
+            j2 = __ffs(b0) - 1;
+        } else {
+            const uint32_t b1 = __ballot_sync(0xffffffffu, lane + 32 < n_l2 && s_l2[lane + 32] >= x);
+            j2 = b1 ? 31 + __ffs(b1) : n_l2 - 1;
+        }
+    }
+    const uint32_t b3 = __ballot_sync(0xffffffffu, s_l3[j2 * 32 + lane] >= x);
+    const uint32_t j3 = j2 * 32 + (b3 ? __ffs(b3) - 1 : 31);
+    const uint32_t b4 = __ballot_sync(0xffffffffu, __ldg(l4row + j3 * 32 + lane) >= x);
+    return j3 * 32 + (b4 ? __ffs(b4) - 1 : 31);
+}
+
 template <int NT>
 __global__ void __launch_bounds__(NT) sampler_kernel(SamplerArgs a) {
     extern __shared__ __align__(16) float sm[];
     float* s_bhat = sm;
-    float* s_l3 = sm + a.K_pad;
+    const uint32_t l3s32 = (a.n_l3 + 31) & ~31u;
+    float* s_l3 = sm + a.K_pad;             // l3s32 (padded with the total)
+    float* s_l2 = s_l3 + l3s32;             // 64
+    float* s_ck = s_l2 + 64;                // [kCheckpoints][NT]
 
     const Unit unit = a.units[blockIdx.x];
     const uint32_t v = unit.word;
+    const float* l4row = a.l4 + static_cast<size_t>(v) * a.K_pad;
+    const float total = __ldg(l4row + a.K_pad - 1);  // padded with the row total
     {
         const float4* gb = reinterpret_cast<const float4*>(a.bhat + static_cast<size_t>(v) * a.K_pad);
         float4* sb = reinterpret_cast<float4*>(s_bhat);
@@ -53,91 +107,144 @@ __global__ void __launch_bounds__(NT) sampler_kernel(SamplerArgs a) {
         const float4* gl = reinterpret_cast<const float4*>(a.l3 + static_cast<size_t>(v) * a.l3_stride);
         float4* sl = reinterpret_cast<float4*>(s_l3);
         for (uint32_t i = threadIdx.x; i < a.l3_stride / 4; i += NT) sl[i] = __ldg(gl + i);
+        for (uint32_t i = a.l3_stride + threadIdx.x; i < l3s32; i += NT) s_l3[i] = total;
+        // L2: maxima of 32-wide L3 blocks (the reference tree's top level for W = 32).
+        if (threadIdx.x < 64) {
+            const uint32_t e = threadIdx.x * 32 + 31;
+            s_l2[threadIdx.x] = e < a.n_l3 ? __ldg(a.l3 + static_cast<size_t>(v) * a.l3_stride + e) : total;
+        }
     }
+    const uint32_t n_l2 = (a.n_l3 + 31) / 32;
     const float qv = __ldg(a.q + v);
-    const float* l4row = a.l4 + static_cast<size_t>(v) * a.K_pad;
-    const float total = __ldg(l4row + a.K_pad - 1);  // padded with the row total
     uint32_t* brow = a.B + static_cast<size_t>(v) * a.K_pad;
     const uint32_t tbits = a.tbits;
     const uint32_t tmask = (1u << tbits) - 1u;
     const uint4* A4 = reinterpret_cast<const uint4*>(a.A);
+    float* ck = s_ck + threadIdx.x;
+    const uint32_t lane = lane_id();
     unsigned long long entries = 0;
     __syncthreads();
 
-    for (uint32_t i = threadIdx.x; i < unit.length; i += NT) {
-        const uint2 t = __ldg(a.tok + unit.offset + i);
-        const uint2 h = __ldg(a.hdr + t.x);
-        const uint64_t id = a.ids ? __ldg(a.ids + t.y) : a.id_base + t.y;
-        float ub, up;
-        draw2_f32(a.seed, a.stream_kind, id, ub, up);
+    // Warp-uniform trip count so the cooperative tree search sees every lane.
+    const uint32_t rounds = (unit.length + NT - 1) / NT;
+    for (uint32_t r = 0; r < rounds; ++r) {
+        const uint32_t i = r * NT + threadIdx.x;
+        const bool active = i < unit.length;
+        uint32_t topic = 0;
+        bool tree = false;
+        float x = 0.0f;
+        uint2 t = make_uint2(0u, 0u);
+        if (active) {
+            t = __ldg(a.tok + unit.offset + i);  // {row quad offset, slot}
+            const uint4* row = A4 + t.x;
+            const Sector h = ldg_sector(row);  // header + first 7 entries
+            const uint64_t id = a.ids ? __ldg(a.ids + t.y) : a.id_base + t.y;
+            float ub, up;
+            draw2_f32(a.seed, a.stream_kind, id, ub, up);
 
-        // make_branch_context: S = sum_i f32(cnt_i) * bhat[top_i], ascending topic.
-        const uint4* row = A4 + h.x;
-        const uint32_t nq = (h.y + 3u) >> 2;  // rows are padded with zero-count entries
-        entries += h.y;
-        float s = 0.0f;
-        for (uint32_t j = 0; j < nq; ++j) {
-            const uint4 e = ldg_nc_v4(row + j);
-            s = __fadd_rn(s, entry_mass(e.x, tbits, tmask, s_bhat));
-            s = __fadd_rn(s, entry_mass(e.y, tbits, tmask, s_bhat));
-            s = __fadd_rn(s, entry_mass(e.z, tbits, tmask, s_bhat));
-            s = __fadd_rn(s, entry_mass(e.w, tbits, tmask, s_bhat));
-        }
-        uint32_t topic;
-        if (ub < __fdiv_rn(s, __fadd_rn(s, qv))) {
-            // Sparse branch: first running prefix >= p*S (prefix_search, sampler.hpp:18-41).
-            // Zero-count padding adds +0 and never precedes a real hit (x <= S).
-            const float x = __fmul_rn(up, s);
-            float run = 0.0f;
-            topic = 0;
-            bool found = false;
-            for (uint32_t j = 0; j < nq && !found; ++j) {
-                const uint4 e = ldg_nc_v4(row + j);
-                const uint32_t es[4] = {e.x, e.y, e.z, e.w};
+            // Row = [header | nnz entries ascending topic | zero-count padding to 8]; the
+            // header entry (nnz-1, count 0) and the padding add +0 to every running sum.
+            const uint32_t nnz = (h.lo.x & tmask) + 1u;
+            const uint32_t nsect = (nnz + 8u) >> 3;
+            const uint32_t ngroups = (nsect + kGroupSectors - 1) / kGroupSectors;
+            entries += nnz;
+
+            // make_branch_context: S = sum_i f32(cnt_i) * bhat[top_i], sequential f32.
+            float s = 0.0f;
+            for (uint32_t g = 0; g < ngroups; ++g) {
+                Sector q[kGroupSectors];
+                const uint32_t base = g * kGroupSectors;
 #pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    run = __fadd_rn(run, entry_mass(es[u], tbits, tmask, s_bhat));
-                    if (!found && run >= x) {
-                        topic = es[u] & tmask;
-                        found = true;
+                for (uint32_t u = 0; u < kGroupSectors; ++u) {
+                    if (u == 0 && g == 0) q[u] = h;
+                    else if (base + u < nsect) q[u] = ldg_sector(row + 2 * (base + u));
+                    else q[u] = Sector{make_uint4(0u, 0u, 0u, 0u), make_uint4(0u, 0u, 0u, 0u)};
+                }
+#pragma unroll
+                for (uint32_t u = 0; u < kGroupSectors; ++u) {
+                    s = acc_quad(s, q[u].lo, tbits, tmask, s_bhat);
+                    s = acc_quad(s, q[u].hi, tbits, tmask, s_bhat);
+                }
+                if (g < kCheckpoints) ck[g * NT] = s;
+            }
+
+            if (ub < __fdiv_rn(s, __fadd_rn(s, qv))) {
+                // Sparse branch: first running prefix >= p*S (prefix_search, sampler.hpp:18-41).
+                const float xs = __fmul_rn(up, s);
+                if (xs == 0.0f) {
+                    topic = h.lo.y & tmask;  // every prefix is >= 0: the first real entry
+                } else {
+                    // The first group whose end-of-group sum reaches xs holds the crossing; the
+                    // re-scan restarts from the previous checkpoint, the same f32 value the first
+                    // pass held there, so it is bit-identical.
+                    const uint32_t stored = ngroups < kCheckpoints ? ngroups : kCheckpoints;
+                    uint32_t g = 0;
+                    float run = 0.0f;
+                    while (g < stored && ck[g * NT] < xs) run = ck[g++ * NT];
+                    bool found = false;
+                    for (; g < ngroups && !found; ++g) {
+                        Sector q[kGroupSectors];
+                        const uint32_t base = g * kGroupSectors;
+#pragma unroll
+                        for (uint32_t u = 0; u < kGroupSectors; ++u)
+                            q[u] = base + u < nsect ? ldg_sector(row + 2 * (base + u))
+                                                    : Sector{make_uint4(0u, 0u, 0u, 0u), make_uint4(0u, 0u, 0u, 0u)};
+#pragma unroll
+                        for (uint32_t u = 0; u < kGroupSectors; ++u) {
+                            const uint32_t es[8] = {q[u].lo.x, q[u].lo.y, q[u].lo.z, q[u].lo.w,
+                                                    q[u].hi.x, q[u].hi.y, q[u].hi.z, q[u].hi.w};
+#pragma unroll
+                            for (int w = 0; w < 8; ++w) {
+                                run = __fadd_rn(run, entry_mass(es[w], tbits, tmask, s_bhat));
+                                if (!found && run >= xs) {
+                                    topic = es[w] & tmask;
+                                    found = true;
+                                }
+                            }
+                        }
                     }
                 }
+            } else {
+                // Word branch: WaryTree::sample(p * total) (sampler.hpp:100-106).
+                tree = true;
+                x = __fmul_rn(up, total);
+                if (!(x <= total)) x = total;
             }
-        } else {
-            // Word branch: WaryTree::sample(p * total) == lower_bound(L4, x), clamped.
-            float x = __fmul_rn(up, total);
-            if (!(x <= total)) x = total;
-            uint32_t lo = 0, hi = a.n_l3;
-            while (lo < hi) {
-                const uint32_t mid = (lo + hi) >> 1;
-                if (s_l3[mid] >= x) hi = mid; else lo = mid + 1;
-            }
-            const float4* blk = reinterpret_cast<const float4*>(l4row + lo * kBlock);
-            uint32_t below = 0;
-#pragma unroll
-            for (int u = 0; u < 8; ++u) {
-                const float4 f = __ldg(blk + u);
-                below += (f.x < x) + (f.y < x) + (f.z < x) + (f.w < x);
-            }
-            topic = lo * kBlock + below;
-            if (topic >= a.K) topic = a.K - 1;
         }
-        a.z[t.y] = static_cast<uint16_t>(topic);
-        atomicAdd(brow + topic, 1u);
+        // Cooperative descents for this round's word-branch tokens, one token at a time.
+        uint32_t pending = __ballot_sync(0xffffffffu, tree);
+        while (pending) {
+            const uint32_t src = __ffs(pending) - 1;
+            pending &= pending - 1;
+            const float xs = __shfl_sync(0xffffffffu, x, src);
+            const uint32_t k = warp_tree_search(xs, s_l2, n_l2, s_l3, l4row, lane);
+            if (lane == src) topic = k < a.K ? k : a.K - 1;
+        }
+        if (active) {
+            a.z[t.y] = static_cast<uint16_t>(topic);
+            atomicAdd(brow + topic, 1u);
+        }
     }
     if (a.row_entries) {
         // One atomic per warp.
         for (int o = 16; o > 0; o >>= 1) entries += __shfl_xor_sync(0xffffffffu, entries, o);
-        if (lane_id() == 0) atomicAdd(a.row_entries, entries);
+        if (lane == 0) atomicAdd(a.row_entries, entries);
     }
 }
 
 cudaError_t launch_sampler(const SamplerArgs& a, uint32_t n_units, cudaStream_t s) {
     if (n_units == 0) return cudaSuccess;
-    const size_t smem = sizeof(float) * (static_cast<size_t>(a.K_pad) + a.l3_stride);
-    if (smem <= 48 * 1024) {
+    const size_t base = sizeof(float) * (static_cast<size_t>(a.K_pad) + ((a.n_l3 + 31) & ~31u) + 64);
+    if (base + sizeof(float) * kCheckpoints * 256 <= 64 * 1024) {
+        const size_t smem = base + sizeof(float) * kCheckpoints * 256;
+        static bool configured = false;
+        if (!configured) {
+            cudaFuncSetAttribute(sampler_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+            configured = true;
+        }
         sampler_kernel<256><<<n_units, 256, smem, s>>>(a);
     } else {
+        const size_t smem = base + sizeof(float) * kCheckpoints * 512;
         static bool configured = false;
         if (!configured) {
             cudaFuncSetAttribute(sampler_kernel<512>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -170,12 +277,8 @@ __global__ void __launch_bounds__(kSscWarps * 32) ssc_warp_kernel(SscArgs a) {
     for (uint32_t d = gw; d < a.D; d += nw) {
         const uint32_t s0 = __ldg(a.doc_start + d);
         const uint32_t n = __ldg(a.doc_start + d + 1) - s0;
-        if (n > kSscWarpCap) continue;  // ssc_long_kernel
-        const uint32_t row = a.hdr[d].x * 4u;
-        if (n == 0) {
-            if (lane == 0) a.hdr[d].y = 0;
-            continue;
-        }
+        if (n > kSscWarpCap || n == 0) continue;  // ssc_long_kernel / empty document
+        const uint32_t row = __ldg(a.row4 + d) * 4u;
         uint32_t N = 1;
         while (N < n) N <<= 1;
         for (uint32_t i = lane; i < N; i += 32) keys[i] = i < n ? a.z[s0 + i] : 0xFFFFFFFFu;
@@ -205,15 +308,16 @@ __global__ void __launch_bounds__(kSscWarps * 32) ssc_warp_kernel(SscArgs a) {
             nnz += __popc(ballot);
         }
         __syncwarp();
+        // Row: header (nnz-1, count 0), entries, zero-count padding to a multiple of 8.
         for (uint32_t r = lane; r < nnz; r += 32) {
             const uint32_t st = starts[r];
             const uint32_t en = r + 1 < nnz ? starts[r + 1] : n;
-            a.A[row + r] = keys[st] | ((en - st) << a.tbits);
+            a.A[row + 1 + r] = keys[st] | ((en - st) << a.tbits);
         }
-        const uint32_t padded = (nnz + 3u) & ~3u;
-        for (uint32_t r = nnz + lane; r < padded; r += 32) a.A[row + r] = 0u;
+        const uint32_t padded = (nnz + 8u) & ~7u;
+        for (uint32_t r = nnz + 1 + lane; r < padded; r += 32) a.A[row + r] = 0u;
         if (lane == 0) {
-            a.hdr[d].y = nnz;
+            a.A[row] = nnz - 1u;
             nnz_acc += nnz;
         }
         __syncwarp();
@@ -233,7 +337,7 @@ __global__ void __launch_bounds__(256) ssc_long_kernel(SscArgs a) {
         const uint32_t d = a.long_docs[li];
         const uint32_t s0 = a.doc_start[d];
         const uint32_t n = a.doc_start[d + 1] - s0;
-        const uint32_t row = a.hdr[d].x * 4u;
+        const uint32_t row = a.row4[d] * 4u;
         for (uint32_t k = tid; k < a.K_pad; k += 256) hist[k] = 0;
         __syncthreads();
         for (uint32_t i = tid; i < n; i += 256) atomicAdd(hist + a.z[s0 + i], 1u);
@@ -253,12 +357,12 @@ __global__ void __launch_bounds__(256) ssc_long_kernel(SscArgs a) {
         uint32_t pos = s_scan[tid] - mine;
         for (uint32_t k = b0; k < b1; ++k) {
             const uint32_t c = hist[k];
-            if (c) a.A[row + pos++] = k | (c << a.tbits);
+            if (c) a.A[row + 1 + pos++] = k | (c << a.tbits);
         }
-        const uint32_t padded = (nnz + 3u) & ~3u;
-        for (uint32_t r = nnz + tid; r < padded; r += 256) a.A[row + r] = 0u;
+        const uint32_t padded = (nnz + 8u) & ~7u;
+        for (uint32_t r = nnz + 1 + tid; r < padded; r += 256) a.A[row + r] = 0u;
         if (tid == 0) {
-            a.hdr[d].y = nnz;
+            a.A[row] = nnz - 1u;
             atomicAdd(a.nnz_total, static_cast<unsigned long long>(nnz));
         }
         __syncthreads();
@@ -510,64 +614,71 @@ cudaError_t launch_invert_perm(const uint32_t* input_of_slot, uint64_t T, uint32
     return cudaGetLastError();
 }
 
-// Keys in slot order so that equal (word, doc) keep slot (== corpus) order
-// under the stable radix sort: the reference's (word, doc, token_id) order
-// (corpus.cpp:157-167).
+// Execution-order sort key, laid out in slot order so that equal keys keep slot
+// (== corpus) order under the stable radix sort:
+//   word | (lmax - len_doc) | doc_local
+// i.e. the reference's (word, doc, token_id) order (corpus.cpp:157-167) refined by
+// descending document length inside each word segment, so the lanes of a sampler
+// warp walk C_dk rows of similar length.  lbits == 0 gives the canonical order.
 __global__ void make_keys_kernel(const uint32_t* word, const uint32_t* doc_local,
-                                 const uint32_t* input_of_slot, uint64_t T, uint32_t dbits,
-                                 unsigned long long* keys, uint32_t* vals) {
+                                 const uint32_t* input_of_slot, const uint32_t* doc_len, uint64_t T,
+                                 KeyLayout kl, unsigned long long* keys, uint32_t* vals) {
     for (uint64_t j = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; j < T;
          j += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
         const uint64_t i = input_of_slot ? input_of_slot[j] : j;
-        keys[j] = (static_cast<unsigned long long>(word[i]) << dbits) | doc_local[i];
+        const uint32_t d = doc_local[i];
+        const unsigned long long lk = kl.lbits ? static_cast<unsigned long long>(kl.lmax - doc_len[d]) : 0ull;
+        keys[j] = (static_cast<unsigned long long>(word[i]) << (kl.dbits + kl.lbits)) | (lk << kl.dbits) | d;
         vals[j] = static_cast<uint32_t>(j);
     }
 }
 
-cudaError_t launch_make_keys(const uint32_t* word, const uint32_t* doc_local,
-                             const uint32_t* input_of_slot, uint64_t T, uint32_t dbits,
-                             unsigned long long* keys, uint32_t* vals, cudaStream_t s) {
+cudaError_t launch_make_keys(const uint32_t* word, const uint32_t* doc_local, const uint32_t* input_of_slot,
+                             const uint32_t* doc_len, uint64_t T, KeyLayout kl, unsigned long long* keys,
+                             uint32_t* vals, cudaStream_t s) {
     if (T == 0) return cudaSuccess;
-    make_keys_kernel<<<grid_for(T, 256), 256, 0, s>>>(word, doc_local, input_of_slot, T, dbits, keys, vals);
+    make_keys_kernel<<<grid_for(T, 256), 256, 0, s>>>(word, doc_local, input_of_slot, doc_len, T, kl, keys, vals);
     return cudaGetLastError();
 }
 
-__global__ void make_tok_kernel(const unsigned long long* keys, const uint32_t* slots, uint64_t T,
-                                uint32_t dbits, uint2* tok, uint32_t* seg_flag) {
-    const unsigned long long dmask = (1ull << dbits) - 1ull;
+// tok = {C_dk row offset (quads), slot}; flags mark word-segment starts.
+__global__ void make_tok_kernel(const unsigned long long* keys, const uint32_t* slots, const uint32_t* row4,
+                                uint64_t T, KeyLayout kl, uint2* tok, uint32_t* seg_flag) {
+    const unsigned long long dmask = (1ull << kl.dbits) - 1ull;
+    const uint32_t ws = kl.dbits + kl.lbits;
     for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < T;
          i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
         const unsigned long long k = keys[i];
-        tok[i] = make_uint2(static_cast<uint32_t>(k & dmask), slots[i]);
-        seg_flag[i] = (i == 0 || (keys[i - 1] >> dbits) != (k >> dbits)) ? 1u : 0u;
+        tok[i] = make_uint2(row4[k & dmask], slots[i]);
+        seg_flag[i] = (i == 0 || (keys[i - 1] >> ws) != (k >> ws)) ? 1u : 0u;
     }
 }
 
-cudaError_t launch_make_tok(const unsigned long long* keys, const uint32_t* slots, uint64_t T,
-                            uint32_t dbits, uint2* tok, uint32_t* seg_flag, cudaStream_t s) {
+cudaError_t launch_make_tok(const unsigned long long* keys, const uint32_t* slots, const uint32_t* row4,
+                            uint64_t T, KeyLayout kl, uint2* tok, uint32_t* seg_flag, cudaStream_t s) {
     if (T == 0) return cudaSuccess;
-    make_tok_kernel<<<grid_for(T, 256), 256, 0, s>>>(keys, slots, T, dbits, tok, seg_flag);
+    make_tok_kernel<<<grid_for(T, 256), 256, 0, s>>>(keys, slots, row4, T, kl, tok, seg_flag);
     return cudaGetLastError();
 }
 
 __global__ void emit_segments_kernel(const unsigned long long* keys, const uint32_t* seg_flag,
-                                     const uint32_t* seg_index, uint64_t T, uint32_t dbits,
+                                     const uint32_t* seg_index, uint64_t T, uint32_t wshift,
                                      uint32_t* seg_word, uint32_t* seg_off) {
     for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < T;
          i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
         if (seg_flag[i]) {
             const uint32_t s = seg_index[i];
-            seg_word[s] = static_cast<uint32_t>(keys[i] >> dbits);
+            seg_word[s] = static_cast<uint32_t>(keys[i] >> wshift);
             seg_off[s] = static_cast<uint32_t>(i);
         }
     }
 }
 
 cudaError_t launch_emit_segments(const unsigned long long* keys, const uint32_t* seg_flag,
-                                 const uint32_t* seg_index, uint64_t T, uint32_t dbits,
+                                 const uint32_t* seg_index, uint64_t T, uint32_t wshift,
                                  uint32_t* seg_word, uint32_t* seg_off, cudaStream_t s) {
     if (T == 0) return cudaSuccess;
-    emit_segments_kernel<<<grid_for(T, 256), 256, 0, s>>>(keys, seg_flag, seg_index, T, dbits, seg_word,
+    emit_segments_kernel<<<grid_for(T, 256), 256, 0, s>>>(keys, seg_flag, seg_index, T, wshift, seg_word,
                                                          seg_off);
     return cudaGetLastError();
 }
@@ -622,28 +733,17 @@ cudaError_t launch_emit_units(const uint32_t* schedule, const uint32_t* seg_word
     return cudaGetLastError();
 }
 
-// A row capacity in uint4 units: nnz_d <= len_d (test_counts.cpp:149-150).
+// C_dk row capacity in uint4 units: header + nnz_d entries with nnz_d <= len_d
+// (test_counts.cpp:149-150), rounded up to 8 entries (one 32-byte sector).
 __global__ void row_quads_kernel(const uint32_t* doc_start, uint32_t D, uint32_t* quads) {
     const uint32_t d = blockIdx.x * blockDim.x + threadIdx.x;
     if (d >= D) return;
-    quads[d] = (doc_start[d + 1] - doc_start[d] + 3u) >> 2;
+    quads[d] = ((doc_start[d + 1] - doc_start[d] + 8u) >> 3) << 1;
 }
 
 cudaError_t launch_row_quads(const uint32_t* doc_start, uint32_t D, uint32_t* quads, cudaStream_t s) {
     if (D == 0) return cudaSuccess;
     row_quads_kernel<<<(D + 255) / 256, 256, 0, s>>>(doc_start, D, quads);
-    return cudaGetLastError();
-}
-
-__global__ void init_hdr_kernel(const uint32_t* row4, uint32_t D, uint2* hdr) {
-    const uint32_t d = blockIdx.x * blockDim.x + threadIdx.x;
-    if (d >= D) return;
-    hdr[d] = make_uint2(row4[d], 0u);
-}
-
-cudaError_t launch_init_hdr(const uint32_t* row4, uint32_t D, uint2* hdr, cudaStream_t s) {
-    if (D == 0) return cudaSuccess;
-    init_hdr_kernel<<<(D + 255) / 256, 256, 0, s>>>(row4, D, hdr);
     return cudaGetLastError();
 }
 

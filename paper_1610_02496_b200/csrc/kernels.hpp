@@ -16,10 +16,9 @@ constexpr uint32_t kUnitMaxTokens = 8192;  // sampler: max tokens per unit (one 
 constexpr uint32_t kSscWarpCap = 512;      // SSC: docs up to this length take the warp path
 
 struct SamplerArgs {
-    const uint2* tok;       // PDOW order: {doc_local, slot}
+    const uint2* tok;       // execution order: {C_dk row offset in uint4 units, slot}
     const Unit* units;      // heavy-first
-    const uint2* hdr;       // per doc: {row offset in uint4 units, nnz}
-    const uint32_t* A;      // packed C_dk entries: topic | count << tbits
+    const uint32_t* A;      // C_dk rows: [nnz-1 | entries topic | count << tbits | zero pad to 8]
     const float* bhat;      // V_pad x K_pad
     const float* l4;        // V_pad x K_pad (inclusive prefix, padded with the total)
     const float* l3;        // V_pad x l3_stride (L4 block maxima)
@@ -39,7 +38,7 @@ struct SscArgs {
     const uint16_t* z;          // topics by slot (doc-grouped)
     const uint32_t* doc_start;  // D+1 slot offsets
     uint32_t D;
-    uint2* hdr;                 // writes .y = nnz
+    const uint32_t* row4;       // per doc: row offset in uint4 units
     uint32_t* A;
     uint32_t tbits, K_pad;
     const uint32_t* long_docs;  // docs longer than kSscWarpCap
@@ -70,13 +69,16 @@ cudaError_t launch_doc_hist(const uint32_t* doc_local, uint64_t T, uint32_t* cou
 cudaError_t launch_iota(uint32_t* out, uint64_t n, cudaStream_t s);
 cudaError_t launch_invert_perm(const uint32_t* input_of_slot, uint64_t T, uint32_t* slot_of_input,
                                cudaStream_t s);
-cudaError_t launch_make_keys(const uint32_t* word, const uint32_t* doc_local,
-                             const uint32_t* input_of_slot, uint64_t T, uint32_t dbits,
-                             unsigned long long* keys, uint32_t* vals, cudaStream_t s);
-cudaError_t launch_make_tok(const unsigned long long* keys, const uint32_t* slots, uint64_t T,
-                            uint32_t dbits, uint2* tok, uint32_t* seg_flag, cudaStream_t s);
+struct KeyLayout {
+    uint32_t dbits, lbits, lmax;  // doc bits, length bits (0 = canonical order), max length
+};
+cudaError_t launch_make_keys(const uint32_t* word, const uint32_t* doc_local, const uint32_t* input_of_slot,
+                             const uint32_t* doc_len, uint64_t T, KeyLayout kl, unsigned long long* keys,
+                             uint32_t* vals, cudaStream_t s);
+cudaError_t launch_make_tok(const unsigned long long* keys, const uint32_t* slots, const uint32_t* row4,
+                            uint64_t T, KeyLayout kl, uint2* tok, uint32_t* seg_flag, cudaStream_t s);
 cudaError_t launch_emit_segments(const unsigned long long* keys, const uint32_t* seg_flag,
-                                 const uint32_t* seg_index, uint64_t T, uint32_t dbits,
+                                 const uint32_t* seg_index, uint64_t T, uint32_t wshift,
                                  uint32_t* seg_word, uint32_t* seg_off, cudaStream_t s);
 cudaError_t launch_segment_lengths(const uint32_t* seg_off, uint32_t nseg, uint64_t T,
                                    uint32_t* seg_len, unsigned long long* sched_keys,
@@ -88,7 +90,6 @@ cudaError_t launch_emit_units(const uint32_t* schedule, const uint32_t* seg_word
                               cudaStream_t s);
 cudaError_t launch_row_quads(const uint32_t* doc_start, uint32_t D, uint32_t* quads,
                              cudaStream_t s);
-cudaError_t launch_init_hdr(const uint32_t* row4, uint32_t D, uint2* hdr, cudaStream_t s);
 cudaError_t launch_long_flags(const uint32_t* doc_start, uint32_t D, uint32_t* flags,
                               cudaStream_t s);
 cudaError_t launch_init_topics(uint64_t T, const uint64_t* ids, uint64_t id_base, uint64_t seed,

@@ -85,7 +85,9 @@ def test_pdow_layout_matches_reference(name, golden):
     # build_schedule (corpus.cpp:200-210): stable by (length desc, word asc).
     order = sorted(range(len(p["seg_word"])), key=lambda s: (-int(p["seg_length"][s]), int(p["seg_word"][s])))
     assert lay["schedule"].tolist() == order
-    # ... and the reference's own chunk arrays (digests from oracle/_ref).
+    # ... and the reference's own chunk arrays (digests from oracle/_ref) when it ran one chunk.
+    if spec.get("chunks", 1) != 1:
+        return
     ref = golden["cases"][name]["pdow"]
     assert digest(lay["sorted_doc"]) == ref["sorted_doc"]
     assert digest(lay["sorted_word"]) == ref["sorted_word"]
