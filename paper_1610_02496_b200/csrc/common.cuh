@@ -18,10 +18,13 @@ constexpr uint32_t kInitAssignStream = 0xFFFFFFFFu; // rng.hpp:43
 constexpr uint32_t kHeldoutInitStream = 0xFFFD0000u;
 constexpr uint32_t kHeldoutSweepBase = 0xFFFE0000u;
 
-// L4 block width of the device sampling tree: the search is lower_bound over
-// the row's inclusive prefix (acceptance.cpp:140-200 proves WaryTree::sample
-// equal to it for every W), staged as one 32-wide block per L3 entry.
+// K is padded to a multiple of kBlock.  The device search is lower_bound over
+// the row's inclusive prefix L4 (acceptance.cpp:140-200 proves WaryTree::sample
+// equal to it for every W).
 constexpr uint32_t kBlock = 32;
+// Leaf width of the device descent: L8[j] = L4[8j+7] is staged in shared memory and
+// the final 8 prefixes are one 32-byte sector.
+constexpr uint32_t kLeaf = 8;
 
 // Philox4x32-10, rng.hpp:14-37.  Counter (kind, elem_lo, elem_hi, block),
 // key (seed_lo, seed_hi) -- rng.hpp:51-54.

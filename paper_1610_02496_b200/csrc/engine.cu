@@ -8,7 +8,7 @@
 //                       position for a doc-sorted corpus)
 //   A     u32[4*Q]      C_dk rows: [nnz-1 | entries topic | count << tbits | zero
 //                       padding to a multiple of 8], 32-byte aligned at row4[d]
-//   B     u32[V_pad][K_pad], bhat/L4 f32[V_pad][K_pad], L3 f32[V_pad][l3s], Q f32[V_pad]
+//   B     u32[V_pad][K_pad], bhat/L4 f32[V_pad][K_pad], L8 f32[V_pad][l8s] (every 8th prefix), Q f32[V_pad]
 // Reference paths are relative to /root/reference/proj.
 #include <dlfcn.h>
 
@@ -138,7 +138,7 @@ struct slda_engine {
     int device = 0;
     cudaStream_t stream = nullptr;
     uint32_t D_all = 0, doc_begin = 0, doc_end = 0, D = 0;  // D = shard documents
-    uint32_t V = 0, V_pad = 0, K = 0, K_pad = 0, l3_stride = 0, n_l3 = 0, tbits = 1;
+    uint32_t V = 0, V_pad = 0, K = 0, K_pad = 0, l8_stride = 0, n_l8 = 0, tbits = 1;
     uint64_t T = 0;
     double alpha = 0, beta = 0;
     float falpha = 0;
@@ -155,7 +155,7 @@ struct slda_engine {
     DevMem tok, z, doc_start, row4, A, units, long_docs, hist_scratch;
     DevMem seg_word, seg_off, seg_len, schedule;  // PDOW getters
     DevMem input_of_slot, ids;                    // only for non doc-major input / explicit ids
-    DevMem B, bhat, l4, l3, q, colsum, denom, zv, counters;
+    DevMem B, bhat, l4, l8, q, colsum, denom, zv, counters;
 
     // Per-iteration phase events, a ring so async iterations can be profiled afterwards.
     static constexpr uint32_t kRing = 64;
@@ -229,8 +229,8 @@ struct slda_engine {
         V = vocab;
         V_pad = (V + world - 1) / world * world;
         K_pad = (K + slda::kBlock - 1) / slda::kBlock * slda::kBlock;
-        n_l3 = K_pad / slda::kBlock;
-        l3_stride = (n_l3 + 3) / 4 * 4;
+        n_l8 = K_pad / slda::kLeaf;
+        l8_stride = (n_l8 + 3) / 4 * 4;
         tbits = bits_for(K - 1 ? K - 1 : 1);
         device = c.device;
         if (device < 0) CK(cudaGetDevice(&device));
@@ -252,7 +252,7 @@ struct slda_engine {
         B.alloc(cells * 4, &device_bytes);
         bhat.alloc(cells * 4, &device_bytes);
         l4.alloc(cells * 4, &device_bytes);
-        l3.alloc(static_cast<size_t>(V_pad) * l3_stride * 4, &device_bytes);
+        l8.alloc(static_cast<size_t>(V_pad) * l8_stride * 4, &device_bytes);
         q.alloc(static_cast<size_t>(V_pad) * 4, &device_bytes);
         colsum.alloc(static_cast<size_t>(K_pad) * 8, &device_bytes);
         denom.alloc(static_cast<size_t>(K_pad) * 8, &device_bytes);
@@ -260,7 +260,7 @@ struct slda_engine {
         counters.alloc(8 * (1 + kRing), &device_bytes);
         CK(cudaMemsetAsync(bhat.p, 0, bhat.bytes, stream));
         CK(cudaMemsetAsync(l4.p, 0, l4.bytes, stream));
-        CK(cudaMemsetAsync(l3.p, 0, l3.bytes, stream));
+        CK(cudaMemsetAsync(l8.p, 0, l8.bytes, stream));
         CK(cudaMemsetAsync(q.p, 0, q.bytes, stream));
     }
 
@@ -382,7 +382,7 @@ void slda_engine::build(const slda_corpus_view& cv, const slda_config& c) {
         CK(slda::launch_row_quads(doc_start.as<uint32_t>(), D, quads.as<uint32_t>(), stream));
         exclusive_sum(quads.as<uint32_t>(), row4.as<uint32_t>(), static_cast<uint64_t>(D) + 1);
         const uint32_t total_quads = D ? d2h_scalar(row4.as<uint32_t>() + D) : 0;
-        A.alloc(static_cast<size_t>(total_quads) * 16 + 256, &device_bytes);
+        A.alloc(static_cast<size_t>(total_quads) * 16 + 512, &device_bytes);  // speculative group reads
         CK(cudaMemsetAsync(A.p, 0, A.bytes, stream));
     }
 
@@ -539,18 +539,18 @@ void slda_engine::m_step() {
                           zv.as<float>(), stream));
     CK(cudaEventRecord(ev[4], stream));
     CK(slda::launch_phi(B.as<uint32_t>(), denom.as<double>(), zv.as<float>(), bhat.as<float>(), l4.as<float>(),
-                        l3.as<float>(), q.as<float>(), r0, r1, K, K_pad, l3_stride, beta, falpha, stream));
+                        l8.as<float>(), q.as<float>(), r0, r1, K, K_pad, l8_stride, beta, falpha, stream));
     launches += 3;
     CK(cudaEventRecord(ev[5], stream));
     if (world > 1) {
         auto& n = nccl();
-        const size_t l3_slice = static_cast<size_t>(slice_rows()) * l3_stride;
+        const size_t l8_slice = static_cast<size_t>(slice_rows()) * l8_stride;
         nccl_check(n.GroupStart(), "ncclGroupStart");
         nccl_check(n.AllGather(bhat.as<float>() + rank * slice_cells, bhat.p, slice_cells, ncclFloat32, comm,
                                stream), "ncclAllGather(bhat)");
         nccl_check(n.AllGather(l4.as<float>() + rank * slice_cells, l4.p, slice_cells, ncclFloat32, comm,
                                stream), "ncclAllGather(L4)");
-        nccl_check(n.AllGather(l3.as<float>() + rank * l3_slice, l3.p, l3_slice, ncclFloat32, comm, stream),
+        nccl_check(n.AllGather(l8.as<float>() + rank * l8_slice, l8.p, l8_slice, ncclFloat32, comm, stream),
                    "ncclAllGather(L3)");
         nccl_check(n.AllGather(q.as<float>() + rank * slice_rows(), q.p, slice_rows(), ncclFloat32, comm,
                                stream), "ncclAllGather(Q)");
@@ -574,7 +574,7 @@ void slda_engine::enqueue_iteration() {
     a.A = A.as<uint32_t>();
     a.bhat = bhat.as<float>();
     a.l4 = l4.as<float>();
-    a.l3 = l3.as<float>();
+    a.l8 = l8.as<float>();
     a.q = q.as<float>();
     a.ids = ids.p ? ids.as<uint64_t>() : nullptr;
     a.z = z.as<uint16_t>();
@@ -584,8 +584,8 @@ void slda_engine::enqueue_iteration() {
     a.stream_kind = iteration;  // trainer.cpp:423
     a.K = K;
     a.K_pad = K_pad;
-    a.l3_stride = l3_stride;
-    a.n_l3 = n_l3;
+    a.l8_stride = l8_stride;
+    a.n_l8 = n_l8;
     a.tbits = tbits;
     a.row_entries = entries_counter();
     CK(slda::launch_sampler(a, n_units, stream));
@@ -979,7 +979,7 @@ int slda_heldout_ll(slda_engine* e, uint32_t num_docs, uint32_t vocab_size, uint
         a.evl_word = d_evl.as<uint32_t>();
         a.bhat = e->bhat.as<float>();
         a.l4 = e->l4.as<float>();
-        a.l3 = e->l3.as<float>();
+        a.l8 = e->l8.as<float>();
         a.q = e->q.as<float>();
         a.row_mass = d_mass.as<double>();
         a.ll_out = d_ll.as<double>();
@@ -988,8 +988,8 @@ int slda_heldout_ll(slda_engine* e, uint32_t num_docs, uint32_t vocab_size, uint
         a.burn_in = burn_in;
         a.K = e->K;
         a.K_pad = e->K_pad;
-        a.l3_stride = e->l3_stride;
-        a.n_l3 = e->n_l3;
+        a.l8_stride = e->l8_stride;
+        a.n_l8 = e->n_l8;
         a.cap = cap;
         CK(slda::launch_heldout(a, num_docs, e->V, e->K, e->K_pad, d_mass.as<double>(), e->stream));
         std::vector<double> ll(n_evl);

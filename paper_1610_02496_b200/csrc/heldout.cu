@@ -112,18 +112,19 @@ __global__ void __launch_bounds__(256) heldout_kernel(HeldoutArgs a) {
                 }
             } else {
                 const float* l4row = a.l4 + static_cast<size_t>(v) * a.K_pad;
-                const float* l3row = a.l3 + static_cast<size_t>(v) * a.l3_stride;
+                const float* l8row = a.l8 + static_cast<size_t>(v) * a.l8_stride;
                 const float total = __ldg(l4row + a.K_pad - 1);
                 float x = __fmul_rn(up, total);
                 if (!(x <= total)) x = total;
-                uint32_t lo = 0, hi = a.n_l3;
+                // lower_bound over L4 (== WaryTree::sample): L8 level, then an 8-prefix leaf.
+                uint32_t lo = 0, hi = a.n_l8 - 1;  // last L8 entry == total >= x
                 while (lo < hi) {
                     const uint32_t mid = (lo + hi) >> 1;
-                    if (__ldg(l3row + mid) >= x) hi = mid; else lo = mid + 1;
+                    if (__ldg(l8row + mid) >= x) hi = mid; else lo = mid + 1;
                 }
                 uint32_t below = 0;
-                for (uint32_t c = 0; c < kBlock; ++c) below += __ldg(l4row + lo * kBlock + c) < x;
-                topic = lo * kBlock + below;
+                for (uint32_t c = 0; c < kLeaf; ++c) below += __ldg(l4row + lo * kLeaf + c) < x;
+                topic = lo * kLeaf + below;
                 if (topic >= a.K) topic = a.K - 1;
             }
             keys[j] = topic;  // keys is free once the counts are built

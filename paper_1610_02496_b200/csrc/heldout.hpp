@@ -13,13 +13,13 @@ struct HeldoutArgs {
     const uint32_t* evl_word;
     const float* bhat;
     const float* l4;
-    const float* l3;
+    const float* l8;
     const float* q;
     const double* row_mass;    // filled by launch_heldout
     double* ll_out;            // per evaluation token log(mass / denom)
     uint64_t seed;
     double alpha;
-    uint32_t burn_in, K, K_pad, l3_stride, n_l3;
+    uint32_t burn_in, K, K_pad, l8_stride, n_l8;
     uint32_t cap;              // power of two >= the longest estimation half
 };
 

@@ -53,48 +53,92 @@ struct Sector {
 };
 __device__ __forceinline__ Sector ldg_sector(const uint4* p) {
     Sector s;
-    asm volatile("ld.global.nc.L1::no_allocate.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+    asm("ld.global.nc.L1::no_allocate.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
                  : "=r"(s.lo.x), "=r"(s.lo.y), "=r"(s.lo.z), "=r"(s.lo.w), "=r"(s.hi.x), "=r"(s.hi.y),
                    "=r"(s.hi.z), "=r"(s.hi.w)
                  : "l"(p));
     return s;
 }
 
-// Rows are consumed in groups of 4 sectors (32 entries) with all 4 loads in flight.
+// Rows are consumed in groups of 4 sectors (32 entries).  The group's loads are issued
+// by one PTX block so all four are in flight together (ptxas otherwise serialises them
+// behind the consuming arithmetic to save registers).  Sectors i >= n are not loaded
+// and keep their (zero) input values, which add +0 like the row padding.
 constexpr uint32_t kGroupSectors = 4;
+#define SLDA_R8(s) "+r"(s.lo.x), "+r"(s.lo.y), "+r"(s.lo.z), "+r"(s.lo.w), "+r"(s.hi.x), "+r"(s.hi.y), \
+                   "+r"(s.hi.z), "+r"(s.hi.w)
+__device__ __forceinline__ void ldg_sectors4(const uint4* p, uint32_t n, Sector& a, Sector& b, Sector& c,
+                                             Sector& d) {
+    asm("{\n\t.reg .pred p0, p1, p2, p3;\n\t"
+        "setp.gt.u32 p0, %33, 0;\n\t"
+        "setp.gt.u32 p1, %33, 1;\n\t"
+        "setp.gt.u32 p2, %33, 2;\n\t"
+        "setp.gt.u32 p3, %33, 3;\n\t"
+        "@p0 ld.global.nc.L1::no_allocate.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%32];\n\t"
+        "@p1 ld.global.nc.L1::no_allocate.v8.u32 {%8,%9,%10,%11,%12,%13,%14,%15}, [%32+32];\n\t"
+        "@p2 ld.global.nc.L1::no_allocate.v8.u32 {%16,%17,%18,%19,%20,%21,%22,%23}, [%32+64];\n\t"
+        "@p3 ld.global.nc.L1::no_allocate.v8.u32 {%24,%25,%26,%27,%28,%29,%30,%31}, [%32+96];\n\t}"
+        : SLDA_R8(a), SLDA_R8(b), SLDA_R8(c), SLDA_R8(d)
+        : "l"(p), "r"(n));
+}
+__device__ __forceinline__ Sector zero_sector() { return Sector{make_uint4(0u, 0u, 0u, 0u), make_uint4(0u, 0u, 0u, 0u)}; }
 // Running sums at the end of the first kCheckpoints groups, so the prefix pass of the
 // sparse branch re-reads one group instead of the row.
 constexpr uint32_t kCheckpoints = 8;
 
-// lower_bound over the word's L4 prefix (== WaryTree::sample, acceptance.cpp:140-200)
-// by one warp: L2 (smem, <= 64 block maxima of L3) -> L3 (smem, one 32-block) -> L4
-// (global, one coalesced 128-byte block).  Returns the first index with L4 >= x.
-__device__ __forceinline__ uint32_t warp_tree_search(float x, const float* s_l2, uint32_t n_l2,
-                                                     const float* s_l3, const float* l4row, uint32_t lane) {
-    uint32_t j2;
-    {
-        const uint32_t b0 = __ballot_sync(0xffffffffu, lane < n_l2 && s_l2[lane] >= x);
-        if (b0) {
-            j2 = __ffs(b0) - 1;
-        } else {
-            const uint32_t b1 = __ballot_sync(0xffffffffu, lane + 32 < n_l2 && s_l2[lane + 32] >= x);
-            j2 = b1 ? 31 + __ffs(b1) : n_l2 - 1;
-        }
+// lower_bound over the word's L4 prefix (== WaryTree::sample, acceptance.cpp:140-200):
+// binary search of the staged L8 level (first 8-block whose last prefix >= x), then one
+// 32-byte sector of L4.  Returns the first index with L4 >= x (x <= total).
+__device__ __forceinline__ uint32_t tree_search(float x, const float* s_l8, uint32_t n_l8, const float* l4row) {
+    uint32_t lo = 0, hi = n_l8 - 1;  // s_l8[n_l8 - 1] == total >= x
+    while (lo < hi) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (s_l8[mid] >= x) hi = mid; else lo = mid + 1;
     }
-    const uint32_t b3 = __ballot_sync(0xffffffffu, s_l3[j2 * 32 + lane] >= x);
-    const uint32_t j3 = j2 * 32 + (b3 ? __ffs(b3) - 1 : 31);
-    const uint32_t b4 = __ballot_sync(0xffffffffu, __ldg(l4row + j3 * 32 + lane) >= x);
-    return j3 * 32 + (b4 ? __ffs(b4) - 1 : 31);
+    const Sector b = ldg_sector(reinterpret_cast<const uint4*>(l4row + lo * kLeaf));
+    const uint32_t below = (__uint_as_float(b.lo.x) < x) + (__uint_as_float(b.lo.y) < x) +
+                           (__uint_as_float(b.lo.z) < x) + (__uint_as_float(b.lo.w) < x) +
+                           (__uint_as_float(b.hi.x) < x) + (__uint_as_float(b.hi.y) < x) +
+                           (__uint_as_float(b.hi.z) < x) + (__uint_as_float(b.hi.w) < x);
+    return lo * kLeaf + below;
+}
+
+// Per-warp staging of C_dk rows: 32 rows x 4 sectors (128 B), 144-byte row stride so both
+// the cooperative stores and each lane's 128-bit reads of its own row are conflict-free.
+// Lane-private random row reads cap at ~1.5 TB/s on B200 (L1TEX: one line per lane per
+// load); the warp-cooperative layout (lane -> row 8j + lane/4, sector lane%4) is coalesced
+// per row and measured at 3.7-6 TB/s (scripts/microbench_rows.cu).
+constexpr uint32_t kStageRow = 144;
+constexpr uint32_t kStageWarp = 32 * kStageRow;
+
+__device__ __forceinline__ void sts_sector(unsigned char* p, const Sector& q) {
+    *reinterpret_cast<uint4*>(p) = q.lo;
+    *reinterpret_cast<uint4*>(p + 16) = q.hi;
+}
+
+// Cooperative load of one 4-sector group of each of the warp's 32 rows into the stage.
+// rq[j] / ns[j]: quad offset and sector count of row 8j + lane/4 (ns = 0: skip the row);
+// gs[j]: first sector of the group for that row.
+__device__ __forceinline__ void stage_group(const uint4* A4, const uint32_t (&rq)[4], const uint32_t (&ns)[4],
+                                            const uint32_t (&gs)[4], uint32_t sub, uint32_t grp,
+                                            unsigned char* stage) {
+    Sector q[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        const uint32_t sec = gs[j] + sub;
+        q[j] = sec < ns[j] ? ldg_sector(A4 + rq[j] + 2 * sec) : zero_sector();
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) sts_sector(stage + (8 * j + grp) * kStageRow + sub * 32, q[j]);
 }
 
 template <int NT>
 __global__ void __launch_bounds__(NT) sampler_kernel(SamplerArgs a) {
     extern __shared__ __align__(16) float sm[];
     float* s_bhat = sm;
-    const uint32_t l3s32 = (a.n_l3 + 31) & ~31u;
-    float* s_l3 = sm + a.K_pad;             // l3s32 (padded with the total)
-    float* s_l2 = s_l3 + l3s32;             // 64
-    float* s_ck = s_l2 + 64;                // [kCheckpoints][NT]
+    float* s_l8 = sm + a.K_pad;             // l8_stride (L4[8j+7], padded with the total)
+    float* s_ck = s_l8 + a.l8_stride;       // [kCheckpoints][NT]
+    unsigned char* s_stage = reinterpret_cast<unsigned char*>(s_ck + kCheckpoints * NT);
 
     const Unit unit = a.units[blockIdx.x];
     const uint32_t v = unit.word;
@@ -104,121 +148,135 @@ __global__ void __launch_bounds__(NT) sampler_kernel(SamplerArgs a) {
         const float4* gb = reinterpret_cast<const float4*>(a.bhat + static_cast<size_t>(v) * a.K_pad);
         float4* sb = reinterpret_cast<float4*>(s_bhat);
         for (uint32_t i = threadIdx.x; i < a.K_pad / 4; i += NT) sb[i] = __ldg(gb + i);
-        const float4* gl = reinterpret_cast<const float4*>(a.l3 + static_cast<size_t>(v) * a.l3_stride);
-        float4* sl = reinterpret_cast<float4*>(s_l3);
-        for (uint32_t i = threadIdx.x; i < a.l3_stride / 4; i += NT) sl[i] = __ldg(gl + i);
-        for (uint32_t i = a.l3_stride + threadIdx.x; i < l3s32; i += NT) s_l3[i] = total;
-        // L2: maxima of 32-wide L3 blocks (the reference tree's top level for W = 32).
-        if (threadIdx.x < 64) {
-            const uint32_t e = threadIdx.x * 32 + 31;
-            s_l2[threadIdx.x] = e < a.n_l3 ? __ldg(a.l3 + static_cast<size_t>(v) * a.l3_stride + e) : total;
-        }
+        const float4* gl = reinterpret_cast<const float4*>(a.l8 + static_cast<size_t>(v) * a.l8_stride);
+        float4* sl = reinterpret_cast<float4*>(s_l8);
+        for (uint32_t i = threadIdx.x; i < a.l8_stride / 4; i += NT) sl[i] = __ldg(gl + i);
     }
-    const uint32_t n_l2 = (a.n_l3 + 31) / 32;
     const float qv = __ldg(a.q + v);
     uint32_t* brow = a.B + static_cast<size_t>(v) * a.K_pad;
     const uint32_t tbits = a.tbits;
     const uint32_t tmask = (1u << tbits) - 1u;
     const uint4* A4 = reinterpret_cast<const uint4*>(a.A);
     float* ck = s_ck + threadIdx.x;
-    const uint32_t lane = lane_id();
+    const uint32_t lane = lane_id(), sub = lane & 3u, grp = lane >> 2;
+    unsigned char* stage = s_stage + (threadIdx.x >> 5) * kStageWarp;
+    const unsigned char* mine = stage + lane * kStageRow;  // this lane's staged row group
     unsigned long long entries = 0;
     __syncthreads();
 
-    // Warp-uniform trip count so the cooperative tree search sees every lane.
-    const uint32_t rounds = (unit.length + NT - 1) / NT;
+    const uint32_t rounds = (unit.length + NT - 1) / NT;  // CTA-uniform
     for (uint32_t r = 0; r < rounds; ++r) {
         const uint32_t i = r * NT + threadIdx.x;
         const bool active = i < unit.length;
-        uint32_t topic = 0;
-        bool tree = false;
-        float x = 0.0f;
-        uint2 t = make_uint2(0u, 0u);
+        const uint2 t = active ? __ldg(a.tok + unit.offset + i) : make_uint2(0u, 0u);  // {row quads, slot}
+        uint32_t rq[4], ns[4], gs[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            rq[j] = __shfl_sync(0xffffffffu, t.x, 8 * j + grp);
+            ns[j] = __shfl_sync(0xffffffffu, active ? 4u : 0u, 8 * j + grp);  // group 0: speculative
+            gs[j] = 0;
+        }
+        __syncwarp();
+        stage_group(A4, rq, ns, gs, sub, grp, stage);
+        __syncwarp();
+
+        // Row = [header | nnz entries ascending topic | zero-count padding to 8]; the
+        // header entry (nnz-1, count 0) and the padding add +0 to every running sum.
+        const uint32_t nnz = active ? (reinterpret_cast<const uint4*>(mine)->x & tmask) + 1u : 0u;
+        const uint32_t nsect = active ? (nnz + 8u) >> 3 : 0u;
+        const uint32_t ngroups = (nsect + 3u) >> 2;
+        entries += nnz;
+        const uint32_t max_groups = __reduce_max_sync(0xffffffffu, ngroups);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) ns[j] = __shfl_sync(0xffffffffu, nsect, 8 * j + grp);
+
+        float ub = 0.0f, up = 0.0f;
         if (active) {
-            t = __ldg(a.tok + unit.offset + i);  // {row quad offset, slot}
-            const uint4* row = A4 + t.x;
-            const Sector h = ldg_sector(row);  // header + first 7 entries
             const uint64_t id = a.ids ? __ldg(a.ids + t.y) : a.id_base + t.y;
-            float ub, up;
             draw2_f32(a.seed, a.stream_kind, id, ub, up);
+        }
 
-            // Row = [header | nnz entries ascending topic | zero-count padding to 8]; the
-            // header entry (nnz-1, count 0) and the padding add +0 to every running sum.
-            const uint32_t nnz = (h.lo.x & tmask) + 1u;
-            const uint32_t nsect = (nnz + 8u) >> 3;
-            const uint32_t ngroups = (nsect + kGroupSectors - 1) / kGroupSectors;
-            entries += nnz;
-
-            // make_branch_context: S = sum_i f32(cnt_i) * bhat[top_i], sequential f32.
-            float s = 0.0f;
-            for (uint32_t g = 0; g < ngroups; ++g) {
-                Sector q[kGroupSectors];
-                const uint32_t base = g * kGroupSectors;
+        // make_branch_context: S = sum_i f32(cnt_i) * bhat[top_i], sequential f32, one
+        // staged group (32 entries) at a time.
+        float s = 0.0f;
+        for (uint32_t g = 0; g < max_groups; ++g) {
+            if (g > 0) {
+                __syncwarp();
 #pragma unroll
-                for (uint32_t u = 0; u < kGroupSectors; ++u) {
-                    if (u == 0 && g == 0) q[u] = h;
-                    else if (base + u < nsect) q[u] = ldg_sector(row + 2 * (base + u));
-                    else q[u] = Sector{make_uint4(0u, 0u, 0u, 0u), make_uint4(0u, 0u, 0u, 0u)};
-                }
+                for (int j = 0; j < 4; ++j) gs[j] = 4 * g;
+                stage_group(A4, rq, ns, gs, sub, grp, stage);
+                __syncwarp();
+            }
+            if (g < ngroups) {
 #pragma unroll
-                for (uint32_t u = 0; u < kGroupSectors; ++u) {
-                    s = acc_quad(s, q[u].lo, tbits, tmask, s_bhat);
-                    s = acc_quad(s, q[u].hi, tbits, tmask, s_bhat);
+                for (uint32_t u = 0; u < 4; ++u) {
+                    if (4 * g + u < nsect) {
+                        s = acc_quad(s, *reinterpret_cast<const uint4*>(mine + 32 * u), tbits, tmask, s_bhat);
+                        s = acc_quad(s, *reinterpret_cast<const uint4*>(mine + 32 * u + 16), tbits, tmask, s_bhat);
+                    }
                 }
                 if (g < kCheckpoints) ck[g * NT] = s;
             }
+        }
 
+        uint32_t topic = 0;
+        bool need = false;  // sparse branch still searching its prefix
+        uint32_t gsearch = 0;
+        float run = 0.0f, xs = 0.0f;
+        if (active) {
             if (ub < __fdiv_rn(s, __fadd_rn(s, qv))) {
                 // Sparse branch: first running prefix >= p*S (prefix_search, sampler.hpp:18-41).
-                const float xs = __fmul_rn(up, s);
+                xs = __fmul_rn(up, s);
                 if (xs == 0.0f) {
-                    topic = h.lo.y & tmask;  // every prefix is >= 0: the first real entry
+                    // every prefix is >= 0: the first real entry (staged group 0 is gone; reload)
+                    topic = __ldg(reinterpret_cast<const uint32_t*>(A4 + t.x) + 1) & tmask;
                 } else {
                     // The first group whose end-of-group sum reaches xs holds the crossing; the
                     // re-scan restarts from the previous checkpoint, the same f32 value the first
                     // pass held there, so it is bit-identical.
                     const uint32_t stored = ngroups < kCheckpoints ? ngroups : kCheckpoints;
-                    uint32_t g = 0;
-                    float run = 0.0f;
-                    while (g < stored && ck[g * NT] < xs) run = ck[g++ * NT];
-                    bool found = false;
-                    for (; g < ngroups && !found; ++g) {
-                        Sector q[kGroupSectors];
-                        const uint32_t base = g * kGroupSectors;
+                    while (gsearch < stored && ck[gsearch * NT] < xs) run = ck[gsearch++ * NT];
+                    need = true;
+                }
+            } else {
+                // Word branch: WaryTree::sample(p * total) (sampler.hpp:100-106).
+                float x = __fmul_rn(up, total);
+                if (!(x <= total)) x = total;
+                const uint32_t k = tree_search(x, s_l8, a.n_l8, l4row);
+                topic = k < a.K ? k : a.K - 1;
+            }
+        }
+        // Cooperative re-staging of the crossing group for every searching lane.
+        while (__any_sync(0xffffffffu, need)) {
+            const uint32_t first = need ? 4 * gsearch : 0u;
+            const uint32_t lim = need ? nsect : 0u;
 #pragma unroll
-                        for (uint32_t u = 0; u < kGroupSectors; ++u)
-                            q[u] = base + u < nsect ? ldg_sector(row + 2 * (base + u))
-                                                    : Sector{make_uint4(0u, 0u, 0u, 0u), make_uint4(0u, 0u, 0u, 0u)};
+            for (int j = 0; j < 4; ++j) {
+                gs[j] = __shfl_sync(0xffffffffu, first, 8 * j + grp);
+                ns[j] = __shfl_sync(0xffffffffu, lim, 8 * j + grp);
+            }
+            __syncwarp();
+            stage_group(A4, rq, ns, gs, sub, grp, stage);
+            __syncwarp();
+            if (need) {
 #pragma unroll
-                        for (uint32_t u = 0; u < kGroupSectors; ++u) {
-                            const uint32_t es[8] = {q[u].lo.x, q[u].lo.y, q[u].lo.z, q[u].lo.w,
-                                                    q[u].hi.x, q[u].hi.y, q[u].hi.z, q[u].hi.w};
+                for (uint32_t u = 0; u < 4; ++u) {
+                    if (4 * gsearch + u < nsect) {
+                        const uint4 lo = *reinterpret_cast<const uint4*>(mine + 32 * u);
+                        const uint4 hi = *reinterpret_cast<const uint4*>(mine + 32 * u + 16);
+                        const uint32_t es[8] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};
 #pragma unroll
-                            for (int w = 0; w < 8; ++w) {
-                                run = __fadd_rn(run, entry_mass(es[w], tbits, tmask, s_bhat));
-                                if (!found && run >= xs) {
-                                    topic = es[w] & tmask;
-                                    found = true;
-                                }
+                        for (int w = 0; w < 8; ++w) {
+                            run = __fadd_rn(run, entry_mass(es[w], tbits, tmask, s_bhat));
+                            if (need && run >= xs) {
+                                topic = es[w] & tmask;
+                                need = false;
                             }
                         }
                     }
                 }
-            } else {
-                // Word branch: WaryTree::sample(p * total) (sampler.hpp:100-106).
-                tree = true;
-                x = __fmul_rn(up, total);
-                if (!(x <= total)) x = total;
+                ++gsearch;
             }
-        }
-        // Cooperative descents for this round's word-branch tokens, one token at a time.
-        uint32_t pending = __ballot_sync(0xffffffffu, tree);
-        while (pending) {
-            const uint32_t src = __ffs(pending) - 1;
-            pending &= pending - 1;
-            const float xs = __shfl_sync(0xffffffffu, x, src);
-            const uint32_t k = warp_tree_search(xs, s_l2, n_l2, s_l3, l4row, lane);
-            if (lane == src) topic = k < a.K ? k : a.K - 1;
         }
         if (active) {
             a.z[t.y] = static_cast<uint16_t>(topic);
@@ -234,17 +292,17 @@ __global__ void __launch_bounds__(NT) sampler_kernel(SamplerArgs a) {
 
 cudaError_t launch_sampler(const SamplerArgs& a, uint32_t n_units, cudaStream_t s) {
     if (n_units == 0) return cudaSuccess;
-    const size_t base = sizeof(float) * (static_cast<size_t>(a.K_pad) + ((a.n_l3 + 31) & ~31u) + 64);
-    if (base + sizeof(float) * kCheckpoints * 256 <= 64 * 1024) {
-        const size_t smem = base + sizeof(float) * kCheckpoints * 256;
+    const size_t base = sizeof(float) * (static_cast<size_t>(a.K_pad) + a.l8_stride);
+    const size_t smem256 = base + (sizeof(float) * kCheckpoints + kStageRow) * 256;
+    if (smem256 <= 100 * 1024) {
         static bool configured = false;
         if (!configured) {
-            cudaFuncSetAttribute(sampler_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+            cudaFuncSetAttribute(sampler_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
             configured = true;
         }
-        sampler_kernel<256><<<n_units, 256, smem, s>>>(a);
+        sampler_kernel<256><<<n_units, 256, smem256, s>>>(a);
     } else {
-        const size_t smem = base + sizeof(float) * kCheckpoints * 512;
+        const size_t smem = base + (sizeof(float) * kCheckpoints + kStageRow) * 512;
         static bool configured = false;
         if (!configured) {
             cudaFuncSetAttribute(sampler_kernel<512>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -473,9 +531,9 @@ __global__ void __launch_bounds__(kPhiRows) phi_kernel(const uint32_t* __restric
                                                        const double* __restrict__ denom,
                                                        const float* __restrict__ zv,
                                                        float* __restrict__ bhat, float* __restrict__ l4,
-                                                       float* __restrict__ l3, float* __restrict__ q,
+                                                       float* __restrict__ l8, float* __restrict__ q,
                                                        uint32_t row_begin, uint32_t row_end, uint32_t K,
-                                                       uint32_t K_pad, uint32_t l3_stride, double beta,
+                                                       uint32_t K_pad, uint32_t l8_stride, double beta,
                                                        float falpha) {
     // t_bh aliases t_in: thread r overwrites cell [r][c] only after reading it.
     __shared__ uint32_t t_in[kPhiRows][kBlock + 1];
@@ -508,7 +566,10 @@ __global__ void __launch_bounds__(kPhiRows) phi_kernel(const uint32_t* __restric
             t_bh[r][c] = bh;
             t_l4[r][c] = run;
         }
-        if (v < row_end) l3[static_cast<size_t>(v) * l3_stride + c0 / kBlock] = run;
+        if (v < row_end) {  // L8: the prefix at every 8th column of this tile
+            const float4 l8v = make_float4(t_l4[r][7], t_l4[r][15], t_l4[r][23], t_l4[r][31]);
+            *reinterpret_cast<float4*>(l8 + static_cast<size_t>(v) * l8_stride + c0 / kLeaf) = l8v;
+        }
         __syncthreads();
 #pragma unroll 8
         for (uint32_t it = 0; it < kBlock; ++it) {
@@ -524,19 +585,19 @@ __global__ void __launch_bounds__(kPhiRows) phi_kernel(const uint32_t* __restric
         __syncthreads();  // the next tile load overwrites t_in (== t_bh)
     }
     if (v < row_end) {
-        for (uint32_t j = K_pad / kBlock; j < l3_stride; ++j) l3[static_cast<size_t>(v) * l3_stride + j] = run;
+        for (uint32_t j = K_pad / kLeaf; j < l8_stride; ++j) l8[static_cast<size_t>(v) * l8_stride + j] = run;
         q[v] = __fmul_rn(falpha, run);  // trainer.cpp:245
     }
 }
 
 cudaError_t launch_phi(const uint32_t* B, const double* denom, const float* zv, float* bhat,
-                       float* l4, float* l3, float* q, uint32_t row_begin, uint32_t row_end,
-                       uint32_t K, uint32_t K_pad, uint32_t l3_stride, double beta, float falpha,
+                       float* l4, float* l8, float* q, uint32_t row_begin, uint32_t row_end,
+                       uint32_t K, uint32_t K_pad, uint32_t l8_stride, double beta, float falpha,
                        cudaStream_t s) {
     if (row_end <= row_begin) return cudaSuccess;
     const uint32_t blocks = (row_end - row_begin + kPhiRows - 1) / kPhiRows;
-    phi_kernel<<<blocks, kPhiRows, 0, s>>>(B, denom, zv, bhat, l4, l3, q, row_begin, row_end, K, K_pad,
-                                           l3_stride, beta, falpha);
+    phi_kernel<<<blocks, kPhiRows, 0, s>>>(B, denom, zv, bhat, l4, l8, q, row_begin, row_end, K, K_pad,
+                                           l8_stride, beta, falpha);
     return cudaGetLastError();
 }
 

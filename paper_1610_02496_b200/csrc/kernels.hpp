@@ -21,14 +21,14 @@ struct SamplerArgs {
     const uint32_t* A;      // C_dk rows: [nnz-1 | entries topic | count << tbits | zero pad to 8]
     const float* bhat;      // V_pad x K_pad
     const float* l4;        // V_pad x K_pad (inclusive prefix, padded with the total)
-    const float* l3;        // V_pad x l3_stride (L4 block maxima)
+    const float* l8;        // V_pad x l8_stride (L4 block maxima)
     const float* q;         // V_pad
     const uint64_t* ids;    // RNG element id per slot, or null -> id_base + slot
     uint16_t* z;            // new topic per slot
     uint32_t* B;            // V_pad x K_pad, zeroed by the caller
     uint64_t seed, id_base;
     uint32_t stream_kind;   // iteration number (trainer.cpp:423)
-    uint32_t K, K_pad, l3_stride, n_l3, tbits;
+    uint32_t K, K_pad, l8_stride, n_l8, tbits;
     unsigned long long* row_entries;  // optional: sum of nnz over tokens (roofline)
 };
 
@@ -54,8 +54,8 @@ cudaError_t launch_colsum(const uint32_t* B, uint32_t row_begin, uint32_t row_en
 cudaError_t launch_denom(const unsigned long long* colsum, uint32_t K, uint32_t K_pad, uint32_t V,
                          double beta, double* denom, float* zv, cudaStream_t s);
 cudaError_t launch_phi(const uint32_t* B, const double* denom, const float* zv, float* bhat,
-                       float* l4, float* l3, float* q, uint32_t row_begin, uint32_t row_end,
-                       uint32_t K, uint32_t K_pad, uint32_t l3_stride, double beta, float falpha,
+                       float* l4, float* l8, float* q, uint32_t row_begin, uint32_t row_end,
+                       uint32_t K, uint32_t K_pad, uint32_t l8_stride, double beta, float falpha,
                        cudaStream_t s);
 
 // Setup kernels.
