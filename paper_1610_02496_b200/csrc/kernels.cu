@@ -14,23 +14,16 @@ inline uint32_t grid_for(uint64_t n, uint32_t threads, uint32_t cap = 148u * 32u
     return static_cast<uint32_t>(g == 0 ? 1 : (g > cap ? cap : g));
 }
 
-__device__ __forceinline__ uint4 ldg_nc_v4(const uint4* p) {
-    uint4 r;
-    asm volatile("ld.global.nc.v4.u32 {%0,%1,%2,%3}, [%4];"
-                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
-                 : "l"(p));
-    return r;
-}
-
 }  // namespace
 
 // ============================================================================
 // K3 sampler -- process_segment (trainer.cpp:265-291) + sample_token<float>
 // (sampler.hpp:166-204) + the C_wk accumulation of accumulate_word_topic
 // (counts.cpp:127-132).  One CTA per heavy-first work unit of one word; the
-// word's phi row and its L3 block maxima are staged in shared memory; each
-// thread samples whole tokens (lane-per-token) so that the sparse mass S and
-// the in-place prefix run as the reference's sequential f32 chains.
+// word's phi row and its L8 level are staged in shared memory; each warp stages
+// its 32 tokens' C_dk rows cooperatively (coalesced), and each lane samples one
+// token so that the sparse mass S and the in-place prefix run as the reference's
+// sequential f32 chains.
 // ============================================================================
 
 __device__ __forceinline__ float entry_mass(uint32_t e, uint32_t tbits, uint32_t tmask,
@@ -60,31 +53,7 @@ __device__ __forceinline__ Sector ldg_sector(const uint4* p) {
     return s;
 }
 
-// Rows are consumed in groups of 4 sectors (32 entries).  The group's loads are issued
-// by one PTX block so all four are in flight together (ptxas otherwise serialises them
-// behind the consuming arithmetic to save registers).  Sectors i >= n are not loaded
-// and keep their (zero) input values, which add +0 like the row padding.
-constexpr uint32_t kGroupSectors = 4;
-#define SLDA_R8(s) "+r"(s.lo.x), "+r"(s.lo.y), "+r"(s.lo.z), "+r"(s.lo.w), "+r"(s.hi.x), "+r"(s.hi.y), \
-                   "+r"(s.hi.z), "+r"(s.hi.w)
-__device__ __forceinline__ void ldg_sectors4(const uint4* p, uint32_t n, Sector& a, Sector& b, Sector& c,
-                                             Sector& d) {
-    asm("{\n\t.reg .pred p0, p1, p2, p3;\n\t"
-        "setp.gt.u32 p0, %33, 0;\n\t"
-        "setp.gt.u32 p1, %33, 1;\n\t"
-        "setp.gt.u32 p2, %33, 2;\n\t"
-        "setp.gt.u32 p3, %33, 3;\n\t"
-        "@p0 ld.global.nc.L1::no_allocate.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%32];\n\t"
-        "@p1 ld.global.nc.L1::no_allocate.v8.u32 {%8,%9,%10,%11,%12,%13,%14,%15}, [%32+32];\n\t"
-        "@p2 ld.global.nc.L1::no_allocate.v8.u32 {%16,%17,%18,%19,%20,%21,%22,%23}, [%32+64];\n\t"
-        "@p3 ld.global.nc.L1::no_allocate.v8.u32 {%24,%25,%26,%27,%28,%29,%30,%31}, [%32+96];\n\t}"
-        : SLDA_R8(a), SLDA_R8(b), SLDA_R8(c), SLDA_R8(d)
-        : "l"(p), "r"(n));
-}
 __device__ __forceinline__ Sector zero_sector() { return Sector{make_uint4(0u, 0u, 0u, 0u), make_uint4(0u, 0u, 0u, 0u)}; }
-// Running sums at the end of the first kCheckpoints groups, so the prefix pass of the
-// sparse branch re-reads one group instead of the row.
-constexpr uint32_t kCheckpoints = 8;
 
 // lower_bound over the word's L4 prefix (== WaryTree::sample, acceptance.cpp:140-200):
 // binary search of the staged L8 level (first 8-block whose last prefix >= x), then one
@@ -103,42 +72,57 @@ __device__ __forceinline__ uint32_t tree_search(float x, const float* s_l8, uint
     return lo * kLeaf + below;
 }
 
-// Per-warp staging of C_dk rows: 32 rows x 4 sectors (128 B), 144-byte row stride so both
-// the cooperative stores and each lane's 128-bit reads of its own row are conflict-free.
-// Lane-private random row reads cap at ~1.5 TB/s on B200 (L1TEX: one line per lane per
-// load); the warp-cooperative layout (lane -> row 8j + lane/4, sector lane%4) is coalesced
-// per row and measured at 3.7-6 TB/s (scripts/microbench_rows.cu).
-constexpr uint32_t kStageRow = 144;
+// Per-warp staging of C_dk rows.  Lane-private random row reads cap at ~1.5 TB/s on B200
+// (L1TEX: one line per lane per load); the warp-cooperative layout (adjacent lanes read
+// adjacent sectors of one row) is coalesced per row and measured at 3.7-6 TB/s
+// (scripts/microbench_rows.cu).  A group is kGroup sectors (16 entries) of each
+// of the warp's 32 rows; the 80-byte row stride keeps the cooperative stores and each
+// lane's 128-bit reads of its own row bank-conflict free.
+constexpr uint32_t kGroup = 2;
+constexpr uint32_t kRowsPerInst = 32 / kGroup;
+constexpr uint32_t kStageRow = 32 * kGroup + 16;
 constexpr uint32_t kStageWarp = 32 * kStageRow;
+// Per-sector running sums for the first kCkSectors sectors (96 entries): the prefix pass
+// of the sparse branch re-reads one sector instead of the row.  (12: at K = 10K two
+// 512-thread CTAs fit one SM.)
+constexpr uint32_t kCkSectors = 12;
 
 __device__ __forceinline__ void sts_sector(unsigned char* p, const Sector& q) {
     *reinterpret_cast<uint4*>(p) = q.lo;
     *reinterpret_cast<uint4*>(p + 16) = q.hi;
 }
 
-// Cooperative load of one 4-sector group of each of the warp's 32 rows into the stage.
-// rq[j] / ns[j]: quad offset and sector count of row 8j + lane/4 (ns = 0: skip the row);
-// gs[j]: first sector of the group for that row.
-__device__ __forceinline__ void stage_group(const uint4* A4, const uint32_t (&rq)[4], const uint32_t (&ns)[4],
-                                            const uint32_t (&gs)[4], uint32_t sub, uint32_t grp,
-                                            unsigned char* stage) {
-    Sector q[4];
+// Cooperative load of sectors [gs, gs + kGroup) of each of the warp's 32 rows (registers),
+// and its store into the stage.  Per row 16j + grp: rq = quad offset, ns = sector limit
+// (0: skip), gs = first sector.
+__device__ __forceinline__ void load_group(const uint4* A4, const uint32_t (&rq)[kGroup], const uint32_t (&ns)[kGroup],
+                                           const uint32_t (&gs)[kGroup], uint32_t sub, Sector (&q)[kGroup]) {
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
+    for (uint32_t j = 0; j < kGroup; ++j) {
         const uint32_t sec = gs[j] + sub;
         q[j] = sec < ns[j] ? ldg_sector(A4 + rq[j] + 2 * sec) : zero_sector();
     }
+}
+__device__ __forceinline__ void store_group(const Sector (&q)[kGroup], uint32_t sub, uint32_t grp,
+                                            unsigned char* stage) {
 #pragma unroll
-    for (int j = 0; j < 4; ++j) sts_sector(stage + (8 * j + grp) * kStageRow + sub * 32, q[j]);
+    for (uint32_t j = 0; j < kGroup; ++j) sts_sector(stage + (kRowsPerInst * j + grp) * kStageRow + sub * 32, q[j]);
+}
+__device__ __forceinline__ void stage_group(const uint4* A4, const uint32_t (&rq)[kGroup],
+                                            const uint32_t (&ns)[kGroup], const uint32_t (&gs)[kGroup],
+                                            uint32_t sub, uint32_t grp, unsigned char* stage) {
+    Sector q[kGroup];
+    load_group(A4, rq, ns, gs, sub, q);
+    store_group(q, sub, grp, stage);
 }
 
 template <int NT>
-__global__ void __launch_bounds__(NT) sampler_kernel(SamplerArgs a) {
+__global__ void __launch_bounds__(NT, 65536 / (NT * 64)) sampler_kernel(SamplerArgs a) {
     extern __shared__ __align__(16) float sm[];
     float* s_bhat = sm;
     float* s_l8 = sm + a.K_pad;             // l8_stride (L4[8j+7], padded with the total)
-    float* s_ck = s_l8 + a.l8_stride;       // [kCheckpoints][NT]
-    unsigned char* s_stage = reinterpret_cast<unsigned char*>(s_ck + kCheckpoints * NT);
+    float* s_ck = s_l8 + a.l8_stride;       // [kCkSectors][NT]
+    unsigned char* s_stage = reinterpret_cast<unsigned char*>(s_ck + kCkSectors * NT);
 
     const Unit unit = a.units[blockIdx.x];
     const uint32_t v = unit.word;
@@ -158,9 +142,12 @@ __global__ void __launch_bounds__(NT) sampler_kernel(SamplerArgs a) {
     const uint32_t tmask = (1u << tbits) - 1u;
     const uint4* A4 = reinterpret_cast<const uint4*>(a.A);
     float* ck = s_ck + threadIdx.x;
-    const uint32_t lane = lane_id(), sub = lane & 3u, grp = lane >> 2;
+    // Cooperative layout: lane -> row kRowsPerInst*j + lane%16, sector lane/16.  A quarter
+    // warp then stores 8 different rows at the same sector offset, which the 80-byte row
+    // stride spreads over all 32 banks; the row's two sectors stay one 64-byte segment.
+    const uint32_t lane = lane_id(), sub = lane / kRowsPerInst, grp = lane % kRowsPerInst;
     unsigned char* stage = s_stage + (threadIdx.x >> 5) * kStageWarp;
-    const unsigned char* mine = stage + lane * kStageRow;  // this lane's staged row group
+    const unsigned char* mine = stage + lane * kStageRow;  // this lane's staged sectors
     unsigned long long entries = 0;
     __syncthreads();
 
@@ -169,11 +156,11 @@ __global__ void __launch_bounds__(NT) sampler_kernel(SamplerArgs a) {
         const uint32_t i = r * NT + threadIdx.x;
         const bool active = i < unit.length;
         const uint2 t = active ? __ldg(a.tok + unit.offset + i) : make_uint2(0u, 0u);  // {row quads, slot}
-        uint32_t rq[4], ns[4], gs[4];
+        uint32_t rq[kGroup], ns[kGroup], gs[kGroup];
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            rq[j] = __shfl_sync(0xffffffffu, t.x, 8 * j + grp);
-            ns[j] = __shfl_sync(0xffffffffu, active ? 4u : 0u, 8 * j + grp);  // group 0: speculative
+        for (uint32_t j = 0; j < kGroup; ++j) {
+            rq[j] = __shfl_sync(0xffffffffu, t.x, kRowsPerInst * j + grp);
+            ns[j] = __shfl_sync(0xffffffffu, active ? kGroup : 0u, kRowsPerInst * j + grp);  // speculative
             gs[j] = 0;
         }
         __syncwarp();
@@ -184,11 +171,11 @@ __global__ void __launch_bounds__(NT) sampler_kernel(SamplerArgs a) {
         // header entry (nnz-1, count 0) and the padding add +0 to every running sum.
         const uint32_t nnz = active ? (reinterpret_cast<const uint4*>(mine)->x & tmask) + 1u : 0u;
         const uint32_t nsect = active ? (nnz + 8u) >> 3 : 0u;
-        const uint32_t ngroups = (nsect + 3u) >> 2;
+        const uint32_t ngroups = (nsect + kGroup - 1) / kGroup;
         entries += nnz;
         const uint32_t max_groups = __reduce_max_sync(0xffffffffu, ngroups);
 #pragma unroll
-        for (int j = 0; j < 4; ++j) ns[j] = __shfl_sync(0xffffffffu, nsect, 8 * j + grp);
+        for (uint32_t j = 0; j < kGroup; ++j) ns[j] = __shfl_sync(0xffffffffu, nsect, kRowsPerInst * j + grp);
 
         float ub = 0.0f, up = 0.0f;
         if (active) {
@@ -196,46 +183,56 @@ __global__ void __launch_bounds__(NT) sampler_kernel(SamplerArgs a) {
             draw2_f32(a.seed, a.stream_kind, id, ub, up);
         }
 
-        // make_branch_context: S = sum_i f32(cnt_i) * bhat[top_i], sequential f32, one
-        // staged group (32 entries) at a time.
+        // make_branch_context: S = sum_i f32(cnt_i) * bhat[top_i], sequential f32.
+        // Group g+1 is loaded into registers while group g is consumed from the stage.
         float s = 0.0f;
         for (uint32_t g = 0; g < max_groups; ++g) {
-            if (g > 0) {
-                __syncwarp();
+            Sector next[kGroup];
+            const bool more = g + 1 < max_groups;
+            if (more) {
 #pragma unroll
-                for (int j = 0; j < 4; ++j) gs[j] = 4 * g;
-                stage_group(A4, rq, ns, gs, sub, grp, stage);
-                __syncwarp();
+                for (uint32_t j = 0; j < kGroup; ++j) gs[j] = kGroup * (g + 1);
+                load_group(A4, rq, ns, gs, sub, next);
             }
-            if (g < ngroups) {
 #pragma unroll
-                for (uint32_t u = 0; u < 4; ++u) {
-                    if (4 * g + u < nsect) {
-                        s = acc_quad(s, *reinterpret_cast<const uint4*>(mine + 32 * u), tbits, tmask, s_bhat);
-                        s = acc_quad(s, *reinterpret_cast<const uint4*>(mine + 32 * u + 16), tbits, tmask, s_bhat);
-                    }
+            for (uint32_t u = 0; u < kGroup; ++u) {
+                const uint32_t sec = kGroup * g + u;
+                if (sec < nsect) {
+                    s = acc_quad(s, *reinterpret_cast<const uint4*>(mine + 32 * u), tbits, tmask, s_bhat);
+                    s = acc_quad(s, *reinterpret_cast<const uint4*>(mine + 32 * u + 16), tbits, tmask, s_bhat);
+                    if (sec < kCkSectors) ck[sec * NT] = s;
                 }
-                if (g < kCheckpoints) ck[g * NT] = s;
+            }
+            if (more) {
+                __syncwarp();
+                store_group(next, sub, grp, stage);
+                __syncwarp();
             }
         }
 
         uint32_t topic = 0;
         bool need = false;  // sparse branch still searching its prefix
-        uint32_t gsearch = 0;
+        uint32_t sec = 0;
         float run = 0.0f, xs = 0.0f;
         if (active) {
             if (ub < __fdiv_rn(s, __fadd_rn(s, qv))) {
                 // Sparse branch: first running prefix >= p*S (prefix_search, sampler.hpp:18-41).
                 xs = __fmul_rn(up, s);
                 if (xs == 0.0f) {
-                    // every prefix is >= 0: the first real entry (staged group 0 is gone; reload)
+                    // every prefix is >= 0: the first real entry
                     topic = __ldg(reinterpret_cast<const uint32_t*>(A4 + t.x) + 1) & tmask;
                 } else {
-                    // The first group whose end-of-group sum reaches xs holds the crossing; the
-                    // re-scan restarts from the previous checkpoint, the same f32 value the first
-                    // pass held there, so it is bit-identical.
-                    const uint32_t stored = ngroups < kCheckpoints ? ngroups : kCheckpoints;
-                    while (gsearch < stored && ck[gsearch * NT] < xs) run = ck[gsearch++ * NT];
+                    // The first sector whose end sum reaches xs holds the crossing; its re-scan
+                    // restarts from the previous checkpoint, the same f32 value the first pass
+                    // held there, so it is bit-identical.
+                    const uint32_t stored = nsect < kCkSectors ? nsect : kCkSectors;
+                    uint32_t lo = 0, hi = stored;  // first checkpoint >= xs (or stored)
+                    while (lo < hi) {
+                        const uint32_t mid = (lo + hi) >> 1;
+                        if (ck[mid * NT] >= xs) hi = mid; else lo = mid + 1;
+                    }
+                    sec = lo;
+                    run = lo > 0 ? ck[(lo - 1) * NT] : 0.0f;
                     need = true;
                 }
             } else {
@@ -246,36 +243,31 @@ __global__ void __launch_bounds__(NT) sampler_kernel(SamplerArgs a) {
                 topic = k < a.K ? k : a.K - 1;
             }
         }
-        // Cooperative re-staging of the crossing group for every searching lane.
+        // Cooperative re-staging of the crossing sector of every searching lane.
         while (__any_sync(0xffffffffu, need)) {
-            const uint32_t first = need ? 4 * gsearch : 0u;
-            const uint32_t lim = need ? nsect : 0u;
+            const uint32_t first = need ? sec : 0u;
+            const uint32_t lim = need ? sec + 1 : 0u;
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                gs[j] = __shfl_sync(0xffffffffu, first, 8 * j + grp);
-                ns[j] = __shfl_sync(0xffffffffu, lim, 8 * j + grp);
+            for (uint32_t j = 0; j < kGroup; ++j) {
+                gs[j] = __shfl_sync(0xffffffffu, first, kRowsPerInst * j + grp);
+                ns[j] = __shfl_sync(0xffffffffu, lim, kRowsPerInst * j + grp);
             }
             __syncwarp();
             stage_group(A4, rq, ns, gs, sub, grp, stage);
             __syncwarp();
             if (need) {
+                const uint4 lo = *reinterpret_cast<const uint4*>(mine);
+                const uint4 hi = *reinterpret_cast<const uint4*>(mine + 16);
+                const uint32_t es[8] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};
 #pragma unroll
-                for (uint32_t u = 0; u < 4; ++u) {
-                    if (4 * gsearch + u < nsect) {
-                        const uint4 lo = *reinterpret_cast<const uint4*>(mine + 32 * u);
-                        const uint4 hi = *reinterpret_cast<const uint4*>(mine + 32 * u + 16);
-                        const uint32_t es[8] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};
-#pragma unroll
-                        for (int w = 0; w < 8; ++w) {
-                            run = __fadd_rn(run, entry_mass(es[w], tbits, tmask, s_bhat));
-                            if (need && run >= xs) {
-                                topic = es[w] & tmask;
-                                need = false;
-                            }
-                        }
+                for (int w = 0; w < 8; ++w) {
+                    run = __fadd_rn(run, entry_mass(es[w], tbits, tmask, s_bhat));
+                    if (need && run >= xs) {
+                        topic = es[w] & tmask;
+                        need = false;
                     }
                 }
-                ++gsearch;
+                ++sec;
             }
         }
         if (active) {
@@ -290,23 +282,28 @@ __global__ void __launch_bounds__(NT) sampler_kernel(SamplerArgs a) {
     }
 }
 
+size_t sampler_smem(const SamplerArgs& a, int nt) {
+    return sizeof(float) * (static_cast<size_t>(a.K_pad) + a.l8_stride) +
+           (sizeof(float) * kCkSectors + kStageRow) * static_cast<size_t>(nt);
+}
+
 cudaError_t launch_sampler(const SamplerArgs& a, uint32_t n_units, cudaStream_t s) {
     if (n_units == 0) return cudaSuccess;
-    const size_t base = sizeof(float) * (static_cast<size_t>(a.K_pad) + a.l8_stride);
-    const size_t smem256 = base + (sizeof(float) * kCheckpoints + kStageRow) * 256;
-    if (smem256 <= 100 * 1024) {
+    // 512 threads share one staged phi row when it is large (K = 10K: 2 CTAs x 16 warps).
+    const bool wide = sizeof(float) * (static_cast<size_t>(a.K_pad) + a.l8_stride) > 24 * 1024;
+    if (!wide) {
         static bool configured = false;
         if (!configured) {
-            cudaFuncSetAttribute(sampler_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+            cudaFuncSetAttribute(sampler_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
             configured = true;
         }
-        sampler_kernel<256><<<n_units, 256, smem256, s>>>(a);
+        sampler_kernel<256><<<n_units, 256, sampler_smem(a, 256), s>>>(a);
     } else {
-        const size_t smem = base + (sizeof(float) * kCheckpoints + kStageRow) * 512;
+        const size_t smem = sampler_smem(a, 512);
+        if (smem > 227 * 1024) return cudaErrorInvalidConfiguration;  // K too large to stage phi
         static bool configured = false;
         if (!configured) {
-            cudaFuncSetAttribute(sampler_kernel<512>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 227 * 1024);
+            cudaFuncSetAttribute(sampler_kernel<512>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
             configured = true;
         }
         sampler_kernel<512><<<n_units, 512, smem, s>>>(a);
@@ -324,11 +321,94 @@ cudaError_t launch_sampler(const SamplerArgs& a, uint32_t n_units, cudaStream_t 
 
 constexpr int kSscWarps = 8;
 
+// Ascending bitonic sort of N = 32*R keys held striped across the warp (key i in lane
+// i % 32, register i / 32): cross-lane stages exchange through shuffles, in-lane stages
+// swap registers.  Integer keys, so any correct sort is bit-identical to std::sort.
+template <int R>
+__device__ __forceinline__ void warp_bitonic(uint32_t (&key)[R], uint32_t lane) {
+#pragma unroll
+    for (uint32_t k = 2; k <= 32u * R; k <<= 1) {
+#pragma unroll
+        for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+            if (j >= 32) {
+                const uint32_t rj = j >> 5;
+#pragma unroll
+                for (uint32_t r = 0; r < R; ++r) {
+                    if ((r & rj) == 0) {
+                        const uint32_t i = r * 32 + lane;
+                        const bool up = (i & k) == 0;
+                        const uint32_t a = key[r], b = key[r | rj];
+                        const uint32_t lo = min(a, b), hi = max(a, b);
+                        key[r] = up ? lo : hi;
+                        key[r | rj] = up ? hi : lo;
+                    }
+                }
+            } else {
+                const bool lower = (lane & j) == 0;
+#pragma unroll
+                for (uint32_t r = 0; r < R; ++r) {
+                    const uint32_t i = r * 32 + lane;
+                    const bool up = (i & k) == 0;
+                    const uint32_t other = __shfl_xor_sync(0xffffffffu, key[r], j);
+                    key[r] = (up == lower) ? min(key[r], other) : max(key[r], other);
+                }
+            }
+        }
+    }
+}
+
+// One document of n <= 32*R tokens: sort, run-length, write the C_dk row (header, entries,
+// zero padding to 8).  starts: per-warp scratch of >= n words.  Returns nnz.
+template <int R>
+__device__ __forceinline__ uint32_t ssc_doc(const uint16_t* z, uint32_t n, uint32_t lane, uint32_t* starts,
+                                            uint32_t* out_row, uint32_t tbits) {
+    uint32_t key[R];
+#pragma unroll
+    for (uint32_t r = 0; r < R; ++r) {
+        const uint32_t i = r * 32 + lane;
+        key[r] = i < n ? static_cast<uint32_t>(z[i]) : 0xFFFFFFFFu;
+    }
+    warp_bitonic<R>(key, lane);
+    // Run starts in sorted order (i == r*32 + lane).
+    uint32_t nnz = 0;
+#pragma unroll
+    for (uint32_t r = 0; r < R; ++r) {
+        const uint32_t i = r * 32 + lane;
+        const uint32_t up1 = __shfl_up_sync(0xffffffffu, key[r], 1);
+        const uint32_t last = __shfl_sync(0xffffffffu, key[r > 0 ? r - 1 : 0], 31);
+        const uint32_t prev = lane != 0 ? up1 : (r == 0 ? 0xFFFFFFFEu : last);
+        const bool start = i < n && (i == 0 || key[r] != prev);
+        const uint32_t ballot = __ballot_sync(0xffffffffu, start);
+        if (start) starts[nnz + __popc(ballot & ((1u << lane) - 1u))] = i;
+        nnz += __popc(ballot);
+        if (32u * (r + 1) >= n) break;
+    }
+    __syncwarp();
+    // Entries: topic of the run's first key, count = distance to the next start.  The sorted
+    // keys are gone from smem, so the topic is recovered from the start position's lane.
+    for (uint32_t base = 0; base < nnz; base += 32) {
+        const uint32_t e = base + lane;
+        const uint32_t st = e < nnz ? starts[e] : 0u;
+        const uint32_t en = e + 1 < nnz ? starts[e + 1] : n;
+        // key at sorted position st lives in lane st % 32, register st / 32.
+        uint32_t topic = 0;
+#pragma unroll
+        for (uint32_t r = 0; r < R; ++r) {
+            const uint32_t kv = __shfl_sync(0xffffffffu, key[r], st & 31u);
+            if ((st >> 5) == r) topic = kv;
+        }
+        if (e < nnz) out_row[1 + e] = topic | ((en - st) << tbits);
+    }
+    const uint32_t padded = (nnz + 8u) & ~7u;
+    for (uint32_t e = nnz + 1 + lane; e < padded; e += 32) out_row[e] = 0u;
+    if (lane == 0) out_row[0] = nnz - 1u;
+    __syncwarp();
+    return nnz;
+}
+
 __global__ void __launch_bounds__(kSscWarps * 32) ssc_warp_kernel(SscArgs a) {
-    __shared__ uint32_t s_keys[kSscWarps][kSscWarpCap];
     __shared__ uint32_t s_start[kSscWarps][kSscWarpCap];
     const uint32_t w = threadIdx.x >> 5, lane = lane_id();
-    uint32_t* keys = s_keys[w];
     uint32_t* starts = s_start[w];
     unsigned long long nnz_acc = 0;
     const uint32_t gw = blockIdx.x * kSscWarps + w, nw = gridDim.x * kSscWarps;
@@ -336,49 +416,15 @@ __global__ void __launch_bounds__(kSscWarps * 32) ssc_warp_kernel(SscArgs a) {
         const uint32_t s0 = __ldg(a.doc_start + d);
         const uint32_t n = __ldg(a.doc_start + d + 1) - s0;
         if (n > kSscWarpCap || n == 0) continue;  // ssc_long_kernel / empty document
-        const uint32_t row = __ldg(a.row4 + d) * 4u;
-        uint32_t N = 1;
-        while (N < n) N <<= 1;
-        for (uint32_t i = lane; i < N; i += 32) keys[i] = i < n ? a.z[s0 + i] : 0xFFFFFFFFu;
-        __syncwarp();
-        for (uint32_t k = 2; k <= N; k <<= 1) {
-            for (uint32_t j = k >> 1; j > 0; j >>= 1) {
-                for (uint32_t i = lane; i < N; i += 32) {
-                    const uint32_t ixj = i ^ j;
-                    if (ixj > i) {
-                        const uint32_t x = keys[i], y = keys[ixj];
-                        const bool up = (i & k) == 0;
-                        if ((x > y) == up) {
-                            keys[i] = y;
-                            keys[ixj] = x;
-                        }
-                    }
-                }
-                __syncwarp();
-            }
-        }
-        uint32_t nnz = 0;
-        for (uint32_t base = 0; base < n; base += 32) {
-            const uint32_t i = base + lane;
-            const bool start = i < n && (i == 0 || keys[i] != keys[i - 1]);
-            const uint32_t ballot = __ballot_sync(0xffffffffu, start);
-            if (start) starts[nnz + __popc(ballot & ((1u << lane) - 1u))] = i;
-            nnz += __popc(ballot);
-        }
-        __syncwarp();
-        // Row: header (nnz-1, count 0), entries, zero-count padding to a multiple of 8.
-        for (uint32_t r = lane; r < nnz; r += 32) {
-            const uint32_t st = starts[r];
-            const uint32_t en = r + 1 < nnz ? starts[r + 1] : n;
-            a.A[row + 1 + r] = keys[st] | ((en - st) << a.tbits);
-        }
-        const uint32_t padded = (nnz + 8u) & ~7u;
-        for (uint32_t r = nnz + 1 + lane; r < padded; r += 32) a.A[row + r] = 0u;
-        if (lane == 0) {
-            a.A[row] = nnz - 1u;
-            nnz_acc += nnz;
-        }
-        __syncwarp();
+        uint32_t* row = a.A + __ldg(a.row4 + d) * 4u;
+        const uint16_t* z = a.z + s0;
+        uint32_t nnz;
+        if (n <= 32) nnz = ssc_doc<1>(z, n, lane, starts, row, a.tbits);
+        else if (n <= 64) nnz = ssc_doc<2>(z, n, lane, starts, row, a.tbits);
+        else if (n <= 128) nnz = ssc_doc<4>(z, n, lane, starts, row, a.tbits);
+        else if (n <= 256) nnz = ssc_doc<8>(z, n, lane, starts, row, a.tbits);
+        else nnz = ssc_doc<16>(z, n, lane, starts, row, a.tbits);
+        nnz_acc += nnz;
     }
     if (lane == 0 && nnz_acc) atomicAdd(a.nnz_total, nnz_acc);
 }
@@ -525,35 +571,50 @@ cudaError_t launch_denom(const unsigned long long* colsum, uint32_t K, uint32_t 
     return cudaGetLastError();
 }
 
+// One thread per word row (the L4 prefix is a sequential f32 chain); 32-column tiles are
+// moved through shared memory for coalescing, and tile c+1 is loaded into registers while
+// tile c is computed.
 constexpr int kPhiRows = 128;
+constexpr int kPhiCols = 32;
+constexpr int kPhiLoads = kPhiRows * kPhiCols / kPhiRows;  // per thread per tile
 
-__global__ void __launch_bounds__(kPhiRows) phi_kernel(const uint32_t* __restrict__ B,
-                                                       const double* __restrict__ denom,
-                                                       const float* __restrict__ zv,
-                                                       float* __restrict__ bhat, float* __restrict__ l4,
-                                                       float* __restrict__ l8, float* __restrict__ q,
-                                                       uint32_t row_begin, uint32_t row_end, uint32_t K,
-                                                       uint32_t K_pad, uint32_t l8_stride, double beta,
-                                                       float falpha) {
+__global__ void __launch_bounds__(kPhiRows, 4) phi_kernel(const uint32_t* __restrict__ B,
+                                                        const double* __restrict__ denom,
+                                                        const float* __restrict__ zv,
+                                                        float* __restrict__ bhat, float* __restrict__ l4,
+                                                        float* __restrict__ l8, float* __restrict__ q,
+                                                        uint32_t row_begin, uint32_t row_end, uint32_t K,
+                                                        uint32_t K_pad, uint32_t l8_stride, double beta,
+                                                        float falpha) {
     // t_bh aliases t_in: thread r overwrites cell [r][c] only after reading it.
-    __shared__ uint32_t t_in[kPhiRows][kBlock + 1];
-    __shared__ float t_l4[kPhiRows][kBlock + 1];
-    float(*t_bh)[kBlock + 1] = reinterpret_cast<float(*)[kBlock + 1]>(t_in);
+    __shared__ uint32_t t_in[kPhiRows][kPhiCols + 1];
+    __shared__ float t_l4[kPhiRows][kPhiCols + 1];
+    float(*t_bh)[kPhiCols + 1] = reinterpret_cast<float(*)[kPhiCols + 1]>(t_in);
     const uint32_t r = threadIdx.x;
     const uint32_t v0 = row_begin + blockIdx.x * kPhiRows;
     const uint32_t v = v0 + r;
     float run = 0.0f;
-    for (uint32_t c0 = 0; c0 < K_pad; c0 += kBlock) {
-#pragma unroll 8
-        for (uint32_t it = 0; it < kBlock; ++it) {
+    uint32_t next[kPhiLoads];
+    auto load_tile = [&](uint32_t c0) {
+#pragma unroll
+        for (int it = 0; it < kPhiLoads; ++it) {
             const uint32_t idx = it * kPhiRows + r;
-            const uint32_t rr = idx >> 5, cc = idx & 31u;
+            const uint32_t rr = idx / kPhiCols, cc = idx % kPhiCols;
             const uint32_t vv = v0 + rr;
-            t_in[rr][cc] = vv < row_end ? __ldg(B + static_cast<size_t>(vv) * K_pad + c0 + cc) : 0u;
+            next[it] = vv < row_end ? __ldg(B + static_cast<size_t>(vv) * K_pad + c0 + cc) : 0u;
+        }
+    };
+    load_tile(0);
+    for (uint32_t c0 = 0; c0 < K_pad; c0 += kPhiCols) {
+#pragma unroll
+        for (int it = 0; it < kPhiLoads; ++it) {
+            const uint32_t idx = it * kPhiRows + r;
+            t_in[idx / kPhiCols][idx % kPhiCols] = next[it];
         }
         __syncthreads();
+        if (c0 + kPhiCols < K_pad) load_tile(c0 + kPhiCols);
 #pragma unroll 4
-        for (uint32_t c = 0; c < kBlock; ++c) {
+        for (uint32_t c = 0; c < kPhiCols; ++c) {
             const uint32_t k = c0 + c;
             float bh = 0.0f;
             if (k < K) {
@@ -571,10 +632,10 @@ __global__ void __launch_bounds__(kPhiRows) phi_kernel(const uint32_t* __restric
             *reinterpret_cast<float4*>(l8 + static_cast<size_t>(v) * l8_stride + c0 / kLeaf) = l8v;
         }
         __syncthreads();
-#pragma unroll 8
-        for (uint32_t it = 0; it < kBlock; ++it) {
+#pragma unroll
+        for (int it = 0; it < kPhiLoads; ++it) {
             const uint32_t idx = it * kPhiRows + r;
-            const uint32_t rr = idx >> 5, cc = idx & 31u;
+            const uint32_t rr = idx / kPhiCols, cc = idx % kPhiCols;
             const uint32_t vv = v0 + rr;
             if (vv < row_end) {
                 const size_t o = static_cast<size_t>(vv) * K_pad + c0 + cc;
@@ -582,7 +643,7 @@ __global__ void __launch_bounds__(kPhiRows) phi_kernel(const uint32_t* __restric
                 l4[o] = t_l4[rr][cc];
             }
         }
-        __syncthreads();  // the next tile load overwrites t_in (== t_bh)
+        __syncthreads();  // the next tile store overwrites t_in (== t_bh)
     }
     if (v < row_end) {
         for (uint32_t j = K_pad / kLeaf; j < l8_stride; ++j) l8[static_cast<size_t>(v) * l8_stride + j] = run;
