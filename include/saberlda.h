@@ -184,6 +184,11 @@ int slda_nccl_unique_id(void* out128);
  * bounds has num_shards+1 entries.  Host-only. */
 int slda_shard_bounds(uint32_t num_docs, uint64_t num_tokens, const uint32_t* doc_lengths,
                       uint32_t num_shards, uint32_t* bounds);
+/* Word-row slice [*row_begin, *row_end) that shard `rank` of `world` owns in the M-step
+ * (reduce-scatter of C_wk, phi/L4 rows, all-gather): V is padded to a multiple of world
+ * (*padded_rows) and split evenly.  Host-only. */
+int slda_word_slice(uint32_t vocab_size, uint32_t world, uint32_t rank, uint32_t* row_begin,
+                    uint32_t* row_end, uint32_t* padded_rows);
 
 /* Synthetic corpora.  Host-only, multi-threaded, deterministic in
  * (params, seed) regardless of thread count.  family 0 = G (LDA-generative: Zipf(1)

@@ -170,9 +170,19 @@ struct slda_engine {
     unsigned long long* entries_counter(uint32_t s) const { return counters.as<unsigned long long>() + 1 + s; }
     unsigned long long* entries_counter() const { return entries_counter(slot); }
 
+    // Word-row slice owned in the M-step: slda_word_slice (host.cpp), the rule the CPU
+    // choreography test (tests/test_sharding_gloo.py) shares.
     uint32_t slice_rows() const { return V_pad / world; }
-    uint32_t row_begin() const { return std::min(V, rank * slice_rows()); }
-    uint32_t row_end() const { return std::min(V, (rank + 1) * slice_rows()); }
+    uint32_t row_begin() const {
+        uint32_t b = 0, e = 0;
+        slda_word_slice(V, world, rank, &b, &e, nullptr);
+        return b;
+    }
+    uint32_t row_end() const {
+        uint32_t b = 0, e = 0;
+        slda_word_slice(V, world, rank, &b, &e, nullptr);
+        return e;
+    }
 
     ~slda_engine() {
         if (device >= 0) cudaSetDevice(device);
@@ -227,7 +237,10 @@ struct slda_engine {
         seed = c.seed;
         falpha = static_cast<float>(alpha);
         V = vocab;
-        V_pad = (V + world - 1) / world * world;
+        {
+            uint32_t b = 0, e = 0;
+            slda_word_slice(V, world, rank, &b, &e, &V_pad);
+        }
         K_pad = (K + slda::kBlock - 1) / slda::kBlock * slda::kBlock;
         n_l8 = K_pad / slda::kLeaf;
         l8_stride = (n_l8 + 3) / 4 * 4;

@@ -223,6 +223,20 @@ int slda_shard_bounds(uint32_t num_docs, uint64_t num_tokens, const uint32_t* do
     return SLDA_OK;
 }
 
+int slda_word_slice(uint32_t vocab_size, uint32_t world, uint32_t rank, uint32_t* row_begin,
+                    uint32_t* row_end, uint32_t* padded_rows) {
+    if (world == 0 || rank >= world || !row_begin || !row_end) {
+        slda_set_error_internal("rank must be < world and world >= 1");
+        return SLDA_ERR_VALIDATION;
+    }
+    const uint64_t padded = (static_cast<uint64_t>(vocab_size) + world - 1) / world * world;
+    const uint64_t rows = padded / world;
+    *row_begin = static_cast<uint32_t>(std::min<uint64_t>(vocab_size, rank * rows));
+    *row_end = static_cast<uint32_t>(std::min<uint64_t>(vocab_size, (rank + 1) * rows));
+    if (padded_rows) *padded_rows = static_cast<uint32_t>(padded);
+    return SLDA_OK;
+}
+
 int slda_generate_corpus_size(const slda_gen_params* params, uint64_t* num_tokens) {
     try {
         const Params p = resolve(params);

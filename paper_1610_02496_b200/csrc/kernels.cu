@@ -26,17 +26,21 @@ inline uint32_t grid_for(uint64_t n, uint32_t threads, uint32_t cap = 148u * 32u
 // sequential f32 chains.
 // ============================================================================
 
-__device__ __forceinline__ float entry_mass(uint32_t e, uint32_t tbits, uint32_t tmask,
-                                            const float* s_bhat) {
-    return __fmul_rn(__uint2float_rn(e >> tbits), s_bhat[e & tmask]);
+// phi row lookup: shared memory (staged row) or, when the row is too large to stage
+// (kGlobalPhi, K >~ 45K), the global row through L1/L2.
+template <bool kGlobalPhi>
+__device__ __forceinline__ float entry_mass(uint32_t e, uint32_t tbits, uint32_t tmask, const float* phi) {
+    const float p = kGlobalPhi ? __ldg(phi + (e & tmask)) : phi[e & tmask];
+    return __fmul_rn(__uint2float_rn(e >> tbits), p);
 }
 
+template <bool kGlobalPhi>
 __device__ __forceinline__ float acc_quad(float s, const uint4& q, uint32_t tbits, uint32_t tmask,
-                                          const float* s_bhat) {
-    s = __fadd_rn(s, entry_mass(q.x, tbits, tmask, s_bhat));
-    s = __fadd_rn(s, entry_mass(q.y, tbits, tmask, s_bhat));
-    s = __fadd_rn(s, entry_mass(q.z, tbits, tmask, s_bhat));
-    return __fadd_rn(s, entry_mass(q.w, tbits, tmask, s_bhat));
+                                          const float* phi) {
+    s = __fadd_rn(s, entry_mass<kGlobalPhi>(q.x, tbits, tmask, phi));
+    s = __fadd_rn(s, entry_mass<kGlobalPhi>(q.y, tbits, tmask, phi));
+    s = __fadd_rn(s, entry_mass<kGlobalPhi>(q.z, tbits, tmask, phi));
+    return __fadd_rn(s, entry_mass<kGlobalPhi>(q.w, tbits, tmask, phi));
 }
 
 // One 32-byte sector (8 C_dk entries) per lane: a 256-bit load (LDG.E.256 on sm_100a),
@@ -116,22 +120,24 @@ __device__ __forceinline__ void stage_group(const uint4* A4, const uint32_t (&rq
     store_group(q, sub, grp, stage);
 }
 
-template <int NT>
+template <int NT, bool kGlobalPhi>
 __global__ void __launch_bounds__(NT, 65536 / (NT * 64)) sampler_kernel(SamplerArgs a) {
     extern __shared__ __align__(16) float sm[];
-    float* s_bhat = sm;
-    float* s_l8 = sm + a.K_pad;             // l8_stride (L4[8j+7], padded with the total)
+    const uint32_t v = a.units[blockIdx.x].word;
+    const float* s_bhat = kGlobalPhi ? a.bhat + static_cast<size_t>(v) * a.K_pad : sm;
+    float* s_l8 = kGlobalPhi ? sm : sm + a.K_pad;  // l8_stride (L4[8j+7], padded with the total)
     float* s_ck = s_l8 + a.l8_stride;       // [kCkSectors][NT]
     unsigned char* s_stage = reinterpret_cast<unsigned char*>(s_ck + kCkSectors * NT);
 
     const Unit unit = a.units[blockIdx.x];
-    const uint32_t v = unit.word;
     const float* l4row = a.l4 + static_cast<size_t>(v) * a.K_pad;
     const float total = __ldg(l4row + a.K_pad - 1);  // padded with the row total
     {
-        const float4* gb = reinterpret_cast<const float4*>(a.bhat + static_cast<size_t>(v) * a.K_pad);
-        float4* sb = reinterpret_cast<float4*>(s_bhat);
-        for (uint32_t i = threadIdx.x; i < a.K_pad / 4; i += NT) sb[i] = __ldg(gb + i);
+        if (!kGlobalPhi) {
+            const float4* gb = reinterpret_cast<const float4*>(a.bhat + static_cast<size_t>(v) * a.K_pad);
+            float4* sb = reinterpret_cast<float4*>(sm);
+            for (uint32_t i = threadIdx.x; i < a.K_pad / 4; i += NT) sb[i] = __ldg(gb + i);
+        }
         const float4* gl = reinterpret_cast<const float4*>(a.l8 + static_cast<size_t>(v) * a.l8_stride);
         float4* sl = reinterpret_cast<float4*>(s_l8);
         for (uint32_t i = threadIdx.x; i < a.l8_stride / 4; i += NT) sl[i] = __ldg(gl + i);
@@ -198,8 +204,8 @@ __global__ void __launch_bounds__(NT, 65536 / (NT * 64)) sampler_kernel(SamplerA
             for (uint32_t u = 0; u < kGroup; ++u) {
                 const uint32_t sec = kGroup * g + u;
                 if (sec < nsect) {
-                    s = acc_quad(s, *reinterpret_cast<const uint4*>(mine + 32 * u), tbits, tmask, s_bhat);
-                    s = acc_quad(s, *reinterpret_cast<const uint4*>(mine + 32 * u + 16), tbits, tmask, s_bhat);
+                    s = acc_quad<kGlobalPhi>(s, *reinterpret_cast<const uint4*>(mine + 32 * u), tbits, tmask, s_bhat);
+                    s = acc_quad<kGlobalPhi>(s, *reinterpret_cast<const uint4*>(mine + 32 * u + 16), tbits, tmask, s_bhat);
                     if (sec < kCkSectors) ck[sec * NT] = s;
                 }
             }
@@ -261,7 +267,7 @@ __global__ void __launch_bounds__(NT, 65536 / (NT * 64)) sampler_kernel(SamplerA
                 const uint32_t es[8] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};
 #pragma unroll
                 for (int w = 0; w < 8; ++w) {
-                    run = __fadd_rn(run, entry_mass(es[w], tbits, tmask, s_bhat));
+                    run = __fadd_rn(run, entry_mass<kGlobalPhi>(es[w], tbits, tmask, s_bhat));
                     if (need && run >= xs) {
                         topic = es[w] & tmask;
                         need = false;
@@ -282,33 +288,30 @@ __global__ void __launch_bounds__(NT, 65536 / (NT * 64)) sampler_kernel(SamplerA
     }
 }
 
-size_t sampler_smem(const SamplerArgs& a, int nt) {
-    return sizeof(float) * (static_cast<size_t>(a.K_pad) + a.l8_stride) +
+size_t sampler_smem(const SamplerArgs& a, int nt, bool global_phi) {
+    return sizeof(float) * ((global_phi ? 0 : static_cast<size_t>(a.K_pad)) + a.l8_stride) +
            (sizeof(float) * kCkSectors + kStageRow) * static_cast<size_t>(nt);
+}
+
+template <int NT, bool G>
+cudaError_t launch_sampler_t(const SamplerArgs& a, uint32_t n_units, cudaStream_t s) {
+    static bool configured = false;
+    if (!configured) {
+        cudaFuncSetAttribute(sampler_kernel<NT, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+        configured = true;
+    }
+    sampler_kernel<NT, G><<<n_units, NT, sampler_smem(a, NT, G), s>>>(a);
+    return cudaGetLastError();
 }
 
 cudaError_t launch_sampler(const SamplerArgs& a, uint32_t n_units, cudaStream_t s) {
     if (n_units == 0) return cudaSuccess;
-    // 512 threads share one staged phi row when it is large (K = 10K: 2 CTAs x 16 warps).
-    const bool wide = sizeof(float) * (static_cast<size_t>(a.K_pad) + a.l8_stride) > 24 * 1024;
-    if (!wide) {
-        static bool configured = false;
-        if (!configured) {
-            cudaFuncSetAttribute(sampler_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-            configured = true;
-        }
-        sampler_kernel<256><<<n_units, 256, sampler_smem(a, 256), s>>>(a);
-    } else {
-        const size_t smem = sampler_smem(a, 512);
-        if (smem > 227 * 1024) return cudaErrorInvalidConfiguration;  // K too large to stage phi
-        static bool configured = false;
-        if (!configured) {
-            cudaFuncSetAttribute(sampler_kernel<512>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-            configured = true;
-        }
-        sampler_kernel<512><<<n_units, 512, smem, s>>>(a);
-    }
-    return cudaGetLastError();
+    const size_t phi_bytes = sizeof(float) * (static_cast<size_t>(a.K_pad) + a.l8_stride);
+    // Small phi rows: 256-thread CTAs.  Large (K = 10K): 512 threads share one staged row
+    // (2 CTAs x 16 warps per SM).  Rows that do not fit shared memory: gather through L1/L2.
+    if (phi_bytes <= 24 * 1024) return launch_sampler_t<256, false>(a, n_units, s);
+    if (sampler_smem(a, 512, false) <= 227 * 1024) return launch_sampler_t<512, false>(a, n_units, s);
+    return launch_sampler_t<512, true>(a, n_units, s);
 }
 
 // ============================================================================

@@ -84,6 +84,7 @@ def lib():
                   "slda_get_tree_prefix", "slda_get_assignments"):
             getattr(L, n).argtypes = [C.c_void_p, C.c_void_p]
         L.slda_shard_bounds.argtypes = [C.c_uint32, C.c_uint64, C.c_void_p, C.c_uint32, C.c_void_p]
+        L.slda_word_slice.argtypes = [C.c_uint32, C.c_uint32, C.c_uint32] + [C.POINTER(C.c_uint32)] * 3
         L.slda_generate_corpus_size.argtypes = [C.POINTER(GenParams), C.POINTER(C.c_uint64)]
         L.slda_generate_corpus.argtypes = [C.POINTER(GenParams), C.c_void_p, C.c_uint64]
         _lib = L

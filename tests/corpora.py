@@ -55,6 +55,9 @@ CASES: dict[str, dict] = {
                      "K": 20, "seed": 4, "iterations": 3, "given_topics_seed": 77},
     "k_large": {"corpus": {"family": U, "D": 50, "V": 50, "T": 5_000, "seed": 13},
                 "K": 20_000, "seed": 2, "iterations": 2},
+    # phi row too large for shared memory: the sampler gathers phi through L1/L2.
+    "k_global_phi": {"corpus": {"family": U, "D": 40, "V": 30, "T": 3_000, "seed": 17},
+                     "K": 40_000, "seed": 6, "iterations": 2},
     "alpha_beta": {"corpus": {"family": G, "D": 400, "V": 600, "T": 40_000, "seed": 14, "latent": 20},
                    "K": 25, "alpha": 0.3, "beta": 0.05, "seed": 8, "iterations": 4,
                    "heldout": {"family": G, "D": 60, "V": 600, "T": 6_000, "seed": 15, "latent": 20}},
