@@ -947,14 +947,32 @@ cudaError_t launch_recount(const uint2* tok, const Unit* units, uint32_t n_units
 
 __global__ void validate_kernel(const uint32_t* __restrict__ aos, uint64_t T, uint32_t doc_begin,
                                 uint32_t doc_end, uint32_t V, uint32_t K, ValidateOut* out) {
+    // Per-thread minima, then one atomic per warp and quantity (a corpus of sentinel topics
+    // would otherwise serialise T atomics on one address).
+    unsigned long long bad_doc = ~0ull, bad_word = ~0ull, first_invalid = ~0ull, first_big = ~0ull;
+    uint32_t unsorted = 0;
     for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < T;
          i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
         const uint32_t d = aos[3 * i], w = aos[3 * i + 1], t = aos[3 * i + 2];
-        if (d < doc_begin || d >= doc_end) atomicMin(&out->bad_doc, static_cast<unsigned long long>(i));
-        if (w >= V) atomicMin(&out->bad_word, static_cast<unsigned long long>(i));
-        if (t == kInvalidTopic) atomicMin(&out->first_invalid, static_cast<unsigned long long>(i));
-        else if (t >= K) atomicMin(&out->first_big, static_cast<unsigned long long>(i));
-        if (i > 0 && aos[3 * (i - 1)] > d) out->unsorted = 1u;
+        if ((d < doc_begin || d >= doc_end) && bad_doc == ~0ull) bad_doc = i;
+        if (w >= V && bad_word == ~0ull) bad_word = i;
+        if (t == kInvalidTopic) first_invalid = min(first_invalid, static_cast<unsigned long long>(i));
+        else if (t >= K) first_big = min(first_big, static_cast<unsigned long long>(i));
+        if (i > 0 && aos[3 * (i - 1)] > d) unsorted = 1u;
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        bad_doc = min(bad_doc, __shfl_xor_sync(0xffffffffu, bad_doc, o));
+        bad_word = min(bad_word, __shfl_xor_sync(0xffffffffu, bad_word, o));
+        first_invalid = min(first_invalid, __shfl_xor_sync(0xffffffffu, first_invalid, o));
+        first_big = min(first_big, __shfl_xor_sync(0xffffffffu, first_big, o));
+        unsorted |= __shfl_xor_sync(0xffffffffu, unsorted, o);
+    }
+    if (lane_id() == 0) {
+        if (bad_doc != ~0ull) atomicMin(&out->bad_doc, bad_doc);
+        if (bad_word != ~0ull) atomicMin(&out->bad_word, bad_word);
+        if (first_invalid != ~0ull) atomicMin(&out->first_invalid, first_invalid);
+        if (first_big != ~0ull) atomicMin(&out->first_big, first_big);
+        if (unsorted) out->unsorted = 1u;
     }
 }
 
