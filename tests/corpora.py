@@ -37,7 +37,7 @@ U = 1
 CASES: dict[str, dict] = {
     # BASELINE.json configs[0]: D=1K, V=1K, T=100K, K=100, 50 iterations.
     "c1": {"corpus": {"family": G, "D": 1000, "V": 1000, "T": 100_000, "seed": 20161008},
-           "K": 100, "seed": 42, "iterations": 50, "pdow": True,
+           "K": 100, "seed": 42, "iterations": 50, "pdow": True, "ll_every": 5,
            "heldout": {"family": G, "D": 200, "V": 1000, "T": 20_000, "seed": 7}},
     "k1": {"corpus": {"family": U, "D": 30, "V": 12, "T": 180, "seed": 5},
            "K": 1, "seed": 11, "iterations": 3},

@@ -43,11 +43,19 @@ def run_case(name: str, spec: dict) -> dict:
            "alpha": m.alpha, "iterations": []}
     out["iterations"].append(m.digests())
     kd = []
-    for _ in range(spec["iterations"]):
+    # Held-out LL curve (the reference's only LL, eval.cpp:49-133) every `ll_every` iterations.
+    curve = {}
+    held = corpus_arrays(spec["heldout"]) if spec.get("heldout") else None
+    for it in range(1, spec["iterations"] + 1):
         m.iterate()
         out["iterations"].append(m.digests())
         kd.append(m.last_mean_doc_topics)
+        if held is not None and spec.get("ll_every") and it % spec["ll_every"] == 0:
+            hd, hw, hD, _ = held
+            curve[str(it)] = m.heldout_ll(hD, V, hd, hw, burn_in=spec.get("burn_in", 20), seed=spec["seed"])[0]
     out["mean_doc_topics"] = kd
+    if curve:
+        out["ll_curve"] = curve
     if spec.get("heldout"):
         hd, hw, hD, _ = corpus_arrays(spec["heldout"])
         ll, n = m.heldout_ll(hD, V, hd, hw, burn_in=spec.get("burn_in", 20), seed=spec["seed"])

@@ -111,6 +111,56 @@ def test_heldout_ll_matches_reference(name, golden):
     assert abs(ll - ref) <= HELDOUT_REL_TOL * abs(ref), (ll, ref)
 
 
+def test_heldout_ll_curve_tracks_reference(golden):
+    """North star: the per-iteration log-likelihood tracks the reference over the full run
+    (C1, 50 iterations, held-out LL every 5 iterations, |rel| <= 1e-12)."""
+    spec = CASES["c1"]
+    curve = golden["cases"]["c1"]["ll_curve"]
+    m, cfg, _ = make_model(spec)
+    hd, hw, hD, V = corpus_arrays(spec["heldout"])
+    held = slda().Corpus.from_arrays(hD, V, hd, hw)
+    for it in range(1, spec["iterations"] + 1):
+        m.run_iteration(cfg)
+        if str(it) in curve:
+            ll, _ = slda().heldout_ll(m, held, burn_in=20, workers=1, seed=spec["seed"])
+            assert abs(ll - curve[str(it)]) <= HELDOUT_REL_TOL * abs(curve[str(it)]), (it, ll, curve[str(it)])
+
+
+def test_device_draws_pass_chi_square():
+    """Acceptance criterion 1 (acceptance.cpp:48-135) on device draws: one document of one
+    word, so every token of an iteration draws from the same law
+    p(k) ~ (A_dk + alpha) * bhat_k; the histogram of the new topics must pass chi-square
+    (z = 3.09, cells < 5 pooled) against the enumerated law."""
+    s = slda()
+    K, T = 24, 200_000
+    doc = np.zeros(T, np.uint32)
+    word = np.zeros(T, np.uint32)
+    corpus = s.Corpus.from_arrays(1, 2, doc, word)
+    cfg = s.TrainConfig()
+    cfg.num_topics = K
+    cfg.seed = 99
+    m = s.init_state(corpus, cfg)
+    offs, tops, cnts = m.doc_topic()
+    bhat = m.word_topic_prob()[0].astype(np.float64)
+    a = np.zeros(K)
+    a[tops] = cnts
+    law = (a + m.alpha) * bhat
+    law /= law.sum()
+    m.run_iteration(cfg)
+    hist = np.bincount(m.assignments(), minlength=K).astype(np.float64)
+    expected = law * T
+    small = expected < 5
+    stat = (((hist[~small] - expected[~small]) ** 2) / expected[~small]).sum()
+    cells = int((~small).sum())
+    if small.any():
+        stat += (hist[small].sum() - expected[small].sum()) ** 2 / expected[small].sum()
+        cells += 1
+    df = max(cells - 1, 1)
+    h = 2.0 / (9.0 * df)
+    critical = df * (1 - h + 3.09 * np.sqrt(h)) ** 3  # Wilson-Hilferty, oracles.cpp:46-84
+    assert stat <= critical, (stat, critical)
+
+
 def test_async_iterations_equal_sync():
     spec = CASES["u_k64"]
     a, cfg, _ = make_model(spec)

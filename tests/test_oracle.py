@@ -155,6 +155,10 @@ def test_oracle_matches_reference_digests(name, golden):
         if it + 1 < len(iters):
             m.iterate()
             assert abs(m.mean_doc_topics() - fx["mean_doc_topics"][it]) == 0
+    if "ll_curve" in fx:  # the last point of the curve: same model state as the run's end
+        hd, hw, hD, _ = corpus_arrays(spec["heldout"])
+        last = str(spec["iterations"])
+        assert m.heldout_ll(hD, V, hd, hw, burn_in=20, seed=spec["seed"])[0] == fx["ll_curve"][last]
     if "heldout" in fx:
         hd, hw, hD, _ = corpus_arrays(spec["heldout"])
         ll, n = m.heldout_ll(hD, V, hd, hw, burn_in=20, seed=spec["seed"])
