@@ -14,6 +14,7 @@
 
 #include <algorithm>
 #include <chrono>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <stdexcept>
@@ -147,6 +148,7 @@ struct slda_engine {
     uint32_t rank = 0, world = 1;
     uint32_t nseg = 0, n_units = 0, n_long = 0;
     bool doc_major = true;
+    bool compact = false;  // C_dk row format (kernels.cu: compact 16-bit slots or wide 32-bit)
     uint32_t wshift = 0;  // word field shift of the execution-order key
     size_t device_bytes = 0;
     uint64_t nnz = 0;
@@ -358,6 +360,16 @@ void slda_engine::build(const slda_corpus_view& cv, const slda_config& c) {
             validation("document of length " + std::to_string(max_len) +
                        " exceeds the packed C_dk count range at this K");
     }
+    // Row format: the 32-bit wide rows by default.  The compact 16-bit format (kernels.cu)
+    // is opt-in (SLDA_ROW_FORMAT=compact): it cuts sampler DRAM bytes ~25% and wins on
+    // short-document corpora at large K (C3: 131 vs 139 ms/iteration) but loses where the
+    // sampler is issue-bound or documents are long (C2 42.7 vs 31.0, C5 K=10K 88.9 vs 55.5;
+    // DESIGN.md §6).
+    compact = false;
+    if (const char* f = std::getenv("SLDA_ROW_FORMAT")) {
+        if (std::string(f) == "compact")
+            compact = K <= slda::kCompactMaxK && max_len <= slda::kCompactMaxLen;
+    }
 
     // Slot permutation for corpora that are not doc-sorted: stable by doc keeps
     // corpus order within a document.
@@ -522,6 +534,7 @@ void slda_engine::ssc() {
     s.row4 = row4.as<uint32_t>();
     s.A = A.as<uint32_t>();
     s.tbits = tbits;
+    s.compact = compact ? 1u : 0u;
     s.K_pad = K_pad;
     s.long_docs = long_docs.as<uint32_t>();
     s.n_long = n_long;
@@ -600,6 +613,7 @@ void slda_engine::enqueue_iteration() {
     a.l8_stride = l8_stride;
     a.n_l8 = n_l8;
     a.tbits = tbits;
+    a.compact = compact ? 1u : 0u;
     a.row_entries = entries_counter();
     CK(slda::launch_sampler(a, n_units, stream));
     launches += n_units > 0;
@@ -833,20 +847,47 @@ int slda_get_assignments(slda_engine* e, uint32_t* out) {
     });
 }
 
+}  // extern "C"
+
 namespace {
-// C_dk rows copied to the host: row d = [nnz-1 | entries], empty documents have none.
+// C_dk rows copied to the host (kernels.cu formats); empty documents have none.
 struct HostRows {
     std::vector<uint32_t> doc_start, row4, A;
+    uint32_t mask = 0, tbits = 0;
+    bool compact = false;
+    const uint32_t* row(uint32_t d) const { return A.data() + static_cast<size_t>(row4[d]) * 4; }
     uint32_t nnz(uint32_t d) const {
-        return doc_start[d + 1] == doc_start[d] ? 0u : (A[static_cast<size_t>(row4[d]) * 4] & mask) + 1u;
+        if (doc_start[d + 1] == doc_start[d]) return 0u;
+        return compact ? row(d)[0] >> 16 : (row(d)[0] & mask) + 1u;
     }
-    const uint32_t* entries(uint32_t d) const { return A.data() + static_cast<size_t>(row4[d]) * 4 + 1; }
-    uint32_t mask = 0;
+    // Decoded (topic, count) pairs in ascending topic order.
+    template <class F>
+    void for_each(uint32_t d, F&& f) const {
+        const uint32_t n = nnz(d);
+        if (n == 0) return;
+        const uint32_t* r = row(d);
+        if (!compact) {
+            for (uint32_t i = 0; i < n; ++i) f(r[1 + i] & mask, r[1 + i] >> tbits);
+            return;
+        }
+        const uint32_t words = (r[0] & 0xFFFFu) * 8u;
+        for (uint32_t w = 1; w < words; ++w) {
+            const uint32_t h0 = r[w] & 0xFFFFu, h1 = r[w] >> 16;
+            if (h0 & 0x8000u) {
+                if (h0 != 0xFFFFu) f(h0 & 0x7FFFu, h1);
+            } else {
+                f(h0, 1u);
+                if (h1 != 0xFFFFu) f(h1, 1u);
+            }
+        }
+    }
 };
 
 HostRows fetch_rows(slda_engine* e) {
     HostRows h;
     h.mask = (1u << e->tbits) - 1u;
+    h.tbits = e->tbits;
+    h.compact = e->compact;
     h.doc_start.resize(static_cast<size_t>(e->D) + 1);
     h.row4.resize(static_cast<size_t>(e->D) + 1);
     h.A.resize(e->A.bytes / 4);
@@ -856,6 +897,8 @@ HostRows fetch_rows(slda_engine* e) {
     return h;
 }
 }  // namespace
+
+extern "C" {
 
 int slda_get_doc_topic_nnz(slda_engine* e, uint64_t* nnz) {
     return guarded([&] {
@@ -878,11 +921,11 @@ int slda_get_doc_topic(slda_engine* e, uint64_t* row_offsets, uint32_t* topics, 
         uint64_t pos = 0;
         row_offsets[0] = 0;
         for (uint32_t d = 0; d < e->D; ++d) {
-            const uint32_t* row = h.entries(d);
-            for (uint32_t i = 0, n = h.nnz(d); i < n; ++i, ++pos) {
-                topics[pos] = row[i] & h.mask;
-                counts[pos] = row[i] >> e->tbits;
-            }
+            h.for_each(d, [&](uint32_t topic, uint32_t count) {
+                topics[pos] = topic;
+                counts[pos] = count;
+                ++pos;
+            });
             row_offsets[d + 1] = pos;
         }
     });

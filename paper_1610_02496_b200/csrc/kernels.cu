@@ -59,6 +59,16 @@ __device__ __forceinline__ Sector ldg_sector(const uint4* p) {
 
 __device__ __forceinline__ Sector zero_sector() { return Sector{make_uint4(0u, 0u, 0u, 0u), make_uint4(0u, 0u, 0u, 0u)}; }
 
+// Compact C_dk rows (K <= kCompactMaxK): 16-bit slots, two per 32-bit word.  Word 0 =
+// nsect | nnz << 16.  Then the entries in ascending topic order: a count-1 entry is one slot
+// holding its topic; a count >= 2 entry is a whole word (topic | 0x8000, count) at an even
+// slot, a null slot (0xFFFF) padding the odd slot before it when needed; the row ends with
+// null slots up to a sector (16 slots).  Pairs never straddle a word, so every word decodes
+// on its own (sector checkpoints carry no parse state), and a count-1 entry needs no count
+// conversion: f32(1) * phi == phi.  Versus the 32-bit wide format this halves the bytes of
+// count-1 entries, the majority while documents are spread over many topics.
+constexpr uint32_t kNull16 = 0xFFFFu;
+
 // lower_bound over the word's L4 prefix (== WaryTree::sample, acceptance.cpp:140-200):
 // binary search of the staged L8 level (first 8-block whose last prefix >= x), then one
 // 32-byte sector of L4.  Returns the first index with L4 >= x (x <= total).
@@ -120,7 +130,102 @@ __device__ __forceinline__ void stage_group(const uint4* A4, const uint32_t (&rq
     store_group(q, sub, grp, stage);
 }
 
-template <int NT, bool kGlobalPhi>
+// ---- Row decoding for the sampler (both row formats) ----------------------------------------
+template <bool kGlobalPhi>
+__device__ __forceinline__ float ld_phi(const float* phi, uint32_t t) {
+    return kGlobalPhi ? __ldg(phi + t) : phi[t];
+}
+
+// Compact format word: up to two entries (see compact_chunk).  f32(1) * phi == phi, so a
+// count-1 entry adds phi[topic] directly, exactly as the reference's s += f32(1) * phi.
+// Branch-free word decode (lanes of a warp see different word kinds): the first slot is a
+// pair (topic|0x8000, count), a single, or null; the second slot is a single or null unless
+// the word is a pair.  Absent entries contribute +0 (s + +0 == s for the running sums, which
+// are >= +0) and their gathers are predicated off.
+struct WordEntries {
+    uint32_t t0, t1;   // topics
+    float c0;          // count of the first entry (1 for a single)
+    bool v0, v1;       // entries present
+};
+__device__ __forceinline__ WordEntries decode_word(uint32_t w) {
+    const uint32_t h0 = w & 0xFFFFu, h1 = w >> 16;
+    const bool pair = (h0 & 0x8000u) != 0;
+    WordEntries e;
+    e.v0 = h0 != kNull16;
+    e.t0 = h0 & 0x7FFFu;
+    e.c0 = pair ? __uint2float_rn(h1) : 1.0f;
+    e.v1 = !pair && h1 != kNull16;
+    e.t1 = h1;
+    return e;
+}
+
+template <bool kGlobalPhi>
+__device__ __forceinline__ float acc_word_compact(float s, uint32_t w, const float* phi) {
+    const WordEntries e = decode_word(w);
+    float p0 = 0.0f, p1 = 0.0f;
+    if (e.v0) p0 = ld_phi<kGlobalPhi>(phi, e.t0);
+    if (e.v1) p1 = ld_phi<kGlobalPhi>(phi, e.t1);
+    s = __fadd_rn(s, __fmul_rn(e.c0, p0));  // f32(1) * phi == phi; f32(c) * phi as the reference
+    return __fadd_rn(s, p1);
+}
+
+template <bool kGlobalPhi>
+__device__ __forceinline__ void scan_word_compact(float& run, bool& need, uint32_t& topic, float xs, uint32_t w,
+                                                  const float* phi) {
+    const WordEntries e = decode_word(w);
+    float p0 = 0.0f, p1 = 0.0f;
+    if (e.v0) p0 = ld_phi<kGlobalPhi>(phi, e.t0);
+    if (e.v1) p1 = ld_phi<kGlobalPhi>(phi, e.t1);
+    run = __fadd_rn(run, __fmul_rn(e.c0, p0));
+    if (need && e.v0 && run >= xs) { topic = e.t0; need = false; }
+    run = __fadd_rn(run, p1);
+    if (need && e.v1 && run >= xs) { topic = e.t1; need = false; }
+}
+
+// First pass over one staged sector (32 bytes) of a row.  Sector 0 starts with the header
+// (compact: skipped; wide: a count-0 entry that adds +0).
+template <bool kGlobalPhi, bool kCompact>
+__device__ __forceinline__ float acc_sector(float s, const unsigned char* p, uint32_t sec, uint32_t tbits,
+                                            uint32_t tmask, const float* phi) {
+    const uint4 lo = *reinterpret_cast<const uint4*>(p);
+    const uint4 hi = *reinterpret_cast<const uint4*>(p + 16);
+    if (kCompact) {
+        if (sec != 0) s = acc_word_compact<kGlobalPhi>(s, lo.x, phi);
+        s = acc_word_compact<kGlobalPhi>(s, lo.y, phi);
+        s = acc_word_compact<kGlobalPhi>(s, lo.z, phi);
+        s = acc_word_compact<kGlobalPhi>(s, lo.w, phi);
+        s = acc_word_compact<kGlobalPhi>(s, hi.x, phi);
+        s = acc_word_compact<kGlobalPhi>(s, hi.y, phi);
+        s = acc_word_compact<kGlobalPhi>(s, hi.z, phi);
+        return acc_word_compact<kGlobalPhi>(s, hi.w, phi);
+    }
+    s = acc_quad<kGlobalPhi>(s, lo, tbits, tmask, phi);
+    return acc_quad<kGlobalPhi>(s, hi, tbits, tmask, phi);
+}
+
+// Prefix re-scan of one staged sector: first running sum >= xs.
+template <bool kGlobalPhi, bool kCompact>
+__device__ __forceinline__ void scan_sector(float& run, bool& need, uint32_t& topic, float xs,
+                                            const unsigned char* p, uint32_t sec, uint32_t tbits,
+                                            uint32_t tmask, const float* phi) {
+    const uint4 lo = *reinterpret_cast<const uint4*>(p);
+    const uint4 hi = *reinterpret_cast<const uint4*>(p + 16);
+    const uint32_t es[8] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};
+#pragma unroll
+    for (int w = 0; w < 8; ++w) {
+        if (kCompact) {
+            if (w > 0 || sec != 0) scan_word_compact<kGlobalPhi>(run, need, topic, xs, es[w], phi);
+        } else {
+            run = __fadd_rn(run, entry_mass<kGlobalPhi>(es[w], tbits, tmask, phi));
+            if (need && run >= xs) {
+                topic = es[w] & tmask;
+                need = false;
+            }
+        }
+    }
+}
+
+template <int NT, bool kGlobalPhi, bool kCompact>
 __global__ void __launch_bounds__(NT, 65536 / (NT * 64)) sampler_kernel(SamplerArgs a) {
     extern __shared__ __align__(16) float sm[];
     const uint32_t v = a.units[blockIdx.x].word;
@@ -173,10 +278,11 @@ __global__ void __launch_bounds__(NT, 65536 / (NT * 64)) sampler_kernel(SamplerA
         stage_group(A4, rq, ns, gs, sub, grp, stage);
         __syncwarp();
 
-        // Row = [header | nnz entries ascending topic | zero-count padding to 8]; the
-        // header entry (nnz-1, count 0) and the padding add +0 to every running sum.
-        const uint32_t nnz = active ? (reinterpret_cast<const uint4*>(mine)->x & tmask) + 1u : 0u;
-        const uint32_t nsect = active ? (nnz + 8u) >> 3 : 0u;
+        // Wide row = [header (nnz-1, count 0) | entries | zero-count padding to 8]: header and
+        // padding add +0 to every running sum.  Compact row: word 0 = nsect | nnz << 16.
+        const uint32_t w0 = reinterpret_cast<const uint4*>(mine)->x;
+        const uint32_t nnz = active ? (kCompact ? w0 >> 16 : (w0 & tmask) + 1u) : 0u;
+        const uint32_t nsect = active ? (kCompact ? w0 & 0xFFFFu : (nnz + 8u) >> 3) : 0u;
         const uint32_t ngroups = (nsect + kGroup - 1) / kGroup;
         entries += nnz;
         const uint32_t max_groups = __reduce_max_sync(0xffffffffu, ngroups);
@@ -204,8 +310,7 @@ __global__ void __launch_bounds__(NT, 65536 / (NT * 64)) sampler_kernel(SamplerA
             for (uint32_t u = 0; u < kGroup; ++u) {
                 const uint32_t sec = kGroup * g + u;
                 if (sec < nsect) {
-                    s = acc_quad<kGlobalPhi>(s, *reinterpret_cast<const uint4*>(mine + 32 * u), tbits, tmask, s_bhat);
-                    s = acc_quad<kGlobalPhi>(s, *reinterpret_cast<const uint4*>(mine + 32 * u + 16), tbits, tmask, s_bhat);
+                    s = acc_sector<kGlobalPhi, kCompact>(s, mine + 32 * u, sec, tbits, tmask, s_bhat);
                     if (sec < kCkSectors) ck[sec * NT] = s;
                 }
             }
@@ -225,8 +330,9 @@ __global__ void __launch_bounds__(NT, 65536 / (NT * 64)) sampler_kernel(SamplerA
                 // Sparse branch: first running prefix >= p*S (prefix_search, sampler.hpp:18-41).
                 xs = __fmul_rn(up, s);
                 if (xs == 0.0f) {
-                    // every prefix is >= 0: the first real entry
-                    topic = __ldg(reinterpret_cast<const uint32_t*>(A4 + t.x) + 1) & tmask;
+                    // every prefix is >= 0: the first real entry (word 1 in both formats)
+                    const uint32_t e1 = __ldg(reinterpret_cast<const uint32_t*>(A4 + t.x) + 1);
+                    topic = kCompact ? (e1 & 0x7FFFu) : (e1 & tmask);
                 } else {
                     // The first sector whose end sum reaches xs holds the crossing; its re-scan
                     // restarts from the previous checkpoint, the same f32 value the first pass
@@ -262,17 +368,7 @@ __global__ void __launch_bounds__(NT, 65536 / (NT * 64)) sampler_kernel(SamplerA
             stage_group(A4, rq, ns, gs, sub, grp, stage);
             __syncwarp();
             if (need) {
-                const uint4 lo = *reinterpret_cast<const uint4*>(mine);
-                const uint4 hi = *reinterpret_cast<const uint4*>(mine + 16);
-                const uint32_t es[8] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};
-#pragma unroll
-                for (int w = 0; w < 8; ++w) {
-                    run = __fadd_rn(run, entry_mass<kGlobalPhi>(es[w], tbits, tmask, s_bhat));
-                    if (need && run >= xs) {
-                        topic = es[w] & tmask;
-                        need = false;
-                    }
-                }
+                scan_sector<kGlobalPhi, kCompact>(run, need, topic, xs, mine, sec, tbits, tmask, s_bhat);
                 ++sec;
             }
         }
@@ -293,14 +389,14 @@ size_t sampler_smem(const SamplerArgs& a, int nt, bool global_phi) {
            (sizeof(float) * kCkSectors + kStageRow) * static_cast<size_t>(nt);
 }
 
-template <int NT, bool G>
+template <int NT, bool G, bool C>
 cudaError_t launch_sampler_t(const SamplerArgs& a, uint32_t n_units, cudaStream_t s) {
     static bool configured = false;
     if (!configured) {
-        cudaFuncSetAttribute(sampler_kernel<NT, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+        cudaFuncSetAttribute(sampler_kernel<NT, G, C>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
         configured = true;
     }
-    sampler_kernel<NT, G><<<n_units, NT, sampler_smem(a, NT, G), s>>>(a);
+    sampler_kernel<NT, G, C><<<n_units, NT, sampler_smem(a, NT, G), s>>>(a);
     return cudaGetLastError();
 }
 
@@ -308,10 +404,16 @@ cudaError_t launch_sampler(const SamplerArgs& a, uint32_t n_units, cudaStream_t 
     if (n_units == 0) return cudaSuccess;
     const size_t phi_bytes = sizeof(float) * (static_cast<size_t>(a.K_pad) + a.l8_stride);
     // Small phi rows: 256-thread CTAs.  Large (K = 10K): 512 threads share one staged row
-    // (2 CTAs x 16 warps per SM).  Rows that do not fit shared memory: gather through L1/L2.
-    if (phi_bytes <= 24 * 1024) return launch_sampler_t<256, false>(a, n_units, s);
-    if (sampler_smem(a, 512, false) <= 227 * 1024) return launch_sampler_t<512, false>(a, n_units, s);
-    return launch_sampler_t<512, true>(a, n_units, s);
+    // (2 CTAs x 16 warps per SM).  Rows that do not fit shared memory (K > kCompactMaxK,
+    // so always the wide row format): gather phi through L1/L2.
+    if (phi_bytes <= 24 * 1024)
+        return a.compact ? launch_sampler_t<256, false, true>(a, n_units, s)
+                         : launch_sampler_t<256, false, false>(a, n_units, s);
+    if (sampler_smem(a, 512, false) <= 227 * 1024)
+        return a.compact ? launch_sampler_t<512, false, true>(a, n_units, s)
+                         : launch_sampler_t<512, false, false>(a, n_units, s);
+    if (a.compact) return cudaErrorInvalidConfiguration;
+    return launch_sampler_t<512, true, false>(a, n_units, s);
 }
 
 // ============================================================================
@@ -327,24 +429,36 @@ constexpr int kSscWarps = 8;
 // Ascending bitonic sort of N = 32*R keys held striped across the warp (key i in lane
 // i % 32, register i / 32): cross-lane stages exchange through shuffles, in-lane stages
 // swap registers.  Integer keys, so any correct sort is bit-identical to std::sort.
+// In-lane stage (partner distance j = 32*RJ): registers r and r|RJ.
+template <int R, int RJ>
+__device__ __forceinline__ void bitonic_inlane(uint32_t (&key)[R], uint32_t lane, uint32_t k) {
+#pragma unroll
+    for (uint32_t r = 0; r < R; ++r) {
+        if ((r & RJ) == 0) {
+            const uint32_t i = r * 32 + lane;
+            const bool up = (i & k) == 0;
+            const uint32_t a = key[r], b = key[r | RJ];
+            const uint32_t lo = min(a, b), hi = max(a, b);
+            key[r] = up ? lo : hi;
+            key[r | RJ] = up ? hi : lo;
+        }
+    }
+}
+
+// Stage loops are not unrolled (only the register dimension is), which keeps the five
+// instantiations within the instruction cache.
 template <int R>
 __device__ __forceinline__ void warp_bitonic(uint32_t (&key)[R], uint32_t lane) {
-#pragma unroll
+#pragma unroll 1
     for (uint32_t k = 2; k <= 32u * R; k <<= 1) {
-#pragma unroll
+#pragma unroll 1
         for (uint32_t j = k >> 1; j > 0; j >>= 1) {
             if (j >= 32) {
-                const uint32_t rj = j >> 5;
-#pragma unroll
-                for (uint32_t r = 0; r < R; ++r) {
-                    if ((r & rj) == 0) {
-                        const uint32_t i = r * 32 + lane;
-                        const bool up = (i & k) == 0;
-                        const uint32_t a = key[r], b = key[r | rj];
-                        const uint32_t lo = min(a, b), hi = max(a, b);
-                        key[r] = up ? lo : hi;
-                        key[r | rj] = up ? hi : lo;
-                    }
+                switch (j >> 5) {
+                    case 1: bitonic_inlane<R, 1>(key, lane, k); break;
+                    case 2: if (R > 2) bitonic_inlane<R, (R > 2 ? 2 : 1)>(key, lane, k); break;
+                    case 4: if (R > 4) bitonic_inlane<R, (R > 4 ? 4 : 1)>(key, lane, k); break;
+                    default: if (R > 8) bitonic_inlane<R, (R > 8 ? 8 : 1)>(key, lane, k); break;
                 }
             } else {
                 const bool lower = (lane & j) == 0;
@@ -360,9 +474,56 @@ __device__ __forceinline__ void warp_bitonic(uint32_t (&key)[R], uint32_t lane) 
     }
 }
 
+// ---- Compact C_dk rows: encoder (format: kNull16 above) -------------------------------------
+
+// Appends up to 32 entries (lane-ordered; invalid lanes skipped) at slot `pos` (warp-uniform,
+// advanced).  Slot positions come from a warp scan over the parity automaton
+// single: (adv 1, parity flips), pair: (adv 2 + parity, parity -> 0).
+__device__ __noinline__ void compact_chunk(uint16_t* row16, uint32_t& pos, bool valid, uint32_t topic,
+                                           uint32_t count, uint32_t lane) {
+    const bool pair = valid && count > 1;
+    // f(p) for p in {0, 1}: advance a_p (8 bits each; <= 96 per chunk), parity out q_p,
+    // packed as a0 | a1 << 8 | q0 << 16 | q1 << 17.  Identity for invalid lanes.
+    uint32_t f = valid ? (pair ? (2u | 3u << 8) : (1u | 1u << 8 | 1u << 16)) : (1u << 17);
+#pragma unroll
+    for (uint32_t o = 1; o < 32; o <<= 1) {
+        const uint32_t b = __shfl_up_sync(0xffffffffu, f, o);
+        if (lane >= o) {  // earlier lanes (b) first, then this one (f)
+            const uint32_t r0 = (b >> 16) & 1u, r1 = (b >> 17) & 1u;
+            const uint32_t n0 = (b & 0xFFu) + ((r0 ? f >> 8 : f) & 0xFFu);
+            const uint32_t n1 = ((b >> 8) & 0xFFu) + ((r1 ? f >> 8 : f) & 0xFFu);
+            const uint32_t m0 = r0 ? (f >> 17) & 1u : (f >> 16) & 1u;
+            const uint32_t m1 = r1 ? (f >> 17) & 1u : (f >> 16) & 1u;
+            f = n0 | n1 << 8 | m0 << 16 | m1 << 17;
+        }
+    }
+    const uint32_t p = pos & 1u;
+    const uint32_t ex = __shfl_up_sync(0xffffffffu, f, 1);
+    const uint32_t start = pos + (lane == 0 ? 0u : ((p ? ex >> 8 : ex) & 0xFFu));
+    if (valid) {
+        if (pair) {
+            uint32_t s = start;
+            if (s & 1u) row16[s++] = static_cast<uint16_t>(kNull16);
+            row16[s] = static_cast<uint16_t>(0x8000u | topic);
+            row16[s + 1] = static_cast<uint16_t>(count);
+        } else {
+            row16[start] = static_cast<uint16_t>(topic);
+        }
+    }
+    const uint32_t tot = __shfl_sync(0xffffffffu, f, 31);
+    pos += (p ? tot >> 8 : tot) & 0xFFu;
+}
+
+// Closes a compact row: null slots to the sector end, header word.
+__device__ __forceinline__ void compact_finish(uint16_t* row16, uint32_t pos, uint32_t nnz, uint32_t lane) {
+    const uint32_t end = (pos + 15u) & ~15u;
+    for (uint32_t s = pos + lane; s < end; s += 32) row16[s] = static_cast<uint16_t>(kNull16);
+    if (lane == 0) reinterpret_cast<uint32_t*>(row16)[0] = (end >> 4) | (nnz << 16);
+}
+
 // One document of n <= 32*R tokens: sort, run-length, write the C_dk row (header, entries,
-// zero padding to 8).  starts: per-warp scratch of >= n words.  Returns nnz.
-template <int R>
+// padding to a sector).  starts: per-warp scratch of >= n words.  Returns nnz.
+template <int R, bool kCompact>
 __device__ __forceinline__ uint32_t ssc_doc(const uint16_t* z, uint32_t n, uint32_t lane, uint32_t* starts,
                                             uint32_t* out_row, uint32_t tbits) {
     uint32_t key[R];
@@ -389,6 +550,8 @@ __device__ __forceinline__ uint32_t ssc_doc(const uint16_t* z, uint32_t n, uint3
     __syncwarp();
     // Entries: topic of the run's first key, count = distance to the next start.  The sorted
     // keys are gone from smem, so the topic is recovered from the start position's lane.
+    uint16_t* row16 = reinterpret_cast<uint16_t*>(out_row);
+    uint32_t pos = 2;  // compact: slots 0-1 are the header word
     for (uint32_t base = 0; base < nnz; base += 32) {
         const uint32_t e = base + lane;
         const uint32_t st = e < nnz ? starts[e] : 0u;
@@ -400,15 +563,21 @@ __device__ __forceinline__ uint32_t ssc_doc(const uint16_t* z, uint32_t n, uint3
             const uint32_t kv = __shfl_sync(0xffffffffu, key[r], st & 31u);
             if ((st >> 5) == r) topic = kv;
         }
-        if (e < nnz) out_row[1 + e] = topic | ((en - st) << tbits);
+        if (kCompact) compact_chunk(row16, pos, e < nnz, topic, en - st, lane);
+        else if (e < nnz) out_row[1 + e] = topic | ((en - st) << tbits);
     }
-    const uint32_t padded = (nnz + 8u) & ~7u;
-    for (uint32_t e = nnz + 1 + lane; e < padded; e += 32) out_row[e] = 0u;
-    if (lane == 0) out_row[0] = nnz - 1u;
+    if (kCompact) {
+        compact_finish(row16, pos, nnz, lane);
+    } else {
+        const uint32_t padded = (nnz + 8u) & ~7u;
+        for (uint32_t e = nnz + 1 + lane; e < padded; e += 32) out_row[e] = 0u;
+        if (lane == 0) out_row[0] = nnz - 1u;
+    }
     __syncwarp();
     return nnz;
 }
 
+template <bool kCompact>
 __global__ void __launch_bounds__(kSscWarps * 32) ssc_warp_kernel(SscArgs a) {
     __shared__ uint32_t s_start[kSscWarps][kSscWarpCap];
     const uint32_t w = threadIdx.x >> 5, lane = lane_id();
@@ -422,18 +591,18 @@ __global__ void __launch_bounds__(kSscWarps * 32) ssc_warp_kernel(SscArgs a) {
         uint32_t* row = a.A + __ldg(a.row4 + d) * 4u;
         const uint16_t* z = a.z + s0;
         uint32_t nnz;
-        if (n <= 32) nnz = ssc_doc<1>(z, n, lane, starts, row, a.tbits);
-        else if (n <= 64) nnz = ssc_doc<2>(z, n, lane, starts, row, a.tbits);
-        else if (n <= 128) nnz = ssc_doc<4>(z, n, lane, starts, row, a.tbits);
-        else if (n <= 256) nnz = ssc_doc<8>(z, n, lane, starts, row, a.tbits);
-        else nnz = ssc_doc<16>(z, n, lane, starts, row, a.tbits);
+        if (n <= 32) nnz = ssc_doc<1, kCompact>(z, n, lane, starts, row, a.tbits);
+        else if (n <= 64) nnz = ssc_doc<2, kCompact>(z, n, lane, starts, row, a.tbits);
+        else if (n <= 128) nnz = ssc_doc<4, kCompact>(z, n, lane, starts, row, a.tbits);
+        else if (n <= 256) nnz = ssc_doc<8, kCompact>(z, n, lane, starts, row, a.tbits);
+        else nnz = ssc_doc<16, kCompact>(z, n, lane, starts, row, a.tbits);
         nnz_acc += nnz;
     }
     if (lane == 0 && nnz_acc) atomicAdd(a.nnz_total, nnz_acc);
 }
 
 // Long documents: one CTA per document (grid-stride over the long-doc list).
-template <bool kSmemHist>
+template <bool kSmemHist, bool kCompact>
 __global__ void __launch_bounds__(256) ssc_long_kernel(SscArgs a) {
     extern __shared__ __align__(16) uint32_t s_dyn[];
     __shared__ uint32_t s_scan[256];
@@ -461,25 +630,37 @@ __global__ void __launch_bounds__(256) ssc_long_kernel(SscArgs a) {
             __syncthreads();
         }
         const uint32_t nnz = s_scan[255];
-        uint32_t pos = s_scan[tid] - mine;
-        for (uint32_t k = b0; k < b1; ++k) {
-            const uint32_t c = hist[k];
-            if (c) a.A[row + 1 + pos++] = k | (c << a.tbits);
+        if (kCompact) {
+            // One warp walks the histogram in topic order and packs the slots.
+            if (tid < 32) {
+                uint16_t* row16 = reinterpret_cast<uint16_t*>(a.A + row);
+                uint32_t pos = 2;
+                for (uint32_t k0 = 0; k0 < a.K_pad; k0 += 32) {
+                    const uint32_t c = hist[k0 + tid];
+                    compact_chunk(row16, pos, c != 0, k0 + tid, c, tid);
+                }
+                compact_finish(row16, pos, nnz, tid);
+            }
+        } else {
+            uint32_t pos = s_scan[tid] - mine;
+            for (uint32_t k = b0; k < b1; ++k) {
+                const uint32_t c = hist[k];
+                if (c) a.A[row + 1 + pos++] = k | (c << a.tbits);
+            }
+            const uint32_t padded = (nnz + 8u) & ~7u;
+            for (uint32_t r = nnz + 1 + tid; r < padded; r += 256) a.A[row + r] = 0u;
+            if (tid == 0) a.A[row] = nnz - 1u;
         }
-        const uint32_t padded = (nnz + 8u) & ~7u;
-        for (uint32_t r = nnz + 1 + tid; r < padded; r += 256) a.A[row + r] = 0u;
-        if (tid == 0) {
-            a.A[row] = nnz - 1u;
-            atomicAdd(a.nnz_total, static_cast<unsigned long long>(nnz));
-        }
+        if (tid == 0) atomicAdd(a.nnz_total, static_cast<unsigned long long>(nnz));
         __syncthreads();
     }
 }
 
-cudaError_t launch_ssc(const SscArgs& a, cudaStream_t s) {
+template <bool kCompact>
+cudaError_t launch_ssc_t(const SscArgs& a, cudaStream_t s) {
     if (a.D > 0) {
         const uint32_t blocks = grid_for(a.D, kSscWarps, 148u * 8u);
-        ssc_warp_kernel<<<blocks, kSscWarps * 32, 0, s>>>(a);
+        ssc_warp_kernel<kCompact><<<blocks, kSscWarps * 32, 0, s>>>(a);
     }
     if (a.n_long > 0) {
         const size_t smem = sizeof(uint32_t) * a.K_pad;
@@ -487,16 +668,20 @@ cudaError_t launch_ssc(const SscArgs& a, cudaStream_t s) {
         if (smem <= 200 * 1024) {
             static bool configured = false;
             if (!configured) {
-                cudaFuncSetAttribute(ssc_long_kernel<true>,
+                cudaFuncSetAttribute(ssc_long_kernel<true, kCompact>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
                 configured = true;
             }
-            ssc_long_kernel<true><<<blocks, 256, smem, s>>>(a);
+            ssc_long_kernel<true, kCompact><<<blocks, 256, smem, s>>>(a);
         } else {
-            ssc_long_kernel<false><<<blocks, 256, 0, s>>>(a);
+            ssc_long_kernel<false, kCompact><<<blocks, 256, 0, s>>>(a);
         }
     }
     return cudaGetLastError();
+}
+
+cudaError_t launch_ssc(const SscArgs& a, cudaStream_t s) {
+    return a.compact ? launch_ssc_t<true>(a, s) : launch_ssc_t<false>(a, s);
 }
 
 // ============================================================================

@@ -13,6 +13,9 @@ struct Unit {
 };
 
 constexpr uint32_t kUnitMaxTokens = 8192;  // sampler: max tokens per unit (one CTA)
+// Compact C_dk rows (16-bit slots, kernels.cu) need topics < 0x7FFF and counts/nnz < 2^16.
+constexpr uint32_t kCompactMaxK = 32767;
+constexpr uint32_t kCompactMaxLen = 65535;
 constexpr uint32_t kSscWarpCap = 512;      // SSC: docs up to this length take the warp path
 
 struct SamplerArgs {
@@ -29,6 +32,7 @@ struct SamplerArgs {
     uint64_t seed, id_base;
     uint32_t stream_kind;   // iteration number (trainer.cpp:423)
     uint32_t K, K_pad, l8_stride, n_l8, tbits;
+    uint32_t compact;       // C_dk rows in the compact 16-bit format
     unsigned long long* row_entries;  // optional: sum of nnz over tokens (roofline)
 };
 
@@ -41,6 +45,7 @@ struct SscArgs {
     const uint32_t* row4;       // per doc: row offset in uint4 units
     uint32_t* A;
     uint32_t tbits, K_pad;
+    uint32_t compact;           // write the compact 16-bit row format
     const uint32_t* long_docs;  // docs longer than kSscWarpCap
     uint32_t n_long;
     uint32_t* hist_scratch;     // n_long_ctas x K_pad (global fallback for large K)
