@@ -15,6 +15,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cstdlib>
+#include <cstdio>
 #include <cstring>
 #include <memory>
 #include <stdexcept>
@@ -289,6 +290,17 @@ struct slda_engine {
 
 // ----------------------------------------------------------------- build --
 void slda_engine::build(const slda_corpus_view& cv, const slda_config& c) {
+    // SLDA_TRACE=1: per-phase wall times of the setup on stderr (stream synchronised).
+    const bool trace = std::getenv("SLDA_TRACE") != nullptr;
+    auto t_last = std::chrono::steady_clock::now();
+    auto phase = [&](const char* name) {
+        if (!trace) return;
+        if (stream) CK(cudaStreamSynchronize(stream));
+        const auto now = std::chrono::steady_clock::now();
+        std::fprintf(stderr, "[slda setup] %-28s %8.1f ms\n", name,
+                     std::chrono::duration<double, std::milli>(now - t_last).count());
+        t_last = now;
+    };
     D_all = cv.num_docs;
     doc_begin = cv.doc_begin;
     doc_end = cv.doc_end;
@@ -300,6 +312,7 @@ void slda_engine::build(const slda_corpus_view& cv, const slda_config& c) {
     id_base = cv.token_id_base;
     configure(c, cv.vocab_size);
     alloc_model();
+    phase("configure+alloc_model");
 
     // Copy the borrowed AoS tokens (sparselda::Token layout) and validate on device.
     DevMem aos, val;
@@ -315,6 +328,7 @@ void slda_engine::build(const slda_corpus_view& cv, const slda_config& c) {
     slda::ValidateOut vo;
     CK(cudaMemcpyAsync(&vo, val.p, sizeof(vo), cudaMemcpyDeviceToHost, stream));
     CK(cudaStreamSynchronize(stream));
+    phase("h2d+validate");
     if (vo.bad_doc != ~0ull) validation("token " + std::to_string(vo.bad_doc) + ": doc outside the shard range");
     if (vo.bad_word != ~0ull) validation("token " + std::to_string(vo.bad_word) + ": word id out of range");
     bool draw = false;
@@ -337,6 +351,7 @@ void slda_engine::build(const slda_corpus_view& cv, const slda_config& c) {
     CK(slda::launch_deinterleave(aos.as<uint32_t>(), T, doc_begin, doc_local.as<uint32_t>(),
                                  word.as<uint32_t>(), draw ? nullptr : topic_in.as<uint32_t>(), stream));
     aos.release();
+    phase("deinterleave");
 
     // Doc-grouped slot offsets (corpus.cpp:186-189).
     doc_start.alloc((static_cast<size_t>(D) + 1) * 4, &device_bytes);
@@ -371,6 +386,7 @@ void slda_engine::build(const slda_corpus_view& cv, const slda_config& c) {
             compact = K <= slda::kCompactMaxK && max_len <= slda::kCompactMaxLen;
     }
 
+    phase("doc_start");
     // Slot permutation for corpora that are not doc-sorted: stable by doc keeps
     // corpus order within a document.
     if (!doc_major) {
@@ -411,6 +427,7 @@ void slda_engine::build(const slda_corpus_view& cv, const slda_config& c) {
         CK(cudaMemsetAsync(A.p, 0, A.bytes, stream));
     }
 
+    phase("row offsets + A alloc");
     // PDOW: stable radix sort of keys laid out in slot order -> the reference's
     // (word, doc, token_id) order (corpus.cpp:157-175), refined by descending doc
     // length inside each word (execution order; getters re-derive the canonical one).
@@ -452,6 +469,7 @@ void slda_engine::build(const slda_corpus_view& cv, const slda_config& c) {
                                       seg_index.as<uint32_t>(), T, wshift, seg_word.as<uint32_t>(),
                                       seg_off.as<uint32_t>(), stream));
     }
+    phase("PDOW sort + segments");
     // build_schedule (corpus.cpp:200-210): heavy first, ties by ascending word.
     if (nseg) {
         DevMem skeys, skeys_sorted, svals, counts, starts;
@@ -481,6 +499,7 @@ void slda_engine::build(const slda_corpus_view& cv, const slda_config& c) {
         units.alloc(sizeof(slda::Unit), &device_bytes);
     }
 
+    phase("schedule + units");
     // Long documents take the CTA histogram path of SSC.
     {
         DevMem flags, iota, cnt;
@@ -515,6 +534,7 @@ void slda_engine::build(const slda_corpus_view& cv, const slda_config& c) {
     word.release();
     topic_in.release();
 
+    phase("long docs + init topics");
     // C_dk (rebuild_doc_topic), C_wk (count_chunk_into), phi + trees.
     ssc();
     CK(cudaMemsetAsync(B.p, 0, B.bytes, stream));
@@ -523,6 +543,7 @@ void slda_engine::build(const slda_corpus_view& cv, const slda_config& c) {
     m_step();
     CK(cudaStreamSynchronize(stream));
     nnz = d2h_scalar(nnz_counter());
+    phase("ssc + recount + m_step");
 }
 
 void slda_engine::ssc() {
@@ -834,16 +855,14 @@ int slda_get_assignments(slda_engine* e, uint32_t* out) {
     return guarded([&] {
         if (!e || (!out && e->T)) validation("null argument");
         e->set_device();
+        if (e->T == 0) return;
+        // Permute/widen on the device, then one D2H straight into the caller's buffer.
+        DevMem d;
+        d.alloc(e->T * 4, nullptr);
+        CK(slda::launch_assignments(e->z.as<uint16_t>(), e->doc_major ? nullptr : e->input_of_slot.as<uint32_t>(),
+                                    e->T, d.as<uint32_t>(), e->stream));
+        CK(cudaMemcpyAsync(out, d.p, e->T * 4, cudaMemcpyDeviceToHost, e->stream));
         CK(cudaStreamSynchronize(e->stream));
-        std::vector<uint16_t> z(e->T);
-        if (e->T) CK(cudaMemcpy(z.data(), e->z.p, e->T * 2, cudaMemcpyDeviceToHost));
-        if (e->doc_major) {
-            for (uint64_t i = 0; i < e->T; ++i) out[i] = z[i];
-        } else {
-            std::vector<uint32_t> inv(e->T);
-            CK(cudaMemcpy(inv.data(), e->input_of_slot.p, e->T * 4, cudaMemcpyDeviceToHost));
-            for (uint64_t j = 0; j < e->T; ++j) out[inv[j]] = z[j];
-        }
     });
 }
 

@@ -1183,3 +1183,22 @@ cudaError_t launch_sched_counts(const uint32_t* schedule, const uint32_t* seg_le
 }
 
 }  // namespace slda
+
+namespace slda {
+
+// gather_assignments (trainer.cpp:203-213): slot-ordered u16 topics -> corpus-order u32.
+// input_of_slot == null: doc-sorted corpus, slot == corpus position (a widening copy).
+__global__ void assignments_kernel(const uint16_t* z, const uint32_t* input_of_slot, uint64_t T, uint32_t* out) {
+    for (uint64_t j = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; j < T;
+         j += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+        out[input_of_slot ? input_of_slot[j] : j] = z[j];
+}
+
+cudaError_t launch_assignments(const uint16_t* z, const uint32_t* input_of_slot, uint64_t T, uint32_t* out,
+                               cudaStream_t s) {
+    if (T == 0) return cudaSuccess;
+    assignments_kernel<<<grid_for(T, 256), 256, 0, s>>>(z, input_of_slot, T, out);
+    return cudaGetLastError();
+}
+
+}  // namespace slda

@@ -113,6 +113,9 @@ cudaError_t launch_validate(const uint32_t* aos, uint64_t T, uint32_t doc_begin,
                             uint32_t V, uint32_t K, ValidateOut* out, cudaStream_t s);
 cudaError_t launch_sched_counts(const uint32_t* schedule, const uint32_t* seg_len, uint32_t nseg,
                                 uint32_t* counts, cudaStream_t s);
+// gather_assignments: u16 topics by slot -> u32 topics in corpus order.
+cudaError_t launch_assignments(const uint16_t* z, const uint32_t* input_of_slot, uint64_t T, uint32_t* out,
+                               cudaStream_t s);
 cudaError_t launch_recount(const uint2* tok, const Unit* units, uint32_t n_units,
                            const uint16_t* z, uint32_t* B, uint32_t K_pad, cudaStream_t s);
 

@@ -194,7 +194,29 @@ PYBIND11_MODULE(_core, m) {
              [](const ModelState& s) { return matrix(s.word_topic(), s.vocab_size, s.num_topics); })
         .def("word_topic_prob",
              [](const ModelState& s) { return matrix(s.word_topic_prob(), s.vocab_size, s.num_topics); })
-        .def("assignments", [](const ModelState& s) { return vec(s.gather_assignments()); })
+        .def("assignments",
+             [](const ModelState& s, py::object out) -> py::object {
+                 // gather_assignments (trainer.cpp:203-213), written straight into a numpy
+                 // buffer (optionally a caller-provided, e.g. pinned, one).
+                 if (!s.has_chunks()) throw ValidationError("model carries no chunks (loaded from a checkpoint)");
+                 py::array_t<std::uint32_t, py::array::c_style> a;
+                 if (out.is_none()) {
+                     a = py::array_t<std::uint32_t>(static_cast<py::ssize_t>(s.num_tokens));
+                 } else {
+                     if (!py::array_t<std::uint32_t, py::array::c_style>::check_(out))
+                         throw ValidationError("out must be a C-contiguous uint32 array");
+                     a = py::reinterpret_borrow<py::array_t<std::uint32_t, py::array::c_style>>(out);
+                     if (a.size() != static_cast<py::ssize_t>(s.num_tokens) || !a.writeable())
+                         throw ValidationError("out must be a writeable uint32 array of num_tokens elements");
+                 }
+                 std::uint32_t* ptr = a.mutable_data();
+                 {
+                     py::gil_scoped_release release;
+                     check(slda_get_assignments(s.engine(), ptr));
+                 }
+                 return a;
+             },
+             py::arg("out") = py::none())
         .def("run_iteration", &run_iteration, py::arg("config"), py::call_guard<py::gil_scoped_release>())
         .def("save", [](const ModelState& s, const std::string& path) { save_checkpoint(path, s); })
         .def_static("load",
