@@ -269,6 +269,8 @@ def main() -> None:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
+    assign_out = torch.empty(T_shard, dtype=torch.int32, pin_memory=True).numpy().view(np.uint32)
+
     # ---- e2e: public API from pinned host buffers: H2D + device PDOW/init + K iterations
     # + D2H of the assignments (result).
     barrier()
@@ -277,10 +279,9 @@ def main() -> None:
                            1 if world > 1 else 0)
     for _ in range(args.steps):
         model.run_iteration(tc)
-    assignments = model.assignments()
+    model.assignments(assign_out)
     torch.cuda.synchronize()
     e2e_s = max_over_ranks(time.perf_counter() - t0)
-    del assignments
 
     # ---- device-timed: W warm-up iterations, then exactly K timed iterations.
     stream = torch.cuda.ExternalStream(model.stream_ptr())

@@ -158,6 +158,7 @@ struct slda_engine {
     DevMem tok, z, doc_start, row4, A, units, long_docs, hist_scratch;
     DevMem seg_word, seg_off, seg_len, schedule;  // PDOW getters
     DevMem input_of_slot, ids;                    // only for non doc-major input / explicit ids
+    DevMem assign_buf;                            // gather_assignments staging (allocated on first use)
     DevMem B, bhat, l4, l8, q, colsum, denom, zv, counters;
 
     // Per-iteration phase events, a ring so async iterations can be profiled afterwards.
@@ -447,10 +448,13 @@ void slda_engine::build(const slda_corpus_view& cv, const slda_config& c) {
                                   kl, keys.as<unsigned long long>(), vals.as<uint32_t>(), stream));
         if (T) {
             cub_call([&](void* t, size_t& b) {
+                // Keys are laid out in slot order, which is doc-ascending (slots are doc-grouped),
+                // and the radix sort is stable: sorting on the (word, length) bits alone already
+                // yields (word, length, doc, slot) order -- 4 passes instead of 7 at C3.
                 return cub::DeviceRadixSort::SortPairs(
                     t, b, keys.as<unsigned long long>(), keys_sorted.as<unsigned long long>(),
-                    vals.as<uint32_t>(), slots_sorted.as<uint32_t>(), static_cast<int64_t>(T), 0,
-                    static_cast<int>(wshift + wbits), stream);
+                    vals.as<uint32_t>(), slots_sorted.as<uint32_t>(), static_cast<int64_t>(T),
+                    static_cast<int>(kl.dbits), static_cast<int>(wshift + wbits), stream);
             });
         }
         keys.release();
@@ -479,18 +483,21 @@ void slda_engine::build(const slda_corpus_view& cv, const slda_config& c) {
         CK(slda::launch_segment_lengths(seg_off.as<uint32_t>(), nseg, T, seg_len.as<uint32_t>(),
                                         skeys.as<unsigned long long>(), svals.as<uint32_t>(),
                                         seg_word.as<uint32_t>(), nullptr, stream));
+        phase("  schedule keys");
         cub_call([&](void* t, size_t& b) {
             return cub::DeviceRadixSort::SortPairs(t, b, skeys.as<unsigned long long>(),
                                                    skeys_sorted.as<unsigned long long>(), svals.as<uint32_t>(),
                                                    schedule.as<uint32_t>(), static_cast<int64_t>(nseg), 0, 64,
                                                    stream);
         });
+        phase("  schedule sort");
         counts.alloc(static_cast<size_t>(nseg) * 4, nullptr);
         starts.alloc(static_cast<size_t>(nseg) * 4, nullptr);
         CK(slda::launch_sched_counts(schedule.as<uint32_t>(), seg_len.as<uint32_t>(), nseg,
                                      counts.as<uint32_t>(), stream));
         exclusive_sum(counts.as<uint32_t>(), starts.as<uint32_t>(), nseg);
         n_units = d2h_scalar(starts.as<uint32_t>() + nseg - 1) + d2h_scalar(counts.as<uint32_t>() + nseg - 1);
+        phase("  unit counts");
         units.alloc(static_cast<size_t>(n_units) * sizeof(slda::Unit), &device_bytes);
         CK(slda::launch_emit_units(schedule.as<uint32_t>(), seg_word.as<uint32_t>(), seg_off.as<uint32_t>(),
                                    seg_len.as<uint32_t>(), starts.as<uint32_t>(), nseg,
@@ -857,11 +864,10 @@ int slda_get_assignments(slda_engine* e, uint32_t* out) {
         e->set_device();
         if (e->T == 0) return;
         // Permute/widen on the device, then one D2H straight into the caller's buffer.
-        DevMem d;
-        d.alloc(e->T * 4, nullptr);
+        if (!e->assign_buf.p) e->assign_buf.alloc(e->T * 4, &e->device_bytes);
         CK(slda::launch_assignments(e->z.as<uint16_t>(), e->doc_major ? nullptr : e->input_of_slot.as<uint32_t>(),
-                                    e->T, d.as<uint32_t>(), e->stream));
-        CK(cudaMemcpyAsync(out, d.p, e->T * 4, cudaMemcpyDeviceToHost, e->stream));
+                                    e->T, e->assign_buf.as<uint32_t>(), e->stream));
+        CK(cudaMemcpyAsync(out, e->assign_buf.p, e->T * 4, cudaMemcpyDeviceToHost, e->stream));
         CK(cudaStreamSynchronize(e->stream));
     });
 }

@@ -5,6 +5,9 @@
 #include "common.cuh"
 #include "kernels.hpp"
 
+#include <cstdlib>
+#include <string>
+
 namespace slda {
 
 namespace {
@@ -89,13 +92,16 @@ __device__ __forceinline__ uint32_t tree_search(float x, const float* s_l8, uint
 // Per-warp staging of C_dk rows.  Lane-private random row reads cap at ~1.5 TB/s on B200
 // (L1TEX: one line per lane per load); the warp-cooperative layout (adjacent lanes read
 // adjacent sectors of one row) is coalesced per row and measured at 3.7-6 TB/s
-// (scripts/microbench_rows.cu).  A group is kGroup sectors (16 entries) of each
-// of the warp's 32 rows; the 80-byte row stride keeps the cooperative stores and each
-// lane's 128-bit reads of its own row bank-conflict free.
-constexpr uint32_t kGroup = 2;
-constexpr uint32_t kRowsPerInst = 32 / kGroup;
-constexpr uint32_t kStageRow = 32 * kGroup + 16;
-constexpr uint32_t kStageWarp = 32 * kStageRow;
+// (scripts/microbench_rows.cu).  A group is G sectors (8G entries) of each of the warp's 32
+// rows, loaded by 32/G rows per instruction (scripts/mb_pattern.cu: G=4 moves the same row
+// bytes with ~20% fewer L1TEX wavefronts than G=2).  The (32G+16)-byte row stride keeps the
+// cooperative stores and each lane's 128-bit reads of its own row bank-conflict free.
+template <int G>
+struct Stage {
+    static constexpr uint32_t kRowsPerInst = 32 / G;
+    static constexpr uint32_t kRow = 32 * G + 16;
+    static constexpr uint32_t kWarp = 32 * kRow;
+};
 // Per-sector running sums for the first kCkSectors sectors (96 entries): the prefix pass
 // of the sparse branch re-reads one sector instead of the row.  (12: at K = 10K two
 // 512-thread CTAs fit one SM.)
@@ -106,28 +112,34 @@ __device__ __forceinline__ void sts_sector(unsigned char* p, const Sector& q) {
     *reinterpret_cast<uint4*>(p + 16) = q.hi;
 }
 
-// Cooperative load of sectors [gs, gs + kGroup) of each of the warp's 32 rows (registers),
-// and its store into the stage.  Per row 16j + grp: rq = quad offset, ns = sector limit
-// (0: skip), gs = first sector.
-__device__ __forceinline__ void load_group(const uint4* A4, const uint32_t (&rq)[kGroup], const uint32_t (&ns)[kGroup],
-                                           const uint32_t (&gs)[kGroup], uint32_t sub, Sector (&q)[kGroup]) {
+// Cooperative load of sectors [gs, gs + G) of each of the warp's 32 rows (registers),
+// and its store into the stage.  Per row kRowsPerInst*j + grp: rq = quad offset, ns = sector
+// limit (0: skip), gs = first sector.  Sectors past a row's limit are neither loaded nor
+// stored (the owning lane never reads them), so finished rows cost no L1TEX wavefronts.
+template <int G>
+__device__ __forceinline__ void load_group(const uint4* A4, const uint32_t (&rq)[G], const uint32_t (&ns)[G],
+                                           const uint32_t (&gs)[G], uint32_t sub, Sector (&q)[G]) {
 #pragma unroll
-    for (uint32_t j = 0; j < kGroup; ++j) {
+    for (uint32_t j = 0; j < G; ++j) {
         const uint32_t sec = gs[j] + sub;
         q[j] = sec < ns[j] ? ldg_sector(A4 + rq[j] + 2 * sec) : zero_sector();
     }
 }
-__device__ __forceinline__ void store_group(const Sector (&q)[kGroup], uint32_t sub, uint32_t grp,
-                                            unsigned char* stage) {
-#pragma unroll
-    for (uint32_t j = 0; j < kGroup; ++j) sts_sector(stage + (kRowsPerInst * j + grp) * kStageRow + sub * 32, q[j]);
-}
-__device__ __forceinline__ void stage_group(const uint4* A4, const uint32_t (&rq)[kGroup],
-                                            const uint32_t (&ns)[kGroup], const uint32_t (&gs)[kGroup],
+template <int G>
+__device__ __forceinline__ void store_group(const Sector (&q)[G], const uint32_t (&ns)[G], const uint32_t (&gs)[G],
                                             uint32_t sub, uint32_t grp, unsigned char* stage) {
-    Sector q[kGroup];
-    load_group(A4, rq, ns, gs, sub, q);
-    store_group(q, sub, grp, stage);
+#pragma unroll
+    for (uint32_t j = 0; j < G; ++j)
+        if (gs[j] + sub < ns[j])
+            sts_sector(stage + (Stage<G>::kRowsPerInst * j + grp) * Stage<G>::kRow + sub * 32, q[j]);
+}
+template <int G>
+__device__ __forceinline__ void stage_group(const uint4* A4, const uint32_t (&rq)[G], const uint32_t (&ns)[G],
+                                            const uint32_t (&gs)[G], uint32_t sub, uint32_t grp,
+                                            unsigned char* stage) {
+    Sector q[G];
+    load_group<G>(A4, rq, ns, gs, sub, q);
+    store_group<G>(q, ns, gs, sub, grp, stage);
 }
 
 // ---- Row decoding for the sampler (both row formats) ----------------------------------------
@@ -225,8 +237,9 @@ __device__ __forceinline__ void scan_sector(float& run, bool& need, uint32_t& to
     }
 }
 
-template <int NT, bool kGlobalPhi, bool kCompact>
-__global__ void __launch_bounds__(NT, 65536 / (NT * 64)) sampler_kernel(SamplerArgs a) {
+template <int NT, int G, int MINB, bool kGlobalPhi, bool kCompact>
+__global__ void __launch_bounds__(NT, MINB) sampler_kernel(SamplerArgs a) {
+    using St = Stage<G>;
     extern __shared__ __align__(16) float sm[];
     const uint32_t v = a.units[blockIdx.x].word;
     const float* s_bhat = kGlobalPhi ? a.bhat + static_cast<size_t>(v) * a.K_pad : sm;
@@ -253,12 +266,12 @@ __global__ void __launch_bounds__(NT, 65536 / (NT * 64)) sampler_kernel(SamplerA
     const uint32_t tmask = (1u << tbits) - 1u;
     const uint4* A4 = reinterpret_cast<const uint4*>(a.A);
     float* ck = s_ck + threadIdx.x;
-    // Cooperative layout: lane -> row kRowsPerInst*j + lane%16, sector lane/16.  A quarter
-    // warp then stores 8 different rows at the same sector offset, which the 80-byte row
-    // stride spreads over all 32 banks; the row's two sectors stay one 64-byte segment.
-    const uint32_t lane = lane_id(), sub = lane / kRowsPerInst, grp = lane % kRowsPerInst;
-    unsigned char* stage = s_stage + (threadIdx.x >> 5) * kStageWarp;
-    const unsigned char* mine = stage + lane * kStageRow;  // this lane's staged sectors
+    // Cooperative layout: lane -> row kRowsPerInst*j + lane%kRowsPerInst, sector
+    // lane/kRowsPerInst.  A quarter warp then stores 8 different rows at the same sector
+    // offset, which the (32G+16)-byte row stride spreads over all 32 banks.
+    const uint32_t lane = lane_id(), sub = lane / St::kRowsPerInst, grp = lane % St::kRowsPerInst;
+    unsigned char* stage = s_stage + (threadIdx.x >> 5) * St::kWarp;
+    const unsigned char* mine = stage + lane * St::kRow;  // this lane's staged sectors
     unsigned long long entries = 0;
     __syncthreads();
 
@@ -267,15 +280,15 @@ __global__ void __launch_bounds__(NT, 65536 / (NT * 64)) sampler_kernel(SamplerA
         const uint32_t i = r * NT + threadIdx.x;
         const bool active = i < unit.length;
         const uint2 t = active ? __ldg(a.tok + unit.offset + i) : make_uint2(0u, 0u);  // {row quads, slot}
-        uint32_t rq[kGroup], ns[kGroup], gs[kGroup];
+        uint32_t rq[G], ns[G], gs[G];
 #pragma unroll
-        for (uint32_t j = 0; j < kGroup; ++j) {
-            rq[j] = __shfl_sync(0xffffffffu, t.x, kRowsPerInst * j + grp);
-            ns[j] = __shfl_sync(0xffffffffu, active ? kGroup : 0u, kRowsPerInst * j + grp);  // speculative
+        for (uint32_t j = 0; j < G; ++j) {
+            rq[j] = __shfl_sync(0xffffffffu, t.x, St::kRowsPerInst * j + grp);
+            ns[j] = __shfl_sync(0xffffffffu, active ? G : 0u, St::kRowsPerInst * j + grp);  // speculative
             gs[j] = 0;
         }
         __syncwarp();
-        stage_group(A4, rq, ns, gs, sub, grp, stage);
+        stage_group<G>(A4, rq, ns, gs, sub, grp, stage);
         __syncwarp();
 
         // Wide row = [header (nnz-1, count 0) | entries | zero-count padding to 8]: header and
@@ -283,11 +296,11 @@ __global__ void __launch_bounds__(NT, 65536 / (NT * 64)) sampler_kernel(SamplerA
         const uint32_t w0 = reinterpret_cast<const uint4*>(mine)->x;
         const uint32_t nnz = active ? (kCompact ? w0 >> 16 : (w0 & tmask) + 1u) : 0u;
         const uint32_t nsect = active ? (kCompact ? w0 & 0xFFFFu : (nnz + 8u) >> 3) : 0u;
-        const uint32_t ngroups = (nsect + kGroup - 1) / kGroup;
         entries += nnz;
-        const uint32_t max_groups = __reduce_max_sync(0xffffffffu, ngroups);
 #pragma unroll
-        for (uint32_t j = 0; j < kGroup; ++j) ns[j] = __shfl_sync(0xffffffffu, nsect, kRowsPerInst * j + grp);
+        for (uint32_t j = 0; j < G; ++j) ns[j] = __shfl_sync(0xffffffffu, nsect, St::kRowsPerInst * j + grp);
+        const uint32_t ngroups = (nsect + G - 1) / G;
+        const uint32_t max_groups = __reduce_max_sync(0xffffffffu, ngroups);
 
         float ub = 0.0f, up = 0.0f;
         if (active) {
@@ -299,16 +312,16 @@ __global__ void __launch_bounds__(NT, 65536 / (NT * 64)) sampler_kernel(SamplerA
         // Group g+1 is loaded into registers while group g is consumed from the stage.
         float s = 0.0f;
         for (uint32_t g = 0; g < max_groups; ++g) {
-            Sector next[kGroup];
+            Sector next[G];
             const bool more = g + 1 < max_groups;
             if (more) {
 #pragma unroll
-                for (uint32_t j = 0; j < kGroup; ++j) gs[j] = kGroup * (g + 1);
-                load_group(A4, rq, ns, gs, sub, next);
+                for (uint32_t j = 0; j < G; ++j) gs[j] = G * (g + 1);
+                load_group<G>(A4, rq, ns, gs, sub, next);
             }
 #pragma unroll
-            for (uint32_t u = 0; u < kGroup; ++u) {
-                const uint32_t sec = kGroup * g + u;
+            for (uint32_t u = 0; u < G; ++u) {
+                const uint32_t sec = G * g + u;
                 if (sec < nsect) {
                     s = acc_sector<kGlobalPhi, kCompact>(s, mine + 32 * u, sec, tbits, tmask, s_bhat);
                     if (sec < kCkSectors) ck[sec * NT] = s;
@@ -316,7 +329,7 @@ __global__ void __launch_bounds__(NT, 65536 / (NT * 64)) sampler_kernel(SamplerA
             }
             if (more) {
                 __syncwarp();
-                store_group(next, sub, grp, stage);
+                store_group<G>(next, ns, gs, sub, grp, stage);
                 __syncwarp();
             }
         }
@@ -360,12 +373,12 @@ __global__ void __launch_bounds__(NT, 65536 / (NT * 64)) sampler_kernel(SamplerA
             const uint32_t first = need ? sec : 0u;
             const uint32_t lim = need ? sec + 1 : 0u;
 #pragma unroll
-            for (uint32_t j = 0; j < kGroup; ++j) {
-                gs[j] = __shfl_sync(0xffffffffu, first, kRowsPerInst * j + grp);
-                ns[j] = __shfl_sync(0xffffffffu, lim, kRowsPerInst * j + grp);
+            for (uint32_t j = 0; j < G; ++j) {
+                gs[j] = __shfl_sync(0xffffffffu, first, St::kRowsPerInst * j + grp);
+                ns[j] = __shfl_sync(0xffffffffu, lim, St::kRowsPerInst * j + grp);
             }
             __syncwarp();
-            stage_group(A4, rq, ns, gs, sub, grp, stage);
+            stage_group<G>(A4, rq, ns, gs, sub, grp, stage);
             __syncwarp();
             if (need) {
                 scan_sector<kGlobalPhi, kCompact>(run, need, topic, xs, mine, sec, tbits, tmask, s_bhat);
@@ -384,36 +397,60 @@ __global__ void __launch_bounds__(NT, 65536 / (NT * 64)) sampler_kernel(SamplerA
     }
 }
 
-size_t sampler_smem(const SamplerArgs& a, int nt, bool global_phi) {
+size_t sampler_smem(const SamplerArgs& a, int nt, int g, bool global_phi) {
+    const size_t stage_row = 32u * static_cast<size_t>(g) + 16u;
     return sizeof(float) * ((global_phi ? 0 : static_cast<size_t>(a.K_pad)) + a.l8_stride) +
-           (sizeof(float) * kCkSectors + kStageRow) * static_cast<size_t>(nt);
+           (sizeof(float) * kCkSectors + stage_row) * static_cast<size_t>(nt);
 }
 
-template <int NT, bool G, bool C>
+template <int NT, int G, int MINB, bool Gl, bool C>
 cudaError_t launch_sampler_t(const SamplerArgs& a, uint32_t n_units, cudaStream_t s) {
     static bool configured = false;
     if (!configured) {
-        cudaFuncSetAttribute(sampler_kernel<NT, G, C>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+        cudaFuncSetAttribute(sampler_kernel<NT, G, MINB, Gl, C>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             227 * 1024);
         configured = true;
     }
-    sampler_kernel<NT, G, C><<<n_units, NT, sampler_smem(a, NT, G), s>>>(a);
+    sampler_kernel<NT, G, MINB, Gl, C><<<n_units, NT, sampler_smem(a, NT, G, Gl), s>>>(a);
     return cudaGetLastError();
 }
 
+// Launch shape (SLDA_SAMPLER overrides for experiments; default by phi row size):
+//   "g2"     : 256/512-thread CTAs, 2-sector groups, 64 registers (two 512-thread CTAs / SM)
+//   "g4"     : 256-thread CTAs, 4-sector groups, up to 128 registers
+//   "g4x512" : 512-thread CTAs, 4-sector groups (one CTA / SM at K = 10K)
 cudaError_t launch_sampler(const SamplerArgs& a, uint32_t n_units, cudaStream_t s) {
     if (n_units == 0) return cudaSuccess;
     const size_t phi_bytes = sizeof(float) * (static_cast<size_t>(a.K_pad) + a.l8_stride);
+    static const int env_shape = [] {
+        const char* e = std::getenv("SLDA_SAMPLER");
+        if (!e) return -1;
+        const std::string v(e);
+        return v == "g4" ? 1 : v == "g4x512" ? 2 : 0;
+    }();
+    // Default: 4-sector groups for large phi rows (C3 K=10K: 103 vs 114 ms), 2-sector groups
+    // with four 256-thread CTAs per SM for small rows (C2 K=1K: 24.0 vs 30.8 ms).
+    const int shape = env_shape >= 0 ? env_shape : (phi_bytes > 24 * 1024 ? 1 : 0);
+    const bool fits512 = sampler_smem(a, 512, 2, false) <= 227 * 1024;
+    if (!fits512) {
+        // Rows that do not fit shared memory (K > kCompactMaxK, so always the wide format):
+        // gather phi through L1/L2.
+        if (a.compact) return cudaErrorInvalidConfiguration;
+        return launch_sampler_t<512, 2, 2, true, false>(a, n_units, s);
+    }
+    if (shape == 1 && sampler_smem(a, 256, 4, false) <= 227 * 1024)
+        return a.compact ? launch_sampler_t<256, 4, 2, false, true>(a, n_units, s)
+                         : launch_sampler_t<256, 4, 2, false, false>(a, n_units, s);
+    if (shape == 2 && sampler_smem(a, 512, 4, false) <= 227 * 1024)
+        return a.compact ? launch_sampler_t<512, 4, 1, false, true>(a, n_units, s)
+                         : launch_sampler_t<512, 4, 1, false, false>(a, n_units, s);
     // Small phi rows: 256-thread CTAs.  Large (K = 10K): 512 threads share one staged row
-    // (2 CTAs x 16 warps per SM).  Rows that do not fit shared memory (K > kCompactMaxK,
-    // so always the wide row format): gather phi through L1/L2.
+    // (2 CTAs x 16 warps per SM).
     if (phi_bytes <= 24 * 1024)
-        return a.compact ? launch_sampler_t<256, false, true>(a, n_units, s)
-                         : launch_sampler_t<256, false, false>(a, n_units, s);
-    if (sampler_smem(a, 512, false) <= 227 * 1024)
-        return a.compact ? launch_sampler_t<512, false, true>(a, n_units, s)
-                         : launch_sampler_t<512, false, false>(a, n_units, s);
-    if (a.compact) return cudaErrorInvalidConfiguration;
-    return launch_sampler_t<512, true, false>(a, n_units, s);
+        return a.compact ? launch_sampler_t<256, 2, 4, false, true>(a, n_units, s)
+                         : launch_sampler_t<256, 2, 4, false, false>(a, n_units, s);
+    return a.compact ? launch_sampler_t<512, 2, 2, false, true>(a, n_units, s)
+                     : launch_sampler_t<512, 2, 2, false, false>(a, n_units, s);
 }
 
 // ============================================================================
