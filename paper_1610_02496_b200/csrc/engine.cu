@@ -150,6 +150,8 @@ struct slda_engine {
     uint32_t nseg = 0, n_units = 0, n_long = 0;
     bool doc_major = true;
     bool compact = false;  // C_dk row format (kernels.cu: compact 16-bit slots or wide 32-bit)
+    int sampler_shape = -1;  // SLDA_SAMPLER (kernels.cu launch_sampler); -1 = default by K
+    bool ssc_sort = false;   // SLDA_SSC=sort: the bitonic-sort SSC instead of the bitmap one
     uint32_t wshift = 0;  // word field shift of the execution-order key
     size_t device_bytes = 0;
     uint64_t nnz = 0;
@@ -381,6 +383,8 @@ void slda_engine::build(const slda_corpus_view& cv, const slda_config& c) {
     // short-document corpora at large K (C3: 131 vs 139 ms/iteration) but loses where the
     // sampler is issue-bound or documents are long (C2 42.7 vs 31.0, C5 K=10K 88.9 vs 55.5;
     // DESIGN.md §6).
+    if (const char* f = std::getenv("SLDA_SAMPLER")) sampler_shape = slda::sampler_shape_from_name(f);
+    if (const char* f = std::getenv("SLDA_SSC")) ssc_sort = std::string(f) == "sort";
     compact = false;
     if (const char* f = std::getenv("SLDA_ROW_FORMAT")) {
         if (std::string(f) == "compact")
@@ -568,6 +572,7 @@ void slda_engine::ssc() {
     s.n_long = n_long;
     s.hist_scratch = hist_scratch.as<uint32_t>();
     s.nnz_total = nnz_counter();
+    s.use_sort = ssc_sort ? 1u : 0u;
     CK(slda::launch_ssc(s, stream));
     launches += (D > 0) + (n_long > 0);
 }
@@ -643,6 +648,7 @@ void slda_engine::enqueue_iteration() {
     a.tbits = tbits;
     a.compact = compact ? 1u : 0u;
     a.row_entries = entries_counter();
+    a.shape = sampler_shape;
     CK(slda::launch_sampler(a, n_units, stream));
     launches += n_units > 0;
     CK(cudaEventRecord(ev[2], stream));

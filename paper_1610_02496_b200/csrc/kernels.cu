@@ -397,6 +397,254 @@ __global__ void __launch_bounds__(NT, MINB) sampler_kernel(SamplerArgs a) {
     }
 }
 
+// ---- K3' streaming sampler: the same draws, bit for bit, with lane refill -----------------------
+// The round-based kernel above advances a warp's 32 tokens in lock step: every round waits for
+// its longest row, re-reads the crossing sector with a second dependent round trip, and loads a
+// speculative group for every row.  Here each lane owns a sequence of tokens instead: the
+// warp streams G-sector groups of its lanes' CURRENT rows (cooperative, coalesced, next group
+// prefetched in registers); a lane whose row ends takes the next token of the unit at once
+// (warp ballot over a 32-token pool, CTA-wide dynamic batches), so the stream never waits for
+// the longest row.  The branch decision needs the whole row (S), so a finished token's last
+// step is deferred by one step: the one sector it still needs -- the sparse branch's crossing
+// sector (found from the per-sector checkpoints) or the tree branch's L4 block -- is loaded
+// lane-private in step t and resolved in step t+1, under the next step's consumption.
+// Arithmetic (make_branch_context, prefix_search, WaryTree::sample) is unchanged.
+template <int NT, int G>
+__global__ void __launch_bounds__(NT, NT <= 128 ? 3 : 2) sampler_stream_kernel(SamplerArgs a) {
+    using St = Stage<G>;
+    extern __shared__ __align__(16) float sm[];
+    __shared__ uint32_t s_next;  // next unclaimed 32-token batch (index within the unit)
+    const Unit unit = a.units[blockIdx.x];
+    const uint32_t v = unit.word;
+    float* s_bhat = sm;
+    float* s_l8 = sm + a.K_pad;
+    float* s_ck = s_l8 + a.l8_stride;  // [kCkSectors][NT]
+    unsigned char* s_stage = reinterpret_cast<unsigned char*>(s_ck + kCkSectors * NT);
+    const float* l4row = a.l4 + static_cast<size_t>(v) * a.K_pad;
+    const float total = __ldg(l4row + a.K_pad - 1);
+    {
+        const float4* gb = reinterpret_cast<const float4*>(a.bhat + static_cast<size_t>(v) * a.K_pad);
+        float4* sb = reinterpret_cast<float4*>(sm);
+        for (uint32_t i = threadIdx.x; i < a.K_pad / 4; i += NT) sb[i] = __ldg(gb + i);
+        const float4* gl = reinterpret_cast<const float4*>(a.l8 + static_cast<size_t>(v) * a.l8_stride);
+        float4* sl = reinterpret_cast<float4*>(s_l8);
+        for (uint32_t i = threadIdx.x; i < a.l8_stride / 4; i += NT) sl[i] = __ldg(gl + i);
+    }
+    if (threadIdx.x == 0) s_next = NT;  // warp w starts with batch [32w, 32w + 32)
+    const float qv = __ldg(a.q + v);
+    uint32_t* brow = a.B + static_cast<size_t>(v) * a.K_pad;
+    const uint32_t tbits = a.tbits, tmask = (1u << tbits) - 1u;
+    const uint4* A4 = reinterpret_cast<const uint4*>(a.A);
+    const uint2* toks = a.tok + unit.offset;
+    const uint32_t len = unit.length;
+    const uint32_t lane = lane_id(), sub = lane / St::kRowsPerInst, grp = lane % St::kRowsPerInst;
+    unsigned char* stage = s_stage + (threadIdx.x >> 5) * St::kWarp;
+    const unsigned char* mine = stage + lane * St::kRow;
+    float* ck = s_ck + threadIdx.x;
+    unsigned long long entries = 0;
+    __syncthreads();
+
+    // Token pool: pool = batch at pool_base (lane l holds token pool_base + l), nxt = the batch
+    // after it; pc = tokens of the pool already handed out.
+    uint32_t pool_base = (threadIdx.x >> 5) * 32u;
+    uint2 pool = pool_base + lane < len ? __ldg(toks + pool_base + lane) : make_uint2(0u, 0u);
+    auto claim = [&]() -> uint32_t {
+        uint32_t b = 0;
+        if (lane == 0) b = atomicAdd(&s_next, 32u);
+        return __shfl_sync(0xffffffffu, b, 0);
+    };
+    uint32_t next_base = claim();
+    uint2 nxt = next_base + lane < len ? __ldg(toks + next_base + lane) : make_uint2(0u, 0u);
+    uint32_t pc = 0;
+
+    // Current row (the one staged this step).
+    bool cur = false, hdr = false;  // hdr: the staged group is the row's first (header unread)
+    uint32_t c_rq = 0, c_slot = 0, c_ns = 0, c_base = 0;
+    float s = 0.0f;
+    // Pending resolution: 0 none, 1 sparse (scan sector p_sec from run p_run for xs), 2 tree
+    // (L4 block p_sec), 3 sparse with xs == 0 (the first real entry).
+    uint32_t p_kind = 0, p_slot = 0, p_sec = 0, p_rq = 0, p_ns = 0;
+    float p_run = 0.0f, p_x = 0.0f;
+    Sector psec = zero_sector();
+
+    // Hands out tokens to the lanes in `need` (ballot), in lane order.
+    auto take = [&](bool want, uint32_t& rq, uint32_t& slot) -> bool {
+        const uint32_t need = __ballot_sync(0xffffffffu, want);
+        const uint32_t idx = pc + __popc(need & ((1u << lane) - 1u));
+        const uint2 ra = make_uint2(__shfl_sync(0xffffffffu, pool.x, idx & 31u),
+                                    __shfl_sync(0xffffffffu, pool.y, idx & 31u));
+        const uint2 rb = make_uint2(__shfl_sync(0xffffffffu, nxt.x, idx & 31u),
+                                    __shfl_sync(0xffffffffu, nxt.y, idx & 31u));
+        const uint32_t gi = idx < 32u ? pool_base + idx : next_base + (idx - 32u);
+        const bool got = want && idx < 64u && gi < len;
+        rq = idx < 32u ? ra.x : rb.x;
+        slot = idx < 32u ? ra.y : rb.y;
+        pc += __popc(need);
+        if (pc >= 32u) {  // pool consumed: the next batch becomes the pool
+            pc -= 32u;
+            pool = nxt;
+            pool_base = next_base;
+            next_base = claim();
+            nxt = next_base + lane < len ? __ldg(toks + next_base + lane) : make_uint2(0u, 0u);
+        }
+        return got;
+    };
+
+    // First tokens and their first groups.
+    uint32_t t_rq = 0, t_slot = 0;
+    cur = take(true, t_rq, t_slot);
+    c_rq = t_rq;
+    c_slot = t_slot;
+    hdr = cur;
+    {
+        uint32_t rq[G], ns[G], gs[G];
+#pragma unroll
+        for (uint32_t j = 0; j < G; ++j) {
+            rq[j] = __shfl_sync(0xffffffffu, c_rq, St::kRowsPerInst * j + grp);
+            ns[j] = __shfl_sync(0xffffffffu, cur ? G : 0u, St::kRowsPerInst * j + grp);
+            gs[j] = 0;
+        }
+        stage_group<G>(A4, rq, ns, gs, sub, grp, stage);
+        __syncwarp();
+    }
+
+    while (__any_sync(0xffffffffu, cur || p_kind != 0)) {
+        // Header of a row whose first group is staged: [nnz-1 | entries | zero pad].
+        if (cur && hdr) {
+            const uint32_t nnz = (reinterpret_cast<const uint4*>(mine)->x & tmask) + 1u;
+            c_ns = (nnz + 8u) >> 3;
+            entries += nnz;
+            hdr = false;
+        }
+        // Next step's group per lane: the rest of this row, or the first group of a new token.
+        const bool ends = cur && c_base + G >= c_ns;
+        uint32_t n_rq = 0, n_slot = 0;
+        const bool got = take(ends, n_rq, n_slot);
+        uint32_t l_rq = 0, l_start = 0, l_lim = 0;
+        if (cur && !ends) {
+            l_rq = c_rq; l_start = c_base + G; l_lim = c_ns;
+        } else if (got) {
+            l_rq = n_rq; l_start = 0; l_lim = G;  // speculative first group (header inside)
+        }
+        uint32_t rq[G], ns[G], gs[G];
+#pragma unroll
+        for (uint32_t j = 0; j < G; ++j) {
+            const uint32_t src = St::kRowsPerInst * j + grp;
+            rq[j] = __shfl_sync(0xffffffffu, l_rq, src);
+            gs[j] = __shfl_sync(0xffffffffu, l_start, src);
+            ns[j] = __shfl_sync(0xffffffffu, l_lim, src);
+        }
+        Sector nx[G];
+        load_group<G>(A4, rq, ns, gs, sub, nx);
+
+        // make_branch_context over this step's sectors (sequential f32 chain).
+        if (cur) {
+#pragma unroll
+            for (uint32_t u = 0; u < G; ++u) {
+                const uint32_t sec = c_base + u;
+                if (sec < c_ns) {
+                    s = acc_sector<false, false>(s, mine + 32 * u, sec, tbits, tmask, s_bhat);
+                    if (sec < kCkSectors) ck[sec * NT] = s;
+                }
+            }
+        }
+
+        // Resolve the token finished in the previous step (its sector arrived meanwhile).
+        if (p_kind != 0) {
+            uint32_t topic;
+            if (p_kind == 2) {
+                const float x = p_x;
+                const uint32_t below = (__uint_as_float(psec.lo.x) < x) + (__uint_as_float(psec.lo.y) < x) +
+                                       (__uint_as_float(psec.lo.z) < x) + (__uint_as_float(psec.lo.w) < x) +
+                                       (__uint_as_float(psec.hi.x) < x) + (__uint_as_float(psec.hi.y) < x) +
+                                       (__uint_as_float(psec.hi.z) < x) + (__uint_as_float(psec.hi.w) < x);
+                const uint32_t k = p_sec * kLeaf + below;
+                topic = k < a.K ? k : a.K - 1;
+            } else if (p_kind == 3) {
+                topic = psec.lo.y & tmask;  // word 1 of sector 0: the first real entry
+            } else {
+                // prefix_search (sampler.hpp:18-41) from the checkpoint: first running sum >= xs.
+                float run = p_run;
+                bool need = true;
+                topic = 0;
+                uint32_t sec = p_sec;
+                Sector q = psec;
+                while (true) {
+                    const uint32_t es[8] = {q.lo.x, q.lo.y, q.lo.z, q.lo.w, q.hi.x, q.hi.y, q.hi.z, q.hi.w};
+#pragma unroll
+                    for (int w = 0; w < 8; ++w) {
+                        run = __fadd_rn(run, entry_mass<false>(es[w], tbits, tmask, s_bhat));
+                        if (need && run >= p_x) { topic = es[w] & tmask; need = false; }
+                    }
+                    if (!need || ++sec >= p_ns) break;
+                    q = ldg_sector(A4 + p_rq + 2 * sec);  // crossing beyond the checkpoints (rare)
+                }
+            }
+            a.z[p_slot] = static_cast<uint16_t>(topic);
+            atomicAdd(brow + topic, 1u);
+            p_kind = 0;
+        }
+
+        // A finished row: sample_token (sampler.hpp:183-204) up to its last sector read.
+        if (ends) {
+            float ub, up;
+            const uint64_t id = a.ids ? __ldg(a.ids + c_slot) : a.id_base + c_slot;
+            draw2_f32(a.seed, a.stream_kind, id, ub, up);
+            p_slot = c_slot;
+            if (ub < __fdiv_rn(s, __fadd_rn(s, qv))) {
+                const float xs = __fmul_rn(up, s);
+                if (xs == 0.0f) {
+                    p_kind = 3;
+                    p_sec = 0;
+                    psec = ldg_sector(A4 + c_rq);
+                } else {
+                    const uint32_t stored = c_ns < kCkSectors ? c_ns : kCkSectors;
+                    uint32_t lo = 0, hi = stored;  // first checkpoint >= xs (or stored)
+                    while (lo < hi) {
+                        const uint32_t mid = (lo + hi) >> 1;
+                        if (ck[mid * NT] >= xs) hi = mid; else lo = mid + 1;
+                    }
+                    p_kind = 1;
+                    p_sec = lo;
+                    p_run = lo > 0 ? ck[(lo - 1) * NT] : 0.0f;
+                    p_x = xs;
+                    p_rq = c_rq;
+                    p_ns = c_ns;
+                    psec = ldg_sector(A4 + c_rq + 2 * lo);
+                }
+            } else {
+                float x = __fmul_rn(up, total);  // WaryTree::sample(p * total)
+                if (!(x <= total)) x = total;
+                uint32_t lo = 0, hi = a.n_l8 - 1;
+                while (lo < hi) {
+                    const uint32_t mid = (lo + hi) >> 1;
+                    if (s_l8[mid] >= x) hi = mid; else lo = mid + 1;
+                }
+                p_kind = 2;
+                p_sec = lo;
+                p_x = x;
+                psec = ldg_sector(reinterpret_cast<const uint4*>(l4row + lo * kLeaf));
+            }
+            // The next token (if any) starts with the group loaded above.
+            cur = got;
+            c_rq = n_rq;
+            c_slot = n_slot;
+            c_base = 0;
+            hdr = got;
+            s = 0.0f;
+        } else if (cur) {
+            c_base += G;
+        }
+        __syncwarp();
+        store_group<G>(nx, ns, gs, sub, grp, stage);
+        __syncwarp();
+    }
+    if (a.row_entries) {
+        for (int o = 16; o > 0; o >>= 1) entries += __shfl_xor_sync(0xffffffffu, entries, o);
+        if (lane == 0) atomicAdd(a.row_entries, entries);
+    }
+}
+
 size_t sampler_smem(const SamplerArgs& a, int nt, int g, bool global_phi) {
     const size_t stage_row = 32u * static_cast<size_t>(g) + 16u;
     return sizeof(float) * ((global_phi ? 0 : static_cast<size_t>(a.K_pad)) + a.l8_stride) +
@@ -415,6 +663,25 @@ cudaError_t launch_sampler_t(const SamplerArgs& a, uint32_t n_units, cudaStream_
     return cudaGetLastError();
 }
 
+template <int NT, int G>
+cudaError_t launch_stream_t(const SamplerArgs& a, uint32_t n_units, cudaStream_t s) {
+    static bool configured = false;
+    if (!configured) {
+        // 227 KB per block minus the kernel's static shared memory (the batch counter).
+        const cudaError_t e = cudaFuncSetAttribute(sampler_stream_kernel<NT, G>,
+                                                   cudaFuncAttributeMaxDynamicSharedMemorySize, 226 * 1024);
+        if (e != cudaSuccess) return e;
+        configured = true;
+    }
+    sampler_stream_kernel<NT, G><<<n_units, NT, sampler_smem(a, NT, G, false), s>>>(a);
+    return cudaGetLastError();
+}
+
+int sampler_shape_from_name(const char* name) {
+    const std::string v(name ? name : "");
+    return v == "g2" ? 0 : v == "g4" ? 1 : v == "g4x512" ? 2 : v == "s4" ? 3 : v == "s2" ? 4 : v == "s4x128" ? 5 : -1;
+}
+
 // Launch shape (SLDA_SAMPLER overrides for experiments; default by phi row size):
 //   "g2"     : 256/512-thread CTAs, 2-sector groups, 64 registers (two 512-thread CTAs / SM)
 //   "g4"     : 256-thread CTAs, 4-sector groups, up to 128 registers
@@ -422,15 +689,7 @@ cudaError_t launch_sampler_t(const SamplerArgs& a, uint32_t n_units, cudaStream_
 cudaError_t launch_sampler(const SamplerArgs& a, uint32_t n_units, cudaStream_t s) {
     if (n_units == 0) return cudaSuccess;
     const size_t phi_bytes = sizeof(float) * (static_cast<size_t>(a.K_pad) + a.l8_stride);
-    static const int env_shape = [] {
-        const char* e = std::getenv("SLDA_SAMPLER");
-        if (!e) return -1;
-        const std::string v(e);
-        return v == "g4" ? 1 : v == "g4x512" ? 2 : 0;
-    }();
-    // Default: 4-sector groups for large phi rows (C3 K=10K: 103 vs 114 ms), 2-sector groups
-    // with four 256-thread CTAs per SM for small rows (C2 K=1K: 24.0 vs 30.8 ms).
-    const int shape = env_shape >= 0 ? env_shape : (phi_bytes > 24 * 1024 ? 1 : 0);
+    const int shape = a.shape >= 0 ? a.shape : (phi_bytes > 24 * 1024 ? 1 : 0);
     const bool fits512 = sampler_smem(a, 512, 2, false) <= 227 * 1024;
     if (!fits512) {
         // Rows that do not fit shared memory (K > kCompactMaxK, so always the wide format):
@@ -438,6 +697,12 @@ cudaError_t launch_sampler(const SamplerArgs& a, uint32_t n_units, cudaStream_t 
         if (a.compact) return cudaErrorInvalidConfiguration;
         return launch_sampler_t<512, 2, 2, true, false>(a, n_units, s);
     }
+    if (!a.compact && shape == 3 && sampler_smem(a, 256, 4, false) <= 227 * 1024)
+        return launch_stream_t<256, 4>(a, n_units, s);
+    if (!a.compact && shape == 4 && sampler_smem(a, 256, 2, false) <= 227 * 1024)
+        return launch_stream_t<256, 2>(a, n_units, s);
+    if (!a.compact && shape == 5 && sampler_smem(a, 128, 4, false) <= 227 * 1024)
+        return launch_stream_t<128, 4>(a, n_units, s);
     if (shape == 1 && sampler_smem(a, 256, 4, false) <= 227 * 1024)
         return a.compact ? launch_sampler_t<256, 4, 2, false, true>(a, n_units, s)
                          : launch_sampler_t<256, 4, 2, false, false>(a, n_units, s);
@@ -638,6 +903,137 @@ __global__ void __launch_bounds__(kSscWarps * 32) ssc_warp_kernel(SscArgs a) {
     if (lane == 0 && nnz_acc) atomicAdd(a.nnz_total, nnz_acc);
 }
 
+// SSC without a sort (wide rows): a two-level topic bitmap per warp.  Setting one bit per
+// token in a K-bit map (and one per 32-topic word in a K/32-bit summary) and reading the
+// map back in order yields the document's distinct topics in ascending order; each token's
+// rank among them is a popcount, so the counts are smem atomics at that rank.  Per document
+// this costs O(len + nnz) warp steps instead of the bitonic sort's O(len log^2 len), and
+// the order-free integer counts are identical to segmented_count's (counts.cpp:65-94).
+struct SscBitmapSmem {
+    uint32_t* bm0;    // K_pad/32 words (bit k = topic k present), all zero between documents
+    uint32_t* bm1;    // ceil(K_pad/1024) words (bit w = bm0[w] != 0)
+    uint16_t* wpre;   // per bm0 word: rank of its first topic
+    uint16_t* wlist;  // non-empty bm0 words in ascending order
+    uint16_t* tlist;  // distinct topics in ascending order
+    uint32_t* cnt;    // count per rank
+};
+
+__device__ __forceinline__ uint32_t warp_incl_scan(uint32_t x, uint32_t lane) {
+#pragma unroll
+    for (uint32_t o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    return x;
+}
+
+template <int R>
+__device__ __forceinline__ uint32_t ssc_doc_bitmap(const uint16_t* z, uint32_t n, uint32_t lane,
+                                                   const SscBitmapSmem& w, uint32_t n1, uint32_t* out_row,
+                                                   uint32_t tbits) {
+    uint32_t key[R];
+#pragma unroll
+    for (uint32_t r = 0; r < R; ++r) {
+        const uint32_t i = r * 32 + lane;
+        key[r] = i < n ? static_cast<uint32_t>(z[i]) : 0xFFFFFFFFu;
+        if (key[r] != 0xFFFFFFFFu) {
+            atomicOr(w.bm0 + (key[r] >> 5), 1u << (key[r] & 31u));
+            atomicOr(w.bm1 + (key[r] >> 10), 1u << ((key[r] >> 5) & 31u));
+        }
+    }
+    __syncwarp();
+    // Non-empty bm0 words in ascending order (and clear the summary).
+    uint32_t m = 0;
+    for (uint32_t b = 0; b < n1; b += 32) {
+        const uint32_t wi = b + lane;
+        const uint32_t bits0 = wi < n1 ? w.bm1[wi] : 0u;
+        const uint32_t c = __popc(bits0);
+        const uint32_t incl = warp_incl_scan(c, lane);
+        uint32_t pos = m + incl - c;
+        for (uint32_t bits = bits0; bits; bits &= bits - 1u) w.wlist[pos++] = static_cast<uint16_t>((wi << 5) | (__ffs(bits) - 1));
+        if (bits0) w.bm1[wi] = 0u;
+        m += __shfl_sync(0xffffffffu, incl, 31);
+    }
+    __syncwarp();
+    // Distinct topics in order, and each word's first rank.
+    uint32_t nnz = 0;
+    for (uint32_t b = 0; b < m; b += 32) {
+        const uint32_t e = b + lane;
+        const uint32_t wi = e < m ? w.wlist[e] : 0u;
+        const uint32_t bits0 = e < m ? w.bm0[wi] : 0u;
+        const uint32_t c = __popc(bits0);
+        const uint32_t incl = warp_incl_scan(c, lane);
+        uint32_t pos = nnz + incl - c;
+        if (e < m) w.wpre[wi] = static_cast<uint16_t>(pos);
+        for (uint32_t bits = bits0; bits; bits &= bits - 1u) {
+            w.tlist[pos] = static_cast<uint16_t>((wi << 5) | (__ffs(bits) - 1));
+            w.cnt[pos++] = 0u;
+        }
+        nnz += __shfl_sync(0xffffffffu, incl, 31);
+    }
+    __syncwarp();
+#pragma unroll
+    for (uint32_t r = 0; r < R; ++r) {
+        if (key[r] != 0xFFFFFFFFu) {
+            const uint32_t wi = key[r] >> 5;
+            const uint32_t rank = w.wpre[wi] + __popc(w.bm0[wi] & ((1u << (key[r] & 31u)) - 1u));
+            atomicAdd(w.cnt + rank, 1u);
+        }
+    }
+    __syncwarp();
+#pragma unroll
+    for (uint32_t r = 0; r < R; ++r)
+        if (key[r] != 0xFFFFFFFFu) w.bm0[key[r] >> 5] = 0u;
+    for (uint32_t e = lane; e < nnz; e += 32) out_row[1 + e] = static_cast<uint32_t>(w.tlist[e]) | (w.cnt[e] << tbits);
+    const uint32_t padded = (nnz + 8u) & ~7u;
+    for (uint32_t e = nnz + 1 + lane; e < padded; e += 32) out_row[e] = 0u;
+    if (lane == 0) out_row[0] = nnz - 1u;
+    __syncwarp();
+    return nnz;
+}
+
+constexpr uint32_t kSscBmWarps = 8;
+
+__host__ __device__ inline size_t ssc_bitmap_warp_bytes(uint32_t K_pad) {
+    const size_t n0 = (K_pad + 31u) / 32u, n1 = (n0 + 31u) / 32u;
+    const size_t b = 4 * n0 + 4 * n1 + 2 * n0 + 2 * kSscWarpCap + 2 * kSscWarpCap + 4 * kSscWarpCap;
+    return (b + 15u) & ~static_cast<size_t>(15u);
+}
+
+__global__ void __launch_bounds__(kSscBmWarps * 32) ssc_bitmap_kernel(SscArgs a) {
+    extern __shared__ __align__(16) unsigned char s_raw[];
+    const uint32_t wid = threadIdx.x >> 5, lane = lane_id();
+    const uint32_t n0 = (a.K_pad + 31u) / 32u, n1 = (n0 + 31u) / 32u;
+    const size_t wb = ssc_bitmap_warp_bytes(a.K_pad);
+    unsigned char* base = s_raw + wid * wb;
+    SscBitmapSmem w;
+    w.bm0 = reinterpret_cast<uint32_t*>(base);
+    w.bm1 = w.bm0 + n0;
+    w.cnt = w.bm1 + n1;
+    w.wpre = reinterpret_cast<uint16_t*>(w.cnt + kSscWarpCap);
+    w.wlist = w.wpre + n0;
+    w.tlist = w.wlist + kSscWarpCap;
+    for (uint32_t i = lane; i < n0 + n1; i += 32) w.bm0[i] = 0u;
+    __syncwarp();
+    unsigned long long nnz_acc = 0;
+    const uint32_t gw = blockIdx.x * kSscBmWarps + wid, nw = gridDim.x * kSscBmWarps;
+    for (uint32_t d = gw; d < a.D; d += nw) {
+        const uint32_t s0 = __ldg(a.doc_start + d);
+        const uint32_t n = __ldg(a.doc_start + d + 1) - s0;
+        if (n > kSscWarpCap || n == 0) continue;  // ssc_long_kernel / empty document
+        uint32_t* row = a.A + __ldg(a.row4 + d) * 4u;
+        const uint16_t* z = a.z + s0;
+        uint32_t nnz;
+        if (n <= 32) nnz = ssc_doc_bitmap<1>(z, n, lane, w, n1, row, a.tbits);
+        else if (n <= 64) nnz = ssc_doc_bitmap<2>(z, n, lane, w, n1, row, a.tbits);
+        else if (n <= 128) nnz = ssc_doc_bitmap<4>(z, n, lane, w, n1, row, a.tbits);
+        else if (n <= 256) nnz = ssc_doc_bitmap<8>(z, n, lane, w, n1, row, a.tbits);
+        else nnz = ssc_doc_bitmap<16>(z, n, lane, w, n1, row, a.tbits);
+        nnz_acc += nnz;
+    }
+    if (lane == 0 && nnz_acc) atomicAdd(a.nnz_total, nnz_acc);
+}
+
 // Long documents: one CTA per document (grid-stride over the long-doc list).
 template <bool kSmemHist, bool kCompact>
 __global__ void __launch_bounds__(256) ssc_long_kernel(SscArgs a) {
@@ -696,8 +1092,19 @@ __global__ void __launch_bounds__(256) ssc_long_kernel(SscArgs a) {
 template <bool kCompact>
 cudaError_t launch_ssc_t(const SscArgs& a, cudaStream_t s) {
     if (a.D > 0) {
-        const uint32_t blocks = grid_for(a.D, kSscWarps, 148u * 8u);
-        ssc_warp_kernel<kCompact><<<blocks, kSscWarps * 32, 0, s>>>(a);
+        const size_t bm_smem = kSscBmWarps * ssc_bitmap_warp_bytes(a.K_pad);
+        if (!kCompact && !a.use_sort && bm_smem <= 200 * 1024) {
+            static bool configured = false;
+            if (!configured) {
+                cudaFuncSetAttribute(ssc_bitmap_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+                configured = true;
+            }
+            const uint32_t blocks = grid_for(a.D, kSscBmWarps, 148u * 8u);
+            ssc_bitmap_kernel<<<blocks, kSscBmWarps * 32, bm_smem, s>>>(a);
+        } else {
+            const uint32_t blocks = grid_for(a.D, kSscWarps, 148u * 8u);
+            ssc_warp_kernel<kCompact><<<blocks, kSscWarps * 32, 0, s>>>(a);
+        }
     }
     if (a.n_long > 0) {
         const size_t smem = sizeof(uint32_t) * a.K_pad;

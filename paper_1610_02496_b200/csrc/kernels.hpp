@@ -34,7 +34,11 @@ struct SamplerArgs {
     uint32_t K, K_pad, l8_stride, n_l8, tbits;
     uint32_t compact;       // C_dk rows in the compact 16-bit format
     unsigned long long* row_entries;  // optional: sum of nnz over tokens (roofline)
+    int shape;              // launch shape (sampler_shape_from_name); -1 = default by K
 };
+
+// "g2" 0, "g4" 1, "g4x512" 2, "s4" 3, "s2" 4, "s4x128" 5; anything else -1 (default).
+int sampler_shape_from_name(const char* name);
 
 cudaError_t launch_sampler(const SamplerArgs& a, uint32_t n_units, cudaStream_t s);
 
@@ -50,6 +54,7 @@ struct SscArgs {
     uint32_t n_long;
     uint32_t* hist_scratch;     // n_long_ctas x K_pad (global fallback for large K)
     unsigned long long* nnz_total;
+    uint32_t use_sort;          // bitonic-sort SSC (else the bitmap SSC for wide rows)
 };
 
 cudaError_t launch_ssc(const SscArgs& a, cudaStream_t s);

@@ -1,6 +1,6 @@
 # usage: bash scripts/gpu_shapes.sh <tag> [configs...]   sampler launch shapes: parity + timing
 TAG=${1:-sh}; shift; CFGS=${@:-c3 c2}
-for SH in g2 g4 g4x512; do
+for SH in ${SHAPES:-g2 g4 g4x512}; do
   SLDA_SAMPLER=$SH timeout 600 python -m pytest tests/test_gpu_parity.py -x -q > gpurun_out/parity_${TAG}_${SH}.log 2>&1
   echo "$SH parity rc=$? $(tail -1 gpurun_out/parity_${TAG}_${SH}.log)"
   for CFG in $CFGS; do
