@@ -139,6 +139,7 @@ struct slda_engine {
     // Shape / config
     int device = 0;
     cudaStream_t stream = nullptr;
+    cudaStream_t side = nullptr;  // SSC, concurrent with the M-step (low priority)
     uint32_t D_all = 0, doc_begin = 0, doc_end = 0, D = 0;  // D = shard documents
     uint32_t V = 0, V_pad = 0, K = 0, K_pad = 0, l8_stride = 0, n_l8 = 0, tbits = 1;
     uint64_t T = 0;
@@ -165,7 +166,8 @@ struct slda_engine {
 
     // Per-iteration phase events, a ring so async iterations can be profiled afterwards.
     static constexpr uint32_t kRing = 64;
-    cudaEvent_t ring[kRing][7] = {};
+    // 0 start, 1 reset, 2 sampler, 3 m-step start, 4 colsum, 5 phi, 6 end, 7 SSC end (side stream)
+    cudaEvent_t ring[kRing][8] = {};
     cudaEvent_t* ev = ring[0];
     uint32_t ring_launches[kRing] = {};
     uint32_t slot = 0;
@@ -197,6 +199,7 @@ struct slda_engine {
             for (auto& e : set)
                 if (e) cudaEventDestroy(e);
         if (comm) nccl().CommDestroy(comm);
+        if (side) cudaStreamDestroy(side);
         if (stream) cudaStreamDestroy(stream);
     }
 
@@ -254,7 +257,14 @@ struct slda_engine {
         device = c.device;
         if (device < 0) CK(cudaGetDevice(&device));
         set_device();
-        CK(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+        {
+            // Main stream at the greatest priority, SSC's side stream at the least, so the
+            // M-step's CTAs are dispatched first while both are pending.
+            int least = 0, greatest = 0;
+            CK(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+            CK(cudaStreamCreateWithPriority(&stream, cudaStreamNonBlocking, greatest));
+            CK(cudaStreamCreateWithPriority(&side, cudaStreamNonBlocking, least));
+        }
         for (auto& set : ring)
             for (auto& e : set) CK(cudaEventCreate(&e));
         if (world > 1) {
@@ -288,7 +298,7 @@ struct slda_engine {
     // ---- run_iteration (trainer.cpp:419-449) ----
     void enqueue_iteration();
     void m_step();
-    void ssc();
+    void ssc(cudaStream_t st);
 };
 
 // ----------------------------------------------------------------- build --
@@ -547,7 +557,7 @@ void slda_engine::build(const slda_corpus_view& cv, const slda_config& c) {
 
     phase("long docs + init topics");
     // C_dk (rebuild_doc_topic), C_wk (count_chunk_into), phi + trees.
-    ssc();
+    ssc(stream);
     CK(cudaMemsetAsync(B.p, 0, B.bytes, stream));
     CK(slda::launch_recount(tok.as<uint2>(), units.as<slda::Unit>(), n_units, z.as<uint16_t>(),
                             B.as<uint32_t>(), K_pad, stream));
@@ -557,8 +567,8 @@ void slda_engine::build(const slda_corpus_view& cv, const slda_config& c) {
     phase("ssc + recount + m_step");
 }
 
-void slda_engine::ssc() {
-    CK(cudaMemsetAsync(nnz_counter(), 0, 8, stream));
+void slda_engine::ssc(cudaStream_t st) {
+    CK(cudaMemsetAsync(nnz_counter(), 0, 8, st));
     slda::SscArgs s{};
     s.z = z.as<uint16_t>();
     s.doc_start = doc_start.as<uint32_t>();
@@ -573,7 +583,7 @@ void slda_engine::ssc() {
     s.hist_scratch = hist_scratch.as<uint32_t>();
     s.nnz_total = nnz_counter();
     s.use_sort = ssc_sort ? 1u : 0u;
-    CK(slda::launch_ssc(s, stream));
+    CK(slda::launch_ssc(s, st));
     launches += (D > 0) + (n_long > 0);
 }
 
@@ -652,8 +662,15 @@ void slda_engine::enqueue_iteration() {
     CK(slda::launch_sampler(a, n_units, stream));
     launches += n_units > 0;
     CK(cudaEventRecord(ev[2], stream));
-    ssc();  // the chunk's doc-topic rebuild (trainer.cpp:319-321), all documents
+    // The chunk's doc-topic rebuild (trainer.cpp:319-321) and the M-step both only read the
+    // sampler's output (z / C_wk): SSC runs on the side stream, overlapped with colsum + phi,
+    // and the iteration ends when both have.
+    CK(cudaStreamWaitEvent(side, ev[2], 0));
+    ssc(side);
+    CK(cudaEventRecord(ev[7], side));
     m_step();
+    CK(cudaStreamWaitEvent(stream, ev[7], 0));
+    CK(cudaEventRecord(ev[6], stream));
     ring_launches[slot] = launches;
     ++iteration;
 }
@@ -791,10 +808,10 @@ int slda_get_kernel_times_avg(const slda_engine* e, uint32_t last_n, slda_kernel
             };
             t->reset_ms += ms(0, 1);
             t->sampler_ms += ms(1, 2);
-            t->ssc_ms += ms(2, 3);
+            t->ssc_ms += ms(2, 7);  // side stream, concurrent with colsum + phi
             t->colsum_ms += ms(3, 4);
             t->phi_ms += ms(4, 5);
-            t->comm_ms += ms(5, 6);
+            t->comm_ms += ms(5, 6);  // NCCL all-gathers + the join with SSC
             t->total_ms += ms(0, 6);
             t->sampler_row_entries += entries[s];
             t->launches += e->ring_launches[s];

@@ -1099,7 +1099,10 @@ cudaError_t launch_ssc_t(const SscArgs& a, cudaStream_t s) {
                 cudaFuncSetAttribute(ssc_bitmap_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
                 configured = true;
             }
-            const uint32_t blocks = grid_for(a.D, kSscBmWarps, 148u * 8u);
+            // Short-lived CTAs (16 documents per warp) rather than a persistent grid: SSC runs
+            // beside the M-step on a low-priority stream, and retiring CTAs let the scheduler
+            // hand SMs to the higher-priority colsum/phi CTAs.
+            const uint32_t blocks = static_cast<uint32_t>((a.D + kSscBmWarps * 16u - 1) / (kSscBmWarps * 16u));
             ssc_bitmap_kernel<<<blocks, kSscBmWarps * 32, bm_smem, s>>>(a);
         } else {
             const uint32_t blocks = grid_for(a.D, kSscWarps, 148u * 8u);
@@ -1221,6 +1224,8 @@ __global__ void __launch_bounds__(kPhiRows, 4) phi_kernel(const uint32_t* __rest
     // t_bh aliases t_in: thread r overwrites cell [r][c] only after reading it.
     __shared__ uint32_t t_in[kPhiRows][kPhiCols + 1];
     __shared__ float t_l4[kPhiRows][kPhiCols + 1];
+    __shared__ double s_den[kPhiCols];
+    __shared__ float s_zv[kPhiCols];
     float(*t_bh)[kPhiCols + 1] = reinterpret_cast<float(*)[kPhiCols + 1]>(t_in);
     const uint32_t r = threadIdx.x;
     const uint32_t v0 = row_begin + blockIdx.x * kPhiRows;
@@ -1243,21 +1248,31 @@ __global__ void __launch_bounds__(kPhiRows, 4) phi_kernel(const uint32_t* __rest
             const uint32_t idx = it * kPhiRows + r;
             t_in[idx / kPhiCols][idx % kPhiCols] = next[it];
         }
+        if (r < kPhiCols) {  // this tile's column constants, off the dependent chain
+            s_den[r] = __ldg(denom + c0 + r);
+            s_zv[r] = __ldg(zv + c0 + r);
+        }
         __syncthreads();
         if (c0 + kPhiCols < K_pad) load_tile(c0 + kPhiCols);
-#pragma unroll 4
-        for (uint32_t c = 0; c < kPhiCols; ++c) {
-            const uint32_t k = c0 + c;
-            float bh = 0.0f;
-            if (k < K) {
+        // Eight independent divisions are issued before the sequential f32 prefix consumes them.
+#pragma unroll
+        for (uint32_t c8 = 0; c8 < kPhiCols; c8 += 8) {
+            float bh[8];
+#pragma unroll
+            for (uint32_t u = 0; u < 8; ++u) {
+                const uint32_t c = c8 + u;
                 const uint32_t cnt = t_in[r][c];
-                bh = cnt ? __double2float_rn(__ddiv_rn(__dadd_rn(static_cast<double>(cnt), beta),
-                                                       __ldg(denom + k)))
-                         : __ldg(zv + k);
-                run = __fadd_rn(run, bh);
+                bh[u] = c0 + c >= K ? 0.0f
+                        : cnt ? __double2float_rn(__ddiv_rn(__dadd_rn(static_cast<double>(cnt), beta), s_den[c]))
+                              : s_zv[c];
             }
-            t_bh[r][c] = bh;
-            t_l4[r][c] = run;
+#pragma unroll
+            for (uint32_t u = 0; u < 8; ++u) {
+                const uint32_t c = c8 + u;
+                if (c0 + c < K) run = __fadd_rn(run, bh[u]);
+                t_bh[r][c] = bh[u];
+                t_l4[r][c] = run;
+            }
         }
         if (v < row_end) {  // L8: the prefix at every 8th column of this tile
             const float4 l8v = make_float4(t_l4[r][7], t_l4[r][15], t_l4[r][23], t_l4[r][31]);
