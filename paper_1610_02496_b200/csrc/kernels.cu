@@ -645,6 +645,167 @@ __global__ void __launch_bounds__(NT, NT <= 128 ? 3 : 2) sampler_stream_kernel(S
     }
 }
 
+// ---- K3'' quad-lane sampler: four lanes per token, no staging ----------------------------------
+// The lane-per-token kernels must move every C_dk row through shared memory (cooperative
+// coalesced loads land a row's sectors in OTHER lanes' registers), and their phi gathers run
+// with a third of the lanes idle.  Here a warp samples 8 tokens at a time with 4 lanes each:
+// one instruction loads one 128-byte line (4 sectors, 32 entries) of each of the 8 rows -- the
+// rows are line-aligned -- straight into the registers of the 4 lanes that consume it, so
+// there is no stage store/load at all, and every lane gathers phi for its own sector's 8
+// entries (full-warp gathers).  The reference's sequential f32 chain (make_branch_context,
+// sampler.hpp:166-178) is kept exactly: the products are formed in parallel, then the running
+// sum visits the 4 sectors of a line in order -- lane j adds its 8 products to the value lane
+// j-1 handed it (shuffle) -- so every intermediate is the reference's.  The per-sector sums
+// double as the prefix_search checkpoints (a few hundred bytes per warp instead of a stage).
+template <int NT>
+__global__ void __launch_bounds__(NT, 1024 / NT) sampler_quad_kernel(SamplerArgs a) {
+    constexpr uint32_t NW = NT / 32;
+    constexpr uint32_t kCk = 16;       // checkpointed sectors per token (128 entries)
+    constexpr uint32_t kCkStride = 17; // odd: the 8 tokens' checkpoints fall in different banks
+    extern __shared__ __align__(16) float sm[];
+    const Unit unit = a.units[blockIdx.x];
+    const uint32_t v = unit.word;
+    float* s_bhat = sm;
+    float* s_l8 = sm + a.K_pad;
+    float* s_ck = s_l8 + a.l8_stride;  // [NW][8 tokens][kCkStride]
+    const float* l4row = a.l4 + static_cast<size_t>(v) * a.K_pad;
+    const float total = __ldg(l4row + a.K_pad - 1);
+    {
+        const float4* gb = reinterpret_cast<const float4*>(a.bhat + static_cast<size_t>(v) * a.K_pad);
+        float4* sb = reinterpret_cast<float4*>(sm);
+        for (uint32_t i = threadIdx.x; i < a.K_pad / 4; i += NT) sb[i] = __ldg(gb + i);
+        const float4* gl = reinterpret_cast<const float4*>(a.l8 + static_cast<size_t>(v) * a.l8_stride);
+        float4* sl = reinterpret_cast<float4*>(s_l8);
+        for (uint32_t i = threadIdx.x; i < a.l8_stride / 4; i += NT) sl[i] = __ldg(gl + i);
+    }
+    const float qv = __ldg(a.q + v);
+    uint32_t* brow = a.B + static_cast<size_t>(v) * a.K_pad;
+    const uint32_t tbits = a.tbits, tmask = (1u << tbits) - 1u;
+    const uint4* A4 = reinterpret_cast<const uint4*>(a.A);
+    const uint32_t lane = lane_id(), t = lane >> 2, sub = lane & 3u, lead = lane & ~3u;
+    const uint32_t warp = threadIdx.x >> 5;
+    float* ck = s_ck + (warp * 8u + t) * kCkStride;
+    unsigned long long entries = 0;
+    __syncthreads();
+
+    // The next round's token record and first line are loaded before the current round's
+    // sampling step, so that step's dependent loads overlap them.
+    uint32_t base = warp * 8u;
+    bool active = base + t < unit.length;
+    uint2 tk = active ? __ldg(a.tok + unit.offset + base + t) : make_uint2(0u, 0u);  // {row quads, slot}
+    Sector cur = active ? ldg_sector(A4 + tk.x + 2 * sub) : zero_sector();
+    while (__any_sync(0xffffffffu, active)) {
+        const uint4* row = A4 + tk.x;
+        const uint32_t hw = __shfl_sync(0xffffffffu, cur.lo.x, lead);  // header: word 0 of sector 0
+        const uint32_t nnz = active ? (hw & tmask) + 1u : 0u;
+        const uint32_t nsect = active ? (nnz + 8u) >> 3 : 0u;
+        if (sub == 0) entries += nnz;
+        const uint32_t max_groups = __reduce_max_sync(0xffffffffu, (nsect + 3u) >> 2);
+        float run = 0.0f;
+        for (uint32_t g = 0; g < max_groups; ++g) {
+            const uint32_t sec = 4u * g + sub;
+            const uint32_t nsec = sec + 4u;
+            const Sector nxt = nsec < nsect ? ldg_sector(row + 2 * nsec) : zero_sector();
+            // Products f32(cnt) * bhat[topic] of this lane's 8 entries (header / padding: count 0).
+            float p[8];
+            const uint32_t es[8] = {cur.lo.x, cur.lo.y, cur.lo.z, cur.lo.w, cur.hi.x, cur.hi.y, cur.hi.z, cur.hi.w};
+            if (sec < nsect) {
+#pragma unroll
+                for (int w = 0; w < 8; ++w) p[w] = entry_mass<false>(es[w], tbits, tmask, s_bhat);
+            }
+            // The sequential chain visits the line's sectors in order (sector 4g+j on lane j).
+#pragma unroll
+            for (uint32_t j = 0; j < 4; ++j) {
+                if (sub == j && sec < nsect) {
+#pragma unroll
+                    for (int w = 0; w < 8; ++w) run = __fadd_rn(run, p[w]);
+                    if (sec < kCk) ck[sec] = run;
+                }
+                run = __shfl_sync(0xffffffffu, run, lead | j);
+            }
+            cur = nxt;
+        }
+        // Next round: token record + first line in flight during this round's sampling step.
+        const bool was_active = active;
+        const uint2 tk_now = tk;
+        const uint32_t ns_now = nsect;
+        base += NW * 8u;
+        active = base + t < unit.length;
+        tk = active ? __ldg(a.tok + unit.offset + base + t) : make_uint2(0u, 0u);
+        cur = active ? ldg_sector(A4 + tk.x + 2 * sub) : zero_sector();
+        __syncwarp();
+
+        // sample_token (sampler.hpp:183-204).  The draws and the branch on every lane of the
+        // token (same values); the crossing sector's 8 products two per lane, then the prefix
+        // walks them in order across the 4 lanes as in the main chain.
+        const float s = run;
+        float ub = 0.0f, up = 0.0f;
+        if (was_active) {
+            const uint64_t id = a.ids ? __ldg(a.ids + tk_now.y) : a.id_base + tk_now.y;
+            draw2_f32(a.seed, a.stream_kind, id, ub, up);
+        }
+        const bool sparse = was_active && ub < __fdiv_rn(s, __fadd_rn(s, qv));
+        const float xs = __fmul_rn(up, s);
+        uint32_t topic = 0;
+        bool need = sparse && xs != 0.0f;
+        uint32_t sc = 0;
+        float r = 0.0f;
+        if (need) {
+            const uint32_t stored = ns_now < kCk ? ns_now : kCk;
+            uint32_t lo = 0, hi = stored;  // first checkpoint >= xs (or stored)
+            while (lo < hi) {
+                const uint32_t mid = (lo + hi) >> 1;
+                if (ck[mid] >= xs) hi = mid; else lo = mid + 1;
+            }
+            sc = lo;
+            r = lo > 0 ? ck[lo - 1] : 0.0f;
+        }
+        while (__any_sync(0xffffffffu, need)) {  // one sector unless past the checkpoints
+            uint2 e2 = make_uint2(0u, 0u);
+            float p0 = 0.0f, p1 = 0.0f;
+            if (need) {
+                e2 = __ldg(reinterpret_cast<const uint2*>(A4 + tk_now.x + 2 * sc) + sub);
+                p0 = entry_mass<false>(e2.x, tbits, tmask, s_bhat);
+                p1 = entry_mass<false>(e2.y, tbits, tmask, s_bhat);
+            }
+            bool found = false;
+#pragma unroll
+            for (uint32_t j = 0; j < 4; ++j) {
+                if (need && sub == j) {
+                    r = __fadd_rn(r, p0);
+                    if (r >= xs) { topic = e2.x & tmask; found = true; }
+                    else {
+                        r = __fadd_rn(r, p1);
+                        if (r >= xs) { topic = e2.y & tmask; found = true; }
+                    }
+                }
+                const uint32_t fj = __shfl_sync(0xffffffffu, found ? 1u : 0u, lead | j);
+                const uint32_t tj = __shfl_sync(0xffffffffu, topic, lead | j);
+                r = __shfl_sync(0xffffffffu, r, lead | j);
+                if (need && fj) { topic = tj; need = false; }
+            }
+            if (++sc >= ns_now) need = false;  // unreachable: xs <= S, the row's last prefix
+        }
+        if (was_active && sub == 0) {
+            if (!sparse) {
+                float x = __fmul_rn(up, total);  // WaryTree::sample(p * total)
+                if (!(x <= total)) x = total;
+                const uint32_t k = tree_search(x, s_l8, a.n_l8, l4row);
+                topic = k < a.K ? k : a.K - 1;
+            } else if (xs == 0.0f) {
+                topic = __ldg(reinterpret_cast<const uint32_t*>(A4 + tk_now.x) + 1) & tmask;  // first real entry
+            }
+            a.z[tk_now.y] = static_cast<uint16_t>(topic);
+            atomicAdd(brow + topic, 1u);
+        }
+        __syncwarp();
+    }
+    if (a.row_entries) {
+        for (int o = 16; o > 0; o >>= 1) entries += __shfl_xor_sync(0xffffffffu, entries, o);
+        if (lane == 0) atomicAdd(a.row_entries, entries);
+    }
+}
+
 size_t sampler_smem(const SamplerArgs& a, int nt, int g, bool global_phi) {
     const size_t stage_row = 32u * static_cast<size_t>(g) + 16u;
     return sizeof(float) * ((global_phi ? 0 : static_cast<size_t>(a.K_pad)) + a.l8_stride) +
@@ -679,7 +840,25 @@ cudaError_t launch_stream_t(const SamplerArgs& a, uint32_t n_units, cudaStream_t
 
 int sampler_shape_from_name(const char* name) {
     const std::string v(name ? name : "");
-    return v == "g2" ? 0 : v == "g4" ? 1 : v == "g4x512" ? 2 : v == "s4" ? 3 : v == "s2" ? 4 : v == "s4x128" ? 5 : -1;
+    return v == "g2" ? 0 : v == "g4" ? 1 : v == "g4x512" ? 2 : v == "s4" ? 3 : v == "s2" ? 4 : v == "s4x128" ? 5
+         : v == "q512" ? 6 : v == "q256" ? 7 : -1;
+}
+
+size_t sampler_quad_smem(const SamplerArgs& a, int nt) {
+    return sizeof(float) * (static_cast<size_t>(a.K_pad) + a.l8_stride + static_cast<size_t>(nt / 32) * 8u * 17u);
+}
+
+template <int NT>
+cudaError_t launch_quad_t(const SamplerArgs& a, uint32_t n_units, cudaStream_t s) {
+    static bool configured = false;
+    if (!configured) {
+        const cudaError_t e = cudaFuncSetAttribute(sampler_quad_kernel<NT>,
+                                                   cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+        if (e != cudaSuccess) return e;
+        configured = true;
+    }
+    sampler_quad_kernel<NT><<<n_units, NT, sampler_quad_smem(a, NT), s>>>(a);
+    return cudaGetLastError();
 }
 
 // Launch shape (SLDA_SAMPLER overrides for experiments; default by phi row size):
@@ -697,6 +876,10 @@ cudaError_t launch_sampler(const SamplerArgs& a, uint32_t n_units, cudaStream_t 
         if (a.compact) return cudaErrorInvalidConfiguration;
         return launch_sampler_t<512, 2, 2, true, false>(a, n_units, s);
     }
+    if (!a.compact && shape == 6 && sampler_quad_smem(a, 512) <= 227 * 1024)
+        return launch_quad_t<512>(a, n_units, s);
+    if (!a.compact && shape == 7 && sampler_quad_smem(a, 256) <= 227 * 1024)
+        return launch_quad_t<256>(a, n_units, s);
     if (!a.compact && shape == 3 && sampler_smem(a, 256, 4, false) <= 227 * 1024)
         return launch_stream_t<256, 4>(a, n_units, s);
     if (!a.compact && shape == 4 && sampler_smem(a, 256, 2, false) <= 227 * 1024)
@@ -1503,11 +1686,14 @@ cudaError_t launch_emit_units(const uint32_t* schedule, const uint32_t* seg_word
 }
 
 // C_dk row capacity in uint4 units: header + nnz_d entries with nnz_d <= len_d
-// (test_counts.cpp:149-150), rounded up to 8 entries (one 32-byte sector).
+// (test_counts.cpp:149-150), rounded up to 32 entries (one 128-byte line).
 __global__ void row_quads_kernel(const uint32_t* doc_start, uint32_t D, uint32_t* quads) {
     const uint32_t d = blockIdx.x * blockDim.x + threadIdx.x;
     if (d >= D) return;
-    quads[d] = ((doc_start[d + 1] - doc_start[d] + 8u) >> 3) << 1;
+    // Rounded up to a whole 128-byte line: every row starts line-aligned, so each 4-sector
+    // group the sampler loads is exactly one L1 line (scripts/mb_pattern.cu: a third fewer
+    // L1TEX wavefronts per loaded byte than 32-byte-aligned rows).
+    quads[d] = ((((doc_start[d + 1] - doc_start[d] + 8u) >> 3) << 1) + 7u) & ~7u;
 }
 
 cudaError_t launch_row_quads(const uint32_t* doc_start, uint32_t D, uint32_t* quads, cudaStream_t s) {

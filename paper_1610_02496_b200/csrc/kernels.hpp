@@ -37,7 +37,7 @@ struct SamplerArgs {
     int shape;              // launch shape (sampler_shape_from_name); -1 = default by K
 };
 
-// "g2" 0, "g4" 1, "g4x512" 2, "s4" 3, "s2" 4, "s4x128" 5; anything else -1 (default).
+// "g2" 0, "g4" 1, "g4x512" 2, "s4" 3, "s2" 4, "s4x128" 5, "q512" 6, "q256" 7; else -1 (default).
 int sampler_shape_from_name(const char* name);
 
 cudaError_t launch_sampler(const SamplerArgs& a, uint32_t n_units, cudaStream_t s);

@@ -19,11 +19,14 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", default="c2", choices=sorted(bench.CONFIGS))
     ap.add_argument("--iters", type=int, default=3)
+    ap.add_argument("--shape", default=None, help="D,V,T,K override (experiments)")
     args = ap.parse_args()
     import paper_1610_02496_b200 as slda
     import paper_1610_02496_b200._core as core
 
-    cfg = bench.CONFIGS[args.config]
+    cfg = dict(bench.CONFIGS[args.config])
+    if args.shape:
+        cfg.update(zip("DVTK", (int(x) for x in args.shape.split(","))))
     toks, _ = core.generate_tokens(0, cfg["D"], cfg["V"], cfg["T"], seed=bench.CORPUS_SEED)
     tc = slda.TrainConfig()
     tc.num_topics = cfg["K"]
