@@ -12,10 +12,10 @@ tail -c 3000 gpurun_out/bench_${TAG}.json
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
     --log-file gpurun_out/launches_c3_${TAG}.csv python scripts/profile_run.py --config c3 --iters 2 > /dev/null 2>&1
 echo ncu-list rc=$?
-# full captures of the second iteration's sampler, SSC and phi
-timeout 1200 ncu --set full --clock-control none --import-source on -k regex:"sampler_kernel" -s 1 -c 1 \
-    -o gpurun_out/prof_sampler_c3_${TAG} python scripts/profile_run.py --config c3 --iters 2 > /dev/null 2>&1
+# full captures at steady state (iteration 13, as bench.py's timed iterations): sampler, SSC, phi
+timeout 1200 ncu --set full --clock-control none --import-source on -k regex:"sampler" -s 12 -c 1 \
+    -o gpurun_out/prof_sampler_c3_${TAG} python scripts/profile_run.py --config c3 --iters 14 > /dev/null 2>&1
 echo ncu-sampler rc=$?
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:"ssc_warp|phi_kernel" -s 2 -c 2 \
-    -o gpurun_out/prof_sscphi_c3_${TAG} python scripts/profile_run.py --config c3 --iters 2 > /dev/null 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"ssc_bitmap|phi_kernel" -s 24 -c 2 \
+    -o gpurun_out/prof_sscphi_c3_${TAG} python scripts/profile_run.py --config c3 --iters 14 > /dev/null 2>&1
 echo ncu-sscphi rc=$?

@@ -264,3 +264,25 @@ def test_checkpoint_roundtrip_and_resume(tmp_path):
     text = open(path).read().splitlines()
     assert text[0].startswith("sparselda-checkpoint 1 ")
     assert len(text) == 1 + half.num_tokens + 1 + int((half.word_topic() != 0).sum())
+
+
+VARIANT_CASES = ["c1", "long_docs", "empty_docs", "shuffled", "k_large", "nytimes_small", "k1"]
+
+
+@pytest.mark.parametrize("variant", ["SLDA_SAMPLER=g2", "SLDA_SAMPLER=g4", "SLDA_SAMPLER=s4",
+                                     "SLDA_SAMPLER=q512", "SLDA_SSC=sort"])
+@pytest.mark.parametrize("name", VARIANT_CASES)
+def test_kernel_variants_match_reference(name, variant, golden, monkeypatch):
+    """Every sampler launch shape (round-based 2/4-sector groups, streaming lane refill,
+    quad-lane) and both SSC kernels (bitmap, bitonic sort) give the reference's digests.
+    The variant is read when the engine is built (engine.cu configure)."""
+    key, value = variant.split("=")
+    monkeypatch.setenv(key, value)
+    spec = CASES[name]
+    fx = golden["cases"][name]
+    m, cfg, _ = make_model(spec)
+    iters = min(spec["iterations"], 10)
+    for it in range(iters + 1):
+        assert model_digests(m) == fx["iterations"][it], (name, variant, it)
+        if it < iters:
+            m.run_iteration(cfg)
