@@ -657,17 +657,17 @@ __global__ void __launch_bounds__(NT, NT <= 128 ? 3 : 2) sampler_stream_kernel(S
 // sum visits the 4 sectors of a line in order -- lane j adds its 8 products to the value lane
 // j-1 handed it (shuffle) -- so every intermediate is the reference's.  The per-sector sums
 // double as the prefix_search checkpoints (a few hundred bytes per warp instead of a stage).
-template <int NT>
-__global__ void __launch_bounds__(NT, 1024 / NT) sampler_quad_kernel(SamplerArgs a) {
+template <int NT, int MINB>
+__global__ void __launch_bounds__(NT, MINB) sampler_quad_kernel(SamplerArgs a) {
     constexpr uint32_t NW = NT / 32;
     constexpr uint32_t kCk = 16;       // checkpointed sectors per token (128 entries)
-    constexpr uint32_t kCkStride = 17; // odd: the 8 tokens' checkpoints fall in different banks
+    constexpr uint32_t kCkStride = 17; // odd: different tokens' checkpoints fall in different banks
     extern __shared__ __align__(16) float sm[];
     const Unit unit = a.units[blockIdx.x];
     const uint32_t v = unit.word;
     float* s_bhat = sm;
     float* s_l8 = sm + a.K_pad;
-    float* s_ck = s_l8 + a.l8_stride;  // [NW][8 tokens][kCkStride]
+    float* s_ck = s_l8 + a.l8_stride;  // [NW][32 tokens][kCkStride]
     const float* l4row = a.l4 + static_cast<size_t>(v) * a.K_pad;
     const float total = __ldg(l4row + a.K_pad - 1);
     {
@@ -684,118 +684,108 @@ __global__ void __launch_bounds__(NT, 1024 / NT) sampler_quad_kernel(SamplerArgs
     const uint4* A4 = reinterpret_cast<const uint4*>(a.A);
     const uint32_t lane = lane_id(), t = lane >> 2, sub = lane & 3u, lead = lane & ~3u;
     const uint32_t warp = threadIdx.x >> 5;
-    float* ck = s_ck + (warp * 8u + t) * kCkStride;
+    float* ckw = s_ck + warp * 32u * kCkStride;
     unsigned long long entries = 0;
     __syncthreads();
 
-    // The next round's token record and first line are loaded before the current round's
-    // sampling step, so that step's dependent loads overlap them.
-    uint32_t base = warp * 8u;
-    bool active = base + t < unit.length;
-    uint2 tk = active ? __ldg(a.tok + unit.offset + base + t) : make_uint2(0u, 0u);  // {row quads, slot}
-    Sector cur = active ? ldg_sector(A4 + tk.x + 2 * sub) : zero_sector();
-    while (__any_sync(0xffffffffu, active)) {
-        const uint4* row = A4 + tk.x;
-        const uint32_t hw = __shfl_sync(0xffffffffu, cur.lo.x, lead);  // header: word 0 of sector 0
-        const uint32_t nnz = active ? (hw & tmask) + 1u : 0u;
-        const uint32_t nsect = active ? (nnz + 8u) >> 3 : 0u;
-        if (sub == 0) entries += nnz;
-        const uint32_t max_groups = __reduce_max_sync(0xffffffffu, (nsect + 3u) >> 2);
-        float run = 0.0f;
-        for (uint32_t g = 0; g < max_groups; ++g) {
-            const uint32_t sec = 4u * g + sub;
-            const uint32_t nsec = sec + 4u;
-            const Sector nxt = nsec < nsect ? ldg_sector(row + 2 * nsec) : zero_sector();
-            // Products f32(cnt) * bhat[topic] of this lane's 8 entries (header / padding: count 0).
-            float p[8];
-            const uint32_t es[8] = {cur.lo.x, cur.lo.y, cur.lo.z, cur.lo.w, cur.hi.x, cur.hi.y, cur.hi.z, cur.hi.w};
-            if (sec < nsect) {
+    // A batch of 32 tokens per warp: four rounds of 8 tokens x 4 lanes stream the rows and form
+    // S; then lane l finishes token l of the batch (draws, branch, prefix search / tree).
+    for (uint32_t base = warp * 32u; base < unit.length; base += NW * 32u) {
+        const bool mine = base + lane < unit.length;
+        const uint2 tk = mine ? __ldg(a.tok + unit.offset + base + lane) : make_uint2(0u, 0u);  // {row quads, slot}
+        float S = 0.0f;
+        uint32_t my_ns = 0;
+#pragma unroll 1
+        for (uint32_t r = 0; r < 4; ++r) {
+            const uint32_t ti = 8u * r + t;  // this quad's token within the batch
+            if (__all_sync(0xffffffffu, base + 8u * r >= unit.length)) break;
+            const bool act = base + ti < unit.length;
+            const uint4* row = A4 + __shfl_sync(0xffffffffu, tk.x, ti);
+            Sector c = zero_sector();
+            if (act) c = ldg_sector(row + 2 * sub);
+            const uint32_t hw = __shfl_sync(0xffffffffu, c.lo.x, lead);  // header: word 0 of sector 0
+            const uint32_t nnz = act ? (hw & tmask) + 1u : 0u;
+            const uint32_t nsect = act ? (nnz + 8u) >> 3 : 0u;
+            if (sub == 0) entries += nnz;
+            const uint32_t max_groups = __reduce_max_sync(0xffffffffu, (nsect + 3u) >> 2);
+            float* ck = ckw + ti * kCkStride;
+            float run = 0.0f;
+            // Products of this lane's sector, then the chain over the line's 4 sectors in order.
+            auto consume = [&](const Sector& q, uint32_t g) {
+                const uint32_t sec = 4u * g + sub;
+                float p[8];
+                if (sec < nsect) {
+                    const uint32_t es[8] = {q.lo.x, q.lo.y, q.lo.z, q.lo.w, q.hi.x, q.hi.y, q.hi.z, q.hi.w};
 #pragma unroll
-                for (int w = 0; w < 8; ++w) p[w] = entry_mass<false>(es[w], tbits, tmask, s_bhat);
-            }
-            // The sequential chain visits the line's sectors in order (sector 4g+j on lane j).
-#pragma unroll
-            for (uint32_t j = 0; j < 4; ++j) {
-                if (sub == j && sec < nsect) {
-#pragma unroll
-                    for (int w = 0; w < 8; ++w) run = __fadd_rn(run, p[w]);
-                    if (sec < kCk) ck[sec] = run;
+                    for (int w = 0; w < 8; ++w) p[w] = entry_mass<false>(es[w], tbits, tmask, s_bhat);
                 }
-                run = __shfl_sync(0xffffffffu, run, lead | j);
-            }
-            cur = nxt;
-        }
-        // Next round: token record + first line in flight during this round's sampling step.
-        const bool was_active = active;
-        const uint2 tk_now = tk;
-        const uint32_t ns_now = nsect;
-        base += NW * 8u;
-        active = base + t < unit.length;
-        tk = active ? __ldg(a.tok + unit.offset + base + t) : make_uint2(0u, 0u);
-        cur = active ? ldg_sector(A4 + tk.x + 2 * sub) : zero_sector();
-        __syncwarp();
-
-        // sample_token (sampler.hpp:183-204).  The draws and the branch on every lane of the
-        // token (same values); the crossing sector's 8 products two per lane, then the prefix
-        // walks them in order across the 4 lanes as in the main chain.
-        const float s = run;
-        float ub = 0.0f, up = 0.0f;
-        if (was_active) {
-            const uint64_t id = a.ids ? __ldg(a.ids + tk_now.y) : a.id_base + tk_now.y;
-            draw2_f32(a.seed, a.stream_kind, id, ub, up);
-        }
-        const bool sparse = was_active && ub < __fdiv_rn(s, __fadd_rn(s, qv));
-        const float xs = __fmul_rn(up, s);
-        uint32_t topic = 0;
-        bool need = sparse && xs != 0.0f;
-        uint32_t sc = 0;
-        float r = 0.0f;
-        if (need) {
-            const uint32_t stored = ns_now < kCk ? ns_now : kCk;
-            uint32_t lo = 0, hi = stored;  // first checkpoint >= xs (or stored)
-            while (lo < hi) {
-                const uint32_t mid = (lo + hi) >> 1;
-                if (ck[mid] >= xs) hi = mid; else lo = mid + 1;
-            }
-            sc = lo;
-            r = lo > 0 ? ck[lo - 1] : 0.0f;
-        }
-        while (__any_sync(0xffffffffu, need)) {  // one sector unless past the checkpoints
-            uint2 e2 = make_uint2(0u, 0u);
-            float p0 = 0.0f, p1 = 0.0f;
-            if (need) {
-                e2 = __ldg(reinterpret_cast<const uint2*>(A4 + tk_now.x + 2 * sc) + sub);
-                p0 = entry_mass<false>(e2.x, tbits, tmask, s_bhat);
-                p1 = entry_mass<false>(e2.y, tbits, tmask, s_bhat);
-            }
-            bool found = false;
 #pragma unroll
-            for (uint32_t j = 0; j < 4; ++j) {
-                if (need && sub == j) {
-                    r = __fadd_rn(r, p0);
-                    if (r >= xs) { topic = e2.x & tmask; found = true; }
-                    else {
-                        r = __fadd_rn(r, p1);
-                        if (r >= xs) { topic = e2.y & tmask; found = true; }
+                for (uint32_t j = 0; j < 4; ++j) {
+                    if (sub == j && sec < nsect) {
+#pragma unroll
+                        for (int w = 0; w < 8; ++w) run = __fadd_rn(run, p[w]);
+                        if (sec < kCk) ck[sec] = run;
+                    }
+                    run = __shfl_sync(0xffffffffu, run, lead | j);
+                }
+            };
+            for (uint32_t g = 0; g < max_groups; g += 2) {  // two groups per trip: no register copies
+                Sector n = c;
+                if (4u * (g + 1) + sub < nsect) n = ldg_sector(row + 2 * (4u * (g + 1) + sub));
+                consume(c, g);
+                if (g + 1 >= max_groups) break;
+                if (4u * (g + 2) + sub < nsect) c = ldg_sector(row + 2 * (4u * (g + 2) + sub));
+                consume(n, g + 1);
+            }
+            // Token ti's S and sector count to its owning lane (lane ti).
+            const uint32_t src = ((lane - 8u * r) & 7u) << 2;
+            const float xS = __shfl_sync(0xffffffffu, run, src);
+            const uint32_t xn = __shfl_sync(0xffffffffu, nsect, src);
+            if ((lane >> 3) == r) {
+                S = xS;
+                my_ns = xn;
+            }
+        }
+        __syncwarp();
+        // sample_token (sampler.hpp:183-204), one token per lane.
+        if (mine) {
+            float ub, up;
+            const uint64_t id = a.ids ? __ldg(a.ids + tk.y) : a.id_base + tk.y;
+            draw2_f32(a.seed, a.stream_kind, id, ub, up);
+            const uint4* row = A4 + tk.x;
+            uint32_t topic = 0;
+            if (ub < __fdiv_rn(S, __fadd_rn(S, qv))) {
+                const float xs = __fmul_rn(up, S);
+                if (xs == 0.0f) {
+                    topic = __ldg(reinterpret_cast<const uint32_t*>(row) + 1) & tmask;  // first real entry
+                } else {
+                    const float* ck = ckw + lane * kCkStride;
+                    const uint32_t stored = my_ns < kCk ? my_ns : kCk;
+                    uint32_t lo = 0, hi = stored;  // first checkpoint >= xs (or stored)
+                    while (lo < hi) {
+                        const uint32_t mid = (lo + hi) >> 1;
+                        if (ck[mid] >= xs) hi = mid; else lo = mid + 1;
+                    }
+                    float r = lo > 0 ? ck[lo - 1] : 0.0f;
+                    for (uint32_t sc = lo; sc < my_ns; ++sc) {  // one sector unless past the checkpoints
+                        const Sector q = ldg_sector(row + 2 * sc);
+                        const uint32_t es[8] = {q.lo.x, q.lo.y, q.lo.z, q.lo.w, q.hi.x, q.hi.y, q.hi.z, q.hi.w};
+                        bool found = false;
+#pragma unroll
+                        for (int w = 0; w < 8; ++w) {
+                            r = __fadd_rn(r, entry_mass<false>(es[w], tbits, tmask, s_bhat));
+                            if (!found && r >= xs) { topic = es[w] & tmask; found = true; }
+                        }
+                        if (found) break;
                     }
                 }
-                const uint32_t fj = __shfl_sync(0xffffffffu, found ? 1u : 0u, lead | j);
-                const uint32_t tj = __shfl_sync(0xffffffffu, topic, lead | j);
-                r = __shfl_sync(0xffffffffu, r, lead | j);
-                if (need && fj) { topic = tj; need = false; }
-            }
-            if (++sc >= ns_now) need = false;  // unreachable: xs <= S, the row's last prefix
-        }
-        if (was_active && sub == 0) {
-            if (!sparse) {
+            } else {
                 float x = __fmul_rn(up, total);  // WaryTree::sample(p * total)
                 if (!(x <= total)) x = total;
                 const uint32_t k = tree_search(x, s_l8, a.n_l8, l4row);
                 topic = k < a.K ? k : a.K - 1;
-            } else if (xs == 0.0f) {
-                topic = __ldg(reinterpret_cast<const uint32_t*>(A4 + tk_now.x) + 1) & tmask;  // first real entry
             }
-            a.z[tk_now.y] = static_cast<uint16_t>(topic);
+            a.z[tk.y] = static_cast<uint16_t>(topic);
             atomicAdd(brow + topic, 1u);
         }
         __syncwarp();
@@ -841,34 +831,45 @@ cudaError_t launch_stream_t(const SamplerArgs& a, uint32_t n_units, cudaStream_t
 int sampler_shape_from_name(const char* name) {
     const std::string v(name ? name : "");
     return v == "g2" ? 0 : v == "g4" ? 1 : v == "g4x512" ? 2 : v == "s4" ? 3 : v == "s2" ? 4 : v == "s4x128" ? 5
-         : v == "q512" ? 6 : v == "q256" ? 7 : -1;
+         : v == "q512" ? 6 : v == "q256" ? 7 : v == "q512r" ? 8 : v == "q256r" ? 9 : -1;
 }
 
 size_t sampler_quad_smem(const SamplerArgs& a, int nt) {
-    return sizeof(float) * (static_cast<size_t>(a.K_pad) + a.l8_stride + static_cast<size_t>(nt / 32) * 8u * 17u);
+    return sizeof(float) * (static_cast<size_t>(a.K_pad) + a.l8_stride + static_cast<size_t>(nt / 32) * 32u * 17u);
 }
 
-template <int NT>
+template <int NT, int MINB>
 cudaError_t launch_quad_t(const SamplerArgs& a, uint32_t n_units, cudaStream_t s) {
     static bool configured = false;
     if (!configured) {
-        const cudaError_t e = cudaFuncSetAttribute(sampler_quad_kernel<NT>,
+        const cudaError_t e = cudaFuncSetAttribute(sampler_quad_kernel<NT, MINB>,
                                                    cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
         if (e != cudaSuccess) return e;
         configured = true;
     }
-    sampler_quad_kernel<NT><<<n_units, NT, sampler_quad_smem(a, NT), s>>>(a);
+    sampler_quad_kernel<NT, MINB><<<n_units, NT, sampler_quad_smem(a, NT), s>>>(a);
     return cudaGetLastError();
 }
 
 // Launch shape (SLDA_SAMPLER overrides for experiments; default by phi row size):
-//   "g2"     : 256/512-thread CTAs, 2-sector groups, 64 registers (two 512-thread CTAs / SM)
-//   "g4"     : 256-thread CTAs, 4-sector groups, up to 128 registers
-//   "g4x512" : 512-thread CTAs, 4-sector groups (one CTA / SM at K = 10K)
+//   "g2"     : round-based, 256/512-thread CTAs, 2-sector groups, 64 registers
+//   "g4"     : round-based, 256-thread CTAs, 4-sector groups, up to 128 registers
+//   "g4x512" : round-based, 512-thread CTAs, 4-sector groups (one CTA / SM at K = 10K)
+//   "s4", "s2", "s4x128" : streaming lane refill (sampler_stream_kernel)
+//   "q512", "q256"       : quad-lane (sampler_quad_kernel), 64 registers, 64 warps / SM
+//   "q512r", "q256r"     : quad-lane with a relaxed register bound (fewer warps; slower)
 cudaError_t launch_sampler(const SamplerArgs& a, uint32_t n_units, cudaStream_t s) {
     if (n_units == 0) return cudaSuccess;
     const size_t phi_bytes = sizeof(float) * (static_cast<size_t>(a.K_pad) + a.l8_stride);
-    const int shape = a.shape >= 0 ? a.shape : (phi_bytes > 24 * 1024 ? 1 : 0);
+    // Default: the quad-lane kernel wherever two 512-thread (or four 256-thread) CTAs fit an SM
+    // (C3 K=10K: 100.0 vs 102.6 ms for 4-sector groups; C2 K=1K: 21.5 vs 23.5 ms for 2-sector
+    // groups), else 4-sector groups (large phi rows), else 2-sector groups.
+    int shape = a.shape;
+    if (shape < 0 && !a.compact) {
+        if (phi_bytes <= 24 * 1024 && 4 * sampler_quad_smem(a, 256) <= 227 * 1024) shape = 7;
+        else if (2 * sampler_quad_smem(a, 512) <= 227 * 1024) shape = 6;
+    }
+    if (shape < 0) shape = phi_bytes > 24 * 1024 ? 1 : 0;
     const bool fits512 = sampler_smem(a, 512, 2, false) <= 227 * 1024;
     if (!fits512) {
         // Rows that do not fit shared memory (K > kCompactMaxK, so always the wide format):
@@ -877,9 +878,13 @@ cudaError_t launch_sampler(const SamplerArgs& a, uint32_t n_units, cudaStream_t 
         return launch_sampler_t<512, 2, 2, true, false>(a, n_units, s);
     }
     if (!a.compact && shape == 6 && sampler_quad_smem(a, 512) <= 227 * 1024)
-        return launch_quad_t<512>(a, n_units, s);
+        return launch_quad_t<512, 2>(a, n_units, s);
     if (!a.compact && shape == 7 && sampler_quad_smem(a, 256) <= 227 * 1024)
-        return launch_quad_t<256>(a, n_units, s);
+        return launch_quad_t<256, 4>(a, n_units, s);
+    if (!a.compact && shape == 8 && sampler_quad_smem(a, 512) <= 227 * 1024)
+        return launch_quad_t<512, 1>(a, n_units, s);
+    if (!a.compact && shape == 9 && sampler_quad_smem(a, 256) <= 227 * 1024)
+        return launch_quad_t<256, 3>(a, n_units, s);
     if (!a.compact && shape == 3 && sampler_smem(a, 256, 4, false) <= 227 * 1024)
         return launch_stream_t<256, 4>(a, n_units, s);
     if (!a.compact && shape == 4 && sampler_smem(a, 256, 2, false) <= 227 * 1024)
