@@ -76,7 +76,7 @@ def kernels(tag):
             summary = {"dram_bytes_per_launch": gb("dram__bytes_read.sum") + gb("dram__bytes_write.sum"),
                        "dram_read_bytes": gb("dram__bytes_read.sum"), "dram_write_bytes": gb("dram__bytes_write.sum"),
                        "duration_ms_under_ncu": k["gpu__time_duration.sum"],
-                       "config": f"C3 iteration 2 (E_t~100), tag {tag}, ncu --set full --clock-control none"}
+                       "config": f"C3 iteration 13 (steady state, as the bench), tag {tag}, ncu --set full --clock-control none"}
             (REPO / "profiles" / "ncu_sampler_summary.json").write_text(json.dumps(summary, indent=1))
     return slim
 
