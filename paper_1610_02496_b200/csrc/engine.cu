@@ -153,6 +153,7 @@ struct slda_engine {
     bool compact = false;  // C_dk row format (kernels.cu: compact 16-bit slots or wide 32-bit)
     int sampler_shape = -1;  // SLDA_SAMPLER (kernels.cu launch_sampler); -1 = default by K
     bool ssc_sort = false;   // SLDA_SSC=sort: the bitonic-sort SSC instead of the bitmap one
+    bool serial = false;     // SLDA_SERIAL=1: SSC on the main stream (measurement of each kernel alone)
     uint32_t wshift = 0;  // word field shift of the execution-order key
     size_t device_bytes = 0;
     uint64_t nnz = 0;
@@ -395,6 +396,7 @@ void slda_engine::build(const slda_corpus_view& cv, const slda_config& c) {
     // DESIGN.md §6).
     if (const char* f = std::getenv("SLDA_SAMPLER")) sampler_shape = slda::sampler_shape_from_name(f);
     if (const char* f = std::getenv("SLDA_SSC")) ssc_sort = std::string(f) == "sort";
+    if (const char* f = std::getenv("SLDA_SERIAL")) serial = std::string(f) == "1";
     compact = false;
     if (const char* f = std::getenv("SLDA_ROW_FORMAT")) {
         if (std::string(f) == "compact")
@@ -665,9 +667,10 @@ void slda_engine::enqueue_iteration() {
     // The chunk's doc-topic rebuild (trainer.cpp:319-321) and the M-step both only read the
     // sampler's output (z / C_wk): SSC runs on the side stream, overlapped with colsum + phi,
     // and the iteration ends when both have.
-    CK(cudaStreamWaitEvent(side, ev[2], 0));
-    ssc(side);
-    CK(cudaEventRecord(ev[7], side));
+    cudaStream_t ssc_stream = serial ? stream : side;
+    CK(cudaStreamWaitEvent(ssc_stream, ev[2], 0));
+    ssc(ssc_stream);
+    CK(cudaEventRecord(ev[7], ssc_stream));
     m_step();
     CK(cudaStreamWaitEvent(stream, ev[7], 0));
     CK(cudaEventRecord(ev[6], stream));
