@@ -657,9 +657,10 @@ __global__ void __launch_bounds__(NT, NT <= 128 ? 3 : 2) sampler_stream_kernel(S
 // sum visits the 4 sectors of a line in order -- lane j adds its 8 products to the value lane
 // j-1 handed it (shuffle) -- so every intermediate is the reference's.  The per-sector sums
 // double as the prefix_search checkpoints (a few hundred bytes per warp instead of a stage).
-template <int NT, int MINB>
+template <int NT, int MINB, int L>
 __global__ void __launch_bounds__(NT, MINB) sampler_quad_kernel(SamplerArgs a) {
     constexpr uint32_t NW = NT / 32;
+    constexpr uint32_t TPR = 32u / L;  // tokens per round (L lanes each, L sectors per group)
     constexpr uint32_t kCk = 16;       // checkpointed sectors per token (128 entries)
     constexpr uint32_t kCkStride = 17; // odd: different tokens' checkpoints fall in different banks
     extern __shared__ __align__(16) float sm[];
@@ -682,7 +683,7 @@ __global__ void __launch_bounds__(NT, MINB) sampler_quad_kernel(SamplerArgs a) {
     uint32_t* brow = a.B + static_cast<size_t>(v) * a.K_pad;
     const uint32_t tbits = a.tbits, tmask = (1u << tbits) - 1u;
     const uint4* A4 = reinterpret_cast<const uint4*>(a.A);
-    const uint32_t lane = lane_id(), t = lane >> 2, sub = lane & 3u, lead = lane & ~3u;
+    const uint32_t lane = lane_id(), t = lane / L, sub = lane % L, lead = lane & ~(L - 1u);
     const uint32_t warp = threadIdx.x >> 5;
     float* ckw = s_ck + warp * 32u * kCkStride;
     unsigned long long entries = 0;
@@ -696,9 +697,9 @@ __global__ void __launch_bounds__(NT, MINB) sampler_quad_kernel(SamplerArgs a) {
         float S = 0.0f;
         uint32_t my_ns = 0;
 #pragma unroll 1
-        for (uint32_t r = 0; r < 4; ++r) {
-            const uint32_t ti = 8u * r + t;  // this quad's token within the batch
-            if (__all_sync(0xffffffffu, base + 8u * r >= unit.length)) break;
+        for (uint32_t r = 0; r < L; ++r) {
+            const uint32_t ti = TPR * r + t;  // this lane group's token within the batch
+            if (__all_sync(0xffffffffu, base + TPR * r >= unit.length)) break;
             const bool act = base + ti < unit.length;
             const uint4* row = A4 + __shfl_sync(0xffffffffu, tk.x, ti);
             Sector c = zero_sector();
@@ -707,12 +708,12 @@ __global__ void __launch_bounds__(NT, MINB) sampler_quad_kernel(SamplerArgs a) {
             const uint32_t nnz = act ? (hw & tmask) + 1u : 0u;
             const uint32_t nsect = act ? (nnz + 8u) >> 3 : 0u;
             if (sub == 0) entries += nnz;
-            const uint32_t max_groups = __reduce_max_sync(0xffffffffu, (nsect + 3u) >> 2);
+            const uint32_t max_groups = __reduce_max_sync(0xffffffffu, (nsect + L - 1u) / L);
             float* ck = ckw + ti * kCkStride;
             float run = 0.0f;
             // Products of this lane's sector, then the chain over the line's 4 sectors in order.
             auto consume = [&](const Sector& q, uint32_t g) {
-                const uint32_t sec = 4u * g + sub;
+                const uint32_t sec = L * g + sub;
                 float p[8];
                 if (sec < nsect) {
                     const uint32_t es[8] = {q.lo.x, q.lo.y, q.lo.z, q.lo.w, q.hi.x, q.hi.y, q.hi.z, q.hi.w};
@@ -720,7 +721,7 @@ __global__ void __launch_bounds__(NT, MINB) sampler_quad_kernel(SamplerArgs a) {
                     for (int w = 0; w < 8; ++w) p[w] = entry_mass<false>(es[w], tbits, tmask, s_bhat);
                 }
 #pragma unroll
-                for (uint32_t j = 0; j < 4; ++j) {
+                for (uint32_t j = 0; j < L; ++j) {
                     if (sub == j && sec < nsect) {
 #pragma unroll
                         for (int w = 0; w < 8; ++w) run = __fadd_rn(run, p[w]);
@@ -731,17 +732,17 @@ __global__ void __launch_bounds__(NT, MINB) sampler_quad_kernel(SamplerArgs a) {
             };
             for (uint32_t g = 0; g < max_groups; g += 2) {  // two groups per trip: no register copies
                 Sector n = c;
-                if (4u * (g + 1) + sub < nsect) n = ldg_sector(row + 2 * (4u * (g + 1) + sub));
+                if (L * (g + 1) + sub < nsect) n = ldg_sector(row + 2 * (L * (g + 1) + sub));
                 consume(c, g);
                 if (g + 1 >= max_groups) break;
-                if (4u * (g + 2) + sub < nsect) c = ldg_sector(row + 2 * (4u * (g + 2) + sub));
+                if (L * (g + 2) + sub < nsect) c = ldg_sector(row + 2 * (L * (g + 2) + sub));
                 consume(n, g + 1);
             }
             // Token ti's S and sector count to its owning lane (lane ti).
-            const uint32_t src = ((lane - 8u * r) & 7u) << 2;
+            const uint32_t src = ((lane - TPR * r) & (TPR - 1u)) * L;
             const float xS = __shfl_sync(0xffffffffu, run, src);
             const uint32_t xn = __shfl_sync(0xffffffffu, nsect, src);
-            if ((lane >> 3) == r) {
+            if (lane / TPR == r) {
                 S = xS;
                 my_ns = xn;
             }
@@ -831,23 +832,24 @@ cudaError_t launch_stream_t(const SamplerArgs& a, uint32_t n_units, cudaStream_t
 int sampler_shape_from_name(const char* name) {
     const std::string v(name ? name : "");
     return v == "g2" ? 0 : v == "g4" ? 1 : v == "g4x512" ? 2 : v == "s4" ? 3 : v == "s2" ? 4 : v == "s4x128" ? 5
-         : v == "q512" ? 6 : v == "q256" ? 7 : v == "q512r" ? 8 : v == "q256r" ? 9 : -1;
+         : v == "q512" ? 6 : v == "q256" ? 7 : v == "q512r" ? 8 : v == "q256r" ? 9
+         : v == "p512" ? 10 : v == "p256" ? 11 : v == "o512" ? 12 : -1;
 }
 
 size_t sampler_quad_smem(const SamplerArgs& a, int nt) {
     return sizeof(float) * (static_cast<size_t>(a.K_pad) + a.l8_stride + static_cast<size_t>(nt / 32) * 32u * 17u);
 }
 
-template <int NT, int MINB>
+template <int NT, int MINB, int L = 4>
 cudaError_t launch_quad_t(const SamplerArgs& a, uint32_t n_units, cudaStream_t s) {
     static bool configured = false;
     if (!configured) {
-        const cudaError_t e = cudaFuncSetAttribute(sampler_quad_kernel<NT, MINB>,
+        const cudaError_t e = cudaFuncSetAttribute(sampler_quad_kernel<NT, MINB, L>,
                                                    cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
         if (e != cudaSuccess) return e;
         configured = true;
     }
-    sampler_quad_kernel<NT, MINB><<<n_units, NT, sampler_quad_smem(a, NT), s>>>(a);
+    sampler_quad_kernel<NT, MINB, L><<<n_units, NT, sampler_quad_smem(a, NT), s>>>(a);
     return cudaGetLastError();
 }
 
@@ -856,7 +858,9 @@ cudaError_t launch_quad_t(const SamplerArgs& a, uint32_t n_units, cudaStream_t s
 //   "g4"     : round-based, 256-thread CTAs, 4-sector groups, up to 128 registers
 //   "g4x512" : round-based, 512-thread CTAs, 4-sector groups (one CTA / SM at K = 10K)
 //   "s4", "s2", "s4x128" : streaming lane refill (sampler_stream_kernel)
-//   "q512", "q256"       : quad-lane (sampler_quad_kernel), 64 registers, 64 warps / SM
+//   "q512", "q256"       : quad-lane (sampler_quad_kernel, L=4 lanes per token), 64 registers
+//   "p512", "p256"       : pair-lane (L=2; C2 20.7 vs 21.5 ms, C3 107.9 vs 100.0 ms)
+//   "o512"               : octet-lane (L=8; slower at both)
 //   "q512r", "q256r"     : quad-lane with a relaxed register bound (fewer warps; slower)
 cudaError_t launch_sampler(const SamplerArgs& a, uint32_t n_units, cudaStream_t s) {
     if (n_units == 0) return cudaSuccess;
@@ -885,6 +889,12 @@ cudaError_t launch_sampler(const SamplerArgs& a, uint32_t n_units, cudaStream_t 
         return launch_quad_t<512, 1>(a, n_units, s);
     if (!a.compact && shape == 9 && sampler_quad_smem(a, 256) <= 227 * 1024)
         return launch_quad_t<256, 3>(a, n_units, s);
+    if (!a.compact && shape == 10 && sampler_quad_smem(a, 512) <= 227 * 1024)
+        return launch_quad_t<512, 2, 2>(a, n_units, s);
+    if (!a.compact && shape == 11 && sampler_quad_smem(a, 256) <= 227 * 1024)
+        return launch_quad_t<256, 4, 2>(a, n_units, s);
+    if (!a.compact && shape == 12 && sampler_quad_smem(a, 512) <= 227 * 1024)
+        return launch_quad_t<512, 2, 8>(a, n_units, s);
     if (!a.compact && shape == 3 && sampler_smem(a, 256, 4, false) <= 227 * 1024)
         return launch_stream_t<256, 4>(a, n_units, s);
     if (!a.compact && shape == 4 && sampler_smem(a, 256, 2, false) <= 227 * 1024)
