@@ -1775,18 +1775,31 @@ cudaError_t launch_ids_by_slot(const uint64_t* ids_in, const uint32_t* input_of_
     return cudaGetLastError();
 }
 
+// count_chunk_into (trainer.cpp:223-235) in word order.  With freshly drawn topics
+// (init_assignments) the topic is recomputed from the token id -- the same Philox draw as
+// init_topics_kernel -- instead of gathered from z by slot (a random 2-byte read per token).
 __global__ void __launch_bounds__(256) recount_kernel(const uint2* tok, const Unit* units,
-                                                      const uint16_t* z, uint32_t* B, uint32_t K_pad) {
+                                                      const uint16_t* z, uint32_t* B, uint32_t K_pad,
+                                                      RecountDraw draw) {
     const Unit u = units[blockIdx.x];
     uint32_t* brow = B + static_cast<size_t>(u.word) * K_pad;
-    for (uint32_t i = threadIdx.x; i < u.length; i += blockDim.x)
-        atomicAdd(brow + z[tok[u.offset + i].y], 1u);
+    for (uint32_t i = threadIdx.x; i < u.length; i += blockDim.x) {
+        const uint32_t slot = tok[u.offset + i].y;
+        uint32_t topic;
+        if (draw.K) {
+            const uint64_t id = draw.ids ? draw.ids[slot] : draw.id_base + slot;
+            topic = uniform_topic(draw.seed, kInitAssignStream, id, draw.K);
+        } else {
+            topic = z[slot];
+        }
+        atomicAdd(brow + topic, 1u);
+    }
 }
 
 cudaError_t launch_recount(const uint2* tok, const Unit* units, uint32_t n_units, const uint16_t* z,
-                           uint32_t* B, uint32_t K_pad, cudaStream_t s) {
+                           uint32_t* B, uint32_t K_pad, RecountDraw draw, cudaStream_t s) {
     if (n_units == 0) return cudaSuccess;
-    recount_kernel<<<n_units, 256, 0, s>>>(tok, units, z, B, K_pad);
+    recount_kernel<<<n_units, 256, 0, s>>>(tok, units, z, B, K_pad, draw);
     return cudaGetLastError();
 }
 

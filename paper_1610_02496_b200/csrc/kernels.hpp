@@ -121,7 +121,13 @@ cudaError_t launch_sched_counts(const uint32_t* schedule, const uint32_t* seg_le
 // gather_assignments: u16 topics by slot -> u32 topics in corpus order.
 cudaError_t launch_assignments(const uint16_t* z, const uint32_t* input_of_slot, uint64_t T, uint32_t* out,
                                cudaStream_t s);
+// K != 0: the topics are init_assignments draws (recomputed from the token ids, not read from z).
+struct RecountDraw {
+    uint64_t seed, id_base;
+    const uint64_t* ids;
+    uint32_t K;
+};
 cudaError_t launch_recount(const uint2* tok, const Unit* units, uint32_t n_units,
-                           const uint16_t* z, uint32_t* B, uint32_t K_pad, cudaStream_t s);
+                           const uint16_t* z, uint32_t* B, uint32_t K_pad, RecountDraw draw, cudaStream_t s);
 
 }  // namespace slda

@@ -269,7 +269,7 @@ def test_checkpoint_roundtrip_and_resume(tmp_path):
 VARIANT_CASES = ["c1", "long_docs", "empty_docs", "shuffled", "k_large", "nytimes_small", "k1"]
 
 
-@pytest.mark.parametrize("variant", ["SLDA_SAMPLER=g2", "SLDA_SAMPLER=g4", "SLDA_SAMPLER=s4",
+@pytest.mark.parametrize("variant", ["SLDA_SAMPLER=g2", "SLDA_SAMPLER=g4", "SLDA_SAMPLER=s4", "SLDA_SAMPLER=q256", "SLDA_SAMPLER=p256",
                                      "SLDA_SAMPLER=q512", "SLDA_SSC=sort"])
 @pytest.mark.parametrize("name", VARIANT_CASES)
 def test_kernel_variants_match_reference(name, variant, golden, monkeypatch):
