@@ -104,32 +104,22 @@ void nccl_check(ncclResult_t r, const char* what) {
 }
 
 // --------------------------------------------------------------- buffers --
-// Device buffer (cudaMalloc).  A stream-ordered variant (cudaMallocAsync on the engine stream)
-// exists for scratch, but fresh pool memory maps slower than cudaMalloc: measured at C3 setup,
-// 0.68 s pooled vs 0.43 s, so setup uses plain allocations.
 struct DevMem {
     void* p = nullptr;
     size_t bytes = 0;
-    cudaStream_t stream = nullptr;
-    bool pooled = false;
     DevMem() = default;
-    explicit DevMem(cudaStream_t s) : stream(s), pooled(true) {}
     DevMem(const DevMem&) = delete;
     DevMem& operator=(const DevMem&) = delete;
     ~DevMem() { release(); }
     void release() {
-        if (p) {
-            if (pooled) cudaFreeAsync(p, stream);
-            else cudaFree(p);
-        }
+        if (p) cudaFree(p);
         p = nullptr;
         bytes = 0;
     }
     void alloc(size_t n, size_t* tally) {
         release();
         if (n == 0) n = 16;
-        if (pooled) cuda_check(cudaMallocAsync(&p, n, stream), "cudaMallocAsync");
-        else cuda_check(cudaMalloc(&p, n), "cudaMalloc");
+        cuda_check(cudaMalloc(&p, n), "cudaMalloc");
         bytes = n;
         if (tally) *tally += n;
     }
@@ -319,7 +309,7 @@ void slda_engine::build(const slda_corpus_view& cv, const slda_config& c) {
     auto t_last = std::chrono::steady_clock::now();
     auto phase = [&](const char* name) {
         if (!trace) return;
-        if  CK(cudaStreamSynchronize);
+        if (stream) CK(cudaStreamSynchronize(stream));
         const auto now = std::chrono::steady_clock::now();
         std::fprintf(stderr, "[slda setup] %-28s %8.1f ms\n", name,
                      std::chrono::duration<double, std::milli>(now - t_last).count());
@@ -351,7 +341,7 @@ void slda_engine::build(const slda_corpus_view& cv, const slda_config& c) {
                              val.as<slda::ValidateOut>(), stream));
     slda::ValidateOut vo;
     CK(cudaMemcpyAsync(&vo, val.p, sizeof(vo), cudaMemcpyDeviceToHost, stream));
-    CK(cudaStreamSynchronize);
+    CK(cudaStreamSynchronize(stream));
     phase("h2d+validate");
     if (vo.bad_doc != ~0ull) validation("token " + std::to_string(vo.bad_doc) + ": doc outside the shard range");
     if (vo.bad_word != ~0ull) validation("token " + std::to_string(vo.bad_word) + ": word id out of range");
@@ -437,7 +427,7 @@ void slda_engine::build(const slda_corpus_view& cv, const slda_config& c) {
         }
         CK(slda::launch_ids_by_slot(cv.token_ids ? ids_in.as<uint64_t>() : nullptr,
                                     input_of_slot.as<uint32_t>(), T, id_base, ids.as<uint64_t>(), stream));
-        CK(cudaStreamSynchronize);
+        CK(cudaStreamSynchronize(stream));
     }
 
     // C_dk rows (header + entries, capacity len_d + 1 rounded to 8 entries, 32-byte
@@ -569,13 +559,12 @@ void slda_engine::build(const slda_corpus_view& cv, const slda_config& c) {
 
     phase("long docs + init topics");
     // C_dk (rebuild_doc_topic), C_wk (count_chunk_into), phi + trees.
-    ssc;
+    ssc(stream);
     CK(cudaMemsetAsync(B.p, 0, B.bytes, stream));
-    slda::RecountDraw rd{seed, id_base, ids.p ? ids.as<uint64_t>() : nullptr, draw ? K : 0u};
     CK(slda::launch_recount(tok.as<uint2>(), units.as<slda::Unit>(), n_units, z.as<uint16_t>(),
-                            B.as<uint32_t>(), K_pad, rd, stream));
+                            B.as<uint32_t>(), K_pad, stream));
     m_step();
-    CK(cudaStreamSynchronize);
+    CK(cudaStreamSynchronize(stream));
     nnz = d2h_scalar(nnz_counter());
     phase("ssc + recount + m_step");
 }
