@@ -561,8 +561,9 @@ void slda_engine::build(const slda_corpus_view& cv, const slda_config& c) {
     // C_dk (rebuild_doc_topic), C_wk (count_chunk_into), phi + trees.
     ssc(stream);
     CK(cudaMemsetAsync(B.p, 0, B.bytes, stream));
+    slda::RecountDraw rd{seed, id_base, ids.p ? ids.as<uint64_t>() : nullptr, draw ? K : 0u};
     CK(slda::launch_recount(tok.as<uint2>(), units.as<slda::Unit>(), n_units, z.as<uint16_t>(),
-                            B.as<uint32_t>(), K_pad, stream));
+                            B.as<uint32_t>(), K_pad, rd, stream));
     m_step();
     CK(cudaStreamSynchronize(stream));
     nnz = d2h_scalar(nnz_counter());
