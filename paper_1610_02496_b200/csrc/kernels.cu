@@ -1112,8 +1112,7 @@ struct SscBitmapSmem {
     uint32_t* bm1;    // ceil(K_pad/1024) words (bit w = bm0[w] != 0)
     uint16_t* wpre;   // per bm0 word: rank of its first topic
     uint16_t* wlist;  // non-empty bm0 words in ascending order
-    uint16_t* tlist;  // distinct topics in ascending order
-    uint32_t* cnt;    // count per rank
+    uint32_t* ent;    // per rank: topic (low 16 bits) | count (high 16 bits, smem atomics)
 };
 
 __device__ __forceinline__ uint32_t warp_incl_scan(uint32_t x, uint32_t lane) {
@@ -1163,10 +1162,7 @@ __device__ __forceinline__ uint32_t ssc_doc_bitmap(const uint16_t* z, uint32_t n
         const uint32_t incl = warp_incl_scan(c, lane);
         uint32_t pos = nnz + incl - c;
         if (e < m) w.wpre[wi] = static_cast<uint16_t>(pos);
-        for (uint32_t bits = bits0; bits; bits &= bits - 1u) {
-            w.tlist[pos] = static_cast<uint16_t>((wi << 5) | (__ffs(bits) - 1));
-            w.cnt[pos++] = 0u;
-        }
+        for (uint32_t bits = bits0; bits; bits &= bits - 1u) w.ent[pos++] = (wi << 5) | (__ffs(bits) - 1);
         nnz += __shfl_sync(0xffffffffu, incl, 31);
     }
     __syncwarp();
@@ -1175,14 +1171,17 @@ __device__ __forceinline__ uint32_t ssc_doc_bitmap(const uint16_t* z, uint32_t n
         if (key[r] != 0xFFFFFFFFu) {
             const uint32_t wi = key[r] >> 5;
             const uint32_t rank = w.wpre[wi] + __popc(w.bm0[wi] & ((1u << (key[r] & 31u)) - 1u));
-            atomicAdd(w.cnt + rank, 1u);
+            atomicAdd(w.ent + rank, 1u << 16);
         }
     }
     __syncwarp();
 #pragma unroll
     for (uint32_t r = 0; r < R; ++r)
         if (key[r] != 0xFFFFFFFFu) w.bm0[key[r] >> 5] = 0u;
-    for (uint32_t e = lane; e < nnz; e += 32) out_row[1 + e] = static_cast<uint32_t>(w.tlist[e]) | (w.cnt[e] << tbits);
+    for (uint32_t e = lane; e < nnz; e += 32) {
+        const uint32_t x = w.ent[e];
+        out_row[1 + e] = (x & 0xFFFFu) | ((x >> 16) << tbits);
+    }
     const uint32_t padded = (nnz + 8u) & ~7u;
     for (uint32_t e = nnz + 1 + lane; e < padded; e += 32) out_row[e] = 0u;
     if (lane == 0) out_row[0] = nnz - 1u;
@@ -1194,7 +1193,7 @@ constexpr uint32_t kSscBmWarps = 8;
 
 __host__ __device__ inline size_t ssc_bitmap_warp_bytes(uint32_t K_pad) {
     const size_t n0 = (K_pad + 31u) / 32u, n1 = (n0 + 31u) / 32u;
-    const size_t b = 4 * n0 + 4 * n1 + 2 * n0 + 2 * kSscWarpCap + 2 * kSscWarpCap + 4 * kSscWarpCap;
+    const size_t b = 4 * n0 + 4 * n1 + 4 * kSscWarpCap + 2 * n0 + 2 * kSscWarpCap;
     return (b + 15u) & ~static_cast<size_t>(15u);
 }
 
@@ -1207,10 +1206,9 @@ __global__ void __launch_bounds__(kSscBmWarps * 32) ssc_bitmap_kernel(SscArgs a)
     SscBitmapSmem w;
     w.bm0 = reinterpret_cast<uint32_t*>(base);
     w.bm1 = w.bm0 + n0;
-    w.cnt = w.bm1 + n1;
-    w.wpre = reinterpret_cast<uint16_t*>(w.cnt + kSscWarpCap);
+    w.ent = w.bm1 + n1;
+    w.wpre = reinterpret_cast<uint16_t*>(w.ent + kSscWarpCap);
     w.wlist = w.wpre + n0;
-    w.tlist = w.wlist + kSscWarpCap;
     for (uint32_t i = lane; i < n0 + n1; i += 32) w.bm0[i] = 0u;
     __syncwarp();
     unsigned long long nnz_acc = 0;
