@@ -657,7 +657,7 @@ __global__ void __launch_bounds__(NT, NT <= 128 ? 3 : 2) sampler_stream_kernel(S
 // sum visits the 4 sectors of a line in order -- lane j adds its 8 products to the value lane
 // j-1 handed it (shuffle) -- so every intermediate is the reference's.  The per-sector sums
 // double as the prefix_search checkpoints (a few hundred bytes per warp instead of a stage).
-template <int NT, int MINB, int L>
+template <int NT, int MINB, int L, bool kCompact>
 __global__ void __launch_bounds__(NT, MINB) sampler_quad_kernel(SamplerArgs a) {
     constexpr uint32_t NW = NT / 32;
     constexpr uint32_t TPR = 32u / L;  // tokens per round (L lanes each, L sectors per group)
@@ -705,8 +705,9 @@ __global__ void __launch_bounds__(NT, MINB) sampler_quad_kernel(SamplerArgs a) {
             Sector c = zero_sector();
             if (act) c = ldg_sector(row + 2 * sub);
             const uint32_t hw = __shfl_sync(0xffffffffu, c.lo.x, lead);  // header: word 0 of sector 0
-            const uint32_t nnz = act ? (hw & tmask) + 1u : 0u;
-            const uint32_t nsect = act ? (nnz + 8u) >> 3 : 0u;
+            // wide: [nnz-1 | entries | pad to 8]; compact: word 0 = nsect | nnz << 16
+            const uint32_t nnz = act ? (kCompact ? hw >> 16 : (hw & tmask) + 1u) : 0u;
+            const uint32_t nsect = act ? (kCompact ? hw & 0xFFFFu : (nnz + 8u) >> 3) : 0u;
             if (sub == 0) entries += nnz;
             const uint32_t max_groups = __reduce_max_sync(0xffffffffu, (nsect + L - 1u) / L);
             float* ck = ckw + ti * kCkStride;
@@ -714,17 +715,32 @@ __global__ void __launch_bounds__(NT, MINB) sampler_quad_kernel(SamplerArgs a) {
             // Products of this lane's sector, then the chain over the line's 4 sectors in order.
             auto consume = [&](const Sector& q, uint32_t g) {
                 const uint32_t sec = L * g + sub;
-                float p[8];
+                constexpr int NP = kCompact ? 16 : 8;  // products per sector
+                float p[NP];
                 if (sec < nsect) {
                     const uint32_t es[8] = {q.lo.x, q.lo.y, q.lo.z, q.lo.w, q.hi.x, q.hi.y, q.hi.z, q.hi.w};
+                    if (kCompact) {
+                        // Each word: (c0 * phi[t0]) then phi[t1]; absent entries are +0 (acc_word_compact).
 #pragma unroll
-                    for (int w = 0; w < 8; ++w) p[w] = entry_mass<false>(es[w], tbits, tmask, s_bhat);
+                        for (int w = 0; w < 8; ++w) {
+                            const WordEntries e = decode_word(es[w]);
+                            const bool hdr = w == 0 && sec == 0;  // the header word
+                            float p0 = 0.0f, p1 = 0.0f;
+                            if (e.v0 && !hdr) p0 = s_bhat[e.t0];
+                            if (e.v1 && !hdr) p1 = s_bhat[e.t1];
+                            p[2 * w] = __fmul_rn(e.c0, p0);
+                            p[2 * w + 1] = p1;
+                        }
+                    } else {
+#pragma unroll
+                        for (int w = 0; w < 8; ++w) p[w] = entry_mass<false>(es[w], tbits, tmask, s_bhat);
+                    }
                 }
 #pragma unroll
                 for (uint32_t j = 0; j < L; ++j) {
                     if (sub == j && sec < nsect) {
 #pragma unroll
-                        for (int w = 0; w < 8; ++w) run = __fadd_rn(run, p[w]);
+                        for (int w = 0; w < NP; ++w) run = __fadd_rn(run, p[w]);
                         if (sec < kCk) ck[sec] = run;
                     }
                     run = __shfl_sync(0xffffffffu, run, lead | j);
@@ -758,7 +774,8 @@ __global__ void __launch_bounds__(NT, MINB) sampler_quad_kernel(SamplerArgs a) {
             if (ub < __fdiv_rn(S, __fadd_rn(S, qv))) {
                 const float xs = __fmul_rn(up, S);
                 if (xs == 0.0f) {
-                    topic = __ldg(reinterpret_cast<const uint32_t*>(row) + 1) & tmask;  // first real entry
+                    const uint32_t e1 = __ldg(reinterpret_cast<const uint32_t*>(row) + 1);  // first real entry
+                    topic = kCompact ? (e1 & 0x7FFFu) : (e1 & tmask);
                 } else {
                     const float* ck = ckw + lane * kCkStride;
                     const uint32_t stored = my_ns < kCk ? my_ns : kCk;
@@ -772,10 +789,18 @@ __global__ void __launch_bounds__(NT, MINB) sampler_quad_kernel(SamplerArgs a) {
                         const Sector q = ldg_sector(row + 2 * sc);
                         const uint32_t es[8] = {q.lo.x, q.lo.y, q.lo.z, q.lo.w, q.hi.x, q.hi.y, q.hi.z, q.hi.w};
                         bool found = false;
+                        if (kCompact) {
+                            bool need = true;
 #pragma unroll
-                        for (int w = 0; w < 8; ++w) {
-                            r = __fadd_rn(r, entry_mass<false>(es[w], tbits, tmask, s_bhat));
-                            if (!found && r >= xs) { topic = es[w] & tmask; found = true; }
+                            for (int w = 0; w < 8; ++w)
+                                if (w > 0 || sc != 0) scan_word_compact<false>(r, need, topic, xs, es[w], s_bhat);
+                            found = !need;
+                        } else {
+#pragma unroll
+                            for (int w = 0; w < 8; ++w) {
+                                r = __fadd_rn(r, entry_mass<false>(es[w], tbits, tmask, s_bhat));
+                                if (!found && r >= xs) { topic = es[w] & tmask; found = true; }
+                            }
                         }
                         if (found) break;
                     }
@@ -840,17 +865,22 @@ size_t sampler_quad_smem(const SamplerArgs& a, int nt) {
     return sizeof(float) * (static_cast<size_t>(a.K_pad) + a.l8_stride + static_cast<size_t>(nt / 32) * 32u * 17u);
 }
 
-template <int NT, int MINB, int L = 4>
-cudaError_t launch_quad_t(const SamplerArgs& a, uint32_t n_units, cudaStream_t s) {
+template <int NT, int MINB, int L = 4, bool C = false>
+cudaError_t launch_quad_t1(const SamplerArgs& a, uint32_t n_units, cudaStream_t s) {
     static bool configured = false;
     if (!configured) {
-        const cudaError_t e = cudaFuncSetAttribute(sampler_quad_kernel<NT, MINB, L>,
+        const cudaError_t e = cudaFuncSetAttribute(sampler_quad_kernel<NT, MINB, L, C>,
                                                    cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
         if (e != cudaSuccess) return e;
         configured = true;
     }
-    sampler_quad_kernel<NT, MINB, L><<<n_units, NT, sampler_quad_smem(a, NT), s>>>(a);
+    sampler_quad_kernel<NT, MINB, L, C><<<n_units, NT, sampler_quad_smem(a, NT), s>>>(a);
     return cudaGetLastError();
+}
+template <int NT, int MINB, int L = 4>
+cudaError_t launch_quad_t(const SamplerArgs& a, uint32_t n_units, cudaStream_t s) {
+    return a.compact ? launch_quad_t1<NT, MINB, L, true>(a, n_units, s)
+                     : launch_quad_t1<NT, MINB, L, false>(a, n_units, s);
 }
 
 // Launch shape (SLDA_SAMPLER overrides for experiments; default by phi row size):
@@ -869,7 +899,7 @@ cudaError_t launch_sampler(const SamplerArgs& a, uint32_t n_units, cudaStream_t 
     // (C3 K=10K: 100.0 vs 102.6 ms for 4-sector groups; C2 K=1K: 21.5 vs 23.5 ms for 2-sector
     // groups), else 4-sector groups (large phi rows), else 2-sector groups.
     int shape = a.shape;
-    if (shape < 0 && !a.compact) {
+    if (shape < 0) {
         if (phi_bytes <= 24 * 1024 && 4 * sampler_quad_smem(a, 256) <= 227 * 1024) shape = 7;
         else if (2 * sampler_quad_smem(a, 512) <= 227 * 1024) shape = 6;
     }
@@ -881,19 +911,19 @@ cudaError_t launch_sampler(const SamplerArgs& a, uint32_t n_units, cudaStream_t 
         if (a.compact) return cudaErrorInvalidConfiguration;
         return launch_sampler_t<512, 2, 2, true, false>(a, n_units, s);
     }
-    if (!a.compact && shape == 6 && sampler_quad_smem(a, 512) <= 227 * 1024)
+    if (shape == 6 && sampler_quad_smem(a, 512) <= 227 * 1024)
         return launch_quad_t<512, 2>(a, n_units, s);
-    if (!a.compact && shape == 7 && sampler_quad_smem(a, 256) <= 227 * 1024)
+    if (shape == 7 && sampler_quad_smem(a, 256) <= 227 * 1024)
         return launch_quad_t<256, 4>(a, n_units, s);
-    if (!a.compact && shape == 8 && sampler_quad_smem(a, 512) <= 227 * 1024)
+    if (shape == 8 && sampler_quad_smem(a, 512) <= 227 * 1024)
         return launch_quad_t<512, 1>(a, n_units, s);
-    if (!a.compact && shape == 9 && sampler_quad_smem(a, 256) <= 227 * 1024)
+    if (shape == 9 && sampler_quad_smem(a, 256) <= 227 * 1024)
         return launch_quad_t<256, 3>(a, n_units, s);
-    if (!a.compact && shape == 10 && sampler_quad_smem(a, 512) <= 227 * 1024)
+    if (shape == 10 && sampler_quad_smem(a, 512) <= 227 * 1024)
         return launch_quad_t<512, 2, 2>(a, n_units, s);
-    if (!a.compact && shape == 11 && sampler_quad_smem(a, 256) <= 227 * 1024)
+    if (shape == 11 && sampler_quad_smem(a, 256) <= 227 * 1024)
         return launch_quad_t<256, 4, 2>(a, n_units, s);
-    if (!a.compact && shape == 12 && sampler_quad_smem(a, 512) <= 227 * 1024)
+    if (shape == 12 && sampler_quad_smem(a, 512) <= 227 * 1024)
         return launch_quad_t<512, 2, 8>(a, n_units, s);
     if (!a.compact && shape == 3 && sampler_smem(a, 256, 4, false) <= 227 * 1024)
         return launch_stream_t<256, 4>(a, n_units, s);
@@ -1124,7 +1154,7 @@ __device__ __forceinline__ uint32_t warp_incl_scan(uint32_t x, uint32_t lane) {
     return x;
 }
 
-template <int R>
+template <int R, bool kCompact>
 __device__ __forceinline__ uint32_t ssc_doc_bitmap(const uint16_t* z, uint32_t n, uint32_t lane,
                                                    const SscBitmapSmem& w, uint32_t n1, uint32_t* out_row,
                                                    uint32_t tbits) {
@@ -1178,13 +1208,24 @@ __device__ __forceinline__ uint32_t ssc_doc_bitmap(const uint16_t* z, uint32_t n
 #pragma unroll
     for (uint32_t r = 0; r < R; ++r)
         if (key[r] != 0xFFFFFFFFu) w.bm0[key[r] >> 5] = 0u;
-    for (uint32_t e = lane; e < nnz; e += 32) {
-        const uint32_t x = w.ent[e];
-        out_row[1 + e] = (x & 0xFFFFu) | ((x >> 16) << tbits);
+    if (kCompact) {  // 16-bit slots (compact_chunk), header written by compact_finish
+        uint16_t* row16 = reinterpret_cast<uint16_t*>(out_row);
+        uint32_t pos = 2;
+        for (uint32_t b = 0; b < nnz; b += 32) {
+            const uint32_t e = b + lane;
+            const uint32_t x = e < nnz ? w.ent[e] : 0u;
+            compact_chunk(row16, pos, e < nnz, x & 0xFFFFu, x >> 16, lane);
+        }
+        compact_finish(row16, pos, nnz, lane);
+    } else {
+        for (uint32_t e = lane; e < nnz; e += 32) {
+            const uint32_t x = w.ent[e];
+            out_row[1 + e] = (x & 0xFFFFu) | ((x >> 16) << tbits);
+        }
+        const uint32_t padded = (nnz + 8u) & ~7u;
+        for (uint32_t e = nnz + 1 + lane; e < padded; e += 32) out_row[e] = 0u;
+        if (lane == 0) out_row[0] = nnz - 1u;
     }
-    const uint32_t padded = (nnz + 8u) & ~7u;
-    for (uint32_t e = nnz + 1 + lane; e < padded; e += 32) out_row[e] = 0u;
-    if (lane == 0) out_row[0] = nnz - 1u;
     __syncwarp();
     return nnz;
 }
@@ -1197,6 +1238,7 @@ __host__ __device__ inline size_t ssc_bitmap_warp_bytes(uint32_t K_pad) {
     return (b + 15u) & ~static_cast<size_t>(15u);
 }
 
+template <bool kCompact>
 __global__ void __launch_bounds__(kSscBmWarps * 32) ssc_bitmap_kernel(SscArgs a) {
     extern __shared__ __align__(16) unsigned char s_raw[];
     const uint32_t wid = threadIdx.x >> 5, lane = lane_id();
@@ -1220,11 +1262,11 @@ __global__ void __launch_bounds__(kSscBmWarps * 32) ssc_bitmap_kernel(SscArgs a)
         uint32_t* row = a.A + __ldg(a.row4 + d) * 4u;
         const uint16_t* z = a.z + s0;
         uint32_t nnz;
-        if (n <= 32) nnz = ssc_doc_bitmap<1>(z, n, lane, w, n1, row, a.tbits);
-        else if (n <= 64) nnz = ssc_doc_bitmap<2>(z, n, lane, w, n1, row, a.tbits);
-        else if (n <= 128) nnz = ssc_doc_bitmap<4>(z, n, lane, w, n1, row, a.tbits);
-        else if (n <= 256) nnz = ssc_doc_bitmap<8>(z, n, lane, w, n1, row, a.tbits);
-        else nnz = ssc_doc_bitmap<16>(z, n, lane, w, n1, row, a.tbits);
+        if (n <= 32) nnz = ssc_doc_bitmap<1, kCompact>(z, n, lane, w, n1, row, a.tbits);
+        else if (n <= 64) nnz = ssc_doc_bitmap<2, kCompact>(z, n, lane, w, n1, row, a.tbits);
+        else if (n <= 128) nnz = ssc_doc_bitmap<4, kCompact>(z, n, lane, w, n1, row, a.tbits);
+        else if (n <= 256) nnz = ssc_doc_bitmap<8, kCompact>(z, n, lane, w, n1, row, a.tbits);
+        else nnz = ssc_doc_bitmap<16, kCompact>(z, n, lane, w, n1, row, a.tbits);
         nnz_acc += nnz;
     }
     if (lane == 0 && nnz_acc) atomicAdd(a.nnz_total, nnz_acc);
@@ -1289,17 +1331,18 @@ template <bool kCompact>
 cudaError_t launch_ssc_t(const SscArgs& a, cudaStream_t s) {
     if (a.D > 0) {
         const size_t bm_smem = kSscBmWarps * ssc_bitmap_warp_bytes(a.K_pad);
-        if (!kCompact && !a.use_sort && bm_smem <= 200 * 1024) {
+        if (!a.use_sort && bm_smem <= 200 * 1024) {
             static bool configured = false;
             if (!configured) {
-                cudaFuncSetAttribute(ssc_bitmap_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+                cudaFuncSetAttribute(ssc_bitmap_kernel<kCompact>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     200 * 1024);
                 configured = true;
             }
             // Short-lived CTAs (16 documents per warp) rather than a persistent grid: SSC runs
             // beside the M-step on a low-priority stream, and retiring CTAs let the scheduler
             // hand SMs to the higher-priority colsum/phi CTAs.
             const uint32_t blocks = static_cast<uint32_t>((a.D + kSscBmWarps * 16u - 1) / (kSscBmWarps * 16u));
-            ssc_bitmap_kernel<<<blocks, kSscBmWarps * 32, bm_smem, s>>>(a);
+            ssc_bitmap_kernel<kCompact><<<blocks, kSscBmWarps * 32, bm_smem, s>>>(a);
         } else {
             const uint32_t blocks = grid_for(a.D, kSscWarps, 148u * 8u);
             ssc_warp_kernel<kCompact><<<blocks, kSscWarps * 32, 0, s>>>(a);
