@@ -664,6 +664,7 @@ __global__ void __launch_bounds__(NT, MINB) sampler_quad_kernel(SamplerArgs a) {
     constexpr uint32_t kCk = 16;       // checkpointed sectors per token (128 entries)
     constexpr uint32_t kCkStride = 17; // odd: different tokens' checkpoints fall in different banks
     extern __shared__ __align__(16) float sm[];
+    __shared__ uint32_t s_next;  // next unclaimed 32-token batch of the unit
     const Unit unit = a.units[blockIdx.x];
     const uint32_t v = unit.word;
     float* s_bhat = sm;
@@ -687,11 +688,14 @@ __global__ void __launch_bounds__(NT, MINB) sampler_quad_kernel(SamplerArgs a) {
     const uint32_t warp = threadIdx.x >> 5;
     float* ckw = s_ck + warp * 32u * kCkStride;
     unsigned long long entries = 0;
+    if (threadIdx.x == 0) s_next = NW * 32u;
     __syncthreads();
 
-    // A batch of 32 tokens per warp: four rounds of 8 tokens x 4 lanes stream the rows and form
-    // S; then lane l finishes token l of the batch (draws, branch, prefix search / tree).
-    for (uint32_t base = warp * 32u; base < unit.length; base += NW * 32u) {
+    // A batch of 32 tokens per warp: L rounds of 32/L tokens x L lanes stream the rows and form
+    // S; then lane l finishes token l of the batch (draws, branch, prefix search / tree).  The
+    // first batch of warp w is tokens [32w, 32w + 32); later ones are claimed dynamically, so
+    // the CTA's warps finish the unit together.
+    for (uint32_t base = warp * 32u; base < unit.length;) {
         const bool mine = base + lane < unit.length;
         const uint2 tk = mine ? __ldg(a.tok + unit.offset + base + lane) : make_uint2(0u, 0u);  // {row quads, slot}
         float S = 0.0f;
@@ -814,7 +818,9 @@ __global__ void __launch_bounds__(NT, MINB) sampler_quad_kernel(SamplerArgs a) {
             a.z[tk.y] = static_cast<uint16_t>(topic);
             atomicAdd(brow + topic, 1u);
         }
-        __syncwarp();
+        uint32_t nb = 0;
+        if (lane == 0) nb = atomicAdd(&s_next, 32u);
+        base = __shfl_sync(0xffffffffu, nb, 0);
     }
     if (a.row_entries) {
         for (int o = 16; o > 0; o >>= 1) entries += __shfl_xor_sync(0xffffffffu, entries, o);
@@ -869,8 +875,9 @@ template <int NT, int MINB, int L = 4, bool C = false>
 cudaError_t launch_quad_t1(const SamplerArgs& a, uint32_t n_units, cudaStream_t s) {
     static bool configured = false;
     if (!configured) {
+        // 227 KB per block minus the kernel's static shared memory (the batch counter).
         const cudaError_t e = cudaFuncSetAttribute(sampler_quad_kernel<NT, MINB, L, C>,
-                                                   cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+                                                   cudaFuncAttributeMaxDynamicSharedMemorySize, 226 * 1024);
         if (e != cudaSuccess) return e;
         configured = true;
     }
