@@ -828,6 +828,223 @@ __global__ void __launch_bounds__(NT, MINB) sampler_quad_kernel(SamplerArgs a) {
     }
 }
 
+// The same algorithm with the next round's first line prefetched in each round's last group
+// slot and the next batch claimed a batch ahead; the per-unit scalars live in shared memory to
+// make room in the 64-register budget (C3 K=10K: 95.5 -> 92.8 ms; C2: 19.8 -> 20.5 ms).
+template <int NT, int MINB, int L, bool kCompact, bool kPrefetchNext = true>
+__global__ void __launch_bounds__(NT, MINB) sampler_quad_pf_kernel(SamplerArgs a) {
+    constexpr uint32_t NW = NT / 32;
+    constexpr uint32_t TPR = 32u / L;  // tokens per round (L lanes each, L sectors per group)
+    constexpr uint32_t kCk = 16;       // checkpointed sectors per token (128 entries)
+    constexpr uint32_t kCkStride = 17; // odd: different tokens' checkpoints fall in different banks
+    extern __shared__ __align__(16) float sm[];
+    __shared__ uint32_t s_next;  // next unclaimed 32-token batch of the unit
+    __shared__ float s_total, s_qv;  // the word's tree total and Q_v (read in the sampling step only)
+    const Unit unit = a.units[blockIdx.x];
+    const uint32_t v = unit.word;
+    float* s_bhat = sm;
+    float* s_l8 = sm + a.K_pad;
+    float* s_ck = s_l8 + a.l8_stride;  // [NW][32 tokens][kCkStride]
+    {
+        const float4* gb = reinterpret_cast<const float4*>(a.bhat + static_cast<size_t>(v) * a.K_pad);
+        float4* sb = reinterpret_cast<float4*>(sm);
+        for (uint32_t i = threadIdx.x; i < a.K_pad / 4; i += NT) sb[i] = __ldg(gb + i);
+        const float4* gl = reinterpret_cast<const float4*>(a.l8 + static_cast<size_t>(v) * a.l8_stride);
+        float4* sl = reinterpret_cast<float4*>(s_l8);
+        for (uint32_t i = threadIdx.x; i < a.l8_stride / 4; i += NT) sl[i] = __ldg(gl + i);
+    }
+    const uint32_t tbits = a.tbits, tmask = (1u << tbits) - 1u;
+    const uint4* A4 = reinterpret_cast<const uint4*>(a.A);
+    const uint32_t lane = lane_id(), t = lane / L, sub = lane % L, lead = lane & ~(L - 1u);
+    const uint32_t warp = threadIdx.x >> 5;
+    float* ckw = s_ck + warp * 32u * kCkStride;
+    uint32_t entries = 0;
+    if (threadIdx.x == 0) {
+        s_next = NW * 32u;
+        s_total = __ldg(a.l4 + static_cast<size_t>(v) * a.K_pad + a.K_pad - 1);  // padded with the total
+        s_qv = __ldg(a.q + v);
+    }
+    __syncthreads();
+
+    // A batch of 32 tokens per warp: L rounds of 32/L tokens x L lanes stream the rows and form
+    // S; then lane l finishes token l of the batch (draws, branch, prefix search / tree).  The
+    // first batch of warp w is tokens [32w, 32w + 32); later ones are claimed dynamically, so
+    // the CTA's warps finish the unit together.
+    // The next batch is claimed when a batch starts, and each round's last group slot loads
+    // the NEXT round's first line (its header sets that round's length), so rounds never start
+    // on an exposed load.
+    uint32_t base = warp * 32u;
+    uint2 tk = base + lane < unit.length ? __ldg(a.tok + unit.offset + base + lane) : make_uint2(0u, 0u);
+    Sector c = zero_sector();
+    if (kPrefetchNext) {
+        const uint32_t rq0 = __shfl_sync(0xffffffffu, tk.x, t);
+        if (base + t < unit.length) c = ldg_sector(A4 + rq0 + 2 * sub);
+    }
+    while (base < unit.length) {
+        const bool mine = base + lane < unit.length;
+        uint32_t nb = 0;
+        uint2 tk_nx = make_uint2(0u, 0u);
+        if (kPrefetchNext) {  // claim the next batch now and load its token records
+            if (lane == 0) nb = atomicAdd(&s_next, 32u);
+            nb = __shfl_sync(0xffffffffu, nb, 0);
+            if (nb + lane < unit.length) tk_nx = __ldg(a.tok + unit.offset + nb + lane);
+        }
+        float S = 0.0f;
+        uint32_t my_ns = 0;
+#pragma unroll 1
+        for (uint32_t r = 0; r < L; ++r) {
+            const uint32_t ti = TPR * r + t;  // this lane group's token within the batch
+            if (__all_sync(0xffffffffu, base + TPR * r >= unit.length)) break;
+            const bool act = base + ti < unit.length;
+            const uint4* row = A4 + __shfl_sync(0xffffffffu, tk.x, ti);
+            if (!kPrefetchNext) {  // this round's first line, loaded now
+                c = zero_sector();
+                if (act) c = ldg_sector(row + 2 * sub);
+            }
+            const uint32_t hw = __shfl_sync(0xffffffffu, c.lo.x, lead);  // header: word 0 of sector 0
+            // wide: [nnz-1 | entries | pad to 8]; compact: word 0 = nsect | nnz << 16
+            const uint32_t nnz = act ? (kCompact ? hw >> 16 : (hw & tmask) + 1u) : 0u;
+            const uint32_t nsect = act ? (kCompact ? hw & 0xFFFFu : (nnz + 8u) >> 3) : 0u;
+            if (sub == 0) entries += nnz;
+            const uint32_t max_groups = __reduce_max_sync(0xffffffffu, (nsect + L - 1u) / L);
+            float* ck = ckw + ti * kCkStride;
+            float run = 0.0f;
+            // Products of this lane's sector, then the chain over the line's 4 sectors in order.
+            auto consume = [&](const Sector& q, uint32_t g) {
+                const uint32_t sec = L * g + sub;
+                constexpr int NP = kCompact ? 16 : 8;  // products per sector
+                float p[NP];
+                if (sec < nsect) {
+                    const uint32_t es[8] = {q.lo.x, q.lo.y, q.lo.z, q.lo.w, q.hi.x, q.hi.y, q.hi.z, q.hi.w};
+                    if (kCompact) {
+                        // Each word: (c0 * phi[t0]) then phi[t1]; absent entries are +0 (acc_word_compact).
+#pragma unroll
+                        for (int w = 0; w < 8; ++w) {
+                            const WordEntries e = decode_word(es[w]);
+                            const bool hdr = w == 0 && sec == 0;  // the header word
+                            float p0 = 0.0f, p1 = 0.0f;
+                            if (e.v0 && !hdr) p0 = s_bhat[e.t0];
+                            if (e.v1 && !hdr) p1 = s_bhat[e.t1];
+                            p[2 * w] = __fmul_rn(e.c0, p0);
+                            p[2 * w + 1] = p1;
+                        }
+                    } else {
+#pragma unroll
+                        for (int w = 0; w < 8; ++w) p[w] = entry_mass<false>(es[w], tbits, tmask, s_bhat);
+                    }
+                }
+#pragma unroll
+                for (uint32_t j = 0; j < L; ++j) {
+                    if (sub == j && sec < nsect) {
+#pragma unroll
+                        for (int w = 0; w < NP; ++w) run = __fadd_rn(run, p[w]);
+                        if (sec < kCk) ck[sec] = run;
+                    }
+                    run = __shfl_sync(0xffffffffu, run, lead | j);
+                }
+            };
+            // Group g+1 (or the next round's first line) loads while group g is consumed; two
+            // groups per trip so no registers are copied.
+            auto fetch = [&](uint32_t g, Sector& dst) {
+                if (g < max_groups) {  // warp-uniform
+                    if (L * g + sub < nsect) dst = ldg_sector(row + 2 * (L * g + sub));
+                } else if (kPrefetchNext) {
+                    const bool last = r + 1 == L || base + TPR * (r + 1) >= unit.length;
+                    const uint32_t nrq = __shfl_sync(0xffffffffu, last ? tk_nx.x : tk.x, last ? t : ti + TPR);
+                    if (last ? nb + t < unit.length : base + ti + TPR < unit.length)
+                        dst = ldg_sector(A4 + nrq + 2 * sub);
+                }
+            };
+            if (max_groups == 0) {
+                fetch(0, c);
+            } else {
+                Sector n = c;
+                for (uint32_t g = 0;; g += 2) {
+                    fetch(g + 1, n);
+                    consume(c, g);
+                    if (g + 1 >= max_groups) { c = n; break; }
+                    fetch(g + 2, c);
+                    consume(n, g + 1);
+                    if (g + 2 >= max_groups) break;
+                }
+            }
+            // Token ti's S and sector count to its owning lane (lane ti).
+            const uint32_t src = ((lane - TPR * r) & (TPR - 1u)) * L;
+            const float xS = __shfl_sync(0xffffffffu, run, src);
+            const uint32_t xn = __shfl_sync(0xffffffffu, nsect, src);
+            if (lane / TPR == r) {
+                S = xS;
+                my_ns = xn;
+            }
+        }
+        __syncwarp();
+        // sample_token (sampler.hpp:183-204), one token per lane.
+        if (mine) {
+            const float qv = s_qv, total = s_total;
+            const float* l4row = a.l4 + static_cast<size_t>(v) * a.K_pad;
+            float ub, up;
+            const uint64_t id = a.ids ? __ldg(a.ids + tk.y) : a.id_base + tk.y;
+            draw2_f32(a.seed, a.stream_kind, id, ub, up);
+            const uint4* row = A4 + tk.x;
+            uint32_t topic = 0;
+            if (ub < __fdiv_rn(S, __fadd_rn(S, qv))) {
+                const float xs = __fmul_rn(up, S);
+                if (xs == 0.0f) {
+                    const uint32_t e1 = __ldg(reinterpret_cast<const uint32_t*>(row) + 1);  // first real entry
+                    topic = kCompact ? (e1 & 0x7FFFu) : (e1 & tmask);
+                } else {
+                    const float* ck = ckw + lane * kCkStride;
+                    const uint32_t stored = my_ns < kCk ? my_ns : kCk;
+                    uint32_t lo = 0, hi = stored;  // first checkpoint >= xs (or stored)
+                    while (lo < hi) {
+                        const uint32_t mid = (lo + hi) >> 1;
+                        if (ck[mid] >= xs) hi = mid; else lo = mid + 1;
+                    }
+                    float r = lo > 0 ? ck[lo - 1] : 0.0f;
+                    for (uint32_t sc = lo; sc < my_ns; ++sc) {  // one sector unless past the checkpoints
+                        const Sector q = ldg_sector(row + 2 * sc);
+                        const uint32_t es[8] = {q.lo.x, q.lo.y, q.lo.z, q.lo.w, q.hi.x, q.hi.y, q.hi.z, q.hi.w};
+                        bool found = false;
+                        if (kCompact) {
+                            bool need = true;
+#pragma unroll
+                            for (int w = 0; w < 8; ++w)
+                                if (w > 0 || sc != 0) scan_word_compact<false>(r, need, topic, xs, es[w], s_bhat);
+                            found = !need;
+                        } else {
+#pragma unroll
+                            for (int w = 0; w < 8; ++w) {
+                                r = __fadd_rn(r, entry_mass<false>(es[w], tbits, tmask, s_bhat));
+                                if (!found && r >= xs) { topic = es[w] & tmask; found = true; }
+                            }
+                        }
+                        if (found) break;
+                    }
+                }
+            } else {
+                float x = __fmul_rn(up, total);  // WaryTree::sample(p * total)
+                if (!(x <= total)) x = total;
+                const uint32_t k = tree_search(x, s_l8, a.n_l8, l4row);
+                topic = k < a.K ? k : a.K - 1;
+            }
+            a.z[tk.y] = static_cast<uint16_t>(topic);
+            atomicAdd(a.B + static_cast<size_t>(v) * a.K_pad + topic, 1u);
+        }
+        if (kPrefetchNext) {
+            base = nb;
+            tk = tk_nx;
+        } else {
+            if (lane == 0) nb = atomicAdd(&s_next, 32u);
+            base = __shfl_sync(0xffffffffu, nb, 0);
+            tk = base + lane < unit.length ? __ldg(a.tok + unit.offset + base + lane) : make_uint2(0u, 0u);
+        }
+    }
+    if (a.row_entries) {
+        for (int o = 16; o > 0; o >>= 1) entries += __shfl_xor_sync(0xffffffffu, entries, o);
+        if (lane == 0) atomicAdd(a.row_entries, static_cast<unsigned long long>(entries));
+    }
+}
+
 size_t sampler_smem(const SamplerArgs& a, int nt, int g, bool global_phi) {
     const size_t stage_row = 32u * static_cast<size_t>(g) + 16u;
     return sizeof(float) * ((global_phi ? 0 : static_cast<size_t>(a.K_pad)) + a.l8_stride) +
@@ -871,23 +1088,25 @@ size_t sampler_quad_smem(const SamplerArgs& a, int nt) {
     return sizeof(float) * (static_cast<size_t>(a.K_pad) + a.l8_stride + static_cast<size_t>(nt / 32) * 32u * 17u);
 }
 
-template <int NT, int MINB, int L = 4, bool C = false>
+template <int NT, int MINB, int L, bool C, bool PF>
 cudaError_t launch_quad_t1(const SamplerArgs& a, uint32_t n_units, cudaStream_t s) {
     static bool configured = false;
+    auto kern = PF ? sampler_quad_pf_kernel<NT, MINB, L, C> : sampler_quad_kernel<NT, MINB, L, C>;
     if (!configured) {
         // 227 KB per block minus the kernel's static shared memory (the batch counter).
-        const cudaError_t e = cudaFuncSetAttribute(sampler_quad_kernel<NT, MINB, L, C>,
-                                                   cudaFuncAttributeMaxDynamicSharedMemorySize, 226 * 1024);
+        const cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 226 * 1024);
         if (e != cudaSuccess) return e;
         configured = true;
     }
-    sampler_quad_kernel<NT, MINB, L, C><<<n_units, NT, sampler_quad_smem(a, NT), s>>>(a);
+    kern<<<n_units, NT, sampler_quad_smem(a, NT), s>>>(a);
     return cudaGetLastError();
 }
-template <int NT, int MINB, int L = 4>
+// PF: the next round's first line is prefetched in each round's last group slot (C3 K=10K:
+// 95.5 -> 92.8 ms; short-phi C2: 19.8 -> 20.5 ms, so only the 512-thread shape uses it).
+template <int NT, int MINB, int L = 4, bool PF = (NT >= 512)>
 cudaError_t launch_quad_t(const SamplerArgs& a, uint32_t n_units, cudaStream_t s) {
-    return a.compact ? launch_quad_t1<NT, MINB, L, true>(a, n_units, s)
-                     : launch_quad_t1<NT, MINB, L, false>(a, n_units, s);
+    return a.compact ? launch_quad_t1<NT, MINB, L, true, PF>(a, n_units, s)
+                     : launch_quad_t1<NT, MINB, L, false, PF>(a, n_units, s);
 }
 
 // Launch shape (SLDA_SAMPLER overrides for experiments; default by phi row size):
