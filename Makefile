@@ -15,7 +15,8 @@ NVFLAGS := $(ARCH) -O3 -lineinfo -fmad=false -std=c++17 -Xcompiler -fPIC,-Wall \
            -Xptxas -v --expt-relaxed-constexpr -Iinclude
 CXXFLAGS := -O2 -std=c++20 -fPIC -Wall -Wextra -ffp-contract=off -Iinclude
 
-CU_SRCS := $(CSRC)/engine.cu $(CSRC)/kernels.cu $(CSRC)/heldout.cu
+CU_SRCS := $(CSRC)/engine.cu $(CSRC)/sampler.cu $(CSRC)/ssc.cu $(CSRC)/mstep.cu $(CSRC)/setup.cu \
+           $(CSRC)/heldout.cu
 CU_OBJS := $(patsubst $(CSRC)/%.cu,$(BUILD)/%.o,$(CU_SRCS))
 HOST_OBJS := $(BUILD)/host.o
 LIB     := $(PKG)/libsaberlda.so

@@ -35,6 +35,10 @@ CONFIGS = {
     "c2": dict(name="C2 NYTimes-shaped", D=300_000, V=100_000, T=100_000_000, K=1_000),
     "c3": dict(name="C3 PubMed-shaped", D=8_200_000, V=141_000, T=738_000_000, K=10_000),
     "c4": dict(name="C4 ClueWeb-subset-shaped", D=19_400_000, V=100_000, T=7_100_000_000, K=10_000),
+    # One rank's document shard of C4 at 8 GPUs (T/8 tokens, D/8 documents): the per-GPU work of
+    # the 8-B200 run, measurable on one GPU (the M-step collectives are not in this number).
+    "c4_shard": dict(name="C4 ClueWeb-subset-shaped, one of 8 document shards", D=2_425_000, V=100_000,
+                     T=887_500_000, K=10_000),
     "c5_k100": dict(name="C5 NYTimes-shaped K=100", D=300_000, V=100_000, T=100_000_000, K=100),
     "c5_k10000": dict(name="C5 NYTimes-shaped K=10K", D=300_000, V=100_000, T=100_000_000, K=10_000),
     "c5_k50000": dict(name="C5 NYTimes-shaped K=50K", D=300_000, V=100_000, T=100_000_000, K=50_000),

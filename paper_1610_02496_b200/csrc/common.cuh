@@ -71,4 +71,10 @@ __device__ __forceinline__ uint32_t uniform_topic(uint64_t seed, uint32_t kind, 
 
 __device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31u; }
 
+// Grid size for a grid-stride kernel over n items: at most `cap` CTAs (default 32 per SM).
+inline uint32_t grid_for(uint64_t n, uint32_t threads, uint32_t cap = 148u * 32u) {
+    const uint64_t g = (n + threads - 1) / threads;
+    return static_cast<uint32_t>(g == 0 ? 1 : (g > cap ? cap : g));
+}
+
 }  // namespace slda

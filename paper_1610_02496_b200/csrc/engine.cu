@@ -200,8 +200,8 @@ struct slda_engine {
     uint32_t rank = 0, world = 1;
     uint32_t nseg = 0, n_units = 0, n_long = 0;
     bool doc_major = true;
-    bool compact = false;  // C_dk row format (kernels.cu: compact 16-bit slots or wide 32-bit)
-    int sampler_shape = -1;  // SLDA_SAMPLER (kernels.cu launch_sampler); -1 = default by K
+    bool compact = false;  // C_dk row format (row_format.cuh: compact 16-bit slots or wide 32-bit)
+    int sampler_shape = -1;  // SLDA_SAMPLER (sampler.cu launch_sampler); -1 = default by K
     bool ssc_sort = false;   // SLDA_SSC=sort: the bitonic-sort SSC instead of the bitmap one
     bool serial = false;     // SLDA_SERIAL=1: SSC on the main stream (measurement of each kernel alone)
     uint32_t wshift = 0;  // word field shift of the execution-order key
@@ -442,7 +442,7 @@ void slda_engine::build(const slda_corpus_view& cv, const slda_config& c) {
             validation("document of length " + std::to_string(max_len) +
                        " exceeds the packed C_dk count range at this K");
     }
-    // Row format: the 32-bit wide rows by default.  The compact 16-bit format (kernels.cu)
+    // Row format: the 32-bit wide rows by default.  The compact 16-bit format (row_format.cuh)
     // is opt-in (SLDA_ROW_FORMAT=compact): it cuts sampler DRAM bytes ~25% and wins on
     // short-document corpora at large K (C3: 131 vs 139 ms/iteration) but loses where the
     // sampler is issue-bound or documents are long (C2 42.7 vs 31.0, C5 K=10K 88.9 vs 55.5;
@@ -955,7 +955,7 @@ int slda_get_assignments(slda_engine* e, uint32_t* out) {
 }  // extern "C"
 
 namespace {
-// C_dk rows copied to the host (kernels.cu formats); empty documents have none.
+// C_dk rows copied to the host (row_format.cuh formats); empty documents have none.
 struct HostRows {
     std::vector<uint32_t> doc_start, row4, A;
     uint32_t mask = 0, tbits = 0;

@@ -1,4 +1,4 @@
-// kernels.hpp -- host launchers for the ESCA device kernels (kernels.cu).
+// kernels.hpp -- host launchers for the ESCA device kernels (sampler.cu, ssc.cu, mstep.cu, setup.cu).
 #pragma once
 
 #include <cstdint>
@@ -13,7 +13,7 @@ struct Unit {
 };
 
 constexpr uint32_t kUnitMaxTokens = 8192;  // sampler: max tokens per unit (one CTA)
-// Compact C_dk rows (16-bit slots, kernels.cu) need topics < 0x7FFF and counts/nnz < 2^16.
+// Compact C_dk rows (16-bit slots, row_format.cuh) need topics < 0x7FFF and counts/nnz < 2^16.
 constexpr uint32_t kCompactMaxK = 32767;
 constexpr uint32_t kCompactMaxLen = 65535;
 constexpr uint32_t kSscWarpCap = 512;      // SSC: docs up to this length take the warp path

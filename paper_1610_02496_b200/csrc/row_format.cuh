@@ -1,0 +1,219 @@
+// row_format.cuh -- device-side C_dk row access shared by the sampler kernels (sampler.cu) and
+// the SSC row encoder (ssc.cu): sector loads, the wide / compact entry decoders, the per-warp
+// cooperative staging, and the tree search.  Layouts: DESIGN.md §3.
+#pragma once
+
+#include "common.cuh"
+#include "kernels.hpp"
+
+namespace slda {
+
+// phi row lookup: shared memory (staged row) or, when the row is too large to stage
+// (kGlobalPhi, K >~ 45K), the global row through L1/L2.
+template <bool kGlobalPhi>
+__device__ __forceinline__ float entry_mass(uint32_t e, uint32_t tbits, uint32_t tmask, const float* phi) {
+    const float p = kGlobalPhi ? __ldg(phi + (e & tmask)) : phi[e & tmask];
+    return __fmul_rn(__uint2float_rn(e >> tbits), p);
+}
+
+template <bool kGlobalPhi>
+__device__ __forceinline__ float acc_quad(float s, const uint4& q, uint32_t tbits, uint32_t tmask,
+                                          const float* phi) {
+    s = __fadd_rn(s, entry_mass<kGlobalPhi>(q.x, tbits, tmask, phi));
+    s = __fadd_rn(s, entry_mass<kGlobalPhi>(q.y, tbits, tmask, phi));
+    s = __fadd_rn(s, entry_mass<kGlobalPhi>(q.z, tbits, tmask, phi));
+    return __fadd_rn(s, entry_mass<kGlobalPhi>(q.w, tbits, tmask, phi));
+}
+
+// One 32-byte sector (8 C_dk entries) per lane: a 256-bit load (LDG.E.256 on sm_100a),
+// not allocated in L1 (rows are streamed; the reuse is in L2).
+struct Sector {
+    uint4 lo, hi;
+};
+__device__ __forceinline__ Sector ldg_sector(const uint4* p) {
+    Sector s;
+    asm("ld.global.nc.L1::no_allocate.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(s.lo.x), "=r"(s.lo.y), "=r"(s.lo.z), "=r"(s.lo.w), "=r"(s.hi.x), "=r"(s.hi.y),
+                   "=r"(s.hi.z), "=r"(s.hi.w)
+                 : "l"(p));
+    return s;
+}
+
+__device__ __forceinline__ Sector zero_sector() { return Sector{make_uint4(0u, 0u, 0u, 0u), make_uint4(0u, 0u, 0u, 0u)}; }
+
+// Compact C_dk rows (K <= kCompactMaxK): 16-bit slots, two per 32-bit word.  Word 0 =
+// nsect | nnz << 16.  Then the entries in ascending topic order: a count-1 entry is one slot
+// holding its topic; a count >= 2 entry is a whole word (topic | 0x8000, count) at an even
+// slot, a null slot (0xFFFF) padding the odd slot before it when needed; the row ends with
+// null slots up to a sector (16 slots).  Pairs never straddle a word, so every word decodes
+// on its own (sector checkpoints carry no parse state), and a count-1 entry needs no count
+// conversion: f32(1) * phi == phi.  Versus the 32-bit wide format this halves the bytes of
+// count-1 entries, the majority while documents are spread over many topics.
+constexpr uint32_t kNull16 = 0xFFFFu;
+
+// lower_bound over the word's L4 prefix (== WaryTree::sample, acceptance.cpp:140-200):
+// binary search of the staged L8 level (first 8-block whose last prefix >= x), then one
+// 32-byte sector of L4.  Returns the first index with L4 >= x (x <= total).
+__device__ __forceinline__ uint32_t tree_search(float x, const float* s_l8, uint32_t n_l8, const float* l4row) {
+    uint32_t lo = 0, hi = n_l8 - 1;  // s_l8[n_l8 - 1] == total >= x
+    while (lo < hi) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (s_l8[mid] >= x) hi = mid; else lo = mid + 1;
+    }
+    const Sector b = ldg_sector(reinterpret_cast<const uint4*>(l4row + lo * kLeaf));
+    const uint32_t below = (__uint_as_float(b.lo.x) < x) + (__uint_as_float(b.lo.y) < x) +
+                           (__uint_as_float(b.lo.z) < x) + (__uint_as_float(b.lo.w) < x) +
+                           (__uint_as_float(b.hi.x) < x) + (__uint_as_float(b.hi.y) < x) +
+                           (__uint_as_float(b.hi.z) < x) + (__uint_as_float(b.hi.w) < x);
+    return lo * kLeaf + below;
+}
+
+// Per-warp staging of C_dk rows.  Lane-private random row reads cap at ~1.5 TB/s on B200
+// (L1TEX: one line per lane per load); the warp-cooperative layout (adjacent lanes read
+// adjacent sectors of one row) is coalesced per row and measured at 3.7-6 TB/s
+// (scripts/microbench_rows.cu).  A group is G sectors (8G entries) of each of the warp's 32
+// rows, loaded by 32/G rows per instruction (scripts/mb_pattern.cu: G=4 moves the same row
+// bytes with ~20% fewer L1TEX wavefronts than G=2).  The (32G+16)-byte row stride keeps the
+// cooperative stores and each lane's 128-bit reads of its own row bank-conflict free.
+template <int G>
+struct Stage {
+    static constexpr uint32_t kRowsPerInst = 32 / G;
+    static constexpr uint32_t kRow = 32 * G + 16;
+    static constexpr uint32_t kWarp = 32 * kRow;
+};
+// Per-sector running sums for the first kCkSectors sectors (96 entries): the prefix pass
+// of the sparse branch re-reads one sector instead of the row.  (12: at K = 10K two
+// 512-thread CTAs fit one SM.)
+constexpr uint32_t kCkSectors = 12;
+
+__device__ __forceinline__ void sts_sector(unsigned char* p, const Sector& q) {
+    *reinterpret_cast<uint4*>(p) = q.lo;
+    *reinterpret_cast<uint4*>(p + 16) = q.hi;
+}
+
+// Cooperative load of sectors [gs, gs + G) of each of the warp's 32 rows (registers),
+// and its store into the stage.  Per row kRowsPerInst*j + grp: rq = quad offset, ns = sector
+// limit (0: skip), gs = first sector.  Sectors past a row's limit are neither loaded nor
+// stored (the owning lane never reads them), so finished rows cost no L1TEX wavefronts.
+template <int G>
+__device__ __forceinline__ void load_group(const uint4* A4, const uint32_t (&rq)[G], const uint32_t (&ns)[G],
+                                           const uint32_t (&gs)[G], uint32_t sub, Sector (&q)[G]) {
+#pragma unroll
+    for (uint32_t j = 0; j < G; ++j) {
+        const uint32_t sec = gs[j] + sub;
+        q[j] = sec < ns[j] ? ldg_sector(A4 + rq[j] + 2 * sec) : zero_sector();
+    }
+}
+template <int G>
+__device__ __forceinline__ void store_group(const Sector (&q)[G], const uint32_t (&ns)[G], const uint32_t (&gs)[G],
+                                            uint32_t sub, uint32_t grp, unsigned char* stage) {
+#pragma unroll
+    for (uint32_t j = 0; j < G; ++j)
+        if (gs[j] + sub < ns[j])
+            sts_sector(stage + (Stage<G>::kRowsPerInst * j + grp) * Stage<G>::kRow + sub * 32, q[j]);
+}
+template <int G>
+__device__ __forceinline__ void stage_group(const uint4* A4, const uint32_t (&rq)[G], const uint32_t (&ns)[G],
+                                            const uint32_t (&gs)[G], uint32_t sub, uint32_t grp,
+                                            unsigned char* stage) {
+    Sector q[G];
+    load_group<G>(A4, rq, ns, gs, sub, q);
+    store_group<G>(q, ns, gs, sub, grp, stage);
+}
+
+// ---- Row decoding for the sampler (both row formats) ----------------------------------------
+template <bool kGlobalPhi>
+__device__ __forceinline__ float ld_phi(const float* phi, uint32_t t) {
+    return kGlobalPhi ? __ldg(phi + t) : phi[t];
+}
+
+// Compact format word: up to two entries (see compact_chunk).  f32(1) * phi == phi, so a
+// count-1 entry adds phi[topic] directly, exactly as the reference's s += f32(1) * phi.
+// Branch-free word decode (lanes of a warp see different word kinds): the first slot is a
+// pair (topic|0x8000, count), a single, or null; the second slot is a single or null unless
+// the word is a pair.  Absent entries contribute +0 (s + +0 == s for the running sums, which
+// are >= +0) and their gathers are predicated off.
+struct WordEntries {
+    uint32_t t0, t1;   // topics
+    float c0;          // count of the first entry (1 for a single)
+    bool v0, v1;       // entries present
+};
+__device__ __forceinline__ WordEntries decode_word(uint32_t w) {
+    const uint32_t h0 = w & 0xFFFFu, h1 = w >> 16;
+    const bool pair = (h0 & 0x8000u) != 0;
+    WordEntries e;
+    e.v0 = h0 != kNull16;
+    e.t0 = h0 & 0x7FFFu;
+    e.c0 = pair ? __uint2float_rn(h1) : 1.0f;
+    e.v1 = !pair && h1 != kNull16;
+    e.t1 = h1;
+    return e;
+}
+
+template <bool kGlobalPhi>
+__device__ __forceinline__ float acc_word_compact(float s, uint32_t w, const float* phi) {
+    const WordEntries e = decode_word(w);
+    float p0 = 0.0f, p1 = 0.0f;
+    if (e.v0) p0 = ld_phi<kGlobalPhi>(phi, e.t0);
+    if (e.v1) p1 = ld_phi<kGlobalPhi>(phi, e.t1);
+    s = __fadd_rn(s, __fmul_rn(e.c0, p0));  // f32(1) * phi == phi; f32(c) * phi as the reference
+    return __fadd_rn(s, p1);
+}
+
+template <bool kGlobalPhi>
+__device__ __forceinline__ void scan_word_compact(float& run, bool& need, uint32_t& topic, float xs, uint32_t w,
+                                                  const float* phi) {
+    const WordEntries e = decode_word(w);
+    float p0 = 0.0f, p1 = 0.0f;
+    if (e.v0) p0 = ld_phi<kGlobalPhi>(phi, e.t0);
+    if (e.v1) p1 = ld_phi<kGlobalPhi>(phi, e.t1);
+    run = __fadd_rn(run, __fmul_rn(e.c0, p0));
+    if (need && e.v0 && run >= xs) { topic = e.t0; need = false; }
+    run = __fadd_rn(run, p1);
+    if (need && e.v1 && run >= xs) { topic = e.t1; need = false; }
+}
+
+// First pass over one staged sector (32 bytes) of a row.  Sector 0 starts with the header
+// (compact: skipped; wide: a count-0 entry that adds +0).
+template <bool kGlobalPhi, bool kCompact>
+__device__ __forceinline__ float acc_sector(float s, const unsigned char* p, uint32_t sec, uint32_t tbits,
+                                            uint32_t tmask, const float* phi) {
+    const uint4 lo = *reinterpret_cast<const uint4*>(p);
+    const uint4 hi = *reinterpret_cast<const uint4*>(p + 16);
+    if (kCompact) {
+        if (sec != 0) s = acc_word_compact<kGlobalPhi>(s, lo.x, phi);
+        s = acc_word_compact<kGlobalPhi>(s, lo.y, phi);
+        s = acc_word_compact<kGlobalPhi>(s, lo.z, phi);
+        s = acc_word_compact<kGlobalPhi>(s, lo.w, phi);
+        s = acc_word_compact<kGlobalPhi>(s, hi.x, phi);
+        s = acc_word_compact<kGlobalPhi>(s, hi.y, phi);
+        s = acc_word_compact<kGlobalPhi>(s, hi.z, phi);
+        return acc_word_compact<kGlobalPhi>(s, hi.w, phi);
+    }
+    s = acc_quad<kGlobalPhi>(s, lo, tbits, tmask, phi);
+    return acc_quad<kGlobalPhi>(s, hi, tbits, tmask, phi);
+}
+
+// Prefix re-scan of one staged sector: first running sum >= xs.
+template <bool kGlobalPhi, bool kCompact>
+__device__ __forceinline__ void scan_sector(float& run, bool& need, uint32_t& topic, float xs,
+                                            const unsigned char* p, uint32_t sec, uint32_t tbits,
+                                            uint32_t tmask, const float* phi) {
+    const uint4 lo = *reinterpret_cast<const uint4*>(p);
+    const uint4 hi = *reinterpret_cast<const uint4*>(p + 16);
+    const uint32_t es[8] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};
+#pragma unroll
+    for (int w = 0; w < 8; ++w) {
+        if (kCompact) {
+            if (w > 0 || sec != 0) scan_word_compact<kGlobalPhi>(run, need, topic, xs, es[w], phi);
+        } else {
+            run = __fadd_rn(run, entry_mass<kGlobalPhi>(es[w], tbits, tmask, phi));
+            if (need && run >= xs) {
+                topic = es[w] & tmask;
+                need = false;
+            }
+        }
+    }
+}
+
+}  // namespace slda

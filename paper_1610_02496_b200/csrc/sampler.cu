@@ -1,0 +1,957 @@
+// sampler.cu -- K3: the ESCA sampling step on sm_100a.
+//
+// Reference paths are relative to /root/reference/proj.  Each kernel names the reference
+// function it replaces.  See DESIGN.md §4 (kernels, rooflines) and §6 (measurements).
+#include <cstdlib>
+#include <string>
+
+#include "row_format.cuh"
+
+namespace slda {
+
+// ============================================================================
+// K3 sampler -- process_segment (trainer.cpp:265-291) + sample_token<float>
+// (sampler.hpp:166-204) + the C_wk accumulation of accumulate_word_topic
+// (counts.cpp:127-132).  One CTA per heavy-first work unit of one word; the
+// word's phi row and its L8 level are staged in shared memory; each warp stages
+// its 32 tokens' C_dk rows cooperatively (coalesced), and each lane samples one
+// token so that the sparse mass S and the in-place prefix run as the reference's
+// sequential f32 chains.
+// ============================================================================
+
+template <int NT, int G, int MINB, bool kGlobalPhi, bool kCompact>
+__global__ void __launch_bounds__(NT, MINB) sampler_kernel(SamplerArgs a) {
+    using St = Stage<G>;
+    extern __shared__ __align__(16) float sm[];
+    const uint32_t v = a.units[blockIdx.x].word;
+    const float* s_bhat = kGlobalPhi ? a.bhat + static_cast<size_t>(v) * a.K_pad : sm;
+    float* s_l8 = kGlobalPhi ? sm : sm + a.K_pad;  // l8_stride (L4[8j+7], padded with the total)
+    float* s_ck = s_l8 + a.l8_stride;       // [kCkSectors][NT]
+    unsigned char* s_stage = reinterpret_cast<unsigned char*>(s_ck + kCkSectors * NT);
+
+    const Unit unit = a.units[blockIdx.x];
+    const float* l4row = a.l4 + static_cast<size_t>(v) * a.K_pad;
+    const float total = __ldg(l4row + a.K_pad - 1);  // padded with the row total
+    {
+        if (!kGlobalPhi) {
+            const float4* gb = reinterpret_cast<const float4*>(a.bhat + static_cast<size_t>(v) * a.K_pad);
+            float4* sb = reinterpret_cast<float4*>(sm);
+            for (uint32_t i = threadIdx.x; i < a.K_pad / 4; i += NT) sb[i] = __ldg(gb + i);
+        }
+        const float4* gl = reinterpret_cast<const float4*>(a.l8 + static_cast<size_t>(v) * a.l8_stride);
+        float4* sl = reinterpret_cast<float4*>(s_l8);
+        for (uint32_t i = threadIdx.x; i < a.l8_stride / 4; i += NT) sl[i] = __ldg(gl + i);
+    }
+    const float qv = __ldg(a.q + v);
+    uint32_t* brow = a.B + static_cast<size_t>(v) * a.K_pad;
+    const uint32_t tbits = a.tbits;
+    const uint32_t tmask = (1u << tbits) - 1u;
+    const uint4* A4 = reinterpret_cast<const uint4*>(a.A);
+    float* ck = s_ck + threadIdx.x;
+    // Cooperative layout: lane -> row kRowsPerInst*j + lane%kRowsPerInst, sector
+    // lane/kRowsPerInst.  A quarter warp then stores 8 different rows at the same sector
+    // offset, which the (32G+16)-byte row stride spreads over all 32 banks.
+    const uint32_t lane = lane_id(), sub = lane / St::kRowsPerInst, grp = lane % St::kRowsPerInst;
+    unsigned char* stage = s_stage + (threadIdx.x >> 5) * St::kWarp;
+    const unsigned char* mine = stage + lane * St::kRow;  // this lane's staged sectors
+    unsigned long long entries = 0;
+    __syncthreads();
+
+    const uint32_t rounds = (unit.length + NT - 1) / NT;  // CTA-uniform
+    for (uint32_t r = 0; r < rounds; ++r) {
+        const uint32_t i = r * NT + threadIdx.x;
+        const bool active = i < unit.length;
+        const uint2 t = active ? __ldg(a.tok + unit.offset + i) : make_uint2(0u, 0u);  // {row quads, slot}
+        uint32_t rq[G], ns[G], gs[G];
+#pragma unroll
+        for (uint32_t j = 0; j < G; ++j) {
+            rq[j] = __shfl_sync(0xffffffffu, t.x, St::kRowsPerInst * j + grp);
+            ns[j] = __shfl_sync(0xffffffffu, active ? G : 0u, St::kRowsPerInst * j + grp);  // speculative
+            gs[j] = 0;
+        }
+        __syncwarp();
+        stage_group<G>(A4, rq, ns, gs, sub, grp, stage);
+        __syncwarp();
+
+        // Wide row = [header (nnz-1, count 0) | entries | zero-count padding to 8]: header and
+        // padding add +0 to every running sum.  Compact row: word 0 = nsect | nnz << 16.
+        const uint32_t w0 = reinterpret_cast<const uint4*>(mine)->x;
+        const uint32_t nnz = active ? (kCompact ? w0 >> 16 : (w0 & tmask) + 1u) : 0u;
+        const uint32_t nsect = active ? (kCompact ? w0 & 0xFFFFu : (nnz + 8u) >> 3) : 0u;
+        entries += nnz;
+#pragma unroll
+        for (uint32_t j = 0; j < G; ++j) ns[j] = __shfl_sync(0xffffffffu, nsect, St::kRowsPerInst * j + grp);
+        const uint32_t ngroups = (nsect + G - 1) / G;
+        const uint32_t max_groups = __reduce_max_sync(0xffffffffu, ngroups);
+
+        float ub = 0.0f, up = 0.0f;
+        if (active) {
+            const uint64_t id = a.ids ? __ldg(a.ids + t.y) : a.id_base + t.y;
+            draw2_f32(a.seed, a.stream_kind, id, ub, up);
+        }
+
+        // make_branch_context: S = sum_i f32(cnt_i) * bhat[top_i], sequential f32.
+        // Group g+1 is loaded into registers while group g is consumed from the stage.
+        float s = 0.0f;
+        for (uint32_t g = 0; g < max_groups; ++g) {
+            Sector next[G];
+            const bool more = g + 1 < max_groups;
+            if (more) {
+#pragma unroll
+                for (uint32_t j = 0; j < G; ++j) gs[j] = G * (g + 1);
+                load_group<G>(A4, rq, ns, gs, sub, next);
+            }
+#pragma unroll
+            for (uint32_t u = 0; u < G; ++u) {
+                const uint32_t sec = G * g + u;
+                if (sec < nsect) {
+                    s = acc_sector<kGlobalPhi, kCompact>(s, mine + 32 * u, sec, tbits, tmask, s_bhat);
+                    if (sec < kCkSectors) ck[sec * NT] = s;
+                }
+            }
+            if (more) {
+                __syncwarp();
+                store_group<G>(next, ns, gs, sub, grp, stage);
+                __syncwarp();
+            }
+        }
+
+        uint32_t topic = 0;
+        bool need = false;  // sparse branch still searching its prefix
+        uint32_t sec = 0;
+        float run = 0.0f, xs = 0.0f;
+        if (active) {
+            if (ub < __fdiv_rn(s, __fadd_rn(s, qv))) {
+                // Sparse branch: first running prefix >= p*S (prefix_search, sampler.hpp:18-41).
+                xs = __fmul_rn(up, s);
+                if (xs == 0.0f) {
+                    // every prefix is >= 0: the first real entry (word 1 in both formats)
+                    const uint32_t e1 = __ldg(reinterpret_cast<const uint32_t*>(A4 + t.x) + 1);
+                    topic = kCompact ? (e1 & 0x7FFFu) : (e1 & tmask);
+                } else {
+                    // The first sector whose end sum reaches xs holds the crossing; its re-scan
+                    // restarts from the previous checkpoint, the same f32 value the first pass
+                    // held there, so it is bit-identical.
+                    const uint32_t stored = nsect < kCkSectors ? nsect : kCkSectors;
+                    uint32_t lo = 0, hi = stored;  // first checkpoint >= xs (or stored)
+                    while (lo < hi) {
+                        const uint32_t mid = (lo + hi) >> 1;
+                        if (ck[mid * NT] >= xs) hi = mid; else lo = mid + 1;
+                    }
+                    sec = lo;
+                    run = lo > 0 ? ck[(lo - 1) * NT] : 0.0f;
+                    need = true;
+                }
+            } else {
+                // Word branch: WaryTree::sample(p * total) (sampler.hpp:100-106).
+                float x = __fmul_rn(up, total);
+                if (!(x <= total)) x = total;
+                const uint32_t k = tree_search(x, s_l8, a.n_l8, l4row);
+                topic = k < a.K ? k : a.K - 1;
+            }
+        }
+        // Cooperative re-staging of the crossing sector of every searching lane.
+        while (__any_sync(0xffffffffu, need)) {
+            const uint32_t first = need ? sec : 0u;
+            const uint32_t lim = need ? sec + 1 : 0u;
+#pragma unroll
+            for (uint32_t j = 0; j < G; ++j) {
+                gs[j] = __shfl_sync(0xffffffffu, first, St::kRowsPerInst * j + grp);
+                ns[j] = __shfl_sync(0xffffffffu, lim, St::kRowsPerInst * j + grp);
+            }
+            __syncwarp();
+            stage_group<G>(A4, rq, ns, gs, sub, grp, stage);
+            __syncwarp();
+            if (need) {
+                scan_sector<kGlobalPhi, kCompact>(run, need, topic, xs, mine, sec, tbits, tmask, s_bhat);
+                ++sec;
+            }
+        }
+        if (active) {
+            a.z[t.y] = static_cast<uint16_t>(topic);
+            atomicAdd(brow + topic, 1u);
+        }
+    }
+    if (a.row_entries) {
+        // One atomic per warp.
+        for (int o = 16; o > 0; o >>= 1) entries += __shfl_xor_sync(0xffffffffu, entries, o);
+        if (lane == 0) atomicAdd(a.row_entries, entries);
+    }
+}
+
+// ---- K3' streaming sampler: the same draws, bit for bit, with lane refill -----------------------
+// The round-based kernel above advances a warp's 32 tokens in lock step: every round waits for
+// its longest row, re-reads the crossing sector with a second dependent round trip, and loads a
+// speculative group for every row.  Here each lane owns a sequence of tokens instead: the
+// warp streams G-sector groups of its lanes' CURRENT rows (cooperative, coalesced, next group
+// prefetched in registers); a lane whose row ends takes the next token of the unit at once
+// (warp ballot over a 32-token pool, CTA-wide dynamic batches), so the stream never waits for
+// the longest row.  The branch decision needs the whole row (S), so a finished token's last
+// step is deferred by one step: the one sector it still needs -- the sparse branch's crossing
+// sector (found from the per-sector checkpoints) or the tree branch's L4 block -- is loaded
+// lane-private in step t and resolved in step t+1, under the next step's consumption.
+// Arithmetic (make_branch_context, prefix_search, WaryTree::sample) is unchanged.
+template <int NT, int G>
+__global__ void __launch_bounds__(NT, NT <= 128 ? 3 : 2) sampler_stream_kernel(SamplerArgs a) {
+    using St = Stage<G>;
+    extern __shared__ __align__(16) float sm[];
+    __shared__ uint32_t s_next;  // next unclaimed 32-token batch (index within the unit)
+    const Unit unit = a.units[blockIdx.x];
+    const uint32_t v = unit.word;
+    float* s_bhat = sm;
+    float* s_l8 = sm + a.K_pad;
+    float* s_ck = s_l8 + a.l8_stride;  // [kCkSectors][NT]
+    unsigned char* s_stage = reinterpret_cast<unsigned char*>(s_ck + kCkSectors * NT);
+    const float* l4row = a.l4 + static_cast<size_t>(v) * a.K_pad;
+    const float total = __ldg(l4row + a.K_pad - 1);
+    {
+        const float4* gb = reinterpret_cast<const float4*>(a.bhat + static_cast<size_t>(v) * a.K_pad);
+        float4* sb = reinterpret_cast<float4*>(sm);
+        for (uint32_t i = threadIdx.x; i < a.K_pad / 4; i += NT) sb[i] = __ldg(gb + i);
+        const float4* gl = reinterpret_cast<const float4*>(a.l8 + static_cast<size_t>(v) * a.l8_stride);
+        float4* sl = reinterpret_cast<float4*>(s_l8);
+        for (uint32_t i = threadIdx.x; i < a.l8_stride / 4; i += NT) sl[i] = __ldg(gl + i);
+    }
+    if (threadIdx.x == 0) s_next = NT;  // warp w starts with batch [32w, 32w + 32)
+    const float qv = __ldg(a.q + v);
+    uint32_t* brow = a.B + static_cast<size_t>(v) * a.K_pad;
+    const uint32_t tbits = a.tbits, tmask = (1u << tbits) - 1u;
+    const uint4* A4 = reinterpret_cast<const uint4*>(a.A);
+    const uint2* toks = a.tok + unit.offset;
+    const uint32_t len = unit.length;
+    const uint32_t lane = lane_id(), sub = lane / St::kRowsPerInst, grp = lane % St::kRowsPerInst;
+    unsigned char* stage = s_stage + (threadIdx.x >> 5) * St::kWarp;
+    const unsigned char* mine = stage + lane * St::kRow;
+    float* ck = s_ck + threadIdx.x;
+    unsigned long long entries = 0;
+    __syncthreads();
+
+    // Token pool: pool = batch at pool_base (lane l holds token pool_base + l), nxt = the batch
+    // after it; pc = tokens of the pool already handed out.
+    uint32_t pool_base = (threadIdx.x >> 5) * 32u;
+    uint2 pool = pool_base + lane < len ? __ldg(toks + pool_base + lane) : make_uint2(0u, 0u);
+    auto claim = [&]() -> uint32_t {
+        uint32_t b = 0;
+        if (lane == 0) b = atomicAdd(&s_next, 32u);
+        return __shfl_sync(0xffffffffu, b, 0);
+    };
+    uint32_t next_base = claim();
+    uint2 nxt = next_base + lane < len ? __ldg(toks + next_base + lane) : make_uint2(0u, 0u);
+    uint32_t pc = 0;
+
+    // Current row (the one staged this step).
+    bool cur = false, hdr = false;  // hdr: the staged group is the row's first (header unread)
+    uint32_t c_rq = 0, c_slot = 0, c_ns = 0, c_base = 0;
+    float s = 0.0f;
+    // Pending resolution: 0 none, 1 sparse (scan sector p_sec from run p_run for xs), 2 tree
+    // (L4 block p_sec), 3 sparse with xs == 0 (the first real entry).
+    uint32_t p_kind = 0, p_slot = 0, p_sec = 0, p_rq = 0, p_ns = 0;
+    float p_run = 0.0f, p_x = 0.0f;
+    Sector psec = zero_sector();
+
+    // Hands out tokens to the lanes in `need` (ballot), in lane order.
+    auto take = [&](bool want, uint32_t& rq, uint32_t& slot) -> bool {
+        const uint32_t need = __ballot_sync(0xffffffffu, want);
+        const uint32_t idx = pc + __popc(need & ((1u << lane) - 1u));
+        const uint2 ra = make_uint2(__shfl_sync(0xffffffffu, pool.x, idx & 31u),
+                                    __shfl_sync(0xffffffffu, pool.y, idx & 31u));
+        const uint2 rb = make_uint2(__shfl_sync(0xffffffffu, nxt.x, idx & 31u),
+                                    __shfl_sync(0xffffffffu, nxt.y, idx & 31u));
+        const uint32_t gi = idx < 32u ? pool_base + idx : next_base + (idx - 32u);
+        const bool got = want && idx < 64u && gi < len;
+        rq = idx < 32u ? ra.x : rb.x;
+        slot = idx < 32u ? ra.y : rb.y;
+        pc += __popc(need);
+        if (pc >= 32u) {  // pool consumed: the next batch becomes the pool
+            pc -= 32u;
+            pool = nxt;
+            pool_base = next_base;
+            next_base = claim();
+            nxt = next_base + lane < len ? __ldg(toks + next_base + lane) : make_uint2(0u, 0u);
+        }
+        return got;
+    };
+
+    // First tokens and their first groups.
+    uint32_t t_rq = 0, t_slot = 0;
+    cur = take(true, t_rq, t_slot);
+    c_rq = t_rq;
+    c_slot = t_slot;
+    hdr = cur;
+    {
+        uint32_t rq[G], ns[G], gs[G];
+#pragma unroll
+        for (uint32_t j = 0; j < G; ++j) {
+            rq[j] = __shfl_sync(0xffffffffu, c_rq, St::kRowsPerInst * j + grp);
+            ns[j] = __shfl_sync(0xffffffffu, cur ? G : 0u, St::kRowsPerInst * j + grp);
+            gs[j] = 0;
+        }
+        stage_group<G>(A4, rq, ns, gs, sub, grp, stage);
+        __syncwarp();
+    }
+
+    while (__any_sync(0xffffffffu, cur || p_kind != 0)) {
+        // Header of a row whose first group is staged: [nnz-1 | entries | zero pad].
+        if (cur && hdr) {
+            const uint32_t nnz = (reinterpret_cast<const uint4*>(mine)->x & tmask) + 1u;
+            c_ns = (nnz + 8u) >> 3;
+            entries += nnz;
+            hdr = false;
+        }
+        // Next step's group per lane: the rest of this row, or the first group of a new token.
+        const bool ends = cur && c_base + G >= c_ns;
+        uint32_t n_rq = 0, n_slot = 0;
+        const bool got = take(ends, n_rq, n_slot);
+        uint32_t l_rq = 0, l_start = 0, l_lim = 0;
+        if (cur && !ends) {
+            l_rq = c_rq; l_start = c_base + G; l_lim = c_ns;
+        } else if (got) {
+            l_rq = n_rq; l_start = 0; l_lim = G;  // speculative first group (header inside)
+        }
+        uint32_t rq[G], ns[G], gs[G];
+#pragma unroll
+        for (uint32_t j = 0; j < G; ++j) {
+            const uint32_t src = St::kRowsPerInst * j + grp;
+            rq[j] = __shfl_sync(0xffffffffu, l_rq, src);
+            gs[j] = __shfl_sync(0xffffffffu, l_start, src);
+            ns[j] = __shfl_sync(0xffffffffu, l_lim, src);
+        }
+        Sector nx[G];
+        load_group<G>(A4, rq, ns, gs, sub, nx);
+
+        // make_branch_context over this step's sectors (sequential f32 chain).
+        if (cur) {
+#pragma unroll
+            for (uint32_t u = 0; u < G; ++u) {
+                const uint32_t sec = c_base + u;
+                if (sec < c_ns) {
+                    s = acc_sector<false, false>(s, mine + 32 * u, sec, tbits, tmask, s_bhat);
+                    if (sec < kCkSectors) ck[sec * NT] = s;
+                }
+            }
+        }
+
+        // Resolve the token finished in the previous step (its sector arrived meanwhile).
+        if (p_kind != 0) {
+            uint32_t topic;
+            if (p_kind == 2) {
+                const float x = p_x;
+                const uint32_t below = (__uint_as_float(psec.lo.x) < x) + (__uint_as_float(psec.lo.y) < x) +
+                                       (__uint_as_float(psec.lo.z) < x) + (__uint_as_float(psec.lo.w) < x) +
+                                       (__uint_as_float(psec.hi.x) < x) + (__uint_as_float(psec.hi.y) < x) +
+                                       (__uint_as_float(psec.hi.z) < x) + (__uint_as_float(psec.hi.w) < x);
+                const uint32_t k = p_sec * kLeaf + below;
+                topic = k < a.K ? k : a.K - 1;
+            } else if (p_kind == 3) {
+                topic = psec.lo.y & tmask;  // word 1 of sector 0: the first real entry
+            } else {
+                // prefix_search (sampler.hpp:18-41) from the checkpoint: first running sum >= xs.
+                float run = p_run;
+                bool need = true;
+                topic = 0;
+                uint32_t sec = p_sec;
+                Sector q = psec;
+                while (true) {
+                    const uint32_t es[8] = {q.lo.x, q.lo.y, q.lo.z, q.lo.w, q.hi.x, q.hi.y, q.hi.z, q.hi.w};
+#pragma unroll
+                    for (int w = 0; w < 8; ++w) {
+                        run = __fadd_rn(run, entry_mass<false>(es[w], tbits, tmask, s_bhat));
+                        if (need && run >= p_x) { topic = es[w] & tmask; need = false; }
+                    }
+                    if (!need || ++sec >= p_ns) break;
+                    q = ldg_sector(A4 + p_rq + 2 * sec);  // crossing beyond the checkpoints (rare)
+                }
+            }
+            a.z[p_slot] = static_cast<uint16_t>(topic);
+            atomicAdd(brow + topic, 1u);
+            p_kind = 0;
+        }
+
+        // A finished row: sample_token (sampler.hpp:183-204) up to its last sector read.
+        if (ends) {
+            float ub, up;
+            const uint64_t id = a.ids ? __ldg(a.ids + c_slot) : a.id_base + c_slot;
+            draw2_f32(a.seed, a.stream_kind, id, ub, up);
+            p_slot = c_slot;
+            if (ub < __fdiv_rn(s, __fadd_rn(s, qv))) {
+                const float xs = __fmul_rn(up, s);
+                if (xs == 0.0f) {
+                    p_kind = 3;
+                    p_sec = 0;
+                    psec = ldg_sector(A4 + c_rq);
+                } else {
+                    const uint32_t stored = c_ns < kCkSectors ? c_ns : kCkSectors;
+                    uint32_t lo = 0, hi = stored;  // first checkpoint >= xs (or stored)
+                    while (lo < hi) {
+                        const uint32_t mid = (lo + hi) >> 1;
+                        if (ck[mid * NT] >= xs) hi = mid; else lo = mid + 1;
+                    }
+                    p_kind = 1;
+                    p_sec = lo;
+                    p_run = lo > 0 ? ck[(lo - 1) * NT] : 0.0f;
+                    p_x = xs;
+                    p_rq = c_rq;
+                    p_ns = c_ns;
+                    psec = ldg_sector(A4 + c_rq + 2 * lo);
+                }
+            } else {
+                float x = __fmul_rn(up, total);  // WaryTree::sample(p * total)
+                if (!(x <= total)) x = total;
+                uint32_t lo = 0, hi = a.n_l8 - 1;
+                while (lo < hi) {
+                    const uint32_t mid = (lo + hi) >> 1;
+                    if (s_l8[mid] >= x) hi = mid; else lo = mid + 1;
+                }
+                p_kind = 2;
+                p_sec = lo;
+                p_x = x;
+                psec = ldg_sector(reinterpret_cast<const uint4*>(l4row + lo * kLeaf));
+            }
+            // The next token (if any) starts with the group loaded above.
+            cur = got;
+            c_rq = n_rq;
+            c_slot = n_slot;
+            c_base = 0;
+            hdr = got;
+            s = 0.0f;
+        } else if (cur) {
+            c_base += G;
+        }
+        __syncwarp();
+        store_group<G>(nx, ns, gs, sub, grp, stage);
+        __syncwarp();
+    }
+    if (a.row_entries) {
+        for (int o = 16; o > 0; o >>= 1) entries += __shfl_xor_sync(0xffffffffu, entries, o);
+        if (lane == 0) atomicAdd(a.row_entries, entries);
+    }
+}
+
+// ---- K3'' quad-lane sampler: four lanes per token, no staging ----------------------------------
+// The lane-per-token kernels must move every C_dk row through shared memory (cooperative
+// coalesced loads land a row's sectors in OTHER lanes' registers), and their phi gathers run
+// with a third of the lanes idle.  Here a warp samples 8 tokens at a time with 4 lanes each:
+// one instruction loads one 128-byte line (4 sectors, 32 entries) of each of the 8 rows -- the
+// rows are line-aligned -- straight into the registers of the 4 lanes that consume it, so
+// there is no stage store/load at all, and every lane gathers phi for its own sector's 8
+// entries (full-warp gathers).  The reference's sequential f32 chain (make_branch_context,
+// sampler.hpp:166-178) is kept exactly: the products are formed in parallel, then the running
+// sum visits the 4 sectors of a line in order -- lane j adds its 8 products to the value lane
+// j-1 handed it (shuffle) -- so every intermediate is the reference's.  The per-sector sums
+// double as the prefix_search checkpoints (a few hundred bytes per warp instead of a stage).
+template <int NT, int MINB, int L, bool kCompact>
+__global__ void __launch_bounds__(NT, MINB) sampler_quad_kernel(SamplerArgs a) {
+    constexpr uint32_t NW = NT / 32;
+    constexpr uint32_t TPR = 32u / L;  // tokens per round (L lanes each, L sectors per group)
+    constexpr uint32_t kCk = 16;       // checkpointed sectors per token (128 entries)
+    constexpr uint32_t kCkStride = 17; // odd: different tokens' checkpoints fall in different banks
+    extern __shared__ __align__(16) float sm[];
+    __shared__ uint32_t s_next;  // next unclaimed 32-token batch of the unit
+    const Unit unit = a.units[blockIdx.x];
+    const uint32_t v = unit.word;
+    float* s_bhat = sm;
+    float* s_l8 = sm + a.K_pad;
+    float* s_ck = s_l8 + a.l8_stride;  // [NW][32 tokens][kCkStride]
+    const float* l4row = a.l4 + static_cast<size_t>(v) * a.K_pad;
+    const float total = __ldg(l4row + a.K_pad - 1);
+    {
+        const float4* gb = reinterpret_cast<const float4*>(a.bhat + static_cast<size_t>(v) * a.K_pad);
+        float4* sb = reinterpret_cast<float4*>(sm);
+        for (uint32_t i = threadIdx.x; i < a.K_pad / 4; i += NT) sb[i] = __ldg(gb + i);
+        const float4* gl = reinterpret_cast<const float4*>(a.l8 + static_cast<size_t>(v) * a.l8_stride);
+        float4* sl = reinterpret_cast<float4*>(s_l8);
+        for (uint32_t i = threadIdx.x; i < a.l8_stride / 4; i += NT) sl[i] = __ldg(gl + i);
+    }
+    const float qv = __ldg(a.q + v);
+    uint32_t* brow = a.B + static_cast<size_t>(v) * a.K_pad;
+    const uint32_t tbits = a.tbits, tmask = (1u << tbits) - 1u;
+    const uint4* A4 = reinterpret_cast<const uint4*>(a.A);
+    const uint32_t lane = lane_id(), t = lane / L, sub = lane % L, lead = lane & ~(L - 1u);
+    const uint32_t warp = threadIdx.x >> 5;
+    float* ckw = s_ck + warp * 32u * kCkStride;
+    unsigned long long entries = 0;
+    if (threadIdx.x == 0) s_next = NW * 32u;
+    __syncthreads();
+
+    // A batch of 32 tokens per warp: L rounds of 32/L tokens x L lanes stream the rows and form
+    // S; then lane l finishes token l of the batch (draws, branch, prefix search / tree).  The
+    // first batch of warp w is tokens [32w, 32w + 32); later ones are claimed dynamically, so
+    // the CTA's warps finish the unit together.
+    for (uint32_t base = warp * 32u; base < unit.length;) {
+        const bool mine = base + lane < unit.length;
+        const uint2 tk = mine ? __ldg(a.tok + unit.offset + base + lane) : make_uint2(0u, 0u);  // {row quads, slot}
+        float S = 0.0f;
+        uint32_t my_ns = 0;
+#pragma unroll 1
+        for (uint32_t r = 0; r < L; ++r) {
+            const uint32_t ti = TPR * r + t;  // this lane group's token within the batch
+            if (__all_sync(0xffffffffu, base + TPR * r >= unit.length)) break;
+            const bool act = base + ti < unit.length;
+            const uint4* row = A4 + __shfl_sync(0xffffffffu, tk.x, ti);
+            Sector c = zero_sector();
+            if (act) c = ldg_sector(row + 2 * sub);
+            const uint32_t hw = __shfl_sync(0xffffffffu, c.lo.x, lead);  // header: word 0 of sector 0
+            // wide: [nnz-1 | entries | pad to 8]; compact: word 0 = nsect | nnz << 16
+            const uint32_t nnz = act ? (kCompact ? hw >> 16 : (hw & tmask) + 1u) : 0u;
+            const uint32_t nsect = act ? (kCompact ? hw & 0xFFFFu : (nnz + 8u) >> 3) : 0u;
+            if (sub == 0) entries += nnz;
+            const uint32_t max_groups = __reduce_max_sync(0xffffffffu, (nsect + L - 1u) / L);
+            float* ck = ckw + ti * kCkStride;
+            float run = 0.0f;
+            // Products of this lane's sector, then the chain over the line's 4 sectors in order.
+            auto consume = [&](const Sector& q, uint32_t g) {
+                const uint32_t sec = L * g + sub;
+                constexpr int NP = kCompact ? 16 : 8;  // products per sector
+                float p[NP];
+                if (sec < nsect) {
+                    const uint32_t es[8] = {q.lo.x, q.lo.y, q.lo.z, q.lo.w, q.hi.x, q.hi.y, q.hi.z, q.hi.w};
+                    if (kCompact) {
+                        // Each word: (c0 * phi[t0]) then phi[t1]; absent entries are +0 (acc_word_compact).
+#pragma unroll
+                        for (int w = 0; w < 8; ++w) {
+                            const WordEntries e = decode_word(es[w]);
+                            const bool hdr = w == 0 && sec == 0;  // the header word
+                            float p0 = 0.0f, p1 = 0.0f;
+                            if (e.v0 && !hdr) p0 = s_bhat[e.t0];
+                            if (e.v1 && !hdr) p1 = s_bhat[e.t1];
+                            p[2 * w] = __fmul_rn(e.c0, p0);
+                            p[2 * w + 1] = p1;
+                        }
+                    } else {
+#pragma unroll
+                        for (int w = 0; w < 8; ++w) p[w] = entry_mass<false>(es[w], tbits, tmask, s_bhat);
+                    }
+                }
+#pragma unroll
+                for (uint32_t j = 0; j < L; ++j) {
+                    if (sub == j && sec < nsect) {
+#pragma unroll
+                        for (int w = 0; w < NP; ++w) run = __fadd_rn(run, p[w]);
+                        if (sec < kCk) ck[sec] = run;
+                    }
+                    run = __shfl_sync(0xffffffffu, run, lead | j);
+                }
+            };
+            for (uint32_t g = 0; g < max_groups; g += 2) {  // two groups per trip: no register copies
+                Sector n = c;
+                if (L * (g + 1) + sub < nsect) n = ldg_sector(row + 2 * (L * (g + 1) + sub));
+                consume(c, g);
+                if (g + 1 >= max_groups) break;
+                if (L * (g + 2) + sub < nsect) c = ldg_sector(row + 2 * (L * (g + 2) + sub));
+                consume(n, g + 1);
+            }
+            // Token ti's S and sector count to its owning lane (lane ti).
+            const uint32_t src = ((lane - TPR * r) & (TPR - 1u)) * L;
+            const float xS = __shfl_sync(0xffffffffu, run, src);
+            const uint32_t xn = __shfl_sync(0xffffffffu, nsect, src);
+            if (lane / TPR == r) {
+                S = xS;
+                my_ns = xn;
+            }
+        }
+        __syncwarp();
+        // sample_token (sampler.hpp:183-204), one token per lane.
+        if (mine) {
+            float ub, up;
+            const uint64_t id = a.ids ? __ldg(a.ids + tk.y) : a.id_base + tk.y;
+            draw2_f32(a.seed, a.stream_kind, id, ub, up);
+            const uint4* row = A4 + tk.x;
+            uint32_t topic = 0;
+            if (ub < __fdiv_rn(S, __fadd_rn(S, qv))) {
+                const float xs = __fmul_rn(up, S);
+                if (xs == 0.0f) {
+                    const uint32_t e1 = __ldg(reinterpret_cast<const uint32_t*>(row) + 1);  // first real entry
+                    topic = kCompact ? (e1 & 0x7FFFu) : (e1 & tmask);
+                } else {
+                    const float* ck = ckw + lane * kCkStride;
+                    const uint32_t stored = my_ns < kCk ? my_ns : kCk;
+                    uint32_t lo = 0, hi = stored;  // first checkpoint >= xs (or stored)
+                    while (lo < hi) {
+                        const uint32_t mid = (lo + hi) >> 1;
+                        if (ck[mid] >= xs) hi = mid; else lo = mid + 1;
+                    }
+                    float r = lo > 0 ? ck[lo - 1] : 0.0f;
+                    for (uint32_t sc = lo; sc < my_ns; ++sc) {  // one sector unless past the checkpoints
+                        const Sector q = ldg_sector(row + 2 * sc);
+                        const uint32_t es[8] = {q.lo.x, q.lo.y, q.lo.z, q.lo.w, q.hi.x, q.hi.y, q.hi.z, q.hi.w};
+                        bool found = false;
+                        if (kCompact) {
+                            bool need = true;
+#pragma unroll
+                            for (int w = 0; w < 8; ++w)
+                                if (w > 0 || sc != 0) scan_word_compact<false>(r, need, topic, xs, es[w], s_bhat);
+                            found = !need;
+                        } else {
+#pragma unroll
+                            for (int w = 0; w < 8; ++w) {
+                                r = __fadd_rn(r, entry_mass<false>(es[w], tbits, tmask, s_bhat));
+                                if (!found && r >= xs) { topic = es[w] & tmask; found = true; }
+                            }
+                        }
+                        if (found) break;
+                    }
+                }
+            } else {
+                float x = __fmul_rn(up, total);  // WaryTree::sample(p * total)
+                if (!(x <= total)) x = total;
+                const uint32_t k = tree_search(x, s_l8, a.n_l8, l4row);
+                topic = k < a.K ? k : a.K - 1;
+            }
+            a.z[tk.y] = static_cast<uint16_t>(topic);
+            atomicAdd(brow + topic, 1u);
+        }
+        uint32_t nb = 0;
+        if (lane == 0) nb = atomicAdd(&s_next, 32u);
+        base = __shfl_sync(0xffffffffu, nb, 0);
+    }
+    if (a.row_entries) {
+        for (int o = 16; o > 0; o >>= 1) entries += __shfl_xor_sync(0xffffffffu, entries, o);
+        if (lane == 0) atomicAdd(a.row_entries, entries);
+    }
+}
+
+// The same algorithm with the next round's first line prefetched in each round's last group
+// slot and the next batch claimed a batch ahead; the per-unit scalars live in shared memory to
+// make room in the 64-register budget (C3 K=10K: 95.5 -> 92.8 ms; C2: 19.8 -> 20.5 ms).
+template <int NT, int MINB, int L, bool kCompact, bool kPrefetchNext = true>
+__global__ void __launch_bounds__(NT, MINB) sampler_quad_pf_kernel(SamplerArgs a) {
+    constexpr uint32_t NW = NT / 32;
+    constexpr uint32_t TPR = 32u / L;  // tokens per round (L lanes each, L sectors per group)
+    constexpr uint32_t kCk = 16;       // checkpointed sectors per token (128 entries)
+    constexpr uint32_t kCkStride = 17; // odd: different tokens' checkpoints fall in different banks
+    extern __shared__ __align__(16) float sm[];
+    __shared__ uint32_t s_next;  // next unclaimed 32-token batch of the unit
+    __shared__ float s_total, s_qv;  // the word's tree total and Q_v (read in the sampling step only)
+    const Unit unit = a.units[blockIdx.x];
+    const uint32_t v = unit.word;
+    float* s_bhat = sm;
+    float* s_l8 = sm + a.K_pad;
+    float* s_ck = s_l8 + a.l8_stride;  // [NW][32 tokens][kCkStride]
+    {
+        const float4* gb = reinterpret_cast<const float4*>(a.bhat + static_cast<size_t>(v) * a.K_pad);
+        float4* sb = reinterpret_cast<float4*>(sm);
+        for (uint32_t i = threadIdx.x; i < a.K_pad / 4; i += NT) sb[i] = __ldg(gb + i);
+        const float4* gl = reinterpret_cast<const float4*>(a.l8 + static_cast<size_t>(v) * a.l8_stride);
+        float4* sl = reinterpret_cast<float4*>(s_l8);
+        for (uint32_t i = threadIdx.x; i < a.l8_stride / 4; i += NT) sl[i] = __ldg(gl + i);
+    }
+    const uint32_t tbits = a.tbits, tmask = (1u << tbits) - 1u;
+    const uint4* A4 = reinterpret_cast<const uint4*>(a.A);
+    const uint32_t lane = lane_id(), t = lane / L, sub = lane % L, lead = lane & ~(L - 1u);
+    const uint32_t warp = threadIdx.x >> 5;
+    float* ckw = s_ck + warp * 32u * kCkStride;
+    uint32_t entries = 0;
+    if (threadIdx.x == 0) {
+        s_next = NW * 32u;
+        s_total = __ldg(a.l4 + static_cast<size_t>(v) * a.K_pad + a.K_pad - 1);  // padded with the total
+        s_qv = __ldg(a.q + v);
+    }
+    __syncthreads();
+
+    // A batch of 32 tokens per warp: L rounds of 32/L tokens x L lanes stream the rows and form
+    // S; then lane l finishes token l of the batch (draws, branch, prefix search / tree).  The
+    // first batch of warp w is tokens [32w, 32w + 32); later ones are claimed dynamically, so
+    // the CTA's warps finish the unit together.
+    // The next batch is claimed when a batch starts, and each round's last group slot loads
+    // the NEXT round's first line (its header sets that round's length), so rounds never start
+    // on an exposed load.
+    uint32_t base = warp * 32u;
+    uint2 tk = base + lane < unit.length ? __ldg(a.tok + unit.offset + base + lane) : make_uint2(0u, 0u);
+    Sector c = zero_sector();
+    if (kPrefetchNext) {
+        const uint32_t rq0 = __shfl_sync(0xffffffffu, tk.x, t);
+        if (base + t < unit.length) c = ldg_sector(A4 + rq0 + 2 * sub);
+    }
+    while (base < unit.length) {
+        const bool mine = base + lane < unit.length;
+        uint32_t nb = 0;
+        uint2 tk_nx = make_uint2(0u, 0u);
+        if (kPrefetchNext) {  // claim the next batch now and load its token records
+            if (lane == 0) nb = atomicAdd(&s_next, 32u);
+            nb = __shfl_sync(0xffffffffu, nb, 0);
+            if (nb + lane < unit.length) tk_nx = __ldg(a.tok + unit.offset + nb + lane);
+        }
+        float S = 0.0f;
+        uint32_t my_ns = 0;
+#pragma unroll 1
+        for (uint32_t r = 0; r < L; ++r) {
+            const uint32_t ti = TPR * r + t;  // this lane group's token within the batch
+            if (__all_sync(0xffffffffu, base + TPR * r >= unit.length)) break;
+            const bool act = base + ti < unit.length;
+            const uint4* row = A4 + __shfl_sync(0xffffffffu, tk.x, ti);
+            if (!kPrefetchNext) {  // this round's first line, loaded now
+                c = zero_sector();
+                if (act) c = ldg_sector(row + 2 * sub);
+            }
+            const uint32_t hw = __shfl_sync(0xffffffffu, c.lo.x, lead);  // header: word 0 of sector 0
+            // wide: [nnz-1 | entries | pad to 8]; compact: word 0 = nsect | nnz << 16
+            const uint32_t nnz = act ? (kCompact ? hw >> 16 : (hw & tmask) + 1u) : 0u;
+            const uint32_t nsect = act ? (kCompact ? hw & 0xFFFFu : (nnz + 8u) >> 3) : 0u;
+            if (sub == 0) entries += nnz;
+            const uint32_t max_groups = __reduce_max_sync(0xffffffffu, (nsect + L - 1u) / L);
+            float* ck = ckw + ti * kCkStride;
+            float run = 0.0f;
+            // Products of this lane's sector, then the chain over the line's 4 sectors in order.
+            auto consume = [&](const Sector& q, uint32_t g) {
+                const uint32_t sec = L * g + sub;
+                constexpr int NP = kCompact ? 16 : 8;  // products per sector
+                float p[NP];
+                if (sec < nsect) {
+                    const uint32_t es[8] = {q.lo.x, q.lo.y, q.lo.z, q.lo.w, q.hi.x, q.hi.y, q.hi.z, q.hi.w};
+                    if (kCompact) {
+                        // Each word: (c0 * phi[t0]) then phi[t1]; absent entries are +0 (acc_word_compact).
+#pragma unroll
+                        for (int w = 0; w < 8; ++w) {
+                            const WordEntries e = decode_word(es[w]);
+                            const bool hdr = w == 0 && sec == 0;  // the header word
+                            float p0 = 0.0f, p1 = 0.0f;
+                            if (e.v0 && !hdr) p0 = s_bhat[e.t0];
+                            if (e.v1 && !hdr) p1 = s_bhat[e.t1];
+                            p[2 * w] = __fmul_rn(e.c0, p0);
+                            p[2 * w + 1] = p1;
+                        }
+                    } else {
+#pragma unroll
+                        for (int w = 0; w < 8; ++w) p[w] = entry_mass<false>(es[w], tbits, tmask, s_bhat);
+                    }
+                }
+#pragma unroll
+                for (uint32_t j = 0; j < L; ++j) {
+                    if (sub == j && sec < nsect) {
+#pragma unroll
+                        for (int w = 0; w < NP; ++w) run = __fadd_rn(run, p[w]);
+                        if (sec < kCk) ck[sec] = run;
+                    }
+                    run = __shfl_sync(0xffffffffu, run, lead | j);
+                }
+            };
+            // Group g+1 (or the next round's first line) loads while group g is consumed; two
+            // groups per trip so no registers are copied.
+            auto fetch = [&](uint32_t g, Sector& dst) {
+                if (g < max_groups) {  // warp-uniform
+                    if (L * g + sub < nsect) dst = ldg_sector(row + 2 * (L * g + sub));
+                } else if (kPrefetchNext) {
+                    const bool last = r + 1 == L || base + TPR * (r + 1) >= unit.length;
+                    const uint32_t nrq = __shfl_sync(0xffffffffu, last ? tk_nx.x : tk.x, last ? t : ti + TPR);
+                    if (last ? nb + t < unit.length : base + ti + TPR < unit.length)
+                        dst = ldg_sector(A4 + nrq + 2 * sub);
+                }
+            };
+            if (max_groups == 0) {
+                fetch(0, c);
+            } else {
+                Sector n = c;
+                for (uint32_t g = 0;; g += 2) {
+                    fetch(g + 1, n);
+                    consume(c, g);
+                    if (g + 1 >= max_groups) { c = n; break; }
+                    fetch(g + 2, c);
+                    consume(n, g + 1);
+                    if (g + 2 >= max_groups) break;
+                }
+            }
+            // Token ti's S and sector count to its owning lane (lane ti).
+            const uint32_t src = ((lane - TPR * r) & (TPR - 1u)) * L;
+            const float xS = __shfl_sync(0xffffffffu, run, src);
+            const uint32_t xn = __shfl_sync(0xffffffffu, nsect, src);
+            if (lane / TPR == r) {
+                S = xS;
+                my_ns = xn;
+            }
+        }
+        __syncwarp();
+        // sample_token (sampler.hpp:183-204), one token per lane.
+        if (mine) {
+            const float qv = s_qv, total = s_total;
+            const float* l4row = a.l4 + static_cast<size_t>(v) * a.K_pad;
+            float ub, up;
+            const uint64_t id = a.ids ? __ldg(a.ids + tk.y) : a.id_base + tk.y;
+            draw2_f32(a.seed, a.stream_kind, id, ub, up);
+            const uint4* row = A4 + tk.x;
+            uint32_t topic = 0;
+            if (ub < __fdiv_rn(S, __fadd_rn(S, qv))) {
+                const float xs = __fmul_rn(up, S);
+                if (xs == 0.0f) {
+                    const uint32_t e1 = __ldg(reinterpret_cast<const uint32_t*>(row) + 1);  // first real entry
+                    topic = kCompact ? (e1 & 0x7FFFu) : (e1 & tmask);
+                } else {
+                    const float* ck = ckw + lane * kCkStride;
+                    const uint32_t stored = my_ns < kCk ? my_ns : kCk;
+                    uint32_t lo = 0, hi = stored;  // first checkpoint >= xs (or stored)
+                    while (lo < hi) {
+                        const uint32_t mid = (lo + hi) >> 1;
+                        if (ck[mid] >= xs) hi = mid; else lo = mid + 1;
+                    }
+                    float r = lo > 0 ? ck[lo - 1] : 0.0f;
+                    for (uint32_t sc = lo; sc < my_ns; ++sc) {  // one sector unless past the checkpoints
+                        const Sector q = ldg_sector(row + 2 * sc);
+                        const uint32_t es[8] = {q.lo.x, q.lo.y, q.lo.z, q.lo.w, q.hi.x, q.hi.y, q.hi.z, q.hi.w};
+                        bool found = false;
+                        if (kCompact) {
+                            bool need = true;
+#pragma unroll
+                            for (int w = 0; w < 8; ++w)
+                                if (w > 0 || sc != 0) scan_word_compact<false>(r, need, topic, xs, es[w], s_bhat);
+                            found = !need;
+                        } else {
+#pragma unroll
+                            for (int w = 0; w < 8; ++w) {
+                                r = __fadd_rn(r, entry_mass<false>(es[w], tbits, tmask, s_bhat));
+                                if (!found && r >= xs) { topic = es[w] & tmask; found = true; }
+                            }
+                        }
+                        if (found) break;
+                    }
+                }
+            } else {
+                float x = __fmul_rn(up, total);  // WaryTree::sample(p * total)
+                if (!(x <= total)) x = total;
+                const uint32_t k = tree_search(x, s_l8, a.n_l8, l4row);
+                topic = k < a.K ? k : a.K - 1;
+            }
+            a.z[tk.y] = static_cast<uint16_t>(topic);
+            atomicAdd(a.B + static_cast<size_t>(v) * a.K_pad + topic, 1u);
+        }
+        if (kPrefetchNext) {
+            base = nb;
+            tk = tk_nx;
+        } else {
+            if (lane == 0) nb = atomicAdd(&s_next, 32u);
+            base = __shfl_sync(0xffffffffu, nb, 0);
+            tk = base + lane < unit.length ? __ldg(a.tok + unit.offset + base + lane) : make_uint2(0u, 0u);
+        }
+    }
+    if (a.row_entries) {
+        for (int o = 16; o > 0; o >>= 1) entries += __shfl_xor_sync(0xffffffffu, entries, o);
+        if (lane == 0) atomicAdd(a.row_entries, static_cast<unsigned long long>(entries));
+    }
+}
+
+size_t sampler_smem(const SamplerArgs& a, int nt, int g, bool global_phi) {
+    const size_t stage_row = 32u * static_cast<size_t>(g) + 16u;
+    return sizeof(float) * ((global_phi ? 0 : static_cast<size_t>(a.K_pad)) + a.l8_stride) +
+           (sizeof(float) * kCkSectors + stage_row) * static_cast<size_t>(nt);
+}
+
+template <int NT, int G, int MINB, bool Gl, bool C>
+cudaError_t launch_sampler_t(const SamplerArgs& a, uint32_t n_units, cudaStream_t s) {
+    static bool configured = false;
+    if (!configured) {
+        cudaFuncSetAttribute(sampler_kernel<NT, G, MINB, Gl, C>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             227 * 1024);
+        configured = true;
+    }
+    sampler_kernel<NT, G, MINB, Gl, C><<<n_units, NT, sampler_smem(a, NT, G, Gl), s>>>(a);
+    return cudaGetLastError();
+}
+
+template <int NT, int G>
+cudaError_t launch_stream_t(const SamplerArgs& a, uint32_t n_units, cudaStream_t s) {
+    static bool configured = false;
+    if (!configured) {
+        // 227 KB per block minus the kernel's static shared memory (the batch counter).
+        const cudaError_t e = cudaFuncSetAttribute(sampler_stream_kernel<NT, G>,
+                                                   cudaFuncAttributeMaxDynamicSharedMemorySize, 226 * 1024);
+        if (e != cudaSuccess) return e;
+        configured = true;
+    }
+    sampler_stream_kernel<NT, G><<<n_units, NT, sampler_smem(a, NT, G, false), s>>>(a);
+    return cudaGetLastError();
+}
+
+int sampler_shape_from_name(const char* name) {
+    const std::string v(name ? name : "");
+    return v == "g2" ? 0 : v == "g4" ? 1 : v == "g4x512" ? 2 : v == "s4" ? 3 : v == "s2" ? 4 : v == "s4x128" ? 5
+         : v == "q512" ? 6 : v == "q256" ? 7 : v == "q512r" ? 8 : v == "q256r" ? 9
+         : v == "p512" ? 10 : v == "p256" ? 11 : v == "o512" ? 12 : -1;
+}
+
+size_t sampler_quad_smem(const SamplerArgs& a, int nt) {
+    return sizeof(float) * (static_cast<size_t>(a.K_pad) + a.l8_stride + static_cast<size_t>(nt / 32) * 32u * 17u);
+}
+
+template <int NT, int MINB, int L, bool C, bool PF>
+cudaError_t launch_quad_t1(const SamplerArgs& a, uint32_t n_units, cudaStream_t s) {
+    static bool configured = false;
+    auto kern = PF ? sampler_quad_pf_kernel<NT, MINB, L, C> : sampler_quad_kernel<NT, MINB, L, C>;
+    if (!configured) {
+        // 227 KB per block minus the kernel's static shared memory (the batch counter).
+        const cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 226 * 1024);
+        if (e != cudaSuccess) return e;
+        configured = true;
+    }
+    kern<<<n_units, NT, sampler_quad_smem(a, NT), s>>>(a);
+    return cudaGetLastError();
+}
+// PF: the next round's first line is prefetched in each round's last group slot (C3 K=10K:
+// 95.5 -> 92.8 ms; short-phi C2: 19.8 -> 20.5 ms, so only the 512-thread shape uses it).
+template <int NT, int MINB, int L = 4, bool PF = (NT >= 512)>
+cudaError_t launch_quad_t(const SamplerArgs& a, uint32_t n_units, cudaStream_t s) {
+    return a.compact ? launch_quad_t1<NT, MINB, L, true, PF>(a, n_units, s)
+                     : launch_quad_t1<NT, MINB, L, false, PF>(a, n_units, s);
+}
+
+// Launch shape (SLDA_SAMPLER overrides for experiments; default by phi row size):
+//   "g2"     : round-based, 256/512-thread CTAs, 2-sector groups, 64 registers
+//   "g4"     : round-based, 256-thread CTAs, 4-sector groups, up to 128 registers
+//   "g4x512" : round-based, 512-thread CTAs, 4-sector groups (one CTA / SM at K = 10K)
+//   "s4", "s2", "s4x128" : streaming lane refill (sampler_stream_kernel)
+//   "q512", "q256"       : quad-lane (sampler_quad_kernel, L=4 lanes per token), 64 registers
+//   "p512", "p256"       : pair-lane (L=2; C2 20.7 vs 21.5 ms, C3 107.9 vs 100.0 ms)
+//   "o512"               : octet-lane (L=8; slower at both)
+//   "q512r", "q256r"     : quad-lane with a relaxed register bound (fewer warps; slower)
+cudaError_t launch_sampler(const SamplerArgs& a, uint32_t n_units, cudaStream_t s) {
+    if (n_units == 0) return cudaSuccess;
+    const size_t phi_bytes = sizeof(float) * (static_cast<size_t>(a.K_pad) + a.l8_stride);
+    // Default: the quad-lane kernel wherever two 512-thread (or four 256-thread) CTAs fit an SM
+    // (C3 K=10K: 100.0 vs 102.6 ms for 4-sector groups; C2 K=1K: 21.5 vs 23.5 ms for 2-sector
+    // groups), else 4-sector groups (large phi rows), else 2-sector groups.
+    int shape = a.shape;
+    if (shape < 0) {
+        if (phi_bytes <= 24 * 1024 && 4 * sampler_quad_smem(a, 256) <= 227 * 1024) shape = 7;
+        else if (2 * sampler_quad_smem(a, 512) <= 227 * 1024) shape = 6;
+    }
+    if (shape < 0) shape = phi_bytes > 24 * 1024 ? 1 : 0;
+    const bool fits512 = sampler_smem(a, 512, 2, false) <= 227 * 1024;
+    if (!fits512) {
+        // Rows that do not fit shared memory (K > kCompactMaxK, so always the wide format):
+        // gather phi through L1/L2.
+        if (a.compact) return cudaErrorInvalidConfiguration;
+        return launch_sampler_t<512, 2, 2, true, false>(a, n_units, s);
+    }
+    if (shape == 6 && sampler_quad_smem(a, 512) <= 227 * 1024)
+        return launch_quad_t<512, 2>(a, n_units, s);
+    if (shape == 7 && sampler_quad_smem(a, 256) <= 227 * 1024)
+        return launch_quad_t<256, 4>(a, n_units, s);
+    if (shape == 8 && sampler_quad_smem(a, 512) <= 227 * 1024)
+        return launch_quad_t<512, 1>(a, n_units, s);
+    if (shape == 9 && sampler_quad_smem(a, 256) <= 227 * 1024)
+        return launch_quad_t<256, 3>(a, n_units, s);
+    if (shape == 10 && sampler_quad_smem(a, 512) <= 227 * 1024)
+        return launch_quad_t<512, 2, 2>(a, n_units, s);
+    if (shape == 11 && sampler_quad_smem(a, 256) <= 227 * 1024)
+        return launch_quad_t<256, 4, 2>(a, n_units, s);
+    if (shape == 12 && sampler_quad_smem(a, 512) <= 227 * 1024)
+        return launch_quad_t<512, 2, 8>(a, n_units, s);
+    if (!a.compact && shape == 3 && sampler_smem(a, 256, 4, false) <= 227 * 1024)
+        return launch_stream_t<256, 4>(a, n_units, s);
+    if (!a.compact && shape == 4 && sampler_smem(a, 256, 2, false) <= 227 * 1024)
+        return launch_stream_t<256, 2>(a, n_units, s);
+    if (!a.compact && shape == 5 && sampler_smem(a, 128, 4, false) <= 227 * 1024)
+        return launch_stream_t<128, 4>(a, n_units, s);
+    if (shape == 1 && sampler_smem(a, 256, 4, false) <= 227 * 1024)
+        return a.compact ? launch_sampler_t<256, 4, 2, false, true>(a, n_units, s)
+                         : launch_sampler_t<256, 4, 2, false, false>(a, n_units, s);
+    if (shape == 2 && sampler_smem(a, 512, 4, false) <= 227 * 1024)
+        return a.compact ? launch_sampler_t<512, 4, 1, false, true>(a, n_units, s)
+                         : launch_sampler_t<512, 4, 1, false, false>(a, n_units, s);
+    // Small phi rows: 256-thread CTAs.  Large (K = 10K): 512 threads share one staged row
+    // (2 CTAs x 16 warps per SM).
+    if (phi_bytes <= 24 * 1024)
+        return a.compact ? launch_sampler_t<256, 2, 4, false, true>(a, n_units, s)
+                         : launch_sampler_t<256, 2, 4, false, false>(a, n_units, s);
+    return a.compact ? launch_sampler_t<512, 2, 2, false, true>(a, n_units, s)
+                     : launch_sampler_t<512, 2, 2, false, false>(a, n_units, s);
+}
+
+}  // namespace slda

@@ -1,7 +1,7 @@
 # K sweep (BASELINE C5, NYTimes shape) + C2 + C3 bench lines, no CPU baseline (one gpurun call).
 # usage: bash scripts/gpu_sweep.sh <tag>
 TAG=${1:-s1}
-for CFG in c2 c5_k100 c5_k10000 c5_k50000 c3; do
+for CFG in ${CFGS:-c2 c5_k100 c5_k10000 c5_k50000 c3}; do
   timeout 900 python bench.py --config $CFG --steps 5 --warmup 3 --no-cpu-baseline \
       > gpurun_out/sweep_${TAG}_${CFG}.json 2> gpurun_out/sweep_${TAG}_${CFG}.err
   echo "$CFG rc=$?"
