@@ -523,12 +523,17 @@ __global__ void __launch_bounds__(NT, MINB) sampler_quad_kernel(SamplerArgs a) {
                     }
                 }
 #pragma unroll
-                for (uint32_t j = 0; j < L; ++j) {
-                    if (sub == j && sec < nsect) {
+                // Branch-free rounds: every lane runs the 8 FADDs (an instruction costs the same
+                // with 8 or 32 lanes active) and only lane j of each group keeps the result.
+                const bool valid = sec < nsect;
 #pragma unroll
-                        for (int w = 0; w < NP; ++w) run = __fadd_rn(run, p[w]);
-                        if (sec < kCk) ck[sec] = run;
-                    }
+                for (uint32_t j = 0; j < L; ++j) {
+                    float r2 = run;
+#pragma unroll
+                    for (int w = 0; w < NP; ++w) r2 = __fadd_rn(r2, p[w]);
+                    const bool mine = sub == j && valid;
+                    run = mine ? r2 : run;
+                    if (mine && sec < kCk) ck[sec] = run;
                     run = __shfl_sync(0xffffffffu, run, lead | j);
                 }
             };
@@ -716,12 +721,17 @@ __global__ void __launch_bounds__(NT, MINB) sampler_quad_pf_kernel(SamplerArgs a
                     }
                 }
 #pragma unroll
-                for (uint32_t j = 0; j < L; ++j) {
-                    if (sub == j && sec < nsect) {
+                // Branch-free rounds: every lane runs the 8 FADDs (an instruction costs the same
+                // with 8 or 32 lanes active) and only lane j of each group keeps the result.
+                const bool valid = sec < nsect;
 #pragma unroll
-                        for (int w = 0; w < NP; ++w) run = __fadd_rn(run, p[w]);
-                        if (sec < kCk) ck[sec] = run;
-                    }
+                for (uint32_t j = 0; j < L; ++j) {
+                    float r2 = run;
+#pragma unroll
+                    for (int w = 0; w < NP; ++w) r2 = __fadd_rn(r2, p[w]);
+                    const bool mine = sub == j && valid;
+                    run = mine ? r2 : run;
+                    if (mine && sec < kCk) ck[sec] = run;
                     run = __shfl_sync(0xffffffffu, run, lead | j);
                 }
             };
