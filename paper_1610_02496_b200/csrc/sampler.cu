@@ -502,8 +502,10 @@ __global__ void __launch_bounds__(NT, MINB) sampler_quad_kernel(SamplerArgs a) {
             auto consume = [&](const Sector& q, uint32_t g) {
                 const uint32_t sec = L * g + sub;
                 constexpr int NP = kCompact ? 16 : 8;  // products per sector
+                // Sectors past the row are loaded as zeros (in-range bhat[0] gathers, broadcast),
+                // so the products need no branch; only valid sectors' products are accumulated.
                 float p[NP];
-                if (sec < nsect) {
+                {
                     const uint32_t es[8] = {q.lo.x, q.lo.y, q.lo.z, q.lo.w, q.hi.x, q.hi.y, q.hi.z, q.hi.w};
                     if (kCompact) {
                         // Each word: (c0 * phi[t0]) then phi[t1]; absent entries are +0 (acc_word_compact).
@@ -522,7 +524,6 @@ __global__ void __launch_bounds__(NT, MINB) sampler_quad_kernel(SamplerArgs a) {
                         for (int w = 0; w < 8; ++w) p[w] = entry_mass<false>(es[w], tbits, tmask, s_bhat);
                     }
                 }
-#pragma unroll
                 // Branch-free rounds: every lane runs the 8 FADDs (an instruction costs the same
                 // with 8 or 32 lanes active) and only lane j of each group keeps the result.
                 const bool valid = sec < nsect;
@@ -539,10 +540,10 @@ __global__ void __launch_bounds__(NT, MINB) sampler_quad_kernel(SamplerArgs a) {
             };
             for (uint32_t g = 0; g < max_groups; g += 2) {  // two groups per trip: no register copies
                 Sector n = c;
-                if (L * (g + 1) + sub < nsect) n = ldg_sector(row + 2 * (L * (g + 1) + sub));
+                n = L * (g + 1) + sub < nsect ? ldg_sector(row + 2 * (L * (g + 1) + sub)) : zero_sector();
                 consume(c, g);
                 if (g + 1 >= max_groups) break;
-                if (L * (g + 2) + sub < nsect) c = ldg_sector(row + 2 * (L * (g + 2) + sub));
+                c = L * (g + 2) + sub < nsect ? ldg_sector(row + 2 * (L * (g + 2) + sub)) : zero_sector();
                 consume(n, g + 1);
             }
             // Token ti's S and sector count to its owning lane (lane ti).
@@ -700,8 +701,10 @@ __global__ void __launch_bounds__(NT, MINB) sampler_quad_pf_kernel(SamplerArgs a
             auto consume = [&](const Sector& q, uint32_t g) {
                 const uint32_t sec = L * g + sub;
                 constexpr int NP = kCompact ? 16 : 8;  // products per sector
+                // Sectors past the row are loaded as zeros (in-range bhat[0] gathers, broadcast),
+                // so the products need no branch; only valid sectors' products are accumulated.
                 float p[NP];
-                if (sec < nsect) {
+                {
                     const uint32_t es[8] = {q.lo.x, q.lo.y, q.lo.z, q.lo.w, q.hi.x, q.hi.y, q.hi.z, q.hi.w};
                     if (kCompact) {
                         // Each word: (c0 * phi[t0]) then phi[t1]; absent entries are +0 (acc_word_compact).
@@ -720,7 +723,6 @@ __global__ void __launch_bounds__(NT, MINB) sampler_quad_pf_kernel(SamplerArgs a
                         for (int w = 0; w < 8; ++w) p[w] = entry_mass<false>(es[w], tbits, tmask, s_bhat);
                     }
                 }
-#pragma unroll
                 // Branch-free rounds: every lane runs the 8 FADDs (an instruction costs the same
                 // with 8 or 32 lanes active) and only lane j of each group keeps the result.
                 const bool valid = sec < nsect;
@@ -739,7 +741,7 @@ __global__ void __launch_bounds__(NT, MINB) sampler_quad_pf_kernel(SamplerArgs a
             // groups per trip so no registers are copied.
             auto fetch = [&](uint32_t g, Sector& dst) {
                 if (g < max_groups) {  // warp-uniform
-                    if (L * g + sub < nsect) dst = ldg_sector(row + 2 * (L * g + sub));
+                    dst = L * g + sub < nsect ? ldg_sector(row + 2 * (L * g + sub)) : zero_sector();
                 } else if (kPrefetchNext) {
                     const bool last = r + 1 == L || base + TPR * (r + 1) >= unit.length;
                     const uint32_t nrq = __shfl_sync(0xffffffffu, last ? tk_nx.x : tk.x, last ? t : ti + TPR);
