@@ -216,4 +216,35 @@ __device__ __forceinline__ void scan_sector(float& run, bool& need, uint32_t& to
     }
 }
 
+
+// ---- phi row + L8 level staged by the TMA engine -----------------------------------------------
+// One thread arms an mbarrier with the byte count and issues two bulk copies (cp.async.bulk,
+// global -> shared, completing on the mbarrier); the CTA waits on the barrier's phase 0.  No
+// registers or LSU instructions are spent on the 45 KB (K = 10K) staging, and the copies run
+// while the CTA's warps start their first token loads.  Sizes are multiples of 16 bytes
+// (K_pad % 32 == 0, l8_stride % 4 == 0) and both rows are 128-byte aligned.
+__device__ __forceinline__ void tma_stage_rows(float* s_phi, const float* g_phi, uint32_t phi_bytes, float* s_l8,
+                                               const float* g_l8, uint32_t l8_bytes, unsigned long long* bar) {
+    const uint32_t b = static_cast<uint32_t>(__cvta_generic_to_shared(bar));
+    if (threadIdx.x == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(b) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(phi_bytes + l8_bytes)
+                     : "memory");
+        asm volatile("cp.async.bulk.shared::cta.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                     ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(s_phi))), "l"(g_phi), "r"(phi_bytes), "r"(b)
+                     : "memory");
+        asm volatile("cp.async.bulk.shared::cta.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                     ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(s_l8))), "l"(g_l8), "r"(l8_bytes), "r"(b)
+                     : "memory");
+    }
+}
+__device__ __forceinline__ void tma_wait_rows(unsigned long long* bar) {
+    const uint32_t b = static_cast<uint32_t>(__cvta_generic_to_shared(bar));
+    asm volatile("{\n\t.reg .pred P1;\n\tWAIT_%=:\n\t"
+                 "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], 0;\n\t"
+                 "@!P1 bra WAIT_%=;\n\t}" ::"r"(b)
+                 : "memory");
+}
+
 }  // namespace slda

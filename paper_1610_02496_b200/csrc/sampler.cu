@@ -454,14 +454,9 @@ __global__ void __launch_bounds__(NT, MINB) sampler_quad_kernel(SamplerArgs a) {
     float* s_ck = s_l8 + a.l8_stride;  // [NW][32 tokens][kCkStride]
     const float* l4row = a.l4 + static_cast<size_t>(v) * a.K_pad;
     const float total = __ldg(l4row + a.K_pad - 1);
-    {
-        const float4* gb = reinterpret_cast<const float4*>(a.bhat + static_cast<size_t>(v) * a.K_pad);
-        float4* sb = reinterpret_cast<float4*>(sm);
-        for (uint32_t i = threadIdx.x; i < a.K_pad / 4; i += NT) sb[i] = __ldg(gb + i);
-        const float4* gl = reinterpret_cast<const float4*>(a.l8 + static_cast<size_t>(v) * a.l8_stride);
-        float4* sl = reinterpret_cast<float4*>(s_l8);
-        for (uint32_t i = threadIdx.x; i < a.l8_stride / 4; i += NT) sl[i] = __ldg(gl + i);
-    }
+    __shared__ __align__(8) unsigned long long s_bar;  // phi/L8 staging (TMA bulk copies)
+    tma_stage_rows(sm, a.bhat + static_cast<size_t>(v) * a.K_pad, a.K_pad * 4u, s_l8,
+                   a.l8 + static_cast<size_t>(v) * a.l8_stride, a.l8_stride * 4u, &s_bar);
     const float qv = __ldg(a.q + v);
     uint32_t* brow = a.B + static_cast<size_t>(v) * a.K_pad;
     const uint32_t tbits = a.tbits, tmask = (1u << tbits) - 1u;
@@ -472,6 +467,7 @@ __global__ void __launch_bounds__(NT, MINB) sampler_quad_kernel(SamplerArgs a) {
     unsigned long long entries = 0;
     if (threadIdx.x == 0) s_next = NW * 32u;
     __syncthreads();
+    tma_wait_rows(&s_bar);
 
     // A batch of 32 tokens per warp: L rounds of 32/L tokens x L lanes stream the rows and form
     // S; then lane l finishes token l of the batch (draws, branch, prefix search / tree).  The
@@ -633,14 +629,9 @@ __global__ void __launch_bounds__(NT, MINB) sampler_quad_pf_kernel(SamplerArgs a
     float* s_bhat = sm;
     float* s_l8 = sm + a.K_pad;
     float* s_ck = s_l8 + a.l8_stride;  // [NW][32 tokens][kCkStride]
-    {
-        const float4* gb = reinterpret_cast<const float4*>(a.bhat + static_cast<size_t>(v) * a.K_pad);
-        float4* sb = reinterpret_cast<float4*>(sm);
-        for (uint32_t i = threadIdx.x; i < a.K_pad / 4; i += NT) sb[i] = __ldg(gb + i);
-        const float4* gl = reinterpret_cast<const float4*>(a.l8 + static_cast<size_t>(v) * a.l8_stride);
-        float4* sl = reinterpret_cast<float4*>(s_l8);
-        for (uint32_t i = threadIdx.x; i < a.l8_stride / 4; i += NT) sl[i] = __ldg(gl + i);
-    }
+    __shared__ __align__(8) unsigned long long s_bar;  // phi/L8 staging (TMA bulk copies)
+    tma_stage_rows(sm, a.bhat + static_cast<size_t>(v) * a.K_pad, a.K_pad * 4u, s_l8,
+                   a.l8 + static_cast<size_t>(v) * a.l8_stride, a.l8_stride * 4u, &s_bar);
     const uint32_t tbits = a.tbits, tmask = (1u << tbits) - 1u;
     const uint4* A4 = reinterpret_cast<const uint4*>(a.A);
     const uint32_t lane = lane_id(), t = lane / L, sub = lane % L, lead = lane & ~(L - 1u);
@@ -668,6 +659,7 @@ __global__ void __launch_bounds__(NT, MINB) sampler_quad_pf_kernel(SamplerArgs a
         const uint32_t rq0 = __shfl_sync(0xffffffffu, tk.x, t);
         if (base + t < unit.length) c = ldg_sector(A4 + rq0 + 2 * sub);
     }
+    tma_wait_rows(&s_bar);  // phi + L8 landed (the first lines are already in flight)
     while (base < unit.length) {
         const bool mine = base + lane < unit.length;
         uint32_t nb = 0;
