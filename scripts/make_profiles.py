@@ -66,6 +66,19 @@ def kernels(tag):
             "smsp__average_warps_issue_stalled_short_scoreboard_per_issue_active.ratio"]
     slim = [{k: kk[k] for k in ["name"] + [m for m in keep if m in kk] + [m + "@unit" for m in keep if m in kk]}
             for kk in out]
+    # The evidence the north star asks for, per kernel: achieved DRAM GB/s (bytes moved / time,
+    # under ncu), warp execution efficiency (active threads per issued instruction / 32) and
+    # shared-memory bank conflicts.
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
+    tscale = {"nsecond": 1e-9, "usecond": 1e-6, "msecond": 1e-3, "second": 1.0, "ns": 1e-9, "us": 1e-6, "ms": 1e-3}
+    for k in slim:
+        try:
+            byts = sum(k[m] * scale.get(k.get(m + "@unit", "byte"), 1) for m in ("dram__bytes_read.sum", "dram__bytes_write.sum"))
+            secs = k["gpu__time_duration.sum"] * tscale.get(k.get("gpu__time_duration.sum@unit", "ms"), 1e-3)
+            k["derived_dram_gbs"] = byts / secs / 1e9
+            k["derived_warp_exec_efficiency"] = k["smsp__thread_inst_executed_per_inst_executed.ratio"] / 32.0
+        except (KeyError, ZeroDivisionError):
+            pass
     (REPO / "profiles" / f"{tag}_ncu_kernels.json").write_text(json.dumps(slim, indent=1))
     for k in slim:
         if "sampler" in k["name"]:
