@@ -216,15 +216,22 @@ __device__ __forceinline__ uint32_t warp_incl_scan(uint32_t x, uint32_t lane) {
     return x;
 }
 
-template <int R, bool kCompact>
-__device__ __forceinline__ uint32_t ssc_doc_bitmap(const uint16_t* z, uint32_t n, uint32_t lane,
-                                                   const SscBitmapSmem& w, uint32_t n1, uint32_t* out_row,
-                                                   uint32_t tbits) {
-    uint32_t key[R];
+// Topics of one document striped over the warp (topic i in lane i % 32, register i / 32),
+// 0xFFFFFFFF past the end.
+template <int R>
+__device__ __forceinline__ void ssc_load_keys(const uint16_t* z, uint32_t n, uint32_t lane, uint32_t* key) {
 #pragma unroll
     for (uint32_t r = 0; r < R; ++r) {
         const uint32_t i = r * 32 + lane;
-        key[r] = i < n ? static_cast<uint32_t>(z[i]) : 0xFFFFFFFFu;
+        key[r] = i < n ? static_cast<uint32_t>(__ldg(z + i)) : 0xFFFFFFFFu;
+    }
+}
+
+template <int R, bool kCompact>
+__device__ __forceinline__ uint32_t ssc_doc_bitmap(const uint32_t* key, uint32_t lane, const SscBitmapSmem& w,
+                                                   uint32_t n1, uint32_t* out_row, uint32_t tbits) {
+#pragma unroll
+    for (uint32_t r = 0; r < R; ++r) {
         if (key[r] != 0xFFFFFFFFu) {
             atomicOr(w.bm0 + (key[r] >> 5), 1u << (key[r] & 31u));
             atomicOr(w.bm1 + (key[r] >> 10), 1u << ((key[r] >> 5) & 31u));
@@ -317,18 +324,40 @@ __global__ void __launch_bounds__(kSscBmWarps * 32) ssc_bitmap_kernel(SscArgs a)
     __syncwarp();
     unsigned long long nnz_acc = 0;
     const uint32_t gw = blockIdx.x * kSscBmWarps + wid, nw = gridDim.x * kSscBmWarps;
+    // Software pipeline over the warp's documents: the next document's extent, row offset and
+    // (up to 128) topics are loaded while this one is counted.
+    auto meta = [&](uint32_t dd, uint32_t& s0, uint32_t& n, uint32_t& rq) {
+        s0 = 0; n = 0; rq = 0;
+        if (dd < a.D) {
+            s0 = __ldg(a.doc_start + dd);
+            n = __ldg(a.doc_start + dd + 1) - s0;
+            rq = __ldg(a.row4 + dd);
+        }
+    };
+    uint32_t s0, n, rq, key[4];
+    meta(gw, s0, n, rq);
+    ssc_load_keys<4>(a.z + s0, n <= 128 ? n : 0u, lane, key);
     for (uint32_t d = gw; d < a.D; d += nw) {
-        const uint32_t s0 = __ldg(a.doc_start + d);
-        const uint32_t n = __ldg(a.doc_start + d + 1) - s0;
-        if (n > kSscWarpCap || n == 0) continue;  // ssc_long_kernel / empty document
-        uint32_t* row = a.A + __ldg(a.row4 + d) * 4u;
-        const uint16_t* z = a.z + s0;
+        const uint32_t cs0 = s0, cn = n;
+        uint32_t* row = a.A + rq * 4u;
+        const uint32_t k0 = key[0], k1 = key[1], k2 = key[2], k3 = key[3];
+        meta(d + nw, s0, n, rq);
+        ssc_load_keys<4>(a.z + s0, n <= 128 ? n : 0u, lane, key);
+        if (cn > kSscWarpCap || cn == 0) continue;  // ssc_long_kernel / empty document
         uint32_t nnz;
-        if (n <= 32) nnz = ssc_doc_bitmap<1, kCompact>(z, n, lane, w, n1, row, a.tbits);
-        else if (n <= 64) nnz = ssc_doc_bitmap<2, kCompact>(z, n, lane, w, n1, row, a.tbits);
-        else if (n <= 128) nnz = ssc_doc_bitmap<4, kCompact>(z, n, lane, w, n1, row, a.tbits);
-        else if (n <= 256) nnz = ssc_doc_bitmap<8, kCompact>(z, n, lane, w, n1, row, a.tbits);
-        else nnz = ssc_doc_bitmap<16, kCompact>(z, n, lane, w, n1, row, a.tbits);
+        const uint32_t ck[4] = {k0, k1, k2, k3};
+        if (cn <= 32) nnz = ssc_doc_bitmap<1, kCompact>(ck, lane, w, n1, row, a.tbits);
+        else if (cn <= 64) nnz = ssc_doc_bitmap<2, kCompact>(ck, lane, w, n1, row, a.tbits);
+        else if (cn <= 128) nnz = ssc_doc_bitmap<4, kCompact>(ck, lane, w, n1, row, a.tbits);
+        else if (cn <= 256) {
+            uint32_t k8[8];
+            ssc_load_keys<8>(a.z + cs0, cn, lane, k8);
+            nnz = ssc_doc_bitmap<8, kCompact>(k8, lane, w, n1, row, a.tbits);
+        } else {
+            uint32_t k16[16];
+            ssc_load_keys<16>(a.z + cs0, cn, lane, k16);
+            nnz = ssc_doc_bitmap<16, kCompact>(k16, lane, w, n1, row, a.tbits);
+        }
         nnz_acc += nnz;
     }
     if (lane == 0 && nnz_acc) atomicAdd(a.nnz_total, nnz_acc);
