@@ -313,8 +313,10 @@ struct slda_engine {
             // M-step's CTAs are dispatched first while both are pending.
             int least = 0, greatest = 0;
             CK(cudaDeviceGetStreamPriorityRange(&least, &greatest));
-            CK(cudaStreamCreateWithPriority(&stream, cudaStreamNonBlocking, greatest));
-            CK(cudaStreamCreateWithPriority(&side, cudaStreamNonBlocking, least));
+            const char* pr = std::getenv("SLDA_SSC_PRIORITY");  // "high": SSC's CTAs first (experiment)
+            const bool ssc_high = pr && std::string(pr) == "high";
+            CK(cudaStreamCreateWithPriority(&stream, cudaStreamNonBlocking, ssc_high ? least : greatest));
+            CK(cudaStreamCreateWithPriority(&side, cudaStreamNonBlocking, ssc_high ? greatest : least));
         }
         for (auto& set : ring)
             for (auto& e : set) CK(cudaEventCreate(&e));
