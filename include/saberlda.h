@@ -74,7 +74,8 @@ typedef struct slda_config {
     int32_t device;           /* CUDA ordinal; -1 = current device */
     uint32_t rank;            /* document shard index (0 for one GPU) */
     uint32_t world_size;      /* number of shards/GPUs (1 = no collectives) */
-    const void* nccl_id;      /* 128-byte ncclUniqueId from rank 0 when world_size > 1 */
+    const void* nccl_id;      /* 128-byte ncclUniqueId from rank 0 when world_size > 1 (NCCL
+                                 collectives); NULL: peer-memory exchange (slda_peer_attach) */
 } slda_config;
 
 /* sparselda::IterationStats (trainer.hpp:38-44) + device timings. */
@@ -214,6 +215,29 @@ int slda_generate_corpus(const slda_gen_params* p, uint32_t* tokens, uint64_t ca
 int slda_generate_doc_lengths(const slda_gen_params* p, uint32_t* lengths);
 int slda_generate_docs(const slda_gen_params* p, uint32_t doc_begin, uint32_t doc_end,
                        uint32_t* tokens, uint64_t capacity);
+
+/* ---- Peer-memory exchange (multi-GPU without NCCL) ------------------------------------------
+ * Create every rank's engine with world_size > 1 and nccl_id == NULL, export each engine's
+ * buffer handles (CUDA IPC), exchange them over any host channel, and attach every engine to
+ * all ranks' handles (indexed by rank).  The M-step then reduce-scatters C_wk, all-reduces C_k
+ * and all-gathers phi / L4 / L8 / Q inside its own kernels over peer memory (NVLink on a
+ * multi-GPU node; the same HBM when ranks share one GPU) -- the NCCL collectives of the default
+ * path (engine m_step, trainer.cpp:395-400 / 436-440 semantics) folded into the computation.
+ * slda_peer_attach runs init_state's first M-step and is collective, as is
+ * slda_get_word_topic on a peer-attached engine. */
+#define SLDA_PEER_HANDLE_BYTES 64
+typedef struct slda_peer_handles {
+    unsigned char word_topic[SLDA_PEER_HANDLE_BYTES];      /* partial / reduced C_wk */
+    unsigned char colsum[SLDA_PEER_HANDLE_BYTES];          /* partial C_k */
+    unsigned char word_topic_prob[SLDA_PEER_HANDLE_BYTES]; /* phi replica */
+    unsigned char tree_prefix[SLDA_PEER_HANDLE_BYTES];     /* L4 replica */
+    unsigned char tree_l8[SLDA_PEER_HANDLE_BYTES];         /* L8 replica */
+    unsigned char tree_mass[SLDA_PEER_HANDLE_BYTES];       /* Q replica */
+    unsigned char barrier[SLDA_PEER_HANDLE_BYTES];         /* barrier counter (rank 0's is used) */
+} slda_peer_handles;
+
+int slda_peer_export(slda_engine* engine, slda_peer_handles* out);
+int slda_peer_attach(slda_engine* engine, const slda_peer_handles* all_ranks);
 
 #ifdef __cplusplus
 }

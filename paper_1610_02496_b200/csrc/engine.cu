@@ -223,6 +223,24 @@ struct slda_engine {
     uint32_t ring_launches[kRing] = {};
     uint32_t slot = 0;
     ncclComm_t comm = nullptr;
+    // Peer-memory exchange (world > 1 without an NCCL id): the other ranks' buffers mapped
+    // through CUDA IPC handles (slda_peer_export / slda_peer_attach).
+    bool peer = false, attached = false;
+    DevMem bar, coltot;                    // barrier counter (rank 0's is the shared one), C_k total
+    void* pB[slda::kMaxPeers] = {};
+    void* pcol[slda::kMaxPeers] = {};
+    void* pbhat[slda::kMaxPeers] = {};
+    void* pl4[slda::kMaxPeers] = {};
+    void* pl8[slda::kMaxPeers] = {};
+    void* pq[slda::kMaxPeers] = {};
+    unsigned long long* pbar = nullptr;
+    uint64_t bar_seq = 0;
+    std::vector<void*> opened;             // IPC mappings to close
+    void peer_barrier() {
+        ++bar_seq;
+        CK(slda::launch_peer_barrier(pbar, static_cast<unsigned long long>(world) * bar_seq, stream));
+    }
+    void m_step_peer();
     uint32_t launches = 0;
 
     unsigned long long* nnz_counter() const { return counters.as<unsigned long long>(); }
@@ -250,6 +268,7 @@ struct slda_engine {
             for (auto& e : set)
                 if (e) cudaEventDestroy(e);
         if (comm) nccl().CommDestroy(comm);
+        for (void* p : opened) cudaIpcCloseMemHandle(p);
         if (side) cudaStreamDestroy(side);
         if (stream) cudaStreamDestroy(stream);
     }
@@ -320,8 +339,12 @@ struct slda_engine {
         }
         for (auto& set : ring)
             for (auto& e : set) CK(cudaEventCreate(&e));
-        if (world > 1) {
-            if (!c.nccl_id) validation("nccl_id required when world_size > 1");
+        if (world > 1 && !c.nccl_id) {
+            // No NCCL id: the ranks exchange through each other's memory (slda_peer_attach).
+            if (world > slda::kMaxPeers)
+                validation("peer-memory exchange supports world_size <= " + std::to_string(slda::kMaxPeers));
+            peer = true;
+        } else if (world > 1) {
             ncclUniqueId id;
             std::memcpy(&id, c.nccl_id, sizeof(id));
             nccl_check(nccl().CommInitRank(&comm, static_cast<int>(world), id, static_cast<int>(rank)),
@@ -619,7 +642,13 @@ void slda_engine::build(const slda_corpus_view& cv, const slda_config& c) {
     slda::RecountDraw rd{seed, id_base, ids.p ? ids.as<uint64_t>() : nullptr, draw ? K : 0u};
     CK(slda::launch_recount(tok.as<uint2>(), units.as<slda::Unit>(), n_units, z.as<uint16_t>(),
                             B.as<uint32_t>(), K_pad, rd, stream));
-    m_step();
+    if (peer) {  // the first M-step needs the other ranks: it runs in slda_peer_attach
+        bar.alloc(8, &device_bytes);
+        CK(cudaMemsetAsync(bar.p, 0, 8, stream));
+        coltot.alloc(static_cast<size_t>(K_pad) * 8, &device_bytes);
+    } else {
+        m_step();
+    }
     CK(cudaStreamSynchronize(stream));
     nnz = d2h_scalar(nnz_counter());
     phase("ssc + recount + m_step");
@@ -648,6 +677,10 @@ void slda_engine::ssc(cudaStream_t st) {
 // M-step after the E-step's B: (reduce-scatter) -> colsum -> (all-reduce) -> phi/L4 on the
 // own word slice -> (all-gather).  preprocess (counts.cpp:37-63) + rebuild_trees.
 void slda_engine::m_step() {
+    if (peer) {
+        m_step_peer();
+        return;
+    }
     const uint32_t r0 = row_begin(), r1 = row_end();
     const size_t slice_cells = static_cast<size_t>(slice_rows()) * K_pad;
     CK(cudaEventRecord(ev[3], stream));
@@ -686,8 +719,52 @@ void slda_engine::m_step() {
     CK(cudaEventRecord(ev[6], stream));
 }
 
+// The M-step with the exchange fused into its kernels over the other ranks' memory (mstep.cu):
+// barrier -> colsum over the own word slice of every rank's partial C_wk (the reduce-scatter;
+// the reduced slice is written into this rank's B) -> barrier -> C_k total from every rank's
+// partial (the all-reduce) -> phi / L4 / L8 / Q of the own slice, stored into every rank's
+// replica (the all-gather) -> barrier.  Integer sums and per-row f32 chains: bit-identical to
+// one GPU and to the NCCL path.
+void slda_engine::m_step_peer() {
+    if (!attached) validation("peer-memory exchange: call slda_peer_attach on every rank first");
+    const uint32_t r0 = row_begin(), r1 = row_end();
+    CK(cudaEventRecord(ev[3], stream));
+    peer_barrier();  // every rank's partial C_wk is complete
+    slda::PeerCounts pcs{};
+    for (uint32_t p = 0; p < world; ++p)
+        pcs.B[p] = p == rank ? B.as<uint32_t>() : static_cast<const uint32_t*>(pB[p]);
+    pcs.n = world;
+    CK(cudaMemsetAsync(colsum.p, 0, colsum.bytes, stream));
+    CK(slda::launch_peer_colsum(pcs, B.as<uint32_t>(), r0, r1, K_pad, colsum.as<unsigned long long>(), stream));
+    peer_barrier();  // every rank's C_k partial is complete (and no rank reads a partial C_wk again)
+    slda::PeerColsums pc{};
+    for (uint32_t p = 0; p < world; ++p)
+        pc.c[p] = p == rank ? colsum.as<unsigned long long>() : static_cast<const unsigned long long*>(pcol[p]);
+    pc.n = world;
+    CK(slda::launch_peer_total(pc, K_pad, coltot.as<unsigned long long>(), stream));
+    CK(slda::launch_denom(coltot.as<unsigned long long>(), K, K_pad, V, beta, denom.as<double>(), zv.as<float>(),
+                          stream));
+    CK(cudaEventRecord(ev[4], stream));
+    slda::PeerMirror m{};
+    for (uint32_t p = 0; p < world; ++p) {
+        if (p == rank) continue;
+        m.bhat[m.n] = static_cast<float*>(pbhat[p]);
+        m.l4[m.n] = static_cast<float*>(pl4[p]);
+        m.l8[m.n] = static_cast<float*>(pl8[p]);
+        m.q[m.n] = static_cast<float*>(pq[p]);
+        ++m.n;
+    }
+    CK(slda::launch_phi(B.as<uint32_t>(), denom.as<double>(), zv.as<float>(), bhat.as<float>(), l4.as<float>(),
+                        l8.as<float>(), q.as<float>(), r0, r1, K, K_pad, l8_stride, beta, falpha, stream, &m));
+    launches += 5;
+    CK(cudaEventRecord(ev[5], stream));
+    peer_barrier();  // every replica holds every slice
+    CK(cudaEventRecord(ev[6], stream));
+}
+
 // run_iteration (trainer.cpp:419-449) on the engine stream.
 void slda_engine::enqueue_iteration() {
+    if (peer && !attached) validation("peer-memory exchange: call slda_peer_attach on every rank first");
     launches = 0;
     slot = iteration % kRing;
     ev = ring[slot];
@@ -907,6 +984,22 @@ int slda_get_word_topic(slda_engine* e, uint32_t* out) {
     return guarded([&] {
         if (!e || !out) validation("null argument");
         e->set_device();
+        if (e->world > 1 && e->peer) {
+            // Collective: each rank's B holds the reduced C_wk of its own slice; copy the others'
+            // slices out of their memory between two barriers.
+            const size_t slice = static_cast<size_t>(e->slice_rows()) * e->K_pad;
+            DevMem full;
+            full.alloc(e->B.bytes, nullptr);
+            e->peer_barrier();
+            for (uint32_t p = 0; p < e->world; ++p) {
+                const uint32_t* src = p == e->rank ? e->B.as<uint32_t>() : static_cast<const uint32_t*>(e->pB[p]);
+                CK(cudaMemcpyAsync(full.as<uint32_t>() + p * slice, src + p * slice, slice * 4,
+                                   cudaMemcpyDeviceToDevice, e->stream));
+            }
+            e->peer_barrier();
+            copy_matrix(e, full, out);
+            return;
+        }
         if (e->world > 1) {
             // After the reduce-scatter each rank owns its slice; gather the rest.
             const size_t slice = static_cast<size_t>(e->slice_rows()) * e->K_pad;
@@ -950,6 +1043,58 @@ int slda_get_assignments(slda_engine* e, uint32_t* out) {
         CK(slda::launch_assignments(e->z.as<uint16_t>(), e->doc_major ? nullptr : e->input_of_slot.as<uint32_t>(),
                                     e->T, e->assign_buf.as<uint32_t>(), e->stream));
         CK(cudaMemcpyAsync(out, e->assign_buf.p, e->T * 4, cudaMemcpyDeviceToHost, e->stream));
+        CK(cudaStreamSynchronize(e->stream));
+    });
+}
+
+int slda_peer_export(slda_engine* e, slda_peer_handles* out) {
+    return guarded([&] {
+        if (!e || !out) validation("null argument");
+        if (!e->peer) validation("slda_peer_export: engine was not created for peer-memory exchange");
+        e->set_device();
+        auto h = [&](const DevMem& m, unsigned char* dst) {
+            cudaIpcMemHandle_t ih;
+            CK(cudaIpcGetMemHandle(&ih, m.p));
+            static_assert(sizeof(ih) == SLDA_PEER_HANDLE_BYTES, "cudaIpcMemHandle_t size");
+            std::memcpy(dst, &ih, sizeof(ih));
+        };
+        h(e->B, out->word_topic);
+        h(e->colsum, out->colsum);
+        h(e->bhat, out->word_topic_prob);
+        h(e->l4, out->tree_prefix);
+        h(e->l8, out->tree_l8);
+        h(e->q, out->tree_mass);
+        h(e->bar, out->barrier);
+    });
+}
+
+int slda_peer_attach(slda_engine* e, const slda_peer_handles* all) {
+    return guarded([&] {
+        if (!e || !all) validation("null argument");
+        if (!e->peer) validation("slda_peer_attach: engine was not created for peer-memory exchange");
+        if (e->attached) validation("slda_peer_attach: already attached");
+        e->set_device();
+        auto open = [&](const unsigned char* src) -> void* {
+            cudaIpcMemHandle_t ih;
+            std::memcpy(&ih, src, sizeof(ih));
+            void* p = nullptr;
+            CK(cudaIpcOpenMemHandle(&p, ih, cudaIpcMemLazyEnablePeerAccess));
+            e->opened.push_back(p);
+            return p;
+        };
+        for (uint32_t r = 0; r < e->world; ++r) {
+            if (r == e->rank) continue;
+            e->pB[r] = open(all[r].word_topic);
+            e->pcol[r] = open(all[r].colsum);
+            e->pbhat[r] = open(all[r].word_topic_prob);
+            e->pl4[r] = open(all[r].tree_prefix);
+            e->pl8[r] = open(all[r].tree_l8);
+            e->pq[r] = open(all[r].tree_mass);
+        }
+        e->pbar = e->rank == 0 ? e->bar.as<unsigned long long>()
+                               : static_cast<unsigned long long*>(open(all[0].barrier));
+        e->attached = true;
+        e->m_step();  // init_state's M-step (trainer.cpp:395-400), now that every rank is reachable
         CK(cudaStreamSynchronize(e->stream));
     });
 }

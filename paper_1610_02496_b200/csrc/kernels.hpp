@@ -63,10 +63,31 @@ cudaError_t launch_colsum(const uint32_t* B, uint32_t row_begin, uint32_t row_en
                           unsigned long long* colsum, cudaStream_t s);
 cudaError_t launch_denom(const unsigned long long* colsum, uint32_t K, uint32_t K_pad, uint32_t V,
                          double beta, double* denom, float* zv, cudaStream_t s);
+// Peer-memory exchange (engine.cu m_step_peer): up to kMaxPeers ranks.
+constexpr uint32_t kMaxPeers = 8;
+struct PeerMirror {  // the other ranks' phi / L4 / L8 / Q replicas
+    float* bhat[kMaxPeers];
+    float* l4[kMaxPeers];
+    float* l8[kMaxPeers];
+    float* q[kMaxPeers];
+    uint32_t n;
+};
+struct PeerCounts {  // every rank's partial C_wk (own included)
+    const uint32_t* B[kMaxPeers];
+    uint32_t n;
+};
+struct PeerColsums {  // every rank's partial C_k (own included)
+    const unsigned long long* c[kMaxPeers];
+    uint32_t n;
+};
 cudaError_t launch_phi(const uint32_t* B, const double* denom, const float* zv, float* bhat,
                        float* l4, float* l8, float* q, uint32_t row_begin, uint32_t row_end,
                        uint32_t K, uint32_t K_pad, uint32_t l8_stride, double beta, float falpha,
-                       cudaStream_t s);
+                       cudaStream_t s, const PeerMirror* mirror = nullptr);
+cudaError_t launch_peer_barrier(unsigned long long* counter, unsigned long long target, cudaStream_t s);
+cudaError_t launch_peer_colsum(const PeerCounts& pc, uint32_t* B, uint32_t row_begin, uint32_t row_end,
+                               uint32_t K_pad, unsigned long long* colsum, cudaStream_t s);
+cudaError_t launch_peer_total(const PeerColsums& pc, uint32_t K_pad, unsigned long long* total, cudaStream_t s);
 
 // Setup kernels.
 cudaError_t launch_deinterleave(const uint32_t* aos, uint64_t T, uint32_t doc_begin,

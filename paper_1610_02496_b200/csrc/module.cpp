@@ -263,6 +263,25 @@ PYBIND11_MODULE(_core, m) {
              py::call_guard<py::gil_scoped_release>())
         .def("synchronize", [](ModelState& s) { check(slda_synchronize(s.engine())); },
              py::call_guard<py::gil_scoped_release>())
+        .def("peer_handles",
+             [](const ModelState& s) {
+                 slda_peer_handles h{};
+                 check(slda_peer_export(s.engine(), &h));
+                 return py::bytes(reinterpret_cast<const char*>(&h), sizeof(h));
+             })
+        .def("peer_attach",
+             [](ModelState& s, const std::vector<std::string>& all) {
+                 std::vector<slda_peer_handles> hs(all.size());
+                 for (std::size_t r = 0; r < all.size(); ++r) {
+                     if (all[r].size() != sizeof(slda_peer_handles))
+                         throw ValidationError("peer handles must be " + std::to_string(sizeof(slda_peer_handles)) +
+                                               " bytes per rank");
+                     std::memcpy(&hs[r], all[r].data(), sizeof(slda_peer_handles));
+                 }
+                 py::gil_scoped_release release;
+                 check(slda_peer_attach(s.engine(), hs.data()));
+             },
+             py::arg("all_ranks"))
         .def("stream_ptr",
              [](const ModelState& s) { return reinterpret_cast<std::uintptr_t>(slda_stream(s.engine())); });
 
@@ -272,10 +291,10 @@ PYBIND11_MODULE(_core, m) {
         "init_shard",
         [](const Corpus& corpus, const TrainConfig& cfg, std::uint32_t rank, std::uint32_t world,
            py::bytes nccl_id) {
-            std::string id = nccl_id;
-            if (world > 1 && id.size() != 128) throw ValidationError("nccl_id must be 128 bytes");
+            std::string id = nccl_id;  // empty with world > 1: peer-memory exchange (Model.peer_attach)
+            if (world > 1 && !id.empty() && id.size() != 128) throw ValidationError("nccl_id must be 128 bytes");
             py::gil_scoped_release release;
-            return init_shard(corpus, cfg, rank, world, world > 1 ? id.data() : nullptr);
+            return init_shard(corpus, cfg, rank, world, world > 1 && !id.empty() ? id.data() : nullptr);
         },
         py::arg("corpus"), py::arg("config"), py::arg("rank"), py::arg("world"), py::arg("nccl_id") = py::bytes());
     m.def("shard_bounds", [](const Corpus& c, std::uint32_t world) { return shard_bounds(c, world); },
@@ -297,8 +316,8 @@ PYBIND11_MODULE(_core, m) {
            std::uint32_t doc_begin, std::uint32_t doc_end, std::uint64_t token_id_base, const TrainConfig& cfg,
            std::uint32_t rank, std::uint32_t world, py::bytes nccl_id, std::uint32_t init_mode) {
             if (tokens.ndim() != 2 || tokens.shape(1) != 3) throw ValidationError("tokens must be (T, 3) uint32");
-            std::string id = nccl_id;
-            if (world > 1 && id.size() != 128) throw ValidationError("nccl_id must be 128 bytes");
+            std::string id = nccl_id;  // empty with world > 1: peer-memory exchange (Model.peer_attach)
+            if (world > 1 && !id.empty() && id.size() != 128) throw ValidationError("nccl_id must be 128 bytes");
             slda_corpus_view v{};
             v.num_docs = num_docs;
             v.vocab_size = vocab_size;
@@ -308,7 +327,7 @@ PYBIND11_MODULE(_core, m) {
             v.doc_end = doc_end;
             v.token_id_base = token_id_base;
             py::gil_scoped_release release;
-            return init_view(v, cfg, rank, world, world > 1 ? id.data() : nullptr, init_mode);
+            return init_view(v, cfg, rank, world, world > 1 && !id.empty() ? id.data() : nullptr, init_mode);
         },
         py::arg("tokens"), py::arg("num_docs"), py::arg("vocab_size"), py::arg("doc_begin"), py::arg("doc_end"),
         py::arg("token_id_base"), py::arg("config"), py::arg("rank") = 0, py::arg("world") = 1,

@@ -1,0 +1,113 @@
+"""GPU, world_size 2 on ONE B200: the peer-memory M-step exchange, bit for bit.
+
+Two processes each own a document shard (the chunk_boundaries rule) and an engine created
+without an NCCL id; they exchange CUDA IPC handles of their C_wk / C_k / phi / L4 / L8 / Q
+buffers and attach (include/saberlda.h, slda_peer_attach).  From then on every M-step does the
+reduce-scatter of C_wk inside its colsum kernel, the all-reduce of C_k inside the denominator
+kernel and the all-gather of phi / L4 / L8 / Q inside the phi kernel's epilogue, over the other
+rank's memory, meeting at device-side barriers (mstep.cu).  On a multi-GPU node the same code
+runs over NVLink peer memory; here both ranks share one GPU, which exercises the same kernels,
+handles and barriers.  The assembled state must equal the reference's digests for the C1 case
+at every iteration -- exactly what one GPU produces.
+"""
+import multiprocessing as mp
+import traceback
+
+import numpy as np
+import pytest
+
+from corpora import CASES, corpus_arrays
+from oracle_lib import digest
+
+pytestmark = pytest.mark.gpu
+
+WORLD = 2
+ITERS = 6
+
+
+def _rank_main(rank, case, to_parent, from_parent):
+    try:
+        import paper_1610_02496_b200 as slda
+        import paper_1610_02496_b200._core as core
+
+        spec = CASES[case]
+        doc, word, D, V = corpus_arrays(spec["corpus"])
+        lens = np.bincount(doc, minlength=D).astype(np.uint32)
+        bounds = core.shard_bounds_from_lengths(lens, WORLD)
+        b, e = bounds[rank], bounds[rank + 1]
+        csum = np.concatenate([[0], np.cumsum(lens.astype(np.int64))])
+        sel = slice(int(csum[b]), int(csum[e]))
+        toks = np.stack([doc[sel], word[sel], np.full(sel.stop - sel.start, 0xFFFFFFFF, np.uint32)], 1)
+        toks = np.ascontiguousarray(toks.astype(np.uint32))
+        cfg = slda.TrainConfig()
+        cfg.num_topics = spec["K"]
+        cfg.seed = spec["seed"]
+        cfg.device = 0
+        m = core.init_view(toks, D, V, int(b), int(e), int(csum[b]), cfg, rank, WORLD, b"", 1)
+        to_parent.put(("handles", rank, m.peer_handles()))
+        all_handles = from_parent.get()
+        m.peer_attach(all_handles)
+        out = []
+        for it in range(ITERS + 1):
+            offs, tops, cnts = m.doc_topic()
+            out.append({
+                "assignments": m.assignments(),
+                "word_topic": m.word_topic(),  # collective in peer mode
+                "word_topic_prob": m.word_topic_prob(),
+                "l4": m.tree_prefix(),
+                "tree_mass": m.tree_mass(),
+                "doc_topic": (offs.astype(np.uint64), tops.copy(), cnts.copy()),
+            })
+            if it < ITERS:
+                m.run_iteration(cfg)
+        to_parent.put(("result", rank, out))
+    except Exception:  # noqa: BLE001 -- reported to the parent
+        to_parent.put(("error", rank, traceback.format_exc()))
+
+
+def test_peer_memory_exchange_matches_reference(golden):
+    case = "c1"
+    ctx = mp.get_context("spawn")
+    to_parent = ctx.Queue()
+    inboxes = [ctx.Queue() for _ in range(WORLD)]
+    procs = [ctx.Process(target=_rank_main, args=(r, case, to_parent, inboxes[r])) for r in range(WORLD)]
+    for p in procs:
+        p.start()
+    handles, results = {}, {}
+    try:
+        while len(results) < WORLD:
+            kind, rank, payload = to_parent.get(timeout=600)
+            if kind == "error":
+                raise AssertionError(f"rank {rank} failed:\n{payload}")
+            if kind == "handles":
+                handles[rank] = payload
+                if len(handles) == WORLD:
+                    for q in inboxes:
+                        q.put([handles[r] for r in range(WORLD)])
+            else:
+                results[rank] = payload
+    finally:
+        for p in procs:
+            p.join(timeout=60)
+            if p.is_alive():
+                p.kill()
+    fx = golden["cases"][case]
+    for it in range(ITERS + 1):
+        r0, r1 = results[0][it], results[1][it]
+        # Replicated state: identical on both ranks.
+        for key in ("word_topic", "word_topic_prob", "l4", "tree_mass"):
+            assert np.array_equal(r0[key], r1[key]), (it, key)
+        offs0, t0, c0 = r0["doc_topic"]
+        offs1, t1, c1 = r1["doc_topic"]
+        offs = np.concatenate([offs0, offs1[1:] + offs0[-1]])
+        got = {
+            "assignments": digest(np.concatenate([r0["assignments"], r1["assignments"]])),
+            "word_topic": digest(r0["word_topic"]),
+            "word_topic_prob": digest(r0["word_topic_prob"]),
+            "l4": digest(r0["l4"]),
+            "tree_mass": digest(r0["tree_mass"]),
+            "doc_topic": digest(np.concatenate([offs.view(np.uint32), np.concatenate([t0, t1]),
+                                                np.concatenate([c0, c1])])),
+        }
+        expect = fx["iterations"][it]
+        assert got == expect, (it, sorted(k for k in got if got[k] != expect[k]))
