@@ -191,6 +191,8 @@ def main() -> None:
     ap.add_argument("--cpu-sample-tokens", type=int, default=16_000_000)
     ap.add_argument("--cpu-steps", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--exchange", default="peer", choices=["peer", "nccl"],
+                    help="N > 1: M-step exchange fused into the kernels over peer memory (default) or NCCL")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
 
@@ -220,12 +222,20 @@ def main() -> None:
 
     import torch
 
-    torch.cuda.set_device(local_rank)
+    # SLDA_BENCH_ONE_GPU=1 (validation only): every rank on cuda:0, gloo for the host-side
+    # plumbing -- exercises the N > 1 path (sharding, peer-memory exchange) on a one-GPU box.
+    one_gpu = os.environ.get("SLDA_BENCH_ONE_GPU") == "1"
+    dev = 0 if one_gpu else local_rank
+    torch.cuda.set_device(dev)
+    coll_dev = "cpu" if one_gpu else "cuda"
     dist = None
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if one_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     import paper_1610_02496_b200 as slda
     import paper_1610_02496_b200._core as core
 
@@ -252,7 +262,7 @@ def main() -> None:
     tc = slda.TrainConfig()
     tc.num_topics = cfg["K"]
     tc.seed = TRAIN_SEED
-    tc.device = local_rank
+    tc.device = dev
     tc.tree_branch = 32 if cfg["K"] <= 32768 else 41
 
     # Context / module warm-up outside any timed region.
@@ -269,7 +279,7 @@ def main() -> None:
     def max_over_ranks(x: float) -> float:
         if not dist:
             return x
-        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        t = torch.tensor([x], dtype=torch.float64, device=coll_dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
@@ -279,8 +289,32 @@ def main() -> None:
     # + D2H of the assignments (result).
     barrier()
     t0 = time.perf_counter()
-    model = core.init_view(host_tokens, cfg["D"], cfg["V"], b, e, int(csum[b]), tc, rank, world, nccl_id,
-                           1 if world > 1 else 0)
+    exchange = args.exchange if world > 1 else "none"
+
+    def create():
+        """init_state over this rank's shard; for N > 1 the engines meet through peer memory
+        (CUDA IPC handles exchanged over torch.distributed, then slda_peer_attach) or NCCL.
+        Any rank failing to map its peers falls every rank back to NCCL."""
+        nonlocal exchange
+        if exchange == "peer":
+            m = core.init_view(host_tokens, cfg["D"], cfg["V"], b, e, int(csum[b]), tc, rank, world, b"", 1)
+            handles = [None] * world
+            dist.all_gather_object(handles, m.peer_handles())
+            ok = torch.tensor([1], dtype=torch.int32, device=coll_dev)
+            try:
+                m.peer_attach(handles)
+            except Exception as exc:  # noqa: BLE001
+                print(f"rank {rank}: peer attach failed ({exc}); falling back to NCCL", file=sys.stderr)
+                ok.zero_()
+            dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+            if int(ok.item()) == 1:
+                return m
+            del m
+            exchange = "nccl"
+        return core.init_view(host_tokens, cfg["D"], cfg["V"], b, e, int(csum[b]), tc, rank, world, nccl_id,
+                              1 if world > 1 else 0)
+
+    model = create()
     for _ in range(args.steps):
         model.run_iteration(tc)
     model.assignments(assign_out)
@@ -290,7 +324,7 @@ def main() -> None:
     # ---- device-timed: W warm-up iterations, then exactly K timed iterations.
     stream = torch.cuda.ExternalStream(model.stream_ptr())
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local_rank) as clocks:
+    with ClockSampler(dev) as clocks:
         for _ in range(args.warmup):
             model.iterate_async()
         model.synchronize()
@@ -324,7 +358,9 @@ def main() -> None:
         "value": value, "ms_per_step": ms_per_step,
         "config": {"workload": cfg["name"], "D": cfg["D"], "V": cfg["V"], "T": cfg["T"], "K": cfg["K"],
                    "alpha": 50.0 / cfg["K"], "beta": 0.01, "seed": TRAIN_SEED, "corpus_seed": CORPUS_SEED,
-                   "parallelism": f"doc-shards x{world}" if world > 1 else "1 GPU",
+                   "parallelism": (f"doc-shards x{world}, M-step exchange: "
+                                   + ("fused into the kernels over NVLink peer memory" if exchange == "peer"
+                                      else "NCCL reduce-scatter / all-reduce / all-gather")) if world > 1 else "1 GPU",
                    "l2": "inputs larger than L2 (C_dk rows, phi, L4 are GBs; no flush needed)"},
         "roofline": {"bound": "hbm", "kernel": "sampler", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "traffic_config": traffic_cfg,
