@@ -290,6 +290,15 @@ def main() -> None:
     barrier()
     t0 = time.perf_counter()
     exchange = args.exchange if world > 1 else "none"
+    if exchange == "peer" and not one_gpu:
+        # Peer-memory exchange needs P2P access between every pair of GPUs (NVLink / NVSwitch);
+        # any rank without it sends every rank to NCCL.
+        local_world = int(os.environ.get("LOCAL_WORLD_SIZE", world))
+        ok = all(torch.cuda.can_device_access_peer(dev, o) for o in range(local_world) if o != dev)
+        flag = torch.tensor([1 if ok and local_world == world else 0], dtype=torch.int32, device=coll_dev)
+        dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+        if int(flag.item()) == 0:
+            exchange = "nccl"
 
     def create():
         """init_state over this rank's shard; for N > 1 the engines meet through peer memory
