@@ -218,7 +218,13 @@ cudaError_t launch_phi(const uint32_t* B, const double* denom, const float* zv, 
 __global__ void peer_barrier_kernel(unsigned long long* counter, unsigned long long target) {
     __threadfence_system();
     atomicAdd_system(counter, 1ull);
-    while (atomicAdd_system(counter, 0ull) < target) __nanosleep(256);
+    // A rank that died never arrives: give up after ~2 minutes (the kernel traps, the stream
+    // reports an error) instead of spinning forever.
+    const long long t0 = clock64();
+    while (atomicAdd_system(counter, 0ull) < target) {
+        __nanosleep(256);
+        if (clock64() - t0 > 240'000'000'000LL) __trap();
+    }
     __threadfence_system();
 }
 
