@@ -463,6 +463,10 @@ void slda_engine::build(const slda_corpus_view& cv, const slda_config& c) {
             });
             max_len = d2h_scalar(mx.as<uint32_t>());
         }
+        // Counts in the high half-word whenever they fit (K <= 65536 is required anyway and no
+        // document has more than 65535 tokens): the sampler's count decode is then one
+        // I2F.U16.H1 (sampler.cu kC16).  Longer documents keep the minimal topic field.
+        if (K <= 65536u && max_len <= 65535u) tbits = 16;
         if (tbits < 32 && (static_cast<uint64_t>(max_len) >> (32 - tbits)) != 0)
             validation("document of length " + std::to_string(max_len) +
                        " exceeds the packed C_dk count range at this K");

@@ -439,7 +439,7 @@ __global__ void __launch_bounds__(NT, NT <= 128 ? 3 : 2) sampler_stream_kernel(S
 // sum visits the 4 sectors of a line in order -- lane j adds its 8 products to the value lane
 // j-1 handed it (shuffle) -- so every intermediate is the reference's.  The per-sector sums
 // double as the prefix_search checkpoints (a few hundred bytes per warp instead of a stage).
-template <int NT, int MINB, int L, bool kCompact>
+template <int NT, int MINB, int L, bool kCompact, bool kC16 = false>
 __global__ void __launch_bounds__(NT, MINB) sampler_quad_kernel(SamplerArgs a) {
     constexpr uint32_t NW = NT / 32;
     constexpr uint32_t TPR = 32u / L;  // tokens per round (L lanes each, L sectors per group)
@@ -459,7 +459,8 @@ __global__ void __launch_bounds__(NT, MINB) sampler_quad_kernel(SamplerArgs a) {
                    a.l8 + static_cast<size_t>(v) * a.l8_stride, a.l8_stride * 4u, &s_bar);
     const float qv = __ldg(a.q + v);
     uint32_t* brow = a.B + static_cast<size_t>(v) * a.K_pad;
-    const uint32_t tbits = a.tbits, tmask = (1u << tbits) - 1u;
+    // kC16: counts in the high half-word (tbits == 16): the count decode folds into one I2F.U16.H1.
+    const uint32_t tbits = kC16 ? 16u : a.tbits, tmask = kC16 ? 0xFFFFu : (1u << a.tbits) - 1u;
     const uint4* A4 = reinterpret_cast<const uint4*>(a.A);
     const uint32_t lane = lane_id(), t = lane / L, sub = lane % L, lead = lane & ~(L - 1u);
     const uint32_t warp = threadIdx.x >> 5;
@@ -615,7 +616,7 @@ __global__ void __launch_bounds__(NT, MINB) sampler_quad_kernel(SamplerArgs a) {
 // The same algorithm with the next round's first line prefetched in each round's last group
 // slot and the next batch claimed a batch ahead; the per-unit scalars live in shared memory to
 // make room in the 64-register budget (C3 K=10K: 95.5 -> 92.8 ms; C2: 19.8 -> 20.5 ms).
-template <int NT, int MINB, int L, bool kCompact, bool kPrefetchNext = true>
+template <int NT, int MINB, int L, bool kCompact, bool kC16 = false, bool kPrefetchNext = true>
 __global__ void __launch_bounds__(NT, MINB) sampler_quad_pf_kernel(SamplerArgs a) {
     constexpr uint32_t NW = NT / 32;
     constexpr uint32_t TPR = 32u / L;  // tokens per round (L lanes each, L sectors per group)
@@ -632,7 +633,8 @@ __global__ void __launch_bounds__(NT, MINB) sampler_quad_pf_kernel(SamplerArgs a
     __shared__ __align__(8) unsigned long long s_bar;  // phi/L8 staging (TMA bulk copies)
     tma_stage_rows(sm, a.bhat + static_cast<size_t>(v) * a.K_pad, a.K_pad * 4u, s_l8,
                    a.l8 + static_cast<size_t>(v) * a.l8_stride, a.l8_stride * 4u, &s_bar);
-    const uint32_t tbits = a.tbits, tmask = (1u << tbits) - 1u;
+    // kC16: counts in the high half-word (tbits == 16): the count decode folds into one I2F.U16.H1.
+    const uint32_t tbits = kC16 ? 16u : a.tbits, tmask = kC16 ? 0xFFFFu : (1u << a.tbits) - 1u;
     const uint4* A4 = reinterpret_cast<const uint4*>(a.A);
     const uint32_t lane = lane_id(), t = lane / L, sub = lane % L, lead = lane & ~(L - 1u);
     const uint32_t warp = threadIdx.x >> 5;
@@ -874,10 +876,10 @@ size_t sampler_quad_smem(const SamplerArgs& a, int nt) {
     return sizeof(float) * (static_cast<size_t>(a.K_pad) + a.l8_stride + static_cast<size_t>(nt / 32) * 32u * 17u);
 }
 
-template <int NT, int MINB, int L, bool C, bool PF>
+template <int NT, int MINB, int L, bool C, bool PF, bool C16>
 cudaError_t launch_quad_t1(const SamplerArgs& a, uint32_t n_units, cudaStream_t s) {
     static bool configured = false;
-    auto kern = PF ? sampler_quad_pf_kernel<NT, MINB, L, C> : sampler_quad_kernel<NT, MINB, L, C>;
+    auto kern = PF ? sampler_quad_pf_kernel<NT, MINB, L, C, C16> : sampler_quad_kernel<NT, MINB, L, C, C16>;
     if (!configured) {
         // 227 KB per block minus the kernel's static shared memory (the batch counter).
         const cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 226 * 1024);
@@ -891,8 +893,9 @@ cudaError_t launch_quad_t1(const SamplerArgs& a, uint32_t n_units, cudaStream_t 
 // 95.5 -> 92.8 ms; short-phi C2: 19.8 -> 20.5 ms, so only the 512-thread shape uses it).
 template <int NT, int MINB, int L = 4, bool PF = (NT >= 512)>
 cudaError_t launch_quad_t(const SamplerArgs& a, uint32_t n_units, cudaStream_t s) {
-    return a.compact ? launch_quad_t1<NT, MINB, L, true, PF>(a, n_units, s)
-                     : launch_quad_t1<NT, MINB, L, false, PF>(a, n_units, s);
+    if (a.compact) return launch_quad_t1<NT, MINB, L, true, PF, false>(a, n_units, s);
+    return a.tbits == 16 ? launch_quad_t1<NT, MINB, L, false, PF, true>(a, n_units, s)
+                         : launch_quad_t1<NT, MINB, L, false, PF, false>(a, n_units, s);
 }
 
 // Launch shape (SLDA_SAMPLER overrides for experiments; default by phi row size):
