@@ -39,6 +39,10 @@ __device__ __forceinline__ Sector ldg_sector(const uint4* p) {
     return s;
 }
 
+__device__ __forceinline__ void prefetch_l2(const void* p) {
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+}
+
 __device__ __forceinline__ Sector zero_sector() { return Sector{make_uint4(0u, 0u, 0u, 0u), make_uint4(0u, 0u, 0u, 0u)}; }
 
 // Compact C_dk rows (K <= kCompactMaxK): 16-bit slots, two per 32-bit word.  Word 0 =
