@@ -235,9 +235,11 @@ __device__ __forceinline__ void tma_stage_rows(float* s_phi, const float* g_phi,
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(phi_bytes + l8_bytes)
                      : "memory");
-        asm volatile("cp.async.bulk.shared::cta.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-                     ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(s_phi))), "l"(g_phi), "r"(phi_bytes), "r"(b)
-                     : "memory");
+        if (phi_bytes)  // 0: phi is read from global memory (rows too large for shared memory)
+            asm volatile("cp.async.bulk.shared::cta.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                         ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(s_phi))), "l"(g_phi), "r"(phi_bytes),
+                         "r"(b)
+                         : "memory");
         asm volatile("cp.async.bulk.shared::cta.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
                      ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(s_l8))), "l"(g_l8), "r"(l8_bytes), "r"(b)
                      : "memory");

@@ -616,7 +616,9 @@ __global__ void __launch_bounds__(NT, MINB) sampler_quad_kernel(SamplerArgs a) {
 // The same algorithm with the next round's first line prefetched in each round's last group
 // slot and the next batch claimed a batch ahead; the per-unit scalars live in shared memory to
 // make room in the 64-register budget (C3 K=10K: 95.5 -> 92.8 ms; C2: 19.8 -> 20.5 ms).
-template <int NT, int MINB, int L, bool kCompact, bool kC16 = false, bool kPrefetchNext = true>
+// kGlobalPhi: the phi row does not fit shared memory (K >~ 45K): only L8 is staged and the
+// products gather phi through L1/L2.
+template <int NT, int MINB, int L, bool kCompact, bool kC16 = false, bool kPrefetchNext = true, bool kGlobalPhi = false>
 __global__ void __launch_bounds__(NT, MINB) sampler_quad_pf_kernel(SamplerArgs a) {
     constexpr uint32_t NW = NT / 32;
     constexpr uint32_t TPR = 32u / L;  // tokens per round (L lanes each, L sectors per group)
@@ -627,11 +629,11 @@ __global__ void __launch_bounds__(NT, MINB) sampler_quad_pf_kernel(SamplerArgs a
     __shared__ float s_total, s_qv;  // the word's tree total and Q_v (read in the sampling step only)
     const Unit unit = a.units[blockIdx.x];
     const uint32_t v = unit.word;
-    float* s_bhat = sm;
-    float* s_l8 = sm + a.K_pad;
+    const float* s_bhat = kGlobalPhi ? a.bhat + static_cast<size_t>(v) * a.K_pad : sm;
+    float* s_l8 = kGlobalPhi ? sm : sm + a.K_pad;
     float* s_ck = s_l8 + a.l8_stride;  // [NW][32 tokens][kCkStride]
     __shared__ __align__(8) unsigned long long s_bar;  // phi/L8 staging (TMA bulk copies)
-    tma_stage_rows(sm, a.bhat + static_cast<size_t>(v) * a.K_pad, a.K_pad * 4u, s_l8,
+    tma_stage_rows(sm, a.bhat + static_cast<size_t>(v) * a.K_pad, kGlobalPhi ? 0u : a.K_pad * 4u, s_l8,
                    a.l8 + static_cast<size_t>(v) * a.l8_stride, a.l8_stride * 4u, &s_bar);
     // kC16: counts in the high half-word (tbits == 16): the count decode folds into one I2F.U16.H1.
     const uint32_t tbits = kC16 ? 16u : a.tbits, tmask = kC16 ? 0xFFFFu : (1u << a.tbits) - 1u;
@@ -718,7 +720,7 @@ __global__ void __launch_bounds__(NT, MINB) sampler_quad_pf_kernel(SamplerArgs a
                         }
                     } else {
 #pragma unroll
-                        for (int w = 0; w < 8; ++w) p[w] = entry_mass<false>(es[w], tbits, tmask, s_bhat);
+                        for (int w = 0; w < 8; ++w) p[w] = entry_mass<kGlobalPhi>(es[w], tbits, tmask, s_bhat);
                     }
                 }
                 // Branch-free rounds: every lane runs the 8 FADDs (an instruction costs the same
@@ -806,7 +808,7 @@ __global__ void __launch_bounds__(NT, MINB) sampler_quad_pf_kernel(SamplerArgs a
                         } else {
 #pragma unroll
                             for (int w = 0; w < 8; ++w) {
-                                r = __fadd_rn(r, entry_mass<false>(es[w], tbits, tmask, s_bhat));
+                                r = __fadd_rn(r, entry_mass<kGlobalPhi>(es[w], tbits, tmask, s_bhat));
                                 if (!found && r >= xs) { topic = es[w] & tmask; found = true; }
                             }
                         }
@@ -902,6 +904,24 @@ cudaError_t launch_quad_t(const SamplerArgs& a, uint32_t n_units, cudaStream_t s
                          : launch_quad_t1<NT, MINB, L, false, PF, false>(a, n_units, s);
 }
 
+cudaError_t launch_quad_global(const SamplerArgs& a, uint32_t n_units, cudaStream_t s) {
+    static bool configured = false;
+    auto kern = a.tbits == 16 ? sampler_quad_pf_kernel<512, 2, 4, false, true, true, true>
+                              : sampler_quad_pf_kernel<512, 2, 4, false, false, true, true>;
+    if (!configured) {
+        const cudaError_t e = cudaFuncSetAttribute(sampler_quad_pf_kernel<512, 2, 4, false, true, true, true>,
+                                                   cudaFuncAttributeMaxDynamicSharedMemorySize, 226 * 1024);
+        if (e != cudaSuccess) return e;
+        const cudaError_t e2 = cudaFuncSetAttribute(sampler_quad_pf_kernel<512, 2, 4, false, false, true, true>,
+                                                    cudaFuncAttributeMaxDynamicSharedMemorySize, 226 * 1024);
+        if (e2 != cudaSuccess) return e2;
+        configured = true;
+    }
+    const size_t smem = sizeof(float) * (static_cast<size_t>(a.l8_stride) + 16u * 32u * 17u);
+    kern<<<n_units, 512, smem, s>>>(a);
+    return cudaGetLastError();
+}
+
 // Launch shape (SLDA_SAMPLER overrides for experiments; default by phi row size):
 //   "g2"     : round-based, 256/512-thread CTAs, 2-sector groups, 64 registers
 //   "g4"     : round-based, 256-thread CTAs, 4-sector groups, up to 128 registers
@@ -926,8 +946,11 @@ cudaError_t launch_sampler(const SamplerArgs& a, uint32_t n_units, cudaStream_t 
     const bool fits512 = sampler_smem(a, 512, 2, false) <= 227 * 1024;
     if (!fits512) {
         // Rows that do not fit shared memory (K > kCompactMaxK, so always the wide format):
-        // gather phi through L1/L2.
+        // gather phi through L1/L2 -- the quad-lane kernel with only L8 staged (C5 K=50K), or
+        // the round-based kernel when asked for (shape 0..2).
         if (a.compact) return cudaErrorInvalidConfiguration;
+        const size_t gsm = sizeof(float) * (static_cast<size_t>(a.l8_stride) + 16u * 32u * 17u);
+        if (a.shape < 0 && 2 * gsm <= 227 * 1024) return launch_quad_global(a, n_units, s);
         return launch_sampler_t<512, 2, 2, true, false>(a, n_units, s);
     }
     if (shape == 6 && sampler_quad_smem(a, 512) <= 227 * 1024)
