@@ -691,10 +691,6 @@ __global__ void __launch_bounds__(NT, MINB) sampler_quad_pf_kernel(SamplerArgs a
             const uint32_t nsect = act ? (kCompact ? hw & 0xFFFFu : (nnz + 8u) >> 3) : 0u;
             if (sub == 0) entries += nnz;
             const uint32_t max_groups = __reduce_max_sync(0xffffffffu, (nsect + L - 1u) / L);
-            // The row's later lines are pulled into L2 now (no registers held): the group loads
-            // below then wait on L2, not HBM.
-            for (uint32_t g = 2; g < max_groups; ++g)
-                if (L * g + sub < nsect) prefetch_l2(row + 2 * (L * g + sub));
             float* ck = ckw + ti * kCkStride;
             float run = 0.0f;
             // Products of this lane's sector, then the chain over the line's 4 sectors in order.
