@@ -270,6 +270,15 @@ def main() -> None:
     warm = core.init_view(w_tok, 64, 64, 0, 64, 0, tc)
     warm.run_iteration(tc)
     del warm
+    # Process warm-up of device memory: the engine's footprint (setup scratch included, ~110
+    # B/token) is mapped and released once, so the e2e leg does not pay the driver's first-touch
+    # of pages another process (pytest, smoke) just freed.  Capped by the free memory.
+    free_b, _ = torch.cuda.mem_get_info()
+    warm_b = min(int(T_shard * 112 + (8 << 30)), int(free_b * 0.9))
+    if warm_b > 0:
+        blob = torch.empty(warm_b, dtype=torch.uint8, device="cuda")
+        del blob
+        torch.cuda.empty_cache()
 
     def barrier():
         torch.cuda.synchronize()
