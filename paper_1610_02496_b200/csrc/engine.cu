@@ -360,7 +360,7 @@ struct slda_engine {
         l8.alloc(static_cast<size_t>(V_pad) * l8_stride * 4, &device_bytes);
         q.alloc(static_cast<size_t>(V_pad) * 4, &device_bytes);
         colsum.alloc(static_cast<size_t>(K_pad) * 8, &device_bytes);
-        denom.alloc(static_cast<size_t>(K_pad) * 8, &device_bytes);
+        denom.alloc(static_cast<size_t>(K_pad) * 16, &device_bytes);
         zv.alloc(static_cast<size_t>(K_pad) * 4, &device_bytes);
         counters.alloc(8 * (1 + kRing), &device_bytes);
         CK(cudaMemsetAsync(bhat.p, 0, bhat.bytes, stream));

@@ -61,6 +61,7 @@ cudaError_t launch_ssc(const SscArgs& a, cudaStream_t s);
 
 cudaError_t launch_colsum(const uint32_t* B, uint32_t row_begin, uint32_t row_end, uint32_t K_pad,
                           unsigned long long* colsum, cudaStream_t s);
+// denom: 2*K_pad doubles -- denom_k, then RN(1/denom_k) (read by the phi kernel).
 cudaError_t launch_denom(const unsigned long long* colsum, uint32_t K, uint32_t K_pad, uint32_t V,
                          double beta, double* denom, float* zv, cudaStream_t s);
 // Peer-memory exchange (engine.cu m_step_peer): up to kMaxPeers ranks.

@@ -9,7 +9,7 @@ namespace slda {
 // ============================================================================
 // K5/K6 -- preprocess (counts.cpp:37-63) + rebuild_trees (trainer.cpp:237-248,
 // sampler.hpp:58-90, :142-149).  colsum: integer column sums (order-free).
-// phi: thread per word row, 32-column tiles transposed through shared memory
+// phi: thread per word row, 16-column tiles staged in shared memory by cp.async
 // so global traffic is coalesced while each thread runs the row's sequential
 // f32 prefix (the L4 level) exactly as WaryTree::build.
 // ============================================================================
@@ -58,6 +58,29 @@ cudaError_t launch_colsum(const uint32_t* B, uint32_t row_begin, uint32_t row_en
     return cudaGetLastError();
 }
 
+// bhat = f32((cnt + beta) / denom_k) with the double quotient correctly rounded
+// (counts.cpp:58-60), without a per-cell double division.  y = RN(x * RN(1/denom)) is within
+// 2.5 double ulps of RN(x / denom), so both round to the same f32 unless an f32 rounding
+// boundary (a midpoint between adjacent floats: low 29 mantissa bits == 2^28) lies within a
+// few ulps of y, or y leaves the f32 normal range; those cells (~2^-22 of them) take the
+// exact division.  rcp is NaN when RN(1/denom) is not a normal double, forcing the exact path.
+__device__ __forceinline__ float phi_quotient(double x, double den, double rcp) {
+    const double y = __dmul_rn(x, rcp);
+    const unsigned long long b = static_cast<unsigned long long>(__double_as_longlong(y));
+    const uint32_t lo = static_cast<uint32_t>(b) & 0x1FFFFFFFu;
+    const uint32_t ex = static_cast<uint32_t>(b >> 52) & 0x7FFu;
+    const bool near_mid = lo - (0x10000000u - 64u) <= 128u;
+    const bool out_of_range = ex - 898u > 1149u - 898u;  // y in [2^-125, 2^127): f32 normal
+    if (__builtin_expect(near_mid || out_of_range, 0)) return __double2float_rn(__ddiv_rn(x, den));
+    return __double2float_rn(y);
+}
+
+__device__ __forceinline__ double phi_reciprocal(double den) {
+    const double r = __ddiv_rn(1.0, den);
+    const uint32_t ex = static_cast<uint32_t>(static_cast<unsigned long long>(__double_as_longlong(r)) >> 52) & 0x7FFu;
+    return ex == 0u || ex == 0x7FFu ? __longlong_as_double(0x7FF8000000000000ll) : r;
+}
+
 // denom_k = f64(colsum_k) + V*beta (counts.cpp:49-50); zero-count cells share
 // bhat = f32(beta / denom_k), so the phi kernel divides only non-zero cells.
 __global__ void denom_kernel(const unsigned long long* colsum, uint32_t K, uint32_t K_pad, uint32_t V,
@@ -68,9 +91,11 @@ __global__ void denom_kernel(const unsigned long long* colsum, uint32_t K, uint3
         const double d = __dadd_rn(static_cast<double>(colsum[k]),
                                    __dmul_rn(static_cast<double>(V), beta));
         denom[k] = d;
+        denom[K_pad + k] = phi_reciprocal(d);
         zv[k] = __double2float_rn(__ddiv_rn(__dadd_rn(0.0, beta), d));
     } else {
         denom[k] = 1.0;
+        denom[K_pad + k] = 1.0;
         zv[k] = 0.0f;
     }
 }
@@ -81,101 +106,132 @@ cudaError_t launch_denom(const unsigned long long* colsum, uint32_t K, uint32_t 
     return cudaGetLastError();
 }
 
-// One thread per word row (the L4 prefix is a sequential f32 chain); 32-column tiles are
-// moved through shared memory for coalescing, and tile c+1 is loaded into registers while
-// tile c is computed.
-constexpr int kPhiRows = 128;
-constexpr int kPhiCols = 32;
-constexpr int kPhiLoads = kPhiRows * kPhiCols / kPhiRows;  // per thread per tile
+// One thread per word row (the L4 prefix is a sequential f32 chain), 64 rows per CTA and
+// 16-column tiles.  A tile of C_wk lands in shared memory by cp.async (4 threads per row
+// segment, coalesced), double-buffered so tile t+1 is in flight while tile t is computed; each
+// thread then reads its own row, writes bhat in place and the L4 prefix beside it, and the CTA
+// stores both tiles back with the copy mapping.  kPhiStages tiles (with their columns' denom,
+// 1/denom and zero-count bhat) are in flight per CTA.  16-byte quads are XOR-swizzled by row so the
+// per-row and the per-segment accesses are both bank-conflict free.  The small footprint
+// (39 KB) keeps 5 CTAs = 320 rows resident per SM with 7 tiles (28 KB per CTA) in flight.  Padded columns (>= K) hold zero counts and zv = 0, so they add +0.0f to the
+// chain (unchanged) and store bhat = 0, as the reference's padding.
+constexpr int kPhiRows = 64;
+constexpr int kPhiCols = 16;
+
+__device__ __forceinline__ uint32_t phi_swz(uint32_t row, uint32_t quad) {
+    return row * kPhiCols + ((quad ^ ((row >> 1) & 3u)) << 2);
+}
+
+__device__ __forceinline__ void phi_cp16(void* smem, const void* gmem, bool valid) {
+    const uint32_t s = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(valid ? 16 : 0)
+                 : "memory");
+}
+
+constexpr int kPhiStages = 8;  // measured: 2 / 4 / 8 / 12 / 16 stages -> 6.4 / 5.3 / 4.9 / 5.5 / 6.4 ms (C3)
+constexpr size_t kPhiSmem =
+    static_cast<size_t>(kPhiStages) * (2 * kPhiCols * 8 + kPhiRows * kPhiCols * 4 + kPhiCols * 4) +
+    kPhiRows * kPhiCols * 4;
 
 template <bool kMirror>
 __global__ void __launch_bounds__(kPhiRows, 4) phi_kernel(const uint32_t* __restrict__ B,
-                                                        const double* __restrict__ denom,
-                                                        const float* __restrict__ zv,
-                                                        float* __restrict__ bhat, float* __restrict__ l4,
-                                                        float* __restrict__ l8, float* __restrict__ q,
-                                                        uint32_t row_begin, uint32_t row_end, uint32_t K,
-                                                        uint32_t K_pad, uint32_t l8_stride, double beta,
-                                                        float falpha, PeerMirror mirror) {
-    // t_bh aliases t_in: thread r overwrites cell [r][c] only after reading it.
-    __shared__ uint32_t t_in[kPhiRows][kPhiCols + 1];
-    __shared__ float t_l4[kPhiRows][kPhiCols + 1];
-    __shared__ double s_den[kPhiCols];
-    __shared__ float s_zv[kPhiCols];
-    float(*t_bh)[kPhiCols + 1] = reinterpret_cast<float(*)[kPhiCols + 1]>(t_in);
-    const uint32_t r = threadIdx.x;
+                                                         const double* __restrict__ denom,
+                                                         const float* __restrict__ zv,
+                                                         float* __restrict__ bhat, float* __restrict__ l4,
+                                                         float* __restrict__ l8, float* __restrict__ q,
+                                                         uint32_t row_begin, uint32_t row_end,
+                                                         uint32_t K_pad, uint32_t l8_stride, double beta,
+                                                         float falpha, PeerMirror mirror) {
+    extern __shared__ __align__(16) unsigned char phi_smem[];
+    // [stage][2][kPhiCols] denom, 1/denom | [stage][rows*cols] counts, then bhat | L4 | [stage] zv
+    auto s_den = reinterpret_cast<double(*)[2][kPhiCols]>(phi_smem);
+    auto t_in = reinterpret_cast<uint32_t(*)[kPhiRows * kPhiCols]>(phi_smem + kPhiStages * 2 * kPhiCols * 8);
+    float* t_l4 = reinterpret_cast<float*>(phi_smem + kPhiStages * (2 * kPhiCols * 8 + kPhiRows * kPhiCols * 4));
+    auto s_zv = reinterpret_cast<float(*)[kPhiCols]>(t_l4 + kPhiRows * kPhiCols);
+    const double* __restrict__ rcp = denom + K_pad;
+    const uint32_t tid = threadIdx.x;
     const uint32_t v0 = row_begin + blockIdx.x * kPhiRows;
-    const uint32_t v = v0 + r;
-    float run = 0.0f;
-    uint32_t next[kPhiLoads];
-    auto load_tile = [&](uint32_t c0) {
+    const uint32_t v = v0 + tid;
+    // Copy / store role: quad cq of rows crow + 16p, p = 0..3.
+    const uint32_t cq = tid & 3u, crow = tid >> 2;
+    const size_t stride16 = static_cast<size_t>(16) * K_pad;
+    const size_t g0 = static_cast<size_t>(v0 + crow) * K_pad + cq * 4u;
+    const uint32_t ntiles = K_pad / kPhiCols;
+    auto issue = [&](uint32_t c0, int st) {
 #pragma unroll
-        for (int it = 0; it < kPhiLoads; ++it) {
-            const uint32_t idx = it * kPhiRows + r;
-            const uint32_t rr = idx / kPhiCols, cc = idx % kPhiCols;
-            const uint32_t vv = v0 + rr;
-            next[it] = vv < row_end ? __ldg(B + static_cast<size_t>(vv) * K_pad + c0 + cc) : 0u;
+        for (uint32_t p = 0; p < 4; ++p) {
+            const bool ok = v0 + crow + 16u * p < row_end;
+            phi_cp16(&t_in[st][phi_swz(crow + 16u * p, cq)], ok ? B + g0 + p * stride16 + c0 : B, ok);
         }
+        if (tid < 8) phi_cp16(&s_den[st][0][tid * 2], denom + c0 + tid * 2, true);
+        else if (tid < 16) phi_cp16(&s_den[st][1][(tid - 8) * 2], rcp + c0 + (tid - 8) * 2, true);
+        else if (tid < 20) phi_cp16(&s_zv[st][(tid - 16) * 4], zv + c0 + (tid - 16) * 4, true);
     };
-    load_tile(0);
-    for (uint32_t c0 = 0; c0 < K_pad; c0 += kPhiCols) {
+    float run = 0.0f;
 #pragma unroll
-        for (int it = 0; it < kPhiLoads; ++it) {
-            const uint32_t idx = it * kPhiRows + r;
-            t_in[idx / kPhiCols][idx % kPhiCols] = next[it];
-        }
-        if (r < kPhiCols) {  // this tile's column constants, off the dependent chain
-            s_den[r] = __ldg(denom + c0 + r);
-            s_zv[r] = __ldg(zv + c0 + r);
-        }
-        __syncthreads();
-        if (c0 + kPhiCols < K_pad) load_tile(c0 + kPhiCols);
-        // Eight independent divisions are issued before the sequential f32 prefix consumes them.
+    for (uint32_t t = 0; t + 1 < kPhiStages; ++t) {
+        if (t < ntiles) issue(t * kPhiCols, t);
+        asm volatile("cp.async.commit_group;\n" ::: "memory");
+    }
+    for (uint32_t t = 0; t < ntiles; ++t) {
+        const int st = t % kPhiStages;
+        const uint32_t c0 = t * kPhiCols;
+        asm volatile("cp.async.wait_group %0;\n" ::"n"(kPhiStages - 2) : "memory");
+        __syncthreads();  // tile t visible; tile t-1's stores have read its stage and t_l4
+        if (t + kPhiStages - 1 < ntiles) issue(c0 + (kPhiStages - 1) * kPhiCols, (t + kPhiStages - 1) % kPhiStages);
+        asm volatile("cp.async.commit_group;\n" ::: "memory");
+        float l8v[2];
 #pragma unroll
-        for (uint32_t c8 = 0; c8 < kPhiCols; c8 += 8) {
-            float bh[8];
-#pragma unroll
-            for (uint32_t u = 0; u < 8; ++u) {
-                const uint32_t c = c8 + u;
-                const uint32_t cnt = t_in[r][c];
-                bh[u] = c0 + c >= K ? 0.0f
-                        : cnt ? __double2float_rn(__ddiv_rn(__dadd_rn(static_cast<double>(cnt), beta), s_den[c]))
-                              : s_zv[c];
+        for (uint32_t j = 0; j < 4; ++j) {
+            const uint32_t o = phi_swz(tid, j);
+            const uint4 cnt = *reinterpret_cast<const uint4*>(&t_in[st][o]);
+            float4 bh = *reinterpret_cast<const float4*>(&s_zv[st][j * 4]);
+            if ((cnt.x | cnt.y | cnt.z | cnt.w) != 0u) {
+                const double* d = &s_den[st][0][j * 4];
+                const double* r = &s_den[st][1][j * 4];
+                if (cnt.x) bh.x = phi_quotient(__dadd_rn(static_cast<double>(cnt.x), beta), d[0], r[0]);
+                if (cnt.y) bh.y = phi_quotient(__dadd_rn(static_cast<double>(cnt.y), beta), d[1], r[1]);
+                if (cnt.z) bh.z = phi_quotient(__dadd_rn(static_cast<double>(cnt.z), beta), d[2], r[2]);
+                if (cnt.w) bh.w = phi_quotient(__dadd_rn(static_cast<double>(cnt.w), beta), d[3], r[3]);
             }
-#pragma unroll
-            for (uint32_t u = 0; u < 8; ++u) {
-                const uint32_t c = c8 + u;
-                if (c0 + c < K) run = __fadd_rn(run, bh[u]);
-                t_bh[r][c] = bh[u];
-                t_l4[r][c] = run;
-            }
+            float4 lv;
+            run = __fadd_rn(run, bh.x);
+            lv.x = run;
+            run = __fadd_rn(run, bh.y);
+            lv.y = run;
+            run = __fadd_rn(run, bh.z);
+            lv.z = run;
+            run = __fadd_rn(run, bh.w);
+            lv.w = run;
+            *reinterpret_cast<float4*>(&t_in[st][o]) = bh;
+            *reinterpret_cast<float4*>(&t_l4[o]) = lv;
+            if (j & 1u) l8v[j >> 1] = lv.w;  // L8: the prefix at every 8th column
         }
-        if (v < row_end) {  // L8: the prefix at every 8th column of this tile
-            const float4 l8v = make_float4(t_l4[r][7], t_l4[r][15], t_l4[r][23], t_l4[r][31]);
-            *reinterpret_cast<float4*>(l8 + static_cast<size_t>(v) * l8_stride + c0 / kLeaf) = l8v;
+        if (v < row_end) {
+            const size_t o8 = static_cast<size_t>(v) * l8_stride + c0 / kLeaf;
+            *reinterpret_cast<float2*>(l8 + o8) = make_float2(l8v[0], l8v[1]);
             if (kMirror)
                 for (uint32_t p = 0; p < mirror.n; ++p)
-                    *reinterpret_cast<float4*>(mirror.l8[p] + static_cast<size_t>(v) * l8_stride + c0 / kLeaf) = l8v;
+                    *reinterpret_cast<float2*>(mirror.l8[p] + o8) = make_float2(l8v[0], l8v[1]);
         }
         __syncthreads();
 #pragma unroll
-        for (int it = 0; it < kPhiLoads; ++it) {
-            const uint32_t idx = it * kPhiRows + r;
-            const uint32_t rr = idx / kPhiCols, cc = idx % kPhiCols;
-            const uint32_t vv = v0 + rr;
-            if (vv < row_end) {
-                const size_t o = static_cast<size_t>(vv) * K_pad + c0 + cc;
-                bhat[o] = t_bh[rr][cc];
-                l4[o] = t_l4[rr][cc];
+        for (uint32_t p = 0; p < 4; ++p) {
+            if (v0 + crow + 16u * p < row_end) {
+                const uint32_t o = phi_swz(crow + 16u * p, cq);
+                const float4 b = *reinterpret_cast<const float4*>(&t_in[st][o]);
+                const float4 l = *reinterpret_cast<const float4*>(&t_l4[o]);
+                const size_t go = g0 + p * stride16 + c0;
+                *reinterpret_cast<float4*>(bhat + go) = b;
+                *reinterpret_cast<float4*>(l4 + go) = l;
                 if (kMirror) {  // the all-gather, fused: the same values into every peer's replica
-                    for (uint32_t p = 0; p < mirror.n; ++p) {
-                        mirror.bhat[p][o] = t_bh[rr][cc];
-                        mirror.l4[p][o] = t_l4[rr][cc];
+                    for (uint32_t m = 0; m < mirror.n; ++m) {
+                        *reinterpret_cast<float4*>(mirror.bhat[m] + go) = b;
+                        *reinterpret_cast<float4*>(mirror.l4[m] + go) = l;
                     }
                 }
             }
         }
-        __syncthreads();  // the next tile store overwrites t_in (== t_bh)
     }
     if (v < row_end) {
         for (uint32_t j = K_pad / kLeaf; j < l8_stride; ++j) l8[static_cast<size_t>(v) * l8_stride + j] = run;
@@ -194,14 +250,22 @@ cudaError_t launch_phi(const uint32_t* B, const double* denom, const float* zv, 
                        float* l4, float* l8, float* q, uint32_t row_begin, uint32_t row_end,
                        uint32_t K, uint32_t K_pad, uint32_t l8_stride, double beta, float falpha,
                        cudaStream_t s, const PeerMirror* mirror) {
+    (void)K;  // columns >= K are zero counts with zv = 0 (see above)
     if (row_end <= row_begin) return cudaSuccess;
+    if (K_pad % kPhiCols) return cudaErrorInvalidValue;
     const uint32_t blocks = (row_end - row_begin + kPhiRows - 1) / kPhiRows;
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(phi_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kPhiSmem));
+        cudaFuncSetAttribute(phi_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kPhiSmem));
+        attr = true;
+    }
     if (mirror && mirror->n > 0)
-        phi_kernel<true><<<blocks, kPhiRows, 0, s>>>(B, denom, zv, bhat, l4, l8, q, row_begin, row_end, K, K_pad,
-                                                     l8_stride, beta, falpha, *mirror);
+        phi_kernel<true><<<blocks, kPhiRows, kPhiSmem, s>>>(B, denom, zv, bhat, l4, l8, q, row_begin, row_end, K_pad,
+                                                            l8_stride, beta, falpha, *mirror);
     else
-        phi_kernel<false><<<blocks, kPhiRows, 0, s>>>(B, denom, zv, bhat, l4, l8, q, row_begin, row_end, K,
-                                                      K_pad, l8_stride, beta, falpha, PeerMirror{});
+        phi_kernel<false><<<blocks, kPhiRows, kPhiSmem, s>>>(B, denom, zv, bhat, l4, l8, q, row_begin, row_end,
+                                                             K_pad, l8_stride, beta, falpha, PeerMirror{});
     return cudaGetLastError();
 }
 
