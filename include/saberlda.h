@@ -26,7 +26,7 @@
 extern "C" {
 #endif
 
-#define SLDA_ABI_VERSION 1u
+#define SLDA_ABI_VERSION 2u
 
 enum {
     SLDA_OK = 0,
@@ -76,7 +76,12 @@ typedef struct slda_config {
     uint32_t world_size;      /* number of shards/GPUs (1 = no collectives) */
     const void* nccl_id;      /* 128-byte ncclUniqueId from rank 0 when world_size > 1 (NCCL
                                  collectives); NULL: peer-memory exchange (slda_peer_attach) */
+    uint32_t sampler;         /* SLDA_SAMPLER_* -- TrainConfig::sampler (trainer.hpp:18, :30) */
 } slda_config;
+
+/* sparselda::SamplerKind (trainer.hpp:18). */
+#define SLDA_SAMPLER_SPARSE 0u   /* ESCA sparsity-aware sampler (sampler.hpp:183-204) */
+#define SLDA_SAMPLER_VANILLA 1u  /* O(K) dense-row baseline (sampler.hpp:222-236) */
 
 /* sparselda::IterationStats (trainer.hpp:38-44) + device timings. */
 typedef struct slda_iteration_stats {

@@ -64,9 +64,11 @@ void ref_uniform2(uint64_t seed, uint32_t kind, uint64_t element, double* u0, do
     *u1 = s.next_double();
 }
 
-// workers: 0 = hardware concurrency; chunks: 0 = auto (budget 2^40 -> 1).
-void* ref_init(uint32_t D, uint32_t V, uint64_t T, const uint32_t* tokens, uint32_t K,
-               double alpha, double beta, uint64_t seed, uint32_t num_chunks, uint32_t workers) {
+// workers: 0 = hardware concurrency; chunks: 0 = auto (budget 2^40 -> 1);
+// sampler: 0 SamplerKind::kSparse, 1 SamplerKind::kVanilla (trainer.hpp:18).
+void* ref_init_sampler(uint32_t D, uint32_t V, uint64_t T, const uint32_t* tokens, uint32_t K,
+                       double alpha, double beta, uint64_t seed, uint32_t num_chunks, uint32_t workers,
+                       uint32_t sampler) {
     try {
         auto* m = new RefModel;
         m->corpus = make_corpus(D, V, T, tokens);
@@ -78,6 +80,7 @@ void* ref_init(uint32_t D, uint32_t V, uint64_t T, const uint32_t* tokens, uint3
         m->cfg.num_workers = workers;
         m->cfg.memory_budget = 1ull << 40;  // never spill
         m->cfg.tree_branch = K > 32768 ? 41 : 32;
+        m->cfg.sampler = sampler ? SamplerKind::kVanilla : SamplerKind::kSparse;
         m->cfg = m->cfg.resolved(m->corpus);
         m->state = init_state(m->corpus, m->cfg);
         return m;
@@ -85,6 +88,11 @@ void* ref_init(uint32_t D, uint32_t V, uint64_t T, const uint32_t* tokens, uint3
         g_error = e.what();
         return nullptr;
     }
+}
+
+void* ref_init(uint32_t D, uint32_t V, uint64_t T, const uint32_t* tokens, uint32_t K,
+               double alpha, double beta, uint64_t seed, uint32_t num_chunks, uint32_t workers) {
+    return ref_init_sampler(D, V, T, tokens, K, alpha, beta, seed, num_chunks, workers, 0);
 }
 
 void ref_free(void* h) { delete static_cast<RefModel*>(h); }
@@ -146,7 +154,10 @@ void ref_get_assignments(void* h, uint32_t* out) {
 uint64_t ref_doc_topic_nnz(void* h) {
     auto& s = static_cast<RefModel*>(h)->state;
     uint64_t nnz = 0;
-    for (size_t c = 0; c < s.chunks.size(); ++c) nnz += s.chunks.acquire(c).doc_topic.nnz();
+    for (size_t c = 0; c < s.chunks.size(); ++c) {
+        const ChunkSlot& slot = s.chunks.acquire(c);
+        nnz += slot.doc_topic_dense.empty() ? slot.doc_topic.nnz() : slot.doc_topic_dense.nnz();
+    }
     return nnz;
 }
 
@@ -157,6 +168,19 @@ void ref_get_doc_topic(void* h, uint64_t* row_offsets, uint32_t* topics, uint32_
     row_offsets[0] = 0;
     for (size_t c = 0; c < s.chunks.size(); ++c) {
         const ChunkSlot& slot = s.chunks.acquire(c);
+        if (!slot.doc_topic_dense.empty()) {  // vanilla mode: the dense rows' nonzero cells
+            for (uint32_t d = 0; d < slot.doc_topic_dense.num_rows(); ++d) {
+                const auto r = slot.doc_topic_dense.row(d);
+                for (uint32_t k = 0; k < r.size(); ++k) {
+                    if (!r[k]) continue;
+                    topics[pos] = k;
+                    counts[pos] = r[k];
+                    ++pos;
+                }
+                row_offsets[++row] = pos;
+            }
+            continue;
+        }
         for (uint32_t d = 0; d < slot.doc_topic.num_rows(); ++d) {
             const auto r = slot.doc_topic.row(d);
             for (size_t i = 0; i < r.size(); ++i) {

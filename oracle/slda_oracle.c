@@ -251,6 +251,25 @@ uint32_t orc_sample_token(uint32_t nnz, const uint32_t* topics, const uint32_t* 
     return result;
 }
 
+/* sampler.hpp:222-236 -- vanilla_sample<float> over the dense count row (the O(K) baseline
+ * mode, trainer.cpp:281-285).  The dense row is the document's CSR row densified on the fly:
+ * DenseDocTopic cell k == count of topic k (trainer.cpp:49-63). */
+uint32_t orc_vanilla_token(uint32_t nnz, const uint32_t* topics, const uint32_t* counts,
+                           const float* bhat_row, uint32_t K, float alpha, double u0) {
+    float* scratch = (float*)malloc(sizeof(float) * (K ? K : 1));
+    float running = 0.0f;
+    uint32_t p = 0;
+    for (uint32_t k = 0; k < K; ++k) {
+        const uint32_t c = (p < nnz && topics[p] == k) ? counts[p++] : 0u;
+        running += ((float)c + alpha) * bhat_row[k];
+        scratch[k] = running;
+    }
+    const float draw = (float)u0 * running;
+    const int64_t pick = orc_prefix_search_f(scratch, K, draw);
+    free(scratch);
+    return pick < 0 ? ORC_INVALID_TOPIC : (uint32_t)pick;
+}
+
 /* ------------------------------------------------------------------ model -- */
 
 struct orc_model {
@@ -259,6 +278,7 @@ struct orc_model {
     double alpha, beta;
     uint64_t seed;
     uint32_t iteration;
+    uint32_t vanilla; /* SamplerKind::kVanilla (trainer.hpp:18) */
     /* PDOW, single chunk (corpus.cpp:125-198) */
     uint32_t *s_doc, *s_word, *s_topic;
     uint64_t* tok_id;
@@ -414,9 +434,12 @@ int orc_iterate(orc_model* m) {
         const uint64_t b = m->a_off[d], e = m->a_off[d + 1];
         double u0, u1;
         orc_uniform2(m->seed, stream, m->tok_id[i], &u0, &u1);
-        const uint32_t next = orc_sample_token((uint32_t)(e - b), m->a_top + b, m->a_cnt + b,
-                                               m->bhat + (size_t)v * m->K, m->q[v],
-                                               m->l4 + (size_t)v * m->K, m->K, u0, u1);
+        const uint32_t next =
+            m->vanilla ? orc_vanilla_token((uint32_t)(e - b), m->a_top + b, m->a_cnt + b,
+                                           m->bhat + (size_t)v * m->K, m->K, (float)m->alpha, u0)
+                       : orc_sample_token((uint32_t)(e - b), m->a_top + b, m->a_cnt + b,
+                                          m->bhat + (size_t)v * m->K, m->q[v],
+                                          m->l4 + (size_t)v * m->K, m->K, u0, u1);
         if (next == ORC_INVALID_TOPIC) return -1;
         m->s_topic[i] = next;
     }
@@ -428,6 +451,7 @@ int orc_iterate(orc_model* m) {
 }
 
 uint32_t orc_iteration(const orc_model* m) { return m->iteration; }
+void orc_set_sampler(orc_model* m, uint32_t vanilla) { m->vanilla = vanilla ? 1u : 0u; }
 double orc_alpha(const orc_model* m) { return m->alpha; }
 void orc_get_word_topic(const orc_model* m, uint32_t* out) { memcpy(out, m->B, 4 * (size_t)m->V * m->K); }
 void orc_get_word_topic_prob(const orc_model* m, float* out) { memcpy(out, m->bhat, 4 * (size_t)m->V * m->K); }

@@ -82,6 +82,12 @@ typedef struct orc_model orc_model;
 /* init_state (trainer.cpp:354-417) over a doc-sorted or arbitrary corpus given as
  * AoS triples (doc, word, topic) exactly like sparselda::Token.  alpha<=0 -> 50/K.
  * num_chunks = 1 always: results do not depend on it (acceptance.cpp:426-445). */
+/* sampler.hpp:222-236: vanilla_sample<float> over the (densified) count row. */
+uint32_t orc_vanilla_token(uint32_t nnz, const uint32_t* topics, const uint32_t* counts,
+                           const float* bhat_row, uint32_t K, float alpha, double u0);
+/* TrainConfig::sampler (trainer.hpp:18, :30): 0 sparse (default), 1 vanilla. */
+void orc_set_sampler(orc_model* m, uint32_t vanilla);
+
 orc_model* orc_init(uint32_t D, uint32_t V, uint64_t T, const uint32_t* tokens, uint32_t K,
                     double alpha, double beta, uint64_t seed, char* err, size_t err_len);
 void orc_free(orc_model* m);

@@ -200,6 +200,7 @@ struct slda_engine {
     uint32_t rank = 0, world = 1;
     uint32_t nseg = 0, n_units = 0, n_long = 0;
     bool doc_major = true;
+    bool vanilla = false;  // SamplerKind::kVanilla (trainer.cpp:281-285)
     bool compact = false;  // C_dk row format (row_format.cuh: compact 16-bit slots or wide 32-bit)
     int sampler_shape = -1;  // SLDA_SAMPLER (sampler.cu launch_sampler); -1 = default by K
     bool ssc_sort = false;   // SLDA_SSC=sort: the bitonic-sort SSC instead of the bitmap one
@@ -309,6 +310,8 @@ struct slda_engine {
         if (K > cap)
             validation("K=" + std::to_string(K) + " exceeds tree capacity W^3=" + std::to_string(cap));
         if (K > 65536) validation("device engine supports K <= 65536 (16-bit topics)");
+        if (c.sampler > SLDA_SAMPLER_VANILLA) validation("unknown sampler kind");
+        vanilla = c.sampler == SLDA_SAMPLER_VANILLA;
         if (vocab == 0) validation("preprocess requires V >= 1");
         world = c.world_size ? c.world_size : 1;
         rank = c.rank;
@@ -480,7 +483,7 @@ void slda_engine::build(const slda_corpus_view& cv, const slda_config& c) {
     if (const char* f = std::getenv("SLDA_SSC")) ssc_sort = std::string(f) == "sort";
     if (const char* f = std::getenv("SLDA_SERIAL")) serial = std::string(f) == "1";
     compact = false;
-    if (const char* f = std::getenv("SLDA_ROW_FORMAT")) {
+    if (const char* f = std::getenv("SLDA_ROW_FORMAT"); f && !vanilla) {
         if (std::string(f) == "compact")
             compact = K <= slda::kCompactMaxK && max_len <= slda::kCompactMaxLen;
     }
@@ -798,6 +801,8 @@ void slda_engine::enqueue_iteration() {
     a.compact = compact ? 1u : 0u;
     a.row_entries = entries_counter();
     a.shape = sampler_shape;
+    a.vanilla = vanilla ? 1u : 0u;
+    a.alpha = falpha;  // static_cast<float>(state.alpha), trainer.cpp:283
     CK(slda::launch_sampler(a, n_units, stream));
     launches += n_units > 0;
     CK(cudaEventRecord(ev[2], stream));

@@ -35,6 +35,8 @@ struct SamplerArgs {
     uint32_t compact;       // C_dk rows in the compact 16-bit format
     unsigned long long* row_entries;  // optional: sum of nnz over tokens (roofline)
     int shape;              // launch shape (sampler_shape_from_name); -1 = default by K
+    uint32_t vanilla;       // SamplerKind::kVanilla: the O(K) dense-row draw (sampler.hpp:222-236)
+    float alpha;            // f32(alpha), the vanilla draw's smoothing (trainer.cpp:283)
 };
 
 // "g2" 0, "g4" 1, "g4x512" 2, "s4" 3, "s2" 4, "s4x128" 5, "q512" 6, "q256" 7; else -1 (default).

@@ -927,8 +927,98 @@ cudaError_t launch_quad_global(const SamplerArgs& a, uint32_t n_units, cudaStrea
 //   "p512", "p256"       : pair-lane (L=2; C2 20.7 vs 21.5 ms, C3 107.9 vs 100.0 ms)
 //   "o512"               : octet-lane (L=8; slower at both)
 //   "q512r", "q256r"     : quad-lane with a relaxed register bound (fewer warps; slower)
+// ---- SamplerKind::kVanilla: the reference's O(K) baseline mode ---------------------------------
+// vanilla_sample<float> over the dense count row (sampler.hpp:222-236, trainer.cpp:281-285): the
+// sequential f32 prefix running_k = running_{k-1} + (f32(n_dk) + alpha) * bhat_k over all K topics,
+// the draw f32(u0) * running_K, and prefix_search (first prefix >= draw).  The dense row is the
+// document's C_dk row densified on the fly (DenseDocTopic cell k == count of topic k,
+// trainer.cpp:49-63).  Lane per token, CTA per work unit (one word: its phi row staged in
+// shared memory when it fits); the search re-runs the same chain and stops at the first prefix
+// >= the draw, which equals the binary lower_bound on a non-decreasing prefix.  A baseline mode
+// (O(K) per token, as in the reference), not a tuned path.
+template <int NT, bool kGlobalPhi>
+__global__ void __launch_bounds__(NT) sampler_vanilla_kernel(SamplerArgs a) {
+    extern __shared__ __align__(16) float s_phi[];
+    const Unit unit = a.units[blockIdx.x];
+    const uint32_t v = unit.word;
+    const float* gphi = a.bhat + static_cast<size_t>(v) * a.K_pad;
+    if (!kGlobalPhi) {
+        for (uint32_t i = threadIdx.x; i < a.K_pad / 4; i += NT)
+            reinterpret_cast<float4*>(s_phi)[i] = __ldg(reinterpret_cast<const float4*>(gphi) + i);
+        __syncthreads();
+    }
+    const float* phi = kGlobalPhi ? gphi : s_phi;
+    uint32_t* brow = a.B + static_cast<size_t>(v) * a.K_pad;
+    const uint32_t tbits = a.tbits, tmask = (1u << tbits) - 1u;
+    const float alpha = a.alpha;
+    unsigned long long entries = 0;
+    for (uint32_t i = threadIdx.x; i < unit.length; i += NT) {
+        const uint2 t = __ldg(a.tok + unit.offset + i);
+        const uint32_t* row = a.A + static_cast<size_t>(t.x) * 4u;  // [nnz-1 | entries ...]
+        const uint32_t nnz = (__ldg(row) & tmask) + 1u;
+        entries += nnz;
+        // The chain: running over k = 0..K-1, the row's entries consumed in ascending topic order.
+        auto chain_step = [&](float run, uint32_t k, uint32_t& p, uint32_t& e) {
+            uint32_t c = 0;
+            if (p <= nnz && (e & tmask) == k) {
+                c = e >> tbits;
+                ++p;
+                e = p <= nnz ? __ldg(row + p) : 0u;
+            }
+            const float w = __fadd_rn(__uint2float_rn(c), alpha);
+            return __fadd_rn(run, __fmul_rn(w, kGlobalPhi ? __ldg(phi + k) : phi[k]));
+        };
+        float total = 0.0f;
+        {
+            uint32_t p = 1, e = __ldg(row + 1);
+            for (uint32_t k = 0; k < a.K; ++k) total = chain_step(total, k, p, e);
+        }
+        float u0 = 0.0f, u1 = 0.0f;
+        const uint64_t id = a.ids ? __ldg(a.ids + t.y) : a.id_base + t.y;
+        draw2_f32(a.seed, a.stream_kind, id, u0, u1);
+        const float x = __fmul_rn(u0, total);
+        uint32_t topic = a.K - 1;  // x > total cannot happen (u0 <= 1); kept as the clamp
+        {
+            uint32_t p = 1, e = __ldg(row + 1);
+            float run = 0.0f;
+            for (uint32_t k = 0; k < a.K; ++k) {
+                run = chain_step(run, k, p, e);
+                if (run >= x) {
+                    topic = k;
+                    break;
+                }
+            }
+        }
+        a.z[t.y] = static_cast<uint16_t>(topic);
+        atomicAdd(brow + topic, 1u);
+    }
+    if (a.row_entries) {
+        for (int o = 16; o > 0; o >>= 1) entries += __shfl_xor_sync(0xffffffffu, entries, o);
+        if ((threadIdx.x & 31u) == 0) atomicAdd(a.row_entries, entries);
+    }
+}
+
+cudaError_t launch_vanilla(const SamplerArgs& a, uint32_t n_units, cudaStream_t s) {
+    if (a.compact) return cudaErrorInvalidConfiguration;  // wide rows only
+    const size_t phi_bytes = sizeof(float) * static_cast<size_t>(a.K_pad);
+    if (phi_bytes <= 200 * 1024) {
+        static bool configured = false;
+        if (!configured) {
+            const cudaError_t e = cudaFuncSetAttribute(sampler_vanilla_kernel<256, false>,
+                                                       cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+            if (e != cudaSuccess) return e;
+            configured = true;
+        }
+        sampler_vanilla_kernel<256, false><<<n_units, 256, phi_bytes, s>>>(a);
+    } else {
+        sampler_vanilla_kernel<256, true><<<n_units, 256, 0, s>>>(a);
+    }
+    return cudaGetLastError();
+}
+
 cudaError_t launch_sampler(const SamplerArgs& a, uint32_t n_units, cudaStream_t s) {
     if (n_units == 0) return cudaSuccess;
+    if (a.vanilla) return launch_vanilla(a, n_units, s);
     const size_t phi_bytes = sizeof(float) * (static_cast<size_t>(a.K_pad) + a.l8_stride);
     // Default: the quad-lane kernel wherever two 512-thread (or four 256-thread) CTAs fit an SM
     // (C3 K=10K: 100.0 vs 102.6 ms for 4-sector groups; C2 K=1K: 21.5 vs 23.5 ms for 2-sector

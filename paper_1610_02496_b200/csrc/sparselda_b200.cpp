@@ -168,8 +168,6 @@ TrainConfig TrainConfig::resolved(const Corpus& corpus) const {
         const unsigned hw = std::thread::hardware_concurrency();
         out.num_workers = hw ? hw : 1;
     }
-    if (out.sampler == SamplerKind::kVanilla)
-        throw ValidationError("the O(K) vanilla sampler is an oracle-only mode, not part of the device engine");
     return out;
 }
 
@@ -271,6 +269,7 @@ ModelState init_state(const Corpus& corpus, const TrainConfig& raw_cfg) {
     c.beta = cfg.beta;
     c.seed = cfg.seed;
     c.tree_branch = cfg.tree_branch;
+    c.sampler = cfg.sampler == SamplerKind::kVanilla ? SLDA_SAMPLER_VANILLA : SLDA_SAMPLER_SPARSE;
     c.init_mode = SLDA_INIT_AUTO;
     c.device = cfg.device;
     c.rank = 0;
@@ -287,6 +286,7 @@ ModelState init_state(const Corpus& corpus, const TrainConfig& raw_cfg) {
     s.alpha = cfg.alpha;
     s.beta = cfg.beta;
     s.seed = cfg.seed;
+    s.sampler = cfg.sampler;
     s.iteration = 0;
     return s;
 }
@@ -340,6 +340,7 @@ ModelState init_shard(const Corpus& corpus, const TrainConfig& raw_cfg, std::uin
     c.beta = cfg.beta;
     c.seed = cfg.seed;
     c.tree_branch = cfg.tree_branch;
+    c.sampler = cfg.sampler == SamplerKind::kVanilla ? SLDA_SAMPLER_VANILLA : SLDA_SAMPLER_SPARSE;
     c.init_mode = mode;
     c.device = cfg.device;
     c.rank = rank;
@@ -357,6 +358,7 @@ ModelState init_shard(const Corpus& corpus, const TrainConfig& raw_cfg, std::uin
     s.alpha = cfg.alpha;
     s.beta = cfg.beta;
     s.seed = cfg.seed;
+    s.sampler = cfg.sampler;
     return s;
 }
 
@@ -371,6 +373,7 @@ ModelState init_view(const slda_corpus_view& view, const TrainConfig& raw_cfg, s
     c.beta = cfg.beta;
     c.seed = cfg.seed;
     c.tree_branch = cfg.tree_branch;
+    c.sampler = cfg.sampler == SamplerKind::kVanilla ? SLDA_SAMPLER_VANILLA : SLDA_SAMPLER_SPARSE;
     c.init_mode = init_mode;
     c.device = cfg.device;
     c.rank = rank;
@@ -388,11 +391,15 @@ ModelState init_view(const slda_corpus_view& view, const TrainConfig& raw_cfg, s
     s.alpha = cfg.alpha;
     s.beta = cfg.beta;
     s.seed = cfg.seed;
+    s.sampler = cfg.sampler;
     return s;
 }
 
-IterationStats run_iteration(ModelState& state, const TrainConfig&) {
+IterationStats run_iteration(ModelState& state, const TrainConfig& cfg) {
     if (!state.engine_) throw ValidationError("model has no engine");
+    // The reference keeps dense or sparse doc-topic rows per the init-time kind
+    // (trainer.cpp:391-397); switching kinds between iterations is not a supported state.
+    if (cfg.sampler != state.sampler) throw ValidationError("sampler kind differs from the one the model was initialised with");
     if (!state.has_chunks_) throw ValidationError("model carries no chunks (loaded from a checkpoint)");
     slda_iteration_stats st{};
     check(slda_iterate(state.engine_.get(), &st));

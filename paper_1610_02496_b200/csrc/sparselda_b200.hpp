@@ -153,6 +153,7 @@ public:
     double beta = 0.0;
     std::uint64_t seed = 0;
     std::uint32_t iteration = 0;
+    SamplerKind sampler = SamplerKind::kSparse;  // TrainConfig::sampler at init (trainer.hpp:30)
 
     // B, B-hat, Q, L4 (V x K row-major / V) copied from the device.
     std::vector<std::uint32_t> word_topic() const;

@@ -27,7 +27,7 @@ class Config(C.Structure):
     _fields_ = [("num_topics", C.c_uint32), ("alpha", C.c_double), ("beta", C.c_double),
                 ("seed", C.c_uint64), ("tree_branch", C.c_uint32), ("init_mode", C.c_uint32),
                 ("device", C.c_int32), ("rank", C.c_uint32), ("world_size", C.c_uint32),
-                ("nccl_id", C.c_void_p)]
+                ("nccl_id", C.c_void_p), ("sampler", C.c_uint32)]
 
 
 class IterationStats(C.Structure):

@@ -63,4 +63,10 @@ CASES: dict[str, dict] = {
                    "heldout": {"family": G, "D": 60, "V": 600, "T": 6_000, "seed": 15, "latent": 20}},
     "nytimes_small": {"corpus": {"family": G, "D": 1000, "V": 5000, "T": 300_000, "seed": 16},
                       "K": 1000, "seed": 42, "iterations": 3, "chunks": 4, "workers": 8},
+    # SamplerKind::kVanilla: the O(K) dense-row baseline mode (trainer.cpp:281-285).
+    "vanilla_c1": {"corpus": {"family": G, "D": 1000, "V": 1000, "T": 100_000, "seed": 20161008},
+                   "K": 100, "seed": 42, "iterations": 8, "sampler": "vanilla"},
+    "vanilla_u_k300": {"corpus": {"family": U, "D": 200, "V": 150, "T": 9_000, "seed": 23},
+                       "K": 300, "alpha": 0.2, "seed": 5, "iterations": 4, "chunks": 3, "workers": 4,
+                       "sampler": "vanilla"},
 }

@@ -38,7 +38,8 @@ def run_case(name: str, spec: dict) -> dict:
         topic = rng.integers(0, spec["K"], size=len(doc), dtype=np.uint32)
     m = RefModel(D, V, doc, word, topic, K=spec["K"], alpha=spec.get("alpha", 0.0),
                  beta=spec.get("beta", 0.01), seed=spec["seed"],
-                 num_chunks=spec.get("chunks", 1), workers=spec.get("workers", 1))
+                 num_chunks=spec.get("chunks", 1), workers=spec.get("workers", 1),
+                 sampler=spec.get("sampler", "sparse"))
     out = {"spec": spec, "corpus_digest": digest(np.stack([doc, word])), "T": int(len(doc)),
            "alpha": m.alpha, "iterations": []}
     out["iterations"].append(m.digests())
@@ -85,8 +86,17 @@ def kats() -> dict:
 
 
 def main() -> None:
-    fixtures = {"kats": kats(), "cases": {}}
+    """`make_golden.py` regenerates every case; `make_golden.py NAME...` (re)generates only
+    those cases and keeps the others from the committed file."""
+    only = sys.argv[1:]
+    path = HERE / "reference_digests.json"
+    if only:
+        fixtures = json.loads(path.read_text())
+    else:
+        fixtures = {"kats": kats(), "cases": {}}
     for name, spec in CASES.items():
+        if only and name not in only:
+            continue
         print("case", name, flush=True)
         fixtures["cases"][name] = run_case(name, spec)
     (HERE / "reference_digests.json").write_text(json.dumps(fixtures, indent=1, sort_keys=True))

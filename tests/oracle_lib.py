@@ -77,6 +77,10 @@ def oracle_lib():
         lib.orc_init.argtypes = [C.c_uint32, C.c_uint32, C.c_uint64, _u32p, C.c_uint32,
                                  C.c_double, C.c_double, C.c_uint64, C.c_char_p, C.c_size_t]
         lib.orc_init.restype = C.c_void_p
+        lib.orc_set_sampler.argtypes = [C.c_void_p, C.c_uint32]
+        lib.orc_vanilla_token.argtypes = [C.c_uint32, _u32p, _u32p, _f32p, C.c_uint32, C.c_float,
+                                          C.c_double]
+        lib.orc_vanilla_token.restype = C.c_uint32
         lib.orc_free.argtypes = [C.c_void_p]
         lib.orc_iterate.argtypes = [C.c_void_p]
         lib.orc_iteration.argtypes = [C.c_void_p]
@@ -118,6 +122,8 @@ def ref_lib():
         lib.ref_init.argtypes = [C.c_uint32, C.c_uint32, C.c_uint64, _u32p, C.c_uint32,
                                  C.c_double, C.c_double, C.c_uint64, C.c_uint32, C.c_uint32]
         lib.ref_init.restype = C.c_void_p
+        lib.ref_init_sampler.argtypes = lib.ref_init.argtypes + [C.c_uint32]
+        lib.ref_init_sampler.restype = C.c_void_p
         lib.ref_free.argtypes = [C.c_void_p]
         lib.ref_iterate.argtypes = [C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_double)]
         for name in ("ref_num_workers", "ref_num_chunks"):
@@ -205,7 +211,8 @@ class _ModelBase:
 
 
 class OracleModel(_ModelBase):
-    def __init__(self, D, V, doc, word, topic=None, K=8, alpha=0.0, beta=0.01, seed=0):
+    def __init__(self, D, V, doc, word, topic=None, K=8, alpha=0.0, beta=0.01, seed=0,
+                 sampler="sparse"):
         super().__init__(D, V, doc, word, topic, K, alpha, beta, seed)
         lib = oracle_lib()
         err = C.create_string_buffer(256)
@@ -214,6 +221,7 @@ class OracleModel(_ModelBase):
         if not h:
             raise ValueError(err.value.decode())
         self.h = h
+        lib.orc_set_sampler(h, 1 if sampler == "vanilla" else 0)
         self.alpha = lib.orc_alpha(h)
 
     def _call(self, name, *args):
@@ -263,11 +271,11 @@ class RefModel(_ModelBase):
     """The reference itself (oracle/_ref)."""
 
     def __init__(self, D, V, doc, word, topic=None, K=8, alpha=0.0, beta=0.01, seed=0,
-                 num_chunks=1, workers=1):
+                 num_chunks=1, workers=1, sampler="sparse"):
         super().__init__(D, V, doc, word, topic, K, alpha, beta, seed)
         lib = ref_lib()
-        h = lib.ref_init(self.D, self.V, self.T, self.tokens.reshape(-1), self.K, alpha, beta,
-                         seed, num_chunks, workers)
+        h = lib.ref_init_sampler(self.D, self.V, self.T, self.tokens.reshape(-1), self.K, alpha, beta,
+                                 seed, num_chunks, workers, 1 if sampler == "vanilla" else 0)
         if not h:
             raise ValueError(lib.ref_last_error().decode())
         self.h = h

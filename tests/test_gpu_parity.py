@@ -39,6 +39,8 @@ def make_model(spec, iterations=None):
     cfg.seed = spec["seed"]
     cfg.iterations = spec["iterations"] if iterations is None else iterations
     cfg.tree_branch = 32 if spec["K"] <= 32768 else 41  # as the reference run (oracle/ref_shim.cpp)
+    if spec.get("sampler") == "vanilla":
+        cfg.sampler = s.SamplerKind.VANILLA
     return s.init_state(corpus, cfg), cfg, corpus
 
 
@@ -70,9 +72,10 @@ def test_engine_matches_reference_every_iteration(name, golden):
             assert st.mean_doc_topics == fx["mean_doc_topics"][it]
 
 
-@pytest.mark.parametrize("name", ["c1", "long_docs", "empty_docs", "u_k7_chunks", "k1"])
+@pytest.mark.parametrize("name", ["c1", "long_docs", "empty_docs", "u_k7_chunks", "k1", "vanilla_c1"])
 def test_compact_rows_match_reference(name, golden, monkeypatch):
-    """The opt-in compact C_dk row format (SLDA_ROW_FORMAT=compact) is bit-identical too."""
+    """The opt-in compact C_dk row format (SLDA_ROW_FORMAT=compact) is bit-identical too
+    (the vanilla mode keeps the wide rows whatever the setting)."""
     monkeypatch.setenv("SLDA_ROW_FORMAT", "compact")
     spec = CASES[name]
     fx = golden["cases"][name]
@@ -202,6 +205,18 @@ def test_raw_c_abi_round_trip(golden):
     t = e.kernel_times()
     assert t.sampler_ms > 0 and t.launches >= 5
     assert t.sampler_row_entries > 0
+
+
+def test_sampler_kind_is_fixed_at_init():
+    """The O(K) vanilla mode (SamplerKind.VANILLA) is chosen at init_state; an iteration asked
+    for with the other kind is refused instead of running on the wrong doc-topic state."""
+    s = slda()
+    m, cfg, _ = make_model(CASES["vanilla_u_k300"], iterations=1)
+    cfg.sampler = s.SamplerKind.SPARSE
+    with pytest.raises(ValueError, match="sampler kind"):
+        m.run_iteration(cfg)
+    cfg.sampler = s.SamplerKind.VANILLA
+    assert m.run_iteration(cfg).iteration == 1
 
 
 def test_validation_errors_map_to_value_error():

@@ -145,7 +145,7 @@ def test_oracle_matches_reference_digests(name, golden):
         topic = np.random.default_rng(spec["given_topics_seed"]).integers(0, spec["K"], size=len(doc),
                                                                           dtype=np.uint32)
     m = OracleModel(D, V, doc, word, topic, K=spec["K"], alpha=spec.get("alpha", 0.0),
-                    beta=spec.get("beta", 0.01), seed=spec["seed"])
+                    beta=spec.get("beta", 0.01), seed=spec["seed"], sampler=spec.get("sampler", "sparse"))
     assert m.alpha == fx["alpha"]
     iters = fx["iterations"]
     # Cheap cases: every iteration.  c1: every iteration too (50 x 100K tokens, ~2 s).
