@@ -10,7 +10,7 @@ compared with a stated tolerance (device log vs glibc log: |rel| <= 1e-12).
 import numpy as np
 import pytest
 
-from corpora import CASES, corpus_arrays
+from corpora import CASES, U, corpus_arrays
 from oracle_lib import OracleModel, digest
 
 pytestmark = pytest.mark.gpu
@@ -301,3 +301,29 @@ def test_kernel_variants_match_reference(name, variant, golden, monkeypatch):
         assert model_digests(m) == fx["iterations"][it], (name, variant, it)
         if it < iters:
             m.run_iteration(cfg)
+
+
+def test_acceptance_sublinear_scaling_in_k():
+    """acceptance.cpp:306-342 (criterion 5) on the device: one sparse-sampler iteration grows
+    by at most 4x from K=100 to K=3200, while the O(K) vanilla mode grows by more than 10x
+    (device time of the iteration, median of 3 after 2 warm-ups; same corpus shape: 50K docs,
+    V=20K, 64 tokens per document)."""
+    s = slda()
+    doc, word, D, V = corpus_arrays({"family": U, "D": 50_000, "V": 20_000, "T": 3_200_000, "seed": 5150})
+    corpus = s.Corpus.from_arrays(D, V, doc, word)
+
+    def iteration_ms(K, kind):
+        cfg = s.TrainConfig()
+        cfg.num_topics = K
+        cfg.seed = 31
+        cfg.sampler = kind
+        m = s.init_state(corpus, cfg)
+        for _ in range(2):
+            m.run_iteration(cfg)
+        return float(np.median([m.run_iteration(cfg).device_ms for _ in range(3)]))
+
+    sparse = iteration_ms(3200, s.SamplerKind.SPARSE) / iteration_ms(100, s.SamplerKind.SPARSE)
+    vanilla = iteration_ms(3200, s.SamplerKind.VANILLA) / iteration_ms(100, s.SamplerKind.VANILLA)
+    print(f"K 100 -> 3200: sparse x{sparse:.2f}, vanilla x{vanilla:.1f}")
+    assert sparse <= 4.0
+    assert vanilla > 10.0
