@@ -10,6 +10,7 @@
 #include <cstdint>
 #include <cstring>
 #include <exception>
+#include <sstream>
 #include <string>
 #include <vector>
 
@@ -234,6 +235,21 @@ int ref_heldout_ll(void* h, uint32_t D, uint32_t V, uint64_t T, const uint32_t* 
         *per_token_ll = r.per_token_ll;
         *tokens_evaluated = r.tokens_evaluated;
         return 0;
+    } catch (const std::exception& e) {
+        g_error = e.what();
+        return -1;
+    }
+}
+
+// load_docword (corpus.cpp:30-68) over a text buffer: the token count (tokens copied up to
+// cap, T x 3 uint32), or -1 with the reference's message in ref_last_error().
+int64_t ref_load_docword(const char* text, uint64_t n, uint32_t* tokens, uint64_t cap) {
+    try {
+        std::istringstream in(std::string(text, n));
+        const Corpus c = load_docword(in);
+        const uint64_t m = c.tokens.size() < cap ? c.tokens.size() : cap;
+        if (tokens && m) std::memcpy(tokens, c.tokens.data(), sizeof(Token) * m);
+        return static_cast<int64_t>(c.tokens.size());
     } catch (const std::exception& e) {
         g_error = e.what();
         return -1;

@@ -112,11 +112,7 @@ PYBIND11_MODULE(_core, m) {
                     py::arg("docword"), py::arg("vocab"))
         .def_static("from_files",
                     [](const std::string& docword_path, const std::string& vocab_path) {
-                        std::ifstream d(docword_path);
-                        if (!d) throw IoError("cannot open docword file " + docword_path);
-                        std::ifstream v(vocab_path);
-                        if (!v) throw IoError("cannot open vocab file " + vocab_path);
-                        return load_uci(d, v);
+                        return load_uci_files(docword_path, vocab_path);
                     },
                     py::arg("docword_path"), py::arg("vocab_path"))
         .def_static("from_arrays", &corpus_from_arrays, py::arg("num_docs"), py::arg("vocab_size"),

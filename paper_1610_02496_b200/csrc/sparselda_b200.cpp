@@ -3,6 +3,12 @@
 #include "sparselda_b200.hpp"
 
 #include <algorithm>
+#include <fcntl.h>
+#include <sys/mman.h>
+#include <sys/stat.h>
+#include <unistd.h>
+#include <cstring>
+#include <iterator>
 #include <chrono>
 #include <cstdio>
 #include <fstream>
@@ -54,39 +60,238 @@ std::uint64_t header_value(std::istream& in, std::uint64_t line, const char* nam
 }  // namespace
 
 // UCI bag-of-words (corpus.cpp:30-68): D, V, NNZ then "docID wordID count", 1-based.
-Corpus load_docword(std::istream& in) {
+//
+// The reference reads the entries line by line on one thread (the ingest bottleneck at
+// PubMed/ClueWeb scale).  Here the NNZ entry lines are split into byte
+// ranges at line boundaries and parsed by all host threads; tokens are then expanded in file
+// order into one allocation.  Accepted input, token order and every error (message and line
+// number -- the first failing line in file order wins) are the reference's: lines the fast
+// integer scanner does not accept outright are re-parsed with the reference's stream
+// semantics (`>>` into long long, trailing-data check).
+namespace {
+
+struct EntryLine {
+    bool ok;
+    long long d, w, n;
+};
+
+bool ws(char c) { return c == ' ' || c == '\t' || c == '\r' || c == '\v' || c == '\f'; }
+
+// Three non-negative decimal fields (<= 18 digits) separated and surrounded by whitespace;
+// false for anything else (signs, overflow, trailing data, missing fields), which then takes
+// the stream path.
+bool scan_entry(const char* p, const char* e, long long* v) {
+    for (int f = 0; f < 3; ++f) {
+        while (p < e && ws(*p)) ++p;
+        const char* q = p;
+        long long x = 0;
+        while (p < e && *p >= '0' && *p <= '9' && p - q < 18) x = x * 10 + (*p++ - '0');
+        if (p == q || (p < e && !ws(*p))) return false;
+        v[f] = x;
+    }
+    while (p < e && ws(*p)) ++p;
+    return p == e;
+}
+
+// The reference's per-line semantics (corpus.cpp:45-58); returns an error message or "".
+std::string parse_entry_stream(const std::string& text, long long* v) {
+    std::istringstream f(text);
+    if (!(f >> v[0] >> v[1] >> v[2])) return "malformed entry, expected \"docID wordID count\"";
+    std::string extra;
+    if (f >> extra) return "trailing data after entry";
+    return "";
+}
+
+struct Chunk {
+    const char* begin;
+    const char* end;          // exclusive; ends after a '\n' or at the buffer end
+    std::uint64_t first_line; // file line number of the chunk's first line
+    std::vector<std::uint32_t> d, w;
+    std::vector<std::uint64_t> n;
+    std::uint64_t tokens = 0;
+    std::uint64_t err_line = 0;  // 0 = none
+    std::string err;
+};
+
+}  // namespace
+
+Corpus load_docword_buffer(const char* data, std::size_t size) {
     Corpus c;
-    std::uint64_t line = 1;
-    const std::uint64_t D = header_value(in, line++, "D");
-    const std::uint64_t V = header_value(in, line++, "V");
-    const std::uint64_t nnz = header_value(in, line++, "NNZ");
+    const char* p = data;
+    const char* const end = data + size;
+    // Header lines through the reference's own stream semantics.
+    auto next_line = [&](std::string& out) -> bool {  // std::getline over the buffer
+        if (p >= end) return false;
+        const char* nl = static_cast<const char*>(std::memchr(p, '\n', static_cast<std::size_t>(end - p)));
+        const char* le = nl ? nl : end;
+        out.assign(p, le);
+        p = nl ? nl + 1 : end;
+        return true;
+    };
+    std::uint64_t hdr[3];
+    const char* names[3] = {"D", "V", "NNZ"};
+    for (int i = 0; i < 3; ++i) {
+        std::string text;
+        if (!next_line(text)) parse_fail(static_cast<std::uint64_t>(i) + 1, std::string("missing ") + names[i] + " header line");
+        std::istringstream hs(text + "\n");
+        hdr[i] = header_value(hs, static_cast<std::uint64_t>(i) + 1, names[i]);
+    }
+    const std::uint64_t D = hdr[0], V = hdr[1], nnz = hdr[2];
     if (D > 0xFFFFFFFFull || V > 0xFFFFFFFFull) parse_fail(1, "dimension exceeds 32-bit id space");
     c.num_docs = static_cast<std::uint32_t>(D);
     c.vocab_size = static_cast<std::uint32_t>(V);
     c.doc_lengths.assign(c.num_docs, 0);
     c.word_freqs.assign(c.vocab_size, 0);
-    std::string text;
-    for (std::uint64_t i = 0; i < nnz; ++i, ++line) {
-        if (!std::getline(in, text)) parse_fail(line, "unexpected end of file, expected entry");
-        std::istringstream f(text);
-        long long d = 0, w = 0, n = 0;
-        if (!(f >> d >> w >> n)) parse_fail(line, "malformed entry, expected \"docID wordID count\"");
-        std::string extra;
-        if (f >> extra) parse_fail(line, "trailing data after entry");
-        if (d < 1 || static_cast<std::uint64_t>(d) > D) parse_fail(line, "docID out of range [1, D]");
-        if (w < 1 || static_cast<std::uint64_t>(w) > V) parse_fail(line, "wordID out of range [1, V]");
-        if (n < 1) parse_fail(line, "count must be >= 1");
-        const Token tok{static_cast<DocId>(d - 1), static_cast<WordId>(w - 1), kInvalidTopic};
-        c.tokens.insert(c.tokens.end(), static_cast<std::size_t>(n), tok);
-        c.doc_lengths[tok.doc] += static_cast<std::uint32_t>(n);
-        c.word_freqs[tok.word] += static_cast<std::uint64_t>(n);
+
+    // Byte ranges at line starts, one or more per thread.
+    const std::size_t body = static_cast<std::size_t>(end - p);
+    unsigned nt = std::thread::hardware_concurrency();
+    nt = nt == 0 ? 1 : (nt > 64 ? 64 : nt);
+    if (body < (1u << 20)) nt = 1;
+    std::vector<Chunk> chunks;
+    {
+        const char* b = p;
+        for (unsigned i = 0; i < nt && b < end; ++i) {
+            const char* e = i + 1 == nt ? end : p + body / nt * (i + 1);
+            if (e < b) e = b;
+            if (e < end) {
+                const char* nl = static_cast<const char*>(std::memchr(e, '\n', static_cast<std::size_t>(end - e)));
+                e = nl ? nl + 1 : end;
+            }
+            Chunk ch;
+            ch.begin = b;
+            ch.end = e;
+            chunks.push_back(std::move(ch));
+            b = e;
+        }
     }
+    // Pass 1: lines per chunk (a line is '\n'-terminated, or the non-empty remainder at EOF).
+    std::vector<std::uint64_t> lines(chunks.size(), 0);
+    auto run = [&](auto&& fn) {
+        std::vector<std::thread> th;
+        for (std::size_t i = 1; i < chunks.size(); ++i) th.emplace_back(fn, i);
+        if (!chunks.empty()) fn(0);
+        for (auto& t : th) t.join();
+    };
+    run([&](std::size_t i) {
+        std::uint64_t n = 0;
+        for (const char* q = chunks[i].begin; q < chunks[i].end;) {
+            const char* nl = static_cast<const char*>(std::memchr(q, '\n', static_cast<std::size_t>(chunks[i].end - q)));
+            ++n;
+            q = nl ? nl + 1 : chunks[i].end;
+        }
+        lines[i] = n;
+    });
+    // Keep exactly the first nnz lines (the reference reads no further).
+    std::uint64_t seen = 0, line0 = 4;
+    std::size_t used = 0;
+    for (; used < chunks.size() && seen < nnz; ++used) {
+        chunks[used].first_line = line0 + seen;
+        if (seen + lines[used] > nnz) {  // cut inside this chunk after (nnz - seen) lines
+            const char* q = chunks[used].begin;
+            for (std::uint64_t k = 0; k < nnz - seen; ++k) {
+                const char* nl = static_cast<const char*>(std::memchr(q, '\n', static_cast<std::size_t>(chunks[used].end - q)));
+                q = nl ? nl + 1 : chunks[used].end;
+            }
+            chunks[used].end = q;
+            lines[used] = nnz - seen;
+        }
+        seen += lines[used];
+    }
+    chunks.resize(used);
+    const std::uint64_t eof_line = seen < nnz ? line0 + seen : 0;  // first missing entry line
+
+    // Pass 2: parse.
+    run([&](std::size_t i) {
+        Chunk& ch = chunks[i];
+        std::uint64_t line = ch.first_line;
+        std::string text;
+        for (const char* q = ch.begin; q < ch.end; ++line) {
+            const char* nl = static_cast<const char*>(std::memchr(q, '\n', static_cast<std::size_t>(ch.end - q)));
+            const char* le = nl ? nl : ch.end;
+            long long v[3];
+            std::string err;
+            if (!scan_entry(q, le, v)) {
+                text.assign(q, le);
+                err = parse_entry_stream(text, v);
+            }
+            q = nl ? nl + 1 : ch.end;
+            if (err.empty()) {
+                if (v[0] < 1 || static_cast<std::uint64_t>(v[0]) > D) err = "docID out of range [1, D]";
+                else if (v[1] < 1 || static_cast<std::uint64_t>(v[1]) > V) err = "wordID out of range [1, V]";
+                else if (v[2] < 1) err = "count must be >= 1";
+            }
+            if (!err.empty()) {
+                ch.err_line = line;
+                ch.err = err;
+                return;
+            }
+            ch.d.push_back(static_cast<std::uint32_t>(v[0] - 1));
+            ch.w.push_back(static_cast<std::uint32_t>(v[1] - 1));
+            ch.n.push_back(static_cast<std::uint64_t>(v[2]));
+            ch.tokens += static_cast<std::uint64_t>(v[2]);
+        }
+    });
+    for (const Chunk& ch : chunks)
+        if (ch.err_line) parse_fail(ch.err_line, ch.err);  // chunks are in file order
+    if (eof_line) parse_fail(eof_line, "unexpected end of file, expected entry");
+
+    // Pass 3: expand tokens in file order; per-document / per-word totals.
+    std::vector<std::uint64_t> off(chunks.size() + 1, 0);
+    for (std::size_t i = 0; i < chunks.size(); ++i) off[i + 1] = off[i] + chunks[i].tokens;
+    c.tokens.resize(off.back());
+    run([&](std::size_t i) {
+        const Chunk& ch = chunks[i];
+        Token* t = c.tokens.data() + off[i];
+        for (std::size_t k = 0; k < ch.d.size(); ++k) {
+            const Token tok{ch.d[k], ch.w[k], kInvalidTopic};
+            std::fill(t, t + ch.n[k], tok);
+            t += ch.n[k];
+            __atomic_fetch_add(&c.doc_lengths[ch.d[k]], static_cast<std::uint32_t>(ch.n[k]), __ATOMIC_RELAXED);
+            __atomic_fetch_add(&c.word_freqs[ch.w[k]], ch.n[k], __ATOMIC_RELAXED);
+        }
+    });
     c.num_tokens = c.tokens.size();
     return c;
 }
 
-Corpus load_uci(std::istream& docword, std::istream& vocab) {
-    Corpus c = load_docword(docword);
+Corpus load_docword(std::istream& in) {
+    std::ostringstream ss;
+    ss << in.rdbuf();
+    const std::string buf = ss.str();
+    return load_docword_buffer(buf.data(), buf.size());
+}
+
+Corpus load_uci_files(const std::string& docword_path, const std::string& vocab_path) {
+    const int fd = ::open(docword_path.c_str(), O_RDONLY);
+    if (fd < 0) throw IoError("cannot open docword file " + docword_path);
+    struct stat st {};
+    if (::fstat(fd, &st) != 0) {
+        ::close(fd);
+        throw IoError("cannot stat docword file " + docword_path);
+    }
+    const std::size_t size = static_cast<std::size_t>(st.st_size);
+    void* map = size ? ::mmap(nullptr, size, PROT_READ, MAP_PRIVATE, fd, 0) : nullptr;
+    ::close(fd);
+    if (size && map == MAP_FAILED) throw IoError("cannot map docword file " + docword_path);
+    std::ifstream vocab(vocab_path);
+    if (!vocab) {
+        if (size) ::munmap(map, size);
+        throw IoError("cannot open vocab file " + vocab_path);
+    }
+    Corpus c;
+    try {
+        c = load_docword_buffer(static_cast<const char*>(map), size);
+    } catch (...) {
+        if (size) ::munmap(map, size);
+        throw;
+    }
+    if (size) ::munmap(map, size);
+    load_vocab(c, vocab);
+    return c;
+}
+
+void load_vocab(Corpus& c, std::istream& vocab) {
     c.vocab.reserve(c.vocab_size);
     std::string term;
     std::uint64_t line = 0;
@@ -101,6 +306,11 @@ Corpus load_uci(std::istream& docword, std::istream& vocab) {
     if (line != c.vocab_size)
         throw ValidationError("vocab line " + std::to_string(line) + ": expected V=" +
                               std::to_string(c.vocab_size) + " entries, got " + std::to_string(line));
+}
+
+Corpus load_uci(std::istream& docword, std::istream& vocab) {
+    Corpus c = load_docword(docword);
+    load_vocab(c, vocab);
     return c;
 }
 

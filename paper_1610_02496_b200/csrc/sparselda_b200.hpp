@@ -67,6 +67,11 @@ struct Corpus {  // corpus.hpp:12-20
 
 Corpus load_uci(std::istream& docword, std::istream& vocab);        // corpus.hpp:49
 Corpus load_docword(std::istream& docword);                          // corpus.hpp:53
+// The same over an in-memory (or mapped) docword file; parses with all host threads.
+Corpus load_docword_buffer(const char* data, std::size_t size);
+// load_uci over files (the docword file memory-mapped); IoError when either cannot be opened.
+Corpus load_uci_files(const std::string& docword_path, const std::string& vocab_path);
+void load_vocab(Corpus& corpus, std::istream& vocab);
 void init_assignments(Corpus& corpus, std::uint32_t num_topics, std::uint64_t seed);  // :57
 // Synthetic corpora; family 0 = G, 1 = U.
 Corpus generate_corpus(const slda_gen_params& params);

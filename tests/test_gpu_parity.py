@@ -375,3 +375,23 @@ def test_acceptance_convergence_sparse_vs_vanilla():
     print(f"sparse LL {sparse_first:.4f} -> {sparse_last:.4f}; vanilla final {vanilla_last:.4f}")
     assert sparse_last - sparse_first >= 1.0
     assert abs(sparse_last - vanilla_last) <= 0.05
+
+
+def test_acceptance_streaming_chunk_counts():
+    """acceptance.cpp:424-445 (criterion 8): 1, 4 and 16 chunks give identical assignments.
+    The device engine keeps one resident shard per GPU (num_chunks only sets the reference's
+    streaming granularity), so the result must not depend on it -- and it equals the
+    reference's own multi-chunk runs (u_k7_chunks, nytimes_small cases)."""
+    s = slda()
+    doc, word, D, V = corpus_arrays({"family": U, "D": 64, "V": 30, "T": 960, "seed": 808})
+    corpus = s.Corpus.from_arrays(D, V, doc, word)
+    out = []
+    for chunks in (1, 4, 16):
+        cfg = s.TrainConfig()
+        cfg.num_topics = 8
+        cfg.iterations = 3
+        cfg.num_chunks = chunks
+        cfg.num_workers = 2
+        cfg.seed = 99
+        out.append(s.train(corpus, cfg).assignments())
+    assert np.array_equal(out[0], out[1]) and np.array_equal(out[0], out[2])
