@@ -286,6 +286,7 @@ struct slda_engine {
     ~slda_engine() {
         if (scratch_thread.joinable()) scratch_thread.join();
         if (device >= 0) cudaSetDevice(device);
+        if (scratch_to_free) cudaFree(scratch_to_free);  // setup failed before the hand-off
         if (stream) cudaStreamSynchronize(stream);
         for (auto& set : ring)
             for (auto& e : set)

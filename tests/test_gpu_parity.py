@@ -395,3 +395,21 @@ def test_acceptance_streaming_chunk_counts():
         cfg.seed = 99
         out.append(s.train(corpus, cfg).assignments())
     assert np.array_equal(out[0], out[1]) and np.array_equal(out[0], out[2])
+
+
+def test_failed_setups_release_device_memory():
+    """A setup that fails validation after its scratch arena was reserved gives the memory back
+    (the arena is normally released by a helper thread after a successful setup)."""
+    import torch
+
+    s = slda()
+    doc, word, D, V = corpus_arrays(CASES["nytimes_small"]["corpus"])
+    cfg = s.TrainConfig()
+    cfg.num_topics = 3
+    bad = s.Corpus.from_arrays(D, V, doc, word, np.full(len(doc), 7, np.uint32))
+    free0 = torch.cuda.mem_get_info()[0]
+    for _ in range(5):
+        with pytest.raises(ValueError, match="exceeds configured K"):
+            s.init_state(bad, cfg)
+    torch.cuda.synchronize()
+    assert torch.cuda.mem_get_info()[0] >= free0 - (64 << 20)
