@@ -4,12 +4,15 @@
 #include "common.cuh"
 #include "kernels.hpp"
 
+#include <cstdlib>
+#include <string>
+
 namespace slda {
 
 // ============================================================================
 // K5/K6 -- preprocess (counts.cpp:37-63) + rebuild_trees (trainer.cpp:237-248,
 // sampler.hpp:58-90, :142-149).  colsum: integer column sums (order-free).
-// phi: thread per word row, 16-column tiles staged in shared memory by cp.async
+// phi: thread per word row, 32-column tiles staged in shared memory by cp.async
 // so global traffic is coalesced while each thread runs the row's sequential
 // f32 prefix (the L4 level) exactly as WaryTree::build.
 // ============================================================================
@@ -107,19 +110,23 @@ cudaError_t launch_denom(const unsigned long long* colsum, uint32_t K, uint32_t 
 }
 
 // One thread per word row (the L4 prefix is a sequential f32 chain), 64 rows per CTA and
-// 16-column tiles.  A tile of C_wk lands in shared memory by cp.async (4 threads per row
-// segment, coalesced), double-buffered so tile t+1 is in flight while tile t is computed; each
-// thread then reads its own row, writes bhat in place and the L4 prefix beside it, and the CTA
-// stores both tiles back with the copy mapping.  kPhiStages tiles (with their columns' denom,
-// 1/denom and zero-count bhat) are in flight per CTA.  16-byte quads are XOR-swizzled by row so the
-// per-row and the per-segment accesses are both bank-conflict free.  The small footprint
-// (39 KB) keeps 5 CTAs = 320 rows resident per SM with 7 tiles (28 KB per CTA) in flight.  Padded columns (>= K) hold zero counts and zv = 0, so they add +0.0f to the
-// chain (unchanged) and store bhat = 0, as the reference's padding.
+// C-column tiles (default C = 32).  A tile of C_wk lands in shared memory by cp.async (C/4
+// threads per row segment, coalesced) in an S-stage pipeline, together with its columns'
+// denom, 1/denom and zero-count bhat; each thread then reads its own row, writes bhat in place
+// and the L4 prefix beside it, and the CTA stores both tiles back with the copy mapping.
+// 16-byte quads are XOR-swizzled by row so the per-row and the per-segment accesses are both
+// bank-conflict free.  32 x 4: 44 KB of shared memory, 5 CTAs = 320 rows per SM, 3 tiles
+// (24 KB per CTA) in flight.  Padded columns (>= K) hold zero counts and zv = 0, so they add
+// +0.0f to the chain (unchanged) and store bhat = 0, as the reference's padding.
 constexpr int kPhiRows = 64;
-constexpr int kPhiCols = 16;
 
+// Word offset of 16-byte quad `quad` of tile row `row` (C columns, C/4 quads per row): quads are
+// XOR-swizzled so eight consecutive rows reading the same quad, and one row-segment's quads
+// read by consecutive threads, both fall in distinct banks.
+template <int C>
 __device__ __forceinline__ uint32_t phi_swz(uint32_t row, uint32_t quad) {
-    return row * kPhiCols + ((quad ^ ((row >> 1) & 3u)) << 2);
+    constexpr uint32_t Q = C / 4, sh = Q == 4 ? 1u : 0u;
+    return row * C + ((quad ^ ((row >> sh) & (Q - 1u))) << 2);
 }
 
 __device__ __forceinline__ void phi_cp16(void* smem, const void* gmem, bool valid) {
@@ -128,12 +135,12 @@ __device__ __forceinline__ void phi_cp16(void* smem, const void* gmem, bool vali
                  : "memory");
 }
 
-constexpr int kPhiStages = 8;  // measured: 2 / 4 / 8 / 12 / 16 stages -> 6.4 / 5.3 / 4.9 / 5.5 / 6.4 ms (C3)
-constexpr size_t kPhiSmem =
-    static_cast<size_t>(kPhiStages) * (2 * kPhiCols * 8 + kPhiRows * kPhiCols * 4 + kPhiCols * 4) +
-    kPhiRows * kPhiCols * 4;
+template <int C, int S>
+constexpr size_t phi_smem_bytes() {
+    return static_cast<size_t>(S) * (2 * C * 8 + kPhiRows * C * 4 + C * 4) + kPhiRows * C * 4;
+}
 
-template <bool kMirror>
+template <int C, int S, bool kMirror>
 __global__ void __launch_bounds__(kPhiRows, 4) phi_kernel(const uint32_t* __restrict__ B,
                                                          const double* __restrict__ denom,
                                                          const float* __restrict__ zv,
@@ -142,48 +149,51 @@ __global__ void __launch_bounds__(kPhiRows, 4) phi_kernel(const uint32_t* __rest
                                                          uint32_t row_begin, uint32_t row_end,
                                                          uint32_t K_pad, uint32_t l8_stride, double beta,
                                                          float falpha, PeerMirror mirror) {
+    static_assert(C == 16 || C == 32, "tile width");
+    constexpr uint32_t Q = C / 4;              // quads per tile row
+    constexpr uint32_t RP = kPhiRows / Q;      // rows per copy pass
     extern __shared__ __align__(16) unsigned char phi_smem[];
-    // [stage][2][kPhiCols] denom, 1/denom | [stage][rows*cols] counts, then bhat | L4 | [stage] zv
-    auto s_den = reinterpret_cast<double(*)[2][kPhiCols]>(phi_smem);
-    auto t_in = reinterpret_cast<uint32_t(*)[kPhiRows * kPhiCols]>(phi_smem + kPhiStages * 2 * kPhiCols * 8);
-    float* t_l4 = reinterpret_cast<float*>(phi_smem + kPhiStages * (2 * kPhiCols * 8 + kPhiRows * kPhiCols * 4));
-    auto s_zv = reinterpret_cast<float(*)[kPhiCols]>(t_l4 + kPhiRows * kPhiCols);
+    // [stage][2][C] denom, 1/denom | [stage][rows*C] counts, then bhat | L4 | [stage][C] zv
+    auto s_den = reinterpret_cast<double(*)[2][C]>(phi_smem);
+    auto t_in = reinterpret_cast<uint32_t(*)[kPhiRows * C]>(phi_smem + S * 2 * C * 8);
+    float* t_l4 = reinterpret_cast<float*>(phi_smem + S * (2 * C * 8 + kPhiRows * C * 4));
+    auto s_zv = reinterpret_cast<float(*)[C]>(t_l4 + kPhiRows * C);
     const double* __restrict__ rcp = denom + K_pad;
     const uint32_t tid = threadIdx.x;
     const uint32_t v0 = row_begin + blockIdx.x * kPhiRows;
     const uint32_t v = v0 + tid;
-    // Copy / store role: quad cq of rows crow + 16p, p = 0..3.
-    const uint32_t cq = tid & 3u, crow = tid >> 2;
-    const size_t stride16 = static_cast<size_t>(16) * K_pad;
+    // Copy / store role: quad cq of rows crow + RP*p, p = 0..Q-1.
+    const uint32_t cq = tid % Q, crow = tid / Q;
+    const size_t stride = static_cast<size_t>(RP) * K_pad;
     const size_t g0 = static_cast<size_t>(v0 + crow) * K_pad + cq * 4u;
-    const uint32_t ntiles = K_pad / kPhiCols;
+    const uint32_t ntiles = K_pad / C;
     auto issue = [&](uint32_t c0, int st) {
 #pragma unroll
-        for (uint32_t p = 0; p < 4; ++p) {
-            const bool ok = v0 + crow + 16u * p < row_end;
-            phi_cp16(&t_in[st][phi_swz(crow + 16u * p, cq)], ok ? B + g0 + p * stride16 + c0 : B, ok);
+        for (uint32_t p = 0; p < Q; ++p) {
+            const bool ok = v0 + crow + RP * p < row_end;
+            phi_cp16(&t_in[st][phi_swz<C>(crow + RP * p, cq)], ok ? B + g0 + p * stride + c0 : B, ok);
         }
-        if (tid < 8) phi_cp16(&s_den[st][0][tid * 2], denom + c0 + tid * 2, true);
-        else if (tid < 16) phi_cp16(&s_den[st][1][(tid - 8) * 2], rcp + c0 + (tid - 8) * 2, true);
-        else if (tid < 20) phi_cp16(&s_zv[st][(tid - 16) * 4], zv + c0 + (tid - 16) * 4, true);
+        if (tid < C / 2) phi_cp16(&s_den[st][0][tid * 2], denom + c0 + tid * 2, true);
+        else if (tid < C) phi_cp16(&s_den[st][1][(tid - C / 2) * 2], rcp + c0 + (tid - C / 2) * 2, true);
+        else if (tid < C + C / 4) phi_cp16(&s_zv[st][(tid - C) * 4], zv + c0 + (tid - C) * 4, true);
     };
     float run = 0.0f;
 #pragma unroll
-    for (uint32_t t = 0; t + 1 < kPhiStages; ++t) {
-        if (t < ntiles) issue(t * kPhiCols, t);
+    for (uint32_t t = 0; t + 1 < S; ++t) {
+        if (t < ntiles) issue(t * C, t);
         asm volatile("cp.async.commit_group;\n" ::: "memory");
     }
     for (uint32_t t = 0; t < ntiles; ++t) {
-        const int st = t % kPhiStages;
-        const uint32_t c0 = t * kPhiCols;
-        asm volatile("cp.async.wait_group %0;\n" ::"n"(kPhiStages - 2) : "memory");
+        const int st = t % S;
+        const uint32_t c0 = t * C;
+        asm volatile("cp.async.wait_group %0;\n" ::"n"(S - 2) : "memory");
         __syncthreads();  // tile t visible; tile t-1's stores have read its stage and t_l4
-        if (t + kPhiStages - 1 < ntiles) issue(c0 + (kPhiStages - 1) * kPhiCols, (t + kPhiStages - 1) % kPhiStages);
+        if (t + S - 1 < ntiles) issue(c0 + (S - 1) * C, (t + S - 1) % S);
         asm volatile("cp.async.commit_group;\n" ::: "memory");
-        float l8v[2];
+        float l8v[Q / 2];
 #pragma unroll
-        for (uint32_t j = 0; j < 4; ++j) {
-            const uint32_t o = phi_swz(tid, j);
+        for (uint32_t j = 0; j < Q; ++j) {
+            const uint32_t o = phi_swz<C>(tid, j);
             const uint4 cnt = *reinterpret_cast<const uint4*>(&t_in[st][o]);
             float4 bh = *reinterpret_cast<const float4*>(&s_zv[st][j * 4]);
             if ((cnt.x | cnt.y | cnt.z | cnt.w) != 0u) {
@@ -209,19 +219,26 @@ __global__ void __launch_bounds__(kPhiRows, 4) phi_kernel(const uint32_t* __rest
         }
         if (v < row_end) {
             const size_t o8 = static_cast<size_t>(v) * l8_stride + c0 / kLeaf;
-            *reinterpret_cast<float2*>(l8 + o8) = make_float2(l8v[0], l8v[1]);
-            if (kMirror)
-                for (uint32_t p = 0; p < mirror.n; ++p)
-                    *reinterpret_cast<float2*>(mirror.l8[p] + o8) = make_float2(l8v[0], l8v[1]);
+            if (C == 32) {
+                const float4 x = make_float4(l8v[0], l8v[1 % (Q / 2)], l8v[2 % (Q / 2)], l8v[3 % (Q / 2)]);
+                *reinterpret_cast<float4*>(l8 + o8) = x;
+                if (kMirror)
+                    for (uint32_t p = 0; p < mirror.n; ++p) *reinterpret_cast<float4*>(mirror.l8[p] + o8) = x;
+            } else {
+                const float2 x = make_float2(l8v[0], l8v[1 % (Q / 2)]);
+                *reinterpret_cast<float2*>(l8 + o8) = x;
+                if (kMirror)
+                    for (uint32_t p = 0; p < mirror.n; ++p) *reinterpret_cast<float2*>(mirror.l8[p] + o8) = x;
+            }
         }
         __syncthreads();
 #pragma unroll
-        for (uint32_t p = 0; p < 4; ++p) {
-            if (v0 + crow + 16u * p < row_end) {
-                const uint32_t o = phi_swz(crow + 16u * p, cq);
+        for (uint32_t p = 0; p < Q; ++p) {
+            if (v0 + crow + RP * p < row_end) {
+                const uint32_t o = phi_swz<C>(crow + RP * p, cq);
                 const float4 b = *reinterpret_cast<const float4*>(&t_in[st][o]);
                 const float4 l = *reinterpret_cast<const float4*>(&t_l4[o]);
-                const size_t go = g0 + p * stride16 + c0;
+                const size_t go = g0 + p * stride + c0;
                 *reinterpret_cast<float4*>(bhat + go) = b;
                 *reinterpret_cast<float4*>(l4 + go) = l;
                 if (kMirror) {  // the all-gather, fused: the same values into every peer's replica
@@ -246,27 +263,44 @@ __global__ void __launch_bounds__(kPhiRows, 4) phi_kernel(const uint32_t* __rest
     }
 }
 
+template <int C, int S>
+cudaError_t launch_phi_t(const uint32_t* B, const double* denom, const float* zv, float* bhat, float* l4,
+                         float* l8, float* q, uint32_t row_begin, uint32_t row_end, uint32_t K_pad,
+                         uint32_t l8_stride, double beta, float falpha, cudaStream_t s, const PeerMirror* mirror) {
+    constexpr size_t smem = phi_smem_bytes<C, S>();
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(phi_kernel<C, S, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+        cudaFuncSetAttribute(phi_kernel<C, S, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+        attr = true;
+    }
+    const uint32_t blocks = (row_end - row_begin + kPhiRows - 1) / kPhiRows;
+    if (mirror && mirror->n > 0)
+        phi_kernel<C, S, true><<<blocks, kPhiRows, smem, s>>>(B, denom, zv, bhat, l4, l8, q, row_begin, row_end,
+                                                              K_pad, l8_stride, beta, falpha, *mirror);
+    else
+        phi_kernel<C, S, false><<<blocks, kPhiRows, smem, s>>>(B, denom, zv, bhat, l4, l8, q, row_begin, row_end,
+                                                               K_pad, l8_stride, beta, falpha, PeerMirror{});
+    return cudaGetLastError();
+}
+
 cudaError_t launch_phi(const uint32_t* B, const double* denom, const float* zv, float* bhat,
                        float* l4, float* l8, float* q, uint32_t row_begin, uint32_t row_end,
                        uint32_t K, uint32_t K_pad, uint32_t l8_stride, double beta, float falpha,
                        cudaStream_t s, const PeerMirror* mirror) {
     (void)K;  // columns >= K are zero counts with zv = 0 (see above)
     if (row_end <= row_begin) return cudaSuccess;
-    if (K_pad % kPhiCols) return cudaErrorInvalidValue;
-    const uint32_t blocks = (row_end - row_begin + kPhiRows - 1) / kPhiRows;
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(phi_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kPhiSmem));
-        cudaFuncSetAttribute(phi_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kPhiSmem));
-        attr = true;
+    if (K_pad % 32) return cudaErrorInvalidValue;
+    const char* e = std::getenv("SLDA_PHI_SHAPE");  // read per launch (tests switch it per engine)
+    const std::string v = e ? e : "";
+    const int shape = v == "16x8" ? 1 : v == "32x3" ? 2 : 0;
+    // Tile columns x pipeline stages, phi alone (ms, C3 / C5 K=50K): 16x8 4.91 / 17.9,
+    // 32x3 4.68 / 14.8, 32x4 4.10 / 15.7, 32x6 5.88 / 16.2.
+    switch (shape) {
+        case 1: return launch_phi_t<16, 8>(B, denom, zv, bhat, l4, l8, q, row_begin, row_end, K_pad, l8_stride, beta, falpha, s, mirror);
+        case 2: return launch_phi_t<32, 3>(B, denom, zv, bhat, l4, l8, q, row_begin, row_end, K_pad, l8_stride, beta, falpha, s, mirror);
+        default: return launch_phi_t<32, 4>(B, denom, zv, bhat, l4, l8, q, row_begin, row_end, K_pad, l8_stride, beta, falpha, s, mirror);
     }
-    if (mirror && mirror->n > 0)
-        phi_kernel<true><<<blocks, kPhiRows, kPhiSmem, s>>>(B, denom, zv, bhat, l4, l8, q, row_begin, row_end, K_pad,
-                                                            l8_stride, beta, falpha, *mirror);
-    else
-        phi_kernel<false><<<blocks, kPhiRows, kPhiSmem, s>>>(B, denom, zv, bhat, l4, l8, q, row_begin, row_end,
-                                                             K_pad, l8_stride, beta, falpha, PeerMirror{});
-    return cudaGetLastError();
 }
 
 // ---- Peer-memory M-step exchange (world > 1 without NCCL; engine.cu m_step_peer) -------------
