@@ -4,6 +4,7 @@
 #include "common.cuh"
 #include "kernels.hpp"
 
+#include <cmath>
 #include <cstdlib>
 #include <string>
 
@@ -149,7 +150,7 @@ __global__ void __launch_bounds__(kPhiRows, 4) phi_kernel(const uint32_t* __rest
                                                          uint32_t row_begin, uint32_t row_end,
                                                          uint32_t K_pad, uint32_t l8_stride, double beta,
                                                          float falpha, PeerMirror mirror) {
-    static_assert(C == 16 || C == 32, "tile width");
+    static_assert(C == 16 || C == 32 || C == 64, "tile width");
     constexpr uint32_t Q = C / 4;              // quads per tile row
     constexpr uint32_t RP = kPhiRows / Q;      // rows per copy pass
     extern __shared__ __align__(16) unsigned char phi_smem[];
@@ -166,16 +167,22 @@ __global__ void __launch_bounds__(kPhiRows, 4) phi_kernel(const uint32_t* __rest
     const uint32_t cq = tid % Q, crow = tid / Q;
     const size_t stride = static_cast<size_t>(RP) * K_pad;
     const size_t g0 = static_cast<size_t>(v0 + crow) * K_pad + cq * 4u;
-    const uint32_t ntiles = K_pad / C;
+    const uint32_t ntiles = (K_pad + C - 1) / C;  // K_pad is a multiple of 32: a 64-column tile may be half
     auto issue = [&](uint32_t c0, int st) {
 #pragma unroll
         for (uint32_t p = 0; p < Q; ++p) {
-            const bool ok = v0 + crow + RP * p < row_end;
+            const bool ok = v0 + crow + RP * p < row_end && (C <= 32 || c0 + cq * 4u < K_pad);
             phi_cp16(&t_in[st][phi_swz<C>(crow + RP * p, cq)], ok ? B + g0 + p * stride + c0 : B, ok);
         }
-        if (tid < C / 2) phi_cp16(&s_den[st][0][tid * 2], denom + c0 + tid * 2, true);
-        else if (tid < C) phi_cp16(&s_den[st][1][(tid - C / 2) * 2], rcp + c0 + (tid - C / 2) * 2, true);
-        else if (tid < C + C / 4) phi_cp16(&s_zv[st][(tid - C) * 4], zv + c0 + (tid - C) * 4, true);
+#pragma unroll
+        for (uint32_t i = tid; i < C + C / 4; i += kPhiRows) {
+            // past K_pad (half tile): zero-filled, so the padding cells read zv = 0
+            const uint32_t col = i < C / 2 ? i * 2 : i < C ? (i - C / 2) * 2 : (i - C) * 4;
+            const bool in = c0 + col < K_pad;
+            if (i < C / 2) phi_cp16(&s_den[st][0][col], in ? denom + c0 + col : denom, in);
+            else if (i < C) phi_cp16(&s_den[st][1][col], in ? rcp + c0 + col : rcp, in);
+            else phi_cp16(&s_zv[st][col], in ? zv + c0 + col : zv, in);
+        }
     };
     float run = 0.0f;
 #pragma unroll
@@ -219,11 +226,17 @@ __global__ void __launch_bounds__(kPhiRows, 4) phi_kernel(const uint32_t* __rest
         }
         if (v < row_end) {
             const size_t o8 = static_cast<size_t>(v) * l8_stride + c0 / kLeaf;
-            if (C == 32) {
-                const float4 x = make_float4(l8v[0], l8v[1 % (Q / 2)], l8v[2 % (Q / 2)], l8v[3 % (Q / 2)]);
-                *reinterpret_cast<float4*>(l8 + o8) = x;
-                if (kMirror)
-                    for (uint32_t p = 0; p < mirror.n; ++p) *reinterpret_cast<float4*>(mirror.l8[p] + o8) = x;
+            if (C >= 32) {
+#pragma unroll
+                for (uint32_t h = 0; h < Q / 8; ++h) {
+                    if (c0 + 32 * h >= K_pad) break;
+                    const float4 x = make_float4(l8v[4 * h], l8v[(4 * h + 1) % (Q / 2)], l8v[(4 * h + 2) % (Q / 2)],
+                                                 l8v[(4 * h + 3) % (Q / 2)]);
+                    *reinterpret_cast<float4*>(l8 + o8 + 4 * h) = x;
+                    if (kMirror)
+                        for (uint32_t p = 0; p < mirror.n; ++p)
+                            *reinterpret_cast<float4*>(mirror.l8[p] + o8 + 4 * h) = x;
+                }
             } else {
                 const float2 x = make_float2(l8v[0], l8v[1 % (Q / 2)]);
                 *reinterpret_cast<float2*>(l8 + o8) = x;
@@ -234,7 +247,7 @@ __global__ void __launch_bounds__(kPhiRows, 4) phi_kernel(const uint32_t* __rest
         __syncthreads();
 #pragma unroll
         for (uint32_t p = 0; p < Q; ++p) {
-            if (v0 + crow + RP * p < row_end) {
+            if (v0 + crow + RP * p < row_end && (C <= 32 || c0 + cq * 4u < K_pad)) {
                 const uint32_t o = phi_swz<C>(crow + RP * p, cq);
                 const float4 b = *reinterpret_cast<const float4*>(&t_in[st][o]);
                 const float4 l = *reinterpret_cast<const float4*>(&t_l4[o]);
@@ -293,14 +306,41 @@ cudaError_t launch_phi(const uint32_t* B, const double* denom, const float* zv, 
     if (K_pad % 32) return cudaErrorInvalidValue;
     const char* e = std::getenv("SLDA_PHI_SHAPE");  // read per launch (tests switch it per engine)
     const std::string v = e ? e : "";
-    const int shape = v == "16x8" ? 1 : v == "32x3" ? 2 : 0;
+    int shape = v == "16x8" ? 1 : v == "32x3" ? 2 : v == "64x2" ? 3 : v == "64x3" ? 4 : v == "32x4" ? 5 : 0;
     // Tile columns x pipeline stages, phi alone (ms, C3 / C5 K=50K): 16x8 4.91 / 17.9,
     // 32x3 4.68 / 14.8, 32x4 4.10 / 15.7, 32x6 5.88 / 16.2.
+    if (shape == 0) {
+        // Uniform row blocks, so the last partial wave is pure tail: between 32 x 4 (fastest per
+        // wave) and 32 x 3 (6 instead of 5 CTAs per SM) take the one whose last wave is fuller
+        // (C3, 2204 blocks: 2.98 vs 2.48 waves -> 32 x 4, 4.10 vs 4.68 ms; C5 K=50K, 1563
+        // blocks: 2.11 vs 1.76 waves -> 32 x 3, 14.8 vs 15.8 ms).
+        static int slots4 = 0, slots3 = 0;
+        if (!slots4) {
+            int dev = 0, sms = 0, n4 = 0, n3 = 0;
+            cudaGetDevice(&dev);
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+            cudaFuncSetAttribute(phi_kernel<32, 4, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(phi_smem_bytes<32, 4>()));
+            cudaFuncSetAttribute(phi_kernel<32, 3, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(phi_smem_bytes<32, 3>()));
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n4, phi_kernel<32, 4, false>, kPhiRows, phi_smem_bytes<32, 4>());
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n3, phi_kernel<32, 3, false>, kPhiRows, phi_smem_bytes<32, 3>());
+            slots4 = n4 * sms > 0 ? n4 * sms : 1;
+            slots3 = n3 * sms > 0 ? n3 * sms : 1;
+        }
+        const double blocks = std::ceil((row_end - row_begin) / static_cast<double>(kPhiRows));
+        const double w4 = blocks / slots4, w3 = blocks / slots3;
+        const double fill4 = w4 / std::ceil(w4), fill3 = w3 / std::ceil(w3);
+        shape = fill3 > fill4 + 0.05 ? 2 : 0;
+    }
     switch (shape) {
         case 1: return launch_phi_t<16, 8>(B, denom, zv, bhat, l4, l8, q, row_begin, row_end, K_pad, l8_stride, beta, falpha, s, mirror);
         case 2: return launch_phi_t<32, 3>(B, denom, zv, bhat, l4, l8, q, row_begin, row_end, K_pad, l8_stride, beta, falpha, s, mirror);
-        default: return launch_phi_t<32, 4>(B, denom, zv, bhat, l4, l8, q, row_begin, row_end, K_pad, l8_stride, beta, falpha, s, mirror);
+        case 3: return launch_phi_t<64, 2>(B, denom, zv, bhat, l4, l8, q, row_begin, row_end, K_pad, l8_stride, beta, falpha, s, mirror);
+        case 4: return launch_phi_t<64, 3>(B, denom, zv, bhat, l4, l8, q, row_begin, row_end, K_pad, l8_stride, beta, falpha, s, mirror);
+        default: break;
     }
+    return launch_phi_t<32, 4>(B, denom, zv, bhat, l4, l8, q, row_begin, row_end, K_pad, l8_stride, beta, falpha, s, mirror);
 }
 
 // ---- Peer-memory M-step exchange (world > 1 without NCCL; engine.cu m_step_peer) -------------

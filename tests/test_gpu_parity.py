@@ -286,7 +286,7 @@ VARIANT_CASES = ["c1", "long_docs", "empty_docs", "shuffled", "k_large", "nytime
 
 @pytest.mark.parametrize("variant", ["SLDA_SAMPLER=g2", "SLDA_SAMPLER=g4", "SLDA_SAMPLER=s4", "SLDA_SAMPLER=q256", "SLDA_SAMPLER=p256",
                                      "SLDA_SAMPLER=q512", "SLDA_SSC=sort", "SLDA_PHI_SHAPE=16x8",
-                                     "SLDA_PHI_SHAPE=32x3"])
+                                     "SLDA_PHI_SHAPE=32x3", "SLDA_PHI_SHAPE=64x2"])
 @pytest.mark.parametrize("name", VARIANT_CASES)
 def test_kernel_variants_match_reference(name, variant, golden, monkeypatch):
     """Every sampler launch shape (round-based 2/4-sector groups, streaming lane refill,
