@@ -43,6 +43,8 @@ def _rank_main(rank, case, to_parent, from_parent):
         cfg.num_topics = spec["K"]
         cfg.seed = spec["seed"]
         cfg.device = 0
+        if spec.get("sampler") == "vanilla":
+            cfg.sampler = slda.SamplerKind.VANILLA
         m = core.init_view(toks, D, V, int(b), int(e), int(csum[b]), cfg, rank, WORLD, b"", 1)
         to_parent.put(("handles", rank, m.peer_handles()))
         all_handles = from_parent.get()
@@ -65,8 +67,8 @@ def _rank_main(rank, case, to_parent, from_parent):
         to_parent.put(("error", rank, traceback.format_exc()))
 
 
-def test_peer_memory_exchange_matches_reference(golden):
-    case = "c1"
+@pytest.mark.parametrize("case", ["c1", "vanilla_c1"])
+def test_peer_memory_exchange_matches_reference(golden, case):
     ctx = mp.get_context("spawn")
     to_parent = ctx.Queue()
     inboxes = [ctx.Queue() for _ in range(WORLD)]
@@ -92,7 +94,7 @@ def test_peer_memory_exchange_matches_reference(golden):
             if p.is_alive():
                 p.kill()
     fx = golden["cases"][case]
-    for it in range(ITERS + 1):
+    for it in range(min(ITERS, len(fx["iterations"]) - 1) + 1):
         r0, r1 = results[0][it], results[1][it]
         # Replicated state: identical on both ranks.
         for key in ("word_topic", "word_topic_prob", "l4", "tree_mass"):
