@@ -299,7 +299,9 @@ __device__ __forceinline__ uint32_t ssc_doc_bitmap(const uint32_t* key, uint32_t
     return nnz;
 }
 
-constexpr uint32_t kSscBmWarps = 8;
+// Warps per CTA (C3, SSC alone / whole iteration): 2 -> 6.22 / 99.85 ms, 4 -> 6.26 / 99.87,
+// 8 -> 6.45 / 100.16, 16 -> 6.57 / 100.40; smaller CTAs hand SMs back to the M-step sooner.
+constexpr uint32_t kSscBmWarps = 4;
 
 __host__ __device__ inline size_t ssc_bitmap_warp_bytes(uint32_t K_pad) {
     const size_t n0 = (K_pad + 31u) / 32u, n1 = (n0 + 31u) / 32u;
