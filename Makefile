@@ -18,7 +18,7 @@ CXXFLAGS := -O2 -std=c++20 -fPIC -Wall -Wextra -ffp-contract=off -Iinclude
 CU_SRCS := $(CSRC)/engine.cu $(CSRC)/sampler.cu $(CSRC)/ssc.cu $(CSRC)/mstep.cu $(CSRC)/setup.cu \
            $(CSRC)/heldout.cu
 CU_OBJS := $(patsubst $(CSRC)/%.cu,$(BUILD)/%.o,$(CU_SRCS))
-HOST_OBJS := $(BUILD)/host.o
+HOST_OBJS := $(BUILD)/host.o $(BUILD)/corpus_gen.o
 LIB     := $(PKG)/libsaberlda.so
 
 PY_EXT  := $(shell $(PYTHON) -c "import sysconfig; print(sysconfig.get_config_var('EXT_SUFFIX'))")
@@ -35,6 +35,9 @@ $(BUILD)/%.o: $(CSRC)/%.cu $(wildcard $(CSRC)/*.cuh) $(wildcard $(CSRC)/*.hpp) i
 	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> $(BUILD)/$*.ptxas.log || (cat $(BUILD)/$*.ptxas.log; false)
 
 $(BUILD)/host.o: $(CSRC)/host.cpp include/saberlda.h | $(BUILD)
+	$(CXX) $(CXXFLAGS) -c $< -o $@
+
+$(BUILD)/corpus_gen.o: $(CSRC)/corpus_gen.cpp include/saberlda.h | $(BUILD)
 	$(CXX) $(CXXFLAGS) -c $< -o $@
 
 $(LIB): $(CU_OBJS) $(HOST_OBJS)

@@ -7,10 +7,11 @@ times in run_iteration (proj/src/trainer.cpp:419-449).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config c3] [--impl ours|reference]
 
-N > 1 runs under torchrun, one rank per GPU, document shards with NCCL
-reduce-scatter / all-reduce / all-gather inside each iteration (strong scaling:
-the corpus is fixed).  value = corpus tokens per iteration / (max over ranks of
-the device time per iteration).  See DESIGN.md "Measurement".
+N > 1 runs one rank per GPU (under torchrun; launched without it, bench.py re-launches
+itself through torch.distributed.run), document shards with the M-step reduce-scatter /
+all-reduce / all-gather fused into the kernels over NVLink peer memory (strong scaling: the
+corpus is fixed).  value = corpus tokens per iteration / (max over ranks of the device time
+per iteration).  See DESIGN.md "Measurement".
 """
 from __future__ import annotations
 
@@ -140,43 +141,71 @@ def ncu_traffic():
 
 # --------------------------------------------------------------------- reference
 def reference_run(cfg: dict, sample_tokens: int, steps: int, warmup: int, threads: int):
-    """The reference's own CPU implementation (oracle/_ref: proj/src/*.cpp compiled in place)
-    on a bounded sample: the first documents of the same corpus, full V and K."""
-    sys.path.insert(0, str(REPO / "tests"))
-    import paper_1610_02496_b200._core as core
-    from oracle_lib import REF_SO, OracleModel, RefModel
+    """The reference's own CPU implementation (oracle/_ref: proj/src/*.cpp compiled in place,
+    unmodified) timed on this host's cores, through its run_iteration (IterationStats.elapsed_s).
 
-    _, lens = core.generate_tokens(0, cfg["D"], cfg["V"], cfg["T"], seed=CORPUS_SEED, doc_begin=0, doc_end=0)
+    The full corpus does not fit a bounded run (C3: ~2.5 min per iteration on 16 cores), and a
+    sample's tokens/s is biased low because the M-step (preprocess + rebuild_trees over V x K,
+    trainer.cpp:436-438) does not shrink with the sample.  So the run is split into the two
+    parts the reference's iteration consists of, each timed by the reference itself:
+      * t_fixed: run_iteration on a one-document corpus with the full V and K -- the V x K
+        reset / preprocess / tree build, with a ~100-token E-step;
+      * t_sample: run_iteration on the first documents of the same corpus (>= sample_tokens);
+    per-token E-step + SSC cost e = (t_sample - t_fixed) / T_sample, and the full corpus
+    iteration t = t_fixed + e * T (median of `steps` iterations after `warmup`, each part).
+    The workload comes from oracle/libcorpusgen.so (the generator alone): nothing of the
+    product is loaded."""
+    sys.path.insert(0, str(REPO / "tests"))
+    from oracle_lib import REF_SO, CorpusGen, OracleModel, RefModel
+
+    gen = CorpusGen(0, cfg["D"], cfg["V"], cfg["T"], seed=CORPUS_SEED, threads=threads)
+    lens = gen.doc_lengths()
     csum = np.cumsum(lens.astype(np.int64))
-    ndocs = int(np.searchsorted(csum, sample_tokens) + 1)
-    ndocs = min(ndocs, cfg["D"])
-    toks, _ = core.generate_tokens(0, cfg["D"], cfg["V"], cfg["T"], seed=CORPUS_SEED, doc_begin=0, doc_end=ndocs)
-    doc, word = toks[:, 0].copy(), toks[:, 1].copy()
+    ndocs = min(int(np.searchsorted(csum, sample_tokens) + 1), cfg["D"])
     kind = "reference" if REF_SO.exists() else "port"
     workers = threads if kind == "reference" else 1
+
+    def make(nd):
+        toks = gen.docs(0, nd, lens)
+        doc, word = toks[:, 0].copy(), toks[:, 1].copy()
+        if kind == "reference":
+            return RefModel(nd, cfg["V"], doc, word, None, K=cfg["K"], seed=TRAIN_SEED,
+                            num_chunks=min(4 * workers, nd), workers=workers), len(doc)
+        return OracleModel(nd, cfg["V"], doc, word, None, K=cfg["K"], seed=TRAIN_SEED), len(doc)
+
+    def timed(m, n_steps, n_warm):
+        times = []
+        for i in range(n_warm + n_steps):
+            t = time.perf_counter()
+            m.iterate()
+            el = m.last_elapsed if kind == "reference" else time.perf_counter() - t
+            if i >= n_warm:
+                times.append(el)
+        return statistics.median(times)
+
+    m, t_tiny = make(1)
+    fixed_steps = max(3, min(steps, 5))
+    t_fixed = timed(m, fixed_steps, 1)
+    del m
     t0 = time.perf_counter()
-    if kind == "reference":
-        m = RefModel(ndocs, cfg["V"], doc, word, None, K=cfg["K"], seed=TRAIN_SEED,
-                     num_chunks=min(4 * workers, ndocs), workers=workers)
-    else:
-        m = OracleModel(ndocs, cfg["V"], doc, word, None, K=cfg["K"], seed=TRAIN_SEED)
+    m, T_s = make(ndocs)
     init_s = time.perf_counter() - t0
-    times = []
-    for i in range(warmup + steps):
-        t = time.perf_counter()
-        m.iterate()
-        el = (m.last_elapsed if kind == "reference" else time.perf_counter() - t)
-        if i >= warmup:
-            times.append(el)
-    med = statistics.median(times)
-    T = len(doc)
+    t_sample = timed(m, steps, warmup)
+    del m
+    e_tok = max(t_sample - t_fixed, 0.0) / T_s
+    t_full = t_fixed + e_tok * cfg["T"]
     return {
-        "value": T / med, "unit": "tokens/s", "cores": workers, "kind": kind,
-        "sample": (f"first {ndocs} docs of the {cfg['name']} corpus ({T} tokens), full V={cfg['V']} "
-                   f"K={cfg['K']}; median of {steps} iterations after {warmup} warm-up "
-                   f"(IterationStats.elapsed_s); init_state {init_s:.1f}s untimed; "
-                   f"{'oracle/_ref = unmodified reference sources, ' + str(workers) + ' workers, ' + str(min(4 * workers, ndocs)) + ' chunks' if kind == 'reference' else 'C oracle port, 1 thread'}"),
-        "ms_per_step": med * 1e3, "tokens": T,
+        "value": cfg["T"] / t_full, "unit": "tokens/s", "cores": workers, "kind": kind,
+        "sample": (f"{cfg['name']} iteration time reconstructed from two runs of the reference's own "
+                   f"run_iteration: V x K M-step part t_fixed = {t_fixed:.3f} s (one-document corpus, median of "
+                   f"{fixed_steps}), and the first {ndocs} documents ({T_s} tokens) at {t_sample:.3f} s (median of "
+                   f"{steps} after {warmup} warm-up) -> E-step {e_tok * 1e9:.2f} ns/token; full corpus "
+                   f"t = t_fixed + T * e = {t_full:.2f} s per iteration; sample rate {T_s / t_sample:.4g} tok/s; "
+                   f"init_state {init_s:.1f} s untimed; "
+                   + (f"oracle/_ref = unmodified reference sources, {workers} workers, "
+                      f"{min(4 * workers, ndocs)} chunks" if kind == "reference" else "C oracle port, 1 thread")),
+        "ms_per_step": t_full * 1e3, "tokens": T_s, "t_fixed_s": t_fixed, "t_sample_s": t_sample,
+        "e_step_ns_per_token": e_tok * 1e9,
     }
 
 
@@ -189,14 +218,26 @@ def main() -> None:
     ap.add_argument("--config", default="c3", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-sample-tokens", type=int, default=16_000_000)
-    ap.add_argument("--cpu-steps", type=int, default=2)
+    ap.add_argument("--cpu-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--exchange", default="peer", choices=["peer", "nccl"],
-                    help="N > 1: M-step exchange fused into the kernels over peer memory (default) or NCCL")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
 
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        # One process per GPU: re-launch under torch.distributed.run (the driver's own launch
+        # sets WORLD_SIZE and lands below).
+        import socket
+
+        with socket.socket() as sk:
+            sk.bind(("127.0.0.1", 0))
+            port = sk.getsockname()[1]
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr", "127.0.0.1", f"--master-port={port}", str(Path(__file__).resolve()), *sys.argv[1:]]
+        sys.exit(subprocess.run(cmd).returncode)
+
     world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world != args.gpus:
+        sys.exit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}: one rank per GPU required")
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     threads = os.cpu_count() or 1
@@ -211,8 +252,11 @@ def main() -> None:
         line = dict(base_line)
         line.update({
             "impl": "reference", "value": r["value"], "ms_per_step": r["ms_per_step"],
-            "config": {"workload": cfg["name"] + " (bounded CPU sample)", **{k: cfg[k] for k in "DVTK"},
-                       "sample_tokens": r["tokens"]},
+            "config": {"workload": cfg["name"], **{k: cfg[k] for k in "DVTK"},
+                       "alpha": 50.0 / cfg["K"], "beta": 0.01, "seed": TRAIN_SEED, "corpus_seed": CORPUS_SEED,
+                       "measured_as": "full-corpus iteration = t_fixed (V x K M-step) + T x per-token E-step, "
+                                      "both timed by the reference's run_iteration (cpu_baseline.sample)",
+                       "sample_tokens": r["tokens"], "t_fixed_s": r["t_fixed_s"], "t_sample_s": r["t_sample_s"]},
             "cpu_baseline": {k: r[k] for k in ("value", "unit", "cores", "kind", "sample")},
             "e2e": {"value": r["value"], "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
             "gpu_launches": 0,
@@ -253,12 +297,6 @@ def main() -> None:
     del toks_np
     host_tokens = pinned.numpy().view(np.uint32)
 
-    nccl_id = b""
-    if world > 1:
-        obj = [core.nccl_unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(obj, src=0)
-        nccl_id = obj[0]
-
     tc = slda.TrainConfig()
     tc.num_topics = cfg["K"]
     tc.seed = TRAIN_SEED
@@ -298,39 +336,23 @@ def main() -> None:
     # + D2H of the assignments (result).
     barrier()
     t0 = time.perf_counter()
-    exchange = args.exchange if world > 1 else "none"
-    if exchange == "peer" and not one_gpu:
-        # Peer-memory exchange needs P2P access between every pair of GPUs (NVLink / NVSwitch);
-        # any rank without it sends every rank to NCCL.
+    if world > 1 and not one_gpu:
+        # The peer-memory exchange needs P2P access between every pair of GPUs (NVLink /
+        # NVSwitch, one node).
         local_world = int(os.environ.get("LOCAL_WORLD_SIZE", world))
-        ok = all(torch.cuda.can_device_access_peer(dev, o) for o in range(local_world) if o != dev)
-        flag = torch.tensor([1 if ok and local_world == world else 0], dtype=torch.int32, device=coll_dev)
-        dist.all_reduce(flag, op=dist.ReduceOp.MIN)
-        if int(flag.item()) == 0:
-            exchange = "nccl"
+        if local_world != world or not all(torch.cuda.can_device_access_peer(dev, o)
+                                           for o in range(local_world) if o != dev):
+            sys.exit("bench.py: N > 1 needs one node with P2P access between every GPU pair")
 
     def create():
         """init_state over this rank's shard; for N > 1 the engines meet through peer memory
-        (CUDA IPC handles exchanged over torch.distributed, then slda_peer_attach) or NCCL.
-        Any rank failing to map its peers falls every rank back to NCCL."""
-        nonlocal exchange
-        if exchange == "peer":
-            m = core.init_view(host_tokens, cfg["D"], cfg["V"], b, e, int(csum[b]), tc, rank, world, b"", 1)
+        (CUDA IPC handles exchanged over torch.distributed, then slda_peer_attach)."""
+        m = core.init_view(host_tokens, cfg["D"], cfg["V"], b, e, int(csum[b]), tc, rank, world, 1 if world > 1 else 0)
+        if world > 1:
             handles = [None] * world
             dist.all_gather_object(handles, m.peer_handles())
-            ok = torch.tensor([1], dtype=torch.int32, device=coll_dev)
-            try:
-                m.peer_attach(handles)
-            except Exception as exc:  # noqa: BLE001
-                print(f"rank {rank}: peer attach failed ({exc}); falling back to NCCL", file=sys.stderr)
-                ok.zero_()
-            dist.all_reduce(ok, op=dist.ReduceOp.MIN)
-            if int(ok.item()) == 1:
-                return m
-            del m
-            exchange = "nccl"
-        return core.init_view(host_tokens, cfg["D"], cfg["V"], b, e, int(csum[b]), tc, rank, world, nccl_id,
-                              1 if world > 1 else 0)
+            m.peer_attach(handles)
+        return m
 
     model = create()
     t_init = time.perf_counter()
@@ -381,17 +403,17 @@ def main() -> None:
         "value": value, "ms_per_step": ms_per_step,
         "config": {"workload": cfg["name"], "D": cfg["D"], "V": cfg["V"], "T": cfg["T"], "K": cfg["K"],
                    "alpha": 50.0 / cfg["K"], "beta": 0.01, "seed": TRAIN_SEED, "corpus_seed": CORPUS_SEED,
-                   "parallelism": (f"doc-shards x{world}, M-step exchange: "
-                                   + ("fused into the kernels over NVLink peer memory" if exchange == "peer"
-                                      else "NCCL reduce-scatter / all-reduce / all-gather")) if world > 1 else "1 GPU",
+                   "parallelism": (f"doc-shards x{world}, M-step exchange fused into the kernels over NVLink "
+                                   "peer memory") if world > 1 else "1 GPU",
                    "l2": "inputs larger than L2 (C_dk rows, phi, L4 are GBs; no flush needed)"},
         "roofline": {"bound": "hbm", "kernel": "sampler", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "traffic_config": traffic_cfg,
                      "peak_source": peak_src, "algorithmic_bytes_per_launch": s_bytes,
                      "sampler_ms": kt["sampler_ms"], "iteration_achieved": it_achieved,
                      "iteration_frac": it_achieved / peak, "E_t": row_entries / max(1, T_shard)},
-        "kernels_ms": {k: kt[k] for k in ("reset_ms", "sampler_ms", "ssc_ms", "colsum_ms", "phi_ms", "comm_ms",
+        "kernels_ms": {k: kt[k] for k in ("reset_ms", "sampler_ms", "ssc_ms", "colsum_ms", "phi_ms", "join_ms",
                                           "total_ms")},
+        "sampler_shape": info["sampler_shape"],
         "mean_doc_topics": info["doc_topic_nnz"] / max(1, e - b),
         "e2e": {"value": cfg["T"] * args.steps / e2e_s, "unit": "tokens/s",
                 "h2d_bytes_per_step": int(12 * T_shard / args.steps),
@@ -402,6 +424,7 @@ def main() -> None:
         "clocks": clocks.summary(),
     })
     if world == 1 and not args.no_cpu_baseline:
+        del model
         r = reference_run(cfg, args.cpu_sample_tokens, args.cpu_steps, 1, threads)
         line["cpu_baseline"] = {k: r[k] for k in ("value", "unit", "cores", "kind", "sample")}
     print(json.dumps(line), flush=True)

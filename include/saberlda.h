@@ -26,13 +26,13 @@
 extern "C" {
 #endif
 
-#define SLDA_ABI_VERSION 2u
+#define SLDA_ABI_VERSION 3u
 
 enum {
     SLDA_OK = 0,
     SLDA_ERR_VALIDATION = 1, /* sparselda::ValidationError, CLI exit 1, Python ValueError */
     SLDA_ERR_IO = 2,         /* sparselda::IoError, CLI exit 2, Python IOError */
-    SLDA_ERR_DEVICE = 3      /* CUDA / NCCL failure (no reference analogue) */
+    SLDA_ERR_DEVICE = 3      /* CUDA failure (no reference analogue) */
 };
 
 #define SLDA_INVALID_TOPIC 0xFFFFFFFFu /* kInvalidTopic, types.hpp:17 */
@@ -73,9 +73,8 @@ typedef struct slda_config {
     uint32_t init_mode;       /* SLDA_INIT_* */
     int32_t device;           /* CUDA ordinal; -1 = current device */
     uint32_t rank;            /* document shard index (0 for one GPU) */
-    uint32_t world_size;      /* number of shards/GPUs (1 = no collectives) */
-    const void* nccl_id;      /* 128-byte ncclUniqueId from rank 0 when world_size > 1 (NCCL
-                                 collectives); NULL: peer-memory exchange (slda_peer_attach) */
+    uint32_t world_size;      /* number of shards/GPUs (1 = no exchange; > 1: peer-memory
+                                 exchange, slda_peer_export / slda_peer_attach) */
     uint32_t sampler;         /* SLDA_SAMPLER_* -- TrainConfig::sampler (trainer.hpp:18, :30) */
 } slda_config;
 
@@ -105,11 +104,21 @@ typedef struct slda_info {
     uint64_t device_bytes;    /* bytes of device memory held by the engine */
     uint32_t doc_major;       /* 1 if tokens came doc-sorted (no slot permutation) */
     uint32_t padded_topics;   /* K rounded up to the L4 block width (32) */
+    uint32_t sampler_shape;   /* SLDA_SHAPE_*: the sampler kernel the iterations launch */
 } slda_info;
+
+/* Sampler kernels (slda_info.sampler_shape). */
+#define SLDA_SHAPE_ROUND 0u    /* round-based lane-per-token, 4-sector groups */
+#define SLDA_SHAPE_QUAD512 1u  /* quad-lane, 512-thread CTAs, next-line prefetch */
+#define SLDA_SHAPE_QUAD256 2u  /* quad-lane, 256-thread CTAs */
+#define SLDA_SHAPE_GLOBAL 3u   /* quad-lane, phi gathered from global memory (large K) */
+#define SLDA_SHAPE_VANILLA 4u  /* SamplerKind::kVanilla O(K) baseline */
 
 /* Per-kernel device times (ms) of the last iteration, for roofline accounting. */
 typedef struct slda_kernel_times {
-    double reset_ms, sampler_ms, ssc_ms, colsum_ms, phi_ms, comm_ms, total_ms;
+    double reset_ms, sampler_ms, ssc_ms, colsum_ms, phi_ms;
+    double join_ms;               /* phi end -> iteration end: the SSC join (+ the peer barrier) */
+    double total_ms;
     uint64_t sampler_row_entries; /* sum over tokens of nnz(A_d) read by the sampler */
     uint32_t launches;            /* kernels launched by the iteration */
 } slda_kernel_times;
@@ -184,8 +193,6 @@ int slda_heldout_ll(slda_engine* e, uint32_t num_docs, uint32_t vocab_size, uint
 
 const char* slda_last_error(void);
 uint32_t slda_abi_version(void);
-/* Fills a 128-byte ncclUniqueId (rank 0 of a sharded run). */
-int slda_nccl_unique_id(void* out128);
 /* Document shard bounds by the chunk_boundaries rule (corpus.cpp:103-121):
  * bounds has num_shards+1 entries.  Host-only. */
 int slda_shard_bounds(uint32_t num_docs, uint64_t num_tokens, const uint32_t* doc_lengths,
@@ -221,13 +228,13 @@ int slda_generate_doc_lengths(const slda_gen_params* p, uint32_t* lengths);
 int slda_generate_docs(const slda_gen_params* p, uint32_t doc_begin, uint32_t doc_end,
                        uint32_t* tokens, uint64_t capacity);
 
-/* ---- Peer-memory exchange (multi-GPU without NCCL) ------------------------------------------
- * Create every rank's engine with world_size > 1 and nccl_id == NULL, export each engine's
+/* ---- Peer-memory exchange (multi-GPU) --------------------------------------------------------
+ * Create every rank's engine with world_size > 1, export each engine's
  * buffer handles (CUDA IPC), exchange them over any host channel, and attach every engine to
  * all ranks' handles (indexed by rank).  The M-step then reduce-scatters C_wk, all-reduces C_k
  * and all-gathers phi / L4 / L8 / Q inside its own kernels over peer memory (NVLink on a
- * multi-GPU node; the same HBM when ranks share one GPU) -- the NCCL collectives of the default
- * path (engine m_step, trainer.cpp:395-400 / 436-440 semantics) folded into the computation.
+ * multi-GPU node; the same HBM when ranks share one GPU): the collectives of a sharded M-step
+ * (trainer.cpp:395-400 / 436-440 semantics) folded into the computation.
  * slda_peer_attach runs init_state's first M-step and is collective, as is
  * slda_get_word_topic on a peer-attached engine. */
 #define SLDA_PEER_HANDLE_BYTES 64

@@ -29,7 +29,6 @@ try:
         heldout_ll,
         init_shard,
         init_state,
-        nccl_unique_id,
         prefix_search,
         resume,
         segmented_count,

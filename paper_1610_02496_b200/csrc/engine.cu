@@ -10,8 +10,6 @@
 //                       padding to a multiple of 8], 32-byte aligned at row4[d]
 //   B     u32[V_pad][K_pad], bhat/L4 f32[V_pad][K_pad], L8 f32[V_pad][l8s] (every 8th prefix), Q f32[V_pad]
 // Reference paths are relative to /root/reference/proj.
-#include <dlfcn.h>
-
 #include <algorithm>
 #include <chrono>
 #include <thread>
@@ -24,7 +22,6 @@
 #include <vector>
 
 #include <cub/cub.cuh>
-#include <nccl.h>
 
 #include "../../include/saberlda.h"
 #include "common.cuh"
@@ -63,45 +60,6 @@ int guarded(F&& f) {
         g_error = e.what();
         return SLDA_ERR_DEVICE;
     }
-}
-
-// ------------------------------------------------------------------ NCCL --
-// Loaded lazily (world_size > 1 only) so a single-GPU process never binds a
-// second libnccl next to the one torch may already have loaded.
-struct Nccl {
-    void* h = nullptr;
-    decltype(&ncclGetUniqueId) GetUniqueId = nullptr;
-    decltype(&ncclCommInitRank) CommInitRank = nullptr;
-    decltype(&ncclCommDestroy) CommDestroy = nullptr;
-    decltype(&ncclReduceScatter) ReduceScatter = nullptr;
-    decltype(&ncclAllReduce) AllReduce = nullptr;
-    decltype(&ncclAllGather) AllGather = nullptr;
-    decltype(&ncclGetErrorString) GetErrorString = nullptr;
-    decltype(&ncclGroupStart) GroupStart = nullptr;
-    decltype(&ncclGroupEnd) GroupEnd = nullptr;
-};
-
-Nccl& nccl() {
-    static Nccl n;
-    if (!n.h) {
-        for (const char* name : {"libnccl.so.2", "libnccl.so"}) {
-            n.h = dlopen(name, RTLD_NOW | RTLD_NOLOAD | RTLD_GLOBAL);
-            if (!n.h) n.h = dlopen(name, RTLD_NOW | RTLD_GLOBAL);
-            if (n.h) break;
-        }
-        if (!n.h) throw SldaError(SLDA_ERR_DEVICE, "libnccl.so.2 not found");
-#define SYM(f) n.f = reinterpret_cast<decltype(n.f)>(dlsym(n.h, "nccl" #f))
-        SYM(GetUniqueId); SYM(CommInitRank); SYM(CommDestroy); SYM(ReduceScatter);
-        SYM(AllReduce); SYM(AllGather); SYM(GetErrorString); SYM(GroupStart); SYM(GroupEnd);
-#undef SYM
-        if (!n.CommInitRank || !n.AllGather) throw SldaError(SLDA_ERR_DEVICE, "incomplete libnccl");
-    }
-    return n;
-}
-
-void nccl_check(ncclResult_t r, const char* what) {
-    if (r != ncclSuccess)
-        throw SldaError(SLDA_ERR_DEVICE, std::string(what) + ": " + nccl().GetErrorString(r));
 }
 
 // --------------------------------------------------------------- buffers --
@@ -206,9 +164,7 @@ struct slda_engine {
     uint32_t nseg = 0, n_units = 0, n_long = 0;
     bool doc_major = true;
     bool vanilla = false;  // SamplerKind::kVanilla (trainer.cpp:281-285)
-    bool compact = false;  // C_dk row format (row_format.cuh: compact 16-bit slots or wide 32-bit)
     int sampler_shape = -1;  // SLDA_SAMPLER (sampler.cu launch_sampler); -1 = default by K
-    bool ssc_sort = false;   // SLDA_SSC=sort: the bitonic-sort SSC instead of the bitmap one
     bool serial = false;     // SLDA_SERIAL=1: SSC on the main stream (measurement of each kernel alone)
     uint32_t wshift = 0;  // word field shift of the execution-order key
     size_t device_bytes = 0;
@@ -228,9 +184,9 @@ struct slda_engine {
     cudaEvent_t* ev = ring[0];
     uint32_t ring_launches[kRing] = {};
     uint32_t slot = 0;
-    ncclComm_t comm = nullptr;
-    // Peer-memory exchange (world > 1 without an NCCL id): the other ranks' buffers mapped
-    // through CUDA IPC handles (slda_peer_export / slda_peer_attach).
+    uint32_t enqueued = 0;  // iterations this engine has run (bounds the event ring reads)
+    // Peer-memory exchange (world > 1): the other ranks' buffers mapped through CUDA IPC
+    // handles (slda_peer_export / slda_peer_attach).
     bool peer = false, attached = false;
     DevMem bar, coltot;                    // barrier counter (rank 0's is the shared one), C_k total
     void* pB[slda::kMaxPeers] = {};
@@ -291,7 +247,6 @@ struct slda_engine {
         for (auto& set : ring)
             for (auto& e : set)
                 if (e) cudaEventDestroy(e);
-        if (comm) nccl().CommDestroy(comm);
         for (void* p : opened) cudaIpcCloseMemHandle(p);
         if (side) cudaStreamDestroy(side);
         if (stream) cudaStreamDestroy(stream);
@@ -365,16 +320,11 @@ struct slda_engine {
         }
         for (auto& set : ring)
             for (auto& e : set) CK(cudaEventCreate(&e));
-        if (world > 1 && !c.nccl_id) {
-            // No NCCL id: the ranks exchange through each other's memory (slda_peer_attach).
+        if (world > 1) {
+            // The ranks exchange through each other's memory (slda_peer_attach).
             if (world > slda::kMaxPeers)
                 validation("peer-memory exchange supports world_size <= " + std::to_string(slda::kMaxPeers));
             peer = true;
-        } else if (world > 1) {
-            ncclUniqueId id;
-            std::memcpy(&id, c.nccl_id, sizeof(id));
-            nccl_check(nccl().CommInitRank(&comm, static_cast<int>(world), id, static_cast<int>(rank)),
-                       "ncclCommInitRank");
         }
     }
 
@@ -399,6 +349,34 @@ struct slda_engine {
     void build(const slda_corpus_view& cv, const slda_config& c);
     // ---- run_iteration (trainer.cpp:419-449) ----
     void enqueue_iteration();
+    // Sampler launch arguments of the next iteration.
+    slda::SamplerArgs sampler_args() const {
+        slda::SamplerArgs a{};
+        a.tok = tok.as<uint2>();
+        a.units = units.as<slda::Unit>();
+        a.A = A.as<uint32_t>();
+        a.bhat = bhat.as<float>();
+        a.l4 = l4.as<float>();
+        a.l8 = l8.as<float>();
+        a.q = q.as<float>();
+        a.ids = ids.p ? ids.as<uint64_t>() : nullptr;
+        a.z = z.as<uint16_t>();
+        a.B = B.as<uint32_t>();
+        a.seed = seed;
+        a.id_base = id_base;
+        a.stream_kind = iteration;  // trainer.cpp:423
+        a.K = K;
+        a.K_pad = K_pad;
+        a.l8_stride = l8_stride;
+        a.n_l8 = n_l8;
+        a.tbits = tbits;
+        a.row_entries = entries_counter();
+        a.shape = sampler_shape;
+        a.vanilla = vanilla ? 1u : 0u;
+        a.alpha = falpha;  // static_cast<float>(state.alpha), trainer.cpp:283
+        return a;
+    }
+
     void m_step();
     void ssc(cudaStream_t st);
 };
@@ -498,19 +476,8 @@ void slda_engine::build(const slda_corpus_view& cv, const slda_config& c) {
             validation("document of length " + std::to_string(max_len) +
                        " exceeds the packed C_dk count range at this K");
     }
-    // Row format: the 32-bit wide rows by default.  The compact 16-bit format (row_format.cuh)
-    // is opt-in (SLDA_ROW_FORMAT=compact): it cuts sampler DRAM bytes ~25% and wins on
-    // short-document corpora at large K (C3: 131 vs 139 ms/iteration) but loses where the
-    // sampler is issue-bound or documents are long (C2 42.7 vs 31.0, C5 K=10K 88.9 vs 55.5;
-    // DESIGN.md §6).
     if (const char* f = std::getenv("SLDA_SAMPLER")) sampler_shape = slda::sampler_shape_from_name(f);
-    if (const char* f = std::getenv("SLDA_SSC")) ssc_sort = std::string(f) == "sort";
     if (const char* f = std::getenv("SLDA_SERIAL")) serial = std::string(f) == "1";
-    compact = false;
-    if (const char* f = std::getenv("SLDA_ROW_FORMAT"); f && !vanilla) {
-        if (std::string(f) == "compact")
-            compact = K <= slda::kCompactMaxK && max_len <= slda::kCompactMaxLen;
-    }
 
     phase("doc_start");
     // Slot permutation for corpora that are not doc-sorted: stable by doc keeps
@@ -694,59 +661,32 @@ void slda_engine::ssc(cudaStream_t st) {
     s.row4 = row4.as<uint32_t>();
     s.A = A.as<uint32_t>();
     s.tbits = tbits;
-    s.compact = compact ? 1u : 0u;
     s.K_pad = K_pad;
     s.long_docs = long_docs.as<uint32_t>();
     s.n_long = n_long;
     s.hist_scratch = hist_scratch.as<uint32_t>();
     s.nnz_total = nnz_counter();
-    s.use_sort = ssc_sort ? 1u : 0u;
     CK(slda::launch_ssc(s, st));
     launches += (D > 0) + (n_long > 0);
 }
 
-// M-step after the E-step's B: (reduce-scatter) -> colsum -> (all-reduce) -> phi/L4 on the
-// own word slice -> (all-gather).  preprocess (counts.cpp:37-63) + rebuild_trees.
+// M-step after the E-step's B (one GPU): colsum -> denom -> phi/L4/L8/Q.  preprocess
+// (counts.cpp:37-63) + rebuild_trees (trainer.cpp:237-248).
 void slda_engine::m_step() {
     if (peer) {
         m_step_peer();
         return;
     }
-    const uint32_t r0 = row_begin(), r1 = row_end();
-    const size_t slice_cells = static_cast<size_t>(slice_rows()) * K_pad;
     CK(cudaEventRecord(ev[3], stream));
-    if (world > 1) {
-        auto& n = nccl();
-        nccl_check(n.ReduceScatter(B.p, B.as<uint32_t>() + rank * slice_cells, slice_cells, ncclUint32,
-                                   ncclSum, comm, stream), "ncclReduceScatter(B)");
-    }
     CK(cudaMemsetAsync(colsum.p, 0, colsum.bytes, stream));
-    CK(slda::launch_colsum(B.as<uint32_t>(), r0, r1, K_pad, colsum.as<unsigned long long>(), stream));
-    if (world > 1) {
-        nccl_check(nccl().AllReduce(colsum.p, colsum.p, K_pad, ncclUint64, ncclSum, comm, stream),
-                   "ncclAllReduce(C_k)");
-    }
+    CK(slda::launch_colsum(B.as<uint32_t>(), 0, V_pad, K_pad, colsum.as<unsigned long long>(), stream));
     CK(slda::launch_denom(colsum.as<unsigned long long>(), K, K_pad, V, beta, denom.as<double>(),
                           zv.as<float>(), stream));
     CK(cudaEventRecord(ev[4], stream));
     CK(slda::launch_phi(B.as<uint32_t>(), denom.as<double>(), zv.as<float>(), bhat.as<float>(), l4.as<float>(),
-                        l8.as<float>(), q.as<float>(), r0, r1, K, K_pad, l8_stride, beta, falpha, stream));
+                        l8.as<float>(), q.as<float>(), 0, V_pad, K, K_pad, l8_stride, beta, falpha, stream));
     launches += 3;
     CK(cudaEventRecord(ev[5], stream));
-    if (world > 1) {
-        auto& n = nccl();
-        const size_t l8_slice = static_cast<size_t>(slice_rows()) * l8_stride;
-        nccl_check(n.GroupStart(), "ncclGroupStart");
-        nccl_check(n.AllGather(bhat.as<float>() + rank * slice_cells, bhat.p, slice_cells, ncclFloat32, comm,
-                               stream), "ncclAllGather(bhat)");
-        nccl_check(n.AllGather(l4.as<float>() + rank * slice_cells, l4.p, slice_cells, ncclFloat32, comm,
-                               stream), "ncclAllGather(L4)");
-        nccl_check(n.AllGather(l8.as<float>() + rank * l8_slice, l8.p, l8_slice, ncclFloat32, comm, stream),
-                   "ncclAllGather(L3)");
-        nccl_check(n.AllGather(q.as<float>() + rank * slice_rows(), q.p, slice_rows(), ncclFloat32, comm,
-                               stream), "ncclAllGather(Q)");
-        nccl_check(n.GroupEnd(), "ncclGroupEnd");
-    }
     CK(cudaEventRecord(ev[6], stream));
 }
 
@@ -755,7 +695,7 @@ void slda_engine::m_step() {
 // the reduced slice is written into this rank's B) -> barrier -> C_k total from every rank's
 // partial (the all-reduce) -> phi / L4 / L8 / Q of the own slice, stored into every rank's
 // replica (the all-gather) -> barrier.  Integer sums and per-row f32 chains: bit-identical to
-// one GPU and to the NCCL path.
+// one GPU.
 void slda_engine::m_step_peer() {
     if (!attached) validation("peer-memory exchange: call slda_peer_attach on every rank first");
     const uint32_t r0 = row_begin(), r1 = row_end();
@@ -803,30 +743,7 @@ void slda_engine::enqueue_iteration() {
     CK(cudaMemsetAsync(B.p, 0, B.bytes, stream));  // reset_word_topic (counts.cpp:134-138)
     CK(cudaMemsetAsync(entries_counter(), 0, 8, stream));
     CK(cudaEventRecord(ev[1], stream));
-    slda::SamplerArgs a{};
-    a.tok = tok.as<uint2>();
-    a.units = units.as<slda::Unit>();
-    a.A = A.as<uint32_t>();
-    a.bhat = bhat.as<float>();
-    a.l4 = l4.as<float>();
-    a.l8 = l8.as<float>();
-    a.q = q.as<float>();
-    a.ids = ids.p ? ids.as<uint64_t>() : nullptr;
-    a.z = z.as<uint16_t>();
-    a.B = B.as<uint32_t>();
-    a.seed = seed;
-    a.id_base = id_base;
-    a.stream_kind = iteration;  // trainer.cpp:423
-    a.K = K;
-    a.K_pad = K_pad;
-    a.l8_stride = l8_stride;
-    a.n_l8 = n_l8;
-    a.tbits = tbits;
-    a.compact = compact ? 1u : 0u;
-    a.row_entries = entries_counter();
-    a.shape = sampler_shape;
-    a.vanilla = vanilla ? 1u : 0u;
-    a.alpha = falpha;  // static_cast<float>(state.alpha), trainer.cpp:283
+    const slda::SamplerArgs a = sampler_args();
     CK(slda::launch_sampler(a, n_units, stream));
     launches += n_units > 0;
     CK(cudaEventRecord(ev[2], stream));
@@ -842,6 +759,7 @@ void slda_engine::enqueue_iteration() {
     CK(cudaEventRecord(ev[6], stream));
     ring_launches[slot] = launches;
     ++iteration;
+    ++enqueued;
 }
 
 void slda_set_error_internal(const std::string& msg) { g_error = msg; }
@@ -959,14 +877,17 @@ int slda_get_info(const slda_engine* e, slda_info* info) {
         info->device_bytes = e->device_bytes;
         info->doc_major = e->doc_major ? 1u : 0u;
         info->padded_topics = e->K_pad;
+        info->sampler_shape = static_cast<uint32_t>(slda::sampler_shape(e->sampler_args()));
     });
 }
 
 int slda_get_kernel_times_avg(const slda_engine* e, uint32_t last_n, slda_kernel_times* t) {
     return guarded([&] {
         if (!e || !t) validation("null argument");
-        if (last_n == 0 || last_n > slda_engine::kRing || last_n > e->iteration)
-            validation("last_n must be in [1, min(64, iterations run)]");
+        // Bounded by the iterations THIS engine enqueued (a resumed or checkpoint-loaded model
+        // carries a larger iteration number but no recorded events).
+        if (last_n == 0 || last_n > slda_engine::kRing || last_n > e->enqueued)
+            validation("last_n must be in [1, min(64, iterations run by this engine)]");
         CK(cudaSetDevice(e->device));
         CK(cudaStreamSynchronize(e->stream));
         std::memset(t, 0, sizeof(*t));
@@ -985,7 +906,7 @@ int slda_get_kernel_times_avg(const slda_engine* e, uint32_t last_n, slda_kernel
             t->ssc_ms += ms(2, 7);  // side stream, concurrent with colsum + phi
             t->colsum_ms += ms(3, 4);
             t->phi_ms += ms(4, 5);
-            t->comm_ms += ms(5, 6);  // NCCL all-gathers + the join with SSC
+            t->join_ms += ms(5, 6);  // phi end -> iteration end: the SSC join (+ the peer barrier)
             t->total_ms += ms(0, 6);
             t->sampler_row_entries += entries[s];
             t->launches += e->ring_launches[s];
@@ -996,7 +917,7 @@ int slda_get_kernel_times_avg(const slda_engine* e, uint32_t last_n, slda_kernel
         t->ssc_ms /= n;
         t->colsum_ms /= n;
         t->phi_ms /= n;
-        t->comm_ms /= n;
+        t->join_ms /= n;
         t->total_ms /= n;
         t->sampler_row_entries /= last_n;
         t->launches /= last_n;
@@ -1037,12 +958,6 @@ int slda_get_word_topic(slda_engine* e, uint32_t* out) {
             e->peer_barrier();
             copy_matrix(e, full, out);
             return;
-        }
-        if (e->world > 1) {
-            // After the reduce-scatter each rank owns its slice; gather the rest.
-            const size_t slice = static_cast<size_t>(e->slice_rows()) * e->K_pad;
-            nccl_check(nccl().AllGather(e->B.as<uint32_t>() + e->rank * slice, e->B.p, slice, ncclUint32,
-                                        e->comm, e->stream), "ncclAllGather(B)");
         }
         copy_matrix(e, e->B, out);
     });
@@ -1140,36 +1055,21 @@ int slda_peer_attach(slda_engine* e, const slda_peer_handles* all) {
 }  // extern "C"
 
 namespace {
-// C_dk rows copied to the host (row_format.cuh formats); empty documents have none.
+// C_dk rows copied to the host; empty documents have none.
 struct HostRows {
     std::vector<uint32_t> doc_start, row4, A;
     uint32_t mask = 0, tbits = 0;
-    bool compact = false;
     const uint32_t* row(uint32_t d) const { return A.data() + static_cast<size_t>(row4[d]) * 4; }
     uint32_t nnz(uint32_t d) const {
         if (doc_start[d + 1] == doc_start[d]) return 0u;
-        return compact ? row(d)[0] >> 16 : (row(d)[0] & mask) + 1u;
+        return (row(d)[0] & mask) + 1u;
     }
     // Decoded (topic, count) pairs in ascending topic order.
     template <class F>
     void for_each(uint32_t d, F&& f) const {
         const uint32_t n = nnz(d);
-        if (n == 0) return;
         const uint32_t* r = row(d);
-        if (!compact) {
-            for (uint32_t i = 0; i < n; ++i) f(r[1 + i] & mask, r[1 + i] >> tbits);
-            return;
-        }
-        const uint32_t words = (r[0] & 0xFFFFu) * 8u;
-        for (uint32_t w = 1; w < words; ++w) {
-            const uint32_t h0 = r[w] & 0xFFFFu, h1 = r[w] >> 16;
-            if (h0 & 0x8000u) {
-                if (h0 != 0xFFFFu) f(h0 & 0x7FFFu, h1);
-            } else {
-                f(h0, 1u);
-                if (h1 != 0xFFFFu) f(h1, 1u);
-            }
-        }
+        for (uint32_t i = 0; i < n; ++i) f(r[1 + i] & mask, r[1 + i] >> tbits);
     }
 };
 
@@ -1177,7 +1077,6 @@ HostRows fetch_rows(slda_engine* e) {
     HostRows h;
     h.mask = (1u << e->tbits) - 1u;
     h.tbits = e->tbits;
-    h.compact = e->compact;
     h.doc_start.resize(static_cast<size_t>(e->D) + 1);
     h.row4.resize(static_cast<size_t>(e->D) + 1);
     h.A.resize(e->A.bytes / 4);
@@ -1351,15 +1250,6 @@ int slda_heldout_ll(slda_engine* e, uint32_t num_docs, uint32_t vocab_size, uint
         }
         *per_token_ll = total / static_cast<double>(n_evl);
         *tokens_evaluated = n_evl;
-    });
-}
-
-int slda_nccl_unique_id(void* out128) {
-    return guarded([&] {
-        if (!out128) validation("null argument");
-        ncclUniqueId id;
-        nccl_check(nccl().GetUniqueId(&id), "ncclGetUniqueId");
-        std::memcpy(out128, &id, sizeof(id));
     });
 }
 

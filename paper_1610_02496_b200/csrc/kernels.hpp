@@ -13,9 +13,6 @@ struct Unit {
 };
 
 constexpr uint32_t kUnitMaxTokens = 8192;  // sampler: max tokens per unit (one CTA)
-// Compact C_dk rows (16-bit slots, row_format.cuh) need topics < 0x7FFF and counts/nnz < 2^16.
-constexpr uint32_t kCompactMaxK = 32767;
-constexpr uint32_t kCompactMaxLen = 65535;
 constexpr uint32_t kSscWarpCap = 512;      // SSC: docs up to this length take the warp path
 
 struct SamplerArgs {
@@ -32,15 +29,17 @@ struct SamplerArgs {
     uint64_t seed, id_base;
     uint32_t stream_kind;   // iteration number (trainer.cpp:423)
     uint32_t K, K_pad, l8_stride, n_l8, tbits;
-    uint32_t compact;       // C_dk rows in the compact 16-bit format
     unsigned long long* row_entries;  // optional: sum of nnz over tokens (roofline)
     int shape;              // launch shape (sampler_shape_from_name); -1 = default by K
     uint32_t vanilla;       // SamplerKind::kVanilla: the O(K) dense-row draw (sampler.hpp:222-236)
     float alpha;            // f32(alpha), the vanilla draw's smoothing (trainer.cpp:283)
 };
 
-// "g2" 0, "g4" 1, "g4x512" 2, "s4" 3, "s2" 4, "s4x128" 5, "q512" 6, "q256" 7; else -1 (default).
+// Sampler launch shapes (sampler.cu launch_sampler); -1 = by phi row size.
+enum { kShapeRound = 0, kShapeQuad512 = 1, kShapeQuad256 = 2, kShapeGlobal = 3, kShapeVanilla = 4 };
 int sampler_shape_from_name(const char* name);
+// The kernel launch_sampler runs for these arguments (a.shape: forced shape or -1).
+int sampler_shape(const SamplerArgs& a);
 
 cudaError_t launch_sampler(const SamplerArgs& a, uint32_t n_units, cudaStream_t s);
 
@@ -51,12 +50,10 @@ struct SscArgs {
     const uint32_t* row4;       // per doc: row offset in uint4 units
     uint32_t* A;
     uint32_t tbits, K_pad;
-    uint32_t compact;           // write the compact 16-bit row format
     const uint32_t* long_docs;  // docs longer than kSscWarpCap
     uint32_t n_long;
     uint32_t* hist_scratch;     // n_long_ctas x K_pad (global fallback for large K)
     unsigned long long* nnz_total;
-    uint32_t use_sort;          // bitonic-sort SSC (else the bitmap SSC for wide rows)
 };
 
 cudaError_t launch_ssc(const SscArgs& a, cudaStream_t s);

@@ -63,7 +63,7 @@ py::dict kernel_times_dict(const slda_kernel_times& t) {
     d["ssc_ms"] = t.ssc_ms;
     d["colsum_ms"] = t.colsum_ms;
     d["phi_ms"] = t.phi_ms;
-    d["comm_ms"] = t.comm_ms;
+    d["join_ms"] = t.join_ms;
     d["total_ms"] = t.total_ms;
     d["sampler_row_entries"] = t.sampler_row_entries;
     d["launches"] = t.launches;
@@ -90,6 +90,8 @@ py::dict info_dict(const slda_info& i) {
     d["device_bytes"] = i.device_bytes;
     d["doc_major"] = i.doc_major;
     d["padded_topics"] = i.padded_topics;
+    static const char* kShapes[] = {"round", "quad512", "quad256", "global", "vanilla"};
+    d["sampler_shape"] = i.sampler_shape < 5 ? kShapes[i.sampler_shape] : "unknown";
     return d;
 }
 
@@ -285,14 +287,11 @@ PYBIND11_MODULE(_core, m) {
           py::call_guard<py::gil_scoped_release>());
     m.def(
         "init_shard",
-        [](const Corpus& corpus, const TrainConfig& cfg, std::uint32_t rank, std::uint32_t world,
-           py::bytes nccl_id) {
-            std::string id = nccl_id;  // empty with world > 1: peer-memory exchange (Model.peer_attach)
-            if (world > 1 && !id.empty() && id.size() != 128) throw ValidationError("nccl_id must be 128 bytes");
+        [](const Corpus& corpus, const TrainConfig& cfg, std::uint32_t rank, std::uint32_t world) {
             py::gil_scoped_release release;
-            return init_shard(corpus, cfg, rank, world, world > 1 && !id.empty() ? id.data() : nullptr);
+            return init_shard(corpus, cfg, rank, world);
         },
-        py::arg("corpus"), py::arg("config"), py::arg("rank"), py::arg("world"), py::arg("nccl_id") = py::bytes());
+        py::arg("corpus"), py::arg("config"), py::arg("rank"), py::arg("world"));
     m.def("shard_bounds", [](const Corpus& c, std::uint32_t world) { return shard_bounds(c, world); },
           py::arg("corpus"), py::arg("world"));
     m.def(
@@ -310,10 +309,8 @@ PYBIND11_MODULE(_core, m) {
         "init_view",
         [](py::array_t<std::uint32_t, py::array::c_style> tokens, std::uint32_t num_docs, std::uint32_t vocab_size,
            std::uint32_t doc_begin, std::uint32_t doc_end, std::uint64_t token_id_base, const TrainConfig& cfg,
-           std::uint32_t rank, std::uint32_t world, py::bytes nccl_id, std::uint32_t init_mode) {
+           std::uint32_t rank, std::uint32_t world, std::uint32_t init_mode) {
             if (tokens.ndim() != 2 || tokens.shape(1) != 3) throw ValidationError("tokens must be (T, 3) uint32");
-            std::string id = nccl_id;  // empty with world > 1: peer-memory exchange (Model.peer_attach)
-            if (world > 1 && !id.empty() && id.size() != 128) throw ValidationError("nccl_id must be 128 bytes");
             slda_corpus_view v{};
             v.num_docs = num_docs;
             v.vocab_size = vocab_size;
@@ -323,11 +320,11 @@ PYBIND11_MODULE(_core, m) {
             v.doc_end = doc_end;
             v.token_id_base = token_id_base;
             py::gil_scoped_release release;
-            return init_view(v, cfg, rank, world, world > 1 && !id.empty() ? id.data() : nullptr, init_mode);
+            return init_view(v, cfg, rank, world, init_mode);
         },
         py::arg("tokens"), py::arg("num_docs"), py::arg("vocab_size"), py::arg("doc_begin"), py::arg("doc_end"),
         py::arg("token_id_base"), py::arg("config"), py::arg("rank") = 0, py::arg("world") = 1,
-        py::arg("nccl_id") = py::bytes(), py::arg("init_mode") = 0);
+        py::arg("init_mode") = 0);
     // Synthetic corpora as raw (T, 3) arrays (bench.py): whole corpus or a document range.
     m.def(
         "generate_tokens",
@@ -357,11 +354,6 @@ PYBIND11_MODULE(_core, m) {
         },
         py::arg("family"), py::arg("num_docs"), py::arg("vocab_size"), py::arg("num_tokens"),
         py::arg("seed") = 20161008, py::arg("doc_begin") = 0, py::arg("doc_end") = -1, py::arg("threads") = 0);
-    m.def("nccl_unique_id", [] {
-        char id[128];
-        check(slda_nccl_unique_id(id));
-        return py::bytes(id, 128);
-    });
     m.def(
         "train", [](const Corpus& corpus, const TrainConfig& cfg) { return train(corpus, cfg); },
         py::arg("corpus"), py::arg("config"), py::call_guard<py::gil_scoped_release>());

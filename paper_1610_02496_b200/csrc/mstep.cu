@@ -281,12 +281,15 @@ cudaError_t launch_phi_t(const uint32_t* B, const double* denom, const float* zv
                          float* l8, float* q, uint32_t row_begin, uint32_t row_end, uint32_t K_pad,
                          uint32_t l8_stride, double beta, float falpha, cudaStream_t s, const PeerMirror* mirror) {
     constexpr size_t smem = phi_smem_bytes<C, S>();
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(phi_kernel<C, S, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-        cudaFuncSetAttribute(phi_kernel<C, S, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-        attr = true;
-    }
+    // Per launch: the opt-in is per device context (a process-wide flag would miss a second GPU).
+    if (const cudaError_t e = cudaFuncSetAttribute(phi_kernel<C, S, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                   static_cast<int>(smem));
+        e != cudaSuccess)
+        return e;
+    if (const cudaError_t e = cudaFuncSetAttribute(phi_kernel<C, S, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                   static_cast<int>(smem));
+        e != cudaSuccess)
+        return e;
     const uint32_t blocks = (row_end - row_begin + kPhiRows - 1) / kPhiRows;
     if (mirror && mirror->n > 0)
         phi_kernel<C, S, true><<<blocks, kPhiRows, smem, s>>>(B, denom, zv, bhat, l4, l8, q, row_begin, row_end,

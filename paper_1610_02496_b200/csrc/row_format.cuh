@@ -1,6 +1,6 @@
-// row_format.cuh -- device-side C_dk row access shared by the sampler kernels (sampler.cu) and
-// the SSC row encoder (ssc.cu): sector loads, the wide / compact entry decoders, the per-warp
-// cooperative staging, and the tree search.  Layouts: DESIGN.md §3.
+// row_format.cuh -- device-side C_dk row access of the sampler kernels (sampler.cu): sector
+// loads, the entry decoder, the per-warp cooperative staging, and the tree search.
+// Layouts: DESIGN.md §3.
 #pragma once
 
 #include "common.cuh"
@@ -44,16 +44,6 @@ __device__ __forceinline__ void prefetch_l2(const void* p) {
 }
 
 __device__ __forceinline__ Sector zero_sector() { return Sector{make_uint4(0u, 0u, 0u, 0u), make_uint4(0u, 0u, 0u, 0u)}; }
-
-// Compact C_dk rows (K <= kCompactMaxK): 16-bit slots, two per 32-bit word.  Word 0 =
-// nsect | nnz << 16.  Then the entries in ascending topic order: a count-1 entry is one slot
-// holding its topic; a count >= 2 entry is a whole word (topic | 0x8000, count) at an even
-// slot, a null slot (0xFFFF) padding the odd slot before it when needed; the row ends with
-// null slots up to a sector (16 slots).  Pairs never straddle a word, so every word decodes
-// on its own (sector checkpoints carry no parse state), and a count-1 entry needs no count
-// conversion: f32(1) * phi == phi.  Versus the 32-bit wide format this halves the bytes of
-// count-1 entries, the majority while documents are spread over many topics.
-constexpr uint32_t kNull16 = 0xFFFFu;
 
 // lower_bound over the word's L4 prefix (== WaryTree::sample, acceptance.cpp:140-200):
 // binary search of the staged L8 level (first 8-block whose last prefix >= x), then one
@@ -125,97 +115,29 @@ __device__ __forceinline__ void stage_group(const uint4* A4, const uint32_t (&rq
     store_group<G>(q, ns, gs, sub, grp, stage);
 }
 
-// ---- Row decoding for the sampler (both row formats) ----------------------------------------
-template <bool kGlobalPhi>
-__device__ __forceinline__ float ld_phi(const float* phi, uint32_t t) {
-    return kGlobalPhi ? __ldg(phi + t) : phi[t];
-}
-
-// Compact format word: up to two entries (see compact_chunk).  f32(1) * phi == phi, so a
-// count-1 entry adds phi[topic] directly, exactly as the reference's s += f32(1) * phi.
-// Branch-free word decode (lanes of a warp see different word kinds): the first slot is a
-// pair (topic|0x8000, count), a single, or null; the second slot is a single or null unless
-// the word is a pair.  Absent entries contribute +0 (s + +0 == s for the running sums, which
-// are >= +0) and their gathers are predicated off.
-struct WordEntries {
-    uint32_t t0, t1;   // topics
-    float c0;          // count of the first entry (1 for a single)
-    bool v0, v1;       // entries present
-};
-__device__ __forceinline__ WordEntries decode_word(uint32_t w) {
-    const uint32_t h0 = w & 0xFFFFu, h1 = w >> 16;
-    const bool pair = (h0 & 0x8000u) != 0;
-    WordEntries e;
-    e.v0 = h0 != kNull16;
-    e.t0 = h0 & 0x7FFFu;
-    e.c0 = pair ? __uint2float_rn(h1) : 1.0f;
-    e.v1 = !pair && h1 != kNull16;
-    e.t1 = h1;
-    return e;
-}
-
-template <bool kGlobalPhi>
-__device__ __forceinline__ float acc_word_compact(float s, uint32_t w, const float* phi) {
-    const WordEntries e = decode_word(w);
-    float p0 = 0.0f, p1 = 0.0f;
-    if (e.v0) p0 = ld_phi<kGlobalPhi>(phi, e.t0);
-    if (e.v1) p1 = ld_phi<kGlobalPhi>(phi, e.t1);
-    s = __fadd_rn(s, __fmul_rn(e.c0, p0));  // f32(1) * phi == phi; f32(c) * phi as the reference
-    return __fadd_rn(s, p1);
-}
-
-template <bool kGlobalPhi>
-__device__ __forceinline__ void scan_word_compact(float& run, bool& need, uint32_t& topic, float xs, uint32_t w,
-                                                  const float* phi) {
-    const WordEntries e = decode_word(w);
-    float p0 = 0.0f, p1 = 0.0f;
-    if (e.v0) p0 = ld_phi<kGlobalPhi>(phi, e.t0);
-    if (e.v1) p1 = ld_phi<kGlobalPhi>(phi, e.t1);
-    run = __fadd_rn(run, __fmul_rn(e.c0, p0));
-    if (need && e.v0 && run >= xs) { topic = e.t0; need = false; }
-    run = __fadd_rn(run, p1);
-    if (need && e.v1 && run >= xs) { topic = e.t1; need = false; }
-}
-
-// First pass over one staged sector (32 bytes) of a row.  Sector 0 starts with the header
-// (compact: skipped; wide: a count-0 entry that adds +0).
-template <bool kGlobalPhi, bool kCompact>
-__device__ __forceinline__ float acc_sector(float s, const unsigned char* p, uint32_t sec, uint32_t tbits,
-                                            uint32_t tmask, const float* phi) {
+// ---- Row decoding for the round-based sampler ----------------------------------------------
+// First pass over one staged sector (32 bytes) of a row.  Sector 0 starts with the header, a
+// count-0 entry that adds +0.
+__device__ __forceinline__ float acc_sector(float s, const unsigned char* p, uint32_t tbits, uint32_t tmask,
+                                            const float* phi) {
     const uint4 lo = *reinterpret_cast<const uint4*>(p);
     const uint4 hi = *reinterpret_cast<const uint4*>(p + 16);
-    if (kCompact) {
-        if (sec != 0) s = acc_word_compact<kGlobalPhi>(s, lo.x, phi);
-        s = acc_word_compact<kGlobalPhi>(s, lo.y, phi);
-        s = acc_word_compact<kGlobalPhi>(s, lo.z, phi);
-        s = acc_word_compact<kGlobalPhi>(s, lo.w, phi);
-        s = acc_word_compact<kGlobalPhi>(s, hi.x, phi);
-        s = acc_word_compact<kGlobalPhi>(s, hi.y, phi);
-        s = acc_word_compact<kGlobalPhi>(s, hi.z, phi);
-        return acc_word_compact<kGlobalPhi>(s, hi.w, phi);
-    }
-    s = acc_quad<kGlobalPhi>(s, lo, tbits, tmask, phi);
-    return acc_quad<kGlobalPhi>(s, hi, tbits, tmask, phi);
+    s = acc_quad<false>(s, lo, tbits, tmask, phi);
+    return acc_quad<false>(s, hi, tbits, tmask, phi);
 }
 
 // Prefix re-scan of one staged sector: first running sum >= xs.
-template <bool kGlobalPhi, bool kCompact>
-__device__ __forceinline__ void scan_sector(float& run, bool& need, uint32_t& topic, float xs,
-                                            const unsigned char* p, uint32_t sec, uint32_t tbits,
-                                            uint32_t tmask, const float* phi) {
+__device__ __forceinline__ void scan_sector(float& run, bool& need, uint32_t& topic, float xs, const unsigned char* p,
+                                            uint32_t tbits, uint32_t tmask, const float* phi) {
     const uint4 lo = *reinterpret_cast<const uint4*>(p);
     const uint4 hi = *reinterpret_cast<const uint4*>(p + 16);
     const uint32_t es[8] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};
 #pragma unroll
     for (int w = 0; w < 8; ++w) {
-        if (kCompact) {
-            if (w > 0 || sec != 0) scan_word_compact<kGlobalPhi>(run, need, topic, xs, es[w], phi);
-        } else {
-            run = __fadd_rn(run, entry_mass<kGlobalPhi>(es[w], tbits, tmask, phi));
-            if (need && run >= xs) {
-                topic = es[w] & tmask;
-                need = false;
-            }
+        run = __fadd_rn(run, entry_mass<false>(es[w], tbits, tmask, phi));
+        if (need && run >= xs) {
+            topic = es[w] & tmask;
+            need = false;
         }
     }
 }

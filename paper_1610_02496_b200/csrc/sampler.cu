@@ -19,13 +19,15 @@ namespace slda {
 // sequential f32 chains.
 // ============================================================================
 
-template <int NT, int G, int MINB, bool kGlobalPhi, bool kCompact>
+// Used where a 512-thread quad-lane CTA pair does not fit an SM but the phi row still fits shared
+// memory (17.5K < K_pad <~ 45K).
+template <int NT, int G, int MINB>
 __global__ void __launch_bounds__(NT, MINB) sampler_kernel(SamplerArgs a) {
     using St = Stage<G>;
     extern __shared__ __align__(16) float sm[];
     const uint32_t v = a.units[blockIdx.x].word;
-    const float* s_bhat = kGlobalPhi ? a.bhat + static_cast<size_t>(v) * a.K_pad : sm;
-    float* s_l8 = kGlobalPhi ? sm : sm + a.K_pad;  // l8_stride (L4[8j+7], padded with the total)
+    const float* s_bhat = sm;
+    float* s_l8 = sm + a.K_pad;  // l8_stride (L4[8j+7], padded with the total)
     float* s_ck = s_l8 + a.l8_stride;       // [kCkSectors][NT]
     unsigned char* s_stage = reinterpret_cast<unsigned char*>(s_ck + kCkSectors * NT);
 
@@ -33,11 +35,9 @@ __global__ void __launch_bounds__(NT, MINB) sampler_kernel(SamplerArgs a) {
     const float* l4row = a.l4 + static_cast<size_t>(v) * a.K_pad;
     const float total = __ldg(l4row + a.K_pad - 1);  // padded with the row total
     {
-        if (!kGlobalPhi) {
-            const float4* gb = reinterpret_cast<const float4*>(a.bhat + static_cast<size_t>(v) * a.K_pad);
-            float4* sb = reinterpret_cast<float4*>(sm);
-            for (uint32_t i = threadIdx.x; i < a.K_pad / 4; i += NT) sb[i] = __ldg(gb + i);
-        }
+        const float4* gb = reinterpret_cast<const float4*>(a.bhat + static_cast<size_t>(v) * a.K_pad);
+        float4* sb = reinterpret_cast<float4*>(sm);
+        for (uint32_t i = threadIdx.x; i < a.K_pad / 4; i += NT) sb[i] = __ldg(gb + i);
         const float4* gl = reinterpret_cast<const float4*>(a.l8 + static_cast<size_t>(v) * a.l8_stride);
         float4* sl = reinterpret_cast<float4*>(s_l8);
         for (uint32_t i = threadIdx.x; i < a.l8_stride / 4; i += NT) sl[i] = __ldg(gl + i);
@@ -73,11 +73,11 @@ __global__ void __launch_bounds__(NT, MINB) sampler_kernel(SamplerArgs a) {
         stage_group<G>(A4, rq, ns, gs, sub, grp, stage);
         __syncwarp();
 
-        // Wide row = [header (nnz-1, count 0) | entries | zero-count padding to 8]: header and
-        // padding add +0 to every running sum.  Compact row: word 0 = nsect | nnz << 16.
+        // Row = [header (nnz-1, count 0) | entries | zero-count padding to 8]: header and
+        // padding add +0 to every running sum.
         const uint32_t w0 = reinterpret_cast<const uint4*>(mine)->x;
-        const uint32_t nnz = active ? (kCompact ? w0 >> 16 : (w0 & tmask) + 1u) : 0u;
-        const uint32_t nsect = active ? (kCompact ? w0 & 0xFFFFu : (nnz + 8u) >> 3) : 0u;
+        const uint32_t nnz = active ? (w0 & tmask) + 1u : 0u;
+        const uint32_t nsect = active ? (nnz + 8u) >> 3 : 0u;
         entries += nnz;
 #pragma unroll
         for (uint32_t j = 0; j < G; ++j) ns[j] = __shfl_sync(0xffffffffu, nsect, St::kRowsPerInst * j + grp);
@@ -105,7 +105,7 @@ __global__ void __launch_bounds__(NT, MINB) sampler_kernel(SamplerArgs a) {
             for (uint32_t u = 0; u < G; ++u) {
                 const uint32_t sec = G * g + u;
                 if (sec < nsect) {
-                    s = acc_sector<kGlobalPhi, kCompact>(s, mine + 32 * u, sec, tbits, tmask, s_bhat);
+                    s = acc_sector(s, mine + 32 * u, tbits, tmask, s_bhat);
                     if (sec < kCkSectors) ck[sec * NT] = s;
                 }
             }
@@ -125,9 +125,9 @@ __global__ void __launch_bounds__(NT, MINB) sampler_kernel(SamplerArgs a) {
                 // Sparse branch: first running prefix >= p*S (prefix_search, sampler.hpp:18-41).
                 xs = __fmul_rn(up, s);
                 if (xs == 0.0f) {
-                    // every prefix is >= 0: the first real entry (word 1 in both formats)
+                    // every prefix is >= 0: the first real entry (word 1)
                     const uint32_t e1 = __ldg(reinterpret_cast<const uint32_t*>(A4 + t.x) + 1);
-                    topic = kCompact ? (e1 & 0x7FFFu) : (e1 & tmask);
+                    topic = e1 & tmask;
                 } else {
                     // The first sector whose end sum reaches xs holds the crossing; its re-scan
                     // restarts from the previous checkpoint, the same f32 value the first pass
@@ -163,7 +163,7 @@ __global__ void __launch_bounds__(NT, MINB) sampler_kernel(SamplerArgs a) {
             stage_group<G>(A4, rq, ns, gs, sub, grp, stage);
             __syncwarp();
             if (need) {
-                scan_sector<kGlobalPhi, kCompact>(run, need, topic, xs, mine, sec, tbits, tmask, s_bhat);
+                scan_sector(run, need, topic, xs, mine, tbits, tmask, s_bhat);
                 ++sec;
             }
         }
@@ -174,254 +174,6 @@ __global__ void __launch_bounds__(NT, MINB) sampler_kernel(SamplerArgs a) {
     }
     if (a.row_entries) {
         // One atomic per warp.
-        for (int o = 16; o > 0; o >>= 1) entries += __shfl_xor_sync(0xffffffffu, entries, o);
-        if (lane == 0) atomicAdd(a.row_entries, entries);
-    }
-}
-
-// ---- K3' streaming sampler: the same draws, bit for bit, with lane refill -----------------------
-// The round-based kernel above advances a warp's 32 tokens in lock step: every round waits for
-// its longest row, re-reads the crossing sector with a second dependent round trip, and loads a
-// speculative group for every row.  Here each lane owns a sequence of tokens instead: the
-// warp streams G-sector groups of its lanes' CURRENT rows (cooperative, coalesced, next group
-// prefetched in registers); a lane whose row ends takes the next token of the unit at once
-// (warp ballot over a 32-token pool, CTA-wide dynamic batches), so the stream never waits for
-// the longest row.  The branch decision needs the whole row (S), so a finished token's last
-// step is deferred by one step: the one sector it still needs -- the sparse branch's crossing
-// sector (found from the per-sector checkpoints) or the tree branch's L4 block -- is loaded
-// lane-private in step t and resolved in step t+1, under the next step's consumption.
-// Arithmetic (make_branch_context, prefix_search, WaryTree::sample) is unchanged.
-template <int NT, int G>
-__global__ void __launch_bounds__(NT, NT <= 128 ? 3 : 2) sampler_stream_kernel(SamplerArgs a) {
-    using St = Stage<G>;
-    extern __shared__ __align__(16) float sm[];
-    __shared__ uint32_t s_next;  // next unclaimed 32-token batch (index within the unit)
-    const Unit unit = a.units[blockIdx.x];
-    const uint32_t v = unit.word;
-    float* s_bhat = sm;
-    float* s_l8 = sm + a.K_pad;
-    float* s_ck = s_l8 + a.l8_stride;  // [kCkSectors][NT]
-    unsigned char* s_stage = reinterpret_cast<unsigned char*>(s_ck + kCkSectors * NT);
-    const float* l4row = a.l4 + static_cast<size_t>(v) * a.K_pad;
-    const float total = __ldg(l4row + a.K_pad - 1);
-    {
-        const float4* gb = reinterpret_cast<const float4*>(a.bhat + static_cast<size_t>(v) * a.K_pad);
-        float4* sb = reinterpret_cast<float4*>(sm);
-        for (uint32_t i = threadIdx.x; i < a.K_pad / 4; i += NT) sb[i] = __ldg(gb + i);
-        const float4* gl = reinterpret_cast<const float4*>(a.l8 + static_cast<size_t>(v) * a.l8_stride);
-        float4* sl = reinterpret_cast<float4*>(s_l8);
-        for (uint32_t i = threadIdx.x; i < a.l8_stride / 4; i += NT) sl[i] = __ldg(gl + i);
-    }
-    if (threadIdx.x == 0) s_next = NT;  // warp w starts with batch [32w, 32w + 32)
-    const float qv = __ldg(a.q + v);
-    uint32_t* brow = a.B + static_cast<size_t>(v) * a.K_pad;
-    const uint32_t tbits = a.tbits, tmask = (1u << tbits) - 1u;
-    const uint4* A4 = reinterpret_cast<const uint4*>(a.A);
-    const uint2* toks = a.tok + unit.offset;
-    const uint32_t len = unit.length;
-    const uint32_t lane = lane_id(), sub = lane / St::kRowsPerInst, grp = lane % St::kRowsPerInst;
-    unsigned char* stage = s_stage + (threadIdx.x >> 5) * St::kWarp;
-    const unsigned char* mine = stage + lane * St::kRow;
-    float* ck = s_ck + threadIdx.x;
-    unsigned long long entries = 0;
-    __syncthreads();
-
-    // Token pool: pool = batch at pool_base (lane l holds token pool_base + l), nxt = the batch
-    // after it; pc = tokens of the pool already handed out.
-    uint32_t pool_base = (threadIdx.x >> 5) * 32u;
-    uint2 pool = pool_base + lane < len ? __ldg(toks + pool_base + lane) : make_uint2(0u, 0u);
-    auto claim = [&]() -> uint32_t {
-        uint32_t b = 0;
-        if (lane == 0) b = atomicAdd(&s_next, 32u);
-        return __shfl_sync(0xffffffffu, b, 0);
-    };
-    uint32_t next_base = claim();
-    uint2 nxt = next_base + lane < len ? __ldg(toks + next_base + lane) : make_uint2(0u, 0u);
-    uint32_t pc = 0;
-
-    // Current row (the one staged this step).
-    bool cur = false, hdr = false;  // hdr: the staged group is the row's first (header unread)
-    uint32_t c_rq = 0, c_slot = 0, c_ns = 0, c_base = 0;
-    float s = 0.0f;
-    // Pending resolution: 0 none, 1 sparse (scan sector p_sec from run p_run for xs), 2 tree
-    // (L4 block p_sec), 3 sparse with xs == 0 (the first real entry).
-    uint32_t p_kind = 0, p_slot = 0, p_sec = 0, p_rq = 0, p_ns = 0;
-    float p_run = 0.0f, p_x = 0.0f;
-    Sector psec = zero_sector();
-
-    // Hands out tokens to the lanes in `need` (ballot), in lane order.
-    auto take = [&](bool want, uint32_t& rq, uint32_t& slot) -> bool {
-        const uint32_t need = __ballot_sync(0xffffffffu, want);
-        const uint32_t idx = pc + __popc(need & ((1u << lane) - 1u));
-        const uint2 ra = make_uint2(__shfl_sync(0xffffffffu, pool.x, idx & 31u),
-                                    __shfl_sync(0xffffffffu, pool.y, idx & 31u));
-        const uint2 rb = make_uint2(__shfl_sync(0xffffffffu, nxt.x, idx & 31u),
-                                    __shfl_sync(0xffffffffu, nxt.y, idx & 31u));
-        const uint32_t gi = idx < 32u ? pool_base + idx : next_base + (idx - 32u);
-        const bool got = want && idx < 64u && gi < len;
-        rq = idx < 32u ? ra.x : rb.x;
-        slot = idx < 32u ? ra.y : rb.y;
-        pc += __popc(need);
-        if (pc >= 32u) {  // pool consumed: the next batch becomes the pool
-            pc -= 32u;
-            pool = nxt;
-            pool_base = next_base;
-            next_base = claim();
-            nxt = next_base + lane < len ? __ldg(toks + next_base + lane) : make_uint2(0u, 0u);
-        }
-        return got;
-    };
-
-    // First tokens and their first groups.
-    uint32_t t_rq = 0, t_slot = 0;
-    cur = take(true, t_rq, t_slot);
-    c_rq = t_rq;
-    c_slot = t_slot;
-    hdr = cur;
-    {
-        uint32_t rq[G], ns[G], gs[G];
-#pragma unroll
-        for (uint32_t j = 0; j < G; ++j) {
-            rq[j] = __shfl_sync(0xffffffffu, c_rq, St::kRowsPerInst * j + grp);
-            ns[j] = __shfl_sync(0xffffffffu, cur ? G : 0u, St::kRowsPerInst * j + grp);
-            gs[j] = 0;
-        }
-        stage_group<G>(A4, rq, ns, gs, sub, grp, stage);
-        __syncwarp();
-    }
-
-    while (__any_sync(0xffffffffu, cur || p_kind != 0)) {
-        // Header of a row whose first group is staged: [nnz-1 | entries | zero pad].
-        if (cur && hdr) {
-            const uint32_t nnz = (reinterpret_cast<const uint4*>(mine)->x & tmask) + 1u;
-            c_ns = (nnz + 8u) >> 3;
-            entries += nnz;
-            hdr = false;
-        }
-        // Next step's group per lane: the rest of this row, or the first group of a new token.
-        const bool ends = cur && c_base + G >= c_ns;
-        uint32_t n_rq = 0, n_slot = 0;
-        const bool got = take(ends, n_rq, n_slot);
-        uint32_t l_rq = 0, l_start = 0, l_lim = 0;
-        if (cur && !ends) {
-            l_rq = c_rq; l_start = c_base + G; l_lim = c_ns;
-        } else if (got) {
-            l_rq = n_rq; l_start = 0; l_lim = G;  // speculative first group (header inside)
-        }
-        uint32_t rq[G], ns[G], gs[G];
-#pragma unroll
-        for (uint32_t j = 0; j < G; ++j) {
-            const uint32_t src = St::kRowsPerInst * j + grp;
-            rq[j] = __shfl_sync(0xffffffffu, l_rq, src);
-            gs[j] = __shfl_sync(0xffffffffu, l_start, src);
-            ns[j] = __shfl_sync(0xffffffffu, l_lim, src);
-        }
-        Sector nx[G];
-        load_group<G>(A4, rq, ns, gs, sub, nx);
-
-        // make_branch_context over this step's sectors (sequential f32 chain).
-        if (cur) {
-#pragma unroll
-            for (uint32_t u = 0; u < G; ++u) {
-                const uint32_t sec = c_base + u;
-                if (sec < c_ns) {
-                    s = acc_sector<false, false>(s, mine + 32 * u, sec, tbits, tmask, s_bhat);
-                    if (sec < kCkSectors) ck[sec * NT] = s;
-                }
-            }
-        }
-
-        // Resolve the token finished in the previous step (its sector arrived meanwhile).
-        if (p_kind != 0) {
-            uint32_t topic;
-            if (p_kind == 2) {
-                const float x = p_x;
-                const uint32_t below = (__uint_as_float(psec.lo.x) < x) + (__uint_as_float(psec.lo.y) < x) +
-                                       (__uint_as_float(psec.lo.z) < x) + (__uint_as_float(psec.lo.w) < x) +
-                                       (__uint_as_float(psec.hi.x) < x) + (__uint_as_float(psec.hi.y) < x) +
-                                       (__uint_as_float(psec.hi.z) < x) + (__uint_as_float(psec.hi.w) < x);
-                const uint32_t k = p_sec * kLeaf + below;
-                topic = k < a.K ? k : a.K - 1;
-            } else if (p_kind == 3) {
-                topic = psec.lo.y & tmask;  // word 1 of sector 0: the first real entry
-            } else {
-                // prefix_search (sampler.hpp:18-41) from the checkpoint: first running sum >= xs.
-                float run = p_run;
-                bool need = true;
-                topic = 0;
-                uint32_t sec = p_sec;
-                Sector q = psec;
-                while (true) {
-                    const uint32_t es[8] = {q.lo.x, q.lo.y, q.lo.z, q.lo.w, q.hi.x, q.hi.y, q.hi.z, q.hi.w};
-#pragma unroll
-                    for (int w = 0; w < 8; ++w) {
-                        run = __fadd_rn(run, entry_mass<false>(es[w], tbits, tmask, s_bhat));
-                        if (need && run >= p_x) { topic = es[w] & tmask; need = false; }
-                    }
-                    if (!need || ++sec >= p_ns) break;
-                    q = ldg_sector(A4 + p_rq + 2 * sec);  // crossing beyond the checkpoints (rare)
-                }
-            }
-            a.z[p_slot] = static_cast<uint16_t>(topic);
-            atomicAdd(brow + topic, 1u);
-            p_kind = 0;
-        }
-
-        // A finished row: sample_token (sampler.hpp:183-204) up to its last sector read.
-        if (ends) {
-            float ub, up;
-            const uint64_t id = a.ids ? __ldg(a.ids + c_slot) : a.id_base + c_slot;
-            draw2_f32(a.seed, a.stream_kind, id, ub, up);
-            p_slot = c_slot;
-            if (ub < __fdiv_rn(s, __fadd_rn(s, qv))) {
-                const float xs = __fmul_rn(up, s);
-                if (xs == 0.0f) {
-                    p_kind = 3;
-                    p_sec = 0;
-                    psec = ldg_sector(A4 + c_rq);
-                } else {
-                    const uint32_t stored = c_ns < kCkSectors ? c_ns : kCkSectors;
-                    uint32_t lo = 0, hi = stored;  // first checkpoint >= xs (or stored)
-                    while (lo < hi) {
-                        const uint32_t mid = (lo + hi) >> 1;
-                        if (ck[mid * NT] >= xs) hi = mid; else lo = mid + 1;
-                    }
-                    p_kind = 1;
-                    p_sec = lo;
-                    p_run = lo > 0 ? ck[(lo - 1) * NT] : 0.0f;
-                    p_x = xs;
-                    p_rq = c_rq;
-                    p_ns = c_ns;
-                    psec = ldg_sector(A4 + c_rq + 2 * lo);
-                }
-            } else {
-                float x = __fmul_rn(up, total);  // WaryTree::sample(p * total)
-                if (!(x <= total)) x = total;
-                uint32_t lo = 0, hi = a.n_l8 - 1;
-                while (lo < hi) {
-                    const uint32_t mid = (lo + hi) >> 1;
-                    if (s_l8[mid] >= x) hi = mid; else lo = mid + 1;
-                }
-                p_kind = 2;
-                p_sec = lo;
-                p_x = x;
-                psec = ldg_sector(reinterpret_cast<const uint4*>(l4row + lo * kLeaf));
-            }
-            // The next token (if any) starts with the group loaded above.
-            cur = got;
-            c_rq = n_rq;
-            c_slot = n_slot;
-            c_base = 0;
-            hdr = got;
-            s = 0.0f;
-        } else if (cur) {
-            c_base += G;
-        }
-        __syncwarp();
-        store_group<G>(nx, ns, gs, sub, grp, stage);
-        __syncwarp();
-    }
-    if (a.row_entries) {
         for (int o = 16; o > 0; o >>= 1) entries += __shfl_xor_sync(0xffffffffu, entries, o);
         if (lane == 0) atomicAdd(a.row_entries, entries);
     }
@@ -439,7 +191,7 @@ __global__ void __launch_bounds__(NT, NT <= 128 ? 3 : 2) sampler_stream_kernel(S
 // sum visits the 4 sectors of a line in order -- lane j adds its 8 products to the value lane
 // j-1 handed it (shuffle) -- so every intermediate is the reference's.  The per-sector sums
 // double as the prefix_search checkpoints (a few hundred bytes per warp instead of a stage).
-template <int NT, int MINB, int L, bool kCompact, bool kC16 = false>
+template <int NT, int MINB, int L, bool kC16 = false>
 __global__ void __launch_bounds__(NT, MINB) sampler_quad_kernel(SamplerArgs a) {
     constexpr uint32_t NW = NT / 32;
     constexpr uint32_t TPR = 32u / L;  // tokens per round (L lanes each, L sectors per group)
@@ -488,9 +240,9 @@ __global__ void __launch_bounds__(NT, MINB) sampler_quad_kernel(SamplerArgs a) {
             Sector c = zero_sector();
             if (act) c = ldg_sector(row + 2 * sub);
             const uint32_t hw = __shfl_sync(0xffffffffu, c.lo.x, lead);  // header: word 0 of sector 0
-            // wide: [nnz-1 | entries | pad to 8]; compact: word 0 = nsect | nnz << 16
-            const uint32_t nnz = act ? (kCompact ? hw >> 16 : (hw & tmask) + 1u) : 0u;
-            const uint32_t nsect = act ? (kCompact ? hw & 0xFFFFu : (nnz + 8u) >> 3) : 0u;
+            // [nnz-1 | entries | pad to 8]
+            const uint32_t nnz = act ? (hw & tmask) + 1u : 0u;
+            const uint32_t nsect = act ? (nnz + 8u) >> 3 : 0u;
             if (sub == 0) entries += nnz;
             const uint32_t max_groups = __reduce_max_sync(0xffffffffu, (nsect + L - 1u) / L);
             float* ck = ckw + ti * kCkStride;
@@ -498,28 +250,14 @@ __global__ void __launch_bounds__(NT, MINB) sampler_quad_kernel(SamplerArgs a) {
             // Products of this lane's sector, then the chain over the line's 4 sectors in order.
             auto consume = [&](const Sector& q, uint32_t g) {
                 const uint32_t sec = L * g + sub;
-                constexpr int NP = kCompact ? 16 : 8;  // products per sector
+                constexpr int NP = 8;  // products per sector
                 // Sectors past the row are loaded as zeros (in-range bhat[0] gathers, broadcast),
                 // so the products need no branch; only valid sectors' products are accumulated.
                 float p[NP];
                 {
                     const uint32_t es[8] = {q.lo.x, q.lo.y, q.lo.z, q.lo.w, q.hi.x, q.hi.y, q.hi.z, q.hi.w};
-                    if (kCompact) {
-                        // Each word: (c0 * phi[t0]) then phi[t1]; absent entries are +0 (acc_word_compact).
 #pragma unroll
-                        for (int w = 0; w < 8; ++w) {
-                            const WordEntries e = decode_word(es[w]);
-                            const bool hdr = w == 0 && sec == 0;  // the header word
-                            float p0 = 0.0f, p1 = 0.0f;
-                            if (e.v0 && !hdr) p0 = s_bhat[e.t0];
-                            if (e.v1 && !hdr) p1 = s_bhat[e.t1];
-                            p[2 * w] = __fmul_rn(e.c0, p0);
-                            p[2 * w + 1] = p1;
-                        }
-                    } else {
-#pragma unroll
-                        for (int w = 0; w < 8; ++w) p[w] = entry_mass<false>(es[w], tbits, tmask, s_bhat);
-                    }
+                    for (int w = 0; w < 8; ++w) p[w] = entry_mass<false>(es[w], tbits, tmask, s_bhat);
                 }
                 // Branch-free rounds: every lane runs the 8 FADDs (an instruction costs the same
                 // with 8 or 32 lanes active) and only lane j of each group keeps the result.
@@ -564,7 +302,7 @@ __global__ void __launch_bounds__(NT, MINB) sampler_quad_kernel(SamplerArgs a) {
                 const float xs = __fmul_rn(up, S);
                 if (xs == 0.0f) {
                     const uint32_t e1 = __ldg(reinterpret_cast<const uint32_t*>(row) + 1);  // first real entry
-                    topic = kCompact ? (e1 & 0x7FFFu) : (e1 & tmask);
+                    topic = e1 & tmask;
                 } else {
                     const float* ck = ckw + lane * kCkStride;
                     const uint32_t stored = my_ns < kCk ? my_ns : kCk;
@@ -578,18 +316,10 @@ __global__ void __launch_bounds__(NT, MINB) sampler_quad_kernel(SamplerArgs a) {
                         const Sector q = ldg_sector(row + 2 * sc);
                         const uint32_t es[8] = {q.lo.x, q.lo.y, q.lo.z, q.lo.w, q.hi.x, q.hi.y, q.hi.z, q.hi.w};
                         bool found = false;
-                        if (kCompact) {
-                            bool need = true;
 #pragma unroll
-                            for (int w = 0; w < 8; ++w)
-                                if (w > 0 || sc != 0) scan_word_compact<false>(r, need, topic, xs, es[w], s_bhat);
-                            found = !need;
-                        } else {
-#pragma unroll
-                            for (int w = 0; w < 8; ++w) {
-                                r = __fadd_rn(r, entry_mass<false>(es[w], tbits, tmask, s_bhat));
-                                if (!found && r >= xs) { topic = es[w] & tmask; found = true; }
-                            }
+                        for (int w = 0; w < 8; ++w) {
+                            r = __fadd_rn(r, entry_mass<false>(es[w], tbits, tmask, s_bhat));
+                            if (!found && r >= xs) { topic = es[w] & tmask; found = true; }
                         }
                         if (found) break;
                     }
@@ -618,7 +348,7 @@ __global__ void __launch_bounds__(NT, MINB) sampler_quad_kernel(SamplerArgs a) {
 // make room in the 64-register budget (C3 K=10K: 95.5 -> 92.8 ms; C2: 19.8 -> 20.5 ms).
 // kGlobalPhi: the phi row does not fit shared memory (K >~ 45K): only L8 is staged and the
 // products gather phi through L1/L2.
-template <int NT, int MINB, int L, bool kCompact, bool kC16 = false, bool kPrefetchNext = true, bool kGlobalPhi = false>
+template <int NT, int MINB, int L, bool kC16 = false, bool kPrefetchNext = true, bool kGlobalPhi = false>
 __global__ void __launch_bounds__(NT, MINB) sampler_quad_pf_kernel(SamplerArgs a) {
     constexpr uint32_t NW = NT / 32;
     constexpr uint32_t TPR = 32u / L;  // tokens per round (L lanes each, L sectors per group)
@@ -686,9 +416,9 @@ __global__ void __launch_bounds__(NT, MINB) sampler_quad_pf_kernel(SamplerArgs a
                 if (act) c = ldg_sector(row + 2 * sub);
             }
             const uint32_t hw = __shfl_sync(0xffffffffu, c.lo.x, lead);  // header: word 0 of sector 0
-            // wide: [nnz-1 | entries | pad to 8]; compact: word 0 = nsect | nnz << 16
-            const uint32_t nnz = act ? (kCompact ? hw >> 16 : (hw & tmask) + 1u) : 0u;
-            const uint32_t nsect = act ? (kCompact ? hw & 0xFFFFu : (nnz + 8u) >> 3) : 0u;
+            // [nnz-1 | entries | pad to 8]
+            const uint32_t nnz = act ? (hw & tmask) + 1u : 0u;
+            const uint32_t nsect = act ? (nnz + 8u) >> 3 : 0u;
             if (sub == 0) entries += nnz;
             const uint32_t max_groups = __reduce_max_sync(0xffffffffu, (nsect + L - 1u) / L);
             float* ck = ckw + ti * kCkStride;
@@ -696,28 +426,14 @@ __global__ void __launch_bounds__(NT, MINB) sampler_quad_pf_kernel(SamplerArgs a
             // Products of this lane's sector, then the chain over the line's 4 sectors in order.
             auto consume = [&](const Sector& q, uint32_t g) {
                 const uint32_t sec = L * g + sub;
-                constexpr int NP = kCompact ? 16 : 8;  // products per sector
+                constexpr int NP = 8;  // products per sector
                 // Sectors past the row are loaded as zeros (in-range bhat[0] gathers, broadcast),
                 // so the products need no branch; only valid sectors' products are accumulated.
                 float p[NP];
                 {
                     const uint32_t es[8] = {q.lo.x, q.lo.y, q.lo.z, q.lo.w, q.hi.x, q.hi.y, q.hi.z, q.hi.w};
-                    if (kCompact) {
-                        // Each word: (c0 * phi[t0]) then phi[t1]; absent entries are +0 (acc_word_compact).
 #pragma unroll
-                        for (int w = 0; w < 8; ++w) {
-                            const WordEntries e = decode_word(es[w]);
-                            const bool hdr = w == 0 && sec == 0;  // the header word
-                            float p0 = 0.0f, p1 = 0.0f;
-                            if (e.v0 && !hdr) p0 = s_bhat[e.t0];
-                            if (e.v1 && !hdr) p1 = s_bhat[e.t1];
-                            p[2 * w] = __fmul_rn(e.c0, p0);
-                            p[2 * w + 1] = p1;
-                        }
-                    } else {
-#pragma unroll
-                        for (int w = 0; w < 8; ++w) p[w] = entry_mass<kGlobalPhi>(es[w], tbits, tmask, s_bhat);
-                    }
+                    for (int w = 0; w < 8; ++w) p[w] = entry_mass<kGlobalPhi>(es[w], tbits, tmask, s_bhat);
                 }
                 // Branch-free rounds: every lane runs the 8 FADDs (an instruction costs the same
                 // with 8 or 32 lanes active) and only lane j of each group keeps the result.
@@ -781,7 +497,7 @@ __global__ void __launch_bounds__(NT, MINB) sampler_quad_pf_kernel(SamplerArgs a
                 const float xs = __fmul_rn(up, S);
                 if (xs == 0.0f) {
                     const uint32_t e1 = __ldg(reinterpret_cast<const uint32_t*>(row) + 1);  // first real entry
-                    topic = kCompact ? (e1 & 0x7FFFu) : (e1 & tmask);
+                    topic = e1 & tmask;
                 } else {
                     const float* ck = ckw + lane * kCkStride;
                     const uint32_t stored = my_ns < kCk ? my_ns : kCk;
@@ -795,18 +511,10 @@ __global__ void __launch_bounds__(NT, MINB) sampler_quad_pf_kernel(SamplerArgs a
                         const Sector q = ldg_sector(row + 2 * sc);
                         const uint32_t es[8] = {q.lo.x, q.lo.y, q.lo.z, q.lo.w, q.hi.x, q.hi.y, q.hi.z, q.hi.w};
                         bool found = false;
-                        if (kCompact) {
-                            bool need = true;
 #pragma unroll
-                            for (int w = 0; w < 8; ++w)
-                                if (w > 0 || sc != 0) scan_word_compact<false>(r, need, topic, xs, es[w], s_bhat);
-                            found = !need;
-                        } else {
-#pragma unroll
-                            for (int w = 0; w < 8; ++w) {
-                                r = __fadd_rn(r, entry_mass<kGlobalPhi>(es[w], tbits, tmask, s_bhat));
-                                if (!found && r >= xs) { topic = es[w] & tmask; found = true; }
-                            }
+                        for (int w = 0; w < 8; ++w) {
+                            r = __fadd_rn(r, entry_mass<kGlobalPhi>(es[w], tbits, tmask, s_bhat));
+                            if (!found && r >= xs) { topic = es[w] & tmask; found = true; }
                         }
                         if (found) break;
                     }
@@ -835,98 +543,65 @@ __global__ void __launch_bounds__(NT, MINB) sampler_quad_pf_kernel(SamplerArgs a
     }
 }
 
-size_t sampler_smem(const SamplerArgs& a, int nt, int g, bool global_phi) {
+// Dynamic shared memory opt-in, set on every launch: the attribute is per device context, so
+// a process-wide "configured" flag would leave a second engine on another GPU without it.
+template <class Kern>
+cudaError_t smem_optin(Kern kern, size_t bytes) {
+    return bytes > 48 * 1024
+               ? cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bytes))
+               : cudaSuccess;
+}
+
+size_t sampler_smem(const SamplerArgs& a, int nt, int g) {
     const size_t stage_row = 32u * static_cast<size_t>(g) + 16u;
-    return sizeof(float) * ((global_phi ? 0 : static_cast<size_t>(a.K_pad)) + a.l8_stride) +
+    return sizeof(float) * (static_cast<size_t>(a.K_pad) + a.l8_stride) +
            (sizeof(float) * kCkSectors + stage_row) * static_cast<size_t>(nt);
 }
 
-template <int NT, int G, int MINB, bool Gl, bool C>
-cudaError_t launch_sampler_t(const SamplerArgs& a, uint32_t n_units, cudaStream_t s) {
-    static bool configured = false;
-    if (!configured) {
-        cudaFuncSetAttribute(sampler_kernel<NT, G, MINB, Gl, C>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             227 * 1024);
-        configured = true;
-    }
-    sampler_kernel<NT, G, MINB, Gl, C><<<n_units, NT, sampler_smem(a, NT, G, Gl), s>>>(a);
+// Round-based 4-sector-group kernel (17.5K < K_pad <~ 45K).
+cudaError_t launch_round(const SamplerArgs& a, uint32_t n_units, cudaStream_t s) {
+    const size_t smem = sampler_smem(a, 256, 4);
+    if (const cudaError_t e = smem_optin(sampler_kernel<256, 4, 2>, smem); e != cudaSuccess) return e;
+    sampler_kernel<256, 4, 2><<<n_units, 256, smem, s>>>(a);
     return cudaGetLastError();
-}
-
-template <int NT, int G>
-cudaError_t launch_stream_t(const SamplerArgs& a, uint32_t n_units, cudaStream_t s) {
-    static bool configured = false;
-    if (!configured) {
-        // 227 KB per block minus the kernel's static shared memory (the batch counter).
-        const cudaError_t e = cudaFuncSetAttribute(sampler_stream_kernel<NT, G>,
-                                                   cudaFuncAttributeMaxDynamicSharedMemorySize, 226 * 1024);
-        if (e != cudaSuccess) return e;
-        configured = true;
-    }
-    sampler_stream_kernel<NT, G><<<n_units, NT, sampler_smem(a, NT, G, false), s>>>(a);
-    return cudaGetLastError();
-}
-
-int sampler_shape_from_name(const char* name) {
-    const std::string v(name ? name : "");
-    return v == "g2" ? 0 : v == "g4" ? 1 : v == "g4x512" ? 2 : v == "s4" ? 3 : v == "s2" ? 4 : v == "s4x128" ? 5
-         : v == "q512" ? 6 : v == "q256" ? 7 : v == "q512r" ? 8 : v == "q256r" ? 9
-         : v == "p512" ? 10 : v == "p256" ? 11 : v == "o512" ? 12 : -1;
 }
 
 size_t sampler_quad_smem(const SamplerArgs& a, int nt) {
     return sizeof(float) * (static_cast<size_t>(a.K_pad) + a.l8_stride + static_cast<size_t>(nt / 32) * 32u * 17u);
 }
 
-template <int NT, int MINB, int L, bool C, bool PF, bool C16>
+template <int NT, int MINB, bool PF, bool C16>
 cudaError_t launch_quad_t1(const SamplerArgs& a, uint32_t n_units, cudaStream_t s) {
-    static bool configured = false;
-    auto kern = PF ? sampler_quad_pf_kernel<NT, MINB, L, C, C16> : sampler_quad_kernel<NT, MINB, L, C, C16>;
-    if (!configured) {
-        // 227 KB per block minus the kernel's static shared memory (the batch counter).
-        const cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 226 * 1024);
-        if (e != cudaSuccess) return e;
-        configured = true;
-    }
-    kern<<<n_units, NT, sampler_quad_smem(a, NT), s>>>(a);
+    auto kern = PF ? sampler_quad_pf_kernel<NT, MINB, 4, C16> : sampler_quad_kernel<NT, MINB, 4, C16>;
+    const size_t smem = sampler_quad_smem(a, NT);
+    if (const cudaError_t e = smem_optin(kern, smem); e != cudaSuccess) return e;
+    kern<<<n_units, NT, smem, s>>>(a);
     return cudaGetLastError();
 }
 // PF: the next round's first line is prefetched in each round's last group slot (C3 K=10K:
 // 95.5 -> 92.8 ms; short-phi C2: 19.8 -> 20.5 ms, so only the 512-thread shape uses it).
-template <int NT, int MINB, int L = 4, bool PF = (NT >= 512)>
+template <int NT, int MINB, bool PF = (NT >= 512)>
 cudaError_t launch_quad_t(const SamplerArgs& a, uint32_t n_units, cudaStream_t s) {
-    if (a.compact) return launch_quad_t1<NT, MINB, L, true, PF, false>(a, n_units, s);
-    return a.tbits == 16 ? launch_quad_t1<NT, MINB, L, false, PF, true>(a, n_units, s)
-                         : launch_quad_t1<NT, MINB, L, false, PF, false>(a, n_units, s);
+    return a.tbits == 16 ? launch_quad_t1<NT, MINB, PF, true>(a, n_units, s)
+                         : launch_quad_t1<NT, MINB, PF, false>(a, n_units, s);
 }
 
+// phi rows too large for shared memory (K_pad * 4 > ~180 KB): quad-lane kernel with only L8 staged.
 cudaError_t launch_quad_global(const SamplerArgs& a, uint32_t n_units, cudaStream_t s) {
-    static bool configured = false;
-    auto kern = a.tbits == 16 ? sampler_quad_pf_kernel<512, 2, 4, false, true, true, true>
-                              : sampler_quad_pf_kernel<512, 2, 4, false, false, true, true>;
-    if (!configured) {
-        const cudaError_t e = cudaFuncSetAttribute(sampler_quad_pf_kernel<512, 2, 4, false, true, true, true>,
-                                                   cudaFuncAttributeMaxDynamicSharedMemorySize, 226 * 1024);
-        if (e != cudaSuccess) return e;
-        const cudaError_t e2 = cudaFuncSetAttribute(sampler_quad_pf_kernel<512, 2, 4, false, false, true, true>,
-                                                    cudaFuncAttributeMaxDynamicSharedMemorySize, 226 * 1024);
-        if (e2 != cudaSuccess) return e2;
-        configured = true;
-    }
+    auto kern = a.tbits == 16 ? sampler_quad_pf_kernel<512, 2, 4, true, true, true>
+                              : sampler_quad_pf_kernel<512, 2, 4, false, true, true>;
     const size_t smem = sizeof(float) * (static_cast<size_t>(a.l8_stride) + 16u * 32u * 17u);
+    if (const cudaError_t e = smem_optin(kern, smem); e != cudaSuccess) return e;
     kern<<<n_units, 512, smem, s>>>(a);
     return cudaGetLastError();
 }
 
-// Launch shape (SLDA_SAMPLER overrides for experiments; default by phi row size):
-//   "g2"     : round-based, 256/512-thread CTAs, 2-sector groups, 64 registers
-//   "g4"     : round-based, 256-thread CTAs, 4-sector groups, up to 128 registers
-//   "g4x512" : round-based, 512-thread CTAs, 4-sector groups (one CTA / SM at K = 10K)
-//   "s4", "s2", "s4x128" : streaming lane refill (sampler_stream_kernel)
-//   "q512", "q256"       : quad-lane (sampler_quad_kernel, L=4 lanes per token), 64 registers
-//   "p512", "p256"       : pair-lane (L=2; C2 20.7 vs 21.5 ms, C3 107.9 vs 100.0 ms)
-//   "o512"               : octet-lane (L=8; slower at both)
-//   "q512r", "q256r"     : quad-lane with a relaxed register bound (fewer warps; slower)
+int sampler_shape_from_name(const char* name) {
+    const std::string v(name ? name : "");
+    return v == "round" ? kShapeRound : v == "quad512" ? kShapeQuad512 : v == "quad256" ? kShapeQuad256
+         : v == "global" ? kShapeGlobal : -1;
+}
+
 // ---- SamplerKind::kVanilla: the reference's O(K) baseline mode ---------------------------------
 // vanilla_sample<float> over the dense count row (sampler.hpp:222-236, trainer.cpp:281-285): the
 // sequential f32 prefix running_k = running_{k-1} + (f32(n_dk) + alpha) * bhat_k over all K topics,
@@ -999,16 +674,9 @@ __global__ void __launch_bounds__(NT) sampler_vanilla_kernel(SamplerArgs a) {
 }
 
 cudaError_t launch_vanilla(const SamplerArgs& a, uint32_t n_units, cudaStream_t s) {
-    if (a.compact) return cudaErrorInvalidConfiguration;  // wide rows only
     const size_t phi_bytes = sizeof(float) * static_cast<size_t>(a.K_pad);
     if (phi_bytes <= 200 * 1024) {
-        static bool configured = false;
-        if (!configured) {
-            const cudaError_t e = cudaFuncSetAttribute(sampler_vanilla_kernel<256, false>,
-                                                       cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-            if (e != cudaSuccess) return e;
-            configured = true;
-        }
+        if (const cudaError_t e = smem_optin(sampler_vanilla_kernel<256, false>, phi_bytes); e != cudaSuccess) return e;
         sampler_vanilla_kernel<256, false><<<n_units, 256, phi_bytes, s>>>(a);
     } else {
         sampler_vanilla_kernel<256, true><<<n_units, 256, 0, s>>>(a);
@@ -1016,62 +684,35 @@ cudaError_t launch_vanilla(const SamplerArgs& a, uint32_t n_units, cudaStream_t 
     return cudaGetLastError();
 }
 
+// Launch shape by phi row size (SLDA_SAMPLER=round|quad512|quad256|global forces one where it fits):
+//   quad256 : K_pad*4 <= 24 KB (C2 K=1K, C5 K=100): 256-thread quad-lane CTAs, 4 per SM
+//   quad512 : two 512-thread quad-lane CTAs fit an SM (K_pad <= ~17.5K; C3 K=10K)
+//   round   : the phi row still fits shared memory (K_pad <= ~45K): round-based 4-sector groups
+//   global  : larger rows (C5 K=50K): quad-lane, phi gathered through L1/L2, L8 staged
+int sampler_shape(const SamplerArgs& a) {
+    if (a.vanilla) return kShapeVanilla;
+    const size_t phi_bytes = sizeof(float) * (static_cast<size_t>(a.K_pad) + a.l8_stride);
+    constexpr size_t kSm = 227 * 1024;
+    const bool q256 = phi_bytes <= 24 * 1024 && 4 * sampler_quad_smem(a, 256) <= kSm;
+    const bool q512 = 2 * sampler_quad_smem(a, 512) <= kSm;
+    const bool round = sampler_smem(a, 256, 4) <= kSm;
+    int shape = a.shape;
+    if (shape == kShapeQuad256 && sampler_quad_smem(a, 256) > kSm) shape = -1;
+    if (shape == kShapeQuad512 && sampler_quad_smem(a, 512) > kSm) shape = -1;
+    if (shape == kShapeRound && !round) shape = -1;
+    if (shape < 0) shape = q256 ? kShapeQuad256 : q512 ? kShapeQuad512 : round ? kShapeRound : kShapeGlobal;
+    return shape;
+}
+
 cudaError_t launch_sampler(const SamplerArgs& a, uint32_t n_units, cudaStream_t s) {
     if (n_units == 0) return cudaSuccess;
-    if (a.vanilla) return launch_vanilla(a, n_units, s);
-    const size_t phi_bytes = sizeof(float) * (static_cast<size_t>(a.K_pad) + a.l8_stride);
-    // Default: the quad-lane kernel wherever two 512-thread (or four 256-thread) CTAs fit an SM
-    // (C3 K=10K: 100.0 vs 102.6 ms for 4-sector groups; C2 K=1K: 21.5 vs 23.5 ms for 2-sector
-    // groups), else 4-sector groups (large phi rows), else 2-sector groups.
-    int shape = a.shape;
-    if (shape < 0) {
-        if (phi_bytes <= 24 * 1024 && 4 * sampler_quad_smem(a, 256) <= 227 * 1024) shape = 7;
-        else if (2 * sampler_quad_smem(a, 512) <= 227 * 1024) shape = 6;
+    switch (sampler_shape(a)) {
+        case kShapeVanilla: return launch_vanilla(a, n_units, s);
+        case kShapeQuad256: return launch_quad_t<256, 4>(a, n_units, s);
+        case kShapeQuad512: return launch_quad_t<512, 2>(a, n_units, s);
+        case kShapeRound: return launch_round(a, n_units, s);
+        default: return launch_quad_global(a, n_units, s);
     }
-    if (shape < 0) shape = phi_bytes > 24 * 1024 ? 1 : 0;
-    const bool fits512 = sampler_smem(a, 512, 2, false) <= 227 * 1024;
-    if (!fits512) {
-        // Rows that do not fit shared memory (K > kCompactMaxK, so always the wide format):
-        // gather phi through L1/L2 -- the quad-lane kernel with only L8 staged (C5 K=50K), or
-        // the round-based kernel when asked for (shape 0..2).
-        if (a.compact) return cudaErrorInvalidConfiguration;
-        const size_t gsm = sizeof(float) * (static_cast<size_t>(a.l8_stride) + 16u * 32u * 17u);
-        if (a.shape < 0 && 2 * gsm <= 227 * 1024) return launch_quad_global(a, n_units, s);
-        return launch_sampler_t<512, 2, 2, true, false>(a, n_units, s);
-    }
-    if (shape == 6 && sampler_quad_smem(a, 512) <= 227 * 1024)
-        return launch_quad_t<512, 2>(a, n_units, s);
-    if (shape == 7 && sampler_quad_smem(a, 256) <= 227 * 1024)
-        return launch_quad_t<256, 4>(a, n_units, s);
-    if (shape == 8 && sampler_quad_smem(a, 512) <= 227 * 1024)
-        return launch_quad_t<512, 1>(a, n_units, s);
-    if (shape == 9 && sampler_quad_smem(a, 256) <= 227 * 1024)
-        return launch_quad_t<256, 3>(a, n_units, s);
-    if (shape == 10 && sampler_quad_smem(a, 512) <= 227 * 1024)
-        return launch_quad_t<512, 2, 2>(a, n_units, s);
-    if (shape == 11 && sampler_quad_smem(a, 256) <= 227 * 1024)
-        return launch_quad_t<256, 4, 2>(a, n_units, s);
-    if (shape == 12 && sampler_quad_smem(a, 512) <= 227 * 1024)
-        return launch_quad_t<512, 2, 8>(a, n_units, s);
-    if (!a.compact && shape == 3 && sampler_smem(a, 256, 4, false) <= 227 * 1024)
-        return launch_stream_t<256, 4>(a, n_units, s);
-    if (!a.compact && shape == 4 && sampler_smem(a, 256, 2, false) <= 227 * 1024)
-        return launch_stream_t<256, 2>(a, n_units, s);
-    if (!a.compact && shape == 5 && sampler_smem(a, 128, 4, false) <= 227 * 1024)
-        return launch_stream_t<128, 4>(a, n_units, s);
-    if (shape == 1 && sampler_smem(a, 256, 4, false) <= 227 * 1024)
-        return a.compact ? launch_sampler_t<256, 4, 2, false, true>(a, n_units, s)
-                         : launch_sampler_t<256, 4, 2, false, false>(a, n_units, s);
-    if (shape == 2 && sampler_smem(a, 512, 4, false) <= 227 * 1024)
-        return a.compact ? launch_sampler_t<512, 4, 1, false, true>(a, n_units, s)
-                         : launch_sampler_t<512, 4, 1, false, false>(a, n_units, s);
-    // Small phi rows: 256-thread CTAs.  Large (K = 10K): 512 threads share one staged row
-    // (2 CTAs x 16 warps per SM).
-    if (phi_bytes <= 24 * 1024)
-        return a.compact ? launch_sampler_t<256, 2, 4, false, true>(a, n_units, s)
-                         : launch_sampler_t<256, 2, 4, false, false>(a, n_units, s);
-    return a.compact ? launch_sampler_t<512, 2, 2, false, true>(a, n_units, s)
-                     : launch_sampler_t<512, 2, 2, false, false>(a, n_units, s);
 }
 
 }  // namespace slda

@@ -508,7 +508,7 @@ std::vector<std::uint32_t> shard_bounds(const Corpus& corpus, std::uint32_t worl
 }
 
 ModelState init_shard(const Corpus& corpus, const TrainConfig& raw_cfg, std::uint32_t rank,
-                      std::uint32_t world, const void* nccl_id) {
+                      std::uint32_t world) {
     const TrainConfig cfg = raw_cfg.resolved(corpus);
     if (rank >= world) throw ValidationError("rank must be < world");
     // The reference's corpus-wide topic rule (trainer.cpp:369-378), decided once for all shards.
@@ -555,7 +555,6 @@ ModelState init_shard(const Corpus& corpus, const TrainConfig& raw_cfg, std::uin
     c.device = cfg.device;
     c.rank = rank;
     c.world_size = world;
-    c.nccl_id = nccl_id;
     slda_engine* eng = nullptr;
     check(slda_create(&view, &c, &eng));
     ModelState s;
@@ -573,7 +572,7 @@ ModelState init_shard(const Corpus& corpus, const TrainConfig& raw_cfg, std::uin
 }
 
 ModelState init_view(const slda_corpus_view& view, const TrainConfig& raw_cfg, std::uint32_t rank,
-                     std::uint32_t world, const void* nccl_id, std::uint32_t init_mode) {
+                     std::uint32_t world, std::uint32_t init_mode) {
     Corpus shape;
     shape.num_docs = view.num_docs;
     const TrainConfig cfg = raw_cfg.resolved(shape);
@@ -588,7 +587,6 @@ ModelState init_view(const slda_corpus_view& view, const TrainConfig& raw_cfg, s
     c.device = cfg.device;
     c.rank = rank;
     c.world_size = world;
-    c.nccl_id = nccl_id;
     slda_engine* eng = nullptr;
     check(slda_create(&view, &c, &eng));
     ModelState s;
@@ -778,6 +776,10 @@ std::uint32_t WaryTree::sample(double x) const {
 
 // Text format of save_checkpoint (trainer.cpp:469-478) + dump_word_topic (counts.cpp:140-150).
 void save_checkpoint(const std::filesystem::path& path, const ModelState& state) {
+    // A document shard holds only its own documents' assignments (and word_topic() is a
+    // collective), so its file would carry the global C_wk with the shard's T: refuse it.
+    if (state.engine() && state.info().world_size > 1)
+        throw ValidationError("save_checkpoint: model is one document shard of a multi-GPU run (world_size > 1)");
     std::ofstream out(path, std::ios::trunc);
     if (!out) throw IoError("cannot write checkpoint " + path.string());
     out << "sparselda-checkpoint 1 " << state.num_docs << ' ' << state.vocab_size << ' ' << state.num_tokens

@@ -182,26 +182,25 @@ private:
     bool has_chunks_ = false;
 
     friend ModelState init_state(const Corpus&, const TrainConfig&);
-    friend ModelState init_shard(const Corpus&, const TrainConfig&, std::uint32_t, std::uint32_t,
-                                 const void*);
+    friend ModelState init_shard(const Corpus&, const TrainConfig&, std::uint32_t, std::uint32_t);
     friend ModelState init_view(const slda_corpus_view&, const TrainConfig&, std::uint32_t, std::uint32_t,
-                                const void*, std::uint32_t);
+                                std::uint32_t);
     friend ModelState model_from_counts(std::uint32_t, std::uint32_t, const std::vector<std::uint32_t>&,
                                         std::uint64_t, std::uint32_t, double, double, std::uint64_t, int);
     friend IterationStats run_iteration(ModelState&, const TrainConfig&);
 };
 
 ModelState init_state(const Corpus& corpus, const TrainConfig& cfg);          // trainer.hpp:172
-// Document shard `rank` of `world` (one process per GPU, NCCL over NVLink): the shard
+// Document shard `rank` of `world` (one process per GPU, peer-memory exchange over NVLink): the shard
 // is the rank-th contiguous document range of the chunk_boundaries rule
 // (corpus.cpp:103-121).  Collective over all ranks.
 std::vector<std::uint32_t> shard_bounds(const Corpus& corpus, std::uint32_t world);
 ModelState init_shard(const Corpus& corpus, const TrainConfig& cfg, std::uint32_t rank,
-                      std::uint32_t world, const void* nccl_id);
+                      std::uint32_t world);
 // Engine over a borrowed corpus view (already sharded by the caller); the config is
 // validated as TrainConfig::resolved would for a corpus of view.num_docs documents.
 ModelState init_view(const slda_corpus_view& view, const TrainConfig& cfg, std::uint32_t rank,
-                     std::uint32_t world, const void* nccl_id, std::uint32_t init_mode);
+                     std::uint32_t world, std::uint32_t init_mode);
 IterationStats run_iteration(ModelState& state, const TrainConfig& cfg);      // trainer.hpp:177
 using HeldoutProbe = std::function<double(ModelState&)>;
 ModelState train(const Corpus& corpus, const TrainConfig& cfg, const MetricsSink& sink = {},

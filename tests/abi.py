@@ -27,7 +27,7 @@ class Config(C.Structure):
     _fields_ = [("num_topics", C.c_uint32), ("alpha", C.c_double), ("beta", C.c_double),
                 ("seed", C.c_uint64), ("tree_branch", C.c_uint32), ("init_mode", C.c_uint32),
                 ("device", C.c_int32), ("rank", C.c_uint32), ("world_size", C.c_uint32),
-                ("nccl_id", C.c_void_p), ("sampler", C.c_uint32)]
+                ("sampler", C.c_uint32)]
 
 
 class IterationStats(C.Structure):
@@ -41,12 +41,13 @@ class Info(C.Structure):
                 ("doc_end", C.c_uint32), ("rank", C.c_uint32), ("world_size", C.c_uint32),
                 ("alpha", C.c_double), ("beta", C.c_double), ("seed", C.c_uint64),
                 ("num_segments", C.c_uint32), ("num_units", C.c_uint32), ("doc_topic_nnz", C.c_uint64),
-                ("device_bytes", C.c_uint64), ("doc_major", C.c_uint32), ("padded_topics", C.c_uint32)]
+                ("device_bytes", C.c_uint64), ("doc_major", C.c_uint32), ("padded_topics", C.c_uint32),
+                ("sampler_shape", C.c_uint32)]
 
 
 class KernelTimes(C.Structure):
     _fields_ = [("reset_ms", C.c_double), ("sampler_ms", C.c_double), ("ssc_ms", C.c_double),
-                ("colsum_ms", C.c_double), ("phi_ms", C.c_double), ("comm_ms", C.c_double),
+                ("colsum_ms", C.c_double), ("phi_ms", C.c_double), ("join_ms", C.c_double),
                 ("total_ms", C.c_double), ("sampler_row_entries", C.c_uint64), ("launches", C.c_uint32)]
 
 

@@ -24,3 +24,10 @@ def golden():
     import json
 
     return json.loads((REPO / "tests" / "golden" / "reference_digests.json").read_text())
+
+
+@pytest.fixture(scope="session")
+def golden_big():
+    import json
+
+    return json.loads((REPO / "tests" / "golden" / "reference_digests_big.json").read_text())

@@ -70,3 +70,24 @@ CASES: dict[str, dict] = {
                        "K": 300, "alpha": 0.2, "seed": 5, "iterations": 4, "chunks": 3, "workers": 4,
                        "sampler": "vanilla"},
 }
+
+
+# Throughput-config cases (BASELINE.json configs), pinned bit for bit against digests the
+# reference itself produced (tests/golden/reference_digests_big.json, make_golden.py --big;
+# the reference ran with 8 workers and 32 chunks -- its results do not depend on either,
+# acceptance.cpp:389-445).  They run the engine's DEFAULT kernel selection (no SLDA_* knobs).
+BIG_CASES: dict[str, dict] = {
+    # BASELINE configs[1] exactly: NYTimes-shaped D=300K, V=100K, T=100M, K=1K (heavy words split
+    # into 8192-token units, multi-batch claiming in the 256-thread quad kernel).
+    "c2_full": {"corpus": {"family": G, "D": 300_000, "V": 100_000, "T": 100_000_000, "seed": 20161008},
+                "K": 1000, "seed": 42, "iterations": 3, "chunks": 32, "workers": 8},
+    # PubMed-shaped (configs[2]) at a third of a GPU-hour of reference CPU time: V=141K, K=10,000,
+    # T/D = 90, 25M tokens; 199 words exceed the 8192-token unit cap (the longest has 30,426
+    # tokens), so split units and the 512-thread prefetching quad kernel run as in the bench.
+    "pubmed_k10k": {"corpus": {"family": G, "D": 280_000, "V": 141_000, "T": 25_000_000, "seed": 20161008},
+                    "K": 10_000, "seed": 42, "iterations": 3, "chunks": 32, "workers": 8},
+    # C5's K=50,000 point (configs[4]) at a reduced vocabulary: tree_branch 41, the phi row does
+    # not fit shared memory (global-phi quad kernel).
+    "c5_k50k_small": {"corpus": {"family": G, "D": 6_000, "V": 5_000, "T": 2_000_000, "seed": 20161008},
+                      "K": 50_000, "seed": 42, "iterations": 3, "chunks": 32, "workers": 8},
+}

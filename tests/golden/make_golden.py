@@ -13,6 +13,7 @@ Corpora come from the product's host-only synthetic generator
 stores the corpus digest so generator drift is caught.
 
     make oracle && python tests/golden/make_golden.py
+    python tests/golden/make_golden.py --big [NAME...]   # the throughput-config cases
 """
 from __future__ import annotations
 
@@ -27,7 +28,7 @@ sys.path.insert(0, str(HERE.parent))
 sys.path.insert(0, str(HERE.parent.parent))
 
 from oracle_lib import RefModel, digest, ref_lib  # noqa: E402
-from corpora import corpus_arrays, CASES  # noqa: E402
+from corpora import corpus_arrays, BIG_CASES, CASES  # noqa: E402
 
 
 def run_case(name: str, spec: dict) -> dict:
@@ -89,18 +90,21 @@ def main() -> None:
     """`make_golden.py` regenerates every case; `make_golden.py NAME...` (re)generates only
     those cases and keeps the others from the committed file."""
     only = sys.argv[1:]
-    path = HERE / "reference_digests.json"
-    if only:
+    cases, path = CASES, HERE / "reference_digests.json"
+    if only and only[0] == "--big":
+        only = only[1:]
+        cases, path = BIG_CASES, HERE / "reference_digests_big.json"
+    if (only or cases is BIG_CASES) and path.exists():
         fixtures = json.loads(path.read_text())
     else:
         fixtures = {"kats": kats(), "cases": {}}
-    for name, spec in CASES.items():
+    for name, spec in cases.items():
         if only and name not in only:
             continue
         print("case", name, flush=True)
         fixtures["cases"][name] = run_case(name, spec)
-    (HERE / "reference_digests.json").write_text(json.dumps(fixtures, indent=1, sort_keys=True))
-    print("wrote", HERE / "reference_digests.json")
+        path.write_text(json.dumps(fixtures, indent=1, sort_keys=True))
+    print("wrote", path)
 
 
 if __name__ == "__main__":

@@ -20,6 +20,7 @@ import numpy as np
 REPO = Path(__file__).resolve().parent.parent
 ORACLE_SO = REPO / "oracle" / "liboracle.so"
 REF_SO = REPO / "oracle" / "_ref" / "libsparselda_ref.so"
+GEN_SO = REPO / "oracle" / "libcorpusgen.so"
 
 _u32p = np.ctypeslib.ndpointer(dtype=np.uint32, flags="C_CONTIGUOUS")
 _u64p = np.ctypeslib.ndpointer(dtype=np.uint64, flags="C_CONTIGUOUS")
@@ -332,6 +333,44 @@ class RefModel(_ModelBase):
         if getattr(self, "h", None):
             ref_lib().ref_free(self.h)
             self.h = None
+
+
+class _GenParams(C.Structure):  # slda_gen_params (include/saberlda.h)
+    _fields_ = [("family", C.c_uint32), ("num_docs", C.c_uint32), ("vocab_size", C.c_uint32),
+                ("num_tokens", C.c_uint64), ("latent_topics", C.c_uint32), ("zipf_s", C.c_double),
+                ("doc_dirichlet", C.c_double), ("length_sigma", C.c_double), ("seed", C.c_uint64),
+                ("threads", C.c_uint32)]
+
+
+class CorpusGen:
+    """The synthetic-corpus generator built on its own (oracle/libcorpusgen.so, from
+    paper_1610_02496_b200/csrc/corpus_gen.cpp): the workload of bench.py's reference arm,
+    generated without loading the product's libraries."""
+
+    def __init__(self, family, D, V, T, seed=20161008, latent_topics=100, threads=0):
+        self.lib = C.CDLL(str(GEN_SO))
+        self.lib.slda_gen_last_error.restype = C.c_char_p
+        self.p = _GenParams(family=family, num_docs=D, vocab_size=V, num_tokens=T, latent_topics=latent_topics,
+                            seed=seed, threads=threads)
+        self.D = D
+
+    def _check(self, rc):
+        if rc != 0:
+            raise ValueError(self.lib.slda_gen_last_error().decode())
+
+    def doc_lengths(self) -> np.ndarray:
+        out = np.empty(self.D, np.uint32)
+        self._check(self.lib.slda_generate_doc_lengths(C.byref(self.p), out.ctypes.data_as(C.c_void_p)))
+        return out
+
+    def docs(self, doc_begin: int, doc_end: int, lengths: np.ndarray | None = None) -> np.ndarray:
+        """(T, 3) tokens (doc, word, kInvalidTopic) of documents [doc_begin, doc_end)."""
+        lens = self.doc_lengths() if lengths is None else lengths
+        n = int(lens[doc_begin:doc_end].astype(np.int64).sum())
+        out = np.empty((n, 3), np.uint32)
+        self._check(self.lib.slda_generate_docs(C.byref(self.p), doc_begin, doc_end,
+                                                out.ctypes.data_as(C.c_void_p), C.c_uint64(n)))
+        return out
 
 
 def random_corpus(num_docs: int, vocab: int, mean_len: float, seed: int):

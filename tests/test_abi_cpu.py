@@ -16,7 +16,7 @@ def test_library_exports_every_declared_symbol():
     assert len(syms) >= 25
     missing = [s for s in syms if not hasattr(lib, s)]
     assert missing == []
-    assert lib.slda_abi_version() == 2
+    assert lib.slda_abi_version() == 3
 
 
 def test_shard_bounds_follow_chunk_boundaries():
@@ -187,3 +187,18 @@ def test_config_validation_without_gpu():
     cfg.num_topics = 40000  # beyond 32^3 (test_trainer.cpp:250-252)
     with pytest.raises(ValueError):
         slda.train(c, cfg)
+
+
+def test_standalone_generator_equals_the_products():
+    """oracle/libcorpusgen.so (bench.py's reference-arm workload) is the product's generator
+    source compiled on its own: same lengths and tokens, whole corpus and a document range."""
+    import paper_1610_02496_b200._core as core
+    from oracle_lib import CorpusGen
+
+    for family, D, V, T in ((0, 700, 900, 60_000), (1, 300, 250, 9_000)):
+        gen = CorpusGen(family, D, V, T, seed=77)
+        toks, lens = core.generate_tokens(family, D, V, T, seed=77)
+        assert np.array_equal(gen.doc_lengths(), lens)
+        assert np.array_equal(gen.docs(0, D), toks)
+        part, _ = core.generate_tokens(family, D, V, T, seed=77, doc_begin=100, doc_end=250)
+        assert np.array_equal(gen.docs(100, 250), part)

@@ -10,7 +10,7 @@ compared with a stated tolerance (device log vs glibc log: |rel| <= 1e-12).
 import numpy as np
 import pytest
 
-from corpora import CASES, G, U, corpus_arrays
+from corpora import BIG_CASES, CASES, G, U, corpus_arrays
 from oracle_lib import OracleModel, digest
 
 pytestmark = pytest.mark.gpu
@@ -25,6 +25,7 @@ def slda():
 
 
 def make_model(spec, iterations=None):
+    """init_state through the public API (pybind -> C++ shim -> C-ABI)."""
     s = slda()
     doc, word, D, V = corpus_arrays(spec["corpus"])
     topic = None
@@ -70,21 +71,6 @@ def test_engine_matches_reference_every_iteration(name, golden):
             assert st.iteration == it + 1
             assert st.tokens == fx["T"]
             assert st.mean_doc_topics == fx["mean_doc_topics"][it]
-
-
-@pytest.mark.parametrize("name", ["c1", "long_docs", "empty_docs", "u_k7_chunks", "k1", "vanilla_c1"])
-def test_compact_rows_match_reference(name, golden, monkeypatch):
-    """The opt-in compact C_dk row format (SLDA_ROW_FORMAT=compact) is bit-identical too
-    (the vanilla mode keeps the wide rows whatever the setting)."""
-    monkeypatch.setenv("SLDA_ROW_FORMAT", "compact")
-    spec = CASES[name]
-    fx = golden["cases"][name]
-    m, cfg, _ = make_model(spec)
-    iters = min(spec["iterations"], 10)
-    for it in range(iters + 1):
-        assert model_digests(m) == fx["iterations"][it], (name, it)
-        if it < iters:
-            m.run_iteration(cfg)
 
 
 @pytest.mark.parametrize("name", sorted(n for n, s in CASES.items() if s.get("pdow")))
@@ -281,28 +267,55 @@ def test_checkpoint_roundtrip_and_resume(tmp_path):
     assert len(text) == 1 + half.num_tokens + 1 + int((half.word_topic() != 0).sum())
 
 
-VARIANT_CASES = ["c1", "long_docs", "empty_docs", "shuffled", "k_large", "nytimes_small", "k1"]
+VARIANT_CASES = ["c1", "long_docs", "empty_docs", "k_large", "nytimes_small", "k1"]
 
 
-@pytest.mark.parametrize("variant", ["SLDA_SAMPLER=g2", "SLDA_SAMPLER=g4", "SLDA_SAMPLER=s4", "SLDA_SAMPLER=q256", "SLDA_SAMPLER=p256",
-                                     "SLDA_SAMPLER=q512", "SLDA_SSC=sort", "SLDA_PHI_SHAPE=16x8",
-                                     "SLDA_PHI_SHAPE=32x3", "SLDA_PHI_SHAPE=64x2"])
+@pytest.mark.parametrize("variant", ["SLDA_SAMPLER=round", "SLDA_SAMPLER=quad512", "SLDA_SAMPLER=quad256",
+                                     "SLDA_SAMPLER=global", "SLDA_PHI_SHAPE=16x8", "SLDA_PHI_SHAPE=32x3",
+                                     "SLDA_PHI_SHAPE=64x2"])
 @pytest.mark.parametrize("name", VARIANT_CASES)
 def test_kernel_variants_match_reference(name, variant, golden, monkeypatch):
-    """Every sampler launch shape (round-based 2/4-sector groups, streaming lane refill,
-    quad-lane), both SSC kernels (bitmap, bitonic sort) and every phi tile shape give the
-    reference's digests.  Sampler/SSC variants are read when the engine is built (engine.cu
-    configure), the phi shape at each launch."""
+    """Every sampler launch shape (quad-lane 256/512-thread CTAs, the round-based kernel, the
+    global-phi quad kernel) and every phi tile shape gives the reference's digests, whichever
+    shape the default selection would pick for the case.  The sampler shape is read when the
+    engine is built (engine.cu), the phi shape at each launch."""
     key, value = variant.split("=")
     monkeypatch.setenv(key, value)
     spec = CASES[name]
     fx = golden["cases"][name]
     m, cfg, _ = make_model(spec)
-    iters = min(spec["iterations"], 10)
+    iters = min(spec["iterations"], 6)
     for it in range(iters + 1):
         assert model_digests(m) == fx["iterations"][it], (name, variant, it)
         if it < iters:
             m.run_iteration(cfg)
+
+
+# Default kernel selection per throughput case (sampler.cu launch_sampler): the shape the bench
+# configs run.
+BIG_SHAPES = {"c2_full": "quad256", "pubmed_k10k": "quad512", "c5_k50k_small": "global"}
+
+
+@pytest.mark.parametrize("name", sorted(BIG_CASES))
+def test_throughput_configs_match_reference_every_iteration(name, golden_big, monkeypatch):
+    """BASELINE's throughput configs (C2 exactly; PubMed-shaped K=10,000 at 25M tokens; C5's
+    K=50,000) against digests the reference itself produced, at every iteration, through the
+    DEFAULT kernel selection: heavy words split into 8192-token units with in-CTA batch claiming,
+    the 512-thread prefetching quad-lane kernel at K=10K, the global-phi kernel at K=50K."""
+    for k in ("SLDA_SAMPLER", "SLDA_PHI_SHAPE", "SLDA_SERIAL"):
+        monkeypatch.delenv(k, raising=False)
+    spec = BIG_CASES[name]
+    fx = golden_big["cases"][name]
+    m, cfg, _ = make_model(spec)
+    info = m.info()
+    assert info["sampler_shape"] == BIG_SHAPES[name]
+    assert info["num_units"] > info["num_segments"]  # some words were split (> 8192 tokens)
+    for it, expect in enumerate(fx["iterations"]):
+        got = model_digests(m)
+        assert got == expect, (name, it, sorted(k for k in got if got[k] != expect[k]))
+        if it + 1 < len(fx["iterations"]):
+            st = m.run_iteration(cfg)
+            assert st.mean_doc_topics == fx["mean_doc_topics"][it]
 
 
 def test_acceptance_sublinear_scaling_in_k():

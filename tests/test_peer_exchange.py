@@ -1,13 +1,13 @@
-"""GPU, world_size 2 on ONE B200: the peer-memory M-step exchange, bit for bit.
+"""GPU, world_size 2, 4 and 8 on ONE B200: the peer-memory M-step exchange, bit for bit.
 
-Two processes each own a document shard (the chunk_boundaries rule) and an engine created
-without an NCCL id; they exchange CUDA IPC handles of their C_wk / C_k / phi / L4 / L8 / Q
+N processes each own a document shard (the chunk_boundaries rule) and an engine created
+with world_size N; they exchange CUDA IPC handles of their C_wk / C_k / phi / L4 / L8 / Q
 buffers and attach (include/saberlda.h, slda_peer_attach).  From then on every M-step does the
 reduce-scatter of C_wk inside its colsum kernel, the all-reduce of C_k inside the denominator
 kernel and the all-gather of phi / L4 / L8 / Q inside the phi kernel's epilogue, over the other
 rank's memory, meeting at device-side barriers (mstep.cu).  On a multi-GPU node the same code
-runs over NVLink peer memory; here both ranks share one GPU, which exercises the same kernels,
-handles and barriers.  The assembled state must equal the reference's digests for the C1 case
+runs over NVLink peer memory; here all ranks share one GPU, which exercises the same kernels,
+handles, barrier targets, word-row slices and mirror lists (PeerMirror.n = N-1 up to 7).  The assembled state must equal the reference's digests for the C1 case
 at every iteration -- exactly what one GPU produces.
 """
 import multiprocessing as mp
@@ -21,11 +21,10 @@ from oracle_lib import digest
 
 pytestmark = pytest.mark.gpu
 
-WORLD = 2
 ITERS = 6
 
 
-def _rank_main(rank, case, to_parent, from_parent):
+def _rank_main(rank, world, case, to_parent, from_parent):
     try:
         import paper_1610_02496_b200 as slda
         import paper_1610_02496_b200._core as core
@@ -33,7 +32,7 @@ def _rank_main(rank, case, to_parent, from_parent):
         spec = CASES[case]
         doc, word, D, V = corpus_arrays(spec["corpus"])
         lens = np.bincount(doc, minlength=D).astype(np.uint32)
-        bounds = core.shard_bounds_from_lengths(lens, WORLD)
+        bounds = core.shard_bounds_from_lengths(lens, world)
         b, e = bounds[rank], bounds[rank + 1]
         csum = np.concatenate([[0], np.cumsum(lens.astype(np.int64))])
         sel = slice(int(csum[b]), int(csum[e]))
@@ -45,7 +44,7 @@ def _rank_main(rank, case, to_parent, from_parent):
         cfg.device = 0
         if spec.get("sampler") == "vanilla":
             cfg.sampler = slda.SamplerKind.VANILLA
-        m = core.init_view(toks, D, V, int(b), int(e), int(csum[b]), cfg, rank, WORLD, b"", 1)
+        m = core.init_view(toks, D, V, int(b), int(e), int(csum[b]), cfg, rank, world, 1)
         to_parent.put(("handles", rank, m.peer_handles()))
         all_handles = from_parent.get()
         m.peer_attach(all_handles)
@@ -67,25 +66,25 @@ def _rank_main(rank, case, to_parent, from_parent):
         to_parent.put(("error", rank, traceback.format_exc()))
 
 
-@pytest.mark.parametrize("case", ["c1", "vanilla_c1"])
-def test_peer_memory_exchange_matches_reference(golden, case):
+@pytest.mark.parametrize("case,world", [("c1", 2), ("c1", 4), ("c1", 8), ("vanilla_c1", 2), ("u_k7_chunks", 3)])
+def test_peer_memory_exchange_matches_reference(golden, case, world):
     ctx = mp.get_context("spawn")
     to_parent = ctx.Queue()
-    inboxes = [ctx.Queue() for _ in range(WORLD)]
-    procs = [ctx.Process(target=_rank_main, args=(r, case, to_parent, inboxes[r])) for r in range(WORLD)]
+    inboxes = [ctx.Queue() for _ in range(world)]
+    procs = [ctx.Process(target=_rank_main, args=(r, world, case, to_parent, inboxes[r])) for r in range(world)]
     for p in procs:
         p.start()
     handles, results = {}, {}
     try:
-        while len(results) < WORLD:
+        while len(results) < world:
             kind, rank, payload = to_parent.get(timeout=600)
             if kind == "error":
                 raise AssertionError(f"rank {rank} failed:\n{payload}")
             if kind == "handles":
                 handles[rank] = payload
-                if len(handles) == WORLD:
+                if len(handles) == world:
                     for q in inboxes:
-                        q.put([handles[r] for r in range(WORLD)])
+                        q.put([handles[r] for r in range(world)])
             else:
                 results[rank] = payload
     finally:
@@ -95,21 +94,26 @@ def test_peer_memory_exchange_matches_reference(golden, case):
                 p.kill()
     fx = golden["cases"][case]
     for it in range(min(ITERS, len(fx["iterations"]) - 1) + 1):
-        r0, r1 = results[0][it], results[1][it]
-        # Replicated state: identical on both ranks.
+        rs = [results[r][it] for r in range(world)]
+        # Replicated state: identical on every rank.
         for key in ("word_topic", "word_topic_prob", "l4", "tree_mass"):
-            assert np.array_equal(r0[key], r1[key]), (it, key)
-        offs0, t0, c0 = r0["doc_topic"]
-        offs1, t1, c1 = r1["doc_topic"]
-        offs = np.concatenate([offs0, offs1[1:] + offs0[-1]])
+            for r in range(1, world):
+                assert np.array_equal(rs[0][key], rs[r][key]), (it, key, r)
+        offs, tops, cnts = [rs[0]["doc_topic"][0]], [], []
+        for r in range(world):
+            o, t, c = rs[r]["doc_topic"]
+            if r:
+                offs.append(o[1:] + offs[-1][-1])
+            tops.append(t)
+            cnts.append(c)
         got = {
-            "assignments": digest(np.concatenate([r0["assignments"], r1["assignments"]])),
-            "word_topic": digest(r0["word_topic"]),
-            "word_topic_prob": digest(r0["word_topic_prob"]),
-            "l4": digest(r0["l4"]),
-            "tree_mass": digest(r0["tree_mass"]),
-            "doc_topic": digest(np.concatenate([offs.view(np.uint32), np.concatenate([t0, t1]),
-                                                np.concatenate([c0, c1])])),
+            "assignments": digest(np.concatenate([rs[r]["assignments"] for r in range(world)])),
+            "word_topic": digest(rs[0]["word_topic"]),
+            "word_topic_prob": digest(rs[0]["word_topic_prob"]),
+            "l4": digest(rs[0]["l4"]),
+            "tree_mass": digest(rs[0]["tree_mass"]),
+            "doc_topic": digest(np.concatenate([np.concatenate(offs).view(np.uint32), np.concatenate(tops),
+                                                np.concatenate(cnts)])),
         }
         expect = fx["iterations"][it]
-        assert got == expect, (it, sorted(k for k in got if got[k] != expect[k]))
+        assert got == expect, (world, it, sorted(k for k in got if got[k] != expect[k]))
