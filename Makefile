@@ -26,7 +26,9 @@ PY_INC  := $(shell $(PYTHON) -c "import sysconfig; print(sysconfig.get_paths()['
 PYBIND_INC := $(shell $(PYTHON) -c "import pybind11; print(pybind11.get_include())")
 MOD     := $(PKG)/_core$(PY_EXT)
 
-all: $(LIB) $(MOD)
+CLI     := $(PKG)/sparselda
+
+all: $(LIB) $(MOD) $(CLI)
 
 $(BUILD):
 	mkdir -p $(BUILD)
@@ -53,11 +55,18 @@ $(MOD): $(BUILD)/module.o $(BUILD)/sparselda_b200.o $(LIB)
 	$(CXX) -shared -o $@ $(BUILD)/module.o $(BUILD)/sparselda_b200.o -L$(PKG) -lsaberlda \
 	    -Wl,-rpath,'$$ORIGIN'
 
+$(BUILD)/cli.o: $(CSRC)/cli.cpp $(CSRC)/sparselda_b200.hpp include/saberlda.h | $(BUILD)
+	$(CXX) $(CXXFLAGS) -c $< -o $@
+
+# The reference CLI's replacement (proj/tools/main.cpp): train / eval / topics.
+$(CLI): $(BUILD)/cli.o $(BUILD)/sparselda_b200.o $(LIB)
+	$(CXX) -o $@ $(BUILD)/cli.o $(BUILD)/sparselda_b200.o -L$(PKG) -lsaberlda -Wl,-rpath,'$$ORIGIN'
+
 oracle:
 	$(MAKE) -C oracle all
 	if [ -d /root/reference/proj ]; then $(MAKE) -C oracle ref; fi
 
 clean:
-	rm -rf $(BUILD) $(LIB) $(PKG)/_core*.so
+	rm -rf $(BUILD) $(LIB) $(PKG)/_core*.so $(CLI)
 
 .PHONY: all oracle clean

@@ -241,6 +241,18 @@ int ref_heldout_ll(void* h, uint32_t D, uint32_t V, uint64_t T, const uint32_t* 
     }
 }
 
+// save_checkpoint (trainer.cpp:469-478) of the reference model: the byte format the device
+// checkpoint must reproduce (acceptance criterion 7, acceptance.cpp:389-421).
+int ref_save_checkpoint(void* h, const char* path) {
+    try {
+        save_checkpoint(path, static_cast<RefModel*>(h)->state);
+        return 0;
+    } catch (const std::exception& e) {
+        g_error = e.what();
+        return -1;
+    }
+}
+
 // load_docword (corpus.cpp:30-68) over a text buffer: the token count (tokens copied up to
 // cap, T x 3 uint32), or -1 with the reference's message in ref_last_error().
 int64_t ref_load_docword(const char* text, uint64_t n, uint32_t* tokens, uint64_t cap) {

@@ -706,6 +706,20 @@ std::vector<std::vector<std::pair<WordId, float>>> top_words(const ModelState& m
     return out;
 }
 
+void print_topics(std::ostream& out, const ModelState& model, const std::vector<std::string>& vocab,
+                  std::uint32_t n) {
+    const auto ranked = top_words(model, n);
+    for (TopicId k = 0; k < ranked.size(); ++k) {
+        out << "topic " << k << ':';
+        for (const auto& [word, prob] : ranked[k]) {
+            char p[48];
+            std::snprintf(p, sizeof(p), "%.6f", prob);
+            out << ' ' << (word < vocab.size() && !vocab[word].empty() ? vocab[word] : std::to_string(word)) << ':' << p;
+        }
+        out << '\n';
+    }
+}
+
 // ------------------------------------------------------ building blocks --
 
 SparseTopicRow segmented_count(std::span<const TopicId> segment) {

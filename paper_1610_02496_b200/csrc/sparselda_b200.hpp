@@ -222,6 +222,9 @@ EvalReport heldout_ll(ModelState& model, const Corpus& heldout, std::uint32_t bu
                       unsigned workers = 1, std::uint64_t seed = 0);
 double throughput_mtokens(std::uint64_t tokens, double elapsed_s);
 std::vector<std::vector<std::pair<WordId, float>>> top_words(const ModelState& model, std::uint32_t n);
+// "topic k: word:prob ..." per topic (eval.cpp:163-181); vocab entries empty or missing print the id.
+void print_topics(std::ostream& out, const ModelState& model, const std::vector<std::string>& vocab,
+                  std::uint32_t n);
 
 // ------------------------------------------------------ building blocks --
 SparseTopicRow segmented_count(std::span<const TopicId> segment);  // counts.cpp:65-94

@@ -11,32 +11,52 @@ namespace slda {
 // ============================================================================
 // K4 SSC -- rebuild_doc_topic (counts.cpp:103-125) + segmented_count (:65-94).
 // Topics are already doc-grouped (the sampler writes them by slot), so the
-// shuffle is fused into the sampler's store.  Warp per document: a two-level
+// shuffle is fused into the sampler's store.  Warp per document: a lane-ranged
 // topic bitmap (below).  Long documents: CTA per document, K-bin histogram +
 // ordered compaction.
 // ============================================================================
 
-// SSC without a sort (wide rows): a two-level topic bitmap per warp.  Setting one bit per
-// token in a K-bit map (and one per 32-topic word in a K/32-bit summary) and reading the
-// map back in order yields the document's distinct topics in ascending order; each token's
-// rank among them is a popcount, so the counts are smem atomics at that rank.  Per document
-// this costs O(len + nnz) warp steps instead of the bitonic sort's O(len log^2 len), and
-// the order-free integer counts are identical to segmented_count's (counts.cpp:65-94).
-struct SscBitmapSmem {
-    uint32_t* bm0;    // K_pad/32 words (bit k = topic k present), all zero between documents
-    uint32_t* bm1;    // ceil(K_pad/1024) words (bit w = bm0[w] != 0)
-    uint16_t* wpre;   // per bm0 word: rank of its first topic
-    uint16_t* wlist;  // non-empty bm0 words in ascending order
-    uint32_t* ent;    // per rank: topic (low 16 bits) | count (high 16 bits, smem atomics)
+// SSC without a sort: a lane-ranged topic bitmap per warp.  Each token sets its topic's bit
+// in a K-bit map; lane l owns the contiguous map words [4*cq*l, 4*cq*(l+1)), so one warp
+// exclusive scan of the lanes' popcounts, plus a running prefix inside each lane's range,
+// gives every map word the rank of its first topic (wpre).  A token's rank among the
+// document's distinct topics is then wpre[word] + popc(word & below-bit mask): the counts
+// are smem atomics at that rank and the topic is a plain store there (all duplicates store
+// the same value), so the ordered (topic, count) row falls out with no sort and no emit
+// loop.  Per document this costs O(len + K/1024) warp steps; the integer counts are order
+// free, identical to segmented_count's (counts.cpp:65-94), and the row is topic-ascending
+// like rebuild_doc_topic's CSR row (counts.cpp:103-125).
+//
+// cq (16-byte map chunks per lane) is odd, so the lanes' LDS.128 chunk reads (stride 16*cq
+// bytes) hit distinct 4-bank groups in every quarter-warp phase.
+struct SscWarpSmem {
+    uint32_t* bm;    // 128*cq words (bit k = topic k present), all zero between documents
+    uint16_t* wpre;  // per map word: rank of its first topic
+    uint16_t* top;   // per rank: topic
+    uint32_t* cnt;   // per rank: count (zero between documents)
 };
 
-__device__ __forceinline__ uint32_t warp_incl_scan(uint32_t x, uint32_t lane) {
+__host__ __device__ inline uint32_t ssc_chunks_per_lane(uint32_t K_pad) {
+    const uint32_t words = (K_pad + 31u) / 32u;
+    const uint32_t cq = (words + 127u) / 128u;
+    return cq | 1u;
+}
+
+__host__ __device__ inline size_t ssc_warp_bytes(uint32_t K_pad) {
+    const size_t cq = ssc_chunks_per_lane(K_pad);
+    const size_t b = 512 * cq + 256 * cq + 2 * kSscWarpCap + 4 * kSscWarpCap;
+    return (b + 15u) & ~static_cast<size_t>(15u);
+}
+
+__device__ __forceinline__ uint32_t warp_excl_scan(uint32_t x, uint32_t lane, uint32_t& total) {
+    uint32_t incl = x;
 #pragma unroll
     for (uint32_t o = 1; o < 32; o <<= 1) {
-        const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
-        if (lane >= o) x += y;
+        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
     }
-    return x;
+    total = __shfl_sync(0xffffffffu, incl, 31);
+    return incl - x;
 }
 
 // Topics of one document striped over the warp (topic i in lane i % 32, register i / 32),
@@ -50,95 +70,107 @@ __device__ __forceinline__ void ssc_load_keys(const uint16_t* z, uint32_t n, uin
     }
 }
 
-template <int R>
-__device__ __forceinline__ uint32_t ssc_doc_bitmap(const uint32_t* key, uint32_t lane, const SscBitmapSmem& w,
-                                                   uint32_t n1, uint32_t* out_row, uint32_t tbits) {
+// One document of n <= kSscWarpCap tokens: its first 128 topics are in key[] (prefetched),
+// the rest are re-read from z (L1) by a runtime loop, so one code body serves every length
+// (several length-specialised bodies overflow the instruction cache: ncu no_instruction stalls).
+__device__ __forceinline__ uint32_t ssc_doc(const uint32_t* key, const uint16_t* z, uint32_t n, uint32_t lane,
+                                            const SscWarpSmem& w, uint32_t cq, uint32_t* out_row, uint32_t tbits) {
+    auto set_bit = [&](uint32_t k) { atomicOr(w.bm + (k >> 5), 1u << (k & 31u)); };
+    auto count = [&](uint32_t k) {
+        const uint32_t wi = k >> 5;
+        const uint32_t rank = w.wpre[wi] + __popc(w.bm[wi] & ((1u << (k & 31u)) - 1u));
+        atomicAdd(w.cnt + rank, 1u);
+        w.top[rank] = static_cast<uint16_t>(k);
+    };
 #pragma unroll
-    for (uint32_t r = 0; r < R; ++r) {
-        if (key[r] != 0xFFFFFFFFu) {
-            atomicOr(w.bm0 + (key[r] >> 5), 1u << (key[r] & 31u));
-            atomicOr(w.bm1 + (key[r] >> 10), 1u << ((key[r] >> 5) & 31u));
+    for (uint32_t r = 0; r < 4; ++r)
+        if (key[r] != 0xFFFFFFFFu) set_bit(key[r]);
+#pragma unroll 1
+    for (uint32_t i = 128 + lane; i < n; i += 32) set_bit(__ldg(z + i));
+    __syncwarp();
+    // Lane-range popcounts -> warp exclusive scan -> per-word first ranks.  Up to kScanRegs
+    // chunks per lane stay in registers between the two passes (K <= 12288: one read of the map).
+    constexpr uint32_t kScanRegs = 3;
+    const uint4* mine = reinterpret_cast<const uint4*>(w.bm) + lane * cq;
+    uint2* wp = reinterpret_cast<uint2*>(w.wpre) + lane * cq;
+    auto ranks = [](uint4 v, uint32_t& run) {
+        const uint32_t r1 = run + __popc(v.x), r2 = r1 + __popc(v.y), r3 = r2 + __popc(v.z);
+        const uint2 out = make_uint2(run | (r1 << 16), r2 | (r3 << 16));
+        run = r3 + __popc(v.w);
+        return out;
+    };
+    uint32_t nnz;
+    if (cq <= kScanRegs) {
+        uint4 v[kScanRegs];
+        uint32_t c = 0;
+#pragma unroll
+        for (uint32_t j = 0; j < kScanRegs; ++j) {
+            v[j] = j < cq ? mine[j] : make_uint4(0u, 0u, 0u, 0u);
+            c += __popc(v[j].x) + __popc(v[j].y) + __popc(v[j].z) + __popc(v[j].w);
         }
-    }
-    __syncwarp();
-    // Non-empty bm0 words in ascending order (and clear the summary).
-    uint32_t m = 0;
-    for (uint32_t b = 0; b < n1; b += 32) {
-        const uint32_t wi = b + lane;
-        const uint32_t bits0 = wi < n1 ? w.bm1[wi] : 0u;
-        const uint32_t c = __popc(bits0);
-        const uint32_t incl = warp_incl_scan(c, lane);
-        uint32_t pos = m + incl - c;
-        for (uint32_t bits = bits0; bits; bits &= bits - 1u) w.wlist[pos++] = static_cast<uint16_t>((wi << 5) | (__ffs(bits) - 1));
-        if (bits0) w.bm1[wi] = 0u;
-        m += __shfl_sync(0xffffffffu, incl, 31);
-    }
-    __syncwarp();
-    // Distinct topics in order, and each word's first rank.
-    uint32_t nnz = 0;
-    for (uint32_t b = 0; b < m; b += 32) {
-        const uint32_t e = b + lane;
-        const uint32_t wi = e < m ? w.wlist[e] : 0u;
-        const uint32_t bits0 = e < m ? w.bm0[wi] : 0u;
-        const uint32_t c = __popc(bits0);
-        const uint32_t incl = warp_incl_scan(c, lane);
-        uint32_t pos = nnz + incl - c;
-        if (e < m) w.wpre[wi] = static_cast<uint16_t>(pos);
-        for (uint32_t bits = bits0; bits; bits &= bits - 1u) w.ent[pos++] = (wi << 5) | (__ffs(bits) - 1);
-        nnz += __shfl_sync(0xffffffffu, incl, 31);
+        uint32_t run = warp_excl_scan(c, lane, nnz);
+#pragma unroll
+        for (uint32_t j = 0; j < kScanRegs; ++j)
+            if (j < cq) wp[j] = ranks(v[j], run);
+    } else {
+        uint32_t c = 0;
+#pragma unroll 1
+        for (uint32_t j = 0; j < cq; ++j) {
+            const uint4 v = mine[j];
+            c += __popc(v.x) + __popc(v.y) + __popc(v.z) + __popc(v.w);
+        }
+        uint32_t run = warp_excl_scan(c, lane, nnz);
+#pragma unroll 1
+        for (uint32_t j = 0; j < cq; ++j) wp[j] = ranks(mine[j], run);
     }
     __syncwarp();
 #pragma unroll
-    for (uint32_t r = 0; r < R; ++r) {
-        if (key[r] != 0xFFFFFFFFu) {
-            const uint32_t wi = key[r] >> 5;
-            const uint32_t rank = w.wpre[wi] + __popc(w.bm0[wi] & ((1u << (key[r] & 31u)) - 1u));
-            atomicAdd(w.ent + rank, 1u << 16);
-        }
-    }
+    for (uint32_t r = 0; r < 4; ++r)
+        if (key[r] != 0xFFFFFFFFu) count(key[r]);
+#pragma unroll 1
+    for (uint32_t i = 128 + lane; i < n; i += 32) count(__ldg(z + i));
     __syncwarp();
 #pragma unroll
-    for (uint32_t r = 0; r < R; ++r)
-        if (key[r] != 0xFFFFFFFFu) w.bm0[key[r] >> 5] = 0u;
-    {
-        for (uint32_t e = lane; e < nnz; e += 32) {
-            const uint32_t x = w.ent[e];
-            out_row[1 + e] = (x & 0xFFFFu) | ((x >> 16) << tbits);
-        }
-        const uint32_t padded = (nnz + 8u) & ~7u;
-        for (uint32_t e = nnz + 1 + lane; e < padded; e += 32) out_row[e] = 0u;
-        if (lane == 0) out_row[0] = nnz - 1u;
+    for (uint32_t r = 0; r < 4; ++r)
+        if (key[r] != 0xFFFFFFFFu) w.bm[key[r] >> 5] = 0u;
+#pragma unroll 1
+    for (uint32_t i = 128 + lane; i < n; i += 32) w.bm[__ldg(z + i) >> 5] = 0u;
+#pragma unroll 1
+    for (uint32_t e = lane; e < nnz; e += 32) {
+        const uint32_t k = w.cnt[e];
+        w.cnt[e] = 0u;
+        out_row[1 + e] = static_cast<uint32_t>(w.top[e]) | (k << tbits);
     }
+    const uint32_t padded = (nnz + 8u) & ~7u;
+    if (nnz + 1 + lane < padded) out_row[nnz + 1 + lane] = 0u;  // < 8 pad words
+    if (lane == 0) out_row[0] = nnz - 1u;
     __syncwarp();
     return nnz;
 }
 
-// Warps per CTA (C3, SSC alone / whole iteration): 2 -> 6.22 / 99.85 ms, 4 -> 6.26 / 99.87,
-// 8 -> 6.45 / 100.16, 16 -> 6.57 / 100.40; smaller CTAs hand SMs back to the M-step sooner.
-constexpr uint32_t kSscBmWarps = 4;
+// Warps per CTA: short-lived 4-warp CTAs hand SMs back to the concurrent M-step sooner
+// (bitmap SSC, C3, SSC alone / whole iteration: 2 -> 6.22 / 99.85 ms, 4 -> 6.26 / 99.87,
+// 8 -> 6.45 / 100.16, 16 -> 6.57 / 100.40).
+constexpr uint32_t kSscWarps = 4;
 
-__host__ __device__ inline size_t ssc_bitmap_warp_bytes(uint32_t K_pad) {
-    const size_t n0 = (K_pad + 31u) / 32u, n1 = (n0 + 31u) / 32u;
-    const size_t b = 4 * n0 + 4 * n1 + 4 * kSscWarpCap + 2 * n0 + 2 * kSscWarpCap;
-    return (b + 15u) & ~static_cast<size_t>(15u);
-}
-
-__global__ void __launch_bounds__(kSscBmWarps * 32) ssc_bitmap_kernel(SscArgs a) {
+__global__ void __launch_bounds__(kSscWarps * 32, 8) ssc_warp_kernel(SscArgs a) {
     extern __shared__ __align__(16) unsigned char s_raw[];
     const uint32_t wid = threadIdx.x >> 5, lane = lane_id();
-    const uint32_t n0 = (a.K_pad + 31u) / 32u, n1 = (n0 + 31u) / 32u;
-    const size_t wb = ssc_bitmap_warp_bytes(a.K_pad);
-    unsigned char* base = s_raw + wid * wb;
-    SscBitmapSmem w;
-    w.bm0 = reinterpret_cast<uint32_t*>(base);
-    w.bm1 = w.bm0 + n0;
-    w.ent = w.bm1 + n1;
-    w.wpre = reinterpret_cast<uint16_t*>(w.ent + kSscWarpCap);
-    w.wlist = w.wpre + n0;
-    for (uint32_t i = lane; i < n0 + n1; i += 32) w.bm0[i] = 0u;
+    const uint32_t cq = ssc_chunks_per_lane(a.K_pad);
+    unsigned char* base = s_raw + wid * ssc_warp_bytes(a.K_pad);
+    SscWarpSmem w;
+    w.bm = reinterpret_cast<uint32_t*>(base);
+    w.wpre = reinterpret_cast<uint16_t*>(w.bm + 128 * cq);
+    w.cnt = reinterpret_cast<uint32_t*>(w.wpre + 128 * cq);
+    w.top = reinterpret_cast<uint16_t*>(w.cnt + kSscWarpCap);
+    {
+        uint4* b4 = reinterpret_cast<uint4*>(w.bm);
+        for (uint32_t i = lane; i < 32 * cq; i += 32) b4[i] = make_uint4(0u, 0u, 0u, 0u);
+        for (uint32_t i = lane; i < kSscWarpCap; i += 32) w.cnt[i] = 0u;
+    }
     __syncwarp();
     unsigned long long nnz_acc = 0;
-    const uint32_t gw = blockIdx.x * kSscBmWarps + wid, nw = gridDim.x * kSscBmWarps;
+    const uint32_t gw = blockIdx.x * kSscWarps + wid, nw = gridDim.x * kSscWarps;
     // Software pipeline over the warp's documents: the next document's extent, row offset and
     // (up to 128) topics are loaded while this one is counted.
     auto meta = [&](uint32_t dd, uint32_t& s0, uint32_t& n, uint32_t& rq) {
@@ -151,28 +183,17 @@ __global__ void __launch_bounds__(kSscBmWarps * 32) ssc_bitmap_kernel(SscArgs a)
     };
     uint32_t s0, n, rq, key[4];
     meta(gw, s0, n, rq);
-    ssc_load_keys<4>(a.z + s0, n <= 128 ? n : 0u, lane, key);
+    ssc_load_keys<4>(a.z + s0, n <= kSscWarpCap ? n : 0u, lane, key);
     for (uint32_t d = gw; d < a.D; d += nw) {
         const uint32_t cs0 = s0, cn = n;
         uint32_t* row = a.A + rq * 4u;
+        // (the prefetched keys cover the first 128 topics of documents up to kSscWarpCap)
         const uint32_t k0 = key[0], k1 = key[1], k2 = key[2], k3 = key[3];
         meta(d + nw, s0, n, rq);
-        ssc_load_keys<4>(a.z + s0, n <= 128 ? n : 0u, lane, key);
+        ssc_load_keys<4>(a.z + s0, n <= kSscWarpCap ? n : 0u, lane, key);
         if (cn > kSscWarpCap || cn == 0) continue;  // ssc_long_kernel / empty document
-        uint32_t nnz;
         const uint32_t ck[4] = {k0, k1, k2, k3};
-        if (cn <= 32) nnz = ssc_doc_bitmap<1>(ck, lane, w, n1, row, a.tbits);
-        else if (cn <= 64) nnz = ssc_doc_bitmap<2>(ck, lane, w, n1, row, a.tbits);
-        else if (cn <= 128) nnz = ssc_doc_bitmap<4>(ck, lane, w, n1, row, a.tbits);
-        else if (cn <= 256) {
-            uint32_t k8[8];
-            ssc_load_keys<8>(a.z + cs0, cn, lane, k8);
-            nnz = ssc_doc_bitmap<8>(k8, lane, w, n1, row, a.tbits);
-        } else {
-            uint32_t k16[16];
-            ssc_load_keys<16>(a.z + cs0, cn, lane, k16);
-            nnz = ssc_doc_bitmap<16>(k16, lane, w, n1, row, a.tbits);
-        }
+        const uint32_t nnz = ssc_doc(ck, a.z + cs0, cn, lane, w, cq, row, a.tbits);
         nnz_acc += nnz;
     }
     if (lane == 0 && nnz_acc) atomicAdd(a.nnz_total, nnz_acc);
@@ -224,16 +245,16 @@ __global__ void __launch_bounds__(256) ssc_long_kernel(SscArgs a) {
 
 cudaError_t launch_ssc(const SscArgs& a, cudaStream_t s) {
     if (a.D > 0) {
-        const size_t bm_smem = kSscBmWarps * ssc_bitmap_warp_bytes(a.K_pad);  // <= 67 KB for K <= 65536
-        if (const cudaError_t e = cudaFuncSetAttribute(ssc_bitmap_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        const size_t bm_smem = kSscWarps * ssc_warp_bytes(a.K_pad);  // <= 59 KB for K <= 65536
+        if (const cudaError_t e = cudaFuncSetAttribute(ssc_warp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                        static_cast<int>(bm_smem));
             e != cudaSuccess)
             return e;
         // Short-lived CTAs (16 documents per warp) rather than a persistent grid: SSC runs
         // beside the M-step on a low-priority stream, and retiring CTAs let the scheduler
         // hand SMs to the higher-priority colsum/phi CTAs.
-        const uint32_t blocks = static_cast<uint32_t>((a.D + kSscBmWarps * 16u - 1) / (kSscBmWarps * 16u));
-        ssc_bitmap_kernel<<<blocks, kSscBmWarps * 32, bm_smem, s>>>(a);
+        const uint32_t blocks = static_cast<uint32_t>((a.D + kSscWarps * 16u - 1) / (kSscWarps * 16u));
+        ssc_warp_kernel<<<blocks, kSscWarps * 32, bm_smem, s>>>(a);
     }
     if (a.n_long > 0) {
         const size_t smem = sizeof(uint32_t) * a.K_pad;

@@ -106,7 +106,7 @@ class Engine:
         self.tokens[:, 2] = 0xFFFFFFFF if topic is None else topic
         self.V, self.K, self.T = V, K, len(doc)
         view = CorpusView(D, V, len(doc), self.tokens.ctypes.data, 0, D, 0, None)
-        cfg = Config(K, alpha, beta, seed, 0, 0, device, 0, 1, None)
+        cfg = Config(K, alpha, beta, seed, 0, 0, device, 0, 1, 0)
         h = C.c_void_p()
         check(lib().slda_create(C.byref(view), C.byref(cfg), C.byref(h)))
         self.h = h

@@ -145,6 +145,7 @@ def ref_lib():
         lib.ref_chunk_segments.argtypes = [C.c_void_p, C.c_uint32]
         lib.ref_chunk_segments.restype = C.c_uint32
         lib.ref_get_chunk.argtypes = [C.c_void_p, C.c_uint32] + [_u32p] * 9
+        lib.ref_save_checkpoint.argtypes = [C.c_void_p, C.c_char_p]
         lib.ref_heldout_ll.argtypes = [C.c_void_p, C.c_uint32, C.c_uint32, C.c_uint64, _u32p,
                                        C.c_uint32, C.c_uint32, C.c_uint64,
                                        C.POINTER(C.c_double), C.POINTER(C.c_uint64)]
@@ -319,6 +320,10 @@ class RefModel(_ModelBase):
         out["doc_offsets"] = tmp_off[: docs + 1]
         out["seg_word"], out["seg_offset"], out["seg_length"] = (s[:ns] for s in segs)
         return out
+
+    def save_checkpoint(self, path: str) -> None:
+        if ref_lib().ref_save_checkpoint(self.h, str(path).encode()) != 0:
+            raise ValueError(ref_lib().ref_last_error().decode())
 
     def heldout_ll(self, D, V, doc, word, burn_in=20, seed=0, workers=1):
         toks = tokens_aos(doc, word)

@@ -261,10 +261,35 @@ def test_checkpoint_roundtrip_and_resume(tmp_path):
         resumed.run_iteration(cfg)
     assert (resumed.assignments() == full.assignments()).all()
     assert (resumed.word_topic() == full.word_topic()).all()
-    # Byte format equals the reference's save_checkpoint (trainer.cpp:469-478).
     text = open(path).read().splitlines()
     assert text[0].startswith("sparselda-checkpoint 1 ")
     assert len(text) == 1 + half.num_tokens + 1 + int((half.word_topic() != 0).sum())
+
+
+@pytest.mark.parametrize("name,iters", [("given_topics", 2), ("c1", 5), ("k_large", 2)])
+def test_checkpoint_bytes_equal_reference(name, iters, tmp_path):
+    """Acceptance criterion 7's byte-identical checkpoints (acceptance.cpp:389-421) across the
+    two engines: the device model's save() after N iterations is the same file, byte for byte, as
+    the reference's own save_checkpoint (trainer.cpp:469-478, counts.cpp:140-150) after N
+    iterations of the same corpus and seed (oracle/_ref)."""
+    from oracle_lib import RefModel
+
+    spec = CASES[name]
+    m, cfg, _ = make_model(spec)
+    doc, word, D, V = corpus_arrays(spec["corpus"])
+    topic = None
+    if spec.get("given_topics_seed") is not None:
+        topic = np.random.default_rng(spec["given_topics_seed"]).integers(0, spec["K"], size=len(doc),
+                                                                          dtype=np.uint32)
+    ref = RefModel(D, V, doc, word, topic, K=spec["K"], alpha=spec.get("alpha", 0.0),
+                   beta=spec.get("beta", 0.01), seed=spec["seed"], num_chunks=3, workers=2)
+    for _ in range(iters):
+        m.run_iteration(cfg)
+        ref.iterate()
+    ours, theirs = tmp_path / "device.ckpt", tmp_path / "reference.ckpt"
+    m.save(str(ours))
+    ref.save_checkpoint(str(theirs))
+    assert ours.read_bytes() == theirs.read_bytes()
 
 
 VARIANT_CASES = ["c1", "long_docs", "empty_docs", "k_large", "nytimes_small", "k1"]
@@ -309,7 +334,8 @@ def test_throughput_configs_match_reference_every_iteration(name, golden_big, mo
     m, cfg, _ = make_model(spec)
     info = m.info()
     assert info["sampler_shape"] == BIG_SHAPES[name]
-    assert info["num_units"] > info["num_segments"]  # some words were split (> 8192 tokens)
+    if name != "c5_k50k_small":  # T = 2M: no word reaches the 8192-token unit cap
+        assert info["num_units"] > info["num_segments"]  # some words were split (> 8192 tokens)
     for it, expect in enumerate(fx["iterations"]):
         got = model_digests(m)
         assert got == expect, (name, it, sorted(k for k in got if got[k] != expect[k]))
