@@ -27,8 +27,10 @@ PYBIND_INC := $(shell $(PYTHON) -c "import pybind11; print(pybind11.get_include(
 MOD     := $(PKG)/_core$(PY_EXT)
 
 CLI     := $(PKG)/sparselda
+# The source-compatible `sparselda` C++ API (compat/sparselda/*.hpp) as one library.
+COMPAT  := $(PKG)/libsparselda_compat.so
 
-all: $(LIB) $(MOD) $(CLI)
+all: $(LIB) $(MOD) $(CLI) $(COMPAT)
 
 $(BUILD):
 	mkdir -p $(BUILD)
@@ -61,6 +63,13 @@ $(BUILD)/cli.o: $(CSRC)/cli.cpp $(CSRC)/sparselda_b200.hpp include/saberlda.h | 
 # The reference CLI's replacement (proj/tools/main.cpp): train / eval / topics.
 $(CLI): $(BUILD)/cli.o $(BUILD)/sparselda_b200.o $(LIB)
 	$(CXX) -o $@ $(BUILD)/cli.o $(BUILD)/sparselda_b200.o -L$(PKG) -lsaberlda -Wl,-rpath,'$$ORIGIN'
+
+$(BUILD)/compat.o: $(CSRC)/compat.cpp $(wildcard $(PKG)/compat/sparselda/*.hpp) $(CSRC)/sparselda_b200.hpp include/saberlda.h | $(BUILD)
+	$(CXX) $(CXXFLAGS) -I$(CSRC) -I$(PKG)/compat -c $< -o $@
+
+$(COMPAT): $(BUILD)/compat.o $(BUILD)/sparselda_b200.o $(LIB)
+	$(CXX) -shared -o $@ $(BUILD)/compat.o $(BUILD)/sparselda_b200.o -L$(PKG) -lsaberlda -Wl,-rpath,'$$ORIGIN' \
+	    -Wl,-soname=libsparselda_compat.so
 
 oracle:
 	$(MAKE) -C oracle all

@@ -130,16 +130,13 @@ __device__ __forceinline__ uint32_t ssc_doc(const uint32_t* key, const uint16_t*
 #pragma unroll 1
     for (uint32_t i = 128 + lane; i < n; i += 32) count(__ldg(z + i));
     __syncwarp();
-#pragma unroll
-    for (uint32_t r = 0; r < 4; ++r)
-        if (key[r] != 0xFFFFFFFFu) w.bm[key[r] >> 5] = 0u;
-#pragma unroll 1
-    for (uint32_t i = 128 + lane; i < n; i += 32) w.bm[__ldg(z + i) >> 5] = 0u;
+    // Emit the row; the map is cleared once per distinct topic (nnz stores, not len).
 #pragma unroll 1
     for (uint32_t e = lane; e < nnz; e += 32) {
-        const uint32_t k = w.cnt[e];
+        const uint32_t k = w.cnt[e], t = w.top[e];
         w.cnt[e] = 0u;
-        out_row[1 + e] = static_cast<uint32_t>(w.top[e]) | (k << tbits);
+        w.bm[t >> 5] = 0u;
+        out_row[1 + e] = t | (k << tbits);
     }
     const uint32_t padded = (nnz + 8u) & ~7u;
     if (nnz + 1 + lane < padded) out_row[nnz + 1 + lane] = 0u;  // < 8 pad words
