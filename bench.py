@@ -396,6 +396,7 @@ def main() -> None:
                                info["num_units"])
     it_achieved = it_bytes / (kt["total_ms"] / 1e3) / 1e9
 
+    xbytes = max_over_ranks(float(kt["exchange_bytes"]))
     if rank != 0:
         return
     line = dict(base_line)
@@ -403,16 +404,16 @@ def main() -> None:
         "value": value, "ms_per_step": ms_per_step,
         "config": {"workload": cfg["name"], "D": cfg["D"], "V": cfg["V"], "T": cfg["T"], "K": cfg["K"],
                    "alpha": 50.0 / cfg["K"], "beta": 0.01, "seed": TRAIN_SEED, "corpus_seed": CORPUS_SEED,
-                   "parallelism": (f"doc-shards x{world}, M-step exchange fused into the kernels over NVLink "
-                                   "peer memory") if world > 1 else "1 GPU",
+                   "parallelism": (f"doc-shards x{world}, sparse C_wk reduce-scatter + all-gather inside the M-step "
+                                   "kernels over NVLink peer memory") if world > 1 else "1 GPU",
                    "l2": "inputs larger than L2 (C_dk rows, phi, L4 are GBs; no flush needed)"},
         "roofline": {"bound": "hbm", "kernel": "sampler", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "traffic_config": traffic_cfg,
                      "peak_source": peak_src, "algorithmic_bytes_per_launch": s_bytes,
                      "sampler_ms": kt["sampler_ms"], "iteration_achieved": it_achieved,
                      "iteration_frac": it_achieved / peak, "E_t": row_entries / max(1, T_shard)},
-        "kernels_ms": {k: kt[k] for k in ("reset_ms", "sampler_ms", "ssc_ms", "colsum_ms", "phi_ms", "join_ms",
-                                          "total_ms")},
+        "kernels_ms": {k: kt[k] for k in ("reset_ms", "sampler_ms", "ssc_ms", "exchange_ms", "colsum_ms", "phi_ms",
+                                          "join_ms", "total_ms")},
         "sampler_shape": info["sampler_shape"],
         "mean_doc_topics": info["doc_topic_nnz"] / max(1, e - b),
         "e2e": {"value": cfg["T"] * args.steps / e2e_s, "unit": "tokens/s",
@@ -423,6 +424,12 @@ def main() -> None:
         "gpu_launches": int(kt["launches"]) * args.steps,
         "clocks": clocks.summary(),
     })
+    if world > 1:
+        line["exchange"] = {"bytes_read_per_rank": xbytes, "dense_c_wk_bytes": 4 * cfg["V"] * cfg["K"],
+                            "what": "bytes each rank read from the other ranks' memory per M-step (sparse "
+                                    "C_wk lists: reduce-scatter + all-gather), max over ranks"}
+        if one_gpu:
+            line["exchange"]["note"] = "all ranks shared one GPU (SLDA_BENCH_ONE_GPU=1): validation, not NVLink timing"
     if world == 1 and not args.no_cpu_baseline:
         del model
         r = reference_run(cfg, args.cpu_sample_tokens, args.cpu_steps, 1, threads)

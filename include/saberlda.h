@@ -26,7 +26,7 @@
 extern "C" {
 #endif
 
-#define SLDA_ABI_VERSION 3u
+#define SLDA_ABI_VERSION 4u
 
 enum {
     SLDA_OK = 0,
@@ -117,10 +117,12 @@ typedef struct slda_info {
 /* Per-kernel device times (ms) of the last iteration, for roofline accounting. */
 typedef struct slda_kernel_times {
     double reset_ms, sampler_ms, ssc_ms, colsum_ms, phi_ms;
-    double join_ms;               /* phi end -> iteration end: the SSC join (+ the peer barrier) */
+    double join_ms;               /* phi end -> iteration end: the wait for the side-stream SSC */
     double total_ms;
     uint64_t sampler_row_entries; /* sum over tokens of nnz(A_d) read by the sampler */
     uint32_t launches;            /* kernels launched by the iteration */
+    double exchange_ms;           /* world > 1: the sparse C_wk reduce-scatter + all-gather (0 on one GPU) */
+    uint64_t exchange_bytes;      /* world > 1: bytes this rank read from the other ranks' memory */
 } slda_kernel_times;
 
 /* ------------------------------------------------------------------ engine -- */
@@ -229,22 +231,21 @@ int slda_generate_docs(const slda_gen_params* p, uint32_t doc_begin, uint32_t do
                        uint32_t* tokens, uint64_t capacity);
 
 /* ---- Peer-memory exchange (multi-GPU) --------------------------------------------------------
- * Create every rank's engine with world_size > 1, export each engine's
- * buffer handles (CUDA IPC), exchange them over any host channel, and attach every engine to
- * all ranks' handles (indexed by rank).  The M-step then reduce-scatters C_wk, all-reduces C_k
- * and all-gathers phi / L4 / L8 / Q inside its own kernels over peer memory (NVLink on a
- * multi-GPU node; the same HBM when ranks share one GPU): the collectives of a sharded M-step
- * (trainer.cpp:395-400 / 436-440 semantics) folded into the computation.
- * slda_peer_attach runs init_state's first M-step and is collective, as is
- * slda_get_word_topic on a peer-attached engine. */
+ * Create every rank's engine with world_size > 1, export each engine's buffer handles (CUDA
+ * IPC), exchange them over any host channel, and attach every engine to all ranks' handles
+ * (indexed by rank).  Every M-step then exchanges C_wk SPARSE over peer memory inside its own
+ * kernels -- each rank lists its partial C_wk's non-zeros, adds the other ranks' entries of its
+ * word slice (the reduce-scatter), lists its reduced slice, and adds every other slice's entries
+ * (the all-gather) -- after which every rank holds the full reduced C_wk and computes phi / L4 /
+ * L8 / Q locally (trainer.cpp:395-400 / 436-440 semantics).  NVLink on a multi-GPU node; the
+ * same HBM when ranks share one GPU.  slda_peer_attach runs init_state's first M-step and is
+ * collective. */
 #define SLDA_PEER_HANDLE_BYTES 64
 typedef struct slda_peer_handles {
-    unsigned char word_topic[SLDA_PEER_HANDLE_BYTES];      /* partial / reduced C_wk */
-    unsigned char colsum[SLDA_PEER_HANDLE_BYTES];          /* partial C_k */
-    unsigned char word_topic_prob[SLDA_PEER_HANDLE_BYTES]; /* phi replica */
-    unsigned char tree_prefix[SLDA_PEER_HANDLE_BYTES];     /* L4 replica */
-    unsigned char tree_l8[SLDA_PEER_HANDLE_BYTES];         /* L8 replica */
-    unsigned char tree_mass[SLDA_PEER_HANDLE_BYTES];       /* Q replica */
+    unsigned char partial_index[SLDA_PEER_HANDLE_BYTES];   /* {offset, n} per word row of the partial C_wk list */
+    unsigned char partial_entries[SLDA_PEER_HANDLE_BYTES]; /* its entries: topic | count << 16 */
+    unsigned char slice_index[SLDA_PEER_HANDLE_BYTES];     /* the same for the rank's reduced word slice */
+    unsigned char slice_entries[SLDA_PEER_HANDLE_BYTES];
     unsigned char barrier[SLDA_PEER_HANDLE_BYTES];         /* barrier counter (rank 0's is used) */
 } slda_peer_handles;
 

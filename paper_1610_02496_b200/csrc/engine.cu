@@ -179,22 +179,26 @@ struct slda_engine {
 
     // Per-iteration phase events, a ring so async iterations can be profiled afterwards.
     static constexpr uint32_t kRing = 64;
-    // 0 start, 1 reset, 2 sampler, 3 m-step start, 4 colsum, 5 phi, 6 end, 7 SSC end (side stream)
-    cudaEvent_t ring[kRing][8] = {};
+    // 0 start, 1 reset, 2 sampler, 3 m-step start, 4 colsum, 5 phi, 6 end, 7 SSC end (side stream),
+    // 8 exchange end (world > 1: the sparse reduce-scatter + all-gather; == 3 on one GPU)
+    cudaEvent_t ring[kRing][9] = {};
     cudaEvent_t* ev = ring[0];
     uint32_t ring_launches[kRing] = {};
     uint32_t slot = 0;
     uint32_t enqueued = 0;  // iterations this engine has run (bounds the event ring reads)
-    // Peer-memory exchange (world > 1): the other ranks' buffers mapped through CUDA IPC
-    // handles (slda_peer_export / slda_peer_attach).
+    // Peer-memory exchange (world > 1): the other ranks' sparse C_wk lists mapped through CUDA
+    // IPC handles (slda_peer_export / slda_peer_attach); mstep.cu describes the exchange.
     bool peer = false, attached = false;
-    DevMem bar, coltot;                    // barrier counter (rank 0's is the shared one), C_k total
-    void* pB[slda::kMaxPeers] = {};
-    void* pcol[slda::kMaxPeers] = {};
-    void* pbhat[slda::kMaxPeers] = {};
-    void* pl4[slda::kMaxPeers] = {};
-    void* pl8[slda::kMaxPeers] = {};
-    void* pq[slda::kMaxPeers] = {};
+    DevMem bar;                            // barrier counter (rank 0's is the shared one)
+    DevMem info1, ent1;                    // this rank's partial C_wk, all rows: {offset, n} + entries
+    DevMem info2, ent2;                    // this rank's reduced word slice
+    DevMem xcnt;                           // [cursor1, cursor2, overflow] (u32)
+    DevMem xbytes;                         // per ring slot: bytes read from the other ranks (u64)
+    uint64_t cap1 = 0, cap2 = 0;           // entry capacities (pieces of counts, see alloc_exchange)
+    void* pinfo1[slda::kMaxPeers] = {};
+    void* pent1[slda::kMaxPeers] = {};
+    void* pinfo2[slda::kMaxPeers] = {};
+    void* pent2[slda::kMaxPeers] = {};
     unsigned long long* pbar = nullptr;
     uint64_t bar_seq = 0;
     std::vector<void*> opened;             // IPC mappings to close
@@ -202,7 +206,26 @@ struct slda_engine {
         ++bar_seq;
         CK(slda::launch_peer_barrier(pbar, static_cast<unsigned long long>(world) * bar_seq, stream));
     }
-    void m_step_peer();
+    // Capacities in u32 entries (a count c takes ceil(c / 65535) of them):
+    //   partial : <= min(V*K_pad, T_rank) non-zero cells + T_rank/65535 extra pieces;
+    //   slice   : <= slice cells + T_total/65535, T_total < 2^32 * kMaxPeers.
+    void alloc_exchange() {
+        const uint64_t cells = static_cast<uint64_t>(V) * K_pad;
+        cap1 = std::min<uint64_t>(cells, T) + T / 65535 + 64;
+        cap2 = static_cast<uint64_t>(slice_rows()) * K_pad + ((1ull << 32) * slda::kMaxPeers) / 65535 + 64;
+        if (cap1 > 0xFFFFFFFFull || cap2 > 0xFFFFFFFFull)
+            validation("peer-memory exchange: a rank's sparse C_wk list exceeds 2^32 entries");
+        bar.alloc(8, &device_bytes);
+        info1.alloc(static_cast<size_t>(V) * 8 + 8, &device_bytes);
+        ent1.alloc(cap1 * 4, &device_bytes);
+        info2.alloc(static_cast<size_t>(slice_rows()) * 8 + 8, &device_bytes);
+        ent2.alloc(cap2 * 4, &device_bytes);
+        xcnt.alloc(16, &device_bytes);
+        xbytes.alloc(8 * kRing, &device_bytes);
+        CK(cudaMemsetAsync(bar.p, 0, 8, stream));
+        CK(cudaMemsetAsync(xbytes.p, 0, xbytes.bytes, stream));
+    }
+    void exchange();
     uint32_t launches = 0;
 
     unsigned long long* nnz_counter() const { return counters.as<unsigned long long>(); }
@@ -641,9 +664,7 @@ void slda_engine::build(const slda_corpus_view& cv, const slda_config& c) {
     CK(slda::launch_recount(tok.as<uint2>(), units.as<slda::Unit>(), n_units, z.as<uint16_t>(),
                             B.as<uint32_t>(), K_pad, rd, stream));
     if (peer) {  // the first M-step needs the other ranks: it runs in slda_peer_attach
-        bar.alloc(8, &device_bytes);
-        CK(cudaMemsetAsync(bar.p, 0, 8, stream));
-        coltot.alloc(static_cast<size_t>(K_pad) * 8, &device_bytes);
+        alloc_exchange();
     } else {
         m_step();
     }
@@ -670,14 +691,13 @@ void slda_engine::ssc(cudaStream_t st) {
     launches += (D > 0) + (n_long > 0);
 }
 
-// M-step after the E-step's B (one GPU): colsum -> denom -> phi/L4/L8/Q.  preprocess
-// (counts.cpp:37-63) + rebuild_trees (trainer.cpp:237-248).
+// M-step after the E-step's B: colsum -> denom -> phi/L4/L8/Q over every word row.  preprocess
+// (counts.cpp:37-63) + rebuild_trees (trainer.cpp:237-248).  With world > 1 the sparse C_wk
+// exchange first turns each rank's partial B into the full reduced C_wk (exchange()).
 void slda_engine::m_step() {
-    if (peer) {
-        m_step_peer();
-        return;
-    }
     CK(cudaEventRecord(ev[3], stream));
+    if (peer) exchange();
+    CK(cudaEventRecord(ev[8], stream));
     CK(cudaMemsetAsync(colsum.p, 0, colsum.bytes, stream));
     CK(slda::launch_colsum(B.as<uint32_t>(), 0, V_pad, K_pad, colsum.as<unsigned long long>(), stream));
     CK(slda::launch_denom(colsum.as<unsigned long long>(), K, K_pad, V, beta, denom.as<double>(),
@@ -690,47 +710,40 @@ void slda_engine::m_step() {
     CK(cudaEventRecord(ev[6], stream));
 }
 
-// The M-step with the exchange fused into its kernels over the other ranks' memory (mstep.cu):
-// barrier -> colsum over the own word slice of every rank's partial C_wk (the reduce-scatter;
-// the reduced slice is written into this rank's B) -> barrier -> C_k total from every rank's
-// partial (the all-reduce) -> phi / L4 / L8 / Q of the own slice, stored into every rank's
-// replica (the all-gather) -> barrier.  Integer sums and per-row f32 chains: bit-identical to
-// one GPU.
-void slda_engine::m_step_peer() {
+// The C_wk reduce-scatter + all-gather over the other ranks' memory, sparse (mstep.cu):
+// sparsify the partial B -> barrier -> add the other ranks' entries of the own word slice ->
+// sparsify the reduced slice, clear the other rows -> barrier -> add every other slice's
+// entries.  Afterwards B is the full reduced C_wk on every rank.  No trailing barrier: a
+// rank's lists are next rewritten only after the next iteration's first barrier, which no rank
+// passes before finishing this all-gather.  Integer sums: bit-identical to one GPU.
+void slda_engine::exchange() {
     if (!attached) validation("peer-memory exchange: call slda_peer_attach on every rank first");
-    const uint32_t r0 = row_begin(), r1 = row_end();
-    CK(cudaEventRecord(ev[3], stream));
-    peer_barrier();  // every rank's partial C_wk is complete
-    slda::PeerCounts pcs{};
+    const uint32_t r0 = row_begin(), r1 = row_end(), rows = slice_rows();
+    uint32_t* cnt = xcnt.as<uint32_t>();
+    unsigned long long* xb = xbytes.as<unsigned long long>() + slot;
+    CK(cudaMemsetAsync(cnt, 0, 8, stream));  // cursors (the overflow flag stays sticky)
+    CK(cudaMemsetAsync(xb, 0, 8, stream));
+    CK(slda::launch_sparsify(B.as<uint32_t>(), 0, V, K_pad, info1.as<uint2>(), ent1.as<uint32_t>(), cnt,
+                             static_cast<uint32_t>(cap1), cnt + 2, stream));
+    peer_barrier();  // every rank's partial list is complete
+    slda::PeerSparse rs{};
     for (uint32_t p = 0; p < world; ++p)
-        pcs.B[p] = p == rank ? B.as<uint32_t>() : static_cast<const uint32_t*>(pB[p]);
-    pcs.n = world;
-    CK(cudaMemsetAsync(colsum.p, 0, colsum.bytes, stream));
-    CK(slda::launch_peer_colsum(pcs, B.as<uint32_t>(), r0, r1, K_pad, colsum.as<unsigned long long>(), stream));
-    peer_barrier();  // every rank's C_k partial is complete (and no rank reads a partial C_wk again)
-    slda::PeerColsums pc{};
+        if (p != rank)
+            rs.src[rs.n++] = {static_cast<const uint2*>(pinfo1[p]), static_cast<const uint32_t*>(pent1[p]), 0u};
+    CK(slda::launch_gather_add(rs, r0, r1, r1, r1, 0, B.as<uint32_t>(), K_pad, xb, stream));
+    CK(slda::launch_sparsify(B.as<uint32_t>(), r0, r1, K_pad, info2.as<uint2>(), ent2.as<uint32_t>(), cnt + 1,
+                             static_cast<uint32_t>(cap2), cnt + 2, stream));
+    const size_t row_bytes = static_cast<size_t>(K_pad) * 4;
+    if (r0 > 0) CK(cudaMemsetAsync(B.p, 0, r0 * row_bytes, stream));
+    if (r1 < V_pad) CK(cudaMemsetAsync(B.as<uint32_t>() + static_cast<size_t>(r1) * K_pad, 0, (V_pad - r1) * row_bytes, stream));
+    peer_barrier();  // every rank's reduced slice is listed
+    slda::PeerSparse ag{};
+    ag.n = world;
     for (uint32_t p = 0; p < world; ++p)
-        pc.c[p] = p == rank ? colsum.as<unsigned long long>() : static_cast<const unsigned long long*>(pcol[p]);
-    pc.n = world;
-    CK(slda::launch_peer_total(pc, K_pad, coltot.as<unsigned long long>(), stream));
-    CK(slda::launch_denom(coltot.as<unsigned long long>(), K, K_pad, V, beta, denom.as<double>(), zv.as<float>(),
-                          stream));
-    CK(cudaEventRecord(ev[4], stream));
-    slda::PeerMirror m{};
-    for (uint32_t p = 0; p < world; ++p) {
-        if (p == rank) continue;
-        m.bhat[m.n] = static_cast<float*>(pbhat[p]);
-        m.l4[m.n] = static_cast<float*>(pl4[p]);
-        m.l8[m.n] = static_cast<float*>(pl8[p]);
-        m.q[m.n] = static_cast<float*>(pq[p]);
-        ++m.n;
-    }
-    CK(slda::launch_phi(B.as<uint32_t>(), denom.as<double>(), zv.as<float>(), bhat.as<float>(), l4.as<float>(),
-                        l8.as<float>(), q.as<float>(), r0, r1, K, K_pad, l8_stride, beta, falpha, stream, &m));
-    launches += 5;
-    CK(cudaEventRecord(ev[5], stream));
-    peer_barrier();  // every replica holds every slice
-    CK(cudaEventRecord(ev[6], stream));
+        if (p != rank)
+            ag.src[p] = {static_cast<const uint2*>(pinfo2[p]), static_cast<const uint32_t*>(pent2[p]), p * rows};
+    CK(slda::launch_gather_add(ag, 0, V, r0, r1, rows, B.as<uint32_t>(), K_pad, xb, stream));
+    launches += 4;
 }
 
 // run_iteration (trainer.cpp:419-449) on the engine stream.
@@ -904,7 +917,8 @@ int slda_get_kernel_times_avg(const slda_engine* e, uint32_t last_n, slda_kernel
             t->reset_ms += ms(0, 1);
             t->sampler_ms += ms(1, 2);
             t->ssc_ms += ms(2, 7);  // side stream, concurrent with colsum + phi
-            t->colsum_ms += ms(3, 4);
+            t->exchange_ms += ms(3, 8);
+            t->colsum_ms += ms(8, 4);
             t->phi_ms += ms(4, 5);
             t->join_ms += ms(5, 6);  // phi end -> iteration end: the SSC join (+ the peer barrier)
             t->total_ms += ms(0, 6);
@@ -916,6 +930,13 @@ int slda_get_kernel_times_avg(const slda_engine* e, uint32_t last_n, slda_kernel
         t->sampler_ms /= n;
         t->ssc_ms /= n;
         t->colsum_ms /= n;
+        t->exchange_ms /= n;
+        if (e->xbytes.p) {
+            std::vector<unsigned long long> xb(slda_engine::kRing);
+            CK(cudaMemcpy(xb.data(), e->xbytes.p, 8 * slda_engine::kRing, cudaMemcpyDeviceToHost));
+            for (uint32_t i = 0; i < last_n; ++i) t->exchange_bytes += xb[(e->iteration - 1 - i) % slda_engine::kRing];
+            t->exchange_bytes /= last_n;
+        }
         t->phi_ms /= n;
         t->join_ms /= n;
         t->total_ms /= n;
@@ -943,22 +964,7 @@ int slda_get_word_topic(slda_engine* e, uint32_t* out) {
     return guarded([&] {
         if (!e || !out) validation("null argument");
         e->set_device();
-        if (e->world > 1 && e->peer) {
-            // Collective: each rank's B holds the reduced C_wk of its own slice; copy the others'
-            // slices out of their memory between two barriers.
-            const size_t slice = static_cast<size_t>(e->slice_rows()) * e->K_pad;
-            DevMem full;
-            full.alloc(e->B.bytes, nullptr);
-            e->peer_barrier();
-            for (uint32_t p = 0; p < e->world; ++p) {
-                const uint32_t* src = p == e->rank ? e->B.as<uint32_t>() : static_cast<const uint32_t*>(e->pB[p]);
-                CK(cudaMemcpyAsync(full.as<uint32_t>() + p * slice, src + p * slice, slice * 4,
-                                   cudaMemcpyDeviceToDevice, e->stream));
-            }
-            e->peer_barrier();
-            copy_matrix(e, full, out);
-            return;
-        }
+        // With world > 1 every rank's B holds the full reduced C_wk after the exchange.
         copy_matrix(e, e->B, out);
     });
 }
@@ -1011,12 +1017,10 @@ int slda_peer_export(slda_engine* e, slda_peer_handles* out) {
             static_assert(sizeof(ih) == SLDA_PEER_HANDLE_BYTES, "cudaIpcMemHandle_t size");
             std::memcpy(dst, &ih, sizeof(ih));
         };
-        h(e->B, out->word_topic);
-        h(e->colsum, out->colsum);
-        h(e->bhat, out->word_topic_prob);
-        h(e->l4, out->tree_prefix);
-        h(e->l8, out->tree_l8);
-        h(e->q, out->tree_mass);
+        h(e->info1, out->partial_index);
+        h(e->ent1, out->partial_entries);
+        h(e->info2, out->slice_index);
+        h(e->ent2, out->slice_entries);
         h(e->bar, out->barrier);
     });
 }
@@ -1037,12 +1041,10 @@ int slda_peer_attach(slda_engine* e, const slda_peer_handles* all) {
         };
         for (uint32_t r = 0; r < e->world; ++r) {
             if (r == e->rank) continue;
-            e->pB[r] = open(all[r].word_topic);
-            e->pcol[r] = open(all[r].colsum);
-            e->pbhat[r] = open(all[r].word_topic_prob);
-            e->pl4[r] = open(all[r].tree_prefix);
-            e->pl8[r] = open(all[r].tree_l8);
-            e->pq[r] = open(all[r].tree_mass);
+            e->pinfo1[r] = open(all[r].partial_index);
+            e->pent1[r] = open(all[r].partial_entries);
+            e->pinfo2[r] = open(all[r].slice_index);
+            e->pent2[r] = open(all[r].slice_entries);
         }
         e->pbar = e->rank == 0 ? e->bar.as<unsigned long long>()
                                : static_cast<unsigned long long*>(open(all[0].barrier));

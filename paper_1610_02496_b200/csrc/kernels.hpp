@@ -63,31 +63,28 @@ cudaError_t launch_colsum(const uint32_t* B, uint32_t row_begin, uint32_t row_en
 // denom: 2*K_pad doubles -- denom_k, then RN(1/denom_k) (read by the phi kernel).
 cudaError_t launch_denom(const unsigned long long* colsum, uint32_t K, uint32_t K_pad, uint32_t V,
                          double beta, double* denom, float* zv, cudaStream_t s);
-// Peer-memory exchange (engine.cu m_step_peer): up to kMaxPeers ranks.
+// Peer-memory exchange (engine.cu m_step_peer): up to kMaxPeers ranks, C_wk exchanged as
+// sparse per-row entries (topic | count << 16) with a {offset, n} index per row.
 constexpr uint32_t kMaxPeers = 8;
-struct PeerMirror {  // the other ranks' phi / L4 / L8 / Q replicas
-    float* bhat[kMaxPeers];
-    float* l4[kMaxPeers];
-    float* l8[kMaxPeers];
-    float* q[kMaxPeers];
-    uint32_t n;
+struct SparseRows {
+    const uint2* info;        // per row: {entry offset, entry count}, indexed by row - base
+    const uint32_t* entries;
+    uint32_t base;
 };
-struct PeerCounts {  // every rank's partial C_wk (own included)
-    const uint32_t* B[kMaxPeers];
-    uint32_t n;
-};
-struct PeerColsums {  // every rank's partial C_k (own included)
-    const unsigned long long* c[kMaxPeers];
+struct PeerSparse {
+    SparseRows src[kMaxPeers];
     uint32_t n;
 };
 cudaError_t launch_phi(const uint32_t* B, const double* denom, const float* zv, float* bhat,
                        float* l4, float* l8, float* q, uint32_t row_begin, uint32_t row_end,
                        uint32_t K, uint32_t K_pad, uint32_t l8_stride, double beta, float falpha,
-                       cudaStream_t s, const PeerMirror* mirror = nullptr);
+                       cudaStream_t s);
 cudaError_t launch_peer_barrier(unsigned long long* counter, unsigned long long target, cudaStream_t s);
-cudaError_t launch_peer_colsum(const PeerCounts& pc, uint32_t* B, uint32_t row_begin, uint32_t row_end,
-                               uint32_t K_pad, unsigned long long* colsum, cudaStream_t s);
-cudaError_t launch_peer_total(const PeerColsums& pc, uint32_t K_pad, unsigned long long* total, cudaStream_t s);
+cudaError_t launch_sparsify(const uint32_t* B, uint32_t row_lo, uint32_t row_hi, uint32_t K_pad, uint2* info,
+                            uint32_t* entries, uint32_t* cursor, uint32_t cap, uint32_t* overflow, cudaStream_t s);
+cudaError_t launch_gather_add(const PeerSparse& ps, uint32_t row_lo, uint32_t row_hi, uint32_t skip_lo,
+                              uint32_t skip_hi, uint32_t per_slice, uint32_t* B, uint32_t K_pad,
+                              unsigned long long* bytes, cudaStream_t s);
 
 // Setup kernels.
 cudaError_t launch_deinterleave(const uint32_t* aos, uint64_t T, uint32_t doc_begin,

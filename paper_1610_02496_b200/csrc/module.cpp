@@ -67,6 +67,8 @@ py::dict kernel_times_dict(const slda_kernel_times& t) {
     d["total_ms"] = t.total_ms;
     d["sampler_row_entries"] = t.sampler_row_entries;
     d["launches"] = t.launches;
+    d["exchange_ms"] = t.exchange_ms;
+    d["exchange_bytes"] = t.exchange_bytes;
     return d;
 }
 

@@ -141,7 +141,7 @@ constexpr size_t phi_smem_bytes() {
     return static_cast<size_t>(S) * (2 * C * 8 + kPhiRows * C * 4 + C * 4) + kPhiRows * C * 4;
 }
 
-template <int C, int S, bool kMirror>
+template <int C, int S>
 __global__ void __launch_bounds__(kPhiRows, 4) phi_kernel(const uint32_t* __restrict__ B,
                                                          const double* __restrict__ denom,
                                                          const float* __restrict__ zv,
@@ -149,7 +149,7 @@ __global__ void __launch_bounds__(kPhiRows, 4) phi_kernel(const uint32_t* __rest
                                                          float* __restrict__ l8, float* __restrict__ q,
                                                          uint32_t row_begin, uint32_t row_end,
                                                          uint32_t K_pad, uint32_t l8_stride, double beta,
-                                                         float falpha, PeerMirror mirror) {
+                                                         float falpha) {
     static_assert(C == 16 || C == 32 || C == 64, "tile width");
     constexpr uint32_t Q = C / 4;              // quads per tile row
     constexpr uint32_t RP = kPhiRows / Q;      // rows per copy pass
@@ -233,15 +233,10 @@ __global__ void __launch_bounds__(kPhiRows, 4) phi_kernel(const uint32_t* __rest
                     const float4 x = make_float4(l8v[4 * h], l8v[(4 * h + 1) % (Q / 2)], l8v[(4 * h + 2) % (Q / 2)],
                                                  l8v[(4 * h + 3) % (Q / 2)]);
                     *reinterpret_cast<float4*>(l8 + o8 + 4 * h) = x;
-                    if (kMirror)
-                        for (uint32_t p = 0; p < mirror.n; ++p)
-                            *reinterpret_cast<float4*>(mirror.l8[p] + o8 + 4 * h) = x;
                 }
             } else {
                 const float2 x = make_float2(l8v[0], l8v[1 % (Q / 2)]);
                 *reinterpret_cast<float2*>(l8 + o8) = x;
-                if (kMirror)
-                    for (uint32_t p = 0; p < mirror.n; ++p) *reinterpret_cast<float2*>(mirror.l8[p] + o8) = x;
             }
         }
         __syncthreads();
@@ -254,56 +249,35 @@ __global__ void __launch_bounds__(kPhiRows, 4) phi_kernel(const uint32_t* __rest
                 const size_t go = g0 + p * stride + c0;
                 *reinterpret_cast<float4*>(bhat + go) = b;
                 *reinterpret_cast<float4*>(l4 + go) = l;
-                if (kMirror) {  // the all-gather, fused: the same values into every peer's replica
-                    for (uint32_t m = 0; m < mirror.n; ++m) {
-                        *reinterpret_cast<float4*>(mirror.bhat[m] + go) = b;
-                        *reinterpret_cast<float4*>(mirror.l4[m] + go) = l;
-                    }
-                }
             }
         }
     }
     if (v < row_end) {
         for (uint32_t j = K_pad / kLeaf; j < l8_stride; ++j) l8[static_cast<size_t>(v) * l8_stride + j] = run;
         q[v] = __fmul_rn(falpha, run);  // trainer.cpp:245
-        if (kMirror) {
-            for (uint32_t p = 0; p < mirror.n; ++p) {
-                for (uint32_t j = K_pad / kLeaf; j < l8_stride; ++j)
-                    mirror.l8[p][static_cast<size_t>(v) * l8_stride + j] = run;
-                mirror.q[p][v] = __fmul_rn(falpha, run);
-            }
-        }
     }
 }
 
 template <int C, int S>
 cudaError_t launch_phi_t(const uint32_t* B, const double* denom, const float* zv, float* bhat, float* l4,
                          float* l8, float* q, uint32_t row_begin, uint32_t row_end, uint32_t K_pad,
-                         uint32_t l8_stride, double beta, float falpha, cudaStream_t s, const PeerMirror* mirror) {
+                         uint32_t l8_stride, double beta, float falpha, cudaStream_t s) {
     constexpr size_t smem = phi_smem_bytes<C, S>();
     // Per launch: the opt-in is per device context (a process-wide flag would miss a second GPU).
-    if (const cudaError_t e = cudaFuncSetAttribute(phi_kernel<C, S, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                   static_cast<int>(smem));
-        e != cudaSuccess)
-        return e;
-    if (const cudaError_t e = cudaFuncSetAttribute(phi_kernel<C, S, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    if (const cudaError_t e = cudaFuncSetAttribute(phi_kernel<C, S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                    static_cast<int>(smem));
         e != cudaSuccess)
         return e;
     const uint32_t blocks = (row_end - row_begin + kPhiRows - 1) / kPhiRows;
-    if (mirror && mirror->n > 0)
-        phi_kernel<C, S, true><<<blocks, kPhiRows, smem, s>>>(B, denom, zv, bhat, l4, l8, q, row_begin, row_end,
-                                                              K_pad, l8_stride, beta, falpha, *mirror);
-    else
-        phi_kernel<C, S, false><<<blocks, kPhiRows, smem, s>>>(B, denom, zv, bhat, l4, l8, q, row_begin, row_end,
-                                                               K_pad, l8_stride, beta, falpha, PeerMirror{});
+    phi_kernel<C, S><<<blocks, kPhiRows, smem, s>>>(B, denom, zv, bhat, l4, l8, q, row_begin, row_end, K_pad,
+                                                    l8_stride, beta, falpha);
     return cudaGetLastError();
 }
 
 cudaError_t launch_phi(const uint32_t* B, const double* denom, const float* zv, float* bhat,
                        float* l4, float* l8, float* q, uint32_t row_begin, uint32_t row_end,
                        uint32_t K, uint32_t K_pad, uint32_t l8_stride, double beta, float falpha,
-                       cudaStream_t s, const PeerMirror* mirror) {
+                       cudaStream_t s) {
     (void)K;  // columns >= K are zero counts with zv = 0 (see above)
     if (row_end <= row_begin) return cudaSuccess;
     if (K_pad % 32) return cudaErrorInvalidValue;
@@ -322,12 +296,12 @@ cudaError_t launch_phi(const uint32_t* B, const double* denom, const float* zv, 
             int dev = 0, sms = 0, n4 = 0, n3 = 0;
             cudaGetDevice(&dev);
             cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-            cudaFuncSetAttribute(phi_kernel<32, 4, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+            cudaFuncSetAttribute(phi_kernel<32, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(phi_smem_bytes<32, 4>()));
-            cudaFuncSetAttribute(phi_kernel<32, 3, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+            cudaFuncSetAttribute(phi_kernel<32, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(phi_smem_bytes<32, 3>()));
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n4, phi_kernel<32, 4, false>, kPhiRows, phi_smem_bytes<32, 4>());
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n3, phi_kernel<32, 3, false>, kPhiRows, phi_smem_bytes<32, 3>());
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n4, phi_kernel<32, 4>, kPhiRows, phi_smem_bytes<32, 4>());
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n3, phi_kernel<32, 3>, kPhiRows, phi_smem_bytes<32, 3>());
             slots4 = n4 * sms > 0 ? n4 * sms : 1;
             slots3 = n3 * sms > 0 ? n3 * sms : 1;
         }
@@ -337,22 +311,26 @@ cudaError_t launch_phi(const uint32_t* B, const double* denom, const float* zv, 
         shape = fill3 > fill4 + 0.05 ? 2 : 0;
     }
     switch (shape) {
-        case 1: return launch_phi_t<16, 8>(B, denom, zv, bhat, l4, l8, q, row_begin, row_end, K_pad, l8_stride, beta, falpha, s, mirror);
-        case 2: return launch_phi_t<32, 3>(B, denom, zv, bhat, l4, l8, q, row_begin, row_end, K_pad, l8_stride, beta, falpha, s, mirror);
-        case 3: return launch_phi_t<64, 2>(B, denom, zv, bhat, l4, l8, q, row_begin, row_end, K_pad, l8_stride, beta, falpha, s, mirror);
-        case 4: return launch_phi_t<64, 3>(B, denom, zv, bhat, l4, l8, q, row_begin, row_end, K_pad, l8_stride, beta, falpha, s, mirror);
+        case 1: return launch_phi_t<16, 8>(B, denom, zv, bhat, l4, l8, q, row_begin, row_end, K_pad, l8_stride, beta, falpha, s);
+        case 2: return launch_phi_t<32, 3>(B, denom, zv, bhat, l4, l8, q, row_begin, row_end, K_pad, l8_stride, beta, falpha, s);
+        case 3: return launch_phi_t<64, 2>(B, denom, zv, bhat, l4, l8, q, row_begin, row_end, K_pad, l8_stride, beta, falpha, s);
+        case 4: return launch_phi_t<64, 3>(B, denom, zv, bhat, l4, l8, q, row_begin, row_end, K_pad, l8_stride, beta, falpha, s);
         default: break;
     }
-    return launch_phi_t<32, 4>(B, denom, zv, bhat, l4, l8, q, row_begin, row_end, K_pad, l8_stride, beta, falpha, s, mirror);
+    return launch_phi_t<32, 4>(B, denom, zv, bhat, l4, l8, q, row_begin, row_end, K_pad, l8_stride, beta, falpha, s);
 }
 
-// ---- Peer-memory M-step exchange (world > 1 without NCCL; engine.cu m_step_peer) -------------
-// Every rank maps every other rank's buffers (CUDA IPC handles, NVLink peer memory on a multi-GPU
-// node, the same HBM when the ranks share one GPU) and the collectives become parts of the
-// kernels that need them: the reduce-scatter of C_wk is the colsum kernel reading its word
-// slice from all ranks' partial C_wk; the all-reduce of C_k is the denominator kernel summing
-// the ranks' column-sum partials; the all-gather of phi / L4 / L8 / Q is the phi kernel's
-// epilogue storing its slice into every replica (above).  Ranks meet at device-side barriers.
+// ---- Peer-memory M-step exchange (world > 1; engine.cu m_step_peer) ---------------------------
+// Every rank maps the other ranks' exchange buffers (CUDA IPC handles: NVLink peer memory on a
+// multi-GPU node, the same HBM when ranks share one GPU).  C_wk is exchanged SPARSE: a rank's
+// partial C_wk has at most T_rank non-zero cells, the reduced one at most min(V*K, T), against
+// V*K dense cells (C3: 1.41G).  A row's non-zeros become u32 entries topic | count << 16 (counts
+// above 65535 split into several entries, which the receivers add), indexed per row by
+// {offset, n}.  Reduce-scatter: each rank adds the other ranks' entries of its word slice into
+// its own B.  All-gather: each rank sparsifies its reduced slice and every rank adds the other
+// slices' entries into its (zeroed) other rows -- after which every rank holds the full reduced
+// C_wk and runs the ordinary colsum + phi over all rows locally.  Integer sums: bit-identical to
+// one GPU at any rank count.
 
 // All ranks increment rank 0's counter; each waits for the round's total.  System-scope fences
 // publish this rank's prior writes (kernels earlier on the stream) before it arrives.
@@ -374,67 +352,110 @@ cudaError_t launch_peer_barrier(unsigned long long* counter, unsigned long long 
     return cudaGetLastError();
 }
 
-// Reduce-scatter fused into colsum: own slice rows of every rank's partial C_wk are summed
-// (integers: order-free, bit-identical to NCCL's), written back into this rank's B (its slice
-// of the reduced C_wk) and column-summed into this rank's C_k partial.
-__global__ void __launch_bounds__(256) peer_colsum_kernel(PeerCounts pc, uint32_t* __restrict__ B, uint32_t row_begin,
-                                                          uint32_t row_end, uint32_t cols4, uint32_t rows_per_chunk,
-                                                          unsigned long long* __restrict__ colsum) {
-    __shared__ unsigned long long s_acc[256][4];
-    const uint32_t c4 = blockIdx.x * blockDim.x + threadIdx.x;
-    const uint32_t r0 = row_begin + blockIdx.y * rows_per_chunk;
-    const uint32_t r1 = min(row_end, r0 + rows_per_chunk);
-    unsigned long long acc[4] = {0, 0, 0, 0};
-    if (c4 < cols4) {
-        for (uint32_t r = r0 + threadIdx.y; r < r1; r += blockDim.y) {
-            const size_t o = static_cast<size_t>(r) * cols4 + c4;
-            uint4 t = make_uint4(0u, 0u, 0u, 0u);
-            for (uint32_t p = 0; p < pc.n; ++p) {
-                const uint4 b = reinterpret_cast<const uint4*>(pc.B[p])[o];
-                t.x += b.x; t.y += b.y; t.z += b.z; t.w += b.w;
-            }
-            reinterpret_cast<uint4*>(B)[o] = t;
-            acc[0] += t.x; acc[1] += t.y; acc[2] += t.z; acc[3] += t.w;
+__device__ __forceinline__ uint32_t count_pieces(uint32_t c) { return (c + 65534u) / 65535u; }  // 0 for c == 0
+
+// Warp per row of [row_lo, row_hi): pass 1 counts the row's entries, one atomic reserves them,
+// pass 2 re-reads the row (L1/L2-hot) and writes them in topic order.  A reservation past
+// `cap` (cannot happen with the engine's capacity bound) records an empty row and flags it.
+__global__ void __launch_bounds__(256) sparsify_kernel(const uint32_t* __restrict__ B, uint32_t row_lo,
+                                                       uint32_t row_hi, uint32_t K_pad, uint2* __restrict__ info,
+                                                       uint32_t* __restrict__ entries, uint32_t* cursor, uint32_t cap,
+                                                       uint32_t* overflow) {
+    const uint32_t lane = threadIdx.x & 31u;
+    const uint32_t nq = K_pad / 4u;
+    for (uint32_t v = row_lo + (blockIdx.x * blockDim.x + threadIdx.x) / 32u; v < row_hi;
+         v += gridDim.x * blockDim.x / 32u) {
+        const uint4* row = reinterpret_cast<const uint4*>(B + static_cast<size_t>(v) * K_pad);
+        uint32_t n = 0;
+        for (uint32_t i = lane; i < nq; i += 32u) {
+            const uint4 c = __ldg(row + i);
+            n += count_pieces(c.x) + count_pieces(c.y) + count_pieces(c.z) + count_pieces(c.w);
         }
-    }
-    const uint32_t tid = threadIdx.y * blockDim.x + threadIdx.x;
-    for (int j = 0; j < 4; ++j) s_acc[tid][j] = acc[j];
-    __syncthreads();
-    if (threadIdx.y == 0 && c4 < cols4) {
-        for (uint32_t y = 1; y < blockDim.y; ++y)
-            for (int j = 0; j < 4; ++j) acc[j] += s_acc[y * blockDim.x + threadIdx.x][j];
-        for (int j = 0; j < 4; ++j)
-            if (acc[j]) atomicAdd(colsum + 4 * c4 + j, acc[j]);
+        n = __reduce_add_sync(0xffffffffu, n);
+        uint32_t off = 0;
+        if (lane == 0 && n) {
+            off = atomicAdd(cursor, n);
+            if (off + n > cap || off + n < off) {
+                atomicOr(overflow, 1u);
+                n = 0;
+            }
+        }
+        off = __shfl_sync(0xffffffffu, off, 0);
+        n = __shfl_sync(0xffffffffu, n, 0);
+        if (lane == 0) info[v - row_lo] = make_uint2(off, n);
+        if (n == 0) continue;
+        for (uint32_t i0 = 0; i0 < nq; i0 += 32u) {
+            const uint32_t i = i0 + lane;
+            const uint4 c = i < nq ? __ldg(row + i) : make_uint4(0u, 0u, 0u, 0u);
+            const uint32_t m = count_pieces(c.x) + count_pieces(c.y) + count_pieces(c.z) + count_pieces(c.w);
+            uint32_t incl = m;
+#pragma unroll
+            for (uint32_t o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += y;
+            }
+            uint32_t pos = off + incl - m;
+            const uint32_t cs[4] = {c.x, c.y, c.z, c.w};
+#pragma unroll
+            for (uint32_t j = 0; j < 4; ++j) {
+                uint32_t left = cs[j];
+                const uint32_t k = 4u * i + j;
+                while (left) {
+                    const uint32_t piece = left < 65535u ? left : 65535u;
+                    entries[pos++] = k | (piece << 16);
+                    left -= piece;
+                }
+            }
+            off += __shfl_sync(0xffffffffu, incl, 31);
+        }
     }
 }
 
-cudaError_t launch_peer_colsum(const PeerCounts& pc, uint32_t* B, uint32_t row_begin, uint32_t row_end,
-                               uint32_t K_pad, unsigned long long* colsum, cudaStream_t s) {
-    if (row_end <= row_begin) return cudaSuccess;
-    const uint32_t cols4 = K_pad / 4;
-    const uint32_t bx = cols4 < 256 ? cols4 : 256;
-    const uint32_t by = 256 / bx;
-    const uint32_t gx = (cols4 + bx - 1) / bx;
-    const uint32_t rows = row_end - row_begin;
-    uint32_t gy = (148u * 8u + gx - 1) / gx;
-    uint32_t per = (rows + gy - 1) / gy;
-    if (per < by) per = by;
-    gy = (rows + per - 1) / per;
-    peer_colsum_kernel<<<dim3(gx, gy), dim3(bx, by), 0, s>>>(pc, B, row_begin, row_end, cols4, per, colsum);
+cudaError_t launch_sparsify(const uint32_t* B, uint32_t row_lo, uint32_t row_hi, uint32_t K_pad, uint2* info,
+                            uint32_t* entries, uint32_t* cursor, uint32_t cap, uint32_t* overflow, cudaStream_t s) {
+    if (row_hi <= row_lo) return cudaSuccess;
+    const uint32_t rows = row_hi - row_lo;
+    const uint32_t blocks = rows / 8u + 1u < 148u * 16u ? rows / 8u + 1u : 148u * 16u;
+    sparsify_kernel<<<blocks, 256, 0, s>>>(B, row_lo, row_hi, K_pad, info, entries, cursor, cap, overflow);
     return cudaGetLastError();
 }
 
-// All-reduce of C_k fused into the denominator: sum of the ranks' partials (u64, order-free).
-__global__ void peer_total_kernel(PeerColsums pc, uint32_t K_pad, unsigned long long* total) {
-    const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
-    if (k >= K_pad) return;
-    unsigned long long t = 0;
-    for (uint32_t p = 0; p < pc.n; ++p) t += pc.c[p][k];
-    total[k] = t;
+// Warp per row of [row_lo, row_hi), skipping [skip_lo, skip_hi): adds the row's entries from
+// its sources into B.  Reduce-scatter (per_slice == 0): every source, row index v - base.
+// All-gather (per_slice > 0): the one source owning the row, src[v / per_slice], row index
+// v - its base.  `bytes` tallies what was read from the sources (entries + row index).
+__global__ void __launch_bounds__(256) gather_add_kernel(PeerSparse ps, uint32_t row_lo, uint32_t row_hi,
+                                                         uint32_t skip_lo, uint32_t skip_hi, uint32_t per_slice,
+                                                         uint32_t* __restrict__ B, uint32_t K_pad,
+                                                         unsigned long long* bytes) {
+    const uint32_t lane = threadIdx.x & 31u;
+    unsigned long long got = 0;
+    for (uint32_t v = row_lo + (blockIdx.x * blockDim.x + threadIdx.x) / 32u; v < row_hi;
+         v += gridDim.x * blockDim.x / 32u) {
+        if (v >= skip_lo && v < skip_hi) continue;
+        uint32_t* brow = B + static_cast<size_t>(v) * K_pad;
+        const uint32_t s0 = per_slice ? v / per_slice : 0u, s1 = per_slice ? s0 + 1u : ps.n;
+        for (uint32_t si = s0; si < s1; ++si) {
+            const SparseRows src = ps.src[si];
+            if (!src.info) continue;
+            const uint2 in = src.info[v - src.base];
+            for (uint32_t e = lane; e < in.y; e += 32u) {
+                const uint32_t x = src.entries[in.x + e];
+                atomicAdd(brow + (x & 0xFFFFu), x >> 16);
+            }
+            if (lane == 0) got += 8ull + 4ull * in.y;
+        }
+    }
+    if (lane == 0 && got) atomicAdd(bytes, got);
 }
 
-cudaError_t launch_peer_total(const PeerColsums& pc, uint32_t K_pad, unsigned long long* total, cudaStream_t s) {
-    peer_total_kernel<<<(K_pad + 255) / 256, 256, 0, s>>>(pc, K_pad, total);
+cudaError_t launch_gather_add(const PeerSparse& ps, uint32_t row_lo, uint32_t row_hi, uint32_t skip_lo,
+                              uint32_t skip_hi, uint32_t per_slice, uint32_t* B, uint32_t K_pad,
+                              unsigned long long* bytes, cudaStream_t s) {
+    if (row_hi <= row_lo) return cudaSuccess;
+    const uint32_t rows = row_hi - row_lo;
+    const uint32_t blocks = rows / 8u + 1u < 148u * 16u ? rows / 8u + 1u : 148u * 16u;
+    gather_add_kernel<<<blocks, 256, 0, s>>>(ps, row_lo, row_hi, skip_lo, skip_hi, per_slice, B, K_pad, bytes);
     return cudaGetLastError();
 }
 

@@ -1,13 +1,14 @@
 """GPU, world_size 2, 4 and 8 on ONE B200: the peer-memory M-step exchange, bit for bit.
 
 N processes each own a document shard (the chunk_boundaries rule) and an engine created
-with world_size N; they exchange CUDA IPC handles of their C_wk / C_k / phi / L4 / L8 / Q
-buffers and attach (include/saberlda.h, slda_peer_attach).  From then on every M-step does the
-reduce-scatter of C_wk inside its colsum kernel, the all-reduce of C_k inside the denominator
-kernel and the all-gather of phi / L4 / L8 / Q inside the phi kernel's epilogue, over the other
-rank's memory, meeting at device-side barriers (mstep.cu).  On a multi-GPU node the same code
-runs over NVLink peer memory; here all ranks share one GPU, which exercises the same kernels,
-handles, barrier targets, word-row slices and mirror lists (PeerMirror.n = N-1 up to 7).  The assembled state must equal the reference's digests for the C1 case
+with world_size N; they exchange CUDA IPC handles of their sparse C_wk lists and attach
+(include/saberlda.h, slda_peer_attach).  From then on every M-step lists the partial C_wk's
+non-zeros, adds the other ranks' entries of its word slice (reduce-scatter), lists the reduced
+slice and adds every other slice's entries (all-gather), over the other ranks' memory, meeting
+at device-side barriers (mstep.cu sparsify / gather_add); phi / L4 / L8 / Q are then computed
+locally.  On a multi-GPU node the same code runs over NVLink peer memory; here all ranks share
+one GPU, which exercises the same kernels, handles, barrier targets and word-row slices (up to
+7 sources per gather).  The assembled state must equal the reference's digests for the C1 case
 at every iteration -- exactly what one GPU produces.
 """
 import multiprocessing as mp
@@ -24,13 +25,26 @@ pytestmark = pytest.mark.gpu
 ITERS = 6
 
 
+def _heavy_corpus():
+    """K=1 (or 2): one word carries 160K of 200K tokens, so per-rank partial counts and the
+    reduced counts exceed 65535 and the sparse lists split them into several entries."""
+    rng = np.random.default_rng(5)
+    D, V, T = 64, 5, 200_000
+    doc = np.sort(rng.integers(0, D, T)).astype(np.uint32)
+    word = np.where(rng.random(T) < 0.8, 0, rng.integers(1, V, T)).astype(np.uint32)
+    return doc, word, D, V
+
+
+HEAVY = {"heavy_k1": {"K": 1, "seed": 3}, "heavy_k2": {"K": 2, "seed": 4}}
+
+
 def _rank_main(rank, world, case, to_parent, from_parent):
     try:
         import paper_1610_02496_b200 as slda
         import paper_1610_02496_b200._core as core
 
-        spec = CASES[case]
-        doc, word, D, V = corpus_arrays(spec["corpus"])
+        spec = CASES[case] if case in CASES else HEAVY[case]
+        doc, word, D, V = corpus_arrays(spec["corpus"]) if case in CASES else _heavy_corpus()
         lens = np.bincount(doc, minlength=D).astype(np.uint32)
         bounds = core.shard_bounds_from_lengths(lens, world)
         b, e = bounds[rank], bounds[rank + 1]
@@ -45,9 +59,10 @@ def _rank_main(rank, world, case, to_parent, from_parent):
         if spec.get("sampler") == "vanilla":
             cfg.sampler = slda.SamplerKind.VANILLA
         m = core.init_view(toks, D, V, int(b), int(e), int(csum[b]), cfg, rank, world, 1)
-        to_parent.put(("handles", rank, m.peer_handles()))
-        all_handles = from_parent.get()
-        m.peer_attach(all_handles)
+        if world > 1:
+            to_parent.put(("handles", rank, m.peer_handles()))
+            all_handles = from_parent.get()
+            m.peer_attach(all_handles)
         out = []
         for it in range(ITERS + 1):
             offs, tops, cnts = m.doc_topic()
@@ -58,6 +73,7 @@ def _rank_main(rank, world, case, to_parent, from_parent):
                 "l4": m.tree_prefix(),
                 "tree_mass": m.tree_mass(),
                 "doc_topic": (offs.astype(np.uint64), tops.copy(), cnts.copy()),
+                "exchange_bytes": m.kernel_times()["exchange_bytes"] if it else 0,
             })
             if it < ITERS:
                 m.run_iteration(cfg)
@@ -66,8 +82,8 @@ def _rank_main(rank, world, case, to_parent, from_parent):
         to_parent.put(("error", rank, traceback.format_exc()))
 
 
-@pytest.mark.parametrize("case,world", [("c1", 2), ("c1", 4), ("c1", 8), ("vanilla_c1", 2), ("u_k7_chunks", 3)])
-def test_peer_memory_exchange_matches_reference(golden, case, world):
+def _run(case, world):
+    """Per rank, per iteration state of a world-rank run (all ranks on cuda:0)."""
     ctx = mp.get_context("spawn")
     to_parent = ctx.Queue()
     inboxes = [ctx.Queue() for _ in range(world)]
@@ -92,28 +108,52 @@ def test_peer_memory_exchange_matches_reference(golden, case, world):
             p.join(timeout=60)
             if p.is_alive():
                 p.kill()
+    return results
+
+
+def _assembled(results, world, it):
+    rs = [results[r][it] for r in range(world)]
+    for key in ("word_topic", "word_topic_prob", "l4", "tree_mass"):  # replicated state
+        for r in range(1, world):
+            assert np.array_equal(rs[0][key], rs[r][key]), (it, key, r)
+    offs, tops, cnts = [rs[0]["doc_topic"][0]], [], []
+    for r in range(world):
+        o, t, c = rs[r]["doc_topic"]
+        if r:
+            offs.append(o[1:] + offs[-1][-1])
+        tops.append(t)
+        cnts.append(c)
+    return {
+        "assignments": digest(np.concatenate([rs[r]["assignments"] for r in range(world)])),
+        "word_topic": digest(rs[0]["word_topic"]),
+        "word_topic_prob": digest(rs[0]["word_topic_prob"]),
+        "l4": digest(rs[0]["l4"]),
+        "tree_mass": digest(rs[0]["tree_mass"]),
+        "doc_topic": digest(np.concatenate([np.concatenate(offs).view(np.uint32), np.concatenate(tops),
+                                            np.concatenate(cnts)])),
+    }
+
+
+@pytest.mark.parametrize("case,world", [("heavy_k1", 2), ("heavy_k2", 3)])
+def test_peer_exchange_splits_large_counts(case, world):
+    """Counts above 65535 (one word, K <= 2) travel as several sparse entries; N ranks must equal
+    one GPU (itself bit-exact to the reference) at every iteration."""
+    one = _run(case, 1)
+    many = _run(case, world)
+    assert int(np.asarray(one[0][0]["word_topic"]).max()) > 65535
+    for it in range(ITERS + 1):
+        assert _assembled(many, world, it) == _assembled(one, 1, it), it
+
+
+@pytest.mark.parametrize("case,world", [("c1", 2), ("c1", 4), ("c1", 8), ("vanilla_c1", 2), ("u_k7_chunks", 3)])
+def test_peer_memory_exchange_matches_reference(golden, case, world):
+    results = _run(case, world)
     fx = golden["cases"][case]
     for it in range(min(ITERS, len(fx["iterations"]) - 1) + 1):
-        rs = [results[r][it] for r in range(world)]
-        # Replicated state: identical on every rank.
-        for key in ("word_topic", "word_topic_prob", "l4", "tree_mass"):
-            for r in range(1, world):
-                assert np.array_equal(rs[0][key], rs[r][key]), (it, key, r)
-        offs, tops, cnts = [rs[0]["doc_topic"][0]], [], []
-        for r in range(world):
-            o, t, c = rs[r]["doc_topic"]
-            if r:
-                offs.append(o[1:] + offs[-1][-1])
-            tops.append(t)
-            cnts.append(c)
-        got = {
-            "assignments": digest(np.concatenate([rs[r]["assignments"] for r in range(world)])),
-            "word_topic": digest(rs[0]["word_topic"]),
-            "word_topic_prob": digest(rs[0]["word_topic_prob"]),
-            "l4": digest(rs[0]["l4"]),
-            "tree_mass": digest(rs[0]["tree_mass"]),
-            "doc_topic": digest(np.concatenate([np.concatenate(offs).view(np.uint32), np.concatenate(tops),
-                                                np.concatenate(cnts)])),
-        }
+        got = _assembled(results, world, it)
         expect = fx["iterations"][it]
         assert got == expect, (world, it, sorted(k for k in got if got[k] != expect[k]))
+    # The sparse exchange read something from the other ranks, and far less than dense C_wk.
+    xb = [results[r][ITERS]["exchange_bytes"] for r in range(world)]
+    V_pad, K = len(results[0][0]["tree_mass"]), results[0][0]["word_topic"].shape[1]
+    assert all(0 < x < 2 * V_pad * K * 4 for x in xb), xb

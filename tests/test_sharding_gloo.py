@@ -1,12 +1,17 @@
 """CPU, world_size 2 over gloo: the multi-GPU choreography of one ESCA iteration.
 
 The engine shards documents across ranks and exchanges only in the M-step
-(engine.cu m_step): reduce-scatter of C_wk by word-row slices,
-all-reduce of the column sums C_k, phi/L4/Q on the own slice, all-gather.
-This test runs exactly that choreography on 2 CPU processes with gloo, using
-the product's own host rules (slda_shard_bounds, slda_word_slice through the
-C-ABI) and the C oracle for the per-token math, and checks that the result is
-bit-identical to the single-process oracle (hence to the reference).
+(engine.cu exchange / mstep.cu sparsify + gather_add): each rank
+lists its partial C_wk's non-zeros per word row (entries topic | count << 16,
+counts above 65535 split into several entries) with an {offset, n} index; the
+reduce-scatter adds the other ranks' entries of the own word slice; the reduced
+slice is listed the same way; the all-gather adds every other slice's entries
+into the (cleared) other rows; every rank then holds the full reduced C_wk and
+computes phi / L4 / Q over all rows.  This test runs exactly that choreography on
+2 CPU processes with gloo (all_gather_object standing in for the peer-memory
+reads), using the product's own host rules (slda_shard_bounds, slda_word_slice
+through the C-ABI) and the C oracle for the per-token math, and checks that the
+result is bit-identical to the single-process oracle (hence to the reference).
 """
 import ctypes as C
 import os
@@ -37,6 +42,41 @@ def _free_port():
     return port
 
 
+def sparsify(Bm, lo, hi):
+    """mstep.cu sparsify_kernel: rows [lo, hi) -> ({offset, n} per row, u32 entries)."""
+    info, ent = [], []
+    for v in range(lo, hi):
+        start = len(ent)
+        for k in np.nonzero(Bm[v])[0]:
+            left = int(Bm[v, k])
+            while left:
+                piece = min(left, 65535)
+                ent.append(int(k) | (piece << 16))
+                left -= piece
+        info.append((start, len(ent) - start))
+    return info, ent
+
+
+def gather_add(Bm, lst, base, rows):
+    """mstep.cu gather_add_kernel for one source list."""
+    info, ent = lst
+    for v in rows:
+        off, n = info[v - base]
+        for x in ent[off:off + n]:
+            Bm[v, x & 0xFFFF] += x >> 16
+
+
+def test_sparse_entries_split_large_counts():
+    Bm = np.zeros((3, 4), np.int64)
+    Bm[1, 2] = 200_000
+    Bm[2, 0] = 65535
+    info, ent = sparsify(Bm, 0, 3)
+    assert info == [(0, 0), (0, 4), (4, 1)]
+    back = np.zeros_like(Bm)
+    gather_add(back, (info, ent), 0, range(3))
+    assert np.array_equal(back, Bm)
+
+
 def _rank_main(rank, world, port, out_dir):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
@@ -57,36 +97,42 @@ def _rank_main(rank, world, port, out_dir):
     # trainer.cpp:383-388: uniform initial topics keyed by corpus position
     topic = np.array([lib.orc_uniform_topic(SEED, 0xFFFFFFFF, int(t), K) for t in mine], np.uint32)
 
+    rows_per_slice = vpad // world
+
     def m_step(topic):
-        # local C_wk, then reduce-scatter by word rows (gloo: all_reduce + own slice)
-        Bl = np.zeros((vpad, K), np.int64)
+        Bl = np.zeros((vpad, K), np.int64)  # this rank's partial C_wk
         np.add.at(Bl, (word[mine], topic), 1)
-        Bt = torch.from_numpy(Bl)
-        dist.all_reduce(Bt)
-        Bs = Bt.numpy()[r0:r1]
-        colsum = torch.from_numpy(Bs.sum(axis=0).astype(np.int64))
-        dist.all_reduce(colsum)  # C_k
-        denom = colsum.numpy().astype(np.float64) + np.float64(V) * BETA
-        bhat_s = ((Bs.astype(np.float64) + BETA) / denom).astype(np.float32)
-        l4_s = np.zeros_like(bhat_s)
-        q_s = np.zeros(r1 - r0, np.float32)
-        for i in range(r1 - r0):
-            row = np.ascontiguousarray(bhat_s[i])
+        # partial list over all rows [0, V): index v - 0
+        info1, ent1 = sparsify(Bl, 0, V)
+        lists = [None] * world
+        dist.all_gather_object(lists, (info1, ent1))
+        # reduce-scatter: own slice += the other ranks' entries of it
+        for p in range(world):
+            if p != rank:
+                gather_add(Bl, lists[p], 0, range(r0, r1))
+        info2, ent2 = sparsify(Bl, r0, r1)
+        Bl[:r0] = 0
+        Bl[r1:] = 0
+        slices = [None] * world
+        dist.all_gather_object(slices, (info2, ent2))
+        # all-gather: row v of another slice from its owner v // rows_per_slice, index v - base
+        for v in range(V):
+            owner = v // rows_per_slice
+            if owner != rank:
+                gather_add(Bl, slices[owner], owner * rows_per_slice, [v])
+        B = Bl[:V]
+        # every rank: phi / L4 / Q over all rows
+        colsum = B.sum(axis=0)
+        denom = colsum.astype(np.float64) + np.float64(V) * BETA
+        bhat = ((B.astype(np.float64) + BETA) / denom).astype(np.float32)
+        l4 = np.zeros_like(bhat)
+        q = np.zeros(V, np.float32)
+        for v in range(V):
             out = np.zeros(K, np.float32)
-            total = lib.orc_row_prefix(row, K, out)
-            l4_s[i] = out
-            q_s[i] = falpha * np.float32(total)
-        # all-gather the slices (equal-sized over V_pad rows)
-        rows = vpad // world
-
-        def gather(x):
-            pad = np.zeros((rows,) + x.shape[1:], x.dtype)
-            pad[: len(x)] = x
-            parts = [torch.zeros_like(torch.from_numpy(pad)) for _ in range(world)]
-            dist.all_gather(parts, torch.from_numpy(pad))
-            return np.concatenate([p.numpy() for p in parts])[:V]
-
-        return gather(bhat_s), gather(l4_s), gather(q_s), gather(Bs.astype(np.int64))
+            total = lib.orc_row_prefix(np.ascontiguousarray(bhat[v]), K, out)
+            l4[v] = out
+            q[v] = falpha * np.float32(total)
+        return bhat, l4, q, B.copy()
 
     bhat, l4, q, B = m_step(topic)
     for it in range(ITERS):
