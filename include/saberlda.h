@@ -131,7 +131,10 @@ typedef struct slda_kernel_times {
  * (build_chunks corpus.cpp:125-198, build_schedule :200-210), initial topics
  * (init_assignments corpus.cpp:87-96), C_dk (rebuild_doc_topic counts.cpp:103-125),
  * C_wk (count_chunk_into trainer.cpp:223-235), phi (preprocess counts.cpp:37-63)
- * and the sampling trees (rebuild_trees trainer.cpp:237-248). */
+ * and the sampling trees (rebuild_trees trainer.cpp:237-248).
+ * Device limits the reference does not have (SLDA_ERR_VALIDATION, never silent): K <= 65536;
+ * every document shorter than 2^(32 - ceil(log2 K)) tokens (its counts share a 32-bit C_dk
+ * entry with the topic: 2^18 at K = 10K). */
 int slda_create(const slda_corpus_view* corpus, const slda_config* config, slda_engine** out);
 
 /* Eval-only model from checkpointed counts (model_from_checkpoint trainer.cpp:514-532):
@@ -186,7 +189,8 @@ int slda_get_pdow(slda_engine* e, uint32_t* sorted_doc, uint32_t* sorted_word,
 /* ------------------------------------------------------------------ eval -- */
 
 /* heldout_ll (eval.cpp:49-133) over a held-out corpus (AoS tokens, all docs), split by
- * HeldoutSet::from_corpus (eval.cpp:14-28). */
+ * HeldoutSet::from_corpus (eval.cpp:14-28).  Device limit: a document's estimation half (its
+ * even positions) holds at most 8192 tokens (SLDA_ERR_VALIDATION otherwise). */
 int slda_heldout_ll(slda_engine* e, uint32_t num_docs, uint32_t vocab_size, uint64_t num_tokens,
                     const uint32_t* tokens, uint32_t burn_in, uint64_t seed,
                     double* per_token_ll, uint64_t* tokens_evaluated);
