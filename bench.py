@@ -128,15 +128,16 @@ def iteration_bytes(T: int, row_entries: int, K: int, V: int, D: int, nnz: int, 
 
 
 def ncu_traffic():
-    """dram__bytes_read+write per sampler launch from the committed ncu --set full summary."""
+    """dram__bytes_read+write of one sampler launch from the committed ncu --set full summary,
+    with the algorithmic bytes of THAT launch (its iteration's E_t), so the two pair up."""
     p = REPO / "profiles" / "ncu_sampler_summary.json"
     if p.exists():
         try:
             d = json.loads(p.read_text())
-            return d.get("dram_bytes_per_launch"), d.get("config")
+            return d.get("dram_bytes_per_launch"), d.get("config"), d.get("algorithmic_bytes_at_capture")
         except (ValueError, KeyError):
             pass
-    return None, None
+    return None, None, None
 
 
 # --------------------------------------------------------------------- reference
@@ -391,7 +392,7 @@ def main() -> None:
     s_bytes = sampler_bytes(T_shard, row_entries, cfg["K"], info["num_units"])
     peak, peak_src = measured_peak()
     achieved = s_bytes / (kt["sampler_ms"] / 1e3) / 1e9
-    traffic, traffic_cfg = ncu_traffic()
+    traffic, traffic_cfg, traffic_alg = ncu_traffic()
     it_bytes = iteration_bytes(T_shard, row_entries, cfg["K"], cfg["V"], e - b, info["doc_topic_nnz"],
                                info["num_units"])
     it_achieved = it_bytes / (kt["total_ms"] / 1e3) / 1e9
@@ -409,6 +410,8 @@ def main() -> None:
                    "l2": "inputs larger than L2 (C_dk rows, phi, L4 are GBs; no flush needed)"},
         "roofline": {"bound": "hbm", "kernel": "sampler", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "traffic_config": traffic_cfg,
+                     "traffic_algorithmic_bytes": traffic_alg,
+                     "traffic_over_algorithmic": traffic / traffic_alg if traffic and traffic_alg else None,
                      "peak_source": peak_src, "algorithmic_bytes_per_launch": s_bytes,
                      "sampler_ms": kt["sampler_ms"], "iteration_achieved": it_achieved,
                      "iteration_frac": it_achieved / peak, "E_t": row_entries / max(1, T_shard)},

@@ -164,6 +164,7 @@ struct slda_engine {
     uint32_t nseg = 0, n_units = 0, n_long = 0;
     bool doc_major = true;
     bool vanilla = false;  // SamplerKind::kVanilla (trainer.cpp:281-285)
+    uint32_t row_pf = 0;     // SLDA_ROW_PREFETCH (experiment)
     int sampler_shape = -1;  // SLDA_SAMPLER (sampler.cu launch_sampler); -1 = default by K
     bool serial = false;     // SLDA_SERIAL=1: SSC on the main stream (measurement of each kernel alone)
     uint32_t wshift = 0;  // word field shift of the execution-order key
@@ -395,6 +396,7 @@ struct slda_engine {
         a.tbits = tbits;
         a.row_entries = entries_counter();
         a.shape = sampler_shape;
+        a.row_pf = row_pf;
         a.vanilla = vanilla ? 1u : 0u;
         a.alpha = falpha;  // static_cast<float>(state.alpha), trainer.cpp:283
         return a;
@@ -500,6 +502,7 @@ void slda_engine::build(const slda_corpus_view& cv, const slda_config& c) {
                        " exceeds the packed C_dk count range at this K");
     }
     if (const char* f = std::getenv("SLDA_SAMPLER")) sampler_shape = slda::sampler_shape_from_name(f);
+    if (const char* f = std::getenv("SLDA_ROW_PREFETCH")) row_pf = static_cast<uint32_t>(std::atoi(f));
     if (const char* f = std::getenv("SLDA_SERIAL")) serial = std::string(f) == "1";
 
     phase("doc_start");

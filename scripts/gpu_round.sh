@@ -14,8 +14,8 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
 echo ncu-list rc=$?
 # full captures at steady state (iteration 13, as bench.py's timed iterations): sampler, SSC, phi
 timeout 1200 ncu --set full --clock-control none --import-source on -k regex:"sampler" -s 12 -c 1 \
-    -o gpurun_out/prof_sampler_c3_${TAG} python scripts/profile_run.py --config c3 --iters 14 > /dev/null 2>&1
+    -o gpurun_out/prof_sampler_c3_${TAG} python scripts/profile_run.py --config c3 --iters 14 > gpurun_out/prof_sampler_c3_${TAG}.log 2>&1
 echo ncu-sampler rc=$?
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:"ssc_warp|phi_kernel|colsum" -s 36 -c 3 \
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"ssc_warp|phi_kernel|colsum|denom" -s 48 -c 4 \
     -o gpurun_out/prof_sscphi_c3_${TAG} python scripts/profile_run.py --config c3 --iters 14 > /dev/null 2>&1
 echo ncu-sscphi rc=$?

@@ -49,6 +49,29 @@ def launches(tag):
     return out
 
 
+def capture_algorithmic_bytes(tag):
+    """SURVEY §8(d) sampler bytes of the captured launch (iteration 13 of the ncu'd profile_run,
+    whose log prints entries/T per iteration): T*18 + 4*sum(len*nnz) + 8*K*U."""
+    log = REPO / "gpurun_out" / f"prof_sampler_c3_{tag}.log"
+    if not log.exists():
+        return None
+    import re
+    sys.path.insert(0, str(REPO))
+    import bench
+    cfg = bench.CONFIGS["c3"]
+    et, units = None, None
+    for line in log.read_text().splitlines():
+        m = re.match(r"iter 13: .* entries/T=([0-9.]+)", line)
+        if m:
+            et = float(m.group(1))
+        m = re.search(r"'num_units': (\d+)", line)
+        if m:
+            units = int(m.group(1))
+    if et is None or units is None:
+        return None
+    return bench.sampler_bytes(cfg["T"], int(et * cfg["T"]), cfg["K"], units)
+
+
 def kernels(tag):
     out = []
     for rep in (f"prof_sampler_c3_{tag}.ncu-rep", f"prof_sscphi_c3_{tag}.ncu-rep"):
@@ -86,7 +109,11 @@ def kernels(tag):
                 u = k.get(m + "@unit", "byte")
                 f = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}.get(u, 1)
                 return k[m] * f
-            summary = {"dram_bytes_per_launch": gb("dram__bytes_read.sum") + gb("dram__bytes_write.sum"),
+            alg = capture_algorithmic_bytes(tag)
+            dram = gb("dram__bytes_read.sum") + gb("dram__bytes_write.sum")
+            summary = {"dram_bytes_per_launch": dram,
+                       "algorithmic_bytes_at_capture": alg,
+                       "dram_over_algorithmic": dram / alg if alg else None,
                        "dram_read_bytes": gb("dram__bytes_read.sum"), "dram_write_bytes": gb("dram__bytes_write.sum"),
                        "duration_ms_under_ncu": k["gpu__time_duration.sum"],
                        "config": f"C3 iteration 13 (steady state, as the bench), tag {tag}, ncu --set full --clock-control none"}
