@@ -76,6 +76,14 @@ typedef struct slda_config {
     uint32_t world_size;      /* number of shards/GPUs (1 = no exchange; > 1: peer-memory
                                  exchange, slda_peer_export / slda_peer_attach) */
     uint32_t sampler;         /* SLDA_SAMPLER_* -- TrainConfig::sampler (trainer.hpp:18, :30) */
+    uint32_t num_chunks;      /* TrainConfig::num_chunks (trainer.hpp:25); 0/1 = one resident shard */
+    uint64_t device_budget;   /* bytes of device memory the corpus state may use (0 = the free
+                                 memory).  With num_chunks > 1 and a state (~16 B/token, ~88 B/token
+                                 while building) above it, the engine STREAMS: each chunk's state
+                                 lives in pinned host memory and passes through the GPU once per
+                                 iteration -- the reference's file-backed ChunkStore
+                                 (trainer.cpp:65-198, :406-415) with HBM as the budget.  Results
+                                 are bit-identical either way. */
 } slda_config;
 
 /* sparselda::SamplerKind (trainer.hpp:18). */
@@ -105,6 +113,8 @@ typedef struct slda_info {
     uint32_t doc_major;       /* 1 if tokens came doc-sorted (no slot permutation) */
     uint32_t padded_topics;   /* K rounded up to the L4 block width (32) */
     uint32_t sampler_shape;   /* SLDA_SHAPE_*: the sampler kernel the iterations launch */
+    uint32_t num_chunks;      /* chunks the state is held in (1 unless streaming) */
+    uint32_t streaming;       /* 1: chunks stream through the GPU each iteration (device_budget) */
 } slda_info;
 
 /* Sampler kernels (slda_info.sampler_shape). */

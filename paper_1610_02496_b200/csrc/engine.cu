@@ -139,6 +139,36 @@ struct DevMem {
     template <class T> T* as() const { return static_cast<T*>(p); }
 };
 
+// Pinned host buffer: the chunk images of the streaming mode (slda_config.num_chunks).
+struct HostBuf {
+    void* p = nullptr;
+    size_t bytes = 0;
+    HostBuf() = default;
+    HostBuf(const HostBuf&) = delete;
+    HostBuf& operator=(const HostBuf&) = delete;
+    HostBuf(HostBuf&& o) noexcept : p(o.p), bytes(o.bytes) { o.p = nullptr, o.bytes = 0; }
+    ~HostBuf() {
+        if (p) cudaFreeHost(p);
+    }
+    void alloc(size_t n) {
+        if (p) cudaFreeHost(p);
+        p = nullptr;
+        bytes = n;
+        if (n) cuda_check(cudaMallocHost(&p, n), "cudaMallocHost");
+    }
+};
+
+// One chunk of a streaming engine (the reference's file-backed ChunkStore slot,
+// trainer.cpp:65-198, held in pinned host memory instead of a spill file): the device state
+// build_state() produced for its document range, and the scalars that describe it.
+struct ChunkImage {
+    uint32_t doc_begin = 0, doc_end = 0, D = 0, nseg = 0, n_units = 0, n_long = 0, tbits = 1, wshift = 0;
+    uint64_t T = 0, id_base = 0, out_offset = 0;
+    bool doc_major = true, have_ids = false;
+    std::vector<uint64_t> view_pos;  // gathered chunks: position in the engine's view per chunk token
+    HostBuf tok, z, doc_start, row4, A, units, long_docs, ids, input_of_slot, seg_word, seg_off, seg_len, schedule;
+};
+
 uint32_t bits_for(uint64_t max_value) {
     uint32_t b = 1;
     while (b < 64 && (max_value >> b) != 0) ++b;
@@ -163,8 +193,18 @@ struct slda_engine {
     uint32_t rank = 0, world = 1;
     uint32_t nseg = 0, n_units = 0, n_long = 0;
     bool doc_major = true;
+    bool have_ids = false;  // per-slot RNG element ids (non doc-major input or explicit ids)
     bool vanilla = false;  // SamplerKind::kVanilla (trainer.cpp:281-285)
-    uint32_t row_pf = 0;     // SLDA_ROW_PREFETCH (experiment)
+    uint32_t tbits0 = 1;   // minimal C_dk topic field for K (configure)
+    // Streaming mode (slda_config.num_chunks > 1 and the corpus state over device_budget): the
+    // shard's documents in chunks whose state lives in pinned host memory and passes through
+    // the device buffers above one chunk at a time.  T_view / D_view: the whole engine view.
+    bool streaming = false;
+    std::vector<ChunkImage> chunks;
+    int resident = -1;      // chunk whose state is in the device buffers
+    HostBuf chunk_nnz;      // per chunk: nnz of its C_dk after the last SSC (u64, pinned)
+    uint64_t T_view = 0;
+    uint32_t D_view = 0, view_begin = 0, view_end = 0;
     int sampler_shape = -1;  // SLDA_SAMPLER (sampler.cu launch_sampler); -1 = default by K
     bool serial = false;     // SLDA_SERIAL=1: SSC on the main stream (measurement of each kernel alone)
     uint32_t wshift = 0;  // word field shift of the execution-order key
@@ -328,7 +368,7 @@ struct slda_engine {
         K_pad = (K + slda::kBlock - 1) / slda::kBlock * slda::kBlock;
         n_l8 = K_pad / slda::kLeaf;
         l8_stride = (n_l8 + 3) / 4 * 4;
-        tbits = bits_for(K - 1 ? K - 1 : 1);
+        tbits = tbits0 = bits_for(K - 1 ? K - 1 : 1);
         device = c.device;
         if (device < 0) CK(cudaGetDevice(&device));
         set_device();
@@ -371,6 +411,16 @@ struct slda_engine {
 
     // ---- init_state (trainer.cpp:354-417) ----
     void build(const slda_corpus_view& cv, const slda_config& c);
+    // The device state of one document range (PDOW, C_dk, initial topics, its C_wk counts added
+    // into B; B zeroed first when `first`).  `defer_scratch`: release the setup arena off the
+    // caller's path (single-shard engines).
+    void build_state(const slda_corpus_view& cv, const slda_config& c, bool first, bool defer_scratch);
+    void build_streaming(const slda_corpus_view& cv, const slda_config& c);
+    void save_image(ChunkImage& im);
+    void swap_in(uint32_t ci);
+    void swap_out(uint32_t ci);
+    void enqueue_streaming_iteration();
+    uint64_t doc_topic_nnz_total() const;
     // ---- run_iteration (trainer.cpp:419-449) ----
     void enqueue_iteration();
     // Sampler launch arguments of the next iteration.
@@ -383,7 +433,7 @@ struct slda_engine {
         a.l4 = l4.as<float>();
         a.l8 = l8.as<float>();
         a.q = q.as<float>();
-        a.ids = ids.p ? ids.as<uint64_t>() : nullptr;
+        a.ids = have_ids ? ids.as<uint64_t>() : nullptr;
         a.z = z.as<uint16_t>();
         a.B = B.as<uint32_t>();
         a.seed = seed;
@@ -396,7 +446,6 @@ struct slda_engine {
         a.tbits = tbits;
         a.row_entries = entries_counter();
         a.shape = sampler_shape;
-        a.row_pf = row_pf;
         a.vanilla = vanilla ? 1u : 0u;
         a.alpha = falpha;  // static_cast<float>(state.alpha), trainer.cpp:283
         return a;
@@ -408,6 +457,43 @@ struct slda_engine {
 
 // ----------------------------------------------------------------- build --
 void slda_engine::build(const slda_corpus_view& cv, const slda_config& c) {
+    D_all = cv.num_docs;
+    if (cv.doc_begin > cv.doc_end || cv.doc_end > D_all) validation("invalid document shard range");
+    if (cv.num_tokens > 0 && !cv.tokens) validation("tokens is null");
+    configure(c, cv.vocab_size);
+    alloc_model();
+    // Streaming (the reference's file-backed chunks, trainer.cpp:406-415, with the GPU's memory
+    // as the budget): the corpus state (~16 B/token resident, ~72 B/token more while building)
+    // does not fit the device budget and more than one chunk was asked for.
+    if (c.num_chunks > 1 && world == 1 && cv.num_tokens > 0) {
+        uint64_t budget = c.device_budget;
+        if (!budget) {
+            size_t free_b = 0, total_b = 0;
+            CK(cudaMemGetInfo(&free_b, &total_b));
+            budget = static_cast<uint64_t>(free_b * 0.9);
+        }
+        const uint64_t need = cv.num_tokens * 88 + static_cast<uint64_t>(cv.doc_end - cv.doc_begin) * 144;
+        streaming = need > budget;
+    }
+    if (streaming) {
+        build_streaming(cv, c);
+        return;
+    }
+    build_state(cv, c, true, true);
+    T_view = T;
+    D_view = D;
+    view_begin = doc_begin;
+    view_end = doc_end;
+    if (peer) {  // the first M-step needs the other ranks: it runs in slda_peer_attach
+        alloc_exchange();
+    } else {
+        m_step();
+    }
+    CK(cudaStreamSynchronize(stream));
+    nnz = d2h_scalar(nnz_counter());
+}
+
+void slda_engine::build_state(const slda_corpus_view& cv, const slda_config& c, bool first, bool defer_scratch) {
     // SLDA_TRACE=1: per-phase wall times of the setup on stderr (stream synchronised).
     const bool trace = std::getenv("SLDA_TRACE") != nullptr;
     auto t_last = std::chrono::steady_clock::now();
@@ -419,21 +505,18 @@ void slda_engine::build(const slda_corpus_view& cv, const slda_config& c) {
                      std::chrono::duration<double, std::milli>(now - t_last).count());
         t_last = now;
     };
-    D_all = cv.num_docs;
     doc_begin = cv.doc_begin;
     doc_end = cv.doc_end;
-    if (doc_begin > doc_end || doc_end > D_all) validation("invalid document shard range");
     D = doc_end - doc_begin;
     T = cv.num_tokens;
     if (T >= (1ull << 32)) validation("a single engine holds < 2^32 tokens; shard documents across GPUs");
-    if (T > 0 && !cv.tokens) validation("tokens is null");
     id_base = cv.token_id_base;
-    configure(c, cv.vocab_size);
-    alloc_model();
+    tbits = tbits0;
+    have_ids = false;
     // Scratch for every setup temporary below (~70 B/token at most); without room, plain
     // allocations.
     Arena arena(static_cast<size_t>(T) * 72 + static_cast<size_t>(D) * 64 + (256u << 20));
-    arena.deferred = &scratch_to_free;  // freed off the caller's path (release_scratch_async)
+    if (defer_scratch) arena.deferred = &scratch_to_free;  // freed off the caller's path (release_scratch_async)
     phase("configure+alloc_model");
 
     // Copy the borrowed AoS tokens (sparselda::Token layout) and validate on device.
@@ -502,7 +585,6 @@ void slda_engine::build(const slda_corpus_view& cv, const slda_config& c) {
                        " exceeds the packed C_dk count range at this K");
     }
     if (const char* f = std::getenv("SLDA_SAMPLER")) sampler_shape = slda::sampler_shape_from_name(f);
-    if (const char* f = std::getenv("SLDA_ROW_PREFETCH")) row_pf = static_cast<uint32_t>(std::atoi(f));
     if (const char* f = std::getenv("SLDA_SERIAL")) serial = std::string(f) == "1";
 
     phase("doc_start");
@@ -522,6 +604,7 @@ void slda_engine::build(const slda_corpus_view& cv, const slda_config& c) {
         });
         // RNG element id per slot (trainer.cpp:275 keys streams by corpus position).
         ids.alloc(T * 8, &device_bytes);
+        have_ids = true;
         DevMem ids_in;
         if (cv.token_ids) {
             ids_in.alloc(T * 8, nullptr);
@@ -649,7 +732,7 @@ void slda_engine::build(const slda_corpus_view& cv, const slda_config& c) {
     // Initial topics (trainer.cpp:383-388 / corpus.cpp:87-96), by slot.
     z.alloc(T * 2, &device_bytes);
     if (draw) {
-        CK(slda::launch_init_topics(T, ids.p ? ids.as<uint64_t>() : nullptr, id_base, seed, K,
+        CK(slda::launch_init_topics(T, have_ids ? ids.as<uint64_t>() : nullptr, id_base, seed, K,
                                     z.as<uint16_t>(), stream));
     } else {
         CK(slda::launch_given_topics(topic_in.as<uint32_t>(), doc_major ? nullptr : input_of_slot.as<uint32_t>(),
@@ -660,20 +743,254 @@ void slda_engine::build(const slda_corpus_view& cv, const slda_config& c) {
     topic_in.release();
 
     phase("long docs + init topics");
-    // C_dk (rebuild_doc_topic), C_wk (count_chunk_into), phi + trees.
+    // C_dk (rebuild_doc_topic), C_wk (count_chunk_into); phi + trees follow in build().
     ssc(stream);
-    CK(cudaMemsetAsync(B.p, 0, B.bytes, stream));
-    slda::RecountDraw rd{seed, id_base, ids.p ? ids.as<uint64_t>() : nullptr, draw ? K : 0u};
+    if (first) CK(cudaMemsetAsync(B.p, 0, B.bytes, stream));
+    slda::RecountDraw rd{seed, id_base, have_ids ? ids.as<uint64_t>() : nullptr, draw ? K : 0u};
     CK(slda::launch_recount(tok.as<uint2>(), units.as<slda::Unit>(), n_units, z.as<uint16_t>(),
                             B.as<uint32_t>(), K_pad, rd, stream));
-    if (peer) {  // the first M-step needs the other ranks: it runs in slda_peer_attach
-        alloc_exchange();
-    } else {
-        m_step();
+    phase("ssc + recount");
+}
+
+// ---- streaming mode (out-of-core chunks) ----
+// The reference streams chunks through host RAM when their state exceeds memory_budget
+// (trainer.cpp:406-415, ChunkStore :65-198: one chunk acquired at a time, spilled to a file
+// on release).  Here the budget is the GPU's: each chunk's device state is built once, kept
+// in pinned host memory, and passed through the engine's device buffers once per iteration
+// (H2D of the chunk, sampler + SSC, D2H of its topics and C_dk rows), C_wk accumulating over
+// the chunks before one M-step.  Token ids key the RNG and C_wk sums are integers, so the
+// result is bit-identical to one resident shard (acceptance.cpp:426-445).
+void slda_engine::build_streaming(const slda_corpus_view& cv, const slda_config& c) {
+    const uint32_t b0 = cv.doc_begin, b1 = cv.doc_end;
+    const uint64_t Tv = cv.num_tokens;
+    const uint32_t* tk = cv.tokens;  // sparselda::Token AoS {doc, word, topic}
+    // One host pass: validation (the device's messages), document lengths, doc-sortedness, and
+    // the corpus-wide topic rule (trainer.cpp:369-378), decided once for every chunk.
+    std::vector<uint32_t> lens(static_cast<size_t>(b1 - b0), 0u);
+    bool sorted = cv.token_ids == nullptr;
+    uint32_t mode = c.init_mode;
+    bool decided = mode != SLDA_INIT_AUTO;
+    for (uint64_t i = 0; i < Tv; ++i) {
+        const uint32_t d = tk[3 * i], w = tk[3 * i + 1], t = tk[3 * i + 2];
+        if (d < b0 || d >= b1) validation("token " + std::to_string(i) + ": doc outside the shard range");
+        if (w >= V) validation("token " + std::to_string(i) + ": word id out of range");
+        ++lens[d - b0];
+        if (i && d < tk[3 * (i - 1)]) sorted = false;
+        if (!decided) {
+            if (t == 0xFFFFFFFFu) {
+                mode = SLDA_INIT_DRAW;
+                decided = true;
+            } else if (t >= K) {
+                validation("token topic exceeds configured K");
+            }
+        } else if (mode == SLDA_INIT_GIVEN && t >= K) {
+            validation("token topic exceeds configured K");
+        }
     }
+    if (mode == SLDA_INIT_AUTO) mode = SLDA_INIT_GIVEN;
+    const uint32_t Dv = b1 - b0;
+    const uint32_t n = std::max<uint32_t>(1u, std::min<uint32_t>(c.num_chunks, std::max<uint32_t>(Dv, 1u)));
+    std::vector<uint32_t> bnd(static_cast<size_t>(n) + 1, 0u);
+    if (slda_shard_bounds(Dv, Tv, lens.data(), n, bnd.data()) != SLDA_OK) validation(g_error);
+    std::vector<uint64_t> tok_first(static_cast<size_t>(n) + 1, 0);
+    for (uint32_t ci = 0; ci < n; ++ci) {
+        uint64_t t = 0;
+        for (uint32_t d = bnd[ci]; d < bnd[ci + 1]; ++d) t += lens[d];
+        tok_first[ci + 1] = tok_first[ci] + t;
+    }
+    chunks.clear();
+    chunks.resize(n);
+    std::vector<uint64_t> nnzs(n, 0);
+    slda_config cc = c;
+    cc.init_mode = mode;
+    std::vector<uint32_t> gtok;
+    std::vector<uint64_t> gids;
+    for (uint32_t ci = 0; ci < n; ++ci) {
+        ChunkImage& im = chunks[ci];
+        slda_corpus_view sv = cv;
+        sv.doc_begin = b0 + bnd[ci];
+        sv.doc_end = b0 + bnd[ci + 1];
+        if (sorted) {  // a contiguous token range
+            const uint64_t f = tok_first[ci];
+            sv.tokens = tk + 3 * f;
+            sv.num_tokens = tok_first[ci + 1] - f;
+            sv.token_id_base = cv.token_id_base + f;
+            sv.token_ids = nullptr;
+            im.out_offset = f;
+        } else {  // gathered, in view order, with explicit ids
+            gtok.clear();
+            gids.clear();
+            im.view_pos.clear();
+            for (uint64_t i = 0; i < Tv; ++i) {
+                const uint32_t d = tk[3 * i];
+                if (d < sv.doc_begin || d >= sv.doc_end) continue;
+                gtok.insert(gtok.end(), tk + 3 * i, tk + 3 * i + 3);
+                gids.push_back(cv.token_ids ? cv.token_ids[i] : cv.token_id_base + i);
+                im.view_pos.push_back(i);
+            }
+            sv.tokens = gtok.data();
+            sv.num_tokens = gids.size();
+            sv.token_id_base = 0;
+            sv.token_ids = gids.data();
+        }
+        build_state(sv, cc, ci == 0, false);
+        CK(cudaStreamSynchronize(stream));
+        nnzs[ci] = d2h_scalar(nnz_counter());
+        save_image(im);
+    }
+    chunk_nnz.alloc(8ull * n);
+    std::memcpy(chunk_nnz.p, nnzs.data(), 8ull * n);
+    resident = static_cast<int>(n) - 1;  // the last chunk built is still in the device buffers
+    // Device buffers sized for the largest chunk, so iterations never allocate.
+    auto grow = [&](DevMem& d, size_t need) {
+        if (d.bytes < need) {
+            DevMem t;
+            t.alloc(need, &device_bytes);
+            if (d.p && d.bytes) CK(cudaMemcpyAsync(t.p, d.p, d.bytes, cudaMemcpyDeviceToDevice, stream));
+            CK(cudaStreamSynchronize(stream));
+            std::swap(d.p, t.p);
+            std::swap(d.bytes, t.bytes);
+        }
+    };
+    size_t m[13] = {};
+    for (const ChunkImage& im : chunks) {
+        const HostBuf* hb[13] = {&im.tok, &im.z, &im.doc_start, &im.row4, &im.A, &im.units, &im.long_docs,
+                                 &im.ids, &im.input_of_slot, &im.seg_word, &im.seg_off, &im.seg_len, &im.schedule};
+        for (int j = 0; j < 13; ++j) m[j] = std::max(m[j], hb[j]->bytes);
+    }
+    DevMem* db[13] = {&tok, &z, &doc_start, &row4, &A, &units, &long_docs, &ids, &input_of_slot,
+                      &seg_word, &seg_off, &seg_len, &schedule};
+    for (int j = 0; j < 13; ++j) grow(*db[j], m[j]);
+    uint64_t max_t = 0;
+    uint32_t max_long = 0;
+    for (const ChunkImage& im : chunks) {
+        max_t = std::max(max_t, im.T);
+        max_long = std::max(max_long, im.n_long);
+    }
+    if (max_long && static_cast<size_t>(K_pad) * 4 > 200 * 1024)
+        grow(hist_scratch, static_cast<size_t>(std::min<uint32_t>(max_long, 296)) * K_pad * 4);
+    if (!assign_buf.p || assign_buf.bytes < max_t * 4) assign_buf.alloc(std::max<uint64_t>(max_t, 1) * 4, &device_bytes);
+    T_view = Tv;
+    D_view = Dv;
+    view_begin = b0;
+    view_end = b1;
+    m_step();
     CK(cudaStreamSynchronize(stream));
-    nnz = d2h_scalar(nnz_counter());
-    phase("ssc + recount + m_step");
+    nnz = doc_topic_nnz_total();
+}
+
+void slda_engine::save_image(ChunkImage& im) {
+    im.doc_begin = doc_begin;
+    im.doc_end = doc_end;
+    im.D = D;
+    im.T = T;
+    im.id_base = id_base;
+    im.nseg = nseg;
+    im.n_units = n_units;
+    im.n_long = n_long;
+    im.tbits = tbits;
+    im.wshift = wshift;
+    im.doc_major = doc_major;
+    im.have_ids = have_ids;
+    auto save = [&](HostBuf& h, const DevMem& d, size_t bytes) {
+        h.alloc(bytes);
+        if (bytes) CK(cudaMemcpyAsync(h.p, d.p, bytes, cudaMemcpyDeviceToHost, stream));
+    };
+    save(im.tok, tok, T * 8);
+    save(im.z, z, T * 2);
+    save(im.doc_start, doc_start, (static_cast<size_t>(D) + 1) * 4);
+    save(im.row4, row4, (static_cast<size_t>(D) + 1) * 4);
+    save(im.A, A, A.bytes);
+    save(im.units, units, units.bytes);
+    save(im.long_docs, long_docs, static_cast<size_t>(n_long) * 4);
+    save(im.ids, ids, have_ids ? T * 8 : 0);
+    save(im.input_of_slot, input_of_slot, doc_major ? 0 : T * 4);
+    save(im.seg_word, seg_word, static_cast<size_t>(nseg) * 4);
+    save(im.seg_off, seg_off, static_cast<size_t>(nseg) * 4);
+    save(im.seg_len, seg_len, static_cast<size_t>(nseg) * 4);
+    save(im.schedule, schedule, static_cast<size_t>(nseg) * 4);
+    CK(cudaStreamSynchronize(stream));
+}
+
+// Chunk ci's state into the device buffers (stream-ordered, pinned -> HBM).
+void slda_engine::swap_in(uint32_t ci) {
+    if (resident == static_cast<int>(ci)) return;
+    const ChunkImage& im = chunks[ci];
+    auto load = [&](DevMem& d, const HostBuf& h) {
+        if (!h.bytes) return;
+        if (d.bytes < h.bytes) d.alloc(h.bytes, &device_bytes);  // only if build_streaming's sizing was short
+        CK(cudaMemcpyAsync(d.p, h.p, h.bytes, cudaMemcpyHostToDevice, stream));
+    };
+    load(tok, im.tok);
+    load(z, im.z);
+    load(doc_start, im.doc_start);
+    load(row4, im.row4);
+    load(A, im.A);
+    load(units, im.units);
+    load(long_docs, im.long_docs);
+    load(ids, im.ids);
+    load(input_of_slot, im.input_of_slot);
+    load(seg_word, im.seg_word);
+    load(seg_off, im.seg_off);
+    load(seg_len, im.seg_len);
+    load(schedule, im.schedule);
+    doc_begin = im.doc_begin;
+    doc_end = im.doc_end;
+    D = im.D;
+    T = im.T;
+    id_base = im.id_base;
+    nseg = im.nseg;
+    n_units = im.n_units;
+    n_long = im.n_long;
+    tbits = im.tbits;
+    wshift = im.wshift;
+    doc_major = im.doc_major;
+    have_ids = im.have_ids;
+    resident = static_cast<int>(ci);
+}
+
+// The resident chunk's mutable state (topics, C_dk rows, its nnz) back to its image.
+void slda_engine::swap_out(uint32_t ci) {
+    ChunkImage& im = chunks[ci];
+    if (im.z.bytes) CK(cudaMemcpyAsync(im.z.p, z.p, im.z.bytes, cudaMemcpyDeviceToHost, stream));
+    if (im.A.bytes) CK(cudaMemcpyAsync(im.A.p, A.p, im.A.bytes, cudaMemcpyDeviceToHost, stream));
+    CK(cudaMemcpyAsync(static_cast<uint64_t*>(chunk_nnz.p) + ci, nnz_counter(), 8, cudaMemcpyDeviceToHost, stream));
+}
+
+uint64_t slda_engine::doc_topic_nnz_total() const {
+    if (!streaming) return nnz;
+    uint64_t t = 0;
+    for (size_t ci = 0; ci < chunks.size(); ++ci) t += static_cast<const uint64_t*>(chunk_nnz.p)[ci];
+    return t;
+}
+
+// run_iteration over the chunks (trainer.cpp:425-432 with a file-backed store): reset C_wk,
+// then per chunk (the resident one first) H2D -> sampler -> SSC -> D2H, then one M-step.
+void slda_engine::enqueue_streaming_iteration() {
+    launches = 0;
+    slot = iteration % kRing;
+    ev = ring[slot];
+    CK(cudaEventRecord(ev[0], stream));
+    CK(cudaMemsetAsync(B.p, 0, B.bytes, stream));  // reset_word_topic (counts.cpp:134-138)
+    CK(cudaMemsetAsync(entries_counter(), 0, 8, stream));
+    CK(cudaEventRecord(ev[1], stream));
+    const uint32_t n = static_cast<uint32_t>(chunks.size());
+    const uint32_t first = resident >= 0 ? static_cast<uint32_t>(resident) : 0u;
+    for (uint32_t k = 0; k < n; ++k) {
+        const uint32_t ci = (first + k) % n;
+        swap_in(ci);
+        CK(slda::launch_sampler(sampler_args(), n_units, stream));
+        launches += n_units > 0;
+        ssc(stream);
+        swap_out(ci);
+    }
+    CK(cudaEventRecord(ev[2], stream));
+    CK(cudaEventRecord(ev[7], stream));
+    m_step();
+    CK(cudaEventRecord(ev[6], stream));
+    ring_launches[slot] = launches;
+    ++iteration;
+    ++enqueued;
 }
 
 void slda_engine::ssc(cudaStream_t st) {
@@ -751,6 +1068,10 @@ void slda_engine::exchange() {
 
 // run_iteration (trainer.cpp:419-449) on the engine stream.
 void slda_engine::enqueue_iteration() {
+    if (streaming) {
+        enqueue_streaming_iteration();
+        return;
+    }
     if (peer && !attached) validation("peer-memory exchange: call slda_peer_attach on every rank first");
     launches = 0;
     slot = iteration % kRing;
@@ -849,17 +1170,18 @@ int slda_iterate(slda_engine* e, slda_iteration_stats* stats) {
         e->enqueue_iteration();
         CK(cudaStreamSynchronize(e->stream));
         unsigned long long nnz_local = 0;
-        CK(cudaMemcpy(&nnz_local, e->nnz_counter(), 8, cudaMemcpyDeviceToHost));
+        if (e->streaming) nnz_local = e->doc_topic_nnz_total();
+        else CK(cudaMemcpy(&nnz_local, e->nnz_counter(), 8, cudaMemcpyDeviceToHost));
         e->nnz = nnz_local;
         const double elapsed = std::chrono::duration<double>(std::chrono::steady_clock::now() - start).count();
         if (stats) {
             float ms = 0;
             CK(cudaEventElapsedTime(&ms, e->ev[0], e->ev[6]));
             stats->iteration = e->iteration;
-            stats->tokens = e->T;
+            stats->tokens = e->T_view;
             stats->elapsed_s = elapsed;
-            stats->mtokens_per_s = elapsed > 0 ? static_cast<double>(e->T) / elapsed / 1e6 : 0.0;
-            stats->mean_doc_topics = e->D ? static_cast<double>(nnz_local) / e->D : 0.0;
+            stats->mtokens_per_s = elapsed > 0 ? static_cast<double>(e->T_view) / elapsed / 1e6 : 0.0;
+            stats->mean_doc_topics = e->D_view ? static_cast<double>(nnz_local) / e->D_view : 0.0;
             stats->device_ms = ms;
         }
     });
@@ -879,9 +1201,9 @@ int slda_get_info(const slda_engine* e, slda_info* info) {
         info->vocab_size = e->V;
         info->num_topics = e->K;
         info->iteration = e->iteration;
-        info->num_tokens = e->T;
-        info->doc_begin = e->doc_begin;
-        info->doc_end = e->doc_end;
+        info->num_tokens = e->T_view;
+        info->doc_begin = e->view_begin;
+        info->doc_end = e->view_end;
         info->rank = e->rank;
         info->world_size = e->world;
         info->alpha = e->alpha;
@@ -889,7 +1211,16 @@ int slda_get_info(const slda_engine* e, slda_info* info) {
         info->seed = e->seed;
         info->num_segments = e->nseg;
         info->num_units = e->n_units;
-        info->doc_topic_nnz = e->nnz;
+        if (e->streaming) {
+            info->num_segments = info->num_units = 0;
+            for (const ChunkImage& im : e->chunks) {
+                info->num_segments += im.nseg;
+                info->num_units += im.n_units;
+            }
+        }
+        info->doc_topic_nnz = e->streaming ? e->doc_topic_nnz_total() : e->nnz;
+        info->num_chunks = e->streaming ? static_cast<uint32_t>(e->chunks.size()) : 1u;
+        info->streaming = e->streaming ? 1u : 0u;
         info->device_bytes = e->device_bytes;
         info->doc_major = e->doc_major ? 1u : 0u;
         info->padded_topics = e->K_pad;
@@ -997,8 +1328,28 @@ int slda_get_tree_mass(slda_engine* e, float* out) {
 
 int slda_get_assignments(slda_engine* e, uint32_t* out) {
     return guarded([&] {
-        if (!e || (!out && e->T)) validation("null argument");
+        if (!e || (!out && e->T_view)) validation("null argument");
         e->set_device();
+        if (e->streaming) {  // chunk by chunk through the device buffers, into its positions
+            std::vector<uint32_t> tmp;
+            for (uint32_t ci = 0; ci < e->chunks.size(); ++ci) {
+                const ChunkImage& im = e->chunks[ci];
+                if (im.T == 0) continue;
+                e->swap_in(ci);
+                CK(slda::launch_assignments(e->z.as<uint16_t>(), e->doc_major ? nullptr : e->input_of_slot.as<uint32_t>(),
+                                            e->T, e->assign_buf.as<uint32_t>(), e->stream));
+                if (im.view_pos.empty()) {
+                    CK(cudaMemcpyAsync(out + im.out_offset, e->assign_buf.p, im.T * 4, cudaMemcpyDeviceToHost, e->stream));
+                } else {
+                    tmp.resize(im.T);
+                    CK(cudaMemcpyAsync(tmp.data(), e->assign_buf.p, im.T * 4, cudaMemcpyDeviceToHost, e->stream));
+                    CK(cudaStreamSynchronize(e->stream));
+                    for (uint64_t i = 0; i < im.T; ++i) out[im.view_pos[i]] = tmp[i];
+                }
+            }
+            CK(cudaStreamSynchronize(e->stream));
+            return;
+        }
         if (e->T == 0) return;
         // Permute/widen on the device, then one D2H straight into the caller's buffer.
         if (!e->assign_buf.p) e->assign_buf.alloc(e->T * 4, &e->device_bytes);
@@ -1090,6 +1441,31 @@ HostRows fetch_rows(slda_engine* e) {
     CK(cudaMemcpy(h.A.data(), e->A.p, e->A.bytes, cudaMemcpyDeviceToHost));
     return h;
 }
+
+// A streaming engine's chunk rows, from the chunk's pinned image (current after every
+// completed iteration: swap_out copies them back).
+HostRows image_rows(const ChunkImage& im) {
+    HostRows h;
+    h.mask = (1u << im.tbits) - 1u;
+    h.tbits = im.tbits;
+    const uint32_t* ds = static_cast<const uint32_t*>(im.doc_start.p);
+    const uint32_t* r4 = static_cast<const uint32_t*>(im.row4.p);
+    const uint32_t* a = static_cast<const uint32_t*>(im.A.p);
+    h.doc_start.assign(ds, ds + im.D + 1);
+    h.row4.assign(r4, r4 + im.D + 1);
+    h.A.assign(a, a + im.A.bytes / 4);
+    return h;
+}
+
+// Every (rows, D) of the engine: its resident shard, or each streamed chunk in document order.
+template <class F>
+void for_each_rows(slda_engine* e, F&& f) {
+    if (!e->streaming) {
+        f(fetch_rows(e), e->D);
+        return;
+    }
+    for (const ChunkImage& im : e->chunks) f(image_rows(im), im.D);
+}
 }  // namespace
 
 extern "C" {
@@ -1099,9 +1475,10 @@ int slda_get_doc_topic_nnz(slda_engine* e, uint64_t* nnz) {
         if (!e || !nnz) validation("null argument");
         e->set_device();
         CK(cudaStreamSynchronize(e->stream));
-        const HostRows h = fetch_rows(e);
         uint64_t n = 0;
-        for (uint32_t d = 0; d < e->D; ++d) n += h.nnz(d);
+        for_each_rows(e, [&](const HostRows& h, uint32_t D) {
+            for (uint32_t d = 0; d < D; ++d) n += h.nnz(d);
+        });
         *nnz = n;
     });
 }
@@ -1111,17 +1488,18 @@ int slda_get_doc_topic(slda_engine* e, uint64_t* row_offsets, uint32_t* topics, 
         if (!e || !row_offsets) validation("null argument");
         e->set_device();
         CK(cudaStreamSynchronize(e->stream));
-        const HostRows h = fetch_rows(e);
-        uint64_t pos = 0;
+        uint64_t pos = 0, row = 0;
         row_offsets[0] = 0;
-        for (uint32_t d = 0; d < e->D; ++d) {
-            h.for_each(d, [&](uint32_t topic, uint32_t count) {
-                topics[pos] = topic;
-                counts[pos] = count;
-                ++pos;
-            });
-            row_offsets[d + 1] = pos;
-        }
+        for_each_rows(e, [&](const HostRows& h, uint32_t D) {
+            for (uint32_t d = 0; d < D; ++d) {
+                h.for_each(d, [&](uint32_t topic, uint32_t count) {
+                    topics[pos] = topic;
+                    counts[pos] = count;
+                    ++pos;
+                });
+                row_offsets[++row] = pos;
+            }
+        });
     });
 }
 
@@ -1130,6 +1508,7 @@ int slda_get_pdow(slda_engine* e, uint32_t* sorted_doc, uint32_t* sorted_word, u
                   uint32_t* seg_offset, uint32_t* seg_length, uint32_t* schedule) {
     return guarded([&] {
         if (!e) validation("null engine");
+        if (e->streaming) validation("the PDOW layout is per chunk in streaming mode (num_chunks > 1)");
         e->set_device();
         CK(cudaStreamSynchronize(e->stream));
         const uint64_t T = e->T;
@@ -1145,7 +1524,7 @@ int slda_get_pdow(slda_engine* e, uint32_t* sorted_doc, uint32_t* sorted_word, u
             CK(cudaMemcpy(sl.data(), e->seg_len.p, e->nseg * 4ull, cudaMemcpyDeviceToHost));
             CK(cudaMemcpy(sc.data(), e->schedule.p, e->nseg * 4ull, cudaMemcpyDeviceToHost));
         }
-        if (e->ids.p) {
+        if (e->have_ids) {
             ids.resize(T);
             CK(cudaMemcpy(ids.data(), e->ids.p, T * 8, cudaMemcpyDeviceToHost));
         }

@@ -94,6 +94,8 @@ py::dict info_dict(const slda_info& i) {
     d["padded_topics"] = i.padded_topics;
     static const char* kShapes[] = {"round", "quad512", "quad256", "global", "vanilla"};
     d["sampler_shape"] = i.sampler_shape < 5 ? kShapes[i.sampler_shape] : "unknown";
+    d["num_chunks"] = i.num_chunks;
+    d["streaming"] = i.streaming != 0;
     return d;
 }
 
@@ -169,6 +171,7 @@ PYBIND11_MODULE(_core, m) {
         .def_readwrite("num_workers", &TrainConfig::num_workers)
         .def_readwrite("seed", &TrainConfig::seed)
         .def_readwrite("memory_budget", &TrainConfig::memory_budget)
+        .def_readwrite("device_budget", &TrainConfig::device_budget)
         .def_readwrite("eval_every", &TrainConfig::eval_every)
         .def_readwrite("sampler", &TrainConfig::sampler)
         .def_readwrite("tree_branch", &TrainConfig::tree_branch)

@@ -348,8 +348,7 @@ __global__ void __launch_bounds__(NT, MINB) sampler_quad_kernel(SamplerArgs a) {
 // make room in the 64-register budget (C3 K=10K: 95.5 -> 92.8 ms; C2: 19.8 -> 20.5 ms).
 // kGlobalPhi: the phi row does not fit shared memory (K >~ 45K): only L8 is staged and the
 // products gather phi through L1/L2.
-template <int NT, int MINB, int L, bool kC16 = false, bool kPrefetchNext = true, bool kGlobalPhi = false,
-          int kRowPf = 0>
+template <int NT, int MINB, int L, bool kC16 = false, bool kPrefetchNext = true, bool kGlobalPhi = false>
 __global__ void __launch_bounds__(NT, MINB) sampler_quad_pf_kernel(SamplerArgs a) {
     constexpr uint32_t NW = NT / 32;
     constexpr uint32_t TPR = 32u / L;  // tokens per round (L lanes each, L sectors per group)
@@ -412,9 +411,6 @@ __global__ void __launch_bounds__(NT, MINB) sampler_quad_pf_kernel(SamplerArgs a
             if (__all_sync(0xffffffffu, base + TPR * r >= unit.length)) break;
             const bool act = base + ti < unit.length;
             const uint4* row = A4 + __shfl_sync(0xffffffffu, tk.x, ti);
-            if (kRowPf && kPrefetchNext && r == 1 && nb + lane < unit.length)  // next batch's rows -> L2
-                asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(A4 + tk_nx.x), "r"(kRowPf * 128u)
-                             : "memory");
             if (!kPrefetchNext) {  // this round's first line, loaded now
                 c = zero_sector();
                 if (act) c = ldg_sector(row + 2 * sub);
@@ -576,11 +572,7 @@ size_t sampler_quad_smem(const SamplerArgs& a, int nt) {
 
 template <int NT, int MINB, bool PF, bool C16>
 cudaError_t launch_quad_t1(const SamplerArgs& a, uint32_t n_units, cudaStream_t s) {
-    auto kern = !PF ? sampler_quad_kernel<NT, MINB, 4, C16>
-              : a.row_pf == 2 ? sampler_quad_pf_kernel<NT, MINB, 4, C16, true, false, 2>
-              : a.row_pf == 3 ? sampler_quad_pf_kernel<NT, MINB, 4, C16, true, false, 3>
-              : a.row_pf == 4 ? sampler_quad_pf_kernel<NT, MINB, 4, C16, true, false, 4>
-                              : sampler_quad_pf_kernel<NT, MINB, 4, C16>;
+    auto kern = PF ? sampler_quad_pf_kernel<NT, MINB, 4, C16> : sampler_quad_kernel<NT, MINB, 4, C16>;
     const size_t smem = sampler_quad_smem(a, NT);
     if (const cudaError_t e = smem_optin(kern, smem); e != cudaSuccess) return e;
     kern<<<n_units, NT, smem, s>>>(a);

@@ -480,6 +480,8 @@ ModelState init_state(const Corpus& corpus, const TrainConfig& raw_cfg) {
     c.seed = cfg.seed;
     c.tree_branch = cfg.tree_branch;
     c.sampler = cfg.sampler == SamplerKind::kVanilla ? SLDA_SAMPLER_VANILLA : SLDA_SAMPLER_SPARSE;
+    c.num_chunks = cfg.num_chunks;
+    c.device_budget = cfg.device_budget;
     c.init_mode = SLDA_INIT_AUTO;
     c.device = cfg.device;
     c.rank = 0;
@@ -551,6 +553,8 @@ ModelState init_shard(const Corpus& corpus, const TrainConfig& raw_cfg, std::uin
     c.seed = cfg.seed;
     c.tree_branch = cfg.tree_branch;
     c.sampler = cfg.sampler == SamplerKind::kVanilla ? SLDA_SAMPLER_VANILLA : SLDA_SAMPLER_SPARSE;
+    c.num_chunks = cfg.num_chunks;
+    c.device_budget = cfg.device_budget;
     c.init_mode = mode;
     c.device = cfg.device;
     c.rank = rank;
@@ -583,6 +587,8 @@ ModelState init_view(const slda_corpus_view& view, const TrainConfig& raw_cfg, s
     c.seed = cfg.seed;
     c.tree_branch = cfg.tree_branch;
     c.sampler = cfg.sampler == SamplerKind::kVanilla ? SLDA_SAMPLER_VANILLA : SLDA_SAMPLER_SPARSE;
+    c.num_chunks = cfg.num_chunks;
+    c.device_budget = cfg.device_budget;
     c.init_mode = init_mode;
     c.device = cfg.device;
     c.rank = rank;

@@ -4,9 +4,10 @@
 // Same names, argument meaning and error behaviour as the reference so a caller
 // switches with `namespace sparselda = sparselda_b200;`.  Differences: the
 // model state lives in HBM, so ModelState exposes its matrices through
-// copying getters instead of public members; num_workers / num_chunks /
-// memory_budget / spill_dir are accepted and validated but have no effect
-// (results never depended on them: acceptance.cpp:389-445).
+// copying getters instead of public members; num_workers / memory_budget /
+// spill_dir are accepted and validated but have no effect (results never
+// depended on them: acceptance.cpp:389-445); num_chunks > 1 with a corpus state
+// above device_budget streams the chunks through the GPU (out-of-core).
 #pragma once
 
 #include <cstdint>
@@ -93,6 +94,9 @@ struct TrainConfig {  // trainer.hpp:20-36
     std::uint32_t tree_branch = 32;
     std::string spill_dir;
     int device = -1;  // CUDA ordinal (-1: current)
+    // Device memory the corpus state may use (0: the free memory).  With num_chunks > 1 and a
+    // larger state the engine streams its chunks through the GPU (slda_config.device_budget).
+    std::uint64_t device_budget = 0;
 
     TrainConfig resolved(const Corpus& corpus) const;  // trainer.cpp:15-35
 };

@@ -20,6 +20,8 @@ def main():
     ap.add_argument("--config", default="c2", choices=sorted(bench.CONFIGS))
     ap.add_argument("--iters", type=int, default=3)
     ap.add_argument("--shape", default=None, help="D,V,T,K override (experiments)")
+    ap.add_argument("--chunks", type=int, default=0, help="num_chunks (streaming with --device-budget)")
+    ap.add_argument("--device-budget", type=int, default=0, help="bytes; 1 forces streaming")
     args = ap.parse_args()
     import paper_1610_02496_b200 as slda
     import paper_1610_02496_b200._core as core
@@ -33,6 +35,8 @@ def main():
     tc.seed = bench.TRAIN_SEED
     tc.device = 0
     tc.tree_branch = 32 if cfg["K"] <= 32768 else 41
+    tc.num_chunks = args.chunks
+    tc.device_budget = args.device_budget
     m = core.init_view(toks, cfg["D"], cfg["V"], 0, cfg["D"], 0, tc)
     for _ in range(args.iters):
         t = time.perf_counter()

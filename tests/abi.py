@@ -27,7 +27,7 @@ class Config(C.Structure):
     _fields_ = [("num_topics", C.c_uint32), ("alpha", C.c_double), ("beta", C.c_double),
                 ("seed", C.c_uint64), ("tree_branch", C.c_uint32), ("init_mode", C.c_uint32),
                 ("device", C.c_int32), ("rank", C.c_uint32), ("world_size", C.c_uint32),
-                ("sampler", C.c_uint32)]
+                ("sampler", C.c_uint32), ("num_chunks", C.c_uint32), ("device_budget", C.c_uint64)]
 
 
 class IterationStats(C.Structure):
@@ -42,7 +42,7 @@ class Info(C.Structure):
                 ("alpha", C.c_double), ("beta", C.c_double), ("seed", C.c_uint64),
                 ("num_segments", C.c_uint32), ("num_units", C.c_uint32), ("doc_topic_nnz", C.c_uint64),
                 ("device_bytes", C.c_uint64), ("doc_major", C.c_uint32), ("padded_topics", C.c_uint32),
-                ("sampler_shape", C.c_uint32)]
+                ("sampler_shape", C.c_uint32), ("num_chunks", C.c_uint32), ("streaming", C.c_uint32)]
 
 
 class KernelTimes(C.Structure):
