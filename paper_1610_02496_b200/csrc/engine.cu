@@ -205,6 +205,7 @@ struct slda_engine {
     HostBuf chunk_nnz;      // per chunk: nnz of its C_dk after the last SSC (u64, pinned)
     uint64_t T_view = 0;
     uint32_t D_view = 0, view_begin = 0, view_end = 0;
+    uint32_t deep = 0;       // SLDA_DEEP (experiment)
     int sampler_shape = -1;  // SLDA_SAMPLER (sampler.cu launch_sampler); -1 = default by K
     bool serial = false;     // SLDA_SERIAL=1: SSC on the main stream (measurement of each kernel alone)
     uint32_t wshift = 0;  // word field shift of the execution-order key
@@ -446,6 +447,7 @@ struct slda_engine {
         a.tbits = tbits;
         a.row_entries = entries_counter();
         a.shape = sampler_shape;
+        a.deep = deep;
         a.vanilla = vanilla ? 1u : 0u;
         a.alpha = falpha;  // static_cast<float>(state.alpha), trainer.cpp:283
         return a;
@@ -585,6 +587,7 @@ void slda_engine::build_state(const slda_corpus_view& cv, const slda_config& c, 
                        " exceeds the packed C_dk count range at this K");
     }
     if (const char* f = std::getenv("SLDA_SAMPLER")) sampler_shape = slda::sampler_shape_from_name(f);
+    if (const char* f = std::getenv("SLDA_DEEP")) deep = static_cast<uint32_t>(std::atoi(f));
     if (const char* f = std::getenv("SLDA_SERIAL")) serial = std::string(f) == "1";
 
     phase("doc_start");
