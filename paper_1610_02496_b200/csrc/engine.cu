@@ -203,9 +203,28 @@ struct slda_engine {
     std::vector<ChunkImage> chunks;
     int resident = -1;      // chunk whose state is in the device buffers
     HostBuf chunk_nnz;      // per chunk: nnz of its C_dk after the last SSC (u64, pinned)
+    DevMem chunk_cnt;       // per chunk: the SSC's nnz counter on the device
+    unsigned long long* nnz_dst = nullptr;  // SSC nnz target (a chunk's counter while streaming)
+    // The second device window: the next chunk is uploaded into it on `copy` while the current
+    // one computes, then the windows swap (pointer swap) -- H2D, compute and D2H overlap.
+    static constexpr int kStateBufs = 13;
+    DevMem shadow[kStateBufs];
+    cudaStream_t copy = nullptr;
+    cudaEvent_t ev_in = nullptr, ev_done = nullptr, ev_copy_end = nullptr;
+    DevMem* state_buf(int j) {
+        DevMem* m[kStateBufs] = {&tok, &z, &doc_start, &row4, &A, &units, &long_docs, &ids, &input_of_slot,
+                                 &seg_word, &seg_off, &seg_len, &schedule};
+        return m[j];
+    }
+    static const HostBuf& image_buf(const ChunkImage& im, int j) {
+        const HostBuf* m[kStateBufs] = {&im.tok, &im.z, &im.doc_start, &im.row4, &im.A, &im.units, &im.long_docs,
+                                        &im.ids, &im.input_of_slot, &im.seg_word, &im.seg_off, &im.seg_len,
+                                        &im.schedule};
+        return *m[j];
+    }
+    void set_scalars(uint32_t ci);
     uint64_t T_view = 0;
     uint32_t D_view = 0, view_begin = 0, view_end = 0;
-    uint32_t deep = 0;       // SLDA_DEEP (experiment)
     int sampler_shape = -1;  // SLDA_SAMPLER (sampler.cu launch_sampler); -1 = default by K
     bool serial = false;     // SLDA_SERIAL=1: SSC on the main stream (measurement of each kernel alone)
     uint32_t wshift = 0;  // word field shift of the execution-order key
@@ -313,6 +332,11 @@ struct slda_engine {
             for (auto& e : set)
                 if (e) cudaEventDestroy(e);
         for (void* p : opened) cudaIpcCloseMemHandle(p);
+        if (copy) cudaStreamSynchronize(copy);
+        if (ev_in) cudaEventDestroy(ev_in);
+        if (ev_done) cudaEventDestroy(ev_done);
+        if (ev_copy_end) cudaEventDestroy(ev_copy_end);
+        if (copy) cudaStreamDestroy(copy);
         if (side) cudaStreamDestroy(side);
         if (stream) cudaStreamDestroy(stream);
     }
@@ -447,7 +471,6 @@ struct slda_engine {
         a.tbits = tbits;
         a.row_entries = entries_counter();
         a.shape = sampler_shape;
-        a.deep = deep;
         a.vanilla = vanilla ? 1u : 0u;
         a.alpha = falpha;  // static_cast<float>(state.alpha), trainer.cpp:283
         return a;
@@ -587,7 +610,6 @@ void slda_engine::build_state(const slda_corpus_view& cv, const slda_config& c, 
                        " exceeds the packed C_dk count range at this K");
     }
     if (const char* f = std::getenv("SLDA_SAMPLER")) sampler_shape = slda::sampler_shape_from_name(f);
-    if (const char* f = std::getenv("SLDA_DEEP")) deep = static_cast<uint32_t>(std::atoi(f));
     if (const char* f = std::getenv("SLDA_SERIAL")) serial = std::string(f) == "1";
 
     phase("doc_start");
@@ -864,6 +886,14 @@ void slda_engine::build_streaming(const slda_corpus_view& cv, const slda_config&
     DevMem* db[13] = {&tok, &z, &doc_start, &row4, &A, &units, &long_docs, &ids, &input_of_slot,
                       &seg_word, &seg_off, &seg_len, &schedule};
     for (int j = 0; j < 13; ++j) grow(*db[j], m[j]);
+    for (int j = 0; j < kStateBufs; ++j)
+        if (n > 1 && m[j]) shadow[j].alloc(m[j], &device_bytes);
+    chunk_cnt.alloc(8ull * n, &device_bytes);
+    CK(cudaMemcpyAsync(chunk_cnt.p, nnzs.data(), 8ull * n, cudaMemcpyHostToDevice, stream));
+    CK(cudaStreamCreateWithFlags(&copy, cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&ev_in, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&ev_done, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&ev_copy_end, cudaEventDisableTiming));
     uint64_t max_t = 0;
     uint32_t max_long = 0;
     for (const ChunkImage& im : chunks) {
@@ -919,24 +949,18 @@ void slda_engine::save_image(ChunkImage& im) {
 void slda_engine::swap_in(uint32_t ci) {
     if (resident == static_cast<int>(ci)) return;
     const ChunkImage& im = chunks[ci];
-    auto load = [&](DevMem& d, const HostBuf& h) {
-        if (!h.bytes) return;
+    for (int j = 0; j < kStateBufs; ++j) {
+        const HostBuf& h = image_buf(im, j);
+        if (!h.bytes) continue;
+        DevMem& d = *state_buf(j);
         if (d.bytes < h.bytes) d.alloc(h.bytes, &device_bytes);  // only if build_streaming's sizing was short
         CK(cudaMemcpyAsync(d.p, h.p, h.bytes, cudaMemcpyHostToDevice, stream));
-    };
-    load(tok, im.tok);
-    load(z, im.z);
-    load(doc_start, im.doc_start);
-    load(row4, im.row4);
-    load(A, im.A);
-    load(units, im.units);
-    load(long_docs, im.long_docs);
-    load(ids, im.ids);
-    load(input_of_slot, im.input_of_slot);
-    load(seg_word, im.seg_word);
-    load(seg_off, im.seg_off);
-    load(seg_len, im.seg_len);
-    load(schedule, im.schedule);
+    }
+    set_scalars(ci);
+}
+
+void slda_engine::set_scalars(uint32_t ci) {
+    const ChunkImage& im = chunks[ci];
     doc_begin = im.doc_begin;
     doc_end = im.doc_end;
     D = im.D;
@@ -957,7 +981,8 @@ void slda_engine::swap_out(uint32_t ci) {
     ChunkImage& im = chunks[ci];
     if (im.z.bytes) CK(cudaMemcpyAsync(im.z.p, z.p, im.z.bytes, cudaMemcpyDeviceToHost, stream));
     if (im.A.bytes) CK(cudaMemcpyAsync(im.A.p, A.p, im.A.bytes, cudaMemcpyDeviceToHost, stream));
-    CK(cudaMemcpyAsync(static_cast<uint64_t*>(chunk_nnz.p) + ci, nnz_counter(), 8, cudaMemcpyDeviceToHost, stream));
+    CK(cudaMemcpyAsync(static_cast<uint64_t*>(chunk_nnz.p) + ci, chunk_cnt.as<unsigned long long>() + ci, 8,
+                       cudaMemcpyDeviceToHost, stream));
 }
 
 uint64_t slda_engine::doc_topic_nnz_total() const {
@@ -968,7 +993,11 @@ uint64_t slda_engine::doc_topic_nnz_total() const {
 }
 
 // run_iteration over the chunks (trainer.cpp:425-432 with a file-backed store): reset C_wk,
-// then per chunk (the resident one first) H2D -> sampler -> SSC -> D2H, then one M-step.
+// then every chunk (the resident one first) through sampler + SSC, then one M-step.  Two device
+// windows pipeline the chunks: while chunk k computes on the engine stream, the copy stream
+// brings chunk k+1 into the other window (after writing chunk k-1's topics and C_dk rows back
+// from it); then the windows swap.  Each transfer is ordered by events, so H2D, compute and D2H
+// of neighbouring chunks overlap.
 void slda_engine::enqueue_streaming_iteration() {
     launches = 0;
     slot = iteration % kRing;
@@ -979,14 +1008,49 @@ void slda_engine::enqueue_streaming_iteration() {
     CK(cudaEventRecord(ev[1], stream));
     const uint32_t n = static_cast<uint32_t>(chunks.size());
     const uint32_t first = resident >= 0 ? static_cast<uint32_t>(resident) : 0u;
+    swap_in(first);  // no-op unless a getter left another chunk resident
+    auto order = [&](uint32_t k) { return (first + k) % n; };
+    auto upload = [&](uint32_t ci) {  // into the shadow window, on the copy stream
+        const ChunkImage& im = chunks[ci];
+        for (int j = 0; j < kStateBufs; ++j) {
+            const HostBuf& h = image_buf(im, j);
+            if (h.bytes) CK(cudaMemcpyAsync(shadow[j].p, h.p, h.bytes, cudaMemcpyHostToDevice, copy));
+        }
+        CK(cudaEventRecord(ev_in, copy));
+    };
+    auto download = [&](uint32_t ci, DevMem* zb, DevMem* ab, cudaStream_t st) {  // topics + C_dk rows back
+        ChunkImage& im = chunks[ci];
+        if (im.z.bytes) CK(cudaMemcpyAsync(im.z.p, zb->p, im.z.bytes, cudaMemcpyDeviceToHost, st));
+        if (im.A.bytes) CK(cudaMemcpyAsync(im.A.p, ab->p, im.A.bytes, cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(static_cast<uint64_t*>(chunk_nnz.p) + ci, chunk_cnt.as<unsigned long long>() + ci, 8,
+                           cudaMemcpyDeviceToHost, st));
+    };
+    CK(cudaStreamWaitEvent(copy, ev[1], 0));  // the previous iteration is done with both windows
+    if (n > 1) upload(order(1));
     for (uint32_t k = 0; k < n; ++k) {
-        const uint32_t ci = (first + k) % n;
-        swap_in(ci);
+        const uint32_t ci = order(k);
+        nnz_dst = chunk_cnt.as<unsigned long long>() + ci;
         CK(slda::launch_sampler(sampler_args(), n_units, stream));
         launches += n_units > 0;
         ssc(stream);
-        swap_out(ci);
+        nnz_dst = nullptr;
+        if (k + 1 == n) {
+            download(ci, &z, &A, stream);
+            break;
+        }
+        CK(cudaEventRecord(ev_done, stream));
+        CK(cudaStreamWaitEvent(stream, ev_in, 0));  // chunk k+1 has landed in the shadow window
+        for (int j = 0; j < kStateBufs; ++j) {
+            std::swap(state_buf(j)->p, shadow[j].p);
+            std::swap(state_buf(j)->bytes, shadow[j].bytes);
+        }
+        set_scalars(order(k + 1));
+        CK(cudaStreamWaitEvent(copy, ev_done, 0));  // chunk k's results are final
+        download(ci, &shadow[1], &shadow[4], copy);  // shadow now holds chunk k (z = 1, A = 4)
+        if (k + 2 < n) upload(order(k + 2));
     }
+    CK(cudaEventRecord(ev_copy_end, copy));
+    CK(cudaStreamWaitEvent(stream, ev_copy_end, 0));  // syncing the engine stream covers the copies
     CK(cudaEventRecord(ev[2], stream));
     CK(cudaEventRecord(ev[7], stream));
     m_step();
@@ -997,7 +1061,7 @@ void slda_engine::enqueue_streaming_iteration() {
 }
 
 void slda_engine::ssc(cudaStream_t st) {
-    CK(cudaMemsetAsync(nnz_counter(), 0, 8, st));
+    CK(cudaMemsetAsync(nnz_dst ? nnz_dst : nnz_counter(), 0, 8, st));
     slda::SscArgs s{};
     s.z = z.as<uint16_t>();
     s.doc_start = doc_start.as<uint32_t>();
@@ -1009,7 +1073,7 @@ void slda_engine::ssc(cudaStream_t st) {
     s.long_docs = long_docs.as<uint32_t>();
     s.n_long = n_long;
     s.hist_scratch = hist_scratch.as<uint32_t>();
-    s.nnz_total = nnz_counter();
+    s.nnz_total = nnz_dst ? nnz_dst : nnz_counter();
     CK(slda::launch_ssc(s, st));
     launches += (D > 0) + (n_long > 0);
 }

@@ -33,7 +33,6 @@ struct SamplerArgs {
     int shape;              // launch shape (sampler_shape_from_name); -1 = default by K
     uint32_t vanilla;       // SamplerKind::kVanilla: the O(K) dense-row draw (sampler.hpp:222-236)
     float alpha;            // f32(alpha), the vanilla draw's smoothing (trainer.cpp:283)
-    uint32_t deep;          // experiment (SLDA_DEEP=1): two row groups in flight per warp
 };
 
 // Sampler launch shapes (sampler.cu launch_sampler); -1 = by phi row size.

@@ -348,8 +348,7 @@ __global__ void __launch_bounds__(NT, MINB) sampler_quad_kernel(SamplerArgs a) {
 // make room in the 64-register budget (C3 K=10K: 95.5 -> 92.8 ms; C2: 19.8 -> 20.5 ms).
 // kGlobalPhi: the phi row does not fit shared memory (K >~ 45K): only L8 is staged and the
 // products gather phi through L1/L2.
-template <int NT, int MINB, int L, bool kC16 = false, bool kPrefetchNext = true, bool kGlobalPhi = false,
-          bool kDeep = false>
+template <int NT, int MINB, int L, bool kC16 = false, bool kPrefetchNext = true, bool kGlobalPhi = false>
 __global__ void __launch_bounds__(NT, MINB) sampler_quad_pf_kernel(SamplerArgs a) {
     constexpr uint32_t NW = NT / 32;
     constexpr uint32_t TPR = 32u / L;  // tokens per round (L lanes each, L sectors per group)
@@ -455,7 +454,7 @@ __global__ void __launch_bounds__(NT, MINB) sampler_quad_pf_kernel(SamplerArgs a
             auto fetch = [&](uint32_t g, Sector& dst) {
                 if (g < max_groups) {  // warp-uniform
                     dst = L * g + sub < nsect ? ldg_sector(row + 2 * (L * g + sub)) : zero_sector();
-                } else if (kPrefetchNext && (!kDeep || g == max_groups)) {
+                } else if (kPrefetchNext) {
                     const bool last = r + 1 == L || base + TPR * (r + 1) >= unit.length;
                     const uint32_t nrq = __shfl_sync(0xffffffffu, last ? tk_nx.x : tk.x, last ? t : ti + TPR);
                     if (last ? nb + t < unit.length : base + ti + TPR < unit.length)
@@ -464,20 +463,6 @@ __global__ void __launch_bounds__(NT, MINB) sampler_quad_pf_kernel(SamplerArgs a
             };
             if (max_groups == 0) {
                 fetch(0, c);
-            } else if (kDeep) {  // two groups in flight while one is consumed (three buffers)
-                Sector b1 = c, b2 = c;
-                fetch(1, b1);
-                for (uint32_t g = 0;; g += 3) {
-                    fetch(g + 2, b2);
-                    consume(c, g);
-                    if (g + 1 >= max_groups) { c = b1; break; }
-                    fetch(g + 3, c);
-                    consume(b1, g + 1);
-                    if (g + 2 >= max_groups) { c = b2; break; }
-                    fetch(g + 4, b1);
-                    consume(b2, g + 2);
-                    if (g + 3 >= max_groups) break;
-                }
             } else {
                 Sector n = c;
                 for (uint32_t g = 0;; g += 2) {
@@ -587,9 +572,7 @@ size_t sampler_quad_smem(const SamplerArgs& a, int nt) {
 
 template <int NT, int MINB, bool PF, bool C16>
 cudaError_t launch_quad_t1(const SamplerArgs& a, uint32_t n_units, cudaStream_t s) {
-    auto kern = PF ? (a.deep ? sampler_quad_pf_kernel<NT, MINB, 4, C16, true, false, true>
-                             : sampler_quad_pf_kernel<NT, MINB, 4, C16>)
-                   : sampler_quad_kernel<NT, MINB, 4, C16>;
+    auto kern = PF ? sampler_quad_pf_kernel<NT, MINB, 4, C16> : sampler_quad_kernel<NT, MINB, 4, C16>;
     const size_t smem = sampler_quad_smem(a, NT);
     if (const cudaError_t e = smem_optin(kern, smem); e != cudaSuccess) return e;
     kern<<<n_units, NT, smem, s>>>(a);
