@@ -225,6 +225,7 @@ struct slda_engine {
     void set_scalars(uint32_t ci);
     uint64_t T_view = 0;
     uint32_t D_view = 0, view_begin = 0, view_end = 0;
+    uint32_t nseg_view = 0;  // streaming: distinct words over all chunks (the merged layout's segments)
     int sampler_shape = -1;  // SLDA_SAMPLER (sampler.cu launch_sampler); -1 = default by K
     bool serial = false;     // SLDA_SERIAL=1: SSC on the main stream (measurement of each kernel alone)
     uint32_t wshift = 0;  // word field shift of the execution-order key
@@ -907,6 +908,15 @@ void slda_engine::build_streaming(const slda_corpus_view& cv, const slda_config&
     D_view = Dv;
     view_begin = b0;
     view_end = b1;
+    {
+        std::vector<uint32_t> words;
+        for (const ChunkImage& im : chunks) {
+            const uint32_t* w = static_cast<const uint32_t*>(im.seg_word.p);
+            words.insert(words.end(), w, w + im.nseg);
+        }
+        std::sort(words.begin(), words.end());
+        nseg_view = static_cast<uint32_t>(std::unique(words.begin(), words.end()) - words.begin());
+    }
     m_step();
     CK(cudaStreamSynchronize(stream));
     nnz = doc_topic_nnz_total();
@@ -1279,11 +1289,9 @@ int slda_get_info(const slda_engine* e, slda_info* info) {
         info->num_segments = e->nseg;
         info->num_units = e->n_units;
         if (e->streaming) {
-            info->num_segments = info->num_units = 0;
-            for (const ChunkImage& im : e->chunks) {
-                info->num_segments += im.nseg;
-                info->num_units += im.n_units;
-            }
+            info->num_segments = e->nseg_view;
+            info->num_units = 0;
+            for (const ChunkImage& im : e->chunks) info->num_units += im.n_units;
         }
         info->doc_topic_nnz = e->streaming ? e->doc_topic_nnz_total() : e->nnz;
         info->num_chunks = e->streaming ? static_cast<uint32_t>(e->chunks.size()) : 1u;
@@ -1570,54 +1578,134 @@ int slda_get_doc_topic(slda_engine* e, uint64_t* row_offsets, uint32_t* topics, 
     });
 }
 
+}  // extern "C"
+
+namespace {
+// The reference's single-chunk PDOW layout of the engine's resident shard (corpus.cpp:125-198).
+struct Layout {
+    std::vector<uint32_t> sorted_doc, sorted_word, shuffle_ptrs, doc_offsets, seg_word, seg_off, seg_len, schedule;
+    std::vector<uint64_t> token_ids;
+};
+
+Layout shard_layout(slda_engine* e) {
+    CK(cudaStreamSynchronize(e->stream));
+    const uint64_t T = e->T;
+    std::vector<uint2> tok(T);
+    std::vector<uint32_t> dst(static_cast<size_t>(e->D) + 1), sw(e->nseg), so(e->nseg), sl(e->nseg), sc(e->nseg);
+    std::vector<uint64_t> ids;
+    if (T) CK(cudaMemcpy(tok.data(), e->tok.p, T * 8, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(dst.data(), e->doc_start.p, dst.size() * 4, cudaMemcpyDeviceToHost));
+    if (e->nseg) {
+        CK(cudaMemcpy(sw.data(), e->seg_word.p, e->nseg * 4ull, cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(so.data(), e->seg_off.p, e->nseg * 4ull, cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(sl.data(), e->seg_len.p, e->nseg * 4ull, cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(sc.data(), e->schedule.p, e->nseg * 4ull, cudaMemcpyDeviceToHost));
+    }
+    if (e->have_ids) {
+        ids.resize(T);
+        CK(cudaMemcpy(ids.data(), e->ids.p, T * 8, cudaMemcpyDeviceToHost));
+    }
+    // Canonical chunk order (word, doc, token_id) from the execution order: within a word
+    // segment, sort by doc; slots are doc-grouped in corpus order, so sorting by slot gives
+    // (doc, token_id).
+    std::vector<uint32_t> slot(T), doc(T);
+    for (uint64_t i = 0; i < T; ++i) slot[i] = tok[i].y;
+    for (uint32_t s = 0; s < e->nseg; ++s) std::sort(slot.begin() + so[s], slot.begin() + so[s] + sl[s]);
+    for (uint64_t i = 0; i < T; ++i)
+        doc[i] = static_cast<uint32_t>(std::upper_bound(dst.begin(), dst.end(), slot[i]) - dst.begin() - 1);
+    Layout L;
+    L.sorted_doc.resize(T);
+    L.sorted_word.resize(T);
+    L.token_ids.resize(T);
+    L.shuffle_ptrs.resize(T);
+    // shuffle_ptrs: doc-grouped slot in word-major order per doc (corpus.cpp:190-195).
+    std::vector<uint32_t> cursor(dst.begin(), dst.end() - 1);
+    uint32_t seg = 0;
+    for (uint64_t i = 0; i < T; ++i) {
+        while (seg + 1 < e->nseg && so[seg + 1] <= i) ++seg;
+        L.sorted_doc[i] = doc[i] + e->doc_begin;
+        L.sorted_word[i] = sw[seg];
+        L.token_ids[i] = ids.empty() ? e->id_base + slot[i] : ids[slot[i]];
+        L.shuffle_ptrs[i] = cursor[doc[i]]++;
+    }
+    L.doc_offsets = std::move(dst);
+    L.seg_word = std::move(sw);
+    L.seg_off = std::move(so);
+    L.seg_len = std::move(sl);
+    L.schedule = std::move(sc);
+    return L;
+}
+
+// A streaming engine's layout as one chunk (what build_chunks(corpus, 1) gives): per word, the
+// chunks' segments in chunk order (their documents ascend), doc-grouped slots offset by the
+// tokens of the earlier chunks, and the schedule rebuilt over the merged segments
+// (corpus.cpp:200-210).
+Layout merged_layout(slda_engine* e) {
+    std::vector<Layout> parts;
+    for (uint32_t ci = 0; ci < e->chunks.size(); ++ci) {
+        e->swap_in(ci);
+        parts.push_back(shard_layout(e));
+    }
+    Layout L;
+    L.doc_offsets.push_back(0);
+    std::vector<uint64_t> base(parts.size() + 1, 0);
+    for (size_t c = 0; c < parts.size(); ++c) {
+        base[c + 1] = base[c] + parts[c].sorted_doc.size();
+        for (size_t d = 1; d < parts[c].doc_offsets.size(); ++d)
+            L.doc_offsets.push_back(static_cast<uint32_t>(base[c] + parts[c].doc_offsets[d]));
+    }
+    std::vector<size_t> next(parts.size(), 0);  // next segment of each chunk
+    for (;;) {
+        uint32_t w = 0xFFFFFFFFu;
+        for (size_t c = 0; c < parts.size(); ++c)
+            if (next[c] < parts[c].seg_word.size()) w = std::min(w, parts[c].seg_word[next[c]]);
+        if (w == 0xFFFFFFFFu) break;
+        L.seg_word.push_back(w);
+        L.seg_off.push_back(static_cast<uint32_t>(L.sorted_doc.size()));
+        for (size_t c = 0; c < parts.size(); ++c) {
+            const Layout& P = parts[c];
+            if (next[c] >= P.seg_word.size() || P.seg_word[next[c]] != w) continue;
+            const uint32_t o = P.seg_off[next[c]], n = P.seg_len[next[c]];
+            for (uint32_t i = o; i < o + n; ++i) {
+                L.sorted_doc.push_back(P.sorted_doc[i]);
+                L.sorted_word.push_back(P.sorted_word[i]);
+                L.token_ids.push_back(P.token_ids[i]);
+                L.shuffle_ptrs.push_back(static_cast<uint32_t>(base[c] + P.shuffle_ptrs[i]));
+            }
+            ++next[c];
+        }
+        L.seg_len.push_back(static_cast<uint32_t>(L.sorted_doc.size()) - L.seg_off.back());
+    }
+    L.schedule.resize(L.seg_word.size());
+    for (uint32_t i = 0; i < L.schedule.size(); ++i) L.schedule[i] = i;
+    std::stable_sort(L.schedule.begin(), L.schedule.end(), [&](uint32_t a, uint32_t b) {
+        return L.seg_len[a] != L.seg_len[b] ? L.seg_len[a] > L.seg_len[b] : L.seg_word[a] < L.seg_word[b];
+    });
+    return L;
+}
+}  // namespace
+
+extern "C" {
+
 int slda_get_pdow(slda_engine* e, uint32_t* sorted_doc, uint32_t* sorted_word, uint64_t* token_ids,
                   uint32_t* shuffle_ptrs, uint32_t* doc_offsets, uint32_t* seg_word,
                   uint32_t* seg_offset, uint32_t* seg_length, uint32_t* schedule) {
     return guarded([&] {
         if (!e) validation("null engine");
-        if (e->streaming) validation("the PDOW layout is per chunk in streaming mode (num_chunks > 1)");
         e->set_device();
-        CK(cudaStreamSynchronize(e->stream));
-        const uint64_t T = e->T;
-        std::vector<uint2> tok(T);
-        std::vector<uint32_t> dst(static_cast<size_t>(e->D) + 1), sw(e->nseg), so(e->nseg), sl(e->nseg),
-            sc(e->nseg);
-        std::vector<uint64_t> ids;
-        if (T) CK(cudaMemcpy(tok.data(), e->tok.p, T * 8, cudaMemcpyDeviceToHost));
-        CK(cudaMemcpy(dst.data(), e->doc_start.p, dst.size() * 4, cudaMemcpyDeviceToHost));
-        if (e->nseg) {
-            CK(cudaMemcpy(sw.data(), e->seg_word.p, e->nseg * 4ull, cudaMemcpyDeviceToHost));
-            CK(cudaMemcpy(so.data(), e->seg_off.p, e->nseg * 4ull, cudaMemcpyDeviceToHost));
-            CK(cudaMemcpy(sl.data(), e->seg_len.p, e->nseg * 4ull, cudaMemcpyDeviceToHost));
-            CK(cudaMemcpy(sc.data(), e->schedule.p, e->nseg * 4ull, cudaMemcpyDeviceToHost));
-        }
-        if (e->have_ids) {
-            ids.resize(T);
-            CK(cudaMemcpy(ids.data(), e->ids.p, T * 8, cudaMemcpyDeviceToHost));
-        }
-        // Canonical chunk order (word, doc, token_id) from the execution order: within a
-        // word segment, sort by doc; slots are doc-grouped in corpus order, so sorting by
-        // slot gives (doc, token_id).
-        std::vector<uint32_t> slot(T), doc(T);
-        for (uint64_t i = 0; i < T; ++i) slot[i] = tok[i].y;
-        for (uint32_t s = 0; s < e->nseg; ++s) std::sort(slot.begin() + so[s], slot.begin() + so[s] + sl[s]);
-        for (uint64_t i = 0; i < T; ++i)
-            doc[i] = static_cast<uint32_t>(std::upper_bound(dst.begin(), dst.end(), slot[i]) - dst.begin() - 1);
-        // shuffle_ptrs: doc-grouped slot in word-major order per doc (corpus.cpp:190-195).
-        std::vector<uint32_t> cursor(dst.begin(), dst.end() - 1);
-        uint32_t seg = 0;
-        for (uint64_t i = 0; i < T; ++i) {
-            while (seg + 1 < e->nseg && so[seg + 1] <= i) ++seg;
-            if (sorted_doc) sorted_doc[i] = doc[i] + e->doc_begin;
-            if (sorted_word) sorted_word[i] = sw[seg];
-            if (token_ids) token_ids[i] = ids.empty() ? e->id_base + slot[i] : ids[slot[i]];
-            if (shuffle_ptrs) shuffle_ptrs[i] = cursor[doc[i]]++;
-        }
-        if (doc_offsets) std::memcpy(doc_offsets, dst.data(), dst.size() * 4);
-        if (seg_word) std::memcpy(seg_word, sw.data(), sw.size() * 4);
-        if (seg_offset) std::memcpy(seg_offset, so.data(), so.size() * 4);
-        if (seg_length) std::memcpy(seg_length, sl.data(), sl.size() * 4);
-        if (schedule) std::memcpy(schedule, sc.data(), sc.size() * 4);
+        const Layout L = e->streaming ? merged_layout(e) : shard_layout(e);
+        auto put = [](auto* dst, const auto& v) {
+            if (dst && !v.empty()) std::memcpy(dst, v.data(), v.size() * sizeof(v[0]));
+        };
+        put(sorted_doc, L.sorted_doc);
+        put(sorted_word, L.sorted_word);
+        put(token_ids, L.token_ids);
+        put(shuffle_ptrs, L.shuffle_ptrs);
+        put(doc_offsets, L.doc_offsets);
+        put(seg_word, L.seg_word);
+        put(seg_offset, L.seg_off);
+        put(seg_length, L.seg_len);
+        put(schedule, L.schedule);
     });
 }
 

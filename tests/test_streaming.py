@@ -68,3 +68,17 @@ def test_streamed_heldout_ll_matches_resident():
     doc, word = np.arange(60, dtype=np.uint32).repeat(20), (np.arange(1200, dtype=np.uint32) * 7) % 1000
     held = s.Corpus.from_arrays(60, 1000, doc, word)
     assert s.heldout_ll(m, held, burn_in=5, workers=1, seed=3) == s.heldout_ll(ms, held, burn_in=5, workers=1, seed=3)
+
+
+@pytest.mark.parametrize("name,chunks", [("c1", 4), ("shuffled", 3), ("empty_docs", 5)])
+def test_streamed_layout_is_the_single_chunk_layout(name, chunks):
+    """chunk_layout() of a streaming engine merges its chunks into build_chunks(corpus, 1)'s
+    arrays -- the same the resident engine (itself checked against the reference) returns."""
+    spec = CASES[name]
+    m, _, _ = make_model(spec, iterations=0)
+    ms, _ = streamed(spec, chunks)
+    a, b = m.chunk_layout(), ms.chunk_layout()
+    for key in ("sorted_doc", "sorted_word", "token_ids", "shuffle_ptrs", "doc_offsets", "seg_word", "seg_offset",
+                "seg_length", "schedule"):
+        assert np.array_equal(np.asarray(a[key]), np.asarray(b[key])), key
+    assert ms.info()["num_segments"] == m.info()["num_segments"]
