@@ -123,7 +123,6 @@ typedef struct slda_info {
 #define SLDA_SHAPE_QUAD256 2u  /* quad-lane, 256-thread CTAs */
 #define SLDA_SHAPE_GLOBAL 3u   /* quad-lane, phi gathered from global memory (large K) */
 #define SLDA_SHAPE_VANILLA 4u  /* SamplerKind::kVanilla O(K) baseline */
-#define SLDA_SHAPE_PAIR512 5u  /* two tokens per 4-lane group, packed f32x2 chains, 512-thread CTAs */
 
 /* Per-kernel device times (ms) of the last iteration, for roofline accounting. */
 typedef struct slda_kernel_times {

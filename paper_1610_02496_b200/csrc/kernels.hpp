@@ -36,7 +36,7 @@ struct SamplerArgs {
 };
 
 // Sampler launch shapes (sampler.cu launch_sampler); -1 = by phi row size.
-enum { kShapeRound = 0, kShapeQuad512 = 1, kShapeQuad256 = 2, kShapeGlobal = 3, kShapeVanilla = 4, kShapePair512 = 5 };
+enum { kShapeRound = 0, kShapeQuad512 = 1, kShapeQuad256 = 2, kShapeGlobal = 3, kShapeVanilla = 4 };
 int sampler_shape_from_name(const char* name);
 // The kernel launch_sampler runs for these arguments (a.shape: forced shape or -1).
 int sampler_shape(const SamplerArgs& a);

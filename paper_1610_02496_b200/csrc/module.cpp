@@ -92,8 +92,8 @@ py::dict info_dict(const slda_info& i) {
     d["device_bytes"] = i.device_bytes;
     d["doc_major"] = i.doc_major;
     d["padded_topics"] = i.padded_topics;
-    static const char* kShapes[] = {"round", "quad512", "quad256", "global", "vanilla", "pair512"};
-    d["sampler_shape"] = i.sampler_shape < 6 ? kShapes[i.sampler_shape] : "unknown";
+    static const char* kShapes[] = {"round", "quad512", "quad256", "global", "vanilla"};
+    d["sampler_shape"] = i.sampler_shape < 5 ? kShapes[i.sampler_shape] : "unknown";
     d["num_chunks"] = i.num_chunks;
     d["streaming"] = i.streaming != 0;
     return d;

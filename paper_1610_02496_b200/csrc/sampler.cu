@@ -552,194 +552,6 @@ cudaError_t smem_optin(Kern kern, size_t bytes) {
                : cudaSuccess;
 }
 
-// ---- K3 pair kernel: two tokens per lane group, packed f32x2 chains ----------------------------
-// The quad-lane chain keeps one lane in four busy per FADD (lane j of a token's group adds its
-// sector's products in round j).  Here each 4-lane group carries TWO tokens (t and t + 8 of a
-// 16-token round) and both chains advance in one packed instruction: add.rn.f32x2 /
-// mul.rn.f32x2 (FADD2 / FMUL2 on sm_100a) round each component exactly as two scalar
-// __fadd_rn / __fmul_rn, so every running sum is still the reference's sequential f32 value
-// (make_branch_context, sampler.hpp:166-178).  Chain and product instructions per token halve;
-// the two tokens' lines are loaded together, so two lines per group are in flight.
-__device__ __forceinline__ unsigned long long pk2(float x, float y) {
-    unsigned long long r;
-    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(x), "f"(y));
-    return r;
-}
-__device__ __forceinline__ void up2(unsigned long long r, float& x, float& y) {
-    asm("mov.b64 {%0, %1}, %2;" : "=f"(x), "=f"(y) : "l"(r));
-}
-__device__ __forceinline__ unsigned long long fadd2(unsigned long long a, unsigned long long b) {
-    unsigned long long r;
-    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
-    return r;
-}
-__device__ __forceinline__ unsigned long long fmul2(unsigned long long a, unsigned long long b) {
-    unsigned long long r;
-    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
-    return r;
-}
-
-template <int NT, int MINB, bool kC16>
-__global__ void __launch_bounds__(NT, MINB) sampler_pair_kernel(SamplerArgs a) {
-    constexpr uint32_t NW = NT / 32;
-    constexpr uint32_t L = 4, TPR = 8;  // 4 lanes per group, 8 groups, 2 tokens per group
-    constexpr uint32_t kCk = 16, kCkStride = 17;
-    extern __shared__ __align__(16) float sm[];
-    __shared__ uint32_t s_next;
-    __shared__ float s_total, s_qv;
-    __shared__ __align__(8) unsigned long long s_bar;
-    const Unit unit = a.units[blockIdx.x];
-    const uint32_t v = unit.word;
-    const float* s_bhat = sm;
-    float* s_l8 = sm + a.K_pad;
-    float* s_ck = s_l8 + a.l8_stride;  // [NW][32 tokens][kCkStride]
-    tma_stage_rows(sm, a.bhat + static_cast<size_t>(v) * a.K_pad, a.K_pad * 4u, s_l8,
-                   a.l8 + static_cast<size_t>(v) * a.l8_stride, a.l8_stride * 4u, &s_bar);
-    const uint32_t tbits = kC16 ? 16u : a.tbits, tmask = kC16 ? 0xFFFFu : (1u << a.tbits) - 1u;
-    const uint4* A4 = reinterpret_cast<const uint4*>(a.A);
-    const uint32_t lane = lane_id(), t = lane / L, sub = lane % L, lead = lane & ~(L - 1u);
-    const uint32_t warp = threadIdx.x >> 5;
-    float* ckw = s_ck + warp * 32u * kCkStride;
-    uint32_t entries = 0;
-    if (threadIdx.x == 0) {
-        s_next = NW * 32u;
-        s_total = __ldg(a.l4 + static_cast<size_t>(v) * a.K_pad + a.K_pad - 1);
-        s_qv = __ldg(a.q + v);
-    }
-    __syncthreads();
-    uint32_t base = warp * 32u;
-    tma_wait_rows(&s_bar);
-    while (base < unit.length) {
-        const bool mine = base + lane < unit.length;
-        const uint2 tk = mine ? __ldg(a.tok + unit.offset + base + lane) : make_uint2(0u, 0u);
-        float S = 0.0f;
-        uint32_t my_ns = 0;
-#pragma unroll 1
-        for (uint32_t r = 0; r < 2; ++r) {  // 16 tokens per round: A = 16r + t, B = 16r + 8 + t
-            if (__all_sync(0xffffffffu, base + 16u * r >= unit.length)) break;
-            const uint32_t tiA = 16u * r + t, tiB = tiA + TPR;
-            const bool actA = base + tiA < unit.length, actB = base + tiB < unit.length;
-            const uint4* rowA = A4 + __shfl_sync(0xffffffffu, tk.x, tiA);
-            const uint4* rowB = A4 + __shfl_sync(0xffffffffu, tk.x, tiB);
-            Sector cA = actA ? ldg_sector(rowA + 2 * sub) : zero_sector();
-            Sector cB = actB ? ldg_sector(rowB + 2 * sub) : zero_sector();
-            const uint32_t hwA = __shfl_sync(0xffffffffu, cA.lo.x, lead), hwB = __shfl_sync(0xffffffffu, cB.lo.x, lead);
-            const uint32_t nnzA = actA ? (hwA & tmask) + 1u : 0u, nnzB = actB ? (hwB & tmask) + 1u : 0u;
-            const uint32_t nsA = actA ? (nnzA + 8u) >> 3 : 0u, nsB = actB ? (nnzB + 8u) >> 3 : 0u;
-            if (sub == 0) entries += nnzA + nnzB;
-            const uint32_t gA = (nsA + L - 1u) / L, gB = (nsB + L - 1u) / L;
-            const uint32_t max_groups = __reduce_max_sync(0xffffffffu, gA > gB ? gA : gB);
-            float* ckA = ckw + tiA * kCkStride;
-            float* ckB = ckw + tiB * kCkStride;
-            float runA = 0.0f, runB = 0.0f;
-#pragma unroll 1
-            for (uint32_t g = 0; g < max_groups; ++g) {
-                const uint32_t sec = L * g + sub;
-                if (g) {
-                    cA = sec < nsA ? ldg_sector(rowA + 2 * sec) : zero_sector();
-                    cB = sec < nsB ? ldg_sector(rowB + 2 * sec) : zero_sector();
-                }
-                unsigned long long p2[8];
-                {
-                    const uint32_t ea[8] = {cA.lo.x, cA.lo.y, cA.lo.z, cA.lo.w, cA.hi.x, cA.hi.y, cA.hi.z, cA.hi.w};
-                    const uint32_t eb[8] = {cB.lo.x, cB.lo.y, cB.lo.z, cB.lo.w, cB.hi.x, cB.hi.y, cB.hi.z, cB.hi.w};
-#pragma unroll
-                    for (int w = 0; w < 8; ++w)
-                        p2[w] = fmul2(pk2(__uint2float_rn(ea[w] >> tbits), __uint2float_rn(eb[w] >> tbits)),
-                                      pk2(s_bhat[ea[w] & tmask], s_bhat[eb[w] & tmask]));
-                }
-                const bool vA = sec < nsA, vB = sec < nsB;
-#pragma unroll
-                for (uint32_t j = 0; j < L; ++j) {
-                    unsigned long long r2 = pk2(runA, runB);
-#pragma unroll
-                    for (int w = 0; w < 8; ++w) r2 = fadd2(r2, p2[w]);
-                    float xA, xB;
-                    up2(r2, xA, xB);
-                    const bool mj = sub == j;
-                    runA = mj && vA ? xA : runA;
-                    runB = mj && vB ? xB : runB;
-                    if (mj && sec < kCk) {
-                        if (vA) ckA[sec] = runA;
-                        if (vB) ckB[sec] = runB;
-                    }
-                    runA = __shfl_sync(0xffffffffu, runA, lead | j);
-                    runB = __shfl_sync(0xffffffffu, runB, lead | j);
-                }
-            }
-            // Tokens 16r..16r+7 (A of group l - 16r) and 16r+8..16r+15 (B) to their lanes.
-            const uint32_t o = lane - 16u * r;
-            const float xA = __shfl_sync(0xffffffffu, runA, (o & 7u) * L);
-            const float xB = __shfl_sync(0xffffffffu, runB, (o & 7u) * L);
-            const uint32_t nA = __shfl_sync(0xffffffffu, nsA, (o & 7u) * L);
-            const uint32_t nB = __shfl_sync(0xffffffffu, nsB, (o & 7u) * L);
-            if (o < 16u) {
-                S = o < 8u ? xA : xB;
-                my_ns = o < 8u ? nA : nB;
-            }
-        }
-        __syncwarp();
-        if (mine) {  // sample_token (sampler.hpp:183-204), one token per lane
-            const float qv = s_qv, total = s_total;
-            const float* l4row = a.l4 + static_cast<size_t>(v) * a.K_pad;
-            float ub, up;
-            const uint64_t id = a.ids ? __ldg(a.ids + tk.y) : a.id_base + tk.y;
-            draw2_f32(a.seed, a.stream_kind, id, ub, up);
-            const uint4* row = A4 + tk.x;
-            uint32_t topic = 0;
-            if (ub < __fdiv_rn(S, __fadd_rn(S, qv))) {
-                const float xs = __fmul_rn(up, S);
-                if (xs == 0.0f) {
-                    topic = __ldg(reinterpret_cast<const uint32_t*>(row) + 1) & tmask;  // first real entry
-                } else {
-                    const float* ck = ckw + lane * kCkStride;
-                    const uint32_t stored = my_ns < kCk ? my_ns : kCk;
-                    uint32_t lo = 0, hi = stored;  // first checkpoint >= xs (or stored)
-                    while (lo < hi) {
-                        const uint32_t mid = (lo + hi) >> 1;
-                        if (ck[mid] >= xs) hi = mid; else lo = mid + 1;
-                    }
-                    float rr = lo > 0 ? ck[lo - 1] : 0.0f;
-                    for (uint32_t sc = lo; sc < my_ns; ++sc) {
-                        const Sector q = ldg_sector(row + 2 * sc);
-                        const uint32_t es[8] = {q.lo.x, q.lo.y, q.lo.z, q.lo.w, q.hi.x, q.hi.y, q.hi.z, q.hi.w};
-                        bool found = false;
-#pragma unroll
-                        for (int w = 0; w < 8; ++w) {
-                            rr = __fadd_rn(rr, entry_mass<false>(es[w], tbits, tmask, s_bhat));
-                            if (!found && rr >= xs) { topic = es[w] & tmask; found = true; }
-                        }
-                        if (found) break;
-                    }
-                }
-            } else {
-                float x = __fmul_rn(up, total);  // WaryTree::sample(p * total)
-                if (!(x <= total)) x = total;
-                const uint32_t k = tree_search(x, s_l8, a.n_l8, l4row);
-                topic = k < a.K ? k : a.K - 1;
-            }
-            a.z[tk.y] = static_cast<uint16_t>(topic);
-            atomicAdd(a.B + static_cast<size_t>(v) * a.K_pad + topic, 1u);
-        }
-        uint32_t nb = 0;
-        if (lane == 0) nb = atomicAdd(&s_next, 32u);
-        base = __shfl_sync(0xffffffffu, nb, 0);
-    }
-    if (a.row_entries) {
-        for (int o = 16; o > 0; o >>= 1) entries += __shfl_xor_sync(0xffffffffu, entries, o);
-        if (lane == 0) atomicAdd(a.row_entries, static_cast<unsigned long long>(entries));
-    }
-}
-
-template <bool C16>
-cudaError_t launch_pair_t(const SamplerArgs& a, uint32_t n_units, cudaStream_t s) {
-    auto kern = sampler_pair_kernel<512, 2, C16>;
-    const size_t smem = sizeof(float) * (static_cast<size_t>(a.K_pad) + a.l8_stride + 16u * 32u * 17u);
-    if (const cudaError_t e = smem_optin(kern, smem); e != cudaSuccess) return e;
-    kern<<<n_units, 512, smem, s>>>(a);
-    return cudaGetLastError();
-}
-
 size_t sampler_smem(const SamplerArgs& a, int nt, int g) {
     const size_t stage_row = 32u * static_cast<size_t>(g) + 16u;
     return sizeof(float) * (static_cast<size_t>(a.K_pad) + a.l8_stride) +
@@ -787,7 +599,7 @@ cudaError_t launch_quad_global(const SamplerArgs& a, uint32_t n_units, cudaStrea
 int sampler_shape_from_name(const char* name) {
     const std::string v(name ? name : "");
     return v == "round" ? kShapeRound : v == "quad512" ? kShapeQuad512 : v == "quad256" ? kShapeQuad256
-         : v == "global" ? kShapeGlobal : v == "pair512" ? kShapePair512 : -1;
+         : v == "global" ? kShapeGlobal : -1;
 }
 
 // ---- SamplerKind::kVanilla: the reference's O(K) baseline mode ---------------------------------
@@ -888,7 +700,6 @@ int sampler_shape(const SamplerArgs& a) {
     if (shape == kShapeQuad256 && sampler_quad_smem(a, 256) > kSm) shape = -1;
     if (shape == kShapeQuad512 && sampler_quad_smem(a, 512) > kSm) shape = -1;
     if (shape == kShapeRound && !round) shape = -1;
-    if (shape == kShapePair512 && !q512) shape = -1;
     if (shape < 0) shape = q256 ? kShapeQuad256 : q512 ? kShapeQuad512 : round ? kShapeRound : kShapeGlobal;
     return shape;
 }
@@ -899,7 +710,6 @@ cudaError_t launch_sampler(const SamplerArgs& a, uint32_t n_units, cudaStream_t 
         case kShapeVanilla: return launch_vanilla(a, n_units, s);
         case kShapeQuad256: return launch_quad_t<256, 4>(a, n_units, s);
         case kShapeQuad512: return launch_quad_t<512, 2>(a, n_units, s);
-        case kShapePair512: return a.tbits == 16 ? launch_pair_t<true>(a, n_units, s) : launch_pair_t<false>(a, n_units, s);
         case kShapeRound: return launch_round(a, n_units, s);
         default: return launch_quad_global(a, n_units, s);
     }
