@@ -357,15 +357,19 @@ def main() -> None:
 
     model = create()
     t_init = time.perf_counter()
+    it_wall = []
     for _ in range(args.steps):
+        t_it = time.perf_counter()
         model.run_iteration(tc)
+        it_wall.append(time.perf_counter() - t_it)
     t_iters = time.perf_counter()
     model.assignments(assign_out)
     torch.cuda.synchronize()
     e2e_s = max_over_ranks(time.perf_counter() - t0)
     if os.environ.get("SLDA_BENCH_E2E_TRACE"):
         print(f"e2e: init {t_init - t0:.3f} s, {args.steps} iterations {t_iters - t_init:.3f} s, "
-              f"assignments {time.perf_counter() - t_iters:.3f} s", file=sys.stderr)
+              f"assignments {time.perf_counter() - t_iters:.3f} s; per iteration (ms): "
+              + " ".join(f"{1e3 * w:.1f}" for w in it_wall), file=sys.stderr)
 
     # ---- device-timed: W warm-up iterations, then exactly K timed iterations.
     stream = torch.cuda.ExternalStream(model.stream_ptr())

