@@ -237,7 +237,7 @@ struct slda_engine {
     DevMem seg_word, seg_off, seg_len, schedule;  // PDOW getters
     DevMem input_of_slot, ids;                    // only for non doc-major input / explicit ids
     DevMem assign_buf;                            // gather_assignments staging (allocated on first use)
-    DevMem B, bhat, l4, l8, q, colsum, denom, zv, counters;
+    DevMem B, bhat, l8, q, colsum, denom, zv, counters;
 
     // Per-iteration phase events, a ring so async iterations can be profiled afterwards.
     static constexpr uint32_t kRing = 64;
@@ -430,7 +430,6 @@ struct slda_engine {
         const size_t cells = static_cast<size_t>(V_pad) * K_pad;
         B.alloc(cells * 4, &device_bytes);
         bhat.alloc(cells * 4, &device_bytes);
-        l4.alloc(cells * 4, &device_bytes);
         l8.alloc(static_cast<size_t>(V_pad) * l8_stride * 4, &device_bytes);
         q.alloc(static_cast<size_t>(V_pad) * 4, &device_bytes);
         colsum.alloc(static_cast<size_t>(K_pad) * 8, &device_bytes);
@@ -438,7 +437,6 @@ struct slda_engine {
         zv.alloc(static_cast<size_t>(K_pad) * 4, &device_bytes);
         counters.alloc(8 * (1 + kRing), &device_bytes);
         CK(cudaMemsetAsync(bhat.p, 0, bhat.bytes, stream));
-        CK(cudaMemsetAsync(l4.p, 0, l4.bytes, stream));
         CK(cudaMemsetAsync(l8.p, 0, l8.bytes, stream));
         CK(cudaMemsetAsync(q.p, 0, q.bytes, stream));
     }
@@ -464,7 +462,6 @@ struct slda_engine {
         a.units = units.as<slda::Unit>();
         a.A = A.as<uint32_t>();
         a.bhat = bhat.as<float>();
-        a.l4 = l4.as<float>();
         a.l8 = l8.as<float>();
         a.q = q.as<float>();
         a.ids = have_ids ? ids.as<uint64_t>() : nullptr;
@@ -1108,7 +1105,7 @@ void slda_engine::m_step() {
     CK(slda::launch_denom(colsum.as<unsigned long long>(), K, K_pad, V, beta, denom.as<double>(),
                           zv.as<float>(), stream));
     CK(cudaEventRecord(ev[4], stream));
-    CK(slda::launch_phi(B.as<uint32_t>(), denom.as<double>(), zv.as<float>(), bhat.as<float>(), l4.as<float>(),
+    CK(slda::launch_phi(B.as<uint32_t>(), denom.as<double>(), zv.as<float>(), bhat.as<float>(),
                         l8.as<float>(), q.as<float>(), 0, V_pad, K, K_pad, l8_stride, beta, falpha, stream));
     launches += 3;
     CK(cudaEventRecord(ev[5], stream));
@@ -1396,7 +1393,11 @@ int slda_get_word_topic_prob(slda_engine* e, float* out) {
 int slda_get_tree_prefix(slda_engine* e, float* out) {
     return guarded([&] {
         if (!e || !out) validation("null argument");
-        copy_matrix(e, e->l4, out);
+        // L4 is not kept (the sampler re-derives it from L8 and phi): materialise it here.
+        DevMem l4;
+        l4.alloc(e->bhat.bytes, nullptr);
+        CK(slda::launch_l4(e->bhat.as<float>(), e->V_pad, e->K_pad, l4.as<float>(), e->stream));
+        copy_matrix(e, l4, out);
     });
 }
 
@@ -1770,7 +1771,6 @@ int slda_heldout_ll(slda_engine* e, uint32_t num_docs, uint32_t vocab_size, uint
         a.evl_off = d_evl_off.as<uint64_t>();
         a.evl_word = d_evl.as<uint32_t>();
         a.bhat = e->bhat.as<float>();
-        a.l4 = e->l4.as<float>();
         a.l8 = e->l8.as<float>();
         a.q = e->q.as<float>();
         a.row_mass = d_mass.as<double>();

@@ -8,6 +8,7 @@
 // written out and summed on the host in the reference's order.
 #include "common.cuh"
 #include "heldout.hpp"
+#include "row_format.cuh"
 
 namespace slda {
 
@@ -111,20 +112,13 @@ __global__ void __launch_bounds__(256) heldout_kernel(HeldoutArgs a) {
                     }
                 }
             } else {
-                const float* l4row = a.l4 + static_cast<size_t>(v) * a.K_pad;
                 const float* l8row = a.l8 + static_cast<size_t>(v) * a.l8_stride;
-                const float total = __ldg(l4row + a.K_pad - 1);
+                const float total = __ldg(l8row + a.n_l8 - 1);  // L8's last entry is the row total
                 float x = __fmul_rn(up, total);
                 if (!(x <= total)) x = total;
-                // lower_bound over L4 (== WaryTree::sample): L8 level, then an 8-prefix leaf.
-                uint32_t lo = 0, hi = a.n_l8 - 1;  // last L8 entry == total >= x
-                while (lo < hi) {
-                    const uint32_t mid = (lo + hi) >> 1;
-                    if (__ldg(l8row + mid) >= x) hi = mid; else lo = mid + 1;
-                }
-                uint32_t below = 0;
-                for (uint32_t c = 0; c < kLeaf; ++c) below += __ldg(l4row + lo * kLeaf + c) < x;
-                topic = lo * kLeaf + below;
+                // lower_bound over L4 (== WaryTree::sample): the L8 level, then the block's 8
+                // prefixes continued from L8 over the phi row (row_format.cuh tree_search).
+                topic = tree_search<true>(x, l8row, a.n_l8, brow);
                 if (topic >= a.K) topic = a.K - 1;
             }
             keys[j] = topic;  // keys is free once the counts are built

@@ -12,7 +12,6 @@ struct HeldoutArgs {
     const uint64_t* evl_off;   // D+1, evaluation tokens (odd positions)
     const uint32_t* evl_word;
     const float* bhat;
-    const float* l4;
     const float* l8;
     const float* q;
     const double* row_mass;    // filled by launch_heldout

@@ -20,7 +20,6 @@ struct SamplerArgs {
     const Unit* units;      // heavy-first
     const uint32_t* A;      // C_dk rows: [nnz-1 | entries topic | count << tbits | zero pad to 8]
     const float* bhat;      // V_pad x K_pad
-    const float* l4;        // V_pad x K_pad (inclusive prefix, padded with the total)
     const float* l8;        // V_pad x l8_stride (L4 block maxima)
     const float* q;         // V_pad
     const uint64_t* ids;    // RNG element id per slot, or null -> id_base + slot
@@ -76,9 +75,11 @@ struct PeerSparse {
     uint32_t n;
 };
 cudaError_t launch_phi(const uint32_t* B, const double* denom, const float* zv, float* bhat,
-                       float* l4, float* l8, float* q, uint32_t row_begin, uint32_t row_end,
+                       float* l8, float* q, uint32_t row_begin, uint32_t row_end,
                        uint32_t K, uint32_t K_pad, uint32_t l8_stride, double beta, float falpha,
                        cudaStream_t s);
+// L4 (the inclusive f32 prefix of every phi row) materialised for the getter.
+cudaError_t launch_l4(const float* bhat, uint32_t rows, uint32_t K_pad, float* l4, cudaStream_t s);
 cudaError_t launch_peer_barrier(unsigned long long* counter, unsigned long long target, cudaStream_t s);
 cudaError_t launch_sparsify(const uint32_t* B, uint32_t row_lo, uint32_t row_hi, uint32_t K_pad, uint2* info,
                             uint32_t* entries, uint32_t* cursor, uint32_t cap, uint32_t* overflow, cudaStream_t s);

@@ -138,14 +138,14 @@ __device__ __forceinline__ void phi_cp16(void* smem, const void* gmem, bool vali
 
 template <int C, int S>
 constexpr size_t phi_smem_bytes() {
-    return static_cast<size_t>(S) * (2 * C * 8 + kPhiRows * C * 4 + C * 4) + kPhiRows * C * 4;
+    return static_cast<size_t>(S) * (2 * C * 8 + kPhiRows * C * 4 + C * 4);
 }
 
 template <int C, int S>
 __global__ void __launch_bounds__(kPhiRows, 4) phi_kernel(const uint32_t* __restrict__ B,
                                                          const double* __restrict__ denom,
                                                          const float* __restrict__ zv,
-                                                         float* __restrict__ bhat, float* __restrict__ l4,
+                                                         float* __restrict__ bhat,
                                                          float* __restrict__ l8, float* __restrict__ q,
                                                          uint32_t row_begin, uint32_t row_end,
                                                          uint32_t K_pad, uint32_t l8_stride, double beta,
@@ -154,11 +154,10 @@ __global__ void __launch_bounds__(kPhiRows, 4) phi_kernel(const uint32_t* __rest
     constexpr uint32_t Q = C / 4;              // quads per tile row
     constexpr uint32_t RP = kPhiRows / Q;      // rows per copy pass
     extern __shared__ __align__(16) unsigned char phi_smem[];
-    // [stage][2][C] denom, 1/denom | [stage][rows*C] counts, then bhat | L4 | [stage][C] zv
+    // [stage][2][C] denom, 1/denom | [stage][rows*C] counts, then bhat | [stage][C] zv
     auto s_den = reinterpret_cast<double(*)[2][C]>(phi_smem);
     auto t_in = reinterpret_cast<uint32_t(*)[kPhiRows * C]>(phi_smem + S * 2 * C * 8);
-    float* t_l4 = reinterpret_cast<float*>(phi_smem + S * (2 * C * 8 + kPhiRows * C * 4));
-    auto s_zv = reinterpret_cast<float(*)[C]>(t_l4 + kPhiRows * C);
+    auto s_zv = reinterpret_cast<float(*)[C]>(phi_smem + S * (2 * C * 8 + kPhiRows * C * 4));
     const double* __restrict__ rcp = denom + K_pad;
     const uint32_t tid = threadIdx.x;
     const uint32_t v0 = row_begin + blockIdx.x * kPhiRows;
@@ -194,7 +193,7 @@ __global__ void __launch_bounds__(kPhiRows, 4) phi_kernel(const uint32_t* __rest
         const int st = t % S;
         const uint32_t c0 = t * C;
         asm volatile("cp.async.wait_group %0;\n" ::"n"(S - 2) : "memory");
-        __syncthreads();  // tile t visible; tile t-1's stores have read its stage and t_l4
+        __syncthreads();  // tile t visible; tile t-1's stores have read its stage
         if (t + S - 1 < ntiles) issue(c0 + (S - 1) * C, (t + S - 1) % S);
         asm volatile("cp.async.commit_group;\n" ::: "memory");
         float l8v[Q / 2];
@@ -211,18 +210,15 @@ __global__ void __launch_bounds__(kPhiRows, 4) phi_kernel(const uint32_t* __rest
                 if (cnt.z) bh.z = phi_quotient(__dadd_rn(static_cast<double>(cnt.z), beta), d[2], r[2]);
                 if (cnt.w) bh.w = phi_quotient(__dadd_rn(static_cast<double>(cnt.w), beta), d[3], r[3]);
             }
-            float4 lv;
+            // The L4 prefix (sequential f32 chain, WaryTree::build) is not stored: only its value
+            // at every 8th column (L8) and the total.  The sampler re-derives a block's 8 prefixes
+            // from L8 and the phi row when it needs them (row_format.cuh tree_search).
             run = __fadd_rn(run, bh.x);
-            lv.x = run;
             run = __fadd_rn(run, bh.y);
-            lv.y = run;
             run = __fadd_rn(run, bh.z);
-            lv.z = run;
             run = __fadd_rn(run, bh.w);
-            lv.w = run;
             *reinterpret_cast<float4*>(&t_in[st][o]) = bh;
-            *reinterpret_cast<float4*>(&t_l4[o]) = lv;
-            if (j & 1u) l8v[j >> 1] = lv.w;  // L8: the prefix at every 8th column
+            if (j & 1u) l8v[j >> 1] = run;  // L8: the prefix at every 8th column
         }
         if (v < row_end) {
             const size_t o8 = static_cast<size_t>(v) * l8_stride + c0 / kLeaf;
@@ -245,10 +241,7 @@ __global__ void __launch_bounds__(kPhiRows, 4) phi_kernel(const uint32_t* __rest
             if (v0 + crow + RP * p < row_end && (C <= 32 || c0 + cq * 4u < K_pad)) {
                 const uint32_t o = phi_swz<C>(crow + RP * p, cq);
                 const float4 b = *reinterpret_cast<const float4*>(&t_in[st][o]);
-                const float4 l = *reinterpret_cast<const float4*>(&t_l4[o]);
-                const size_t go = g0 + p * stride + c0;
-                *reinterpret_cast<float4*>(bhat + go) = b;
-                *reinterpret_cast<float4*>(l4 + go) = l;
+                *reinterpret_cast<float4*>(bhat + g0 + p * stride + c0) = b;
             }
         }
     }
@@ -259,7 +252,7 @@ __global__ void __launch_bounds__(kPhiRows, 4) phi_kernel(const uint32_t* __rest
 }
 
 template <int C, int S>
-cudaError_t launch_phi_t(const uint32_t* B, const double* denom, const float* zv, float* bhat, float* l4,
+cudaError_t launch_phi_t(const uint32_t* B, const double* denom, const float* zv, float* bhat,
                          float* l8, float* q, uint32_t row_begin, uint32_t row_end, uint32_t K_pad,
                          uint32_t l8_stride, double beta, float falpha, cudaStream_t s) {
     constexpr size_t smem = phi_smem_bytes<C, S>();
@@ -269,13 +262,13 @@ cudaError_t launch_phi_t(const uint32_t* B, const double* denom, const float* zv
         e != cudaSuccess)
         return e;
     const uint32_t blocks = (row_end - row_begin + kPhiRows - 1) / kPhiRows;
-    phi_kernel<C, S><<<blocks, kPhiRows, smem, s>>>(B, denom, zv, bhat, l4, l8, q, row_begin, row_end, K_pad,
+    phi_kernel<C, S><<<blocks, kPhiRows, smem, s>>>(B, denom, zv, bhat, l8, q, row_begin, row_end, K_pad,
                                                     l8_stride, beta, falpha);
     return cudaGetLastError();
 }
 
 cudaError_t launch_phi(const uint32_t* B, const double* denom, const float* zv, float* bhat,
-                       float* l4, float* l8, float* q, uint32_t row_begin, uint32_t row_end,
+                       float* l8, float* q, uint32_t row_begin, uint32_t row_end,
                        uint32_t K, uint32_t K_pad, uint32_t l8_stride, double beta, float falpha,
                        cudaStream_t s) {
     (void)K;  // columns >= K are zero counts with zv = 0 (see above)
@@ -311,13 +304,37 @@ cudaError_t launch_phi(const uint32_t* B, const double* denom, const float* zv, 
         shape = fill3 > fill4 + 0.05 ? 2 : 0;
     }
     switch (shape) {
-        case 1: return launch_phi_t<16, 8>(B, denom, zv, bhat, l4, l8, q, row_begin, row_end, K_pad, l8_stride, beta, falpha, s);
-        case 2: return launch_phi_t<32, 3>(B, denom, zv, bhat, l4, l8, q, row_begin, row_end, K_pad, l8_stride, beta, falpha, s);
-        case 3: return launch_phi_t<64, 2>(B, denom, zv, bhat, l4, l8, q, row_begin, row_end, K_pad, l8_stride, beta, falpha, s);
-        case 4: return launch_phi_t<64, 3>(B, denom, zv, bhat, l4, l8, q, row_begin, row_end, K_pad, l8_stride, beta, falpha, s);
+        case 1: return launch_phi_t<16, 8>(B, denom, zv, bhat, l8, q, row_begin, row_end, K_pad, l8_stride, beta, falpha, s);
+        case 2: return launch_phi_t<32, 3>(B, denom, zv, bhat, l8, q, row_begin, row_end, K_pad, l8_stride, beta, falpha, s);
+        case 3: return launch_phi_t<64, 2>(B, denom, zv, bhat, l8, q, row_begin, row_end, K_pad, l8_stride, beta, falpha, s);
+        case 4: return launch_phi_t<64, 3>(B, denom, zv, bhat, l8, q, row_begin, row_end, K_pad, l8_stride, beta, falpha, s);
         default: break;
     }
-    return launch_phi_t<32, 4>(B, denom, zv, bhat, l4, l8, q, row_begin, row_end, K_pad, l8_stride, beta, falpha, s);
+    return launch_phi_t<32, 4>(B, denom, zv, bhat, l8, q, row_begin, row_end, K_pad, l8_stride, beta, falpha, s);
+}
+
+// The L4 level on demand (slda_get_tree_prefix): thread per row, the same sequential f32 chain
+// over the stored phi row as the phi kernel ran, so every value is the one WaryTree::build makes.
+__global__ void l4_kernel(const float* __restrict__ bhat, uint32_t rows, uint32_t K_pad, float* __restrict__ l4) {
+    const uint32_t v = blockIdx.x * blockDim.x + threadIdx.x;
+    if (v >= rows) return;
+    const float4* src = reinterpret_cast<const float4*>(bhat + static_cast<size_t>(v) * K_pad);
+    float4* dst = reinterpret_cast<float4*>(l4 + static_cast<size_t>(v) * K_pad);
+    float run = 0.0f;
+    for (uint32_t i = 0; i < K_pad / 4; ++i) {
+        const float4 b = __ldg(src + i);
+        float4 o;
+        o.x = run = __fadd_rn(run, b.x);
+        o.y = run = __fadd_rn(run, b.y);
+        o.z = run = __fadd_rn(run, b.z);
+        o.w = run = __fadd_rn(run, b.w);
+        dst[i] = o;
+    }
+}
+
+cudaError_t launch_l4(const float* bhat, uint32_t rows, uint32_t K_pad, float* l4, cudaStream_t s) {
+    if (rows) l4_kernel<<<(rows + 127) / 128, 128, 0, s>>>(bhat, rows, K_pad, l4);
+    return cudaGetLastError();
 }
 
 // ---- Peer-memory M-step exchange (world > 1; engine.cu m_step_peer) ---------------------------

@@ -46,20 +46,31 @@ __device__ __forceinline__ void prefetch_l2(const void* p) {
 __device__ __forceinline__ Sector zero_sector() { return Sector{make_uint4(0u, 0u, 0u, 0u), make_uint4(0u, 0u, 0u, 0u)}; }
 
 // lower_bound over the word's L4 prefix (== WaryTree::sample, acceptance.cpp:140-200):
-// binary search of the staged L8 level (first 8-block whose last prefix >= x), then one
-// 32-byte sector of L4.  Returns the first index with L4 >= x (x <= total).
-__device__ __forceinline__ uint32_t tree_search(float x, const float* s_l8, uint32_t n_l8, const float* l4row) {
+// binary search of the staged L8 level (first 8-block whose last prefix >= x), then the block's
+// 8 prefixes re-derived from the previous block's end: L4 is the sequential f32 chain
+// L4[c] = L4[c-1] + phi[c] (WaryTree::build) and L8[j-1] == L4[8j-1] exactly, so continuing the
+// chain over the phi row (shared memory, or global when it is too large to stage) gives the
+// very values the reference's tree holds -- no L4 array is stored or read.  Returns the first
+// index with L4 >= x (x <= total; L8[j] = L4[8j+7] >= x ends the scan).
+template <bool kGlobalPhi>
+__device__ __forceinline__ uint32_t tree_search(float x, const float* s_l8, uint32_t n_l8, const float* phi) {
     uint32_t lo = 0, hi = n_l8 - 1;  // s_l8[n_l8 - 1] == total >= x
     while (lo < hi) {
         const uint32_t mid = (lo + hi) >> 1;
         if (s_l8[mid] >= x) hi = mid; else lo = mid + 1;
     }
-    const Sector b = ldg_sector(reinterpret_cast<const uint4*>(l4row + lo * kLeaf));
-    const uint32_t below = (__uint_as_float(b.lo.x) < x) + (__uint_as_float(b.lo.y) < x) +
-                           (__uint_as_float(b.lo.z) < x) + (__uint_as_float(b.lo.w) < x) +
-                           (__uint_as_float(b.hi.x) < x) + (__uint_as_float(b.hi.y) < x) +
-                           (__uint_as_float(b.hi.z) < x) + (__uint_as_float(b.hi.w) < x);
-    return lo * kLeaf + below;
+    float run = lo ? s_l8[lo - 1] : 0.0f;
+    const float4* p4 = reinterpret_cast<const float4*>(phi + lo * kLeaf);
+    const float4 a = kGlobalPhi ? __ldg(p4) : p4[0];
+    const float4 b = kGlobalPhi ? __ldg(p4 + 1) : p4[1];
+    const float f[7] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z};
+    uint32_t i = 0;
+#pragma unroll
+    for (int k = 0; k < 7; ++k) {
+        run = __fadd_rn(run, f[k]);
+        i += run < x;  // non-decreasing: the count of prefixes below x is the first index >= x
+    }
+    return lo * kLeaf + i;
 }
 
 // Per-warp staging of C_dk rows.  Lane-private random row reads cap at ~1.5 TB/s on B200

@@ -32,8 +32,7 @@ __global__ void __launch_bounds__(NT, MINB) sampler_kernel(SamplerArgs a) {
     unsigned char* s_stage = reinterpret_cast<unsigned char*>(s_ck + kCkSectors * NT);
 
     const Unit unit = a.units[blockIdx.x];
-    const float* l4row = a.l4 + static_cast<size_t>(v) * a.K_pad;
-    const float total = __ldg(l4row + a.K_pad - 1);  // padded with the row total
+    const float total = __ldg(a.l8 + static_cast<size_t>(v) * a.l8_stride + a.n_l8 - 1);  // L8's last = the row total
     {
         const float4* gb = reinterpret_cast<const float4*>(a.bhat + static_cast<size_t>(v) * a.K_pad);
         float4* sb = reinterpret_cast<float4*>(sm);
@@ -146,7 +145,7 @@ __global__ void __launch_bounds__(NT, MINB) sampler_kernel(SamplerArgs a) {
                 // Word branch: WaryTree::sample(p * total) (sampler.hpp:100-106).
                 float x = __fmul_rn(up, total);
                 if (!(x <= total)) x = total;
-                const uint32_t k = tree_search(x, s_l8, a.n_l8, l4row);
+                const uint32_t k = tree_search<false>(x, s_l8, a.n_l8, s_bhat);
                 topic = k < a.K ? k : a.K - 1;
             }
         }
@@ -204,8 +203,7 @@ __global__ void __launch_bounds__(NT, MINB) sampler_quad_kernel(SamplerArgs a) {
     float* s_bhat = sm;
     float* s_l8 = sm + a.K_pad;
     float* s_ck = s_l8 + a.l8_stride;  // [NW][32 tokens][kCkStride]
-    const float* l4row = a.l4 + static_cast<size_t>(v) * a.K_pad;
-    const float total = __ldg(l4row + a.K_pad - 1);
+    const float total = __ldg(a.l8 + static_cast<size_t>(v) * a.l8_stride + a.n_l8 - 1);  // L8's last = the row total
     __shared__ __align__(8) unsigned long long s_bar;  // phi/L8 staging (TMA bulk copies)
     tma_stage_rows(sm, a.bhat + static_cast<size_t>(v) * a.K_pad, a.K_pad * 4u, s_l8,
                    a.l8 + static_cast<size_t>(v) * a.l8_stride, a.l8_stride * 4u, &s_bar);
@@ -327,7 +325,7 @@ __global__ void __launch_bounds__(NT, MINB) sampler_quad_kernel(SamplerArgs a) {
             } else {
                 float x = __fmul_rn(up, total);  // WaryTree::sample(p * total)
                 if (!(x <= total)) x = total;
-                const uint32_t k = tree_search(x, s_l8, a.n_l8, l4row);
+                const uint32_t k = tree_search<false>(x, s_l8, a.n_l8, s_bhat);
                 topic = k < a.K ? k : a.K - 1;
             }
             a.z[tk.y] = static_cast<uint16_t>(topic);
@@ -374,7 +372,7 @@ __global__ void __launch_bounds__(NT, MINB) sampler_quad_pf_kernel(SamplerArgs a
     uint32_t entries = 0;
     if (threadIdx.x == 0) {
         s_next = NW * 32u;
-        s_total = __ldg(a.l4 + static_cast<size_t>(v) * a.K_pad + a.K_pad - 1);  // padded with the total
+        s_total = __ldg(a.l8 + static_cast<size_t>(v) * a.l8_stride + a.n_l8 - 1);  // L8's last = the row total
         s_qv = __ldg(a.q + v);
     }
     __syncthreads();
@@ -487,7 +485,6 @@ __global__ void __launch_bounds__(NT, MINB) sampler_quad_pf_kernel(SamplerArgs a
         // sample_token (sampler.hpp:183-204), one token per lane.
         if (mine) {
             const float qv = s_qv, total = s_total;
-            const float* l4row = a.l4 + static_cast<size_t>(v) * a.K_pad;
             float ub, up;
             const uint64_t id = a.ids ? __ldg(a.ids + tk.y) : a.id_base + tk.y;
             draw2_f32(a.seed, a.stream_kind, id, ub, up);
@@ -522,7 +519,7 @@ __global__ void __launch_bounds__(NT, MINB) sampler_quad_pf_kernel(SamplerArgs a
             } else {
                 float x = __fmul_rn(up, total);  // WaryTree::sample(p * total)
                 if (!(x <= total)) x = total;
-                const uint32_t k = tree_search(x, s_l8, a.n_l8, l4row);
+                const uint32_t k = tree_search<kGlobalPhi>(x, s_l8, a.n_l8, s_bhat);
                 topic = k < a.K ? k : a.K - 1;
             }
             a.z[tk.y] = static_cast<uint16_t>(topic);
