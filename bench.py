@@ -120,11 +120,13 @@ def sampler_bytes(T: int, row_entries: int, K: int, units: int) -> int:
 
 
 def iteration_bytes(T: int, row_entries: int, K: int, V: int, D: int, nnz: int, units: int) -> int:
-    """Whole iteration: sampler + SSC + recount + phi/L4."""
+    """Whole iteration: sampler + SSC + recount + the M-step.  The M-step moves
+    C_wk in (4 V K) and phi + the L8 level out (4.5 V K): SURVEY's canonical phi + L4 write
+    (12 V K) counted an L4 array this engine no longer stores."""
     ssc = T * 6 + 4 * nnz + 8 * D
     recount = 2 * T + 4 * V * K
-    phi = 12 * V * K
-    return sampler_bytes(T, row_entries, K, units) + ssc + recount + phi
+    mstep = 4 * V * K + (9 * V * K) // 2
+    return sampler_bytes(T, row_entries, K, units) + ssc + recount + mstep
 
 
 def ncu_traffic():
