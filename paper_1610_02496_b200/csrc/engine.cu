@@ -163,7 +163,6 @@ struct HostBuf {
 // build_state() produced for its document range, and the scalars that describe it.
 struct ChunkImage {
     uint32_t doc_begin = 0, doc_end = 0, D = 0, nseg = 0, n_units = 0, n_long = 0, tbits = 1, wshift = 0;
-    uint32_t compact_max = 0;
     uint64_t T = 0, id_base = 0, out_offset = 0;
     bool doc_major = true, have_ids = false;
     std::vector<uint64_t> view_pos;  // gathered chunks: position in the engine's view per chunk token
@@ -197,7 +196,6 @@ struct slda_engine {
     bool have_ids = false;  // per-slot RNG element ids (non doc-major input or explicit ids)
     bool vanilla = false;  // SamplerKind::kVanilla (trainer.cpp:281-285)
     uint32_t tbits0 = 1;   // minimal C_dk topic field for K (configure)
-    uint32_t compact_max = 0;  // documents of at most this many tokens have compact C_dk rows
     // Streaming mode (slda_config.num_chunks > 1 and the corpus state over device_budget): the
     // shard's documents in chunks whose state lives in pinned host memory and passes through
     // the device buffers above one chunk at a time.  T_view / D_view: the whole engine view.
@@ -618,15 +616,6 @@ void slda_engine::build_state(const slda_corpus_view& cv, const slda_config& c, 
                        " exceeds the packed C_dk count range at this K");
     }
     if (const char* f = std::getenv("SLDA_SAMPLER")) sampler_shape = slda::sampler_shape_from_name(f);
-    {
-        // Compact rows (u16 topic + u8 count per entry, kernels.hpp) where the quad-lane sampler
-        // reads them: counts in the high half-word layout (tbits 16), the sparse trainer, and a
-        // quad-lane launch shape.  SLDA_ROW_FORMAT=wide keeps every row wide.
-        const char* rf = std::getenv("SLDA_ROW_FORMAT");
-        const int shape = slda::sampler_shape(sampler_args());
-        const bool quad = shape == slda::kShapeQuad256 || shape == slda::kShapeQuad512 || shape == slda::kShapeGlobal;
-        compact_max = tbits == 16 && !vanilla && quad && !(rf && std::string(rf) == "wide") ? slda::kCompactMaxLen : 0u;
-    }
     if (const char* f = std::getenv("SLDA_SERIAL")) serial = std::string(f) == "1";
 
     phase("doc_start");
@@ -664,7 +653,7 @@ void slda_engine::build_state(const slda_corpus_view& cv, const slda_config& c, 
         DevMem quads;
         quads.alloc((static_cast<size_t>(D) + 1) * 4, nullptr);
         CK(cudaMemsetAsync(quads.p, 0, quads.bytes, stream));
-        CK(slda::launch_row_quads(doc_start.as<uint32_t>(), D, compact_max, quads.as<uint32_t>(), stream));
+        CK(slda::launch_row_quads(doc_start.as<uint32_t>(), D, quads.as<uint32_t>(), stream));
         exclusive_sum(quads.as<uint32_t>(), row4.as<uint32_t>(), static_cast<uint64_t>(D) + 1);
         const uint32_t total_quads = D ? d2h_scalar(row4.as<uint32_t>() + D) : 0;
         A.alloc(static_cast<size_t>(total_quads) * 16 + 512, &device_bytes);  // speculative group reads
@@ -705,8 +694,7 @@ void slda_engine::build_state(const slda_corpus_view& cv, const slda_config& c, 
         flags.alloc(T * 4, nullptr);
         seg_index.alloc(T * 4, nullptr);
         CK(slda::launch_make_tok(keys_sorted.as<unsigned long long>(), slots_sorted.as<uint32_t>(),
-                                 row4.as<uint32_t>(), counts.as<uint32_t>(), compact_max, T, kl, tok.as<uint2>(),
-                                 flags.as<uint32_t>(), stream));
+                                 row4.as<uint32_t>(), T, kl, tok.as<uint2>(), flags.as<uint32_t>(), stream));
         exclusive_sum(flags.as<uint32_t>(), seg_index.as<uint32_t>(), T);
         nseg = T ? d2h_scalar(seg_index.as<uint32_t>() + T - 1) + d2h_scalar(flags.as<uint32_t>() + T - 1) : 0;
         seg_word.alloc(static_cast<size_t>(nseg) * 4, &device_bytes);
@@ -949,7 +937,6 @@ void slda_engine::save_image(ChunkImage& im) {
     im.n_units = n_units;
     im.n_long = n_long;
     im.tbits = tbits;
-    im.compact_max = compact_max;
     im.wshift = wshift;
     im.doc_major = doc_major;
     im.have_ids = have_ids;
@@ -998,7 +985,6 @@ void slda_engine::set_scalars(uint32_t ci) {
     n_units = im.n_units;
     n_long = im.n_long;
     tbits = im.tbits;
-    compact_max = im.compact_max;
     wshift = im.wshift;
     doc_major = im.doc_major;
     have_ids = im.have_ids;
@@ -1098,7 +1084,6 @@ void slda_engine::ssc(cudaStream_t st) {
     s.row4 = row4.as<uint32_t>();
     s.A = A.as<uint32_t>();
     s.tbits = tbits;
-    s.compact_max = compact_max;
     s.K_pad = K_pad;
     s.long_docs = long_docs.as<uint32_t>();
     s.n_long = n_long;
@@ -1513,26 +1498,16 @@ namespace {
 // C_dk rows copied to the host; empty documents have none.
 struct HostRows {
     std::vector<uint32_t> doc_start, row4, A;
-    uint32_t mask = 0, tbits = 0, compact_max = 0;
+    uint32_t mask = 0, tbits = 0;
     const uint32_t* row(uint32_t d) const { return A.data() + static_cast<size_t>(row4[d]) * 4; }
-    bool compact(uint32_t d) const { return doc_start[d + 1] - doc_start[d] <= compact_max; }
     uint32_t nnz(uint32_t d) const {
         if (doc_start[d + 1] == doc_start[d]) return 0u;
-        if (compact(d)) return reinterpret_cast<const uint16_t*>(row(d))[0] + 1u;
         return (row(d)[0] & mask) + 1u;
     }
-    // Decoded (topic, count) pairs in ascending topic order (entry 0 is the header).
+    // Decoded (topic, count) pairs in ascending topic order.
     template <class F>
     void for_each(uint32_t d, F&& f) const {
         const uint32_t n = nnz(d);
-        if (compact(d)) {  // 96-byte blocks: 32 u16 topics, then 32 u8 counts (kernels.hpp)
-            const unsigned char* r = reinterpret_cast<const unsigned char*>(row(d));
-            for (uint32_t i = 1; i <= n; ++i) {
-                const unsigned char* b = r + 96 * (i >> 5);
-                f(static_cast<uint32_t>(reinterpret_cast<const uint16_t*>(b)[i & 31u]), static_cast<uint32_t>(b[64 + (i & 31u)]));
-            }
-            return;
-        }
         const uint32_t* r = row(d);
         for (uint32_t i = 0; i < n; ++i) f(r[1 + i] & mask, r[1 + i] >> tbits);
     }
@@ -1542,7 +1517,6 @@ HostRows fetch_rows(slda_engine* e) {
     HostRows h;
     h.mask = (1u << e->tbits) - 1u;
     h.tbits = e->tbits;
-    h.compact_max = e->compact_max;
     h.doc_start.resize(static_cast<size_t>(e->D) + 1);
     h.row4.resize(static_cast<size_t>(e->D) + 1);
     h.A.resize(e->A.bytes / 4);
@@ -1558,7 +1532,6 @@ HostRows image_rows(const ChunkImage& im) {
     HostRows h;
     h.mask = (1u << im.tbits) - 1u;
     h.tbits = im.tbits;
-    h.compact_max = im.compact_max;
     const uint32_t* ds = static_cast<const uint32_t*>(im.doc_start.p);
     const uint32_t* r4 = static_cast<const uint32_t*>(im.row4.p);
     const uint32_t* a = static_cast<const uint32_t*>(im.A.p);

@@ -13,11 +13,6 @@ struct Unit {
 };
 
 constexpr uint32_t kUnitMaxTokens = 8192;  // sampler: max tokens per unit (one CTA)
-// Compact C_dk rows (documents of at most kCompactMaxLen tokens, when enabled): 32-entry blocks
-// of 96 bytes -- 32 u16 topics, then 32 u8 counts -- instead of 32 u32 entries (128 bytes).  The
-// token record's row offset (uint4 units) carries the format in its top bit.
-constexpr uint32_t kCompactMaxLen = 255;
-constexpr uint32_t kCompactRow = 0x80000000u;
 constexpr uint32_t kSscWarpCap = 512;      // SSC: docs up to this length take the warp path
 
 struct SamplerArgs {
@@ -54,7 +49,6 @@ struct SscArgs {
     const uint32_t* row4;       // per doc: row offset in uint4 units
     uint32_t* A;
     uint32_t tbits, K_pad;
-    uint32_t compact_max;       // documents of at most this many tokens get compact rows (0: none)
     const uint32_t* long_docs;  // docs longer than kSscWarpCap
     uint32_t n_long;
     uint32_t* hist_scratch;     // n_long_ctas x K_pad (global fallback for large K)
@@ -110,10 +104,8 @@ struct KeyLayout {
 cudaError_t launch_make_keys(const uint32_t* word, const uint32_t* doc_local, const uint32_t* input_of_slot,
                              const uint32_t* doc_len, uint64_t T, KeyLayout kl, unsigned long long* keys,
                              uint32_t* vals, cudaStream_t s);
-// doc_len (per shard document) and compact_max (0: no compact rows) set the token's format bit.
 cudaError_t launch_make_tok(const unsigned long long* keys, const uint32_t* slots, const uint32_t* row4,
-                            const uint32_t* doc_len, uint32_t compact_max, uint64_t T, KeyLayout kl, uint2* tok,
-                            uint32_t* seg_flag, cudaStream_t s);
+                            uint64_t T, KeyLayout kl, uint2* tok, uint32_t* seg_flag, cudaStream_t s);
 cudaError_t launch_emit_segments(const unsigned long long* keys, const uint32_t* seg_flag,
                                  const uint32_t* seg_index, uint64_t T, uint32_t wshift,
                                  uint32_t* seg_word, uint32_t* seg_off, cudaStream_t s);
@@ -125,7 +117,7 @@ cudaError_t launch_emit_units(const uint32_t* schedule, const uint32_t* seg_word
                               const uint32_t* seg_off, const uint32_t* seg_len,
                               const uint32_t* unit_start, uint32_t nseg, Unit* units,
                               cudaStream_t s);
-cudaError_t launch_row_quads(const uint32_t* doc_start, uint32_t D, uint32_t compact_max, uint32_t* quads,
+cudaError_t launch_row_quads(const uint32_t* doc_start, uint32_t D, uint32_t* quads,
                              cudaStream_t s);
 cudaError_t launch_long_flags(const uint32_t* doc_start, uint32_t D, uint32_t* flags,
                               cudaStream_t s);

@@ -45,34 +45,6 @@ __device__ __forceinline__ void prefetch_l2(const void* p) {
 
 __device__ __forceinline__ Sector zero_sector() { return Sector{make_uint4(0u, 0u, 0u, 0u), make_uint4(0u, 0u, 0u, 0u)}; }
 
-// Piece `sec` (8 entries) of the C_dk row at `rq` (uint4 units, kCompactRow bit = format) as eight
-// u32 entries topic | count << 16 -- the wide format of an engine with tbits == 16, which is the
-// only one compact rows coexist with.  Wide row: one 32-byte sector.  Compact row: the piece's
-// 16 bytes of u16 topics and 8 bytes of u8 counts in its 96-byte block, widened by byte permutes.
-__device__ __forceinline__ Sector load_piece(const uint4* A4, uint32_t rq, uint32_t sec) {
-    if (!(rq & kCompactRow)) return ldg_sector(A4 + rq + 2 * sec);
-    const unsigned char* b = reinterpret_cast<const unsigned char*>(A4 + (rq & ~kCompactRow)) + 96u * (sec >> 2);
-    uint4 t;
-    uint2 c;
-    asm("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
-        : "=r"(t.x), "=r"(t.y), "=r"(t.z), "=r"(t.w) : "l"(b + 16u * (sec & 3u)));
-    asm("ld.global.nc.L1::no_allocate.v2.u32 {%0,%1}, [%2];" : "=r"(c.x), "=r"(c.y) : "l"(b + 64u + 8u * (sec & 3u)));
-    const uint32_t ce0 = c.x & 0x00FF00FFu, co0 = (c.x >> 8) & 0x00FF00FFu;  // counts 0,2 | 1,3
-    const uint32_t ce1 = c.y & 0x00FF00FFu, co1 = (c.y >> 8) & 0x00FF00FFu;  // counts 4,6 | 5,7
-    Sector s;
-    s.lo = make_uint4(__byte_perm(t.x, ce0, 0x5410), __byte_perm(t.x, co0, 0x5432), __byte_perm(t.y, ce0, 0x7610),
-                      __byte_perm(t.y, co0, 0x7632));
-    s.hi = make_uint4(__byte_perm(t.z, ce1, 0x5410), __byte_perm(t.z, co1, 0x5432), __byte_perm(t.w, ce1, 0x7610),
-                      __byte_perm(t.w, co1, 0x7632));
-    return s;
-}
-
-// The topic of a row's first real entry (entry 1), either format.
-__device__ __forceinline__ uint32_t first_topic(const uint4* A4, uint32_t rq, uint32_t tmask) {
-    if (rq & kCompactRow) return __ldg(reinterpret_cast<const uint16_t*>(A4 + (rq & ~kCompactRow)) + 1);
-    return __ldg(reinterpret_cast<const uint32_t*>(A4 + rq) + 1) & tmask;
-}
-
 // lower_bound over the word's L4 prefix (== WaryTree::sample, acceptance.cpp:140-200):
 // binary search of the staged L8 level (first 8-block whose last prefix >= x), then the block's
 // 8 prefixes re-derived from the previous block's end: L4 is the sequential f32 chain

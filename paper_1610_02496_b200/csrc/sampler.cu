@@ -234,9 +234,9 @@ __global__ void __launch_bounds__(NT, MINB) sampler_quad_kernel(SamplerArgs a) {
             const uint32_t ti = TPR * r + t;  // this lane group's token within the batch
             if (__all_sync(0xffffffffu, base + TPR * r >= unit.length)) break;
             const bool act = base + ti < unit.length;
-            const uint32_t rq = __shfl_sync(0xffffffffu, tk.x, ti);  // row offset | format bit
+            const uint4* row = A4 + __shfl_sync(0xffffffffu, tk.x, ti);
             Sector c = zero_sector();
-            if (act) c = load_piece(A4, rq, sub);
+            if (act) c = ldg_sector(row + 2 * sub);
             const uint32_t hw = __shfl_sync(0xffffffffu, c.lo.x, lead);  // header: word 0 of sector 0
             // [nnz-1 | entries | pad to 8]
             const uint32_t nnz = act ? (hw & tmask) + 1u : 0u;
@@ -273,10 +273,10 @@ __global__ void __launch_bounds__(NT, MINB) sampler_quad_kernel(SamplerArgs a) {
             };
             for (uint32_t g = 0; g < max_groups; g += 2) {  // two groups per trip: no register copies
                 Sector n = c;
-                n = L * (g + 1) + sub < nsect ? load_piece(A4, rq, L * (g + 1) + sub) : zero_sector();
+                n = L * (g + 1) + sub < nsect ? ldg_sector(row + 2 * (L * (g + 1) + sub)) : zero_sector();
                 consume(c, g);
                 if (g + 1 >= max_groups) break;
-                c = L * (g + 2) + sub < nsect ? load_piece(A4, rq, L * (g + 2) + sub) : zero_sector();
+                c = L * (g + 2) + sub < nsect ? ldg_sector(row + 2 * (L * (g + 2) + sub)) : zero_sector();
                 consume(n, g + 1);
             }
             // Token ti's S and sector count to its owning lane (lane ti).
@@ -294,11 +294,13 @@ __global__ void __launch_bounds__(NT, MINB) sampler_quad_kernel(SamplerArgs a) {
             float ub, up;
             const uint64_t id = a.ids ? __ldg(a.ids + tk.y) : a.id_base + tk.y;
             draw2_f32(a.seed, a.stream_kind, id, ub, up);
+            const uint4* row = A4 + tk.x;
             uint32_t topic = 0;
             if (ub < __fdiv_rn(S, __fadd_rn(S, qv))) {
                 const float xs = __fmul_rn(up, S);
                 if (xs == 0.0f) {
-                    topic = first_topic(A4, tk.x, tmask);  // first real entry
+                    const uint32_t e1 = __ldg(reinterpret_cast<const uint32_t*>(row) + 1);  // first real entry
+                    topic = e1 & tmask;
                 } else {
                     const float* ck = ckw + lane * kCkStride;
                     const uint32_t stored = my_ns < kCk ? my_ns : kCk;
@@ -309,7 +311,7 @@ __global__ void __launch_bounds__(NT, MINB) sampler_quad_kernel(SamplerArgs a) {
                     }
                     float r = lo > 0 ? ck[lo - 1] : 0.0f;
                     for (uint32_t sc = lo; sc < my_ns; ++sc) {  // one sector unless past the checkpoints
-                        const Sector q = load_piece(A4, tk.x, sc);
+                        const Sector q = ldg_sector(row + 2 * sc);
                         const uint32_t es[8] = {q.lo.x, q.lo.y, q.lo.z, q.lo.w, q.hi.x, q.hi.y, q.hi.z, q.hi.w};
                         bool found = false;
 #pragma unroll
@@ -387,7 +389,7 @@ __global__ void __launch_bounds__(NT, MINB) sampler_quad_pf_kernel(SamplerArgs a
     Sector c = zero_sector();
     if (kPrefetchNext) {
         const uint32_t rq0 = __shfl_sync(0xffffffffu, tk.x, t);
-        if (base + t < unit.length) c = load_piece(A4, rq0, sub);
+        if (base + t < unit.length) c = ldg_sector(A4 + rq0 + 2 * sub);
     }
     tma_wait_rows(&s_bar);  // phi + L8 landed (the first lines are already in flight)
     while (base < unit.length) {
@@ -406,10 +408,10 @@ __global__ void __launch_bounds__(NT, MINB) sampler_quad_pf_kernel(SamplerArgs a
             const uint32_t ti = TPR * r + t;  // this lane group's token within the batch
             if (__all_sync(0xffffffffu, base + TPR * r >= unit.length)) break;
             const bool act = base + ti < unit.length;
-            const uint32_t rq = __shfl_sync(0xffffffffu, tk.x, ti);  // row offset | format bit
+            const uint4* row = A4 + __shfl_sync(0xffffffffu, tk.x, ti);
             if (!kPrefetchNext) {  // this round's first line, loaded now
                 c = zero_sector();
-                if (act) c = load_piece(A4, rq, sub);
+                if (act) c = ldg_sector(row + 2 * sub);
             }
             const uint32_t hw = __shfl_sync(0xffffffffu, c.lo.x, lead);  // header: word 0 of sector 0
             // [nnz-1 | entries | pad to 8]
@@ -449,12 +451,12 @@ __global__ void __launch_bounds__(NT, MINB) sampler_quad_pf_kernel(SamplerArgs a
             // groups per trip so no registers are copied.
             auto fetch = [&](uint32_t g, Sector& dst) {
                 if (g < max_groups) {  // warp-uniform
-                    dst = L * g + sub < nsect ? load_piece(A4, rq, L * g + sub) : zero_sector();
+                    dst = L * g + sub < nsect ? ldg_sector(row + 2 * (L * g + sub)) : zero_sector();
                 } else if (kPrefetchNext) {
                     const bool last = r + 1 == L || base + TPR * (r + 1) >= unit.length;
                     const uint32_t nrq = __shfl_sync(0xffffffffu, last ? tk_nx.x : tk.x, last ? t : ti + TPR);
                     if (last ? nb + t < unit.length : base + ti + TPR < unit.length)
-                        dst = load_piece(A4, nrq, sub);
+                        dst = ldg_sector(A4 + nrq + 2 * sub);
                 }
             };
             if (max_groups == 0) {
@@ -486,11 +488,13 @@ __global__ void __launch_bounds__(NT, MINB) sampler_quad_pf_kernel(SamplerArgs a
             float ub, up;
             const uint64_t id = a.ids ? __ldg(a.ids + tk.y) : a.id_base + tk.y;
             draw2_f32(a.seed, a.stream_kind, id, ub, up);
+            const uint4* row = A4 + tk.x;
             uint32_t topic = 0;
             if (ub < __fdiv_rn(S, __fadd_rn(S, qv))) {
                 const float xs = __fmul_rn(up, S);
                 if (xs == 0.0f) {
-                    topic = first_topic(A4, tk.x, tmask);  // first real entry
+                    const uint32_t e1 = __ldg(reinterpret_cast<const uint32_t*>(row) + 1);  // first real entry
+                    topic = e1 & tmask;
                 } else {
                     const float* ck = ckw + lane * kCkStride;
                     const uint32_t stored = my_ns < kCk ? my_ns : kCk;
@@ -501,7 +505,7 @@ __global__ void __launch_bounds__(NT, MINB) sampler_quad_pf_kernel(SamplerArgs a
                     }
                     float r = lo > 0 ? ck[lo - 1] : 0.0f;
                     for (uint32_t sc = lo; sc < my_ns; ++sc) {  // one sector unless past the checkpoints
-                        const Sector q = load_piece(A4, tk.x, sc);
+                        const Sector q = ldg_sector(row + 2 * sc);
                         const uint32_t es[8] = {q.lo.x, q.lo.y, q.lo.z, q.lo.w, q.hi.x, q.hi.y, q.hi.z, q.hi.w};
                         bool found = false;
 #pragma unroll

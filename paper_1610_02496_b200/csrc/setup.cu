@@ -110,24 +110,21 @@ cudaError_t launch_make_keys(const uint32_t* word, const uint32_t* doc_local, co
 
 // tok = {C_dk row offset (quads), slot}; flags mark word-segment starts.
 __global__ void make_tok_kernel(const unsigned long long* keys, const uint32_t* slots, const uint32_t* row4,
-                                const uint32_t* doc_len, uint32_t compact_max, uint64_t T, KeyLayout kl, uint2* tok,
-                                uint32_t* seg_flag) {
+                                uint64_t T, KeyLayout kl, uint2* tok, uint32_t* seg_flag) {
     const unsigned long long dmask = (1ull << kl.dbits) - 1ull;
     const uint32_t ws = kl.dbits + kl.lbits;
     for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < T;
          i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
         const unsigned long long k = keys[i];
-        const uint32_t d = static_cast<uint32_t>(k & dmask);
-        tok[i] = make_uint2(row4[d] | (doc_len[d] <= compact_max ? kCompactRow : 0u), slots[i]);
+        tok[i] = make_uint2(row4[k & dmask], slots[i]);
         seg_flag[i] = (i == 0 || (keys[i - 1] >> ws) != (k >> ws)) ? 1u : 0u;
     }
 }
 
 cudaError_t launch_make_tok(const unsigned long long* keys, const uint32_t* slots, const uint32_t* row4,
-                            const uint32_t* doc_len, uint32_t compact_max, uint64_t T, KeyLayout kl, uint2* tok,
-                            uint32_t* seg_flag, cudaStream_t s) {
+                            uint64_t T, KeyLayout kl, uint2* tok, uint32_t* seg_flag, cudaStream_t s) {
     if (T == 0) return cudaSuccess;
-    make_tok_kernel<<<grid_for(T, 256), 256, 0, s>>>(keys, slots, row4, doc_len, compact_max, T, kl, tok, seg_flag);
+    make_tok_kernel<<<grid_for(T, 256), 256, 0, s>>>(keys, slots, row4, T, kl, tok, seg_flag);
     return cudaGetLastError();
 }
 
@@ -205,25 +202,18 @@ cudaError_t launch_emit_units(const uint32_t* schedule, const uint32_t* seg_word
 
 // C_dk row capacity in uint4 units: header + nnz_d entries with nnz_d <= len_d
 // (test_counts.cpp:149-150), rounded up to 32 entries (one 128-byte line).
-__global__ void row_quads_kernel(const uint32_t* doc_start, uint32_t D, uint32_t compact_max, uint32_t* quads) {
+__global__ void row_quads_kernel(const uint32_t* doc_start, uint32_t D, uint32_t* quads) {
     const uint32_t d = blockIdx.x * blockDim.x + threadIdx.x;
     if (d >= D) return;
-    const uint32_t len = doc_start[d + 1] - doc_start[d];
-    const uint32_t pieces = (len + 8u) >> 3;  // 8-entry pieces for the header + <= len entries
-    if (len <= compact_max) {
-        // Compact: 96-byte blocks of 4 pieces (6 uint4 each); rows stay 32-byte aligned.
-        quads[d] = 6u * ((pieces + 3u) >> 2);
-    } else {
-        // Rounded up to a whole 128-byte line (a row's 4-sector group is one L1 line when all
-        // rows are wide: scripts/mb_pattern.cu, a third fewer L1TEX wavefronts per byte).
-        quads[d] = ((pieces << 1) + 7u) & ~7u;
-    }
+    // Rounded up to a whole 128-byte line: every row starts line-aligned, so each 4-sector
+    // group the sampler loads is exactly one L1 line (scripts/mb_pattern.cu: a third fewer
+    // L1TEX wavefronts per loaded byte than 32-byte-aligned rows).
+    quads[d] = ((((doc_start[d + 1] - doc_start[d] + 8u) >> 3) << 1) + 7u) & ~7u;
 }
 
-cudaError_t launch_row_quads(const uint32_t* doc_start, uint32_t D, uint32_t compact_max, uint32_t* quads,
-                             cudaStream_t s) {
+cudaError_t launch_row_quads(const uint32_t* doc_start, uint32_t D, uint32_t* quads, cudaStream_t s) {
     if (D == 0) return cudaSuccess;
-    row_quads_kernel<<<(D + 255) / 256, 256, 0, s>>>(doc_start, D, compact_max, quads);
+    row_quads_kernel<<<(D + 255) / 256, 256, 0, s>>>(doc_start, D, quads);
     return cudaGetLastError();
 }
 

@@ -74,8 +74,7 @@ __device__ __forceinline__ void ssc_load_keys(const uint16_t* z, uint32_t n, uin
 // the rest are re-read from z (L1) by a runtime loop, so one code body serves every length
 // (several length-specialised bodies overflow the instruction cache: ncu no_instruction stalls).
 __device__ __forceinline__ uint32_t ssc_doc(const uint32_t* key, const uint16_t* z, uint32_t n, uint32_t lane,
-                                            const SscWarpSmem& w, uint32_t cq, uint32_t* out_row, uint32_t tbits,
-                                            bool compact) {
+                                            const SscWarpSmem& w, uint32_t cq, uint32_t* out_row, uint32_t tbits) {
     auto set_bit = [&](uint32_t k) { atomicOr(w.bm + (k >> 5), 1u << (k & 31u)); };
     auto count = [&](uint32_t k) {
         const uint32_t wi = k >> 5;
@@ -132,34 +131,16 @@ __device__ __forceinline__ uint32_t ssc_doc(const uint32_t* key, const uint16_t*
     for (uint32_t i = 128 + lane; i < n; i += 32) count(__ldg(z + i));
     __syncwarp();
     // Emit the row; the map is cleared once per distinct topic (nnz stores, not len).
-    const uint32_t padded = (nnz + 8u) & ~7u;
-    if (compact) {  // 96-byte blocks: 32 u16 topics, then 32 u8 counts (kernels.hpp kCompactMaxLen)
-        unsigned char* rb = reinterpret_cast<unsigned char*>(out_row);
-        auto put = [&](uint32_t i, uint32_t t, uint32_t k) {
-            unsigned char* b = rb + 96u * (i >> 5);
-            reinterpret_cast<uint16_t*>(b)[i & 31u] = static_cast<uint16_t>(t);
-            b[64u + (i & 31u)] = static_cast<unsigned char>(k);
-        };
 #pragma unroll 1
-        for (uint32_t e = lane; e < nnz; e += 32) {
-            const uint32_t k = w.cnt[e], t = w.top[e];
-            w.cnt[e] = 0u;
-            w.bm[t >> 5] = 0u;
-            put(1 + e, t, k);
-        }
-        if (nnz + 1 + lane < padded) put(nnz + 1 + lane, 0u, 0u);  // < 8 pad entries
-        if (lane == 0) put(0u, nnz - 1u, 0u);                      // header: count 0 adds +0
-    } else {
-#pragma unroll 1
-        for (uint32_t e = lane; e < nnz; e += 32) {
-            const uint32_t k = w.cnt[e], t = w.top[e];
-            w.cnt[e] = 0u;
-            w.bm[t >> 5] = 0u;
-            out_row[1 + e] = t | (k << tbits);
-        }
-        if (nnz + 1 + lane < padded) out_row[nnz + 1 + lane] = 0u;  // < 8 pad words
-        if (lane == 0) out_row[0] = nnz - 1u;
+    for (uint32_t e = lane; e < nnz; e += 32) {
+        const uint32_t k = w.cnt[e], t = w.top[e];
+        w.cnt[e] = 0u;
+        w.bm[t >> 5] = 0u;
+        out_row[1 + e] = t | (k << tbits);
     }
+    const uint32_t padded = (nnz + 8u) & ~7u;
+    if (nnz + 1 + lane < padded) out_row[nnz + 1 + lane] = 0u;  // < 8 pad words
+    if (lane == 0) out_row[0] = nnz - 1u;
     __syncwarp();
     return nnz;
 }
@@ -209,7 +190,7 @@ __global__ void __launch_bounds__(kSscWarps * 32, 8) ssc_warp_kernel(SscArgs a) 
         ssc_load_keys<4>(a.z + s0, n <= kSscWarpCap ? n : 0u, lane, key);
         if (cn > kSscWarpCap || cn == 0) continue;  // ssc_long_kernel / empty document
         const uint32_t ck[4] = {k0, k1, k2, k3};
-        const uint32_t nnz = ssc_doc(ck, a.z + cs0, cn, lane, w, cq, row, a.tbits, cn <= a.compact_max);
+        const uint32_t nnz = ssc_doc(ck, a.z + cs0, cn, lane, w, cq, row, a.tbits);
         nnz_acc += nnz;
     }
     if (lane == 0 && nnz_acc) atomicAdd(a.nnz_total, nnz_acc);
