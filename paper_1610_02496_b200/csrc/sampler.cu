@@ -706,13 +706,7 @@ cudaError_t launch_sampler(const SamplerArgs& a, uint32_t n_units, cudaStream_t 
     switch (sampler_shape(a)) {
         case kShapeVanilla: return launch_vanilla(a, n_units, s);
         case kShapeQuad256: return launch_quad_t<256, 4>(a, n_units, s);
-        case kShapeQuad512: {
-            const char* e = std::getenv("SLDA_QUAD_NT");  // experiment: CTA size of the 2-per-SM quad kernel
-            const int nt = e ? std::atoi(e) : 512;
-            if (nt == 640) return launch_quad_t<640, 2, true>(a, n_units, s);
-            if (nt == 576) return launch_quad_t<576, 2, true>(a, n_units, s);
-            return launch_quad_t<512, 2>(a, n_units, s);
-        }
+        case kShapeQuad512: return launch_quad_t<512, 2>(a, n_units, s);
         case kShapeRound: return launch_round(a, n_units, s);
         default: return launch_quad_global(a, n_units, s);
     }
