@@ -1101,7 +1101,12 @@ void slda_engine::m_step() {
     if (peer) exchange();
     CK(cudaEventRecord(ev[8], stream));
     CK(cudaMemsetAsync(colsum.p, 0, colsum.bytes, stream));
-    CK(slda::launch_colsum(B.as<uint32_t>(), 0, V_pad, K_pad, colsum.as<unsigned long long>(), stream));
+    // C_k: the topic histogram when this engine's z holds every token C_wk counts (one resident
+    // shard: 2 B/token instead of 4 B/cell), else the column sums of the (exchanged) C_wk.
+    if (!peer && !streaming && T > 0 && z.p && slda::zhist_fits(K_pad))
+        CK(slda::launch_zhist(z.as<uint16_t>(), T, K_pad, colsum.as<unsigned long long>(), stream));
+    else
+        CK(slda::launch_colsum(B.as<uint32_t>(), 0, V_pad, K_pad, colsum.as<unsigned long long>(), stream));
     CK(slda::launch_denom(colsum.as<unsigned long long>(), K, K_pad, V, beta, denom.as<double>(),
                           zv.as<float>(), stream));
     CK(cudaEventRecord(ev[4], stream));

@@ -59,6 +59,10 @@ cudaError_t launch_ssc(const SscArgs& a, cudaStream_t s);
 
 cudaError_t launch_colsum(const uint32_t* B, uint32_t row_begin, uint32_t row_end, uint32_t K_pad,
                           unsigned long long* colsum, cudaStream_t s);
+// C_k as the histogram of the topics (engines holding all of C_wk's tokens); zhist_fits:
+// the K_pad bins fit shared memory.
+bool zhist_fits(uint32_t K_pad);
+cudaError_t launch_zhist(const uint16_t* z, uint64_t T, uint32_t K_pad, unsigned long long* colsum, cudaStream_t s);
 // denom: 2*K_pad doubles -- denom_k, then RN(1/denom_k) (read by the phi kernel).
 cudaError_t launch_denom(const unsigned long long* colsum, uint32_t K, uint32_t K_pad, uint32_t V,
                          double beta, double* denom, float* zv, cudaStream_t s);

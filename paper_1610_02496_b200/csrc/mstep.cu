@@ -62,6 +62,52 @@ cudaError_t launch_colsum(const uint32_t* B, uint32_t row_begin, uint32_t row_en
     return cudaGetLastError();
 }
 
+// C_k from the topics themselves (one engine holding every token of C_wk): C_k is the number of
+// tokens assigned topic k, so a histogram of z (2 B/token, 1.48 GB at C3) gives exactly the
+// column sums of C_wk (4 B/cell, 5.64 GB).  Per-CTA shared-memory bins, flushed once.
+__global__ void __launch_bounds__(512) zhist_kernel(const uint16_t* __restrict__ z, uint64_t T, uint32_t K_pad,
+                                                    unsigned long long* __restrict__ colsum) {
+    extern __shared__ uint32_t s_bin[];
+    for (uint32_t i = threadIdx.x; i < K_pad; i += blockDim.x) s_bin[i] = 0u;
+    __syncthreads();
+    const uint64_t n8 = T / 8, stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+    const uint4* z8 = reinterpret_cast<const uint4*>(z);
+    for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n8; i += stride) {
+        const uint4 v = __ldg(z8 + i);
+        const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            atomicAdd(s_bin + (w[j] & 0xFFFFu), 1u);
+            atomicAdd(s_bin + (w[j] >> 16), 1u);
+        }
+    }
+    for (uint64_t i = n8 * 8 + blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < T; i += stride)
+        atomicAdd(s_bin + z[i], 1u);
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < K_pad; i += blockDim.x)
+        if (s_bin[i]) atomicAdd(colsum + i, static_cast<unsigned long long>(s_bin[i]));
+}
+
+bool zhist_fits(uint32_t K_pad) { return static_cast<size_t>(K_pad) * 4 <= 200 * 1024; }
+
+cudaError_t launch_zhist(const uint16_t* z, uint64_t T, uint32_t K_pad, unsigned long long* colsum, cudaStream_t s) {
+    const size_t smem = static_cast<size_t>(K_pad) * 4;
+    if (!zhist_fits(K_pad)) return cudaErrorInvalidValue;
+    if (const cudaError_t e = cudaFuncSetAttribute(zhist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                   static_cast<int>(smem));
+        e != cudaSuccess)
+        return e;
+    int dev = 0, sms = 0, per_sm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, zhist_kernel, 512, smem);
+    const uint64_t want = (T / 8 + 511) / 512;
+    uint64_t grid = static_cast<uint64_t>(sms) * (per_sm > 0 ? per_sm : 1);
+    if (want < grid) grid = want ? want : 1;
+    zhist_kernel<<<static_cast<uint32_t>(grid), 512, smem, s>>>(z, T, K_pad, colsum);
+    return cudaGetLastError();
+}
+
 // bhat = f32((cnt + beta) / denom_k) with the double quotient correctly rounded
 // (counts.cpp:58-60), without a per-cell double division.  y = RN(x * RN(1/denom)) is within
 // 2.5 double ulps of RN(x / denom), so both round to the same f32 unless an f32 rounding
