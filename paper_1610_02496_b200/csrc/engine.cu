@@ -196,6 +196,11 @@ struct slda_engine {
     bool have_ids = false;  // per-slot RNG element ids (non doc-major input or explicit ids)
     bool vanilla = false;  // SamplerKind::kVanilla (trainer.cpp:281-285)
     uint32_t tbits0 = 1;   // minimal C_dk topic field for K (configure)
+    // One resident shard zeroes C_wk right after the phi kernel, inside the wait for the
+    // side-stream SSC, instead of at the start of the next iteration (reset_word_topic off the
+    // critical path); C_wk is then recounted from z when a caller asks for it.
+    bool b_zeroed = false;
+    bool early_reset() const { return !peer && !streaming && T > 0; }
     // Streaming mode (slda_config.num_chunks > 1 and the corpus state over device_budget): the
     // shard's documents in chunks whose state lives in pinned host memory and passes through
     // the device buffers above one chunk at a time.  T_view / D_view: the whole engine view.
@@ -519,6 +524,10 @@ void slda_engine::build(const slda_corpus_view& cv, const slda_config& c) {
         alloc_exchange();
     } else {
         m_step();
+        if (early_reset()) {
+            CK(cudaMemsetAsync(B.p, 0, B.bytes, stream));
+            b_zeroed = true;
+        }
     }
     CK(cudaStreamSynchronize(stream));
     nnz = d2h_scalar(nnz_counter());
@@ -1164,7 +1173,8 @@ void slda_engine::enqueue_iteration() {
     slot = iteration % kRing;
     ev = ring[slot];
     CK(cudaEventRecord(ev[0], stream));
-    CK(cudaMemsetAsync(B.p, 0, B.bytes, stream));  // reset_word_topic (counts.cpp:134-138)
+    if (!b_zeroed) CK(cudaMemsetAsync(B.p, 0, B.bytes, stream));  // reset_word_topic (counts.cpp:134-138)
+    b_zeroed = false;
     CK(cudaMemsetAsync(entries_counter(), 0, 8, stream));
     CK(cudaEventRecord(ev[1], stream));
     const slda::SamplerArgs a = sampler_args();
@@ -1179,6 +1189,10 @@ void slda_engine::enqueue_iteration() {
     ssc(ssc_stream);
     CK(cudaEventRecord(ev[7], ssc_stream));
     m_step();
+    if (early_reset()) {  // the next iteration's reset_word_topic, overlapped with SSC's tail
+        CK(cudaMemsetAsync(B.p, 0, B.bytes, stream));
+        b_zeroed = true;
+    }
     CK(cudaStreamWaitEvent(stream, ev[7], 0));
     CK(cudaEventRecord(ev[6], stream));
     ring_launches[slot] = launches;
@@ -1384,7 +1398,19 @@ int slda_get_word_topic(slda_engine* e, uint32_t* out) {
         if (!e || !out) validation("null argument");
         e->set_device();
         // With world > 1 every rank's B holds the full reduced C_wk after the exchange.
-        copy_matrix(e, e->B, out);
+        if (!e->b_zeroed) {
+            copy_matrix(e, e->B, out);
+            return;
+        }
+        // C_wk was zeroed for the next iteration: count_chunk_into (trainer.cpp:223-235) again
+        // from the current topics, into a temporary.
+        DevMem c;
+        c.alloc(e->B.bytes, nullptr);
+        CK(cudaMemsetAsync(c.p, 0, c.bytes, e->stream));
+        slda::RecountDraw rd{e->seed, e->id_base, e->have_ids ? e->ids.as<uint64_t>() : nullptr, 0u};
+        CK(slda::launch_recount(e->tok.as<uint2>(), e->units.as<slda::Unit>(), e->n_units, e->z.as<uint16_t>(),
+                                c.as<uint32_t>(), e->K_pad, rd, e->stream));
+        copy_matrix(e, c, out);
     });
 }
 
