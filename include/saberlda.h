@@ -53,7 +53,7 @@ typedef struct slda_engine slda_engine;
 typedef struct slda_corpus_view {
     uint32_t num_docs;        /* D of the whole corpus */
     uint32_t vocab_size;      /* V */
-    uint64_t num_tokens;      /* T of this view (< 2^32 per engine) */
+    uint64_t num_tokens;      /* T of this view (< 2^32 unless streaming: then < 2^32 per chunk) */
     const uint32_t* tokens;   /* T x 3 AoS */
     uint32_t doc_begin;       /* shard document range; [0, D) for one GPU */
     uint32_t doc_end;
