@@ -76,34 +76,17 @@ __device__ __forceinline__ void ssc_load_keys(const uint16_t* z, uint32_t n, uin
 __device__ __forceinline__ uint32_t ssc_doc(const uint32_t* key, const uint16_t* z, uint32_t n, uint32_t lane,
                                             const SscWarpSmem& w, uint32_t cq, uint32_t* out_row, uint32_t tbits) {
     auto set_bit = [&](uint32_t k) { atomicOr(w.bm + (k >> 5), 1u << (k & 31u)); };
-    auto rank_of = [&](uint32_t k) {
-        const uint32_t wi = k >> 5;
-        return w.wpre[wi] + __popc(w.bm[wi] & ((1u << (k & 31u)) - 1u));
-    };
     auto count = [&](uint32_t k) {
-        const uint32_t rank = rank_of(k);
+        const uint32_t wi = k >> 5;
+        const uint32_t rank = w.wpre[wi] + __popc(w.bm[wi] & ((1u << (k & 31u)) - 1u));
         atomicAdd(w.cnt + rank, 1u);
         w.top[rank] = static_cast<uint16_t>(k);
     };
-    // Documents of <= 128 tokens (all topics in registers): the bit-setting atomic returns the
-    // old word, so each topic's first occurrence is known -- it alone stores the topic at its
-    // rank and the others count (count = 1 + cnt): one shared-memory access per token fewer.
-    const bool short_doc = n <= 128u;
-    uint32_t first = 0;  // bit r: key[r] is its topic's first occurrence
-    if (short_doc) {
 #pragma unroll
-        for (uint32_t r = 0; r < 4; ++r)
-            if (key[r] != 0xFFFFFFFFu) {
-                const uint32_t bit = 1u << (key[r] & 31u);
-                if (!(atomicOr(w.bm + (key[r] >> 5), bit) & bit)) first |= 1u << r;
-            }
-    } else {
-#pragma unroll
-        for (uint32_t r = 0; r < 4; ++r)
-            if (key[r] != 0xFFFFFFFFu) set_bit(key[r]);
+    for (uint32_t r = 0; r < 4; ++r)
+        if (key[r] != 0xFFFFFFFFu) set_bit(key[r]);
 #pragma unroll 1
-        for (uint32_t i = 128 + lane; i < n; i += 32) set_bit(__ldg(z + i));
-    }
+    for (uint32_t i = 128 + lane; i < n; i += 32) set_bit(__ldg(z + i));
     __syncwarp();
     // Lane-range popcounts -> warp exclusive scan -> per-word first ranks.  Up to kScanRegs
     // chunks per lane stay in registers between the two passes (K <= 12288: one read of the map).
@@ -141,26 +124,16 @@ __device__ __forceinline__ uint32_t ssc_doc(const uint32_t* key, const uint16_t*
         for (uint32_t j = 0; j < cq; ++j) wp[j] = ranks(mine[j], run);
     }
     __syncwarp();
-    if (short_doc) {
 #pragma unroll
-        for (uint32_t r = 0; r < 4; ++r)
-            if (key[r] != 0xFFFFFFFFu) {
-                const uint32_t rank = rank_of(key[r]);
-                if (first & (1u << r)) w.top[rank] = static_cast<uint16_t>(key[r]);
-                else atomicAdd(w.cnt + rank, 1u);
-            }
-    } else {
-#pragma unroll
-        for (uint32_t r = 0; r < 4; ++r)
-            if (key[r] != 0xFFFFFFFFu) count(key[r]);
+    for (uint32_t r = 0; r < 4; ++r)
+        if (key[r] != 0xFFFFFFFFu) count(key[r]);
 #pragma unroll 1
-        for (uint32_t i = 128 + lane; i < n; i += 32) count(__ldg(z + i));
-    }
+    for (uint32_t i = 128 + lane; i < n; i += 32) count(__ldg(z + i));
     __syncwarp();
     // Emit the row; the map is cleared once per distinct topic (nnz stores, not len).
 #pragma unroll 1
     for (uint32_t e = lane; e < nnz; e += 32) {
-        const uint32_t k = w.cnt[e] + (short_doc ? 1u : 0u), t = w.top[e];
+        const uint32_t k = w.cnt[e], t = w.top[e];
         w.cnt[e] = 0u;
         w.bm[t >> 5] = 0u;
         out_row[1 + e] = t | (k << tbits);
