@@ -162,7 +162,7 @@ struct HostBuf {
 // trainer.cpp:65-198, held in pinned host memory instead of a spill file): the device state
 // build_state() produced for its document range, and the scalars that describe it.
 struct ChunkImage {
-    uint32_t doc_begin = 0, doc_end = 0, D = 0, nseg = 0, n_units = 0, n_long = 0, tbits = 1, wshift = 0;
+    uint32_t doc_begin = 0, doc_end = 0, D = 0, nseg = 0, n_units = 0, n_long = 0, n_huge = 0, tbits = 1, wshift = 0;
     uint64_t T = 0, id_base = 0, out_offset = 0;
     bool doc_major = true, have_ids = false;
     std::vector<uint64_t> view_pos;  // gathered chunks: position in the engine's view per chunk token
@@ -191,7 +191,7 @@ struct slda_engine {
     uint64_t seed = 0, id_base = 0;
     uint32_t iteration = 0;
     uint32_t rank = 0, world = 1;
-    uint32_t nseg = 0, n_units = 0, n_long = 0;
+    uint32_t nseg = 0, n_units = 0, n_long = 0, n_huge = 0;
     bool doc_major = true;
     bool have_ids = false;  // per-slot RNG element ids (non doc-major input or explicit ids)
     bool vanilla = false;  // SamplerKind::kVanilla (trainer.cpp:281-285)
@@ -748,7 +748,8 @@ void slda_engine::build_state(const slda_corpus_view& cv, const slda_config& c, 
     }
 
     phase("schedule + units");
-    // Long documents take the CTA histogram path of SSC.
+    // Documents longer than kSscWarpCap, for SSC's later passes: those longer than kSscMidCap
+    // (the CTA histogram path) first, then the medium ones (the medium warp pass).
     {
         DevMem flags, iota, cnt;
         flags.alloc(static_cast<size_t>(D) * 4, nullptr);
@@ -756,17 +757,21 @@ void slda_engine::build_state(const slda_corpus_view& cv, const slda_config& c, 
         cnt.alloc(8, nullptr);
         long_docs.alloc(static_cast<size_t>(D) * 4, &device_bytes);
         if (D) {
-            CK(slda::launch_long_flags(doc_start.as<uint32_t>(), D, flags.as<uint32_t>(), stream));
             CK(slda::launch_iota(iota.as<uint32_t>(), D, stream));
-            cub_call([&](void* t, size_t& b) {
-                return cub::DeviceSelect::Flagged(t, b, iota.as<uint32_t>(), flags.as<uint32_t>(),
-                                                  long_docs.as<uint32_t>(), cnt.as<uint32_t>(),
-                                                  static_cast<int64_t>(D), stream);
-            });
-            n_long = d2h_scalar(cnt.as<uint32_t>());
+            auto select = [&](uint32_t lo, uint32_t hi, uint32_t at) {
+                CK(slda::launch_long_flags(doc_start.as<uint32_t>(), D, lo, hi, flags.as<uint32_t>(), stream));
+                cub_call([&](void* t, size_t& b) {
+                    return cub::DeviceSelect::Flagged(t, b, iota.as<uint32_t>(), flags.as<uint32_t>(),
+                                                      long_docs.as<uint32_t>() + at, cnt.as<uint32_t>(),
+                                                      static_cast<int64_t>(D), stream);
+                });
+                return d2h_scalar(cnt.as<uint32_t>());
+            };
+            n_huge = select(slda::kSscMidCap, 0xFFFFFFFFu, 0);
+            n_long = n_huge + select(slda::kSscWarpCap, slda::kSscMidCap, n_huge);
         }
-        if (n_long && static_cast<size_t>(K_pad) * 4 > 200 * 1024)
-            hist_scratch.alloc(static_cast<size_t>(std::min<uint32_t>(n_long, 296)) * K_pad * 4, &device_bytes);
+        if (n_huge && static_cast<size_t>(K_pad) * 4 > 200 * 1024)
+            hist_scratch.alloc(static_cast<size_t>(std::min<uint32_t>(n_huge, 296)) * K_pad * 4, &device_bytes);
     }
 
     // Initial topics (trainer.cpp:383-388 / corpus.cpp:87-96), by slot.
@@ -913,7 +918,7 @@ void slda_engine::build_streaming(const slda_corpus_view& cv, const slda_config&
     uint32_t max_long = 0;
     for (const ChunkImage& im : chunks) {
         max_t = std::max(max_t, im.T);
-        max_long = std::max(max_long, im.n_long);
+        max_long = std::max(max_long, im.n_huge);
     }
     if (max_long && static_cast<size_t>(K_pad) * 4 > 200 * 1024)
         grow(hist_scratch, static_cast<size_t>(std::min<uint32_t>(max_long, 296)) * K_pad * 4);
@@ -945,6 +950,7 @@ void slda_engine::save_image(ChunkImage& im) {
     im.nseg = nseg;
     im.n_units = n_units;
     im.n_long = n_long;
+    im.n_huge = n_huge;
     im.tbits = tbits;
     im.wshift = wshift;
     im.doc_major = doc_major;
@@ -993,6 +999,7 @@ void slda_engine::set_scalars(uint32_t ci) {
     nseg = im.nseg;
     n_units = im.n_units;
     n_long = im.n_long;
+    n_huge = im.n_huge;
     tbits = im.tbits;
     wshift = im.wshift;
     doc_major = im.doc_major;
@@ -1096,10 +1103,11 @@ void slda_engine::ssc(cudaStream_t st) {
     s.K_pad = K_pad;
     s.long_docs = long_docs.as<uint32_t>();
     s.n_long = n_long;
+    s.n_huge = n_huge;
     s.hist_scratch = hist_scratch.as<uint32_t>();
     s.nnz_total = nnz_dst ? nnz_dst : nnz_counter();
     CK(slda::launch_ssc(s, st));
-    launches += (D > 0) + (n_long > 0);
+    launches += (D > 0) + (n_long > n_huge) + (n_huge > 0);
 }
 
 // M-step after the E-step's B: colsum -> denom -> phi/L4/L8/Q over every word row.  preprocess

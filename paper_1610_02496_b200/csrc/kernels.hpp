@@ -14,6 +14,7 @@ struct Unit {
 
 constexpr uint32_t kUnitMaxTokens = 8192;  // sampler: max tokens per unit (one CTA)
 constexpr uint32_t kSscWarpCap = 512;      // SSC: docs up to this length take the warp path
+constexpr uint32_t kSscMidCap = 2048;      // SSC: longer ones up to this take the medium warp pass
 
 struct SamplerArgs {
     const uint2* tok;       // execution order: {C_dk row offset in uint4 units, slot}
@@ -49,8 +50,8 @@ struct SscArgs {
     const uint32_t* row4;       // per doc: row offset in uint4 units
     uint32_t* A;
     uint32_t tbits, K_pad;
-    const uint32_t* long_docs;  // docs longer than kSscWarpCap
-    uint32_t n_long;
+    const uint32_t* long_docs;  // docs longer than kSscWarpCap: the n_huge > kSscMidCap first
+    uint32_t n_long, n_huge;
     uint32_t* hist_scratch;     // n_long_ctas x K_pad (global fallback for large K)
     unsigned long long* nnz_total;
 };
@@ -123,7 +124,7 @@ cudaError_t launch_emit_units(const uint32_t* schedule, const uint32_t* seg_word
                               cudaStream_t s);
 cudaError_t launch_row_quads(const uint32_t* doc_start, uint32_t D, uint32_t* quads,
                              cudaStream_t s);
-cudaError_t launch_long_flags(const uint32_t* doc_start, uint32_t D, uint32_t* flags,
+cudaError_t launch_long_flags(const uint32_t* doc_start, uint32_t D, uint32_t lo, uint32_t hi, uint32_t* flags,
                               cudaStream_t s);
 cudaError_t launch_init_topics(uint64_t T, const uint64_t* ids, uint64_t id_base, uint64_t seed,
                                uint32_t K, uint16_t* z, cudaStream_t s);

@@ -217,15 +217,18 @@ cudaError_t launch_row_quads(const uint32_t* doc_start, uint32_t D, uint32_t* qu
     return cudaGetLastError();
 }
 
-__global__ void long_flags_kernel(const uint32_t* doc_start, uint32_t D, uint32_t* flags) {
+// flags[d] = lo < length(d) <= hi
+__global__ void long_flags_kernel(const uint32_t* doc_start, uint32_t D, uint32_t lo, uint32_t hi, uint32_t* flags) {
     const uint32_t d = blockIdx.x * blockDim.x + threadIdx.x;
     if (d >= D) return;
-    flags[d] = (doc_start[d + 1] - doc_start[d]) > kSscWarpCap ? 1u : 0u;
+    const uint32_t n = doc_start[d + 1] - doc_start[d];
+    flags[d] = n > lo && n <= hi ? 1u : 0u;
 }
 
-cudaError_t launch_long_flags(const uint32_t* doc_start, uint32_t D, uint32_t* flags, cudaStream_t s) {
+cudaError_t launch_long_flags(const uint32_t* doc_start, uint32_t D, uint32_t lo, uint32_t hi, uint32_t* flags,
+                              cudaStream_t s) {
     if (D == 0) return cudaSuccess;
-    long_flags_kernel<<<(D + 255) / 256, 256, 0, s>>>(doc_start, D, flags);
+    long_flags_kernel<<<(D + 255) / 256, 256, 0, s>>>(doc_start, D, lo, hi, flags);
     return cudaGetLastError();
 }
 

@@ -33,7 +33,7 @@ struct SscWarpSmem {
     uint32_t* bm;    // 128*cq words (bit k = topic k present), all zero between documents
     uint16_t* wpre;  // per map word: rank of its first topic
     uint16_t* top;   // per rank: topic
-    uint32_t* cnt;   // per rank: count (zero between documents)
+    uint32_t* cnt;   // per rank: count (zero between documents); packed: two 16-bit counts per word
 };
 
 __host__ __device__ inline uint32_t ssc_chunks_per_lane(uint32_t K_pad) {
@@ -42,11 +42,15 @@ __host__ __device__ inline uint32_t ssc_chunks_per_lane(uint32_t K_pad) {
     return cq | 1u;
 }
 
-__host__ __device__ inline size_t ssc_warp_bytes(uint32_t K_pad) {
+// Per-warp shared memory: the map (512 cq B), the word ranks (256 cq B), and per-rank topics and
+// counts for up to `cap` distinct topics (nnz <= document length <= cap).
+__host__ __device__ inline size_t ssc_warp_bytes(uint32_t K_pad, uint32_t cap = kSscWarpCap) {
     const size_t cq = ssc_chunks_per_lane(K_pad);
-    const size_t b = 512 * cq + 256 * cq + 2 * kSscWarpCap + 4 * kSscWarpCap;
+    const size_t cnt_bytes = (cap > kSscWarpCap ? 2 : 4) * static_cast<size_t>(cap);  // packed past 512
+    const size_t b = 512 * cq + 256 * cq + 2 * static_cast<size_t>(cap) + cnt_bytes;
     return (b + 15u) & ~static_cast<size_t>(15u);
 }
+
 
 __device__ __forceinline__ uint32_t warp_excl_scan(uint32_t x, uint32_t lane, uint32_t& total) {
     uint32_t incl = x;
@@ -70,23 +74,39 @@ __device__ __forceinline__ void ssc_load_keys(const uint16_t* z, uint32_t n, uin
     }
 }
 
-// One document of n <= kSscWarpCap tokens: its first 128 topics are in key[] (prefetched),
-// the rest are re-read from z (L1) by a runtime loop, so one code body serves every length
-// (several length-specialised bodies overflow the instruction cache: ncu no_instruction stalls).
+// One document of n <= cap tokens: its first 128 topics are in key[] (prefetched), the rest are
+// re-read from z (L1) by a runtime loop, so one code body serves every length (several
+// length-specialised bodies overflow the instruction cache: ncu no_instruction stalls).  The
+// loop issues four loads before their shared-memory updates (the medium pass is all loop).
+// kPacked: counts (<= cap <= 65535) two per word, so the medium pass fits more warps per SM.
+template <bool kPacked>
 __device__ __forceinline__ uint32_t ssc_doc(const uint32_t* key, const uint16_t* z, uint32_t n, uint32_t lane,
                                             const SscWarpSmem& w, uint32_t cq, uint32_t* out_row, uint32_t tbits) {
     auto set_bit = [&](uint32_t k) { atomicOr(w.bm + (k >> 5), 1u << (k & 31u)); };
     auto count = [&](uint32_t k) {
         const uint32_t wi = k >> 5;
         const uint32_t rank = w.wpre[wi] + __popc(w.bm[wi] & ((1u << (k & 31u)) - 1u));
-        atomicAdd(w.cnt + rank, 1u);
+        if (kPacked)
+            atomicAdd(w.cnt + (rank >> 1), 1u << ((rank & 1u) * 16u));
+        else
+            atomicAdd(w.cnt + rank, 1u);
         w.top[rank] = static_cast<uint16_t>(k);
+    };
+    auto rest = [&](auto&& f) {
+#pragma unroll 1
+        for (uint32_t i = 128 + lane; i < n; i += 128) {
+            uint32_t t[4];
+#pragma unroll
+            for (uint32_t r = 0; r < 4; ++r) t[r] = i + 32 * r < n ? __ldg(z + i + 32 * r) : 0xFFFFFFFFu;
+#pragma unroll
+            for (uint32_t r = 0; r < 4; ++r)
+                if (t[r] != 0xFFFFFFFFu) f(t[r]);
+        }
     };
 #pragma unroll
     for (uint32_t r = 0; r < 4; ++r)
         if (key[r] != 0xFFFFFFFFu) set_bit(key[r]);
-#pragma unroll 1
-    for (uint32_t i = 128 + lane; i < n; i += 32) set_bit(__ldg(z + i));
+    rest(set_bit);
     __syncwarp();
     // Lane-range popcounts -> warp exclusive scan -> per-word first ranks.  Up to kScanRegs
     // chunks per lane stay in registers between the two passes (K <= 12288: one read of the map).
@@ -127,14 +147,14 @@ __device__ __forceinline__ uint32_t ssc_doc(const uint32_t* key, const uint16_t*
 #pragma unroll
     for (uint32_t r = 0; r < 4; ++r)
         if (key[r] != 0xFFFFFFFFu) count(key[r]);
-#pragma unroll 1
-    for (uint32_t i = 128 + lane; i < n; i += 32) count(__ldg(z + i));
+    rest(count);
     __syncwarp();
     // Emit the row; the map is cleared once per distinct topic (nnz stores, not len).
 #pragma unroll 1
     for (uint32_t e = lane; e < nnz; e += 32) {
-        const uint32_t k = w.cnt[e], t = w.top[e];
-        w.cnt[e] = 0u;
+        const uint32_t k = kPacked ? (w.cnt[e >> 1] >> ((e & 1u) * 16u)) & 0xFFFFu : w.cnt[e];
+        const uint32_t t = w.top[e];
+        w.cnt[kPacked ? e >> 1 : e] = 0u;  // (packed: both lanes of a word read it before either clears)
         w.bm[t >> 5] = 0u;
         out_row[1 + e] = t | (k << tbits);
     }
@@ -150,47 +170,54 @@ __device__ __forceinline__ uint32_t ssc_doc(const uint32_t* key, const uint16_t*
 // 8 -> 6.45 / 100.16, 16 -> 6.57 / 100.40).
 constexpr uint32_t kSscWarps = 4;
 
-__global__ void __launch_bounds__(kSscWarps * 32, 8) ssc_warp_kernel(SscArgs a) {
+// kCap = kSscWarpCap: every document (those longer are skipped); kCap = kSscMidCap: the
+// long-document list, those of at most kCap tokens.
+template <uint32_t kCap, int MINB>
+__global__ void __launch_bounds__(kSscWarps * 32, MINB) ssc_warp_kernel(SscArgs a) {
+    constexpr bool kList = kCap > kSscWarpCap;
     extern __shared__ __align__(16) unsigned char s_raw[];
     const uint32_t wid = threadIdx.x >> 5, lane = lane_id();
     const uint32_t cq = ssc_chunks_per_lane(a.K_pad);
-    unsigned char* base = s_raw + wid * ssc_warp_bytes(a.K_pad);
+    unsigned char* base = s_raw + wid * ssc_warp_bytes(a.K_pad, kCap);
     SscWarpSmem w;
     w.bm = reinterpret_cast<uint32_t*>(base);
     w.wpre = reinterpret_cast<uint16_t*>(w.bm + 128 * cq);
     w.cnt = reinterpret_cast<uint32_t*>(w.wpre + 128 * cq);
-    w.top = reinterpret_cast<uint16_t*>(w.cnt + kSscWarpCap);
+    w.top = reinterpret_cast<uint16_t*>(w.cnt + (kList ? kCap / 2 : kCap));
     {
         uint4* b4 = reinterpret_cast<uint4*>(w.bm);
         for (uint32_t i = lane; i < 32 * cq; i += 32) b4[i] = make_uint4(0u, 0u, 0u, 0u);
-        for (uint32_t i = lane; i < kSscWarpCap; i += 32) w.cnt[i] = 0u;
+        for (uint32_t i = lane; i < (kList ? kCap / 2 : kCap); i += 32) w.cnt[i] = 0u;
     }
     __syncwarp();
     unsigned long long nnz_acc = 0;
     const uint32_t gw = blockIdx.x * kSscWarps + wid, nw = gridDim.x * kSscWarps;
+    const uint32_t ndocs = kList ? a.n_long - a.n_huge : a.D;
+    const uint32_t* list = a.long_docs + a.n_huge;
     // Software pipeline over the warp's documents: the next document's extent, row offset and
     // (up to 128) topics are loaded while this one is counted.
     auto meta = [&](uint32_t dd, uint32_t& s0, uint32_t& n, uint32_t& rq) {
         s0 = 0; n = 0; rq = 0;
-        if (dd < a.D) {
-            s0 = __ldg(a.doc_start + dd);
-            n = __ldg(a.doc_start + dd + 1) - s0;
-            rq = __ldg(a.row4 + dd);
+        if (dd < ndocs) {
+            const uint32_t doc = kList ? __ldg(list + dd) : dd;
+            s0 = __ldg(a.doc_start + doc);
+            n = __ldg(a.doc_start + doc + 1) - s0;
+            rq = __ldg(a.row4 + doc);
         }
     };
     uint32_t s0, n, rq, key[4];
     meta(gw, s0, n, rq);
-    ssc_load_keys<4>(a.z + s0, n <= kSscWarpCap ? n : 0u, lane, key);
-    for (uint32_t d = gw; d < a.D; d += nw) {
+    ssc_load_keys<4>(a.z + s0, n <= kCap ? n : 0u, lane, key);
+    for (uint32_t d = gw; d < ndocs; d += nw) {
         const uint32_t cs0 = s0, cn = n;
         uint32_t* row = a.A + rq * 4u;
-        // (the prefetched keys cover the first 128 topics of documents up to kSscWarpCap)
+        // (the prefetched keys cover the first 128 topics of documents up to kCap)
         const uint32_t k0 = key[0], k1 = key[1], k2 = key[2], k3 = key[3];
         meta(d + nw, s0, n, rq);
-        ssc_load_keys<4>(a.z + s0, n <= kSscWarpCap ? n : 0u, lane, key);
-        if (cn > kSscWarpCap || cn == 0) continue;  // ssc_long_kernel / empty document
+        ssc_load_keys<4>(a.z + s0, n <= kCap ? n : 0u, lane, key);
+        if (cn > kCap || cn == 0) continue;  // a longer document's kernel / empty document
         const uint32_t ck[4] = {k0, k1, k2, k3};
-        const uint32_t nnz = ssc_doc(ck, a.z + cs0, cn, lane, w, cq, row, a.tbits);
+        const uint32_t nnz = ssc_doc<kList>(ck, a.z + cs0, cn, lane, w, cq, row, a.tbits);
         nnz_acc += nnz;
     }
     if (lane == 0 && nnz_acc) atomicAdd(a.nnz_total, nnz_acc);
@@ -204,7 +231,7 @@ __global__ void __launch_bounds__(256) ssc_long_kernel(SscArgs a) {
     uint32_t* hist = kSmemHist ? s_dyn : a.hist_scratch + static_cast<size_t>(blockIdx.x) * a.K_pad;
     const uint32_t tid = threadIdx.x;
     const uint32_t per = (a.K_pad + 255u) / 256u;
-    for (uint32_t li = blockIdx.x; li < a.n_long; li += gridDim.x) {
+    for (uint32_t li = blockIdx.x; li < a.n_huge; li += gridDim.x) {
         const uint32_t d = a.long_docs[li];
         const uint32_t s0 = a.doc_start[d];
         const uint32_t n = a.doc_start[d + 1] - s0;
@@ -243,7 +270,8 @@ __global__ void __launch_bounds__(256) ssc_long_kernel(SscArgs a) {
 cudaError_t launch_ssc(const SscArgs& a, cudaStream_t s) {
     if (a.D > 0) {
         const size_t bm_smem = kSscWarps * ssc_warp_bytes(a.K_pad);  // <= 59 KB for K <= 65536
-        if (const cudaError_t e = cudaFuncSetAttribute(ssc_warp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        auto kern = ssc_warp_kernel<kSscWarpCap, 8>;
+        if (const cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                        static_cast<int>(bm_smem));
             e != cudaSuccess)
             return e;
@@ -251,11 +279,21 @@ cudaError_t launch_ssc(const SscArgs& a, cudaStream_t s) {
         // beside the M-step on a low-priority stream, and retiring CTAs let the scheduler
         // hand SMs to the higher-priority colsum/phi CTAs.
         const uint32_t blocks = static_cast<uint32_t>((a.D + kSscWarps * 16u - 1) / (kSscWarps * 16u));
-        ssc_warp_kernel<<<blocks, kSscWarps * 32, bm_smem, s>>>(a);
+        kern<<<blocks, kSscWarps * 32, bm_smem, s>>>(a);
     }
-    if (a.n_long > 0) {
+    if (a.n_long > a.n_huge) {  // medium documents: warps with kSscMidCap rank arrays
+        const size_t mid_smem = kSscWarps * ssc_warp_bytes(a.K_pad, kSscMidCap);  // <= 84 KB
+        auto kern = ssc_warp_kernel<kSscMidCap, 4>;
+        if (const cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                       static_cast<int>(mid_smem));
+            e != cudaSuccess)
+            return e;
+        const uint32_t blocks = (a.n_long - a.n_huge + kSscWarps * 4u - 1) / (kSscWarps * 4u);
+        kern<<<blocks, kSscWarps * 32, mid_smem, s>>>(a);
+    }
+    if (a.n_huge > 0) {  // documents longer than kSscMidCap: one CTA histogram each
         const size_t smem = sizeof(uint32_t) * a.K_pad;
-        const uint32_t blocks = a.n_long < 148u * 2u ? a.n_long : 148u * 2u;
+        const uint32_t blocks = a.n_huge < 148u * 2u ? a.n_huge : 148u * 2u;
         if (smem <= 200 * 1024) {
             if (const cudaError_t e = cudaFuncSetAttribute(ssc_long_kernel<true>,
                                                            cudaFuncAttributeMaxDynamicSharedMemorySize,

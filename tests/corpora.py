@@ -53,6 +53,12 @@ CASES: dict[str, dict] = {
                    "K": 12, "seed": 5, "iterations": 3, "pdow": True},
     "given_topics": {"corpus": {"family": U, "D": 150, "V": 120, "T": 6_000, "seed": 12},
                      "K": 20, "seed": 4, "iterations": 3, "given_topics_seed": 77},
+    # Lognormal lengths 127..5413 tokens: every SSC pass (warp <= 512, medium warp <= 2048, CTA
+    # histogram beyond), the last with the histogram in shared memory, then (K = 60,000) in global.
+    "ssc_lengths": {"corpus": {"family": G, "D": 300, "V": 2000, "T": 300_000, "seed": 31},
+                    "K": 3000, "seed": 9, "iterations": 3},
+    "ssc_lengths_k60k": {"corpus": {"family": G, "D": 40, "V": 300, "T": 50_000, "seed": 32},
+                         "K": 60_000, "seed": 5, "iterations": 2},
     "k_large": {"corpus": {"family": U, "D": 50, "V": 50, "T": 5_000, "seed": 13},
                 "K": 20_000, "seed": 2, "iterations": 2},
     # phi row too large for shared memory: the sampler gathers phi through L1/L2.

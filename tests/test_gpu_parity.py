@@ -266,7 +266,8 @@ def test_checkpoint_roundtrip_and_resume(tmp_path):
     assert len(text) == 1 + half.num_tokens + 1 + int((half.word_topic() != 0).sum())
 
 
-@pytest.mark.parametrize("name,iters", [("given_topics", 2), ("c1", 5), ("k_large", 2)])
+@pytest.mark.parametrize("name,iters", [("given_topics", 2), ("c1", 5), ("k_large", 2), ("ssc_lengths", 3),
+                                        ("ssc_lengths_k60k", 2)])
 def test_checkpoint_bytes_equal_reference(name, iters, tmp_path):
     """Acceptance criterion 7's byte-identical checkpoints (acceptance.cpp:389-421) across the
     two engines: the device model's save() after N iterations is the same file, byte for byte, as
