@@ -4,6 +4,9 @@
 #include "common.cuh"
 #include "kernels.hpp"
 
+#include <cuda.h>  // CUtensorMap (the encoder is fetched through the runtime: no -lcuda)
+#include <cudaTypedefs.h>
+
 #include <cmath>
 #include <cstdlib>
 #include <string>
@@ -297,6 +300,184 @@ __global__ void __launch_bounds__(kPhiRows, 4) phi_kernel(const uint32_t* __rest
     }
 }
 
+// ---- phi by TMA tiles: warp per 32 word rows ---------------------------------------------------
+// The same per-row computation as phi_kernel (thread = row, the sequential f32 chain over the
+// row), but each warp owns its 32 rows and moves 32 x 32 tiles with the TMA engine: a 2-D tensor
+// load of C_wk (128-byte swizzle: lane r reads 16-byte chunk j of its row at j ^ (r & 7), so
+// every quarter-warp covers all 32 banks) plus 1-D bulk copies of the tile's denom / 1/denom /
+// zero-count phi, all completing on one mbarrier per stage; phi is written back into the tile
+// in place and a 2-D tensor store returns it.  No CTA barriers, no per-thread copy or store
+// loops: one lane issues three TMA operations per tile.  The tensor maps start at row_begin with
+// row_end - row_begin rows, so the last group's rows past the slice are zero-filled on load and
+// clipped on store.
+constexpr uint32_t kPhiTileBytes = 32u * 32u * 4u;          // 32 rows x 32 columns, u32 / f32
+constexpr uint32_t kPhiAuxBytes = 32u * 8u * 2u + 32u * 4u;  // denom, 1/denom (f64), zero-count phi
+
+template <int S, int W>
+constexpr size_t phi_tma_smem_bytes() {
+    return 1024 + static_cast<size_t>(W) * S * (kPhiTileBytes + kPhiAuxBytes + 8);
+}
+
+__device__ __forceinline__ void mbar_wait_parity(uint32_t bar, uint32_t parity) {
+    asm volatile("{\n\t.reg .pred P1;\n\tWAIT_%=:\n\t"
+                 "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+                 "@!P1 bra WAIT_%=;\n\t}" ::"r"(bar), "r"(parity)
+                 : "memory");
+}
+
+template <int S, int W>
+__global__ void __launch_bounds__(W * 32) phi_tma_kernel(const __grid_constant__ CUtensorMap t_cnt,
+                                                         const __grid_constant__ CUtensorMap t_phi,
+                                                         const double* __restrict__ denom,
+                                                         const float* __restrict__ zv, float* __restrict__ l8,
+                                                         float* __restrict__ q, uint32_t row_begin, uint32_t rows,
+                                                         uint32_t K_pad, uint32_t l8_stride, double beta,
+                                                         float falpha) {
+    static_assert(S >= 3, "one stage computing, one being stored, at least one loading");
+    extern __shared__ unsigned char phi_tma_raw[];
+    // 128-byte swizzled TMA tiles need 1024-byte aligned destinations.
+    unsigned char* base = reinterpret_cast<unsigned char*>(
+        (reinterpret_cast<uintptr_t>(phi_tma_raw) + 1023u) & ~static_cast<uintptr_t>(1023u));
+    const uint32_t wid = threadIdx.x >> 5, lane = threadIdx.x & 31u;
+    const uint32_t r0 = (blockIdx.x * W + wid) * 32u;  // first row of this warp (slice-relative)
+    if (r0 >= rows) return;                             // warp-uniform; no CTA barriers below
+    unsigned char* tiles = base + wid * S * kPhiTileBytes;
+    unsigned char* aux = base + W * S * kPhiTileBytes + wid * S * kPhiAuxBytes;
+    const uint32_t bars = static_cast<uint32_t>(__cvta_generic_to_shared(
+        base + W * S * (kPhiTileBytes + kPhiAuxBytes) + wid * S * 8u));
+    const uint32_t ntiles = K_pad / 32u;
+    if (lane == 0) {
+#pragma unroll
+        for (int st = 0; st < S; ++st)
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bars + st * 8u) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncwarp();
+    auto load = [&](uint32_t t) {  // lane 0
+        const uint32_t st = t % S, bar = bars + st * 8u, c0 = t * 32u;
+        const uint32_t dst = static_cast<uint32_t>(__cvta_generic_to_shared(tiles + st * kPhiTileBytes));
+        const uint32_t adst = static_cast<uint32_t>(__cvta_generic_to_shared(aux + st * kPhiAuxBytes));
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar),
+                     "r"(kPhiTileBytes + kPhiAuxBytes)
+                     : "memory");
+        asm volatile(
+            "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
+            ::"r"(dst), "l"(reinterpret_cast<uint64_t>(&t_cnt)), "r"(c0), "r"(r0), "r"(bar)
+            : "memory");
+        asm volatile("cp.async.bulk.shared::cta.global.mbarrier::complete_tx::bytes [%0], [%1], 256, [%2];"
+                     ::"r"(adst), "l"(denom + c0), "r"(bar)
+                     : "memory");
+        asm volatile("cp.async.bulk.shared::cta.global.mbarrier::complete_tx::bytes [%0], [%1], 256, [%2];"
+                     ::"r"(adst + 256u), "l"(denom + K_pad + c0), "r"(bar)
+                     : "memory");
+        asm volatile("cp.async.bulk.shared::cta.global.mbarrier::complete_tx::bytes [%0], [%1], 128, [%2];"
+                     ::"r"(adst + 512u), "l"(zv + c0), "r"(bar)
+                     : "memory");
+    };
+    if (lane == 0)
+        for (uint32_t t = 0; t + 2 < S && t < ntiles; ++t) load(t);
+    const uint32_t v = row_begin + r0 + lane;
+    const bool live = r0 + lane < rows;
+    float* l8row = l8 + static_cast<size_t>(v) * l8_stride;
+    float run = 0.0f;
+    for (uint32_t t = 0; t < ntiles; ++t) {
+        const uint32_t st = t % S, c0 = t * 32u;
+        if (lane == 0 && t + S - 2 < ntiles) {
+            // stage of tile t - 2: its tensor store must have finished reading shared memory
+            asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+            load(t + S - 2);
+        }
+        mbar_wait_parity(bars + st * 8u, (t / S) & 1u);
+        uint32_t* tile = reinterpret_cast<uint32_t*>(tiles + st * kPhiTileBytes) + lane * 32u;
+        const double* den = reinterpret_cast<const double*>(aux + st * kPhiAuxBytes);
+        const double* rcp = den + 32;
+        const float* zt = reinterpret_cast<const float*>(aux + st * kPhiAuxBytes + 512u);
+        float l8v[4];
+#pragma unroll
+        for (uint32_t j = 0; j < 8; ++j) {
+            uint32_t* cell = tile + ((j ^ (lane & 7u)) << 2);
+            const uint4 cnt = *reinterpret_cast<const uint4*>(cell);
+            float4 bh = *reinterpret_cast<const float4*>(zt + j * 4);
+            if ((cnt.x | cnt.y | cnt.z | cnt.w) != 0u) {
+                const double* d = den + j * 4;
+                const double* r = rcp + j * 4;
+                if (cnt.x) bh.x = phi_quotient(__dadd_rn(static_cast<double>(cnt.x), beta), d[0], r[0]);
+                if (cnt.y) bh.y = phi_quotient(__dadd_rn(static_cast<double>(cnt.y), beta), d[1], r[1]);
+                if (cnt.z) bh.z = phi_quotient(__dadd_rn(static_cast<double>(cnt.z), beta), d[2], r[2]);
+                if (cnt.w) bh.w = phi_quotient(__dadd_rn(static_cast<double>(cnt.w), beta), d[3], r[3]);
+            }
+            run = __fadd_rn(run, bh.x);  // WaryTree::build's sequential chain (see phi_kernel)
+            run = __fadd_rn(run, bh.y);
+            run = __fadd_rn(run, bh.z);
+            run = __fadd_rn(run, bh.w);
+            *reinterpret_cast<float4*>(cell) = bh;
+            if (j & 1u) l8v[j >> 1] = run;
+        }
+        if (live) *reinterpret_cast<float4*>(l8row + c0 / kLeaf) = make_float4(l8v[0], l8v[1], l8v[2], l8v[3]);
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> TMA store
+        __syncwarp();
+        if (lane == 0) {
+            asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];"
+                         ::"l"(reinterpret_cast<uint64_t>(&t_phi)), "r"(c0), "r"(r0),
+                         "r"(static_cast<uint32_t>(__cvta_generic_to_shared(tiles + st * kPhiTileBytes)))
+                         : "memory");
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        }
+    }
+    if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    if (live) {
+        for (uint32_t j = K_pad / kLeaf; j < l8_stride; ++j) l8row[j] = run;
+        q[v] = __fmul_rn(falpha, run);  // trainer.cpp:245
+    }
+}
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no libcuda link dependency).
+static cudaError_t encode_tile_map(CUtensorMap* m, CUtensorMapDataType type, void* base, uint32_t cols,
+                                   uint32_t rows) {
+    static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+    if (!encode) {
+        void* fn = nullptr;
+        cudaDriverEntryPointQueryResult qr{};
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &qr) != cudaSuccess ||
+            qr != cudaDriverEntryPointSuccess || !fn)
+            return cudaErrorNotSupported;
+        encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    }
+    const cuuint64_t dims[2] = {cols, rows};
+    const cuuint64_t strides[1] = {static_cast<cuuint64_t>(cols) * 4u};
+    const cuuint32_t box[2] = {32u, 32u};
+    const cuuint32_t estr[2] = {1u, 1u};
+    const CUresult r = encode(m, type, 2, base, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                              CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
+}
+
+template <int S, int W>
+cudaError_t launch_phi_tma_t(const uint32_t* B, const double* denom, const float* zv, float* bhat, float* l8,
+                             float* q, uint32_t row_begin, uint32_t row_end, uint32_t K_pad, uint32_t l8_stride,
+                             double beta, float falpha, cudaStream_t s) {
+    const uint32_t rows = row_end - row_begin;
+    CUtensorMap tc, tp;
+    const size_t off = static_cast<size_t>(row_begin) * K_pad;
+    if (const cudaError_t e = encode_tile_map(&tc, CU_TENSOR_MAP_DATA_TYPE_UINT32, const_cast<uint32_t*>(B) + off,
+                                              K_pad, rows);
+        e != cudaSuccess)
+        return e;
+    if (const cudaError_t e = encode_tile_map(&tp, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, bhat + off, K_pad, rows);
+        e != cudaSuccess)
+        return e;
+    constexpr size_t smem = phi_tma_smem_bytes<S, W>();
+    if (const cudaError_t e = cudaFuncSetAttribute(phi_tma_kernel<S, W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                   static_cast<int>(smem));
+        e != cudaSuccess)
+        return e;
+    const uint32_t groups = (rows + 31u) / 32u;
+    phi_tma_kernel<S, W><<<(groups + W - 1) / W, W * 32, smem, s>>>(tc, tp, denom, zv, l8, q, row_begin, rows, K_pad,
+                                                                   l8_stride, beta, falpha);
+    return cudaGetLastError();
+}
+
 template <int C, int S>
 cudaError_t launch_phi_t(const uint32_t* B, const double* denom, const float* zv, float* bhat,
                          float* l8, float* q, uint32_t row_begin, uint32_t row_end, uint32_t K_pad,
@@ -322,6 +503,10 @@ cudaError_t launch_phi(const uint32_t* B, const double* denom, const float* zv, 
     if (K_pad % 32) return cudaErrorInvalidValue;
     const char* e = std::getenv("SLDA_PHI_SHAPE");  // read per launch (tests switch it per engine)
     const std::string v = e ? e : "";
+    if (v == "tma4x1") return launch_phi_tma_t<4, 1>(B, denom, zv, bhat, l8, q, row_begin, row_end, K_pad, l8_stride, beta, falpha, s);
+    if (v == "tma3x1") return launch_phi_tma_t<3, 1>(B, denom, zv, bhat, l8, q, row_begin, row_end, K_pad, l8_stride, beta, falpha, s);
+    if (v == "tma4x2") return launch_phi_tma_t<4, 2>(B, denom, zv, bhat, l8, q, row_begin, row_end, K_pad, l8_stride, beta, falpha, s);
+    if (v == "tma6x1") return launch_phi_tma_t<6, 1>(B, denom, zv, bhat, l8, q, row_begin, row_end, K_pad, l8_stride, beta, falpha, s);
     int shape = v == "16x8" ? 1 : v == "32x3" ? 2 : v == "64x2" ? 3 : v == "64x3" ? 4 : v == "32x4" ? 5 : 0;
     // Tile columns x pipeline stages, phi alone (ms, C3 / C5 K=50K): 16x8 4.91 / 17.9,
     // 32x3 4.68 / 14.8, 32x4 4.10 / 15.7, 32x6 5.88 / 16.2.
