@@ -353,7 +353,7 @@ __global__ void __launch_bounds__(W * 32) phi_tma_kernel(const __grid_constant__
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncwarp();
-    auto load = [&](uint32_t t) {  // lane 0
+    auto load = [&](uint32_t t) {  // lane 0: tile t of C_wk + its columns' denom, 1/denom, zv
         const uint32_t st = t % S, bar = bars + st * 8u, c0 = t * 32u;
         const uint32_t dst = static_cast<uint32_t>(__cvta_generic_to_shared(tiles + st * kPhiTileBytes));
         const uint32_t adst = static_cast<uint32_t>(__cvta_generic_to_shared(aux + st * kPhiAuxBytes));
@@ -392,25 +392,32 @@ __global__ void __launch_bounds__(W * 32) phi_tma_kernel(const __grid_constant__
         const double* den = reinterpret_cast<const double*>(aux + st * kPhiAuxBytes);
         const double* rcp = den + 32;
         const float* zt = reinterpret_cast<const float*>(aux + st * kPhiAuxBytes + 512u);
+        // All eight quads are loaded before any is written back, so their quotients are
+        // independent work (the per-quad load -> divide -> store order serialises them).
+        uint4 cnt[8];
+        float4 bh[8];
+#pragma unroll
+        for (uint32_t j = 0; j < 8; ++j) {
+            cnt[j] = *reinterpret_cast<const uint4*>(tile + ((j ^ (lane & 7u)) << 2));
+            bh[j] = *reinterpret_cast<const float4*>(zt + j * 4);
+        }
+#pragma unroll
+        for (uint32_t j = 0; j < 8; ++j) {
+            const double* d = den + j * 4;
+            const double* r = rcp + j * 4;
+            if (cnt[j].x) bh[j].x = phi_quotient(__dadd_rn(static_cast<double>(cnt[j].x), beta), d[0], r[0]);
+            if (cnt[j].y) bh[j].y = phi_quotient(__dadd_rn(static_cast<double>(cnt[j].y), beta), d[1], r[1]);
+            if (cnt[j].z) bh[j].z = phi_quotient(__dadd_rn(static_cast<double>(cnt[j].z), beta), d[2], r[2]);
+            if (cnt[j].w) bh[j].w = phi_quotient(__dadd_rn(static_cast<double>(cnt[j].w), beta), d[3], r[3]);
+        }
         float l8v[4];
 #pragma unroll
         for (uint32_t j = 0; j < 8; ++j) {
-            uint32_t* cell = tile + ((j ^ (lane & 7u)) << 2);
-            const uint4 cnt = *reinterpret_cast<const uint4*>(cell);
-            float4 bh = *reinterpret_cast<const float4*>(zt + j * 4);
-            if ((cnt.x | cnt.y | cnt.z | cnt.w) != 0u) {
-                const double* d = den + j * 4;
-                const double* r = rcp + j * 4;
-                if (cnt.x) bh.x = phi_quotient(__dadd_rn(static_cast<double>(cnt.x), beta), d[0], r[0]);
-                if (cnt.y) bh.y = phi_quotient(__dadd_rn(static_cast<double>(cnt.y), beta), d[1], r[1]);
-                if (cnt.z) bh.z = phi_quotient(__dadd_rn(static_cast<double>(cnt.z), beta), d[2], r[2]);
-                if (cnt.w) bh.w = phi_quotient(__dadd_rn(static_cast<double>(cnt.w), beta), d[3], r[3]);
-            }
-            run = __fadd_rn(run, bh.x);  // WaryTree::build's sequential chain (see phi_kernel)
-            run = __fadd_rn(run, bh.y);
-            run = __fadd_rn(run, bh.z);
-            run = __fadd_rn(run, bh.w);
-            *reinterpret_cast<float4*>(cell) = bh;
+            run = __fadd_rn(run, bh[j].x);  // WaryTree::build's sequential chain (see phi_kernel)
+            run = __fadd_rn(run, bh[j].y);
+            run = __fadd_rn(run, bh[j].z);
+            run = __fadd_rn(run, bh[j].w);
+            *reinterpret_cast<float4*>(tile + ((j ^ (lane & 7u)) << 2)) = bh[j];
             if (j & 1u) l8v[j >> 1] = run;
         }
         if (live) *reinterpret_cast<float4*>(l8row + c0 / kLeaf) = make_float4(l8v[0], l8v[1], l8v[2], l8v[3]);
@@ -503,10 +510,10 @@ cudaError_t launch_phi(const uint32_t* B, const double* denom, const float* zv, 
     if (K_pad % 32) return cudaErrorInvalidValue;
     const char* e = std::getenv("SLDA_PHI_SHAPE");  // read per launch (tests switch it per engine)
     const std::string v = e ? e : "";
-    if (v == "tma4x1") return launch_phi_tma_t<4, 1>(B, denom, zv, bhat, l8, q, row_begin, row_end, K_pad, l8_stride, beta, falpha, s);
-    if (v == "tma3x1") return launch_phi_tma_t<3, 1>(B, denom, zv, bhat, l8, q, row_begin, row_end, K_pad, l8_stride, beta, falpha, s);
-    if (v == "tma4x2") return launch_phi_tma_t<4, 2>(B, denom, zv, bhat, l8, q, row_begin, row_end, K_pad, l8_stride, beta, falpha, s);
-    if (v == "tma6x1") return launch_phi_tma_t<6, 1>(B, denom, zv, bhat, l8, q, row_begin, row_end, K_pad, l8_stride, beta, falpha, s);
+    // K_pad > 32768: the TMA warp-per-32-rows kernel (C5 K=50K phi alone 10.5 -> 9.4 ms; at K=10K
+    // it is slower, 3.3 vs 2.9 ms: DESIGN.md §6).  SLDA_PHI_SHAPE=tma forces it (tests).
+    if (v == "tma" || ((v.empty() || v == "default") && K_pad > 32768))
+        return launch_phi_tma_t<3, 4>(B, denom, zv, bhat, l8, q, row_begin, row_end, K_pad, l8_stride, beta, falpha, s);
     int shape = v == "16x8" ? 1 : v == "32x3" ? 2 : v == "64x2" ? 3 : v == "64x3" ? 4 : v == "32x4" ? 5 : 0;
     // Tile columns x pipeline stages, phi alone (ms, C3 / C5 K=50K): 16x8 4.91 / 17.9,
     // 32x3 4.68 / 14.8, 32x4 4.10 / 15.7, 32x6 5.88 / 16.2.

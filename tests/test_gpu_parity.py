@@ -298,8 +298,7 @@ VARIANT_CASES = ["c1", "long_docs", "empty_docs", "k_large", "nytimes_small", "k
 
 @pytest.mark.parametrize("variant", ["SLDA_SAMPLER=round", "SLDA_SAMPLER=quad512", "SLDA_SAMPLER=quad256",
                                      "SLDA_SAMPLER=global", "SLDA_PHI_SHAPE=16x8", "SLDA_PHI_SHAPE=32x3",
-                                     "SLDA_PHI_SHAPE=64x2", "SLDA_PHI_SHAPE=tma3x1", "SLDA_PHI_SHAPE=tma4x1",
-                                     "SLDA_PHI_SHAPE=tma4x2"])
+                                     "SLDA_PHI_SHAPE=64x2", "SLDA_PHI_SHAPE=tma"])
 @pytest.mark.parametrize("name", VARIANT_CASES)
 def test_kernel_variants_match_reference(name, variant, golden, monkeypatch):
     """Every sampler launch shape (quad-lane 256/512-thread CTAs, the round-based kernel, the
