@@ -54,6 +54,7 @@ def _rank_main(rank, world, case, to_parent, from_parent):
         toks = np.ascontiguousarray(toks.astype(np.uint32))
         cfg = slda.TrainConfig()
         cfg.num_topics = spec["K"]
+        cfg.tree_branch = 32 if spec["K"] <= 32768 else 41  # as the reference run (oracle/ref_shim.cpp)
         cfg.seed = spec["seed"]
         cfg.device = 0
         if spec.get("sampler") == "vanilla":
@@ -145,7 +146,8 @@ def test_peer_exchange_splits_large_counts(case, world):
         assert _assembled(many, world, it) == _assembled(one, 1, it), it
 
 
-@pytest.mark.parametrize("case,world", [("c1", 2), ("c1", 4), ("c1", 8), ("vanilla_c1", 2), ("u_k7_chunks", 3)])
+@pytest.mark.parametrize("case,world", [("c1", 2), ("c1", 4), ("c1", 8), ("vanilla_c1", 2), ("u_k7_chunks", 3),
+                                        ("ssc_lengths", 3), ("ssc_lengths_k60k", 2)])
 def test_peer_memory_exchange_matches_reference(golden, case, world):
     results = _run(case, world)
     fx = golden["cases"][case]

@@ -30,7 +30,8 @@ def streamed(spec, chunks):
 
 
 @pytest.mark.parametrize("name,chunks", [("c1", 4), ("shuffled", 3), ("empty_docs", 5), ("long_docs", 2),
-                                         ("given_topics", 3), ("vanilla_c1", 3), ("k_global_phi", 2)])
+                                         ("given_topics", 3), ("vanilla_c1", 3), ("k_global_phi", 2),
+                                         ("ssc_lengths", 3), ("ssc_lengths_k60k", 2)])
 def test_streamed_chunks_match_reference_every_iteration(name, chunks, golden):
     spec = CASES[name]
     fx = golden["cases"][name]
