@@ -8,6 +8,7 @@
 //
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o scripts/mb_rows scripts/microbench_rows.cu
 #include <cstdio>
+#include <cstdlib>
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -124,6 +125,10 @@ int main() {
     cudaMalloc(&a, bytes); cudaMalloc(&out, 4);
     cudaMemset(a, 1, bytes);
     const uint64_t nsect = bytes / 32;
+    if (getenv("MB_CEILING")) {  // the sampler's pattern: ~10-sector random rows, coalesced reads
+        for (int sect : {4, 8, 10, 12, 16, 32}) run("coop", coop, a, nsect, sect, out, 0);
+        return 0;
+    }
     for (int sect : {4, 8, 16}) {
         for (int smem : {0, 48 * 1024}) run("lane256", lane256, a, nsect, sect, out, smem);
         for (int smem : {0, 48 * 1024}) run("coop", coop, a, nsect, sect, out, smem);
