@@ -223,6 +223,9 @@ def main() -> None:
     ap.add_argument("--cpu-sample-tokens", type=int, default=16_000_000)
     ap.add_argument("--cpu-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--trace-iters", type=int, default=50,
+                    help="N=1: a fresh engine run this many iterations; iterations 1, 10 and N reported "
+                         "(K_d and E_t drift, SURVEY.md 8(d)); 0 disables")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
 
@@ -448,8 +451,27 @@ def main() -> None:
                                     "C_wk lists: reduce-scatter + all-gather), max over ranks"}
         if one_gpu:
             line["exchange"]["note"] = "all ranks shared one GPU (SLDA_BENCH_ONE_GPU=1): validation, not NVLink timing"
+    if world == 1 and args.trace_iters > 0:
+        # Per-iteration drift (report iterations 1, 10 and 50): a fresh engine from
+        # the same host tokens, device times of single iterations, outside the timed region.
+        model = None
+        m2 = create()
+        marks = sorted({1, 10, args.trace_iters} & set(range(1, args.trace_iters + 1)))
+        trace = {}
+        for i in range(1, args.trace_iters + 1):
+            m2.run_iteration(tc)
+            if i in marks:
+                kt2, inf2 = m2.kernel_times(), m2.info()
+                trace[str(i)] = {"ms": kt2["total_ms"], "sampler_ms": kt2["sampler_ms"],
+                                 "tokens_per_s": T_shard / (kt2["total_ms"] / 1e3),
+                                 "E_t": kt2["sampler_row_entries"] / max(1, T_shard),
+                                 "K_d": inf2["doc_topic_nnz"] / max(1, e - b)}
+        del m2
+        line["by_iteration"] = {"what": "one fresh engine, device time of single iterations (not the timed "
+                                        "region); E_t = mean C_dk row entries read per token, K_d = "
+                                        "mean_doc_topics after the iteration", "iterations": trace}
     if world == 1 and not args.no_cpu_baseline:
-        del model
+        model = None
         r = reference_run(cfg, args.cpu_sample_tokens, args.cpu_steps, 1, threads)
         line["cpu_baseline"] = {k: r[k] for k in ("value", "unit", "cores", "kind", "sample")}
     print(json.dumps(line), flush=True)
