@@ -16,7 +16,7 @@ NVFLAGS := $(ARCH) -O3 -lineinfo -fmad=false -std=c++17 -Xcompiler -fPIC,-Wall \
 CXXFLAGS := -O2 -std=c++20 -fPIC -Wall -Wextra -ffp-contract=off -Iinclude
 
 CU_SRCS := $(CSRC)/engine.cu $(CSRC)/sampler.cu $(CSRC)/ssc.cu $(CSRC)/mstep.cu $(CSRC)/setup.cu \
-           $(CSRC)/heldout.cu
+           $(CSRC)/heldout.cu $(CSRC)/zmove.cu
 CU_OBJS := $(patsubst $(CSRC)/%.cu,$(BUILD)/%.o,$(CU_SRCS))
 HOST_OBJS := $(BUILD)/host.o $(BUILD)/corpus_gen.o
 LIB     := $(PKG)/libsaberlda.so

@@ -432,7 +432,7 @@ def main() -> None:
                      "peak_source": peak_src, "algorithmic_bytes_per_launch": s_bytes,
                      "sampler_ms": kt["sampler_ms"], "iteration_achieved": it_achieved,
                      "iteration_frac": it_achieved / peak, "E_t": row_entries / max(1, T_shard)},
-        "kernels_ms": {k: kt[k] for k in ("reset_ms", "sampler_ms", "ssc_ms", "exchange_ms", "colsum_ms", "phi_ms",
+        "kernels_ms": {k: kt[k] for k in ("reset_ms", "sampler_ms", "zmove_ms", "ssc_ms", "exchange_ms", "colsum_ms", "phi_ms",
                                           "join_ms", "total_ms")},
         "sampler_shape": info["sampler_shape"],
         "mean_doc_topics": info["doc_topic_nnz"] / max(1, e - b),

@@ -26,7 +26,7 @@
 extern "C" {
 #endif
 
-#define SLDA_ABI_VERSION 4u
+#define SLDA_ABI_VERSION 5u
 
 enum {
     SLDA_OK = 0,
@@ -133,6 +133,7 @@ typedef struct slda_kernel_times {
     uint32_t launches;            /* kernels launched by the iteration */
     double exchange_ms;           /* world > 1: the sparse C_wk reduce-scatter + all-gather (0 on one GPU) */
     uint64_t exchange_bytes;      /* world > 1: bytes this rank read from the other ranks' memory */
+    double zmove_ms;              /* the sampler's topics from execution order to slots (zmove.cu) */
 } slda_kernel_times;
 
 /* ------------------------------------------------------------------ engine -- */

@@ -243,12 +243,19 @@ struct slda_engine {
     DevMem input_of_slot, ids;                    // only for non doc-major input / explicit ids
     DevMem assign_buf;                            // gather_assignments staging (allocated on first use)
     DevMem B, bhat, l8, q, colsum, denom, zv, counters;
+    // z transpose (zmove.cu; resident engines): the sampler's execution-order topics (zx), the
+    // two intermediate orders (zc: slot-range buckets, zf: 16384-slot tiles) and the static
+    // tables of the three passes.
+    DevMem zx, zc, zf, zsrc1, zdst1, zsrc2, zdst2, zloc;
+    bool zmove = false;
+    void build_zlayout();
 
     // Per-iteration phase events, a ring so async iterations can be profiled afterwards.
     static constexpr uint32_t kRing = 64;
     // 0 start, 1 reset, 2 sampler, 3 m-step start, 4 colsum, 5 phi, 6 end, 7 SSC end (side stream),
-    // 8 exchange end (world > 1: the sparse reduce-scatter + all-gather; == 3 on one GPU)
-    cudaEvent_t ring[kRing][9] = {};
+    // 8 exchange end (world > 1: the sparse reduce-scatter + all-gather; == 3 on one GPU),
+    // 9 z transposed to slots (zmove; == 2 without it)
+    cudaEvent_t ring[kRing][10] = {};
     cudaEvent_t* ev = ring[0];
     uint32_t ring_launches[kRing] = {};
     uint32_t slot = 0;
@@ -471,6 +478,8 @@ struct slda_engine {
         a.q = q.as<float>();
         a.ids = have_ids ? ids.as<uint64_t>() : nullptr;
         a.z = z.as<uint16_t>();
+        a.zx = zmove ? zx.as<uint16_t>() : nullptr;
+        a.zx_pos = nullptr;
         a.B = B.as<uint32_t>();
         a.seed = seed;
         a.id_base = id_base;
@@ -795,6 +804,81 @@ void slda_engine::build_state(const slda_corpus_view& cv, const slda_config& c, 
     CK(slda::launch_recount(tok.as<uint2>(), units.as<slda::Unit>(), n_units, z.as<uint16_t>(),
                             B.as<uint32_t>(), K_pad, rd, stream));
     phase("ssc + recount");
+    if (!streaming) build_zlayout();
+    phase("z transpose layout");
+}
+
+// The static tables of the z transpose (zmove.cu): stable radix sorts of positions by (chunk,
+// bucket), by bucket, by (chunk, tile) and by tile.  SLDA_ZMOVE=0 keeps the sampler's direct
+// z[slot] stores (A/B).
+void slda_engine::build_zlayout() {
+    const char* zm = std::getenv("SLDA_ZMOVE");
+    zmove = T > 0 && !(zm && std::string(zm) == "0");
+    if (!zmove) return;
+    auto nbits = [](uint64_t x) { int b = 1; while ((x >> b) != 0) ++b; return b; };
+    uint32_t shift = slda::kZTileLog2;  // level-1 buckets: at most 256 slot ranges
+    while (((T - 1) >> shift) >= 256) ++shift;
+    const int bucket_bits = nbits((T - 1) >> shift), chunk_bits = nbits((T - 1) >> slda::kZChunkLog2);
+    const int tile_bits = nbits((T - 1) >> slda::kZTileLog2);
+    DevMem iota, keys, keys_out, ord, inv, sorted, slot_of;
+    iota.alloc(T * 4, nullptr);
+    keys.alloc(T * 4, nullptr);
+    keys_out.alloc(T * 4, nullptr);
+    ord.alloc(T * 4, nullptr);
+    inv.alloc(T * 4, nullptr);
+    sorted.alloc(T * 4, nullptr);
+    CK(slda::launch_iota(iota.as<uint32_t>(), T, stream));
+    auto sort32 = [&](int bits, DevMem& vals_out) {
+        cub_call([&](void* t, size_t& b) {
+            return cub::DeviceRadixSort::SortPairs(t, b, keys.as<uint32_t>(), keys_out.as<uint32_t>(),
+                                                   iota.as<uint32_t>(), vals_out.as<uint32_t>(),
+                                                   static_cast<int64_t>(T), 0, bits, stream);
+        });
+    };
+    // Level 1: zc = execution positions grouped by bucket (stable); the permute visits each
+    // 16384-position chunk of zx bucket by bucket.
+    CK(slda::launch_zkey_u32(tok.as<uint2>(), nullptr, T, 1, shift, keys.as<uint32_t>(), stream));
+    sort32(bucket_bits, ord);
+    CK(slda::launch_zscatter_inv(ord.as<uint32_t>(), T, inv.as<uint32_t>(), stream));
+    CK(slda::launch_zkey_u32(tok.as<uint2>(), nullptr, T, 0, shift, keys.as<uint32_t>(), stream));
+    sort32(8 + chunk_bits, sorted);
+    zsrc1.alloc(T * 2, &device_bytes);
+    zdst1.alloc(T * 4, &device_bytes);
+    CK(slda::launch_ztables(sorted.as<uint32_t>(), inv.as<uint32_t>(), T, zsrc1.as<uint16_t>(),
+                            zdst1.as<uint32_t>(), stream));
+    // Level 2: zf = zc positions grouped by 16384-slot tile (stable); the permute visits each chunk
+    // of zc tile by tile.
+    slot_of.alloc(T * 4, nullptr);
+    CK(slda::launch_zslot_of(tok.as<uint2>(), ord.as<uint32_t>(), T, slot_of.as<uint32_t>(), stream));
+    CK(slda::launch_zkey_u32(nullptr, slot_of.as<uint32_t>(), T, 2, slda::kZTileLog2, keys.as<uint32_t>(), stream));
+    sort32(tile_bits, ord);
+    CK(slda::launch_zscatter_inv(ord.as<uint32_t>(), T, inv.as<uint32_t>(), stream));
+    zloc.alloc(T * 2, &device_bytes);
+    CK(slda::launch_zloc(slot_of.as<uint32_t>(), ord.as<uint32_t>(), T, zloc.as<uint16_t>(), stream));
+    keys.release();
+    keys_out.release();
+    ord.release();
+    {
+        DevMem k64, k64_out;
+        k64.alloc(T * 8, nullptr);
+        k64_out.alloc(T * 8, nullptr);
+        CK(slda::launch_zkey_u64(slot_of.as<uint32_t>(), T, slda::kZTileLog2, k64.as<unsigned long long>(), stream));
+        cub_call([&](void* t, size_t& b) {
+            return cub::DeviceRadixSort::SortPairs(t, b, k64.as<unsigned long long>(),
+                                                   k64_out.as<unsigned long long>(), iota.as<uint32_t>(),
+                                                   sorted.as<uint32_t>(), static_cast<int64_t>(T), 0,
+                                                   32 + chunk_bits, stream);
+        });
+        CK(cudaStreamSynchronize(stream));
+    }
+    zsrc2.alloc(T * 2, &device_bytes);
+    zdst2.alloc(T * 4, &device_bytes);
+    CK(slda::launch_ztables(sorted.as<uint32_t>(), inv.as<uint32_t>(), T, zsrc2.as<uint16_t>(),
+                            zdst2.as<uint32_t>(), stream));
+    CK(cudaStreamSynchronize(stream));
+    zx.alloc(T * 2, &device_bytes);
+    zc.alloc(T * 2, &device_bytes);
+    zf.alloc(T * 2, &device_bytes);
 }
 
 // ---- streaming mode (out-of-core chunks) ----
@@ -1083,6 +1167,7 @@ void slda_engine::enqueue_streaming_iteration() {
     CK(cudaEventRecord(ev_copy_end, copy));
     CK(cudaStreamWaitEvent(stream, ev_copy_end, 0));  // syncing the engine stream covers the copies
     CK(cudaEventRecord(ev[2], stream));
+    CK(cudaEventRecord(ev[9], stream));
     CK(cudaEventRecord(ev[7], stream));
     m_step();
     CK(cudaEventRecord(ev[6], stream));
@@ -1189,11 +1274,20 @@ void slda_engine::enqueue_iteration() {
     CK(slda::launch_sampler(a, n_units, stream));
     launches += n_units > 0;
     CK(cudaEventRecord(ev[2], stream));
+    if (zmove) {  // execution-order topics -> z by slot (zmove.cu)
+        CK(slda::launch_zpermute(zx.as<uint16_t>(), zsrc1.as<uint16_t>(), zdst1.as<uint32_t>(), T,
+                                 zc.as<uint16_t>(), stream));
+        CK(slda::launch_zpermute(zc.as<uint16_t>(), zsrc2.as<uint16_t>(), zdst2.as<uint32_t>(), T,
+                                 zf.as<uint16_t>(), stream));
+        CK(slda::launch_ztile(zf.as<uint16_t>(), zloc.as<uint16_t>(), T, z.as<uint16_t>(), stream));
+        launches += 3;
+    }
+    CK(cudaEventRecord(ev[9], stream));
     // The chunk's doc-topic rebuild (trainer.cpp:319-321) and the M-step both only read the
     // sampler's output (z / C_wk): SSC runs on the side stream, overlapped with colsum + phi,
     // and the iteration ends when both have.
     cudaStream_t ssc_stream = serial ? stream : side;
-    CK(cudaStreamWaitEvent(ssc_stream, ev[2], 0));
+    CK(cudaStreamWaitEvent(ssc_stream, ev[9], 0));
     ssc(ssc_stream);
     CK(cudaEventRecord(ev[7], ssc_stream));
     m_step();
@@ -1357,7 +1451,8 @@ int slda_get_kernel_times_avg(const slda_engine* e, uint32_t last_n, slda_kernel
             };
             t->reset_ms += ms(0, 1);
             t->sampler_ms += ms(1, 2);
-            t->ssc_ms += ms(2, 7);  // side stream, concurrent with colsum + phi
+            t->zmove_ms += ms(2, 9);
+            t->ssc_ms += ms(9, 7);  // side stream, concurrent with colsum + phi
             t->exchange_ms += ms(3, 8);
             t->colsum_ms += ms(8, 4);
             t->phi_ms += ms(4, 5);
@@ -1370,6 +1465,7 @@ int slda_get_kernel_times_avg(const slda_engine* e, uint32_t last_n, slda_kernel
         t->reset_ms /= n;
         t->sampler_ms /= n;
         t->ssc_ms /= n;
+        t->zmove_ms /= n;
         t->colsum_ms /= n;
         t->exchange_ms /= n;
         if (e->xbytes.p) {

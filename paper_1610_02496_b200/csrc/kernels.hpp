@@ -33,6 +33,11 @@ struct SamplerArgs {
     int shape;              // launch shape (sampler_shape_from_name); -1 = default by K
     uint32_t vanilla;       // SamplerKind::kVanilla: the O(K) dense-row draw (sampler.hpp:222-236)
     float alpha;            // f32(alpha), the vanilla draw's smoothing (trainer.cpp:283)
+    // z staging (resident engines): the new topic of execution position i goes to
+    // zx[zx_pos ? zx_pos[i] : i] instead of z[slot] -- coalesced stores; launch_zmove then
+    // brings the topics to z by slot (zmove.cu).  Null: z[slot] directly (streaming chunks).
+    uint16_t* zx;
+    const uint32_t* zx_pos;
 };
 
 // Sampler launch shapes (sampler.cu launch_sampler); -1 = by phi row size.
@@ -42,6 +47,26 @@ int sampler_shape_from_name(const char* name);
 int sampler_shape(const SamplerArgs& a);
 
 cudaError_t launch_sampler(const SamplerArgs& a, uint32_t n_units, cudaStream_t s);
+
+// ---- z transpose (zmove.cu): execution order -> slot order in three coalesced passes ---------
+constexpr uint32_t kZChunkLog2 = 14;  // permute chunk: 16384 entries (32 KB of topics in smem)
+constexpr uint32_t kZTileLog2 = 14;   // final tile: 16384 slots
+// out[dst[k]] = src[chunk(k) base + srcl[k]] for every position k: each CTA stages a chunk of
+// src in shared memory and writes it in a static order whose destinations form runs.
+cudaError_t launch_zpermute(const uint16_t* src, const uint16_t* srcl, const uint32_t* dst, uint64_t T,
+                            uint16_t* out, cudaStream_t s);
+// z[tile base + loc[m]] = zf[m] per 16384-slot tile, through shared memory.
+cudaError_t launch_ztile(const uint16_t* zf, const uint16_t* loc, uint64_t T, uint16_t* z, cudaStream_t s);
+// Setup helpers for the static tables (engine.cu build_zlayout).
+cudaError_t launch_zkey_u32(const uint2* tok, const uint32_t* ord, uint64_t T, uint32_t mode, uint32_t shift,
+                            uint32_t* key, cudaStream_t s);
+cudaError_t launch_zkey_u64(const uint32_t* slot_of, uint64_t T, uint32_t tile_shift, unsigned long long* key,
+                            cudaStream_t s);
+cudaError_t launch_zscatter_inv(const uint32_t* ord, uint64_t T, uint32_t* inv, cudaStream_t s);
+cudaError_t launch_ztables(const uint32_t* sorted, const uint32_t* inv, uint64_t T, uint16_t* srcl, uint32_t* dst,
+                           cudaStream_t s);
+cudaError_t launch_zslot_of(const uint2* tok, const uint32_t* ord, uint64_t T, uint32_t* slot_of, cudaStream_t s);
+cudaError_t launch_zloc(const uint32_t* slot_of, const uint32_t* ord, uint64_t T, uint16_t* loc, cudaStream_t s);
 
 struct SscArgs {
     const uint16_t* z;          // topics by slot (doc-grouped)

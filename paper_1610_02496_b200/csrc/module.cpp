@@ -69,6 +69,7 @@ py::dict kernel_times_dict(const slda_kernel_times& t) {
     d["launches"] = t.launches;
     d["exchange_ms"] = t.exchange_ms;
     d["exchange_bytes"] = t.exchange_bytes;
+    d["zmove_ms"] = t.zmove_ms;
     return d;
 }
 

@@ -21,6 +21,15 @@ namespace slda {
 
 // Used where a 512-thread quad-lane CTA pair does not fit an SM but the phi row still fits shared
 // memory (17.5K < K_pad <~ 45K).
+// The new topic of execution position `exec` (slot `slot`): staged in execution order when the
+// engine transposes afterwards (zmove.cu: full-sector stores), else straight to z by slot.
+__device__ __forceinline__ void store_topic(const SamplerArgs& a, uint32_t exec, uint32_t slot, uint32_t topic) {
+    if (a.zx)
+        a.zx[a.zx_pos ? __ldg(a.zx_pos + exec) : exec] = static_cast<uint16_t>(topic);
+    else
+        a.z[slot] = static_cast<uint16_t>(topic);
+}
+
 template <int NT, int G, int MINB>
 __global__ void __launch_bounds__(NT, MINB) sampler_kernel(SamplerArgs a) {
     using St = Stage<G>;
@@ -167,7 +176,7 @@ __global__ void __launch_bounds__(NT, MINB) sampler_kernel(SamplerArgs a) {
             }
         }
         if (active) {
-            a.z[t.y] = static_cast<uint16_t>(topic);
+            store_topic(a, unit.offset + i, t.y, topic);
             atomicAdd(brow + topic, 1u);
         }
     }
@@ -328,7 +337,7 @@ __global__ void __launch_bounds__(NT, MINB) sampler_quad_kernel(SamplerArgs a) {
                 const uint32_t k = tree_search<false>(x, s_l8, a.n_l8, s_bhat);
                 topic = k < a.K ? k : a.K - 1;
             }
-            a.z[tk.y] = static_cast<uint16_t>(topic);
+            store_topic(a, unit.offset + base + lane, tk.y, topic);
             atomicAdd(brow + topic, 1u);
         }
         uint32_t nb = 0;
@@ -522,7 +531,7 @@ __global__ void __launch_bounds__(NT, MINB) sampler_quad_pf_kernel(SamplerArgs a
                 const uint32_t k = tree_search<kGlobalPhi>(x, s_l8, a.n_l8, s_bhat);
                 topic = k < a.K ? k : a.K - 1;
             }
-            a.z[tk.y] = static_cast<uint16_t>(topic);
+            store_topic(a, unit.offset + base + lane, tk.y, topic);
             atomicAdd(a.B + static_cast<size_t>(v) * a.K_pad + topic, 1u);
         }
         if (kPrefetchNext) {
@@ -661,7 +670,7 @@ __global__ void __launch_bounds__(NT) sampler_vanilla_kernel(SamplerArgs a) {
                 }
             }
         }
-        a.z[t.y] = static_cast<uint16_t>(topic);
+        store_topic(a, unit.offset + i, t.y, topic);
         atomicAdd(brow + topic, 1u);
     }
     if (a.row_entries) {

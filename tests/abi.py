@@ -49,7 +49,8 @@ class KernelTimes(C.Structure):
     _fields_ = [("reset_ms", C.c_double), ("sampler_ms", C.c_double), ("ssc_ms", C.c_double),
                 ("colsum_ms", C.c_double), ("phi_ms", C.c_double), ("join_ms", C.c_double),
                 ("total_ms", C.c_double), ("sampler_row_entries", C.c_uint64), ("launches", C.c_uint32),
-                ("exchange_ms", C.c_double), ("exchange_bytes", C.c_uint64)]
+                ("exchange_ms", C.c_double), ("exchange_bytes", C.c_uint64),
+                ("zmove_ms", C.c_double)]
 
 
 class GenParams(C.Structure):

@@ -16,7 +16,7 @@ def test_library_exports_every_declared_symbol():
     assert len(syms) >= 25
     missing = [s for s in syms if not hasattr(lib, s)]
     assert missing == []
-    assert lib.slda_abi_version() == 4
+    assert lib.slda_abi_version() == 5
 
 
 def test_shard_bounds_follow_chunk_boundaries():
