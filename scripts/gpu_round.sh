@@ -16,6 +16,6 @@ echo ncu-list rc=$?
 timeout 1200 ncu --set full --clock-control none --import-source on -k regex:"sampler" -s 12 -c 1 \
     -o gpurun_out/prof_sampler_c3_${TAG} python scripts/profile_run.py --config c3 --iters 14 > gpurun_out/prof_sampler_c3_${TAG}.log 2>&1
 echo ncu-sampler rc=$?
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:"ssc_warp|phi_kernel|zhist|denom" -s 48 -c 4 \
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"ssc_warp|phi_kernel|zhist|denom|zpermute|ztile" -s 72 -c 7 \
     -o gpurun_out/prof_sscphi_c3_${TAG} python scripts/profile_run.py --config c3 --iters 14 > /dev/null 2>&1
 echo ncu-sscphi rc=$?
