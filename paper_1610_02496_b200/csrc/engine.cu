@@ -248,7 +248,7 @@ struct slda_engine {
     // tables of the three passes.
     DevMem zx, zc, zf, zsrc1, zdst1, zsrc2, zdst2, zloc;
     bool zmove = false;
-    void build_zlayout();
+    void build_zlayout(bool trace = false);
 
     // Per-iteration phase events, a ring so async iterations can be profiled afterwards.
     static constexpr uint32_t kRing = 64;
@@ -804,81 +804,55 @@ void slda_engine::build_state(const slda_corpus_view& cv, const slda_config& c, 
     CK(slda::launch_recount(tok.as<uint2>(), units.as<slda::Unit>(), n_units, z.as<uint16_t>(),
                             B.as<uint32_t>(), K_pad, rd, stream));
     phase("ssc + recount");
-    if (!streaming) build_zlayout();
+    if (!streaming) build_zlayout(trace);
     phase("z transpose layout");
 }
 
-// The static tables of the z transpose (zmove.cu): stable radix sorts of positions by (chunk,
-// bucket), by bucket, by (chunk, tile) and by tile.  SLDA_ZMOVE=0 keeps the sampler's direct
-// z[slot] stores (A/B).
-void slda_engine::build_zlayout() {
+// The static tables of the z transpose (zmove.cu): per level, (key, chunk) counts -> their
+// exclusive scan (each run's first destination) -> the stable per-chunk ranking that writes the
+// tables.  SLDA_ZMOVE=0 keeps the sampler's direct z[slot] stores (A/B).
+void slda_engine::build_zlayout(bool trace) {
     const char* zm = std::getenv("SLDA_ZMOVE");
     zmove = T > 0 && !(zm && std::string(zm) == "0");
     if (!zmove) return;
-    auto nbits = [](uint64_t x) { int b = 1; while ((x >> b) != 0) ++b; return b; };
+    auto t_last = std::chrono::steady_clock::now();
+    auto phase = [&](const char* name) {
+        if (!trace) return;
+        CK(cudaStreamSynchronize(stream));
+        const auto now = std::chrono::steady_clock::now();
+        std::fprintf(stderr, "[slda setup]   z %-24s %8.1f ms\n", name,
+                     std::chrono::duration<double, std::milli>(now - t_last).count());
+        t_last = now;
+    };
     uint32_t shift = slda::kZTileLog2;  // level-1 buckets: at most 256 slot ranges
     while (((T - 1) >> shift) >= 256) ++shift;
-    const int bucket_bits = nbits((T - 1) >> shift), chunk_bits = nbits((T - 1) >> slda::kZChunkLog2);
-    const int tile_bits = nbits((T - 1) >> slda::kZTileLog2);
-    DevMem iota, keys, keys_out, ord, inv, sorted, slot_of;
-    iota.alloc(T * 4, nullptr);
-    keys.alloc(T * 4, nullptr);
-    keys_out.alloc(T * 4, nullptr);
-    ord.alloc(T * 4, nullptr);
-    inv.alloc(T * 4, nullptr);
-    sorted.alloc(T * 4, nullptr);
-    CK(slda::launch_iota(iota.as<uint32_t>(), T, stream));
-    auto sort32 = [&](int bits, DevMem& vals_out) {
-        cub_call([&](void* t, size_t& b) {
-            return cub::DeviceRadixSort::SortPairs(t, b, keys.as<uint32_t>(), keys_out.as<uint32_t>(),
-                                                   iota.as<uint32_t>(), vals_out.as<uint32_t>(),
-                                                   static_cast<int64_t>(T), 0, bits, stream);
-        });
-    };
-    // Level 1: zc = execution positions grouped by bucket (stable); the permute visits each
-    // 16384-position chunk of zx bucket by bucket.
-    CK(slda::launch_zkey_u32(tok.as<uint2>(), nullptr, T, 1, shift, keys.as<uint32_t>(), stream));
-    sort32(bucket_bits, ord);
-    CK(slda::launch_zscatter_inv(ord.as<uint32_t>(), T, inv.as<uint32_t>(), stream));
-    CK(slda::launch_zkey_u32(tok.as<uint2>(), nullptr, T, 0, shift, keys.as<uint32_t>(), stream));
-    sort32(8 + chunk_bits, sorted);
     zsrc1.alloc(T * 2, &device_bytes);
     zdst1.alloc(T * 4, &device_bytes);
-    CK(slda::launch_ztables(sorted.as<uint32_t>(), inv.as<uint32_t>(), T, zsrc1.as<uint16_t>(),
-                            zdst1.as<uint32_t>(), stream));
-    // Level 2: zf = zc positions grouped by 16384-slot tile (stable); the permute visits each chunk
-    // of zc tile by tile.
-    slot_of.alloc(T * 4, nullptr);
-    CK(slda::launch_zslot_of(tok.as<uint2>(), ord.as<uint32_t>(), T, slot_of.as<uint32_t>(), stream));
-    CK(slda::launch_zkey_u32(nullptr, slot_of.as<uint32_t>(), T, 2, slda::kZTileLog2, keys.as<uint32_t>(), stream));
-    sort32(tile_bits, ord);
-    CK(slda::launch_zscatter_inv(ord.as<uint32_t>(), T, inv.as<uint32_t>(), stream));
-    zloc.alloc(T * 2, &device_bytes);
-    CK(slda::launch_zloc(slot_of.as<uint32_t>(), ord.as<uint32_t>(), T, zloc.as<uint16_t>(), stream));
-    keys.release();
-    keys_out.release();
-    ord.release();
-    {
-        DevMem k64, k64_out;
-        k64.alloc(T * 8, nullptr);
-        k64_out.alloc(T * 8, nullptr);
-        CK(slda::launch_zkey_u64(slot_of.as<uint32_t>(), T, slda::kZTileLog2, k64.as<unsigned long long>(), stream));
-        cub_call([&](void* t, size_t& b) {
-            return cub::DeviceRadixSort::SortPairs(t, b, k64.as<unsigned long long>(),
-                                                   k64_out.as<unsigned long long>(), iota.as<uint32_t>(),
-                                                   sorted.as<uint32_t>(), static_cast<int64_t>(T), 0,
-                                                   32 + chunk_bits, stream);
-        });
-        CK(cudaStreamSynchronize(stream));
-    }
     zsrc2.alloc(T * 2, &device_bytes);
     zdst2.alloc(T * 4, &device_bytes);
-    CK(slda::launch_ztables(sorted.as<uint32_t>(), inv.as<uint32_t>(), T, zsrc2.as<uint16_t>(),
-                            zdst2.as<uint32_t>(), stream));
+    zloc.alloc(T * 2, &device_bytes);
+    DevMem slot_of, cnt, off;
+    slot_of.alloc(T * 4, nullptr);  // slot of every zc position (level 1 writes, level 2 reads)
+    for (uint32_t level = 1; level <= 2; ++level) {
+        const size_t flat = slda::zlayout_flat_size(T, shift, level);
+        cnt.alloc(flat * 4, nullptr);
+        off.alloc(flat * 4, nullptr);
+        CK(slda::launch_zlayout_count(tok.as<uint2>(), slot_of.as<uint32_t>(), T, shift, level, cnt.as<uint32_t>(),
+                                      flat, stream));
+        exclusive_sum(cnt.as<uint32_t>(), off.as<uint32_t>(), flat);
+        CK(slda::launch_zlayout_emit(tok.as<uint2>(), slot_of.as<uint32_t>(), T, shift, level, off.as<uint32_t>(),
+                                     level == 1 ? zsrc1.as<uint16_t>() : zsrc2.as<uint16_t>(),
+                                     level == 1 ? zdst1.as<uint32_t>() : zdst2.as<uint32_t>(),
+                                     slot_of.as<uint32_t>(), zloc.as<uint16_t>(), stream));
+        off.release();
+        cnt.release();
+        phase(level == 1 ? "level 1 tables" : "level 2 tables");
+    }
     CK(cudaStreamSynchronize(stream));
     zx.alloc(T * 2, &device_bytes);
     zc.alloc(T * 2, &device_bytes);
     zf.alloc(T * 2, &device_bytes);
+    phase("zx/zc/zf alloc");
 }
 
 // ---- streaming mode (out-of-core chunks) ----

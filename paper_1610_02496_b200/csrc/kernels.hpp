@@ -57,16 +57,15 @@ cudaError_t launch_zpermute(const uint16_t* src, const uint16_t* srcl, const uin
                             uint16_t* out, cudaStream_t s);
 // z[tile base + loc[m]] = zf[m] per 16384-slot tile, through shared memory.
 cudaError_t launch_ztile(const uint16_t* zf, const uint16_t* loc, uint64_t T, uint16_t* z, cudaStream_t s);
-// Setup helpers for the static tables (engine.cu build_zlayout).
-cudaError_t launch_zkey_u32(const uint2* tok, const uint32_t* ord, uint64_t T, uint32_t mode, uint32_t shift,
-                            uint32_t* key, cudaStream_t s);
-cudaError_t launch_zkey_u64(const uint32_t* slot_of, uint64_t T, uint32_t tile_shift, unsigned long long* key,
-                            cudaStream_t s);
-cudaError_t launch_zscatter_inv(const uint32_t* ord, uint64_t T, uint32_t* inv, cudaStream_t s);
-cudaError_t launch_ztables(const uint32_t* sorted, const uint32_t* inv, uint64_t T, uint16_t* srcl, uint32_t* dst,
-                           cudaStream_t s);
-cudaError_t launch_zslot_of(const uint2* tok, const uint32_t* ord, uint64_t T, uint32_t* slot_of, cudaStream_t s);
-cudaError_t launch_zloc(const uint32_t* slot_of, const uint32_t* ord, uint64_t T, uint16_t* loc, cudaStream_t s);
+// Setup of the static tables (two levels): per-(key, chunk) counts into a flat array in
+// destination order (its exclusive scan gives each run's first destination), then the stable
+// per-chunk ranking that writes srcl / dst and slot_of (level 1) or the tile-local slots (level 2).
+size_t zlayout_flat_size(uint64_t T, uint32_t shift, uint32_t level);
+cudaError_t launch_zlayout_count(const uint2* tok, const uint32_t* slot_of, uint64_t T, uint32_t shift,
+                                 uint32_t level, uint32_t* cnt, size_t flat, cudaStream_t s);
+cudaError_t launch_zlayout_emit(const uint2* tok, const uint32_t* slot_of, uint64_t T, uint32_t shift, uint32_t level,
+                                const uint32_t* off, uint16_t* srcl, uint32_t* dst, uint32_t* slot_of_out,
+                                uint16_t* loc_out, cudaStream_t s);
 
 struct SscArgs {
     const uint16_t* z;          // topics by slot (doc-grouped)

@@ -71,72 +71,152 @@ cudaError_t launch_ztile(const uint16_t* zf, const uint16_t* loc, uint64_t T, ui
 }
 
 // ---- setup: the static tables --------------------------------------------------------------
-#define ZFOR(i) for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < T; \
-                     i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+// Both permutes are per-chunk stable counting sorts by a small key, so the tables come from two
+// counting passes per level instead of global radix sorts (C3: 9 ms instead of ~150 ms):
+//   level 1: chunk c of the execution order, key = slot bucket (slot >> shift, <= 256 keys);
+//            destinations (zc) are bucket-major, execution order inside a bucket;
+//   level 2: chunk c of zc (inside one bucket: buckets are 2^shift >= 2^14 positions), key = the
+//            slot's tile relative to the bucket's first tile (< 2^(shift-14) <= 1024 keys);
+//            destinations (zf) are tile-major, zc order inside a tile.
+// zhist_kernel counts (key, chunk) into a flat array whose order is the destination order, so
+// its exclusive scan is every (key, chunk) run's first destination; zemit_kernel ranks each
+// chunk's positions stably by key (warp segments walked in order, __match_any_sync peers) and
+// writes srcl / dst, plus slot_of at zc (level 1) or the tile-local slot at zf (level 2).
+struct ZKeys {
+    const uint2* tok;        // level 1: execution-order token records (.y = slot)
+    const uint32_t* slot_of; // level 2: slot of every zc position
+    uint64_t T;
+    uint32_t shift;          // bucket = slot >> shift
+    uint32_t level;          // 1 or 2
+    uint32_t R;              // keys per chunk
+    uint32_t nchunks;
+};
+__device__ __forceinline__ uint32_t zkey(const ZKeys& k, uint64_t p) {
+    if (k.level == 1) return __ldg(&k.tok[p].y) >> k.shift;
+    return (__ldg(k.slot_of + p) >> kZTileLog2) - (static_cast<uint32_t>(p >> k.shift) << (k.shift - kZTileLog2));
+}
+// Flat (key, chunk) index in destination order.
+__device__ __forceinline__ size_t zflat(const ZKeys& k, uint32_t key, uint32_t c) {
+    if (k.level == 1) return static_cast<size_t>(key) * k.nchunks + c;
+    const uint32_t cpb = k.R, b = c / cpb;  // chunks per bucket == tiles per bucket
+    return (static_cast<size_t>(b) * cpb + key) * cpb + (c - b * cpb);
+}
 
-// mode 0: key = chunk(i) << 8 | (slot(i) >> shift)   (level-1 permute order)
-// mode 1: key = slot(i) >> shift                    (level-1 destination order)
-// mode 2: key = ord[i] >> shift (ord = the slots of the zc positions: level-2 destination order)
-__global__ void zkey_u32_kernel(const uint2* __restrict__ tok, const uint32_t* __restrict__ ord, uint64_t T,
-                                uint32_t mode, uint32_t shift, uint32_t* __restrict__ key) {
-    ZFOR(i) {
-        const uint32_t b = (mode == 2 ? ord[i] : tok[i].y) >> shift;
-        key[i] = mode == 0 ? static_cast<uint32_t>((i >> kZChunkLog2) << 8) | b : b;
+constexpr uint32_t kZWarps = 16;
+constexpr uint32_t kZMaxKeys = 1024;
+
+__global__ void __launch_bounds__(512) zhist_count_kernel(ZKeys k, uint32_t* __restrict__ cnt) {
+    __shared__ uint32_t h[kZMaxKeys];
+    const uint32_t c = blockIdx.x;
+    for (uint32_t i = threadIdx.x; i < k.R; i += blockDim.x) h[i] = 0;
+    __syncthreads();
+    const uint64_t base = static_cast<uint64_t>(c) * kZChunk;
+    const uint32_t n = static_cast<uint32_t>(min(static_cast<uint64_t>(kZChunk), k.T - base));
+    for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) atomicAdd(h + zkey(k, base + i), 1u);
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < k.R; i += blockDim.x) cnt[zflat(k, i, c)] = h[i];
+}
+
+__global__ void __launch_bounds__(512) zemit_kernel(ZKeys k, const uint32_t* __restrict__ off,
+                                                    uint16_t* __restrict__ srcl, uint32_t* __restrict__ dst,
+                                                    uint32_t* __restrict__ slot_of_out, uint16_t* __restrict__ loc_out) {
+    __shared__ uint16_t h[kZWarps * kZMaxKeys];  // per warp segment and key: count, then next local index
+    __shared__ uint16_t start[kZMaxKeys];        // first local index of each key in the chunk
+    const uint32_t c = blockIdx.x, w = threadIdx.x >> 5, lane = threadIdx.x & 31u, R = k.R;
+    const uint64_t base = static_cast<uint64_t>(c) * kZChunk;
+    const uint32_t n = static_cast<uint32_t>(min(static_cast<uint64_t>(kZChunk), k.T - base));
+    constexpr uint32_t kSeg = kZChunk / kZWarps;
+    const uint32_t s0 = w * kSeg, s1 = min(n, s0 + kSeg);
+    for (uint32_t i = threadIdx.x; i < kZWarps * R; i += blockDim.x) h[i] = 0;
+    __syncthreads();
+    uint16_t* hw = h + w * R;
+    const uint32_t lt = (1u << lane) - 1u;
+    for (uint32_t p0 = s0; p0 < s1; p0 += 32) {
+        const uint32_t p = p0 + lane;
+        const uint32_t key = p < s1 ? zkey(k, base + p) : 0xFFFFFFFFu;
+        const uint32_t peers = __match_any_sync(0xffffffffu, key);
+        if (key != 0xFFFFFFFFu && (peers & lt) == 0) hw[key] = static_cast<uint16_t>(hw[key] + __popc(peers));
+        __syncwarp();
+    }
+    __syncthreads();
+    // Per key: warps' counts -> exclusive offsets over the warps; key totals -> chunk starts.
+    __shared__ uint32_t tot[kZMaxKeys];
+    for (uint32_t key = threadIdx.x; key < R; key += blockDim.x) {
+        uint32_t run = 0;
+        for (uint32_t ww = 0; ww < kZWarps; ++ww) {
+            const uint32_t t = h[ww * R + key];
+            h[ww * R + key] = static_cast<uint16_t>(run);
+            run += t;
+        }
+        tot[key] = run;
+    }
+    __syncthreads();
+    if (w == 0) {  // exclusive scan of the R <= 1024 key totals by one warp (contiguous lane ranges)
+        const uint32_t per = (R + 31u) / 32u, a = min(R, lane * per), b = min(R, a + per);
+        uint32_t mine = 0;
+        for (uint32_t i = a; i < b; ++i) mine += tot[i];
+        uint32_t incl = mine;
+        for (uint32_t o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += y;
+        }
+        uint32_t run = incl - mine;
+        for (uint32_t i = a; i < b; ++i) {
+            start[i] = static_cast<uint16_t>(run);
+            run += tot[i];
+        }
+    }
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < kZWarps * R; i += blockDim.x)
+        h[i] = static_cast<uint16_t>(h[i] + start[i % R]);
+    __syncthreads();
+    for (uint32_t p0 = s0; p0 < s1; p0 += 32) {
+        const uint32_t p = p0 + lane;
+        const bool v = p < s1;
+        const uint32_t key = v ? zkey(k, base + p) : 0xFFFFFFFFu;
+        const uint32_t peers = __match_any_sync(0xffffffffu, key);
+        uint32_t local = 0;
+        if (v) local = hw[key] + __popc(peers & lt);
+        __syncwarp();
+        if (v && (peers & lt) == 0) hw[key] = static_cast<uint16_t>(hw[key] + __popc(peers));
+        __syncwarp();
+        if (v) {
+            const uint64_t kk = base + local;
+            const uint32_t d = __ldg(off + zflat(k, key, c)) + (local - start[key]);
+            srcl[kk] = static_cast<uint16_t>(p);
+            dst[kk] = d;
+            if (k.level == 1) slot_of_out[d] = __ldg(&k.tok[base + p].y);
+            else loc_out[d] = static_cast<uint16_t>(__ldg(k.slot_of + base + p) & (kZTile - 1u));
+        }
     }
 }
-// level 2 permute order: chunk(j) << 32 | tile(slot_of[j])
-__global__ void zkey_u64_kernel(const uint32_t* __restrict__ slot_of, uint64_t T, uint32_t tile_shift,
-                                unsigned long long* __restrict__ key) {
-    ZFOR(j) key[j] = (static_cast<unsigned long long>(j >> kZChunkLog2) << 32) | (slot_of[j] >> tile_shift);
-}
-__global__ void zscatter_inv_kernel(const uint32_t* __restrict__ ord, uint64_t T, uint32_t* __restrict__ inv) {
-    ZFOR(j) inv[ord[j]] = static_cast<uint32_t>(j);
-}
-// permute position k (chunk-major, sorted inside its chunk): its source inside the chunk and its
-// destination (inv = position of the source in the destination order)
-__global__ void ztables_kernel(const uint32_t* __restrict__ sorted, const uint32_t* __restrict__ inv, uint64_t T,
-                               uint16_t* __restrict__ srcl, uint32_t* __restrict__ dst) {
-    ZFOR(k) {
-        const uint32_t from = sorted[k];
-        srcl[k] = static_cast<uint16_t>(from & (kZChunk - 1u));
-        dst[k] = inv[from];
-    }
-}
-__global__ void zslot_of_kernel(const uint2* __restrict__ tok, const uint32_t* __restrict__ ord, uint64_t T,
-                                uint32_t* __restrict__ slot_of) {
-    ZFOR(j) slot_of[j] = tok[ord[j]].y;
-}
-__global__ void zloc_kernel(const uint32_t* __restrict__ slot_of, const uint32_t* __restrict__ ord, uint64_t T,
-                            uint16_t* __restrict__ loc) {
-    ZFOR(m) loc[m] = static_cast<uint16_t>(slot_of[ord[m]] & (kZTile - 1u));
-}
-#undef ZFOR
 
-cudaError_t launch_zkey_u32(const uint2* tok, const uint32_t* ord, uint64_t T, uint32_t mode, uint32_t shift,
-                            uint32_t* key, cudaStream_t s) {
-    if (T) zkey_u32_kernel<<<148 * 8, 256, 0, s>>>(tok, ord, T, mode, shift, key);
+size_t zlayout_flat_size(uint64_t T, uint32_t shift, uint32_t level) {
+    const uint64_t nchunks = (T + kZChunk - 1) / kZChunk, nbuckets = ((T - 1) >> shift) + 1;
+    const uint64_t cpb = 1ull << (shift - kZTileLog2);
+    return level == 1 ? nbuckets * nchunks : nbuckets * cpb * cpb;
+}
+
+cudaError_t launch_zlayout_count(const uint2* tok, const uint32_t* slot_of, uint64_t T, uint32_t shift,
+                                 uint32_t level, uint32_t* cnt, size_t flat, cudaStream_t s) {
+    if (!T) return cudaSuccess;
+    const uint32_t nchunks = static_cast<uint32_t>((T + kZChunk - 1) / kZChunk);
+    const uint32_t R = level == 1 ? static_cast<uint32_t>(((T - 1) >> shift) + 1) : 1u << (shift - kZTileLog2);
+    if (R > kZMaxKeys || shift < kZTileLog2) return cudaErrorInvalidValue;
+    if (const cudaError_t e = cudaMemsetAsync(cnt, 0, flat * 4, s); e != cudaSuccess) return e;
+    zhist_count_kernel<<<nchunks, 512, 0, s>>>(ZKeys{tok, slot_of, T, shift, level, R, nchunks}, cnt);
     return cudaGetLastError();
 }
-cudaError_t launch_zkey_u64(const uint32_t* slot_of, uint64_t T, uint32_t tile_shift, unsigned long long* key,
-                            cudaStream_t s) {
-    if (T) zkey_u64_kernel<<<148 * 8, 256, 0, s>>>(slot_of, T, tile_shift, key);
-    return cudaGetLastError();
-}
-cudaError_t launch_zscatter_inv(const uint32_t* ord, uint64_t T, uint32_t* inv, cudaStream_t s) {
-    if (T) zscatter_inv_kernel<<<148 * 8, 256, 0, s>>>(ord, T, inv);
-    return cudaGetLastError();
-}
-cudaError_t launch_ztables(const uint32_t* sorted, const uint32_t* inv, uint64_t T, uint16_t* srcl, uint32_t* dst,
-                           cudaStream_t s) {
-    if (T) ztables_kernel<<<148 * 8, 256, 0, s>>>(sorted, inv, T, srcl, dst);
-    return cudaGetLastError();
-}
-cudaError_t launch_zslot_of(const uint2* tok, const uint32_t* ord, uint64_t T, uint32_t* slot_of, cudaStream_t s) {
-    if (T) zslot_of_kernel<<<148 * 8, 256, 0, s>>>(tok, ord, T, slot_of);
-    return cudaGetLastError();
-}
-cudaError_t launch_zloc(const uint32_t* slot_of, const uint32_t* ord, uint64_t T, uint16_t* loc, cudaStream_t s) {
-    if (T) zloc_kernel<<<148 * 8, 256, 0, s>>>(slot_of, ord, T, loc);
+
+cudaError_t launch_zlayout_emit(const uint2* tok, const uint32_t* slot_of, uint64_t T, uint32_t shift, uint32_t level,
+                                const uint32_t* off, uint16_t* srcl, uint32_t* dst, uint32_t* slot_of_out,
+                                uint16_t* loc_out, cudaStream_t s) {
+    if (!T) return cudaSuccess;
+    const uint32_t nchunks = static_cast<uint32_t>((T + kZChunk - 1) / kZChunk);
+    const uint32_t R = level == 1 ? static_cast<uint32_t>(((T - 1) >> shift) + 1) : 1u << (shift - kZTileLog2);
+    if (R > kZMaxKeys || shift < kZTileLog2) return cudaErrorInvalidValue;
+    zemit_kernel<<<nchunks, 512, 0, s>>>(ZKeys{tok, slot_of, T, shift, level, R, nchunks}, off, srcl, dst,
+                                         slot_of_out, loc_out);
     return cudaGetLastError();
 }
 
