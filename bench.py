@@ -123,11 +123,11 @@ def iteration_bytes(T: int, row_entries: int, K: int, V: int, D: int, nnz: int, 
     """Whole iteration: sampler + SSC + recount + the M-step.  The M-step moves
     C_wk in (4 V K) and phi + the L8 level out (4.5 V K): SURVEY's canonical phi + L4 write
     (12 V K) counted an L4 array this engine no longer stores.  The z transpose
-    (zmove.cu: the sampler's execution-order topics to slots) adds 26 B per token."""
+    (zmove.cu: the sampler's execution-order topics to slots) adds 22 B per token."""
     ssc = T * 6 + 4 * nnz + 8 * D
     recount = 2 * T + 4 * V * K
     mstep = 4 * V * K + (9 * V * K) // 2
-    zmove = 26 * T
+    zmove = 22 * T
     return sampler_bytes(T, row_entries, K, units) + ssc + recount + mstep + zmove
 
 

@@ -246,7 +246,9 @@ struct slda_engine {
     // z transpose (zmove.cu; resident engines): the sampler's execution-order topics (zx), the
     // two intermediate orders (zc: slot-range buckets, zf: 16384-slot tiles) and the static
     // tables of the three passes.
-    DevMem zx, zc, zf, zsrc1, zdst1, zsrc2, zdst2, zloc;
+    DevMem zx, zc, zf, zsk1, zsk2, zloc;
+    DevMem zbase1, zbase2;                  // per-chunk run tables of the two permutes
+    uint32_t zruns1 = 0, zruns2 = 0;        // runs (keys) per chunk
     bool zmove = false;
     void build_zlayout(bool trace = false);
 
@@ -826,11 +828,14 @@ void slda_engine::build_zlayout(bool trace) {
     };
     uint32_t shift = slda::kZTileLog2;  // level-1 buckets: at most 256 slot ranges
     while (((T - 1) >> shift) >= 256) ++shift;
-    zsrc1.alloc(T * 2, &device_bytes);
-    zdst1.alloc(T * 4, &device_bytes);
-    zsrc2.alloc(T * 2, &device_bytes);
-    zdst2.alloc(T * 4, &device_bytes);
+    const uint64_t nchunks = (T + (1u << slda::kZChunkLog2) - 1) >> slda::kZChunkLog2;
+    zruns1 = slda::zlayout_keys(T, shift, 1);
+    zruns2 = slda::zlayout_keys(T, shift, 2);
+    zsk1.alloc(T * 4, &device_bytes);
+    zsk2.alloc(T * 4, &device_bytes);
     zloc.alloc(T * 2, &device_bytes);
+    zbase1.alloc(nchunks * zruns1 * 4, &device_bytes);
+    zbase2.alloc(nchunks * zruns2 * 4, &device_bytes);
     DevMem slot_of, cnt, off;
     slot_of.alloc(T * 4, nullptr);  // slot of every zc position (level 1 writes, level 2 reads)
     for (uint32_t level = 1; level <= 2; ++level) {
@@ -841,8 +846,8 @@ void slda_engine::build_zlayout(bool trace) {
                                       flat, stream));
         exclusive_sum(cnt.as<uint32_t>(), off.as<uint32_t>(), flat);
         CK(slda::launch_zlayout_emit(tok.as<uint2>(), slot_of.as<uint32_t>(), T, shift, level, off.as<uint32_t>(),
-                                     level == 1 ? zsrc1.as<uint16_t>() : zsrc2.as<uint16_t>(),
-                                     level == 1 ? zdst1.as<uint32_t>() : zdst2.as<uint32_t>(),
+                                     level == 1 ? zsk1.as<uint32_t>() : zsk2.as<uint32_t>(),
+                                     level == 1 ? zbase1.as<uint32_t>() : zbase2.as<uint32_t>(),
                                      slot_of.as<uint32_t>(), zloc.as<uint16_t>(), stream));
         off.release();
         cnt.release();
@@ -1249,9 +1254,9 @@ void slda_engine::enqueue_iteration() {
     launches += n_units > 0;
     CK(cudaEventRecord(ev[2], stream));
     if (zmove) {  // execution-order topics -> z by slot (zmove.cu)
-        CK(slda::launch_zpermute(zx.as<uint16_t>(), zsrc1.as<uint16_t>(), zdst1.as<uint32_t>(), T,
+        CK(slda::launch_zpermute(zx.as<uint16_t>(), zsk1.as<uint32_t>(), zbase1.as<uint32_t>(), zruns1, T,
                                  zc.as<uint16_t>(), stream));
-        CK(slda::launch_zpermute(zc.as<uint16_t>(), zsrc2.as<uint16_t>(), zdst2.as<uint32_t>(), T,
+        CK(slda::launch_zpermute(zc.as<uint16_t>(), zsk2.as<uint32_t>(), zbase2.as<uint32_t>(), zruns2, T,
                                  zf.as<uint16_t>(), stream));
         CK(slda::launch_ztile(zf.as<uint16_t>(), zloc.as<uint16_t>(), T, z.as<uint16_t>(), stream));
         launches += 3;

@@ -51,20 +51,23 @@ cudaError_t launch_sampler(const SamplerArgs& a, uint32_t n_units, cudaStream_t 
 // ---- z transpose (zmove.cu): execution order -> slot order in three coalesced passes ---------
 constexpr uint32_t kZChunkLog2 = 14;  // permute chunk: 16384 entries (32 KB of topics in smem)
 constexpr uint32_t kZTileLog2 = 14;   // final tile: 16384 slots
-// out[dst[k]] = src[chunk(k) base + srcl[k]] for every position k: each CTA stages a chunk of
-// src in shared memory and writes it in a static order whose destinations form runs.
-cudaError_t launch_zpermute(const uint16_t* src, const uint16_t* srcl, const uint32_t* dst, uint64_t T,
+// Per chunk of 16384 positions: out[zbase[run] + k] = src[chunk base + (zsk[k] & 16383)] for every
+// sorted position k of the chunk, run = zsk[k] >> 14 (a run's destinations are consecutive): each
+// CTA stages a chunk of src in shared memory and stores it in runs.
+cudaError_t launch_zpermute(const uint16_t* src, const uint32_t* zsk, const uint32_t* zbase, uint32_t R, uint64_t T,
                             uint16_t* out, cudaStream_t s);
 // z[tile base + loc[m]] = zf[m] per 16384-slot tile, through shared memory.
 cudaError_t launch_ztile(const uint16_t* zf, const uint16_t* loc, uint64_t T, uint16_t* z, cudaStream_t s);
 // Setup of the static tables (two levels): per-(key, chunk) counts into a flat array in
 // destination order (its exclusive scan gives each run's first destination), then the stable
-// per-chunk ranking that writes srcl / dst and slot_of (level 1) or the tile-local slots (level 2).
+// per-chunk ranking that writes zsk (source index | run << 14), the chunk's run table (zbase: R
+// u32) and slot_of (level 1) or the tile-local slots (level 2).
 size_t zlayout_flat_size(uint64_t T, uint32_t shift, uint32_t level);
+uint32_t zlayout_keys(uint64_t T, uint32_t shift, uint32_t level);  // R: runs per chunk
 cudaError_t launch_zlayout_count(const uint2* tok, const uint32_t* slot_of, uint64_t T, uint32_t shift,
                                  uint32_t level, uint32_t* cnt, size_t flat, cudaStream_t s);
 cudaError_t launch_zlayout_emit(const uint2* tok, const uint32_t* slot_of, uint64_t T, uint32_t shift, uint32_t level,
-                                const uint32_t* off, uint16_t* srcl, uint32_t* dst, uint32_t* slot_of_out,
+                                const uint32_t* off, uint32_t* zsk, uint32_t* zbase, uint32_t* slot_of_out,
                                 uint16_t* loc_out, cudaStream_t s);
 
 struct SscArgs {

@@ -11,12 +11,14 @@
 // whose global stores are runs move them to slots:
 //   1. zc = zx permuted to slot-range buckets (<= 256, 4M slots each at C3), bucket entries in
 //      execution order: each CTA stages 16384 entries in shared memory and writes them bucket by
-//      bucket (runs of ~64 entries);
+//      bucket (runs of ~64 entries; a run's destinations are consecutive, so each position carries
+//      its source index and run id in one word, and the chunk's table one base per run);
 //   2. zf = zc permuted to 16384-slot tiles, entries of a tile in zc order: the same kernel;
 //   3. z = zf with each tile scattered inside shared memory by the slot's low 14 bits and stored
 //      whole (fully coalesced).
 // All tables are static (the PDOW order and the slots never change; engine.cu build_zlayout).
-// Bytes per token per iteration: (2 + 2 + 4 + 2) x 2 + (2 + 2 + 2) = 26.
+// Bytes per token per iteration: (2 + 4 + 2) x 2 + (2 + 2 + 2) = 22, plus the run tables
+// (4 bytes per run: ~0.06 byte per token at C3).
 #include "common.cuh"
 #include "kernels.hpp"
 
@@ -24,12 +26,19 @@ namespace slda {
 
 constexpr uint32_t kZChunk = 1u << kZChunkLog2;
 constexpr uint32_t kZTile = 1u << kZTileLog2;
+constexpr uint32_t kZWarps = 16;
+constexpr uint32_t kZMaxKeys = 1024;  // keys per chunk: <= 256 buckets (level 1), <= 1024 tiles (level 2)
 
+// One CTA per chunk: the chunk of src staged in shared memory; sorted position k of the chunk
+// carries its source index (14 bits) and its run (bits 14+); the run's destinations are
+// consecutive, so the chunk's table holds one base per run (first destination - first position,
+// mod 2^32) instead of one destination per token.
 __global__ void __launch_bounds__(512) zpermute_kernel(const uint16_t* __restrict__ src,
-                                                       const uint16_t* __restrict__ srcl,
-                                                       const uint32_t* __restrict__ dst, uint64_t T,
+                                                       const uint32_t* __restrict__ zsk,
+                                                       const uint32_t* __restrict__ zbase, uint32_t R, uint64_t T,
                                                        uint16_t* __restrict__ out) {
     __shared__ __align__(16) uint16_t buf[kZChunk];
+    __shared__ uint32_t s_base[kZMaxKeys];
     const uint64_t base = static_cast<uint64_t>(blockIdx.x) * kZChunk;
     const uint32_t n = static_cast<uint32_t>(min(static_cast<uint64_t>(kZChunk), T - base));
     if (n == kZChunk) {
@@ -39,8 +48,12 @@ __global__ void __launch_bounds__(512) zpermute_kernel(const uint16_t* __restric
     } else {
         for (uint32_t t = threadIdx.x; t < n; t += blockDim.x) buf[t] = src[base + t];
     }
+    for (uint32_t i = threadIdx.x; i < R; i += blockDim.x) s_base[i] = __ldg(zbase + static_cast<size_t>(blockIdx.x) * R + i);
     __syncthreads();
-    for (uint32_t k = threadIdx.x; k < n; k += blockDim.x) out[__ldg(dst + base + k)] = buf[__ldg(srcl + base + k)];
+    for (uint32_t k = threadIdx.x; k < n; k += blockDim.x) {
+        const uint32_t v = __ldg(zsk + base + k);
+        out[s_base[v >> kZChunkLog2] + k] = buf[v & (kZChunk - 1u)];
+    }
 }
 
 __global__ void __launch_bounds__(512) ztile_kernel(const uint16_t* __restrict__ zf, const uint16_t* __restrict__ loc,
@@ -59,9 +72,9 @@ __global__ void __launch_bounds__(512) ztile_kernel(const uint16_t* __restrict__
     }
 }
 
-cudaError_t launch_zpermute(const uint16_t* src, const uint16_t* srcl, const uint32_t* dst, uint64_t T,
+cudaError_t launch_zpermute(const uint16_t* src, const uint32_t* zsk, const uint32_t* zbase, uint32_t R, uint64_t T,
                             uint16_t* out, cudaStream_t s) {
-    if (T) zpermute_kernel<<<static_cast<uint32_t>((T + kZChunk - 1) / kZChunk), 512, 0, s>>>(src, srcl, dst, T, out);
+    if (T) zpermute_kernel<<<static_cast<uint32_t>((T + kZChunk - 1) / kZChunk), 512, 0, s>>>(src, zsk, zbase, R, T, out);
     return cudaGetLastError();
 }
 
@@ -102,9 +115,6 @@ __device__ __forceinline__ size_t zflat(const ZKeys& k, uint32_t key, uint32_t c
     return (static_cast<size_t>(b) * cpb + key) * cpb + (c - b * cpb);
 }
 
-constexpr uint32_t kZWarps = 16;
-constexpr uint32_t kZMaxKeys = 1024;
-
 __global__ void __launch_bounds__(512) zhist_count_kernel(ZKeys k, uint32_t* __restrict__ cnt) {
     __shared__ uint32_t h[kZMaxKeys];
     const uint32_t c = blockIdx.x;
@@ -118,8 +128,9 @@ __global__ void __launch_bounds__(512) zhist_count_kernel(ZKeys k, uint32_t* __r
 }
 
 __global__ void __launch_bounds__(512) zemit_kernel(ZKeys k, const uint32_t* __restrict__ off,
-                                                    uint16_t* __restrict__ srcl, uint32_t* __restrict__ dst,
-                                                    uint32_t* __restrict__ slot_of_out, uint16_t* __restrict__ loc_out) {
+                                                    uint32_t* __restrict__ zsk, uint32_t* __restrict__ zbase,
+                                                    uint32_t* __restrict__ slot_of_out,
+                                                    uint16_t* __restrict__ loc_out) {
     __shared__ uint16_t h[kZWarps * kZMaxKeys];  // per warp segment and key: count, then next local index
     __shared__ uint16_t start[kZMaxKeys];        // first local index of each key in the chunk
     const uint32_t c = blockIdx.x, w = threadIdx.x >> 5, lane = threadIdx.x & 31u, R = k.R;
@@ -169,6 +180,9 @@ __global__ void __launch_bounds__(512) zemit_kernel(ZKeys k, const uint32_t* __r
     __syncthreads();
     for (uint32_t i = threadIdx.x; i < kZWarps * R; i += blockDim.x)
         h[i] = static_cast<uint16_t>(h[i] + start[i % R]);
+    // The chunk's run table: first destination - first sorted position of every run (mod 2^32).
+    for (uint32_t key = threadIdx.x; key < R; key += blockDim.x)
+        zbase[static_cast<size_t>(c) * R + key] = __ldg(off + zflat(k, key, c)) - start[key];
     __syncthreads();
     for (uint32_t p0 = s0; p0 < s1; p0 += 32) {
         const uint32_t p = p0 + lane;
@@ -183,8 +197,7 @@ __global__ void __launch_bounds__(512) zemit_kernel(ZKeys k, const uint32_t* __r
         if (v) {
             const uint64_t kk = base + local;
             const uint32_t d = __ldg(off + zflat(k, key, c)) + (local - start[key]);
-            srcl[kk] = static_cast<uint16_t>(p);
-            dst[kk] = d;
+            zsk[kk] = p | (key << kZChunkLog2);
             if (k.level == 1) slot_of_out[d] = __ldg(&k.tok[base + p].y);
             else loc_out[d] = static_cast<uint16_t>(__ldg(k.slot_of + base + p) & (kZTile - 1u));
         }
@@ -208,14 +221,18 @@ cudaError_t launch_zlayout_count(const uint2* tok, const uint32_t* slot_of, uint
     return cudaGetLastError();
 }
 
+uint32_t zlayout_keys(uint64_t T, uint32_t shift, uint32_t level) {
+    return level == 1 ? static_cast<uint32_t>(((T - 1) >> shift) + 1) : 1u << (shift - kZTileLog2);
+}
+
 cudaError_t launch_zlayout_emit(const uint2* tok, const uint32_t* slot_of, uint64_t T, uint32_t shift, uint32_t level,
-                                const uint32_t* off, uint16_t* srcl, uint32_t* dst, uint32_t* slot_of_out,
+                                const uint32_t* off, uint32_t* zsk, uint32_t* zbase, uint32_t* slot_of_out,
                                 uint16_t* loc_out, cudaStream_t s) {
     if (!T) return cudaSuccess;
     const uint32_t nchunks = static_cast<uint32_t>((T + kZChunk - 1) / kZChunk);
     const uint32_t R = level == 1 ? static_cast<uint32_t>(((T - 1) >> shift) + 1) : 1u << (shift - kZTileLog2);
     if (R > kZMaxKeys || shift < kZTileLog2) return cudaErrorInvalidValue;
-    zemit_kernel<<<nchunks, 512, 0, s>>>(ZKeys{tok, slot_of, T, shift, level, R, nchunks}, off, srcl, dst,
+    zemit_kernel<<<nchunks, 512, 0, s>>>(ZKeys{tok, slot_of, T, shift, level, R, nchunks}, off, zsk, zbase,
                                          slot_of_out, loc_out);
     return cudaGetLastError();
 }
