@@ -61,7 +61,20 @@ __global__ void __launch_bounds__(512) ztile_kernel(const uint16_t* __restrict__
     __shared__ __align__(16) uint16_t buf[kZTile];
     const uint64_t base = static_cast<uint64_t>(blockIdx.x) * kZTile;
     const uint32_t n = static_cast<uint32_t>(min(static_cast<uint64_t>(kZTile), T - base));
-    for (uint32_t k = threadIdx.x; k < n; k += blockDim.x) buf[__ldg(loc + base + k)] = __ldg(zf + base + k);
+    {  // eight entries per thread per step: 16-byte loads of zf and loc (tile bases are 16384-aligned)
+        const uint4* z4 = reinterpret_cast<const uint4*>(zf + base);
+        const uint4* l4 = reinterpret_cast<const uint4*>(loc + base);
+        for (uint32_t t = threadIdx.x; t < n / 8; t += blockDim.x) {
+            const uint4 zv = __ldg(z4 + t), lv = __ldg(l4 + t);
+            const uint32_t zw[4] = {zv.x, zv.y, zv.z, zv.w}, lw[4] = {lv.x, lv.y, lv.z, lv.w};
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                buf[lw[j] & 0xFFFFu] = static_cast<uint16_t>(zw[j]);
+                buf[lw[j] >> 16] = static_cast<uint16_t>(zw[j] >> 16);
+            }
+        }
+        for (uint32_t k = (n & ~7u) + threadIdx.x; k < n; k += blockDim.x) buf[__ldg(loc + base + k)] = __ldg(zf + base + k);
+    }
     __syncthreads();
     if (n == kZTile) {
         const uint4* b4 = reinterpret_cast<const uint4*>(buf);
