@@ -493,6 +493,8 @@ struct slda_engine {
         a.tbits = tbits;
         a.row_entries = entries_counter();
         a.shape = sampler_shape;
+        const char* an = std::getenv("SLDA_ASYNC_NEXT");  // default on; 0 = the register prefetch (A/B)
+        a.async_next = an ? std::atoi(an) != 0 : 1u;
         a.vanilla = vanilla ? 1u : 0u;
         a.alpha = falpha;  // static_cast<float>(state.alpha), trainer.cpp:283
         return a;

@@ -38,6 +38,8 @@ struct SamplerArgs {
     // brings the topics to z by slot (zmove.cu).  Null: z[slot] directly (streaming chunks).
     uint16_t* zx;
     const uint32_t* zx_pos;
+    uint32_t async_next;    // prefetching quad kernels: the next round's first line by cp.async into shared
+                            // memory a round ahead (default; SLDA_ASYNC_NEXT=0: in registers, a group ahead)
 };
 
 // Sampler launch shapes (sampler.cu launch_sampler); -1 = by phi row size.

@@ -350,12 +350,21 @@ __global__ void __launch_bounds__(NT, MINB) sampler_quad_kernel(SamplerArgs a) {
     }
 }
 
-// The same algorithm with the next round's first line prefetched in each round's last group
-// slot and the next batch claimed a batch ahead; the per-unit scalars live in shared memory to
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool valid) {
+    const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(d), "l"(gmem), "r"(valid ? 16 : 0)
+                 : "memory");
+}
+
+// The same algorithm with the next round's first line prefetched -- by cp.async into a 1 KB
+// per-warp shared-memory buffer when a round starts, a whole round ahead (kAsyncNext, C3 sampler
+// 70.3 -> 68.3 ms), or into registers in each round's last group slot -- and the next batch
+// claimed a batch ahead; the per-unit scalars live in shared memory to
 // make room in the 64-register budget (C3 K=10K: 95.5 -> 92.8 ms; C2: 19.8 -> 20.5 ms).
 // kGlobalPhi: the phi row does not fit shared memory (K >~ 45K): only L8 is staged and the
 // products gather phi through L1/L2.
-template <int NT, int MINB, int L, bool kC16 = false, bool kPrefetchNext = true, bool kGlobalPhi = false>
+template <int NT, int MINB, int L, bool kC16 = false, bool kPrefetchNext = true, bool kGlobalPhi = false,
+          bool kAsyncNext = false>
 __global__ void __launch_bounds__(NT, MINB) sampler_quad_pf_kernel(SamplerArgs a) {
     constexpr uint32_t NW = NT / 32;
     constexpr uint32_t TPR = 32u / L;  // tokens per round (L lanes each, L sectors per group)
@@ -369,6 +378,10 @@ __global__ void __launch_bounds__(NT, MINB) sampler_quad_pf_kernel(SamplerArgs a
     const float* s_bhat = kGlobalPhi ? a.bhat + static_cast<size_t>(v) * a.K_pad : sm;
     float* s_l8 = kGlobalPhi ? sm : sm + a.K_pad;
     float* s_ck = s_l8 + a.l8_stride;  // [NW][32 tokens][kCkStride]
+    // kAsyncNext: the next round's first line of each token lands here by cp.async (32 B per lane),
+    // issued when a round starts -- a whole round ahead, in no registers.
+    unsigned char* s_line = reinterpret_cast<unsigned char*>(s_ck + NW * 32u * kCkStride) + (threadIdx.x >> 5) * 1024u +
+                            (threadIdx.x & 31u) * 32u;
     __shared__ __align__(8) unsigned long long s_bar;  // phi/L8 staging (TMA bulk copies)
     tma_stage_rows(sm, a.bhat + static_cast<size_t>(v) * a.K_pad, kGlobalPhi ? 0u : a.K_pad * 4u, s_l8,
                    a.l8 + static_cast<size_t>(v) * a.l8_stride, a.l8_stride * 4u, &s_bar);
@@ -422,6 +435,15 @@ __global__ void __launch_bounds__(NT, MINB) sampler_quad_pf_kernel(SamplerArgs a
                 c = zero_sector();
                 if (act) c = ldg_sector(row + 2 * sub);
             }
+            if (kAsyncNext) {  // the next round's first line (next batch's after the last round)
+                const bool last = r + 1 == L || base + TPR * (r + 1) >= unit.length;
+                const uint32_t nrq = __shfl_sync(0xffffffffu, last ? tk_nx.x : tk.x, last ? t : ti + TPR);
+                const bool ok = last ? nb + t < unit.length : base + ti + TPR < unit.length;
+                const uint4* src = ok ? A4 + nrq + 2 * sub : A4;
+                cp_async16(s_line, src, ok);
+                cp_async16(s_line + 16, src + 1, ok);
+                asm volatile("cp.async.commit_group;\n" ::: "memory");
+            }
             const uint32_t hw = __shfl_sync(0xffffffffu, c.lo.x, lead);  // header: word 0 of sector 0
             // [nnz-1 | entries | pad to 8]
             const uint32_t nnz = act ? (hw & tmask) + 1u : 0u;
@@ -461,7 +483,7 @@ __global__ void __launch_bounds__(NT, MINB) sampler_quad_pf_kernel(SamplerArgs a
             auto fetch = [&](uint32_t g, Sector& dst) {
                 if (g < max_groups) {  // warp-uniform
                     dst = L * g + sub < nsect ? ldg_sector(row + 2 * (L * g + sub)) : zero_sector();
-                } else if (kPrefetchNext) {
+                } else if (kPrefetchNext && !kAsyncNext) {
                     const bool last = r + 1 == L || base + TPR * (r + 1) >= unit.length;
                     const uint32_t nrq = __shfl_sync(0xffffffffu, last ? tk_nx.x : tk.x, last ? t : ti + TPR);
                     if (last ? nb + t < unit.length : base + ti + TPR < unit.length)
@@ -480,6 +502,11 @@ __global__ void __launch_bounds__(NT, MINB) sampler_quad_pf_kernel(SamplerArgs a
                     consume(n, g + 1);
                     if (g + 2 >= max_groups) break;
                 }
+            }
+            if (kAsyncNext) {
+                asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+                c.lo = *reinterpret_cast<const uint4*>(s_line);
+                c.hi = *reinterpret_cast<const uint4*>(s_line + 16);
             }
             // Token ti's S and sector count to its owning lane (lane ti).
             const uint32_t src = ((lane - TPR * r) & (TPR - 1u)) * L;
@@ -578,8 +605,13 @@ size_t sampler_quad_smem(const SamplerArgs& a, int nt) {
 
 template <int NT, int MINB, bool PF, bool C16>
 cudaError_t launch_quad_t1(const SamplerArgs& a, uint32_t n_units, cudaStream_t s) {
-    auto kern = PF ? sampler_quad_pf_kernel<NT, MINB, 4, C16> : sampler_quad_kernel<NT, MINB, 4, C16>;
-    const size_t smem = sampler_quad_smem(a, NT);
+    // The cp.async line buffer (1 KB per warp) only where two CTAs per SM still fit (K_pad <~ 13.5K
+    // at 512 threads); above, the register prefetch.
+    const bool an = PF && a.async_next &&
+                    2 * (sampler_quad_smem(a, NT) + static_cast<size_t>(NT / 32) * 1024u) <= 227u * 1024u;
+    auto kern = an ? sampler_quad_pf_kernel<NT, MINB, 4, C16, true, false, true>
+              : PF ? sampler_quad_pf_kernel<NT, MINB, 4, C16> : sampler_quad_kernel<NT, MINB, 4, C16>;
+    const size_t smem = sampler_quad_smem(a, NT) + (an ? static_cast<size_t>(NT / 32) * 1024u : 0u);
     if (const cudaError_t e = smem_optin(kern, smem); e != cudaSuccess) return e;
     kern<<<n_units, NT, smem, s>>>(a);
     return cudaGetLastError();
@@ -594,6 +626,8 @@ cudaError_t launch_quad_t(const SamplerArgs& a, uint32_t n_units, cudaStream_t s
 
 // phi rows too large for shared memory (K_pad * 4 > ~180 KB): quad-lane kernel with only L8 staged.
 cudaError_t launch_quad_global(const SamplerArgs& a, uint32_t n_units, cudaStream_t s) {
+    // (no cp.async line buffer here: the shared memory it takes comes out of the L1 that serves the
+    // phi gathers -- C5 K=50K sampler 59.6 -> 66.0 ms with it)
     auto kern = a.tbits == 16 ? sampler_quad_pf_kernel<512, 2, 4, true, true, true>
                               : sampler_quad_pf_kernel<512, 2, 4, false, true, true>;
     const size_t smem = sizeof(float) * (static_cast<size_t>(a.l8_stride) + 16u * 32u * 17u);
