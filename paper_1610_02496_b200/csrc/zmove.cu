@@ -98,16 +98,17 @@ cudaError_t launch_ztile(const uint16_t* zf, const uint16_t* loc, uint64_t T, ui
 
 // ---- setup: the static tables --------------------------------------------------------------
 // Both permutes are per-chunk stable counting sorts by a small key, so the tables come from two
-// counting passes per level instead of global radix sorts (C3: 9 ms instead of ~150 ms):
+// counting passes per level instead of global radix sorts (C3: 38 ms instead of 146-179 ms):
 //   level 1: chunk c of the execution order, key = slot bucket (slot >> shift, <= 256 keys);
 //            destinations (zc) are bucket-major, execution order inside a bucket;
 //   level 2: chunk c of zc (inside one bucket: buckets are 2^shift >= 2^14 positions), key = the
 //            slot's tile relative to the bucket's first tile (< 2^(shift-14) <= 1024 keys);
 //            destinations (zf) are tile-major, zc order inside a tile.
-// zhist_kernel counts (key, chunk) into a flat array whose order is the destination order, so
-// its exclusive scan is every (key, chunk) run's first destination; zemit_kernel ranks each
+// zhist_count_kernel counts (key, chunk) into a flat array whose order is the destination order,
+// so its exclusive scan is every (key, chunk) run's first destination; zemit_kernel ranks each
 // chunk's positions stably by key (warp segments walked in order, __match_any_sync peers) and
-// writes srcl / dst, plus slot_of at zc (level 1) or the tile-local slot at zf (level 2).
+// writes zsk (source index | run << 14) and the chunk's run bases, plus slot_of at zc (level 1)
+// or the tile-local slot at zf (level 2).
 struct ZKeys {
     const uint2* tok;        // level 1: execution-order token records (.y = slot)
     const uint32_t* slot_of; // level 2: slot of every zc position
