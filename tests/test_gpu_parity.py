@@ -298,16 +298,19 @@ VARIANT_CASES = ["c1", "long_docs", "empty_docs", "k_large", "nytimes_small", "k
 
 @pytest.mark.parametrize("variant", ["SLDA_SAMPLER=round", "SLDA_SAMPLER=quad512", "SLDA_SAMPLER=quad256",
                                      "SLDA_SAMPLER=global", "SLDA_PHI_SHAPE=16x8", "SLDA_PHI_SHAPE=32x3",
-                                     "SLDA_PHI_SHAPE=64x2", "SLDA_PHI_SHAPE=tma", "SLDA_ZMOVE=0"])
+                                     "SLDA_PHI_SHAPE=64x2", "SLDA_PHI_SHAPE=tma", "SLDA_ZMOVE=0",
+                                     "SLDA_SAMPLER=quad512,SLDA_ASYNC_NEXT=0"])
 @pytest.mark.parametrize("name", VARIANT_CASES)
 def test_kernel_variants_match_reference(name, variant, golden, monkeypatch):
     """Every sampler launch shape (quad-lane 256/512-thread CTAs, the round-based kernel, the
     global-phi quad kernel) and every phi tile shape gives the reference's digests, whichever
     shape the default selection would pick for the case; SLDA_ZMOVE=0 stores the topics straight
-    to z[slot] instead of through the z transpose.  The sampler shape and the z path are read when
+    to z[slot] instead of through the z transpose; SLDA_ASYNC_NEXT=0 prefetches each round's first
+    row line into registers instead of by cp.async.  The sampler shape and the z path are read when
     the engine is built (engine.cu), the phi shape at each launch."""
-    key, value = variant.split("=")
-    monkeypatch.setenv(key, value)
+    for setting in variant.split(","):
+        key, value = setting.split("=")
+        monkeypatch.setenv(key, value)
     spec = CASES[name]
     fx = golden["cases"][name]
     m, cfg, _ = make_model(spec)
@@ -329,7 +332,7 @@ def test_throughput_configs_match_reference_every_iteration(name, golden_big, mo
     K=50,000) against digests the reference itself produced, at every iteration, through the
     DEFAULT kernel selection: heavy words split into 8192-token units with in-CTA batch claiming,
     the 512-thread prefetching quad-lane kernel at K=10K, the global-phi kernel at K=50K."""
-    for k in ("SLDA_SAMPLER", "SLDA_PHI_SHAPE", "SLDA_SERIAL", "SLDA_ZMOVE"):
+    for k in ("SLDA_SAMPLER", "SLDA_PHI_SHAPE", "SLDA_SERIAL", "SLDA_ZMOVE", "SLDA_ASYNC_NEXT"):
         monkeypatch.delenv(k, raising=False)
     spec = BIG_CASES[name]
     fx = golden_big["cases"][name]
